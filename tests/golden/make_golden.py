@@ -1,0 +1,212 @@
+"""Generate golden vectors from the reference package itself.
+
+Run in the authoring container (the GPU box has no /root/reference):
+
+    python tests/golden/make_golden.py
+
+It imports ``gridfield`` read-only from /root/reference/pkg/src, drives the
+reference's own public API on small seeded inputs, and writes compressed .npz
+fixtures next to this script.  Tests pin the oracle (oracle/) against these
+files and then check the CUDA path against the oracle.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = Path(os.environ.get("GRIDFIELD_REFERENCE", "/root/reference/pkg/src"))
+OUT = Path(__file__).resolve().parent
+sys.path.insert(0, str(REF))
+
+import gridfield  # noqa: E402  (the reference)
+from gridfield import core, grid as ggrid, occupancy, render, scene, batched  # noqa: E402
+
+
+def save(name, **arrays):
+    np.savez_compressed(OUT / f"{name}.npz", **arrays)
+    print(f"wrote {name}.npz  ({(OUT / f'{name}.npz').stat().st_size / 1024:.1f} KiB)")
+
+
+def cam_arrays(cam):
+    return dict(
+        cam_w=np.int64(cam.width), cam_h=np.int64(cam.height),
+        cam_f=np.array([cam.fx, cam.fy, cam.cx, cam.cy], np.float64),
+        cam_c2w=np.asarray(cam.c2w, np.float64),
+    )
+
+
+class Tracer:
+    """Wraps NetworkGrid.query_points to record the positions of every field
+    query in call order (one call per block-round)."""
+
+    def __init__(self, g):
+        self.g = g
+        self.aabb = g.aabb
+        self.calls = []
+
+    def query_points(self, p, d):
+        self.calls.append((np.array(p, np.float32), np.array(d, np.float32)))
+        return self.g.query_points(p, d)
+
+
+def unit():
+    return core.Aabb((-1.0, -1.0, -1.0), (1.0, 1.0, 1.0))
+
+
+def gen_rays():
+    out = {}
+    cams = scene.sphere_cameras(unit(), 3, 96, seed=0)
+    odd = render.Camera(37, 23, 31.5, 29.0, 17.25, 12.75, render.look_at_pose(np.array([0.3, -2.5, 0.7]), np.zeros(3)))
+    ident = render.Camera(16, 16, 16.0, 16.0, 8.0, 8.0, np.eye(4))
+    for i, cam in enumerate(cams + [odd, ident]):
+        o, d = render.generate_rays(cam)
+        for k, v in cam_arrays(cam).items():
+            out[f"{k}_{i}"] = v
+        out[f"o_{i}"], out[f"d_{i}"] = o, d
+    out["n"] = np.int64(len(cams) + 2)
+    save("rays", **out)
+
+
+def gen_pcg():
+    ents = np.array([[0, 0], [0, 4096], [7, 12288], [3, 4096 * 156], [2**33 + 5, 4096 * 7], [123456789, 0]], dtype=np.uint64)
+    st = np.zeros((len(ents), 4), np.uint64)
+    draws = np.zeros((len(ents), 64), np.float32)
+    for i, (a, b) in enumerate(ents):
+        s = np.random.PCG64(np.random.SeedSequence([int(a), int(b)])).state["state"]
+        st[i] = [s["state"] >> 64, s["state"] & (2**64 - 1), s["inc"] >> 64, s["inc"] & (2**64 - 1)]
+        draws[i] = np.random.default_rng(np.random.SeedSequence([int(a), int(b)])).random(64, dtype=np.float32)
+    save("pcg64", entropy=ents, state=st, draws=draws)
+
+
+def gen_pointwise():
+    rng = np.random.default_rng(5)
+    v = rng.uniform(-1, 1, (256, 3)).astype(np.float32)
+    v[:4] = [[0, 0, 0], [1, 1, 1], [-1, -1, -1], [0.5, -0.25, 0.125]]
+    d = rng.normal(size=(256, 3)).astype(np.float32)
+    d /= np.linalg.norm(d, axis=-1, keepdims=True)
+    aabb = unit()
+    pts = rng.uniform(-1, 1, (4096, 3)).astype(np.float32)
+    pts[:6] = [[-1, -1, -1], [1, 1, 1], [0, 0, 0], [0.999, 0.5, 0.25], [-0.875, 0.125, 0.9999999], [np.float32(0.125), -0.5, 1]]
+    far = rng.uniform(-1.2, 1.2, (2048, 3)).astype(np.float32)
+    sig = np.concatenate([rng.uniform(0, 50, 1000), [0, 1e-6, 1e6, 10.0]]).astype(np.float32)
+    dl = np.concatenate([rng.uniform(0, 0.02, 1000), [0.1, 0.5, 0.1, 0.01]]).astype(np.float32)
+    save(
+        "pointwise",
+        enc_in=v, enc_x=core.positional_encode(v, 10), enc_d_in=d, enc_d=core.positional_encode(d, 4),
+        bin_pts=pts,
+        bin16=core.flatten_cell_index(core.bin_point(pts, aabb, (16, 16, 16)), (16, 16, 16)),
+        bin256=core.flatten_cell_index(core.bin_point(pts, aabb, (256, 256, 256)), (256, 256, 256)),
+        bin_5_7_3=core.flatten_cell_index(core.bin_point(pts, aabb, (5, 7, 3)), (5, 7, 3)),
+        clip_in=far, clip_out=core.clip_into(far, aabb),
+        alpha_sigma=sig, alpha_delta=dl, alpha=core.density_to_alpha(sig, dl),
+    )
+
+
+def gen_query():
+    aabb = unit()
+    g = ggrid.init_network_grid(aabb, (16, 16, 16), seed=3)
+    rng = np.random.default_rng(0)
+    n = 20000
+    pts = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    dirs = rng.normal(size=(n, 3)).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    c, s = g.query_points(pts, dirs)
+    keys = g.cell_index(pts)
+    lay = batched.group_by_network(batched.QueryBatch(pts, dirs, keys), g.n_cells)
+    # small grid with tagged density bias (test_grid.py:214-229 style)
+    g4 = ggrid.init_network_grid(aabb, (4, 4, 4), seed=5)
+    for k in g4.params.weights:
+        g4.params.weights[k][:] = 0
+        g4.params.biases[k][:] = 0
+    g4.params.biases["density"][:, 0] = np.arange(g4.n_cells, dtype=np.float32)
+    _, s4 = g4.query_points(pts[:2000], dirs[:2000])
+    save(
+        "query16",
+        pts=pts, dirs=dirs, rgb=c, sigma=s, keys=keys,
+        order=lay.order, inverse=lay.inverse, offsets=lay.offsets,
+        tag_sigma=s4,
+        w0_checksum=np.float64(g.params.weights["trunk0"].astype(np.float64).sum()),
+    )
+
+
+def toy_occ(res=256):
+    path = OUT / f"toy_occupancy_{res}.npz"
+    if path.exists():
+        z = np.load(path)
+        return occupancy.OccupancyGrid(unit(), z["res"], z["bits"])
+    t = time.time()
+    sc = scene.standard_toy_scene()
+    occ = occupancy.extract_occupancy(sc.density_at, sc.aabb, (res,) * 3, tau=10.0, workers=os.cpu_count())
+    print(f"toy occupancy {res}^3 in {time.time() - t:.1f}s, {occ.occupied_fraction():.4f} occupied")
+    np.savez_compressed(path, res=occ.resolution, bits=occ.bits)
+    return occ
+
+
+def render_case(name, g, occ, cam, cfg, seed=0, keep_trace=True):
+    tr = Tracer(g)
+    img, st = render.render_image(tr, occ, cam, cfg, seed=seed, workers=1)
+    pos = np.concatenate([c[0] for c in tr.calls]) if tr.calls else np.zeros((0, 3), np.float32)
+    counts = np.array([len(c[0]) for c in tr.calls], np.int64)
+    cells = g.cell_index(pos) if len(pos) else np.zeros(0, np.int64)
+    arr = dict(
+        image=img, total_queries=np.int64(st.total_queries), ess_skipped=np.int64(st.ess_skipped),
+        ert_terminated_rays=np.int64(st.ert_terminated_rays), n_rays=np.int64(st.n_rays),
+        k=np.int64(cfg.k), epsilon=np.float64(cfg.epsilon), background=np.array(cfg.background, np.float64),
+        ert_chunk=np.int64(cfg.ert_chunk), stratified=np.bool_(cfg.stratified), seed=np.int64(seed),
+        call_counts=counts, cell_hist=np.bincount(cells, minlength=g.n_cells).astype(np.int64),
+        pos_checksum=np.float64(pos.astype(np.float64).sum()),
+        **cam_arrays(cam),
+    )
+    if keep_trace:
+        arr["trace_pos"] = pos
+    save(name, **arr)
+    print(f"  {name}: Q={st.total_queries} ess={st.ess_skipped} ert={st.ert_terminated_rays}")
+
+
+def gen_render():
+    aabb = unit()
+    cam64 = scene.sphere_cameras(aabb, 1, 64, seed=0)[0]
+    g0 = ggrid.init_network_grid(aabb, (16, 16, 16), seed=0)
+    solid = occupancy.OccupancyGrid.solid(aabb, (256, 256, 256))
+    # C1: the BASELINE oracle configuration
+    render_case("render_c1", g0, solid, cam64, render.RenderConfig(k=128), keep_trace=False)
+    gb = ggrid.init_network_grid(aabb, (16, 16, 16), seed=0)
+    gb.params.biases["density"][:] = 20.0
+    render_case("render_c1_bias20", gb, solid, cam64, render.RenderConfig(k=128), keep_trace=False)
+    occ = toy_occ(256)
+    cam96 = scene.sphere_cameras(aabb, 1, 96, seed=0)[0]
+    render_case("render_toy96", g0, occ, cam96, render.RenderConfig(), keep_trace=False)
+    render_case("render_toy96_bias20", gb, occ, cam96, render.RenderConfig(), keep_trace=False)
+    # small cases with full per-query traces and edge configurations
+    cam32 = scene.sphere_cameras(aabb, 1, 32, seed=2)[0]
+    render_case("render_s32_trace", gb, occ, cam32, render.RenderConfig(k=96), seed=5)
+    render_case("render_s32_k50", gb, occ, cam32, render.RenderConfig(k=50, ert_chunk=32, background=(0.2, 0.4, 0.6)), seed=1)
+    render_case("render_s32_nostrat", gb, None, cam32, render.RenderConfig(k=64, stratified=False, epsilon=0.0), seed=0)
+    g2 = ggrid.init_network_grid(aabb, (2, 3, 4), seed=9)
+    g2.params.biases["density"][:] = 5.0
+    inside = render.Camera(24, 20, 12.0, 12.0, 12.0, 10.0, render.look_at_pose(np.array([0.2, 0.1, -0.3]), np.array([0.5, 0.9, 0.4])))
+    render_case("render_inside_chunk7", g2, None, inside, render.RenderConfig(k=40, ert_chunk=7, epsilon=0.05), seed=3)
+    axis = render.Camera(16, 16, 16.0, 16.0, 8.0, 8.0, render.look_at_pose(np.array([0.0, 0.0, -3.0]), np.zeros(3)))
+    render_case("render_axis", gb, occ, axis, render.RenderConfig(k=64), seed=0)
+    empty = occupancy.OccupancyGrid.solid(aabb, (8, 8, 8), value=False)
+    render_case("render_empty", g0, empty, cam32, render.RenderConfig(k=32, background=(1.0, 0.5, 0.25)), seed=0)
+    # multi-block ray set (2 blocks + ragged tail) through render_rays
+    cam80 = scene.sphere_cameras(aabb, 1, 80, seed=6)[0]  # 6400 rays = 1 full block + 2304
+    render_case("render_two_blocks", gb, occ, cam80, render.RenderConfig(k=64), seed=11, keep_trace=False)
+
+
+def main():
+    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render"]
+    for w in what:
+        t = time.time()
+        globals()[f"gen_{w}"]()
+        print(f"[{w}] {time.time() - t:.1f}s")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,123 @@
+"""Pin the CPU oracle (oracle/) to golden vectors produced by the reference
+package itself (tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_camera, toy_occupancy_bits
+from oracle import gridfield_oracle as O
+from oracle import seedseq
+
+UNIT_MIN = np.array([-1.0, -1.0, -1.0])
+UNIT_MAX = np.array([1.0, 1.0, 1.0])
+
+
+def test_pcg64_seeding_matches_numpy_golden():
+    z = golden("pcg64")
+    for (a, b), st, draws in zip(z["entropy"], z["state"], z["draws"]):
+        state, inc = seedseq.pcg64_seed([int(a), int(b)])
+        assert state == (int(st[0]) << 64) | int(st[1])
+        assert inc == (int(st[2]) << 64) | int(st[3])
+        assert np.array_equal(np.array(seedseq.float32_draws(state, inc, 64), np.float32), draws)
+
+
+def test_pixel_rays_bit_exact():
+    z = golden("rays")
+    for i in range(int(z["n"])):
+        cam = golden_camera(z, f"_{i}")
+        o, d = O.pixel_rays(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, cam.c2w)
+        assert np.array_equal(o, z[f"o_{i}"])
+        assert np.array_equal(d, z[f"d_{i}"]), f"camera {i}"
+
+
+def test_pointwise_bit_exact():
+    z = golden("pointwise")
+    assert np.array_equal(O.encode(z["enc_in"], 10), z["enc_x"])
+    assert np.array_equal(O.encode(z["enc_d_in"], 4), z["enc_d"])
+    for key, res in (("bin16", (16,) * 3), ("bin256", (256,) * 3), ("bin_5_7_3", (5, 7, 3))):
+        assert np.array_equal(O.bin_cells(z["bin_pts"], UNIT_MIN, UNIT_MAX, np.array(res)), z[key])
+    assert np.array_equal(O.clamp_into_box(z["clip_in"], UNIT_MIN, UNIT_MAX), z["clip_out"])
+    assert np.array_equal(O.alpha_of(z["alpha_sigma"], z["alpha_delta"]), z["alpha"])
+
+
+def test_bin_out_of_bounds_message():
+    with pytest.raises(ValueError, match="component 1"):
+        O.bin_cells(np.array([0.5, 1.5, 0.5]), UNIT_MIN, UNIT_MAX, np.array([16, 16, 16]))
+
+
+def test_query_points_and_grouping():
+    z = golden("query16")
+    lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (16, 16, 16), seed=3)
+    assert lat.weights["trunk0"].astype(np.float64).sum() == float(z["w0_checksum"])
+    keys = O.bin_cells(z["pts"], UNIT_MIN, UNIT_MAX, lat.res)
+    assert np.array_equal(keys, z["keys"])
+    g = O.group(keys, lat.n_cells)
+    assert np.array_equal(g.order, z["order"])
+    assert np.array_equal(g.inverse, z["inverse"])
+    assert np.array_equal(g.offsets, z["offsets"])
+    rgb, sig = O.query_points(lat, z["pts"], z["dirs"])
+    # same stacking -> same sgemm shapes -> bit-identical in practice
+    assert np.max(np.abs(rgb - z["rgb"])) <= 1e-6
+    assert np.max(np.abs(sig - z["sigma"])) <= 1e-6
+
+
+RENDER_CASES = [
+    "render_c1", "render_c1_bias20", "render_toy96", "render_toy96_bias20", "render_s32_trace",
+    "render_s32_k50", "render_s32_nostrat", "render_inside_chunk7", "render_axis", "render_empty",
+    "render_two_blocks",
+]
+
+LATTICES = {
+    "render_c1": ("g0", "solid"), "render_c1_bias20": ("gb", "solid"), "render_toy96": ("g0", "toy"),
+    "render_toy96_bias20": ("gb", "toy"), "render_s32_trace": ("gb", "toy"), "render_s32_k50": ("gb", "toy"),
+    "render_s32_nostrat": ("gb", None), "render_inside_chunk7": ("g2", None), "render_axis": ("gb", "toy"),
+    "render_empty": ("g0", "empty"), "render_two_blocks": ("gb", "toy"),
+}
+
+
+def case_inputs(name):
+    """Rebuild the exact lattice / occupancy a golden render case used."""
+    gname, oname = LATTICES[name]
+    if gname == "g2":
+        lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (2, 3, 4), seed=9)
+        lat.biases["density"][:] = 5.0
+    else:
+        lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (16, 16, 16), seed=0)
+        if gname == "gb":
+            lat.biases["density"][:] = 20.0
+    if oname == "solid":
+        occ = O.Occupancy(UNIT_MIN, UNIT_MAX, np.array([256] * 3), np.full(256**3 // 8, 255, np.uint8))
+    elif oname == "toy":
+        res, bits = toy_occupancy_bits()
+        occ = O.Occupancy(UNIT_MIN, UNIT_MAX, res, bits)
+    elif oname == "empty":
+        occ = O.Occupancy(UNIT_MIN, UNIT_MAX, np.array([8] * 3), np.zeros(64, np.uint8))
+    else:
+        occ = None
+    return lat, occ
+
+
+def case_config(z):
+    return O.MarchConfig(
+        k=int(z["k"]), epsilon=float(z["epsilon"]), background=tuple(z["background"]),
+        ert_chunk=int(z["ert_chunk"]), stratified=bool(z["stratified"]),
+    )
+
+
+@pytest.mark.parametrize("name", RENDER_CASES)
+def test_render_matches_reference(name):
+    z = golden(name)
+    lat, occ = case_inputs(name)
+    cam = golden_camera(z)
+    img, ctr = O.render_image(lat, occ, cam, case_config(z), seed=int(z["seed"]), workers=4, trace=True)
+    assert ctr.total_queries == int(z["total_queries"])
+    assert ctr.ess_skipped == int(z["ess_skipped"])
+    assert ctr.ert_terminated_rays == int(z["ert_terminated_rays"])
+    assert ctr.n_rays == int(z["n_rays"])
+    pos = np.concatenate([r[3] for r in ctr.rounds]) if ctr.rounds else np.zeros((0, 3), np.float32)
+    assert pos.astype(np.float64).sum() == float(z["pos_checksum"])
+    if "trace_pos" in z:
+        assert np.array_equal(pos, z["trace_pos"])
+    cells = O.bin_cells(pos, lat.b_min, lat.b_max, lat.res) if len(pos) else np.zeros(0, np.int64)
+    assert np.array_equal(np.bincount(cells, minlength=lat.n_cells), z["cell_hist"])
+    assert np.max(np.abs(img - z["image"])) <= 1e-6
