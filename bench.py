@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the KiloNeRF render hot path on B200 (BASELINE.json metric).
+
+One step = one 800x800 frame per GPU (config C2: 16^3 grid of 32-wide tiny
+MLPs, random init seed 0, toy-scene occupancy 256^3, K=384, eps=0.01,
+ert_chunk=32), rendered through the device marcher; at N>1 every rank renders
+its own view (sphere_cameras(aabb, 64, 800, seed=0)[rank], the C3 view batch)
+and the images are all-gathered over NCCL inside the step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision fp16|fp32]
+  python bench.py --impl reference      # the reference's CPU algorithm (oracle port) on host cores
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ms/frame and Mpixels/sec at 800x800, 16^3 tiny MLPs; MLP samples/sec vs roofline"
+UNIT = "Mpix/s"
+SIZE = 800
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+PAPER_1080TI_MPIX_S = 800 * 800 / 26e-3 / 1e6  # PAPER.md:166 (26 ms/frame, GTX 1080 Ti), context only
+
+
+def workload_desc(precision):
+    return {
+        "workload": "C2: 800x800 frame, 16^3 grid of 32-wide tiny MLPs (random init, seed 0), toy-scene "
+                    "occupancy 256^3 (tau=10, 10.81% occupied), K=384, eps=0.01, ert_chunk=32, stratified, seed 0",
+        "image": [SIZE, SIZE], "grid": [16, 16, 16], "k": 384, "mlp_precision": precision,
+        "views": "sphere_cameras(aabb, 64, 800, seed=0)[rank]",
+        "l2": "flushed between timed frames (256 MiB write outside the timed window)",
+    }
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {k: float(d[k]) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained")}, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def build_inputs(gf):
+    aabb = gf.Aabb((-1.0,) * 3, (1.0,) * 3)
+    grid = gf.init_network_grid(aabb, (16, 16, 16), seed=0)
+    z = np.load(ROOT / "tests" / "golden" / "toy_occupancy_256.npz")
+    occ = gf.OccupancyGrid(aabb, z["res"], z["bits"].copy())
+    cams = gf.sphere_cameras(aabb, 64, SIZE, seed=0)
+    return aabb, grid, occ, cams
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port of the reference algorithm
+# ---------------------------------------------------------------------------
+def cpu_render_sample(cam, block_stride: int, workers: int):
+    """Render every `block_stride`-th 4096-ray block of the frame with the
+    reference algorithm (oracle port, numpy) on `workers` threads.
+    Returns (seconds, rays, queries)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import gridfield_oracle as O
+
+    lat = O.init_lattice(np.full(3, -1.0), np.ones(3), (16, 16, 16), seed=0)
+    z = np.load(ROOT / "tests" / "golden" / "toy_occupancy_256.npz")
+    occ = O.Occupancy(np.full(3, -1.0), np.ones(3), z["res"], z["bits"])
+    o, d = O.pixel_rays(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, cam.c2w)
+    o64, d64 = o.astype(np.float64), d.astype(np.float64)
+    starts = list(range(0, len(o), O.RAY_BLOCK))[::block_stride]
+    cfg = O.MarchConfig()
+    q = lambda p, dd: O.query_points(lat, p, dd)  # noqa: E731
+
+    def one(s):
+        gen = np.random.default_rng(np.random.SeedSequence([0, s]))
+        e = min(s + O.RAY_BLOCK, len(o))
+        _, _, ctr = O.march_block(q, lat.b_min, lat.b_max, occ, o64[s:e], d64[s:e], cfg, gen)
+        return e - s, ctr.total_queries
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=workers) as pool:
+        res = list(pool.map(one, starts))
+    dt = time.perf_counter() - t0
+    return dt, sum(r[0] for r in res), sum(r[1] for r in res)
+
+
+def cpu_workers():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import paper_2103_13744_b200 as gf
+
+    _, _, _, cams = build_inputs(gf)
+    workers = cpu_workers()
+    stride = args.cpu_block_stride
+    for _ in range(args.warmup):
+        cpu_render_sample(cams[0], stride * 4, workers)
+    times, rays = [], 0
+    for _ in range(args.steps):
+        dt, r, _ = cpu_render_sample(cams[0], stride, workers)
+        times.append(dt)
+        rays = r
+    mpix = rays / statistics.median(times) / 1e6
+    sample = f"every {stride}th 4096-ray block of the C2 frame ({rays} rays), numpy oracle port, {workers} threads"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": mpix, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * SIZE * SIZE / (mpix * 1e6),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 sample placement / f32 MLP",
+        "data": "synthetic", "config": workload_desc("fp32 numpy"),
+        "cpu_baseline": {"value": mpix, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+        "e2e": {"value": mpix, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default=None, choices=[None, "fp16", "fp32"])
+    ap.add_argument("--cpu-block-stride", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2103_13744_b200 as gf
+    from paper_2103_13744_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    aabb, grid, occ, cams = build_inputs(gf)
+    cam = cams[rank % len(cams)]
+    cfg = gf.RenderConfig()
+    precision = args.precision
+    if precision is None:
+        try:
+            grid.device_params("fp16")
+            precision = "fp16"
+        except Exception:  # noqa: BLE001 -- tensor-core path not built: report the fp32 kernel instead
+            precision = "fp32"
+    grid.precision = precision
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    gathered = torch.empty((world, SIZE * SIZE, 3), dtype=torch.float32, device="cuda") if world > 1 else None
+    out = torch.empty((SIZE * SIZE, 3), dtype=torch.float32, device="cuda")
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+
+    def step():
+        stats.zero_()
+        gf.render.render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats)
+        if gathered is not None:
+            dist.all_gather_into_tensor(gathered, out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region (value)
+    launches0 = N.lib().gf_launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = N.lib().gf_launch_count() - launches0
+    per = [a.elapsed_time(b) for a, b in ev]
+    ms = sum(per) / len(per)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * SIZE * SIZE / (ms * 1e-3) / 1e6
+    queries = int(stats[0].item())
+
+    # ---- stage breakdown + roofline (separate frames with stage events on)
+    N.lib().gf_stage_timing(1)
+    n_prof = max(3, min(args.steps, 5))
+    for _ in range(n_prof):
+        flush.fill_(1)
+        stats.zero_()
+        gf.render.render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats)
+    torch.cuda.synchronize()
+    st_ms, st_n = N.stage_times()
+    N.lib().gf_stage_timing(0)
+    st_ms = {k: v / n_prof for k, v in st_ms.items()}
+    st_n = {k: v // n_prof for k, v in st_n.items()}
+    peaks, peak_src = load_peaks()
+    flops_per_q = gf.count_flops(grid.arch)
+    R, Q, rounds = SIZE * SIZE, queries, (cfg.k + cfg.ert_chunk - 1) // cfg.ert_chunk
+    cell_bytes = 2 * grid.arch.parameter_count() if precision == "fp16" else 4 * grid.arch.parameter_count()
+    algo = {  # SURVEY.md §8(d) per-unit figures x units per frame
+        "mlp_flop": Q * flops_per_q,
+        "mlp_bytes": Q * 36 + 791 * cell_bytes,
+        "march_bytes": Q * 40 + R * 12 + R * 16 * rounds + (256 ** 3) // 8,
+        "scatter_bytes": Q * 20,
+    }
+    mlp_tflops = algo["mlp_flop"] / (st_ms["mlp"] * 1e-3) / 1e12 if st_ms["mlp"] > 0 else 0.0
+    march_gbs = algo["march_bytes"] / (st_ms["march"] * 1e-3) / 1e9 if st_ms["march"] > 0 else 0.0
+    scatter_gbs = algo["scatter_bytes"] / (st_ms["scatter"] * 1e-3) / 1e9 if st_ms["scatter"] > 0 else 0.0
+    peak_t = peaks["bf16_tflops_sustained"]
+    stage_roof = {
+        "mlp": {"bound": "tensor", "achieved": mlp_tflops, "peak": peak_t, "unit": "TFLOP/s",
+                "frac": mlp_tflops / peak_t, "ms_per_frame": st_ms["mlp"], "launches_per_frame": st_n["mlp"]},
+        "march": {"bound": "hbm", "achieved": march_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                  "frac": march_gbs / peaks["hbm_gbs"], "ms_per_frame": st_ms["march"],
+                  "launches_per_frame": st_n["march"]},
+        "scatter": {"bound": "hbm", "achieved": scatter_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": scatter_gbs / peaks["hbm_gbs"], "ms_per_frame": st_ms["scatter"],
+                    "launches_per_frame": st_n["scatter"]},
+        "scan": {"ms_per_frame": st_ms["scan"], "launches_per_frame": st_n["scan"]},
+        "setup": {"ms_per_frame": st_ms["setup"], "launches_per_frame": st_n["setup"]},
+    }
+    dominant = max(("mlp", "march", "scatter"), key=lambda k: st_ms[k])
+    traffic = None
+    tfile = ROOT / "profiles" / "ncu_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get(f"{dominant}_{precision}")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    d = stage_roof[dominant]
+    roofline = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
+                "frac": d["frac"], "traffic": traffic, "kernel": dominant, "peak_source": peak_src}
+
+    # ---- end-to-end through the public API (numpy camera in, numpy image out)
+    e2e_times = []
+    for i in range(args.steps + 1):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        img, st = gf.render_image(grid, occ, cam, cfg, seed=0)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, torch.from_numpy(img.reshape(-1, 3)).cuda(non_blocking=True))
+            torch.cuda.synchronize()
+        if i:  # first call re-validates caches; not counted
+            e2e_times.append(time.perf_counter() - t0)
+    e2e_s = statistics.mean(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": world * SIZE * SIZE / e2e_s / 1e6, "unit": UNIT,
+           "h2d_bytes_per_step": int(N.C.sizeof(N.CameraT) + N.C.sizeof(N.MarchCfg)),
+           "d2h_bytes_per_step": int(img.nbytes + 32), "ms_per_frame": e2e_s * 1e3}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+        workers = cpu_workers()
+        dt, rays, _ = cpu_render_sample(cam, args.cpu_block_stride, workers)
+        cpu = {"value": rays / dt / 1e6, "unit": UNIT, "cores": workers, "kind": "port",
+               "sample": f"every {args.cpu_block_stride}th 4096-ray block of the same frame ({rays} rays), "
+                         f"numpy oracle port of the reference algorithm, {workers} threads, {dt:.1f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16" if precision == "fp16" else "f32",
+            "data": "synthetic (random-init 16^3 lattice, analytic toy-scene occupancy)",
+            "config": workload_desc(precision),
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "queries_per_frame": queries, "mlp_samples_per_s": queries / (st_ms["mlp"] * 1e-3) if st_ms["mlp"] else None,
+            "stage_roofline": stage_roof, "paper_1080ti_mpix_s_context": PAPER_1080TI_MPIX_S,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

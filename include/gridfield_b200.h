@@ -1,0 +1,198 @@
+/*
+ * gridfield_b200.h — C ABI of the B200-native KiloNeRF render / network-query
+ * hot path (libgridfield_b200.so).
+ *
+ * Plain pointers and sizes only.  Every pointer named *_dev is device memory
+ * on the current CUDA device; `stream` is a cudaStream_t passed as void*.
+ * All calls are asynchronous on `stream` unless stated otherwise and return a
+ * gf_status_t; on failure gf_last_error() holds a thread-local message.
+ *
+ * The reference (gridfield, pure numpy: /root/reference/pkg/src/gridfield) has
+ * no FFI; each entry point below replaces the Python function cited beside it,
+ * and the Python host mirror (paper_2103_13744_b200/) binds them with ctypes
+ * (see INTEGRATION.md).
+ */
+#ifndef GRIDFIELD_B200_H
+#define GRIDFIELD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GF_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define GF_API __attribute__((visibility("default")))
+#else
+#define GF_API
+#endif
+
+typedef enum {
+  GF_OK = 0,
+  GF_ERR_INVALID = 1,      /* bad argument (host-side validation)            */
+  GF_ERR_CUDA = 2,         /* CUDA launch / runtime error                    */
+  GF_ERR_WORKSPACE = 3,    /* workspace smaller than *_workspace_bytes()     */
+  GF_ERR_UNSUPPORTED = 4,  /* architecture / precision not compiled in       */
+} gf_status_t;
+
+/* Arithmetic used for the per-cell MLP layers. */
+typedef enum {
+  GF_PRECISION_FP32 = 0,   /* SIMT fp32 FMA (reference-faithful, slow)        */
+  GF_PRECISION_FP16 = 1,   /* tcgen05.mma kind::f16, fp16 operands, fp32 acc  */
+} gf_precision_t;
+
+/* mlp.py:30-87 MlpArchitecture + core.py:155-184 PositionalEncoding. */
+typedef struct {
+  int32_t hidden_layers;   /* >= 3; trunk layers = hidden_layers - 2          */
+  int32_t width;           /* hidden width (32 tiny, 64 for config 4)         */
+  int32_t view_width;      /* direction-layer width (== width for tiny nets)  */
+  int32_t pos_freqs;       /* 10 -> 63-wide position encoding                 */
+  int32_t dir_freqs;       /* 4  -> 27-wide direction encoding                */
+  int32_t include_raw;     /* 1: raw coordinates prepended                    */
+} gf_arch_t;
+
+/* grid.py:19-45 NetworkGrid geometry, occupancy.py:29-79 OccupancyGrid. */
+typedef struct {
+  double b_min[3];
+  double b_max[3];
+  int32_t res[3];
+} gf_grid_geom_t;
+
+/* render.py:368-390 RenderConfig plus the call's seed. */
+typedef struct {
+  int32_t k;               /* nominal samples per ray                         */
+  int32_t ert_chunk;       /* samples per marching round                      */
+  int32_t stratified;      /* 1: PCG64 jitter per 4096-ray block              */
+  int32_t eps_compare_f64; /* 0: transmittance < float32(eps) (Python float, NEP 50); 1: float64 compare */
+  double epsilon;          /* ERT threshold, 0 disables                       */
+  float background[3];
+  float _pad;
+  uint64_t seed;           /* render_rays(seed=...)                           */
+} gf_march_cfg_t;
+
+/* render.py:219-251 Camera (pinhole, c2w row-major 3x4). */
+typedef struct {
+  int32_t width, height;
+  double fx, fy, cx, cy;
+  double c2w[12];
+} gf_camera_t;
+
+/* RenderStats counters (render.py:404-416), int64 on device, in this order. */
+enum { GF_STAT_TOTAL_QUERIES = 0, GF_STAT_ESS_SKIPPED = 1, GF_STAT_ERT_TERMINATED = 2, GF_STAT_N_RAYS = 3, GF_STAT_COUNT = 4 };
+
+/* Optional per-sample trace of the marcher (test / debug only). */
+typedef struct {
+  float x, y, z;            /* clipped float32 sample position                */
+  uint32_t ray;             /* ray index within the call                      */
+  uint32_t slot;            /* sample index along the ray (0..k-1)            */
+  uint32_t cell;            /* network cell (flat, x-major)                   */
+} gf_trace_rec_t;
+
+GF_API int gf_abi_version(void);
+GF_API const char* gf_last_error(void);
+
+/* Number of float parameters per cell in manifest order (mlp.py:386-387). */
+GF_API int64_t gf_param_count(const gf_arch_t* arch);
+
+/* --- weight packing ------------------------------------------------------
+ * Replaces the per-bucket gather MlpParams.at(cells) (mlp.py:148-154,
+ * batched.py:140): the reference stores weights layer-major (n_cells,out,in);
+ * the device wants one contiguous blob per cell in the layout the MLP kernel
+ * stages into shared memory.  layer_w_dev[l] / layer_b_dev[l] are the
+ * (n_cells,out,in) / (n_cells,out) float32 arrays of manifest layer l.      */
+GF_API size_t gf_packed_bytes(const gf_arch_t* arch, int64_t n_cells, int precision);
+GF_API int gf_pack_weights(const gf_arch_t* arch, int64_t n_cells, const float* const* layer_w_dev,
+                    const float* const* layer_b_dev, void* packed_dev, int precision, void* stream);
+
+/* --- NetworkGrid.query_points (grid.py:50-56) -----------------------------
+ * Bin at network resolution, bucket by cell, fused encode + tiny MLP,
+ * results written in the caller's query order.  err_dev (int64, device) must
+ * be initialised to INT64_MAX; out-of-bounds inputs leave the first offending
+ * flat component index (point*3 + axis) there (core.py:92-101).           */
+GF_API size_t gf_query_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* grid, int64_t n);
+GF_API int gf_query_points(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed_dev, int precision,
+                    const float* pos_dev, const float* dir_dev, int64_t n, float* rgb_dev, float* sigma_dev,
+                    int64_t* err_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* --- batched.grouped_forward (batched.py:120-151) -------------------------
+ * Rows pos/dir are already grouped: cell c owns rows offsets[c]..offsets[c+1]
+ * (int64, n_cells+1).  Row j's result is written to index order[j] (int64;
+ * NULL = j), i.e. back in the original query order.                        */
+GF_API size_t gf_grouped_workspace_bytes(int64_t n_cells, int64_t n);
+GF_API int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packed_dev, int precision,
+                              const float* pos_dev, const float* dir_dev, int64_t n, const int64_t* offsets_dev,
+                              const int64_t* order_dev, float* rgb_dev, float* sigma_dev, void* ws_dev,
+                              size_t ws_bytes, void* stream);
+
+/* --- render.render_rays / render_image (render.py:545-594) ---------------
+ * Rays come either from `cam` (pixel index = ray_offset + i, row-major) or
+ * from float32 origins/directions (ray i of the call is global ray
+ * ray_offset + i).  ray_offset selects the 4096-ray jitter blocks so shards of
+ * one image reproduce the single-device image bit for bit.  occ_bits_dev may
+ * be NULL (no empty-space skipping).  stats_dev: int64[GF_STAT_COUNT],
+ * accumulated (caller zeroes).  trace_dev / trace_count_dev may be NULL.   */
+GF_API size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* grid, const gf_march_cfg_t* cfg,
+                                 int64_t n_rays);
+GF_API int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed_dev, int precision,
+                   const gf_grid_geom_t* occ, const uint8_t* occ_bits_dev, const gf_march_cfg_t* cfg,
+                   const gf_camera_t* cam, const float* origins_dev, const float* dirs_dev, int64_t ray_offset,
+                   int64_t n_rays, float* rgb_dev, int64_t* stats_dev, gf_trace_rec_t* trace_dev,
+                   int64_t trace_capacity, int64_t* trace_count_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* --- batched.group_by_network (batched.py:60-85) --------------------------
+ * Stable counting sort of keys (< n_keys).  order/inverse: int64[n];
+ * offsets: int64[n_keys+1].  err_dev as above (bad key index).             */
+GF_API size_t gf_group_workspace_bytes(int64_t n, int64_t n_keys);
+GF_API int gf_group_by_key(const int64_t* keys_dev, int64_t n, int64_t n_keys, int64_t* order_dev, int64_t* inverse_dev,
+                    int64_t* offsets_dev, int64_t* err_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* --- pointwise primitives (core.py, occupancy.py, render.py) ------------- */
+/* Points are (n,3) float32 (x_f64 = 0) or float64 (x_f64 = 1); arithmetic
+ * follows numpy's promotion (binning is always float64).                    */
+/* core.py:79-112 bin_point + flatten_cell_index -> flat cell per point.    */
+GF_API int gf_bin_points(const gf_grid_geom_t* grid, const void* x_dev, int32_t x_f64, int64_t n, int64_t* flat_dev,
+                         int64_t* err_dev, void* stream);
+/* occupancy.py:76-79 occupied_at.                                          */
+GF_API int gf_occupied_at(const gf_grid_geom_t* occ, const uint8_t* bits_dev, const void* x_dev, int32_t x_f64,
+                          int64_t n, uint8_t* out_dev, int64_t* err_dev, void* stream);
+/* core.py:52-68 clip_into (float32 points).                                */
+GF_API int gf_clip_into(const double* b_min, const double* b_max, const float* x_dev, int64_t n, float* out_dev,
+                 void* stream);
+/* core.py:132-152 positional_encode in the input dtype, width dim*(raw+2L). */
+GF_API int gf_positional_encode(const void* v_dev, int32_t v_f64, int64_t n, int32_t dim, int32_t n_freqs,
+                                int32_t include_raw, void* out_dev, void* stream);
+/* core.py:187-194 density_to_alpha (elementwise, same length, same dtype). */
+GF_API int gf_density_to_alpha(const void* sigma_dev, const void* delta_dev, int32_t f64, int64_t n, void* out_dev,
+                               void* stream);
+/* render.py:463-478 composite: n_rays x n_samples, float32.                */
+GF_API int gf_composite(const float* colors_dev, const float* alphas_dev, int64_t n_rays, int64_t n_samples,
+                 float* rgb_dev, float* trans_dev, void* stream);
+GF_API int gf_composite_f64(const double* colors_dev, const double* alphas_dev, int64_t n_rays, int64_t n_samples,
+                     double* rgb_dev, double* trans_dev, void* stream);
+/* render.py:333-342 generate_rays for a camera (float32 origins, dirs).    */
+GF_API int gf_generate_rays(const gf_camera_t* cam, float* origins_dev, float* dirs_dev, void* stream);
+
+/* --- instrumentation ------------------------------------------------------
+ * Stage timing: while enabled, gf_render_rays / gf_query_points record CUDA
+ * events on their stream between stages; gf_stage_times() synchronises and
+ * returns accumulated milliseconds per stage (GF_STAGE_*) and launches per
+ * stage, then clears.  gf_launch_count() counts every kernel this library
+ * has launched in the process.                                             */
+enum { GF_STAGE_SETUP = 0, GF_STAGE_MARCH = 1, GF_STAGE_SCAN = 2, GF_STAGE_SCATTER = 3, GF_STAGE_MLP = 4,
+       GF_STAGE_COUNT = 5 };
+GF_API int gf_stage_timing(int32_t enable);
+GF_API int gf_stage_times(double* ms_out, int64_t* launches_out);
+GF_API int64_t gf_launch_count(void);
+
+/* --- host-side helpers (no device work) ---------------------------------- */
+/* PCG64(SeedSequence([seed, block_start])).state as {state_hi, state_lo,
+ * inc_hi, inc_lo} (numpy semantics; render.py:569).                          */
+GF_API int gf_pcg64_block_state(uint64_t seed, uint64_t block_start, uint64_t out4[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRIDFIELD_B200_H */

@@ -1,0 +1,487 @@
+// extern "C" entry points of libgridfield_b200.so (include/gridfield_b200.h).
+//
+// Host-side orchestration only: argument validation, workspace carving and
+// the launch sequence of the render / query pipelines on the caller's stream.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "gf_march.cuh"
+#include "gf_mlp.cuh"
+
+namespace gf {
+size_t group_workspace(int64_t n, int64_t n_keys);
+void launch_group(const int64_t* keys, int64_t n, int64_t n_keys, int64_t* order, int64_t* inverse, int64_t* offsets,
+                  int64_t* err, void* ws, cudaStream_t st);
+void launch_bin_points(const GfGrid& g, const void* x, int f64, int64_t n, int64_t* flat, int64_t* err,
+                       cudaStream_t st);
+void launch_occupied_at(const GfGrid& g, const uint8_t* bits, const void* x, int f64, int64_t n, uint8_t* out,
+                        int64_t* err, cudaStream_t st);
+void launch_clip(const double* lo, const double* hi, const float* x, int64_t n, float* out, cudaStream_t st);
+void launch_encode(const void* v, int f64, int64_t n, int dim, int L, int raw, void* out, cudaStream_t st);
+void launch_alpha(const void* s, const void* d, int f64, int64_t n, void* out, cudaStream_t st);
+void launch_composite(const float* c, const float* a, int64_t nr, int64_t ns, float* rgb, float* tr, cudaStream_t st);
+void launch_composite_f64(const double* c, const double* a, int64_t nr, int64_t ns, double* rgb, double* tr,
+                          cudaStream_t st);
+void launch_gen_rays(const gf_camera_t& c, float* o, float* d, cudaStream_t st);
+
+int num_sms() {
+  static thread_local int dev = -1, sms = 0;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d != dev) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+    dev = d;
+  }
+  return sms > 0 ? sms : 148;
+}
+}  // namespace gf
+
+using namespace gf;
+
+#include <atomic>
+#include <vector>
+
+static thread_local std::string g_err;
+
+// ---------------------------------------------------------------------------
+// instrumentation: launch counter + optional per-stage CUDA-event timing
+// ---------------------------------------------------------------------------
+static std::atomic<int64_t> g_launches{0};
+
+struct StageTimer {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, cudaEvent_t>> marks;  // (stage finished, event)
+  std::vector<std::pair<int, int>> launches;       // (stage, count)
+  size_t used = 0;
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+};
+static thread_local StageTimer g_timer;
+
+// Record that `n` kernels of stage `stage` were just enqueued on `st`.
+static void stage_mark(cudaStream_t st, int stage, int n) {
+  g_launches += n;
+  if (!g_timer.on) return;
+  if (g_timer.marks.empty()) {  // opening mark for this call
+    cudaEvent_t e0 = g_timer.next();
+    cudaEventRecord(e0, st);
+    g_timer.marks.push_back({-1, e0});
+  }
+  cudaEvent_t e = g_timer.next();
+  cudaEventRecord(e, st);
+  g_timer.marks.push_back({stage, e});
+  g_timer.launches.push_back({stage, n});
+}
+
+static void stage_open(cudaStream_t st) {
+  if (!g_timer.on) return;
+  cudaEvent_t e0 = g_timer.next();
+  cudaEventRecord(e0, st);
+  g_timer.marks.push_back({-1, e0});
+}
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+static int check_cuda(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(GF_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  return GF_OK;
+}
+
+// bump allocator over a caller-provided workspace
+struct Carve {
+  char* base;
+  size_t off = 0;
+  explicit Carve(void* p) : base((char*)p) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = gf_align(off);
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+  size_t size() const { return gf_align(off); }
+};
+
+static bool valid_grid(const gf_grid_geom_t* g) {
+  if (!g) return false;
+  for (int a = 0; a < 3; ++a)
+    if (!(g->b_min[a] < g->b_max[a]) || g->res[a] < 1) return false;
+  return true;
+}
+
+static int64_t n_cells_of(const gf_grid_geom_t* g) { return (int64_t)g->res[0] * g->res[1] * g->res[2]; }
+
+extern "C" {
+
+int gf_abi_version(void) { return GF_ABI_VERSION; }
+const char* gf_last_error(void) { return g_err.c_str(); }
+
+int64_t gf_param_count(const gf_arch_t* arch) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t)) return -1;
+  int64_t n = 0;
+  for (int l = 0; l < t.n_layers; ++l) n += (int64_t)t.in[l] * t.out[l] + t.out[l];
+  return n;
+}
+
+size_t gf_packed_bytes(const gf_arch_t* arch, int64_t n_cells, int precision) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t)) return 0;
+  if (precision == GF_PRECISION_FP32) return (size_t)make_fp32_layout(t).cell_floats * 4 * (size_t)n_cells;
+  if (precision == GF_PRECISION_FP16) return fp16_cell_bytes(t) * (size_t)n_cells;
+  return 0;
+}
+
+int gf_pack_weights(const gf_arch_t* arch, int64_t n_cells, const float* const* w, const float* const* b, void* packed,
+                    int precision, void* stream) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_pack_weights: bad architecture");
+  cudaStream_t st = (cudaStream_t)stream;
+  bool ok = false;
+  if (precision == GF_PRECISION_FP32)
+    ok = launch_pack_fp32(t, n_cells, w, b, (float*)packed, st);
+  else if (precision == GF_PRECISION_FP16)
+    ok = launch_pack_fp16(t, n_cells, w, b, packed, st);
+  if (!ok) return fail(GF_ERR_UNSUPPORTED, "gf_pack_weights: precision/architecture not supported");
+  return check_cuda("gf_pack_weights");
+}
+
+// ---------------------------------------------------------------------------
+// query path
+// ---------------------------------------------------------------------------
+struct QueryWs {
+  uint32_t* keys;
+  BucketBufs B;
+};
+
+static size_t query_carve(Carve& c, int64_t n, int64_t n_cells, QueryWs* w) {
+  w->keys = c.take<uint32_t>((size_t)n + 1);
+  w->B.counts = c.take<uint32_t>((size_t)n_cells);
+  w->B.offsets = c.take<uint32_t>((size_t)n_cells + 1);
+  w->B.cursor = c.take<uint32_t>((size_t)n_cells);
+  w->B.tiles = c.take<uint2>((size_t)(n / GF_TILE_ROWS + n_cells + 1));
+  w->B.n_tiles = c.take<uint32_t>(1);
+  w->B.sorted = c.take<uint32_t>((size_t)n + 1);
+  return c.size();
+}
+
+size_t gf_query_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* grid, int64_t n) {
+  (void)arch;
+  if (!valid_grid(grid) || n < 0) return 0;
+  Carve c(nullptr);
+  QueryWs w;
+  return query_carve(c, n, n_cells_of(grid), &w);
+}
+
+static bool run_mlp(const LayerTable& t, const void* packed, int precision, const TileSched& S, const RenderIO* rio,
+                    const QueryIO* qio, cudaStream_t st) {
+  if (precision == GF_PRECISION_FP32)
+    return rio ? launch_mlp_fp32_render(t, (const float*)packed, S, *rio, st)
+               : launch_mlp_fp32_query(t, (const float*)packed, S, *qio, st);
+  if (precision == GF_PRECISION_FP16)
+    return rio ? launch_mlp_tc_render(t, packed, S, *rio, st) : launch_mlp_tc_query(t, packed, S, *qio, st);
+  return false;
+}
+
+int gf_query_points(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed, int precision,
+                    const float* pos, const float* dir, int64_t n, float* rgb, float* sigma, int64_t* err, void* ws,
+                    size_t ws_bytes, void* stream) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_query_points: bad architecture");
+  if (!valid_grid(grid) || n < 0 || n >= (int64_t)0xFFFFFFF0ll)
+    return fail(GF_ERR_INVALID, "gf_query_points: bad grid or size");
+  const int64_t nc = n_cells_of(grid);
+  Carve c(ws);
+  QueryWs w;
+  if (query_carve(c, n, nc, &w) > ws_bytes) return fail(GF_ERR_WORKSPACE, "gf_query_points: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  GfGrid g = gf_make_grid(grid);
+  stage_open(st);
+  cudaMemsetAsync(w.B.counts, 0, (size_t)nc * 4, st);
+  launch_query_keys(g, pos, n, w.keys, w.B.counts, err, st);
+  stage_mark(st, GF_STAGE_MARCH, n > 0 ? 1 : 0);
+  launch_scan_cells(w.B, nc, st);
+  stage_mark(st, GF_STAGE_SCAN, 1);
+  launch_scatter_query(w.keys, n, w.B, st);
+  stage_mark(st, GF_STAGE_SCATTER, n > 0 ? 1 : 0);
+  TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
+  QueryIO io{pos, dir, rgb, sigma, nullptr};
+  if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
+    return fail(GF_ERR_UNSUPPORTED, "gf_query_points: no MLP kernel for this architecture/precision");
+  stage_mark(st, GF_STAGE_MLP, 1);
+  return check_cuda("gf_query_points");
+}
+
+int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packed, int precision, const float* pos,
+                       const float* dir, int64_t n, const int64_t* offsets, const int64_t* order, float* rgb,
+                       float* sigma, void* ws, size_t ws_bytes, void* stream) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_grouped_forward: bad architecture");
+  if (n_cells < 1 || n < 0 || n >= (int64_t)0xFFFFFFF0ll) return fail(GF_ERR_INVALID, "gf_grouped_forward: bad sizes");
+  Carve c(ws);
+  QueryWs w;
+  if (query_carve(c, n, n_cells, &w) > ws_bytes) return fail(GF_ERR_WORKSPACE, "gf_grouped_forward: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  launch_segments_from_offsets(offsets, n_cells, n, w.B, st);
+  TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
+  QueryIO io{pos, dir, rgb, sigma, order};
+  if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
+    return fail(GF_ERR_UNSUPPORTED, "gf_grouped_forward: no MLP kernel for this architecture/precision");
+  return check_cuda("gf_grouped_forward");
+}
+
+size_t gf_grouped_workspace_bytes(int64_t n_cells, int64_t n) {
+  Carve c(nullptr);
+  QueryWs w;
+  return query_carve(c, n, n_cells, &w);
+}
+
+// ---------------------------------------------------------------------------
+// render path
+// ---------------------------------------------------------------------------
+struct RenderWs {
+  u128* seeds;
+  RayState R;
+  RoundBufs RB;
+  BucketBufs B;
+};
+
+static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int stride, int64_t n_cells, RenderWs* w) {
+  const size_t cap = (size_t)n_rays * (size_t)stride;
+  w->seeds = c.take<u128>((size_t)2 * n_blocks);
+  w->R.org = c.take<float4>((size_t)n_rays);
+  w->R.dir = c.take<float4>((size_t)n_rays);
+  w->R.acc = c.take<float4>((size_t)n_rays);
+  w->R.rng = c.take<u128>((size_t)n_rays);
+  w->R.run = c.take<uint32_t>((size_t)n_rays);
+  w->R.flags = c.take<uint8_t>((size_t)n_rays);
+  w->RB.rec = c.take<float4>(cap);
+  w->RB.res = c.take<float4>(cap);
+  w->B.counts = c.take<uint32_t>((size_t)n_cells);
+  w->RB.counts = w->B.counts;
+  w->B.offsets = c.take<uint32_t>((size_t)n_cells + 1);
+  w->B.cursor = c.take<uint32_t>((size_t)n_cells);
+  w->B.tiles = c.take<uint2>(cap / GF_TILE_ROWS + (size_t)n_cells + 1);
+  w->B.n_tiles = c.take<uint32_t>(1);
+  w->B.sorted = c.take<uint32_t>(cap + 1);
+  return c.size();
+}
+
+static void block_range(int64_t ray_offset, int64_t n_rays, int64_t* first, int64_t* count) {
+  *first = ray_offset / GF_RAY_BLOCK;
+  int64_t last = n_rays > 0 ? (ray_offset + n_rays - 1) / GF_RAY_BLOCK : *first;
+  *count = last - *first + 1;
+}
+
+size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* grid, const gf_march_cfg_t* cfg,
+                                 int64_t n_rays) {
+  (void)arch;
+  if (!valid_grid(grid) || !cfg || cfg->k < 1 || cfg->ert_chunk < 1 || n_rays < 0) return 0;
+  int stride = cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k;
+  Carve c(nullptr);
+  RenderWs w;
+  // worst case: the call's rays straddle one more block boundary
+  return render_carve(c, n_rays, n_rays / GF_RAY_BLOCK + 2, stride, n_cells_of(grid), &w);
+}
+
+int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed, int precision,
+                   const gf_grid_geom_t* occ, const uint8_t* occ_bits, const gf_march_cfg_t* cfg,
+                   const gf_camera_t* cam, const float* origins, const float* dirs, int64_t ray_offset,
+                   int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace, int64_t trace_capacity,
+                   int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_render_rays: bad architecture");
+  if (!valid_grid(grid)) return fail(GF_ERR_INVALID, "gf_render_rays: bad grid");
+  if (!cfg || cfg->k < 1 || cfg->ert_chunk < 1 || !(cfg->epsilon >= 0.0 && cfg->epsilon < 1.0))
+    return fail(GF_ERR_INVALID, "gf_render_rays: bad march config");
+  if (occ_bits && !valid_grid(occ)) return fail(GF_ERR_INVALID, "gf_render_rays: bad occupancy grid");
+  if (!cam && (!origins || !dirs) && n_rays > 0) return fail(GF_ERR_INVALID, "gf_render_rays: no rays");
+  if (ray_offset < 0 || n_rays < 0) return fail(GF_ERR_INVALID, "gf_render_rays: bad ray range");
+  const int stride = cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k;
+  if ((double)n_rays * stride >= 4.0e9) return fail(GF_ERR_INVALID, "gf_render_rays: too many rays per call");
+  if (n_rays == 0) return GF_OK;
+  const int64_t nc = n_cells_of(grid);
+  int64_t first_block, n_blocks;
+  block_range(ray_offset, n_rays, &first_block, &n_blocks);
+  Carve c(ws);
+  RenderWs w;
+  if (render_carve(c, n_rays, n_blocks, stride, nc, &w) > ws_bytes)
+    return fail(GF_ERR_WORKSPACE, "gf_render_rays: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+
+  MarchParams P;
+  memset(&P, 0, sizeof(P));
+  P.grid = gf_make_grid(grid);
+  if (occ_bits) P.occ = gf_make_grid(occ);
+  P.occ_bits = occ_bits;
+  if (cam) {
+    P.cam = *cam;
+    P.use_cam = 1;
+  }
+  P.origins = origins;
+  P.dirs = dirs;
+  P.ray_offset = ray_offset;
+  P.n_rays = n_rays;
+  P.first_block = first_block;
+  P.block_seeds = w.seeds;
+  P.k = cfg->k;
+  P.chunk = cfg->ert_chunk;
+  P.n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
+  P.stride = stride;
+  P.stratified = cfg->stratified ? 1 : 0;
+  P.ert = cfg->epsilon > 0.0 ? 1 : 0;
+  P.eps_f64 = cfg->eps_compare_f64 ? 1 : 0;
+  P.epsilon = cfg->epsilon;
+  for (int a = 0; a < 3; ++a) P.bg[a] = cfg->background[a];
+  P.rgb_out = rgb;
+  P.stats = stats;
+  P.trace = trace;
+  P.trace_capacity = trace ? trace_capacity : 0;
+  P.trace_count = trace_count;
+
+  stage_open(st);
+  cudaMemsetAsync(w.B.counts, 0, (size_t)nc * 4, st);
+  if (P.stratified) k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(n_blocks, 64), 64, 0, st>>>(cfg->seed, first_block,
+                                                                                              n_blocks, w.seeds);
+  const unsigned ray_blocks = (unsigned)gf_div_up<int64_t>(n_rays, 128);
+  k_ray_init<<<ray_blocks, 128, 0, st>>>(P, w.R);
+  stage_mark(st, GF_STAGE_SETUP, P.stratified ? 2 : 1);
+  TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
+  RenderIO io{w.RB.rec, w.RB.res, w.R.dir, (uint32_t)stride};
+  for (int r = 0; r < P.n_rounds; ++r) {
+    k_march<<<ray_blocks, 128, 0, st>>>(P, w.R, w.RB, r);
+    stage_mark(st, GF_STAGE_MARCH, 1);
+    launch_scan_cells(w.B, nc, st);
+    stage_mark(st, GF_STAGE_SCAN, 1);
+    launch_scatter_render(w.RB.rec, w.R.run, n_rays, stride, w.B, st);
+    stage_mark(st, GF_STAGE_SCATTER, 1);
+    if (!run_mlp(t, packed, precision, S, &io, nullptr, st))
+      return fail(GF_ERR_UNSUPPORTED, "gf_render_rays: no MLP kernel for this architecture/precision");
+    stage_mark(st, GF_STAGE_MLP, 1);
+  }
+  k_march<<<ray_blocks, 128, 0, st>>>(P, w.R, w.RB, P.n_rounds);
+  stage_mark(st, GF_STAGE_MARCH, 1);
+  return check_cuda("gf_render_rays");
+}
+
+// ---------------------------------------------------------------------------
+// grouping and pointwise
+// ---------------------------------------------------------------------------
+size_t gf_group_workspace_bytes(int64_t n, int64_t n_keys) { return group_workspace(n, n_keys); }
+
+int gf_group_by_key(const int64_t* keys, int64_t n, int64_t n_keys, int64_t* order, int64_t* inverse,
+                    int64_t* offsets, int64_t* err, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || n_keys < 1) return fail(GF_ERR_INVALID, "gf_group_by_key: bad sizes");
+  if (group_workspace(n, n_keys) > ws_bytes) return fail(GF_ERR_WORKSPACE, "gf_group_by_key: workspace too small");
+  launch_group(keys, n, n_keys, order, inverse, offsets, err, ws, (cudaStream_t)stream);
+  return check_cuda("gf_group_by_key");
+}
+
+int gf_bin_points(const gf_grid_geom_t* grid, const void* x, int32_t x_f64, int64_t n, int64_t* flat, int64_t* err,
+                  void* stream) {
+  if (!valid_grid(grid) || n < 0) return fail(GF_ERR_INVALID, "gf_bin_points: bad grid");
+  launch_bin_points(gf_make_grid(grid), x, x_f64, n, flat, err, (cudaStream_t)stream);
+  return check_cuda("gf_bin_points");
+}
+
+int gf_occupied_at(const gf_grid_geom_t* occ, const uint8_t* bits, const void* x, int32_t x_f64, int64_t n,
+                   uint8_t* out, int64_t* err, void* stream) {
+  if (!valid_grid(occ) || n < 0) return fail(GF_ERR_INVALID, "gf_occupied_at: bad grid");
+  launch_occupied_at(gf_make_grid(occ), bits, x, x_f64, n, out, err, (cudaStream_t)stream);
+  return check_cuda("gf_occupied_at");
+}
+
+int gf_clip_into(const double* b_min, const double* b_max, const float* x, int64_t n, float* out, void* stream) {
+  if (n < 0) return fail(GF_ERR_INVALID, "gf_clip_into: bad size");
+  launch_clip(b_min, b_max, x, n, out, (cudaStream_t)stream);
+  return check_cuda("gf_clip_into");
+}
+
+int gf_positional_encode(const void* v, int32_t v_f64, int64_t n, int32_t dim, int32_t L, int32_t raw, void* out,
+                         void* stream) {
+  if (n < 0 || dim < 1 || L < 0) return fail(GF_ERR_INVALID, "gf_positional_encode: bad sizes");
+  launch_encode(v, v_f64, n, dim, L, raw, out, (cudaStream_t)stream);
+  return check_cuda("gf_positional_encode");
+}
+
+int gf_density_to_alpha(const void* s, const void* d, int32_t f64, int64_t n, void* out, void* stream) {
+  if (n < 0) return fail(GF_ERR_INVALID, "gf_density_to_alpha: bad size");
+  launch_alpha(s, d, f64, n, out, (cudaStream_t)stream);
+  return check_cuda("gf_density_to_alpha");
+}
+
+int gf_composite(const float* c, const float* a, int64_t nr, int64_t ns, float* rgb, float* tr, void* stream) {
+  if (nr < 0 || ns < 0) return fail(GF_ERR_INVALID, "gf_composite: bad sizes");
+  launch_composite(c, a, nr, ns, rgb, tr, (cudaStream_t)stream);
+  return check_cuda("gf_composite");
+}
+
+int gf_composite_f64(const double* c, const double* a, int64_t nr, int64_t ns, double* rgb, double* tr, void* stream) {
+  if (nr < 0 || ns < 0) return fail(GF_ERR_INVALID, "gf_composite_f64: bad sizes");
+  launch_composite_f64(c, a, nr, ns, rgb, tr, (cudaStream_t)stream);
+  return check_cuda("gf_composite_f64");
+}
+
+int gf_generate_rays(const gf_camera_t* cam, float* o, float* d, void* stream) {
+  if (!cam || cam->width < 1 || cam->height < 1) return fail(GF_ERR_INVALID, "gf_generate_rays: bad camera");
+  launch_gen_rays(*cam, o, d, (cudaStream_t)stream);
+  return check_cuda("gf_generate_rays");
+}
+
+int gf_stage_timing(int32_t enable) {
+  g_timer.on = enable != 0;
+  g_timer.marks.clear();
+  g_timer.launches.clear();
+  g_timer.used = 0;
+  return GF_OK;
+}
+
+int gf_stage_times(double* ms_out, int64_t* launches_out) {
+  for (int s = 0; s < GF_STAGE_COUNT; ++s) {
+    if (ms_out) ms_out[s] = 0.0;
+    if (launches_out) launches_out[s] = 0;
+  }
+  cudaEvent_t prev = nullptr;
+  for (auto& m : g_timer.marks) {
+    if (m.first < 0) {
+      prev = m.second;
+      continue;
+    }
+    cudaEventSynchronize(m.second);
+    float ms = 0.f;
+    if (prev && cudaEventElapsedTime(&ms, prev, m.second) == cudaSuccess && ms_out) ms_out[m.first] += ms;
+    prev = m.second;
+  }
+  if (launches_out)
+    for (auto& l : g_timer.launches) launches_out[l.first] += l.second;
+  g_timer.marks.clear();
+  g_timer.launches.clear();
+  g_timer.used = 0;
+  return check_cuda("gf_stage_times");
+}
+
+int64_t gf_launch_count(void) { return g_launches.load(); }
+
+int gf_pcg64_block_state(uint64_t seed, uint64_t block_start, uint64_t out4[4]) {
+  u128 s, inc;
+  gf_seed_block(seed, block_start, &s, &inc);
+  out4[0] = (uint64_t)(s >> 64);
+  out4[1] = (uint64_t)s;
+  out4[2] = (uint64_t)(inc >> 64);
+  out4[3] = (uint64_t)inc;
+  return GF_OK;
+}
+
+}  // extern "C"

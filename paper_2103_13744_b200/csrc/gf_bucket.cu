@@ -1,0 +1,188 @@
+// Bucketing of samples by network cell: counting sort with a device scan.
+//
+// Reference: batched.py:60-85 group_by_network (stable argsort + bincount +
+// cumsum offsets) and grid.py:44-45 cell_index.  The render and query paths do
+// not observe the order inside a segment (each query's result depends only on
+// its own inputs and its cell's weights), so they use a warp-aggregated
+// atomic scatter; the public group_by_network entry point uses the stable
+// variant in gf_group.cu.
+#include "gf_bucket.cuh"
+
+namespace gf {
+
+// ---------------------------------------------------------------------------
+// single-CTA scan over the per-cell histogram -> segment offsets, scatter
+// cursors and the MLP tile list (one tile = up to GF_TILE_ROWS rows of one
+// cell).  Also clears the histogram for the next round.
+// ---------------------------------------------------------------------------
+template <int NT>
+__device__ __forceinline__ uint2 block_exclusive_scan2(uint2 v, uint2* warp_tot, uint2& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint2 x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t a = __shfl_up_sync(0xffffffffu, x.x, o), b = __shfl_up_sync(0xffffffffu, x.y, o);
+    if (lane >= o) { x.x += a; x.y += b; }
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint2 t = lane < NT / 32 ? warp_tot[lane] : make_uint2(0, 0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t a = __shfl_up_sync(0xffffffffu, t.x, o), b = __shfl_up_sync(0xffffffffu, t.y, o);
+      if (lane >= o) { t.x += a; t.y += b; }
+    }
+    if (lane < NT / 32) warp_tot[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  uint2 before = wid ? warp_tot[wid - 1] : make_uint2(0, 0);
+  total = warp_tot[NT / 32 - 1];
+  __syncthreads();
+  return make_uint2(before.x + x.x - v.x, before.y + x.y - v.y);
+}
+
+template <int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells) {
+  __shared__ uint2 warp_tot[NT / 32];
+  uint2 carry = make_uint2(0, 0);
+  for (int64_t chunk = 0; chunk < n_cells; chunk += (int64_t)NT * ITEMS) {
+    uint32_t cnt[ITEMS];
+    uint2 loc = make_uint2(0, 0);
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      int64_t c = chunk + (int64_t)threadIdx.x * ITEMS + j;
+      cnt[j] = c < n_cells ? B.counts[c] : 0u;
+      loc.x += cnt[j];
+      loc.y += gf_div_up<uint32_t>(cnt[j], GF_TILE_ROWS);
+    }
+    uint2 tot;
+    uint2 ex = block_exclusive_scan2<NT>(loc, warp_tot, tot);
+    ex.x += carry.x;
+    ex.y += carry.y;
+#pragma unroll
+    for (int j = 0; j < ITEMS; ++j) {
+      int64_t c = chunk + (int64_t)threadIdx.x * ITEMS + j;
+      if (c < n_cells) {
+        B.offsets[c] = ex.x;
+        B.cursor[c] = ex.x;
+        uint32_t nt = gf_div_up<uint32_t>(cnt[j], GF_TILE_ROWS);
+        for (uint32_t t = 0; t < nt; ++t) B.tiles[ex.y + t] = make_uint2((uint32_t)c, t * GF_TILE_ROWS);
+        B.counts[c] = 0;
+        ex.x += cnt[j];
+        ex.y += nt;
+      }
+    }
+    carry.x += tot.x;
+    carry.y += tot.y;
+  }
+  if (threadIdx.x == 0) {
+    B.offsets[n_cells] = carry.x;
+    *B.n_tiles = carry.y;
+  }
+}
+
+void launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st) {
+  k_scan_cells<1024, 4><<<1, 1024, 0, st>>>(B, n_cells);
+}
+
+// warp-aggregated cursor claim
+__device__ __forceinline__ uint32_t claim_slot(uint32_t* cursor, bool pred, uint32_t key) {
+  unsigned act = __ballot_sync(0xffffffffu, pred);
+  uint32_t pos = 0;
+  if (pred) {
+    unsigned peers = __match_any_sync(act, key);
+    int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if ((int)gf_lane() == leader) b = atomicAdd(&cursor[key], (uint32_t)__popc(peers));
+    b = __shfl_sync(peers, b, leader);
+    pos = b + __popc(peers & ((1u << gf_lane()) - 1u));
+  }
+  return pos;
+}
+
+// render path: records of ray i live at rec[i*stride .. +run[i])
+__global__ void __launch_bounds__(128) k_scatter_render(const float4* __restrict__ rec, const uint32_t* __restrict__ run,
+                                                        int64_t n_rays, int stride, BucketBufs B) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t n = i < n_rays ? run[i] : 0u;
+  uint32_t nmax = __reduce_max_sync(0xffffffffu, n);
+  uint64_t base = (uint64_t)i * (uint64_t)stride;
+  for (uint32_t j = 0; j < nmax; ++j) {
+    bool p = j < n;
+    uint32_t key = p ? __float_as_uint(rec[base + j].w) : 0u;
+    uint32_t pos = claim_slot(B.cursor, p, key);
+    if (p) B.sorted[pos] = (uint32_t)(base + j);
+  }
+}
+
+void launch_scatter_render(const float4* rec, const uint32_t* run, int64_t n_rays, int stride, const BucketBufs& B,
+                           cudaStream_t st) {
+  k_scatter_render<<<(unsigned)gf_div_up<int64_t>(n_rays, 128), 128, 0, st>>>(rec, run, n_rays, stride, B);
+}
+
+// query path, pass 1: bounds check (core.py:92-101), network cell, histogram
+__global__ void __launch_bounds__(256) k_query_keys(GfGrid g, const float* __restrict__ pos, int64_t n,
+                                                    uint32_t* keys, uint32_t* counts, int64_t* err) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool p = i < n;
+  uint32_t key = 0;
+  if (p) {
+    float x[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      x[a] = pos[3 * i + a];
+      // core.py:92-101 (NaN is rejected too: it has no cell)
+      if (!((double)x[a] >= g.b_min[a] && (double)x[a] <= g.b_max[a])) {
+        atomicMin((unsigned long long*)err, (unsigned long long)(3 * i + a));
+        p = false;
+      }
+    }
+    if (p) key = gf_flat_cell(g, x[0], x[1], x[2]);
+    keys[i] = p ? key : 0xFFFFFFFFu;
+  }
+  unsigned act = __ballot_sync(0xffffffffu, p);
+  if (p) {
+    unsigned peers = __match_any_sync(act, key);
+    if ((unsigned)__ffs(peers) - 1 == gf_lane()) atomicAdd(&counts[key], (uint32_t)__popc(peers));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scatter_query(const uint32_t* __restrict__ keys, int64_t n, BucketBufs B) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t key = i < n ? keys[i] : 0xFFFFFFFFu;
+  bool p = key != 0xFFFFFFFFu;
+  uint32_t pos = claim_slot(B.cursor, p, key);
+  if (p) B.sorted[pos] = (uint32_t)i;
+}
+
+// grouped_forward: segments given by offsets; rows are already in order
+__global__ void k_counts_from_offsets(const int64_t* __restrict__ offsets, int64_t n_cells, uint32_t* counts) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < n_cells) counts[c] = (uint32_t)(offsets[c + 1] - offsets[c]);
+}
+
+__global__ void k_iota(uint32_t* out, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (uint32_t)i;
+}
+
+void launch_segments_from_offsets(const int64_t* offsets, int64_t n_cells, int64_t n, const BucketBufs& B,
+                                  cudaStream_t st) {
+  k_counts_from_offsets<<<(unsigned)gf_div_up<int64_t>(n_cells, 256), 256, 0, st>>>(offsets, n_cells, B.counts);
+  launch_scan_cells(B, n_cells, st);
+  if (n > 0) k_iota<<<(unsigned)gf_div_up<int64_t>(n, 256), 256, 0, st>>>(B.sorted, n);
+}
+
+void launch_query_keys(const GfGrid& g, const float* pos, int64_t n, uint32_t* keys, uint32_t* counts, int64_t* err,
+                       cudaStream_t st) {
+  if (n == 0) return;
+  k_query_keys<<<(unsigned)gf_div_up<int64_t>(n, 256), 256, 0, st>>>(g, pos, n, keys, counts, err);
+}
+
+void launch_scatter_query(const uint32_t* keys, int64_t n, const BucketBufs& B, cudaStream_t st) {
+  if (n == 0) return;
+  k_scatter_query<<<(unsigned)gf_div_up<int64_t>(n, 256), 256, 0, st>>>(keys, n, B);
+}
+
+}  // namespace gf

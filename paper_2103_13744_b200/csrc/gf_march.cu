@@ -1,0 +1,240 @@
+// Ray marcher: ray generation, slab test, stratified PCG64 jitter, sample
+// placement, clip, empty-space skipping, per-round emission, compositing and
+// early ray termination.
+//
+// Reference: render.py:333-365 (rays, slab), render.py:481-542 (_march_block),
+// render.py:545-578 (4096-ray blocks + SeedSequence jitter streams),
+// core.py:52-112 (clip / bin), occupancy.py:65-79 (bit lookup),
+// core.py:187-194 (alpha).
+//
+// One thread owns one ray for the whole frame.  Rounds (ert_chunk samples)
+// are separate launches because the next round's live set depends on the
+// MLP results of this round (chunk-granular ERT, render.py:532-537).
+#include "gf_march.cuh"
+
+namespace gf {
+
+// -------------------------------------------------------------------------
+// per-block PCG64 seeds: SeedSequence([seed, 4096*b])   (render.py:569)
+// -------------------------------------------------------------------------
+__global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t n_blocks, u128* seeds) {
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n_blocks) return;
+  u128 s, inc;
+  gf_seed_block(seed, (uint64_t)((first_block + b) * GF_RAY_BLOCK), &s, &inc);
+  seeds[2 * b] = s;
+  seeds[2 * b + 1] = inc;
+}
+
+// -------------------------------------------------------------------------
+// ray setup: render.py:333-342 generate_rays (if camera), 368-369 f64 upcast,
+// 486-500 slab test / seg / t0 in float32, and the ray's jitter stream
+// position.
+// -------------------------------------------------------------------------
+__global__ void k_ray_init(MarchParams P, RayState R) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P.n_rays) return;
+  int64_t g = P.ray_offset + i;  // ray index within the render_rays call
+  float o32[3], d32[3];
+  if (P.use_cam) {
+    const gf_camera_t& c = P.cam;
+    int64_t px = g % c.width, py = g / c.width;
+    double u = __ddiv_rn(__dsub_rn(__dadd_rn((double)px, 0.5), c.cx), c.fx);
+    double v = __ddiv_rn(__dsub_rn(__dadd_rn((double)py, 0.5), c.cy), c.fy);
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      d[a] = __dadd_rn(__dadd_rn(__dmul_rn(u, c.c2w[4 * a + 0]), __dmul_rn(v, c.c2w[4 * a + 1])), c.c2w[4 * a + 2]);
+    double nn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2])));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      d32[a] = __double2float_rn(__ddiv_rn(d[a], nn));
+      o32[a] = __double2float_rn(c.c2w[4 * a + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      o32[a] = P.origins[3 * i + a];
+      d32[a] = P.dirs[3 * i + a];
+    }
+  }
+  // slab test in f64 (render.py:345-365)
+  double lo_max = -INFINITY, hi_min = INFINITY;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double o = (double)o32[a], d = (double)d32[a];
+    double lo, hi;
+    if (d == 0.0) {
+      bool inside = (o >= P.grid.b_min[a]) && (o <= P.grid.b_max[a]);
+      lo = inside ? -INFINITY : INFINITY;
+      hi = inside ? INFINITY : -INFINITY;
+    } else {
+      double ta = __ddiv_rn(__dsub_rn(P.grid.b_min[a], o), d);
+      double tb = __ddiv_rn(__dsub_rn(P.grid.b_max[a], o), d);
+      lo = fmin(ta, tb);
+      hi = fmax(ta, tb);
+    }
+    lo_max = fmax(lo_max, lo);
+    hi_min = fmin(hi_min, hi);
+  }
+  double t0 = fmax(lo_max, 0.0), t1 = hi_min;
+  bool hit = t1 > t0;
+  float seg = hit ? __double2float_rn(__ddiv_rn(__dsub_rn(t1, t0), (double)P.k)) : 0.0f;
+  R.org[i] = make_float4(o32[0], o32[1], o32[2], __double2float_rn(t0));
+  R.dir[i] = make_float4(d32[0], d32[1], d32[2], seg);
+  R.acc[i] = make_float4(0.f, 0.f, 0.f, 1.f);
+  R.run[i] = 0;
+  R.flags[i] = hit ? (uint8_t)(GF_RAY_ALIVE | GF_RAY_HIT) : (uint8_t)0;
+  if (P.stratified) {
+    int64_t b = g / GF_RAY_BLOCK - P.first_block;
+    uint64_t draw0 = (uint64_t)(g % GF_RAY_BLOCK) * (uint64_t)P.k;  // float32 draw index of slot 0
+    u128 s = gf_pcg_advance(P.block_seeds[2 * b], P.block_seeds[2 * b + 1], (draw0 >> 1) + 1);
+    R.rng[i] = s;
+  }
+  if (i == 0) atomicAdd((unsigned long long*)&P.stats[GF_STAT_N_RAYS], (unsigned long long)P.n_rays);
+}
+
+// warp-aggregated histogram increment: lanes with `pred` add 1 to hist[key]
+__device__ __forceinline__ void hist_add(uint32_t* hist, bool pred, uint32_t key) {
+  unsigned act = __ballot_sync(0xffffffffu, pred);
+  if (pred) {
+    unsigned peers = __match_any_sync(act, key);
+    if ((unsigned)__ffs(peers) - 1 == gf_lane()) atomicAdd(&hist[key], (uint32_t)__popc(peers));
+  }
+}
+
+__device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (gf_lane() == 0 && v) atomicAdd((unsigned long long*)dst, v);
+}
+
+// -------------------------------------------------------------------------
+// march pass r: composite round r-1 (+ERT), then place / skip / emit round r.
+// At r == n_rounds: composite the last round and write the final colours.
+// -------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundBufs B, int round) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool in_range = i < P.n_rays;
+  uint8_t flags = in_range ? R.flags[i] : 0;
+  bool final_pass = round == P.n_rounds;
+  if (!final_pass && !__any_sync(0xffffffffu, flags & GF_RAY_ALIVE)) return;
+
+  float4 acc = make_float4(0.f, 0.f, 0.f, 1.f);
+  float seg = 0.f;
+  uint64_t base = (uint64_t)i * (uint64_t)P.stride;
+  if (flags & GF_RAY_ALIVE) {
+    acc = R.acc[i];
+    seg = R.dir[i].w;
+    if (round > 0) {
+      // ---- composite round r-1 (render.py:527-531), float32, no contraction
+      uint32_t n = R.run[i];
+      float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
+      for (uint32_t j = 0; j < n; ++j) {
+        float4 q = B.res[base + j];
+        float a = -expm1f(__fmul_rn(-q.w, seg));
+        float w = __fmul_rn(tr, a);
+        tr = __fmul_rn(tr, __fsub_rn(1.0f, a));
+        sr = __fadd_rn(sr, __fmul_rn(w, q.x));
+        sg = __fadd_rn(sg, __fmul_rn(w, q.y));
+        sb = __fadd_rn(sb, __fmul_rn(w, q.z));
+      }
+      acc.x = __fadd_rn(acc.x, __fmul_rn(acc.w, sr));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(acc.w, sg));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
+      acc.w = __fmul_rn(acc.w, tr);
+      // ---- ERT after the round (render.py:532-537)
+      if (P.ert) {
+        bool dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
+        if (dead) {
+          flags &= (uint8_t)~GF_RAY_ALIVE;
+          if ((int64_t)round * P.chunk < P.k) flags |= GF_RAY_TERMINATED;  // rounds remained
+        }
+      }
+      R.acc[i] = acc;
+    }
+  } else if (final_pass && in_range) {
+    acc = R.acc[i];
+  }
+
+  if (final_pass) {
+    if (in_range) {
+      // render.py:539-542: acc + trans*bg, clip to [0,1]
+      float c0 = __fadd_rn(acc.x, __fmul_rn(acc.w, P.bg[0]));
+      float c1 = __fadd_rn(acc.y, __fmul_rn(acc.w, P.bg[1]));
+      float c2 = __fadd_rn(acc.z, __fmul_rn(acc.w, P.bg[2]));
+      P.rgb_out[3 * i + 0] = fminf(fmaxf(c0, 0.f), 1.f);
+      P.rgb_out[3 * i + 1] = fminf(fmaxf(c1, 0.f), 1.f);
+      P.rgb_out[3 * i + 2] = fminf(fmaxf(c2, 0.f), 1.f);
+    }
+    warp_add_u64(&P.stats[GF_STAT_ERT_TERMINATED], (flags & GF_RAY_TERMINATED) ? 1ull : 0ull);
+    return;
+  }
+
+  bool active = (flags & GF_RAY_ALIVE) != 0;
+  if (in_range) R.flags[i] = flags;
+  if (!__any_sync(0xffffffffu, active)) return;
+
+  // ---- sample round r (render.py:505-524)
+  int s0 = round * P.chunk;
+  int m = min(P.chunk, P.k - s0);
+  float4 o = active ? R.org[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 d = active ? R.dir[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  u128 S = 0, inc = 0;
+  uint64_t outw = 0;
+  uint64_t draw = 0;
+  if (P.stratified && active) {
+    int64_t b = (P.ray_offset + i) / GF_RAY_BLOCK - P.first_block;
+    inc = P.block_seeds[2 * b + 1];
+    S = R.rng[i];
+    outw = gf_pcg_output(S);
+    draw = (uint64_t)((P.ray_offset + i) % GF_RAY_BLOCK) * (uint64_t)P.k + (uint64_t)s0;
+  }
+  double t0 = (double)o.w, sg64 = (double)d.w;
+  uint32_t kept = 0;
+  for (int j = 0; j < m; ++j) {
+    float jit = 0.5f;
+    if (P.stratified && active) {
+      uint32_t u = (draw & 1) ? (uint32_t)(outw >> 32) : (uint32_t)outw;
+      jit = gf_u32_to_unit_float(u);
+      ++draw;
+      if (!(draw & 1)) {
+        S = gf_pcg_step(S, inc);
+        outw = gf_pcg_output(S);
+      }
+    }
+    // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
+    double t = __dadd_rn(t0, __dmul_rn(__dadd_rn((double)(s0 + j), (double)jit), sg64));
+    float px = __double2float_rn(__dadd_rn((double)o.x, __dmul_rn(t, (double)d.x)));
+    float py = __double2float_rn(__dadd_rn((double)o.y, __dmul_rn(t, (double)d.y)));
+    float pz = __double2float_rn(__dadd_rn((double)o.z, __dmul_rn(t, (double)d.z)));
+    px = gf_clip_component(px, P.grid.b_min[0], P.grid.b_max[0]);
+    py = gf_clip_component(py, P.grid.b_min[1], P.grid.b_max[1]);
+    pz = gf_clip_component(pz, P.grid.b_min[2], P.grid.b_max[2]);
+    bool keep = active;
+    if (keep && P.occ_bits) {
+      uint32_t f = gf_flat_cell(P.occ, px, py, pz);
+      keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
+    }
+    uint32_t cell = 0;
+    if (keep) {
+      cell = gf_flat_cell(P.grid, px, py, pz);
+      B.rec[base + kept] = make_float4(px, py, pz, __uint_as_float(cell));
+      if (P.trace) {
+        unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
+        if ((int64_t)slotpos < P.trace_capacity)
+          P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)(P.ray_offset + i), (uint32_t)(s0 + j), cell};
+      }
+      ++kept;
+    }
+    hist_add(B.counts, keep, cell);
+  }
+  if (active) {
+    R.run[i] = kept;
+    if (P.stratified) R.rng[i] = S;
+  }
+  warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], kept);
+  warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], active ? (unsigned long long)(m - (int)kept) : 0ull);
+}
+
+}  // namespace gf

@@ -1,0 +1,128 @@
+// Per-cell tiny-MLP evaluation: shared declarations.
+//
+// Reference: mlp.py:73-84 (layer manifest), mlp.py:222-266 (forward),
+// core.py:132-152 (positional encoding), batched.py:120-151 (grouped eval).
+#pragma once
+#include "gf_bucket.cuh"
+
+namespace gf {
+
+#define GF_MAX_LAYERS 16
+
+// Layer table for one architecture; manifest order trunk0..trunk{T-1},
+// density, feature, direction, color (mlp.py:373-384).
+struct LayerTable {
+  int n_layers, trunk, width, view, pos_dim, dir_dim;
+  int in[GF_MAX_LAYERS], out[GF_MAX_LAYERS];
+};
+
+__host__ inline bool make_layer_table(const gf_arch_t* a, LayerTable* t) {
+  if (a->hidden_layers < 3 || a->width < 1 || a->hidden_layers - 2 + 4 > GF_MAX_LAYERS) return false;
+  t->trunk = a->hidden_layers - 2;
+  t->width = a->width;
+  t->view = a->view_width > 0 ? a->view_width : a->width;
+  t->pos_dim = 3 * ((a->include_raw ? 1 : 0) + 2 * a->pos_freqs);
+  t->dir_dim = 3 * ((a->include_raw ? 1 : 0) + 2 * a->dir_freqs);
+  int l = 0;
+  t->in[l] = t->pos_dim; t->out[l++] = t->width;
+  for (int k = 1; k < t->trunk; ++k) { t->in[l] = t->width; t->out[l++] = t->width; }
+  t->in[l] = t->width; t->out[l++] = 1;                      // density
+  t->in[l] = t->width; t->out[l++] = t->width;               // feature
+  t->in[l] = t->width + t->dir_dim; t->out[l++] = t->view;   // direction
+  t->in[l] = t->view; t->out[l++] = 3;                       // color
+  t->n_layers = l;
+  return true;
+}
+
+// fp32 packed layout: per cell, per layer, W rows padded to a multiple of 4
+// floats (16-byte aligned rows for LDS.128), then the bias padded to 4.
+struct Fp32Layout {
+  int w_off[GF_MAX_LAYERS], b_off[GF_MAX_LAYERS], in_pad[GF_MAX_LAYERS];
+  int cell_floats;
+};
+
+__host__ __device__ inline int gf_pad4(int x) { return (x + 3) & ~3; }
+
+__host__ inline Fp32Layout make_fp32_layout(const LayerTable& t) {
+  Fp32Layout L;
+  int off = 0;
+  for (int l = 0; l < t.n_layers; ++l) {
+    L.in_pad[l] = gf_pad4(t.in[l]);
+    L.w_off[l] = off;
+    off += t.out[l] * L.in_pad[l];
+    L.b_off[l] = off;
+    off += gf_pad4(t.out[l]);
+  }
+  L.cell_floats = off;
+  return L;
+}
+
+// Sources / sinks of MLP rows ------------------------------------------------
+// Render: rows are kept samples in the ray-major staging buffer; the view
+// direction is the ray's (render.py:520).
+struct RenderIO {
+  const float4* rec;
+  float4* res;
+  const float4* ray_dir;
+  uint32_t stride;
+  __device__ __forceinline__ void load(uint32_t idx, float* x, float* d) const {
+    float4 r = rec[idx];
+    float4 dd = ray_dir[idx / stride];
+    x[0] = r.x; x[1] = r.y; x[2] = r.z;
+    d[0] = dd.x; d[1] = dd.y; d[2] = dd.z;
+  }
+  __device__ __forceinline__ void store(uint32_t idx, float r, float g, float b, float s) const {
+    res[idx] = make_float4(r, g, b, s);
+  }
+};
+
+// Bulk query: caller's float32 (N,3) arrays, results in caller order.
+struct QueryIO {
+  const float* pos;
+  const float* dir;
+  float* rgb;
+  float* sigma;
+  const int64_t* store_idx;  // optional: row idx is written to store_idx[idx] (grouped_forward)
+  __device__ __forceinline__ void load(uint32_t idx, float* x, float* d) const {
+    const float* p = pos + 3ull * idx;
+    const float* q = dir + 3ull * idx;
+    x[0] = p[0]; x[1] = p[1]; x[2] = p[2];
+    d[0] = q[0]; d[1] = q[1]; d[2] = q[2];
+  }
+  __device__ __forceinline__ void store(uint32_t row, float r, float g, float b, float s) const {
+    const uint64_t idx = store_idx ? (uint64_t)store_idx[row] : (uint64_t)row;
+    rgb[3ull * idx + 0] = r;
+    rgb[3ull * idx + 1] = g;
+    rgb[3ull * idx + 2] = b;
+    sigma[idx] = s;
+  }
+};
+
+struct TileSched {
+  const uint2* tiles;
+  const uint32_t* n_tiles;
+  const uint32_t* offsets;
+  const uint32_t* sorted;
+};
+
+// launchers (gf_mlp_simt.cu / gf_mlp_tc.cu); return false if the architecture
+// has no compiled variant
+bool launch_mlp_fp32_render(const LayerTable& t, const float* packed, const TileSched& S, const RenderIO& io,
+                            cudaStream_t st);
+bool launch_mlp_fp32_query(const LayerTable& t, const float* packed, const TileSched& S, const QueryIO& io,
+                           cudaStream_t st);
+bool launch_pack_fp32(const LayerTable& t, int64_t n_cells, const float* const* w, const float* const* b,
+                      float* packed, cudaStream_t st);
+
+// fp16 tcgen05 path
+size_t fp16_cell_bytes(const LayerTable& t);
+bool launch_pack_fp16(const LayerTable& t, int64_t n_cells, const float* const* w, const float* const* b,
+                      void* packed, cudaStream_t st);
+bool launch_mlp_tc_render(const LayerTable& t, const void* packed, const TileSched& S, const RenderIO& io,
+                          cudaStream_t st);
+bool launch_mlp_tc_query(const LayerTable& t, const void* packed, const TileSched& S, const QueryIO& io,
+                         cudaStream_t st);
+
+int num_sms();
+
+}  // namespace gf

@@ -1,0 +1,11 @@
+// Instantiation of the fp32 SIMT MLP kernel for hidden width 64.
+#include "gf_mlp_simt.cuh"
+
+namespace gf {
+void launch_fp32_w64(const float* packed, const Fp32Layout& L, const TileSched& S, const RenderIO& io, cudaStream_t st) {
+  launch_fp32_width<64>(packed, L, S, io, st);
+}
+void launch_fp32_w64(const float* packed, const Fp32Layout& L, const TileSched& S, const QueryIO& io, cudaStream_t st) {
+  launch_fp32_width<64>(packed, L, S, io, st);
+}
+}  // namespace gf

@@ -1,0 +1,163 @@
+"""The network lattice (mirror of gridfield.grid, /root/reference/pkg/src/gridfield/grid.py).
+
+``NetworkGrid`` keeps the reference's host-side parameter container; its
+device copy (packed per cell, in the layout the MLP kernel stages into shared
+memory) is cached per (device, precision) and rebuilt whenever the parameter
+arrays are replaced or modified in place.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from . import batched, mlp
+from .core import Aabb, PositionalEncoding, bin_point, flatten_cell_index, raise_if_out_of_bounds, validate_resolution
+
+DEFAULT_PRECISION = "fp32"
+
+
+@dataclass
+class NetworkGrid:
+    """grid.py:19-56."""
+
+    aabb: Aabb
+    resolution: np.ndarray
+    arch: mlp.MlpArchitecture
+    encoding: PositionalEncoding
+    params: mlp.MlpParams
+    precision: str | None = None  # None -> module default
+    _cache: dict = field(default_factory=dict, init=False, repr=False, compare=False)
+    _lock: object = field(default_factory=threading.Lock, init=False, repr=False, compare=False)
+
+    def __post_init__(self):
+        self.resolution = validate_resolution(self.resolution)
+        if self.params.lead_shape != (self.n_cells,):
+            raise ValueError(f"parameter stack {self.params.lead_shape} != cell count ({self.n_cells},)")
+        if self.encoding.position_dim != self.arch.position_input_dim:
+            raise ValueError("position encoding width does not match architecture input")
+        if self.encoding.direction_dim != self.arch.direction_input_dim:
+            raise ValueError("direction encoding width does not match architecture input")
+
+    @property
+    def n_cells(self) -> int:
+        return int(np.prod(self.resolution))
+
+    def cell_index(self, x: np.ndarray) -> np.ndarray:
+        """grid.py:44-45 (device binning)."""
+        return flatten_cell_index(bin_point(x, self.aabb, self.resolution), self.resolution)
+
+    def params_at(self, flat_index: int) -> mlp.MlpParams:
+        return self.params.at(flat_index)
+
+    # ---- device side -------------------------------------------------------
+    def resolved_precision(self, precision=None) -> str:
+        p = precision or self.precision or DEFAULT_PRECISION
+        if p not in N.PRECISION:
+            raise ValueError(f"unknown precision {p!r}; expected one of {sorted(N.PRECISION)}")
+        return p
+
+    def native_arch(self) -> N.Arch:
+        return N.make_arch(self.arch, self.encoding)
+
+    def native_geom(self) -> N.GridGeom:
+        return N.make_geom(self.aabb, self.resolution)
+
+    def device_params(self, precision=None):
+        """Packed per-cell parameters on the current device (cached)."""
+        p = self.resolved_precision(precision)
+        t = D.require_cuda()
+        dev = t.cuda.current_device()
+        # re-wrap plain arrays so future in-place edits are tracked
+        for d in (self.params.weights, self.params.biases):
+            for k, v in d.items():
+                if not isinstance(v, D.TrackedArray):
+                    d[k] = D.tracked(v)
+        fp = self.params.fingerprint()
+        key = (dev, p)
+        with self._lock:
+            hit = self._cache.get(key)
+            if hit is not None and hit[0] == fp:
+                return hit[1]
+            arch = self.native_arch()
+            nbytes = N.lib().gf_packed_bytes(arch, self.n_cells, N.PRECISION[p])
+            if nbytes == 0:
+                raise N.NativeError(f"architecture {self.arch} has no {p} device layout")
+            w_dev = [D.to_device(np.asarray(self.params.weights[s.name], np.float32), t.float32)
+                     for s in self.arch.layers()]
+            b_dev = [D.to_device(np.asarray(self.params.biases[s.name], np.float32), t.float32)
+                     for s in self.arch.layers()]
+            wp = (N.C.c_void_p * len(w_dev))(*[x.data_ptr() for x in w_dev])
+            bp = (N.C.c_void_p * len(b_dev))(*[x.data_ptr() for x in b_dev])
+            packed = D.workspace(nbytes)
+            N.check(N.lib().gf_pack_weights(arch, self.n_cells, wp, bp, N.ptr(packed), N.PRECISION[p],
+                                            D.stream_handle()), "pack weights")
+            t.cuda.current_stream().synchronize()
+            self._cache[key] = (fp, packed)
+            return packed
+
+    def query_points(self, positions, directions, precision=None):
+        """grid.py:50-56: bin, group by cell, evaluate, restore order — one
+        device pipeline (bin + histogram, scan, scatter, fused encode+MLP).
+        numpy in -> numpy out; torch CUDA tensors in -> tensors out."""
+        t = D.require_cuda()
+        is_tensor = isinstance(positions, t.Tensor)
+        pos_h = positions if is_tensor else np.asarray(positions)
+        n = int(pos_h.shape[0]) if pos_h.ndim > 1 else 1
+        pos = D.to_device(pos_h, t.float32).reshape(-1, 3)
+        dirs = D.to_device(directions, t.float32).reshape(-1, 3)
+        if dirs.shape[0] != pos.shape[0]:
+            raise ValueError("positions/directions/network_index lengths differ")
+        n = pos.shape[0]
+        p = self.resolved_precision(precision)
+        packed = self.device_params(p)
+        rgb = D.empty((n, 3), t.float32)
+        sigma = D.empty((n,), t.float32)
+        err = D.err_slot()
+        arch, geom = self.native_arch(), self.native_geom()
+        ws = D.workspace(N.lib().gf_query_workspace_bytes(arch, geom, n))
+        N.check(N.lib().gf_query_points(arch, geom, N.ptr(packed), N.PRECISION[p], N.ptr(pos), N.ptr(dirs), n,
+                                        N.ptr(rgb), N.ptr(sigma), N.ptr(err), N.ptr(ws), ws.numel(),
+                                        D.stream_handle()), "query_points")
+        if is_tensor:
+            if int(err.item()) != N.INT64_MAX:
+                raise_if_out_of_bounds(err, pos.cpu().numpy(), self.aabb)
+            return rgb, sigma
+        raise_if_out_of_bounds(err, np.asarray(pos_h, dtype=np.float32).reshape(-1, 3)
+                               if np.asarray(pos_h).dtype != np.float64 else np.asarray(pos_h).reshape(-1, 3),
+                               self.aabb)
+        return rgb.cpu().numpy(), sigma.cpu().numpy()
+
+
+def query_field(grid: NetworkGrid, x: np.ndarray, d: np.ndarray):
+    """grid.py:59-66: single-point query, dispatched to the owning cell."""
+    x = np.asarray(x, dtype=np.float64).reshape(1, 3)
+    dtype = grid.params.dtype
+    grid.cell_index(x)  # bounds check with the reference message
+    c, s = grid.query_points(x.astype(dtype), np.asarray(d, dtype=dtype).reshape(1, 3))
+    return c[0], s[0]
+
+
+def grid_resolution_rule(aabb: Aabb, max_dim: int = 16) -> np.ndarray:
+    """grid.py:69-77."""
+    if max_dim < 1:
+        raise ValueError("max_dim must be positive")
+    cell = aabb.extent.max() / max_dim
+    return validate_resolution(np.maximum(1, np.rint(aabb.extent / cell).astype(np.int64)))
+
+
+def init_network_grid(aabb: Aabb, resolution, seed: int, arch: mlp.MlpArchitecture | None = None,
+                      encoding: PositionalEncoding | None = None, dtype=np.float32, precision=None) -> NetworkGrid:
+    """grid.py:80-99 (identical parameter draws)."""
+    encoding = encoding or PositionalEncoding()
+    if arch is None:
+        arch = mlp.MlpArchitecture(position_input_dim=encoding.position_dim,
+                                   direction_input_dim=encoding.direction_dim)
+    resolution = validate_resolution(resolution)
+    params = mlp.init_params(arch, seed=seed, n_networks=int(np.prod(resolution)), dtype=dtype)
+    return NetworkGrid(aabb=aabb, resolution=resolution, arch=arch, encoding=encoding, params=params,
+                       precision=precision)

@@ -1,0 +1,349 @@
+"""Cameras, rays, compositing and the device ray marcher (mirror of
+gridfield.render, /root/reference/pkg/src/gridfield/render.py).
+
+``render_rays`` / ``render_image`` run the whole march on the GPU: one call
+into ``gf_render_rays`` generates (or takes) the rays, places the stratified
+samples bit-exactly like the numpy reference (same PCG64 streams per 4096-ray
+block), skips empty space, buckets the survivors by cell, evaluates the
+per-cell MLPs, composites front to back and applies chunk-granular ERT.  The
+host only transfers the camera in and the image + 4 counters out.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .core import Aabb
+
+RAY_BLOCK = 4096  # render.py:216
+
+
+@dataclass(frozen=True)
+class Camera:
+    """render.py:219-270 (pinhole; +x right, +y down, +z forward)."""
+
+    width: int
+    height: int
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    c2w: np.ndarray
+
+    def __post_init__(self):
+        if self.width < 1 or self.height < 1:
+            raise ValueError("image dimensions must be positive")
+        c2w = np.asarray(self.c2w, dtype=np.float64).reshape(4, 4)
+        r = c2w[:3, :3]
+        err = np.linalg.norm(r.T @ r - np.eye(3))
+        if err > 1e-5:
+            raise ValueError(f"pose rotation block not orthonormal (|R^T R - I| = {err:.2e})")
+        object.__setattr__(self, "c2w", c2w)
+
+    @property
+    def center(self) -> np.ndarray:
+        return self.c2w[:3, 3]
+
+    @property
+    def rotation(self) -> np.ndarray:
+        return self.c2w[:3, :3]
+
+    def scaled(self, focal_scale: float = 1.0, width: int | None = None, height: int | None = None) -> "Camera":
+        w = width or self.width
+        h = height or self.height
+        sx, sy = w / self.width, h / self.height
+        return Camera(w, h, self.fx * sx * focal_scale, self.fy * sy * focal_scale, self.cx * sx, self.cy * sy,
+                      self.c2w)
+
+
+def look_at_pose(eye, target, up=(0.0, 0.0, 1.0)) -> np.ndarray:
+    """render.py:273-294."""
+    eye = np.asarray(eye, dtype=np.float64)
+    fwd = np.asarray(target, dtype=np.float64) - eye
+    norm = np.linalg.norm(fwd)
+    if norm == 0:
+        raise ValueError("eye and target coincide")
+    z = fwd / norm
+    x = np.cross(z, np.asarray(up, dtype=np.float64))
+    if np.linalg.norm(x) < 1e-8:
+        x = np.cross(z, np.array([0.0, 1.0, 0.0]))
+    x /= np.linalg.norm(x)
+    y = np.cross(z, x)
+    c2w = np.eye(4)
+    c2w[:3, 0], c2w[:3, 1], c2w[:3, 2], c2w[:3, 3] = x, y, z, eye
+    return c2w
+
+
+@dataclass(frozen=True)
+class Ray:
+    """render.py:297-317."""
+
+    origin: np.ndarray
+    direction: np.ndarray
+    t_near: float | None = None
+    t_far: float | None = None
+
+    def __post_init__(self):
+        d = np.asarray(self.direction, dtype=np.float64)
+        if abs(np.linalg.norm(d) - 1.0) > 1e-6:
+            raise ValueError("ray direction must be unit length")
+        object.__setattr__(self, "origin", np.asarray(self.origin, dtype=np.float64))
+        object.__setattr__(self, "direction", d)
+
+    @classmethod
+    def clipped(cls, origin, direction, aabb: Aabb) -> "Ray":
+        t0, t1 = intersect_aabb(np.asarray(origin)[None], np.asarray(direction)[None], aabb)
+        return cls(origin, direction, t_near=float(t0[0]), t_far=float(t1[0]))
+
+
+def generate_ray(cam: Camera, px) -> Ray:
+    """render.py:320-330 (single ray through continuous pixel coords)."""
+    u, v = float(px[0]), float(px[1])
+    d = cam.rotation @ np.array([(u - cam.cx) / cam.fx, (v - cam.cy) / cam.fy, 1.0])
+    return Ray(cam.center, d / np.linalg.norm(d))
+
+
+def generate_rays(cam: Camera):
+    """render.py:333-342 on the device: float32 origins and unit directions,
+    row-major, bit-identical to the numpy reference."""
+    t = D.require_cuda()
+    n = cam.width * cam.height
+    o = D.empty((n, 3), t.float32)
+    d = D.empty((n, 3), t.float32)
+    N.check(N.lib().gf_generate_rays(N.make_camera(cam), N.ptr(o), N.ptr(d), D.stream_handle()), "generate_rays")
+    return o.cpu().numpy(), d.cpu().numpy()
+
+
+def intersect_aabb(origins, directions, aabb: Aabb):
+    """render.py:345-365 slab test (float64).  Host helper for single rays and
+    tests; the marcher runs its own copy of this arithmetic on the device."""
+    o = np.asarray(origins, dtype=np.float64)
+    d = np.asarray(directions, dtype=np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        t_lo = (aabb.b_min - o) / d
+        t_hi = (aabb.b_max - o) / d
+    near, far = np.minimum(t_lo, t_hi), np.maximum(t_lo, t_hi)
+    par = d == 0
+    inside = (o >= aabb.b_min) & (o <= aabb.b_max)
+    near = np.where(par, np.where(inside, -np.inf, np.inf), near)
+    far = np.where(par, np.where(inside, np.inf, -np.inf), far)
+    return np.maximum(near.max(axis=-1), 0.0), far.min(axis=-1)
+
+
+@dataclass
+class RenderConfig:
+    """render.py:368-401."""
+
+    k: int = 384
+    epsilon: float = 0.01
+    background: tuple = (1.0, 1.0, 1.0)
+    ert_chunk: int = 32
+    stratified: bool = True
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ValueError("k must be >= 1")
+        if not (0.0 <= self.epsilon < 1.0):
+            raise ValueError("epsilon must lie in [0, 1)")
+        if self.ert_chunk < 1:
+            raise ValueError("ert_chunk must be >= 1")
+
+    def replace(self, **kw) -> "RenderConfig":
+        merged = dict(k=self.k, epsilon=self.epsilon, background=self.background, ert_chunk=self.ert_chunk,
+                      stratified=self.stratified)
+        merged.update(kw)
+        return RenderConfig(**merged)
+
+    def native(self, seed: int) -> N.MarchCfg:
+        c = N.MarchCfg()
+        c.k, c.ert_chunk, c.stratified = int(self.k), int(self.ert_chunk), int(bool(self.stratified))
+        # numpy compares float32 transmittance with a Python float as float32
+        # (NEP 50); a float64 scalar forces a float64 comparison
+        c.eps_compare_f64 = int(isinstance(self.epsilon, np.floating) and np.dtype(type(self.epsilon)) == np.float64)
+        c.epsilon = float(self.epsilon)
+        for a in range(3):
+            c.background[a] = float(np.float32(self.background[a]))
+        if int(seed) < 0:
+            raise ValueError("seed must be non-negative")
+        c.seed = int(seed)
+        return c
+
+
+@dataclass
+class RenderStats:
+    """render.py:404-425."""
+
+    wall_ms: float = 0.0
+    total_queries: int = 0
+    ess_skipped: int = 0
+    ert_terminated_rays: int = 0
+    n_rays: int = 0
+
+    def merge(self, other: "RenderStats"):
+        self.total_queries += other.total_queries
+        self.ess_skipped += other.ess_skipped
+        self.ert_terminated_rays += other.ert_terminated_rays
+        self.n_rays += other.n_rays
+
+    def to_dict(self) -> dict:
+        return {"wall_ms": self.wall_ms, "total_queries": self.total_queries, "ess_skipped": self.ess_skipped,
+                "ert_terminated_rays": self.ert_terminated_rays, "n_rays": self.n_rays}
+
+
+def sample_ray(ray: Ray, aabb: Aabb, occ=None, cfg: RenderConfig | None = None, rng=None):
+    """render.py:428-460: single-ray sampler used by tests and tools (float64
+    jitter from the caller's Generator; not the marcher's path)."""
+    from .core import clip_into
+
+    cfg = cfg or RenderConfig()
+    t0, t1 = intersect_aabb(ray.origin[None], ray.direction[None], aabb)
+    t0, t1 = float(t0[0]), float(t1[0])
+    if t1 <= t0:
+        return np.zeros((0, 3), dtype=np.float32), np.zeros(0, dtype=np.float32)
+    seg = (t1 - t0) / cfg.k
+    jitter = (rng or np.random.default_rng()).random(cfg.k) if cfg.stratified else np.full(cfg.k, 0.5)
+    ts = t0 + (np.arange(cfg.k) + jitter) * seg
+    pts = clip_into((ray.origin[None, :] + ts[:, None] * ray.direction[None, :]).astype(np.float32), aabb)
+    if occ is not None:
+        pts = pts[occ.occupied_at(pts)]
+    return pts, np.full(len(pts), seg, dtype=np.float32)
+
+
+def composite(colors, alphas):
+    """render.py:463-478 on the device (float32 or float64, batch dims)."""
+    colors = np.asarray(colors)
+    alphas = np.asarray(alphas)
+    dtype = np.result_type(colors.dtype, alphas.dtype)
+    if dtype not in (np.float32, np.float64):
+        dtype = np.float64
+    lead = alphas.shape[:-1]
+    ns = alphas.shape[-1]
+    nr = int(np.prod(lead)) if lead else 1
+    if colors.shape[-2] == 0:
+        return np.zeros((*lead, 3), dtype=colors.dtype), np.ones(lead, dtype=colors.dtype)
+    t = D.require_cuda()
+    tdt = t.float64 if dtype == np.float64 else t.float32
+    cd = D.to_device(np.broadcast_to(colors, (*lead, ns, 3)).reshape(nr, ns, 3), tdt)
+    ad = D.to_device(alphas.reshape(nr, ns), tdt)
+    rgb = D.empty((nr, 3), tdt)
+    tr = D.empty((nr,), tdt)
+    fn = N.lib().gf_composite_f64 if dtype == np.float64 else N.lib().gf_composite
+    N.check(fn(N.ptr(cd), N.ptr(ad), nr, ns, N.ptr(rgb), N.ptr(tr), D.stream_handle()), "composite")
+    rgb_h = rgb.cpu().numpy().reshape(*lead, 3)
+    tr_h = tr.cpu().numpy().reshape(lead)
+    return rgb_h, (tr_h if lead else tr_h[()])
+
+
+# ---------------------------------------------------------------------------
+# the marcher
+# ---------------------------------------------------------------------------
+def _field_grid(field):
+    from .grid import NetworkGrid
+
+    if isinstance(field, NetworkGrid):
+        return field
+    raise NotImplementedError(
+        f"the device marcher evaluates NetworkGrid fields; got {type(field).__name__} "
+        "(analytic fields are not on the B200 hot path yet)"
+    )
+
+
+def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camera | None = None, origins=None,
+                       directions=None, ray_offset: int = 0, n_rays: int | None = None, precision=None,
+                       out=None, stats=None, trace_capacity: int = 0):
+    """Device-resident core of render_rays / render_image.  Returns
+    (rgb (n,3) float32 CUDA tensor, stats int64[4] CUDA tensor, trace or None).
+    ``origins``/``directions`` may be CUDA tensors; ``cam`` generates rays
+    for pixels [ray_offset, ray_offset + n_rays)."""
+    t = D.require_cuda()
+    p = grid.resolved_precision(precision)
+    packed = grid.device_params(p)
+    if cam is not None:
+        total = cam.width * cam.height
+        n = total - ray_offset if n_rays is None else int(n_rays)
+        o_d = d_d = None
+        ccam = N.make_camera(cam)
+    else:
+        o_d = D.to_device(origins, t.float32).reshape(-1, 3)
+        d_d = D.to_device(directions, t.float32).reshape(-1, 3)
+        n = o_d.shape[0]
+        ccam = None
+    ncfg = cfg.native(seed)
+    arch, geom = grid.native_arch(), grid.native_geom()
+    if occupancy is not None:
+        occ_geom, occ_bits = occupancy.native_geom(), occupancy.device_bits()
+    else:
+        occ_geom, occ_bits = None, None
+    rgb = out if out is not None else D.empty((n, 3), t.float32)
+    st = stats if stats is not None else t.zeros(4, dtype=t.int64, device=rgb.device)
+    trace = tcount = None
+    if trace_capacity:
+        trace = D.empty((trace_capacity * N.TRACE_DTYPE.itemsize,), t.uint8)
+        tcount = t.zeros(1, dtype=t.int64, device=rgb.device)
+    ws = D.workspace(N.lib().gf_render_workspace_bytes(arch, geom, ncfg, n))
+    N.check(N.lib().gf_render_rays(
+        arch, geom, N.ptr(packed), N.PRECISION[p], occ_geom, N.ptr(occ_bits), ncfg, ccam, N.ptr(o_d), N.ptr(d_d),
+        int(ray_offset), int(n), N.ptr(rgb), N.ptr(st), N.ptr(trace), int(trace_capacity), N.ptr(tcount),
+        N.ptr(ws), ws.numel(), D.stream_handle()), "render_rays")
+    tr = None
+    if trace_capacity:
+        cnt = int(tcount.item())
+        if cnt > trace_capacity:
+            raise RuntimeError(f"trace capacity {trace_capacity} too small for {cnt} samples")
+        tr = np.frombuffer(trace[: cnt * N.TRACE_DTYPE.itemsize].cpu().numpy().tobytes(), dtype=N.TRACE_DTYPE)
+    return rgb, st, tr
+
+
+def _stats_from(st) -> RenderStats:
+    v = [int(x) for x in st.cpu().tolist()]
+    return RenderStats(total_queries=v[0], ess_skipped=v[1], ert_terminated_rays=v[2], n_rays=v[3])
+
+
+def render_rays(field, occupancy, origins, directions, cfg: RenderConfig, seed: int = 0, workers: int = 1,
+                precision=None):
+    """render.py:545-578.  ``workers`` is accepted for API compatibility; the
+    device result is identical for any value (ray blocks keep their own
+    jitter streams)."""
+    grid = _field_grid(field)
+    o = np.asarray(origins, dtype=np.float64).reshape(-1, 3)
+    d = np.asarray(directions, dtype=np.float64).reshape(-1, 3)
+    # render.py:562-563 upcasts to float64 and the slab test runs on those
+    # values; the device takes float32 rays, so float64 rays must round-trip
+    if not (np.array_equal(o.astype(np.float32).astype(np.float64), o)
+            and np.array_equal(d.astype(np.float32).astype(np.float64), d)):
+        raise ValueError("render_rays on the device requires float32-representable origins/directions")
+    rgb, st, _ = render_rays_device(grid, occupancy, cfg, seed, origins=o.astype(np.float32),
+                                    directions=d.astype(np.float32), precision=precision)
+    return rgb.cpu().numpy(), _stats_from(st)
+
+
+def render_image(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0, workers: int = 1,
+                 precision=None):
+    """render.py:581-594: full frame; stats.wall_ms covers ray generation
+    through the image landing in host memory."""
+    t_start = time.perf_counter()
+    grid = _field_grid(field)
+    t = D.require_cuda()
+    rgb, st, _ = render_rays_device(grid, occupancy, cfg, seed, cam=cam, precision=precision)
+    host = t.empty(rgb.shape, dtype=t.float32, pin_memory=True)
+    host.copy_(rgb, non_blocking=True)
+    stats_h = t.empty(4, dtype=t.int64, pin_memory=True)
+    stats_h.copy_(st, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    stats = _stats_from(stats_h)
+    stats.wall_ms = (time.perf_counter() - t_start) * 1000.0
+    return host.numpy().reshape(cam.height, cam.width, 3), stats
+
+
+def compute_psnr(a, b) -> float:
+    """render.py:597-607."""
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape:
+        raise ValueError(f"image shapes differ: {a.shape} vs {b.shape}")
+    mse = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+    return float("inf") if mse == 0.0 else 10.0 * np.log10(1.0 / mse)
