@@ -172,7 +172,10 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
   }
 
   bool active = (flags & GF_RAY_ALIVE) != 0;
-  if (in_range) R.flags[i] = flags;
+  if (in_range) {
+    R.flags[i] = flags;
+    if (!active) R.run[i] = 0;  // a ray that stops here must not re-emit last round's samples
+  }
   if (!__any_sync(0xffffffffu, active)) return;
 
   // ---- sample round r (render.py:505-524)
