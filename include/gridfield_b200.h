@@ -131,7 +131,10 @@ GF_API int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void
  * Rays come either from `cam` (pixel index = ray_offset + i, row-major) or
  * from float32 origins/directions (ray i of the call is global ray
  * ray_offset + i).  ray_offset selects the 4096-ray jitter blocks so shards of
- * one image reproduce the single-device image bit for bit.  occ_bits_dev may
+ * one image reproduce the single-device image bit for bit.  With
+ * ray_block_stride S > 1 (block-aligned ray_offset) the call's rays are the
+ * interleaved blocks ray_offset/4096 + k*S (k = 0, 1, ...) — the balanced
+ * multi-GPU partition; origins/dirs/rgb stay compact (n_rays rows).  occ_bits_dev may
  * be NULL (no empty-space skipping).  stats_dev: int64[GF_STAT_COUNT],
  * accumulated (caller zeroes).  trace_dev / trace_count_dev may be NULL.   */
 GF_API size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* grid, const gf_march_cfg_t* cfg,
@@ -139,7 +142,7 @@ GF_API size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geo
 GF_API int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed_dev, int precision,
                    const gf_grid_geom_t* occ, const uint8_t* occ_bits_dev, const gf_march_cfg_t* cfg,
                    const gf_camera_t* cam, const float* origins_dev, const float* dirs_dev, int64_t ray_offset,
-                   int64_t n_rays, float* rgb_dev, int64_t* stats_dev, gf_trace_rec_t* trace_dev,
+                   int64_t ray_block_stride, int64_t n_rays, float* rgb_dev, int64_t* stats_dev, gf_trace_rec_t* trace_dev,
                    int64_t trace_capacity, int64_t* trace_count_dev, void* ws_dev, size_t ws_bytes, void* stream);
 
 /* --- batched.group_by_network (batched.py:60-85) --------------------------

@@ -64,7 +64,8 @@ _SIGS = {
                                      _P, C.c_size_t, _P]),
     "gf_render_workspace_bytes": (C.c_size_t, [C.POINTER(Arch), C.POINTER(GridGeom), C.POINTER(MarchCfg), C.c_int64]),
     "gf_render_rays": (C.c_int, [C.POINTER(Arch), C.POINTER(GridGeom), _P, C.c_int, C.POINTER(GridGeom), _P,
-                                 C.POINTER(MarchCfg), C.POINTER(CameraT), _P, _P, C.c_int64, C.c_int64, _P, _P, _P,
+                                 C.POINTER(MarchCfg), C.POINTER(CameraT), _P, _P, C.c_int64, C.c_int64, C.c_int64,
+                                 _P, _P, _P,
                                  C.c_int64, _P, _P, C.c_size_t, _P]),
     "gf_group_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int64]),
     "gf_group_by_key": (C.c_int, [_P, C.c_int64, C.c_int64, _P, _P, _P, _P, _P, C.c_size_t, _P]),

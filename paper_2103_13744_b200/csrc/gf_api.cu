@@ -3,6 +3,8 @@
 // Host-side orchestration only: argument validation, workspace carving and
 // the launch sequence of the render / query pipelines on the caller's stream.
 #include <cstdio>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -256,11 +258,19 @@ struct RenderWs {
   RayState R;
   RoundBufs RB;
   BucketBufs B;
+  uint8_t* coarse_tmp;
+  uint32_t* coarse_bits;
 };
+
+// occupancy grids are capped at 256^3 (occupancy.py:21); the coarse mip never
+// exceeds that many cells
+static const int64_t kMaxCoarseCells = 256ll * 256 * 256;
 
 static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int stride, int64_t n_cells, RenderWs* w) {
   const size_t cap = (size_t)n_rays * (size_t)stride;
   w->seeds = c.take<u128>((size_t)2 * n_blocks);
+  w->coarse_tmp = c.take<uint8_t>((size_t)kMaxCoarseCells);
+  w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->R.org = c.take<float4>((size_t)n_rays);
   w->R.dir = c.take<float4>((size_t)n_rays);
   w->R.acc = c.take<float4>((size_t)n_rays);
@@ -279,8 +289,12 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   return c.size();
 }
 
-static void block_range(int64_t ray_offset, int64_t n_rays, int64_t* first, int64_t* count) {
+static void block_range(int64_t ray_offset, int64_t block_stride, int64_t n_rays, int64_t* first, int64_t* count) {
   *first = ray_offset / GF_RAY_BLOCK;
+  if (block_stride > 1) {
+    *count = n_rays > 0 ? (n_rays + GF_RAY_BLOCK - 1) / GF_RAY_BLOCK : 1;
+    return;
+  }
   int64_t last = n_rays > 0 ? (ray_offset + n_rays - 1) / GF_RAY_BLOCK : *first;
   *count = last - *first + 1;
 }
@@ -299,7 +313,7 @@ size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* gr
 int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed, int precision,
                    const gf_grid_geom_t* occ, const uint8_t* occ_bits, const gf_march_cfg_t* cfg,
                    const gf_camera_t* cam, const float* origins, const float* dirs, int64_t ray_offset,
-                   int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace, int64_t trace_capacity,
+                   int64_t ray_block_stride, int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace, int64_t trace_capacity,
                    int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
   LayerTable t;
   if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_render_rays: bad architecture");
@@ -308,13 +322,15 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
     return fail(GF_ERR_INVALID, "gf_render_rays: bad march config");
   if (occ_bits && !valid_grid(occ)) return fail(GF_ERR_INVALID, "gf_render_rays: bad occupancy grid");
   if (!cam && (!origins || !dirs) && n_rays > 0) return fail(GF_ERR_INVALID, "gf_render_rays: no rays");
-  if (ray_offset < 0 || n_rays < 0) return fail(GF_ERR_INVALID, "gf_render_rays: bad ray range");
+  if (ray_offset < 0 || n_rays < 0 || ray_block_stride < 1) return fail(GF_ERR_INVALID, "gf_render_rays: bad ray range");
+  if (ray_block_stride > 1 && ray_offset % GF_RAY_BLOCK)
+    return fail(GF_ERR_INVALID, "gf_render_rays: interleaved shards need a block-aligned ray_offset");
   const int stride = cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k;
   if ((double)n_rays * stride >= 4.0e9) return fail(GF_ERR_INVALID, "gf_render_rays: too many rays per call");
   if (n_rays == 0) return GF_OK;
   const int64_t nc = n_cells_of(grid);
   int64_t first_block, n_blocks;
-  block_range(ray_offset, n_rays, &first_block, &n_blocks);
+  block_range(ray_offset, ray_block_stride, n_rays, &first_block, &n_blocks);
   Carve c(ws);
   RenderWs w;
   if (render_carve(c, n_rays, n_blocks, stride, nc, &w) > ws_bytes)
@@ -333,6 +349,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   P.origins = origins;
   P.dirs = dirs;
   P.ray_offset = ray_offset;
+  P.block_stride = ray_block_stride;
   P.n_rays = n_rays;
   P.first_block = first_block;
   P.block_seeds = w.seeds;
@@ -351,13 +368,56 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   P.trace_capacity = trace ? trace_capacity : 0;
   P.trace_count = trace_count;
 
+  // ---- coarse empty-space pre-test: a mip of the occupancy
+  // grid dilated by the largest distance between a sample and the midpoint
+  // of its nominal segment (seg/2) plus a float32 evaluation margin.
+  int coarse_launches = 0;
+  {
+    const char* no = getenv("GF_NO_COARSE");
+    bool same_box = occ_bits != nullptr;
+    for (int a = 0; a < 3 && same_box; ++a)
+      same_box = occ->b_min[a] == grid->b_min[a] && occ->b_max[a] == grid->b_max[a];
+    if (same_box && !(no && no[0] == '1')) {
+      double diag2 = 0, maxabs = 0;
+      for (int a = 0; a < 3; ++a) {
+        double e = grid->b_max[a] - grid->b_min[a];
+        diag2 += e * e;
+        maxabs = fmax(maxabs, fmax(fabs(grid->b_min[a]), fabs(grid->b_max[a])));
+      }
+      const double reach = 0.5 * sqrt(diag2) / cfg->k * 1.0001 + 1e-5 * (1.0 + maxabs);
+      const char* fenv = getenv("GF_COARSE_FACTOR");
+      const int want = fenv ? atoi(fenv) : 2;
+      int f = 0, radius = 0;
+      for (int cand : {want, 1, 2, 4, 8}) {
+        if (cand < 1 || occ->res[0] % cand || occ->res[1] % cand || occ->res[2] % cand) continue;
+        double cmin = 1e300;
+        for (int a = 0; a < 3; ++a) cmin = fmin(cmin, (occ->b_max[a] - occ->b_min[a]) / occ->res[a] * cand);
+        const int r = (int)ceil(reach / cmin);
+        if (r <= 2) { f = cand; radius = r < 1 ? 1 : r; break; }
+      }
+      if (f) {
+        int3 ores = make_int3(occ->res[0], occ->res[1], occ->res[2]);
+        int3 cres = make_int3(ores.x / f, ores.y / f, ores.z / f);
+        const int64_t ncc = (int64_t)cres.x * cres.y * cres.z;
+        k_coarse_reduce<<<(unsigned)gf_div_up<int64_t>(ncc, 256), 256, 0, st>>>(occ_bits, ores, f, cres, w.coarse_tmp);
+        k_coarse_dilate<<<(unsigned)gf_div_up<int64_t>(gf_div_up<int64_t>(ncc, 32), 128), 128, 0, st>>>(
+            w.coarse_tmp, cres, radius, w.coarse_bits);
+        gf_grid_geom_t cg = *occ;
+        cg.res[0] = cres.x; cg.res[1] = cres.y; cg.res[2] = cres.z;
+        P.coarse = gf_make_grid(&cg);
+        P.coarse_bits = w.coarse_bits;
+        coarse_launches = 2;
+      }
+    }
+  }
+
   stage_open(st);
   cudaMemsetAsync(w.B.counts, 0, (size_t)nc * 4, st);
-  if (P.stratified) k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(n_blocks, 64), 64, 0, st>>>(cfg->seed, first_block,
-                                                                                              n_blocks, w.seeds);
+  if (P.stratified) k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(n_blocks, 64), 64, 0, st>>>(
+      cfg->seed, first_block, ray_block_stride, n_blocks, w.seeds);
   const unsigned ray_blocks = (unsigned)gf_div_up<int64_t>(n_rays, 128);
   k_ray_init<<<ray_blocks, 128, 0, st>>>(P, w.R);
-  stage_mark(st, GF_STAGE_SETUP, P.stratified ? 2 : 1);
+  stage_mark(st, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
   TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
   RenderIO io{w.RB.rec, w.RB.res, w.R.dir, (uint32_t)stride};
   for (int r = 0; r < P.n_rounds; ++r) {

@@ -107,25 +107,52 @@ __device__ __forceinline__ float gf_u32_to_unit_float(uint32_t u) {
 // ---------------------------------------------------------------------------
 struct GfGrid {
   double b_min[3], b_max[3], cell[3], inv_cell[3];
+  float b_min_f[3], b_max_f[3], inv_cell_f[3];
   int32_t res[3];
-  int32_t pow2;  // all cell sizes are powers of two: x*inv is exact == x/cell
+  int32_t pow2;    // all cell sizes are powers of two: x*inv is exact == x/cell
+  int32_t fast;    // pow2 && bounds exactly representable in float32 (see gf_bin_axis_fast)
 };
 
 __host__ inline GfGrid gf_make_grid(const gf_grid_geom_t* g) {
   GfGrid o;
-  bool p2 = true;
+  bool p2 = true, f32 = true;
   for (int a = 0; a < 3; ++a) {
     o.b_min[a] = g->b_min[a];
     o.b_max[a] = g->b_max[a];
     o.res[a] = g->res[a];
     o.cell[a] = (g->b_max[a] - g->b_min[a]) / (double)g->res[a];
     o.inv_cell[a] = 1.0 / o.cell[a];
+    o.b_min_f[a] = (float)g->b_min[a];
+    o.b_max_f[a] = (float)g->b_max[a];
+    o.inv_cell_f[a] = (float)o.inv_cell[a];
     int e;
     double m = frexp(o.cell[a], &e);
     if (m != 0.5) p2 = false;
+    if ((double)o.b_min_f[a] != g->b_min[a] || (double)o.b_max_f[a] != g->b_max[a] || g->res[a] > (1 << 22) ||
+        (double)o.inv_cell_f[a] != o.inv_cell[a])
+      f32 = false;
   }
   o.pow2 = p2 ? 1 : 0;
+  o.fast = (p2 && f32) ? 1 : 0;
   return o;
+}
+
+// Exact float32 route to floor((f64(x) - b_min) / cell) for x >= b_min, valid
+// when b_min is float32-exact and cell is a power of two (grid.fast):
+// y = RZ(x - b_min) is the largest float <= the exact difference v, and every
+// cell boundary n*cell is a float, so y >= n*cell <=> v >= n*cell; y*inv is an
+// exact power-of-two scaling; adding 2^23 with round-toward-zero leaves
+// floor(q) in the mantissa.  No FP64 and no F2I conversions.
+__device__ __forceinline__ int gf_bin_axis_fast(const GfGrid& g, int a, float x) {
+  const float q = __fmul_rn(__fsub_rz(x, g.b_min_f[a]), g.inv_cell_f[a]);
+  int i = __float_as_int(__fadd_rz(q, 8388608.0f)) - 0x4B000000;
+  i = i < 0 ? 0 : i;
+  return i < g.res[a] - 1 ? i : g.res[a] - 1;
+}
+
+__device__ __forceinline__ uint32_t gf_flat_cell_fast(const GfGrid& g, float x, float y, float z) {
+  int ix = gf_bin_axis_fast(g, 0, x), iy = gf_bin_axis_fast(g, 1, y), iz = gf_bin_axis_fast(g, 2, z);
+  return (uint32_t)(ix + g.res[0] * (iy + g.res[1] * iz));
 }
 
 // floor((f64(x) - b_min) / cell) clamped to res-1; caller guarantees in-bounds.
@@ -149,6 +176,7 @@ __device__ __forceinline__ uint32_t gf_flat_cell(const GfGrid& g, double x, doub
 }
 
 __device__ __forceinline__ uint32_t gf_flat_cell(const GfGrid& g, float x, float y, float z) {
+  if (g.fast) return gf_flat_cell_fast(g, x, y, z);
   int ix = gf_bin_axis(g, 0, x), iy = gf_bin_axis(g, 1, y), iz = gf_bin_axis(g, 2, z);
   return (uint32_t)(ix + g.res[0] * (iy + g.res[1] * iz));
 }
@@ -163,6 +191,10 @@ __device__ __forceinline__ float gf_clip_component(float p, double lo, double hi
   if ((double)c < lo) c = nextafterf(c, INFINITY);
   return c;
 }
+
+// clip_into when the bounds are float32-exact (grid.fast): clamping in f64 and
+// casting back can then never leave the box, so it is a float32 clamp.
+__device__ __forceinline__ float gf_clip_fast(float p, float lo, float hi) { return fminf(fmaxf(p, lo), hi); }
 
 // ---------------------------------------------------------------------------
 // misc

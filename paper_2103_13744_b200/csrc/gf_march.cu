@@ -17,11 +17,12 @@ namespace gf {
 // -------------------------------------------------------------------------
 // per-block PCG64 seeds: SeedSequence([seed, 4096*b])   (render.py:569)
 // -------------------------------------------------------------------------
-__global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t n_blocks, u128* seeds) {
+__global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
+                              u128* seeds) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n_blocks) return;
   u128 s, inc;
-  gf_seed_block(seed, (uint64_t)((first_block + b) * GF_RAY_BLOCK), &s, &inc);
+  gf_seed_block(seed, (uint64_t)((first_block + b * block_stride) * GF_RAY_BLOCK), &s, &inc);
   seeds[2 * b] = s;
   seeds[2 * b + 1] = inc;
 }
@@ -34,7 +35,7 @@ __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t n_bloc
 __global__ void k_ray_init(MarchParams P, RayState R) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.n_rays) return;
-  int64_t g = P.ray_offset + i;  // ray index within the render_rays call
+  const int64_t g = global_ray(P, i);  // ray index within the render_rays call
   float o32[3], d32[3];
   if (P.use_cam) {
     const gf_camera_t& c = P.cam;
@@ -86,12 +87,50 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
   R.run[i] = 0;
   R.flags[i] = hit ? (uint8_t)(GF_RAY_ALIVE | GF_RAY_HIT) : (uint8_t)0;
   if (P.stratified) {
-    int64_t b = g / GF_RAY_BLOCK - P.first_block;
+    const int64_t b = seed_slot(P, g);
     uint64_t draw0 = (uint64_t)(g % GF_RAY_BLOCK) * (uint64_t)P.k;  // float32 draw index of slot 0
     u128 s = gf_pcg_advance(P.block_seeds[2 * b], P.block_seeds[2 * b + 1], (draw0 >> 1) + 1);
     R.rng[i] = s;
   }
   if (i == 0) atomicAdd((unsigned long long*)&P.stats[GF_STAT_N_RAYS], (unsigned long long)P.n_rays);
+}
+
+// -------------------------------------------------------------------------
+// coarse occupancy mip: OR over factor^3 fine cells, then dilation by
+// `radius` coarse cells (Chebyshev), stored as bits.
+// -------------------------------------------------------------------------
+__global__ void k_coarse_reduce(const uint8_t* __restrict__ occ_bits, int3 ores, int f, int3 cres, uint8_t* coarse) {
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)cres.x * cres.y * cres.z;
+  if (c >= n) return;
+  const int cx = (int)(c % cres.x), cy = (int)((c / cres.x) % cres.y), cz = (int)(c / ((int64_t)cres.x * cres.y));
+  uint8_t any = 0;
+  for (int z = cz * f; z < cz * f + f && !any; ++z)
+    for (int y = cy * f; y < cy * f + f && !any; ++y)
+      for (int x = cx * f; x < cx * f + f; ++x) {
+        const int64_t fi = x + (int64_t)ores.x * (y + (int64_t)ores.y * z);
+        if ((occ_bits[fi >> 3] >> (fi & 7)) & 1) { any = 1; break; }
+      }
+  coarse[c] = any;
+}
+
+__global__ void k_coarse_dilate(const uint8_t* __restrict__ coarse, int3 cres, int r, uint32_t* bits) {
+  int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 32-bit word per thread
+  const int64_t n = (int64_t)cres.x * cres.y * cres.z;
+  if (w * 32 >= n) return;
+  uint32_t word = 0;
+  for (int b = 0; b < 32; ++b) {
+    const int64_t c = w * 32 + b;
+    if (c >= n) break;
+    const int cx = (int)(c % cres.x), cy = (int)((c / cres.x) % cres.y), cz = (int)(c / ((int64_t)cres.x * cres.y));
+    bool any = false;
+    for (int z = max(cz - r, 0); z <= min(cz + r, cres.z - 1) && !any; ++z)
+      for (int y = max(cy - r, 0); y <= min(cy + r, cres.y - 1) && !any; ++y)
+        for (int x = max(cx - r, 0); x <= min(cx + r, cres.x - 1); ++x)
+          if (coarse[x + (int64_t)cres.x * (y + (int64_t)cres.y * z)]) { any = true; break; }
+    if (any) word |= 1u << b;
+  }
+  bits[w] = word;
 }
 
 // warp-aggregated histogram increment: lanes with `pred` add 1 to hist[key]
@@ -187,48 +226,82 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
   uint64_t outw = 0;
   uint64_t draw = 0;
   if (P.stratified && active) {
-    int64_t b = (P.ray_offset + i) / GF_RAY_BLOCK - P.first_block;
-    inc = P.block_seeds[2 * b + 1];
+    const int64_t g = global_ray(P, i);
+    inc = P.block_seeds[2 * seed_slot(P, g) + 1];
     S = R.rng[i];
     outw = gf_pcg_output(S);
-    draw = (uint64_t)((P.ray_offset + i) % GF_RAY_BLOCK) * (uint64_t)P.k + (uint64_t)s0;
+    draw = (uint64_t)(g % GF_RAY_BLOCK) * (uint64_t)P.k + (uint64_t)s0;
   }
-  double t0 = (double)o.w, sg64 = (double)d.w;
+  const double t0 = (double)o.w, sg64 = (double)d.w;
+  const double ox = (double)o.x, oy = (double)o.y, oz = (double)o.z;
+  const double dx = (double)d.x, dy = (double)d.y, dz = (double)d.z;
+  // entry point for the conservative coarse test (relative to it, the f32
+  // evaluation error stays ~1e-7 of the box size whatever the camera distance)
+  float ex = 0.f, ey = 0.f, ez = 0.f;
+  if (P.coarse_bits && active) {
+    ex = __double2float_rn(__dadd_rn(ox, __dmul_rn(t0, dx)));
+    ey = __double2float_rn(__dadd_rn(oy, __dmul_rn(t0, dy)));
+    ez = __double2float_rn(__dadd_rn(oz, __dmul_rn(t0, dz)));
+  }
+  const bool fast_clip = P.grid.fast != 0;
   uint32_t kept = 0;
-  for (int j = 0; j < m; ++j) {
-    float jit = 0.5f;
+  double jd = (double)s0;
+  float jm = (float)s0 + 0.5f;
+  for (int j = 0; j < m; ++j, jd += 1.0, jm += 1.0f) {
+    double jit = 0.5;
     if (P.stratified && active) {
-      uint32_t u = (draw & 1) ? (uint32_t)(outw >> 32) : (uint32_t)outw;
-      jit = gf_u32_to_unit_float(u);
+      const uint32_t u = (draw & 1) ? (uint32_t)(outw >> 32) : (uint32_t)outw;
+      // (u >> 8) * 2^-24 exactly, built in f64 without an I2F conversion
+      jit = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, (int)(u >> 8)), 4503599627370496.0),
+                      5.9604644775390625e-8);
       ++draw;
       if (!(draw & 1)) {
         S = gf_pcg_step(S, inc);
         outw = gf_pcg_output(S);
       }
     }
-    // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
-    double t = __dadd_rn(t0, __dmul_rn(__dadd_rn((double)(s0 + j), (double)jit), sg64));
-    float px = __double2float_rn(__dadd_rn((double)o.x, __dmul_rn(t, (double)d.x)));
-    float py = __double2float_rn(__dadd_rn((double)o.y, __dmul_rn(t, (double)d.y)));
-    float pz = __double2float_rn(__dadd_rn((double)o.z, __dmul_rn(t, (double)d.z)));
-    px = gf_clip_component(px, P.grid.b_min[0], P.grid.b_max[0]);
-    py = gf_clip_component(py, P.grid.b_min[1], P.grid.b_max[1]);
-    pz = gf_clip_component(pz, P.grid.b_min[2], P.grid.b_max[2]);
-    bool keep = active;
-    if (keep && P.occ_bits) {
-      uint32_t f = gf_flat_cell(P.occ, px, py, pz);
-      keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
+    // coarse test: the sample lies within seg/2 (+margin) of the segment
+    // midpoint; the mip is dilated by that radius, so a clear bit proves the
+    // exact sample is in an empty fine cell (skipped, counted in ess_skipped)
+    bool cand = active;
+    if (P.coarse_bits && cand) {
+      const float sm = jm * d.w;
+      const float cx = fmaf(sm, d.x, ex), cy = fmaf(sm, d.y, ey), cz = fmaf(sm, d.z, ez);
+      const uint32_t cf = gf_coarse_cell(P.coarse, cx, cy, cz);
+      cand = (__ldg(P.coarse_bits + (cf >> 5)) >> (cf & 31)) & 1;
     }
+    bool keep = false;
     uint32_t cell = 0;
-    if (keep) {
-      cell = gf_flat_cell(P.grid, px, py, pz);
-      B.rec[base + kept] = make_float4(px, py, pz, __uint_as_float(cell));
-      if (P.trace) {
-        unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
-        if ((int64_t)slotpos < P.trace_capacity)
-          P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)(P.ray_offset + i), (uint32_t)(s0 + j), cell};
+    if (__any_sync(0xffffffffu, cand) && cand) {
+      // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
+      const double t = __dadd_rn(t0, __dmul_rn(__dadd_rn(jd, jit), sg64));
+      float px = __double2float_rn(__dadd_rn(ox, __dmul_rn(t, dx)));
+      float py = __double2float_rn(__dadd_rn(oy, __dmul_rn(t, dy)));
+      float pz = __double2float_rn(__dadd_rn(oz, __dmul_rn(t, dz)));
+      if (fast_clip) {
+        px = gf_clip_fast(px, P.grid.b_min_f[0], P.grid.b_max_f[0]);
+        py = gf_clip_fast(py, P.grid.b_min_f[1], P.grid.b_max_f[1]);
+        pz = gf_clip_fast(pz, P.grid.b_min_f[2], P.grid.b_max_f[2]);
+      } else {
+        px = gf_clip_component(px, P.grid.b_min[0], P.grid.b_max[0]);
+        py = gf_clip_component(py, P.grid.b_min[1], P.grid.b_max[1]);
+        pz = gf_clip_component(pz, P.grid.b_min[2], P.grid.b_max[2]);
       }
-      ++kept;
+      keep = true;
+      if (P.occ_bits) {
+        const uint32_t f = gf_flat_cell(P.occ, px, py, pz);
+        keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
+      }
+      if (keep) {
+        cell = gf_flat_cell(P.grid, px, py, pz);
+        B.rec[base + kept] = make_float4(px, py, pz, __uint_as_float(cell));
+        if (P.trace) {
+          unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
+          if ((int64_t)slotpos < P.trace_capacity)
+            P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, i), (uint32_t)(s0 + j), cell};
+        }
+        ++kept;
+      }
     }
     hist_add(B.counts, keep, cell);
   }

@@ -12,11 +12,13 @@ struct MarchParams {
   GfGrid grid;        // network lattice geometry (cell keys)
   GfGrid occ;         // occupancy geometry
   const uint8_t* occ_bits;
+  GfGrid coarse;      // dilated coarse occupancy mip (empty-space pre-test)
+  const uint32_t* coarse_bits;  // NULL: every candidate takes the exact path
   gf_camera_t cam;
   int use_cam;
   const float* origins;
   const float* dirs;
-  int64_t ray_offset, n_rays, first_block;
+  int64_t ray_offset, n_rays, first_block, block_stride;
   const u128* block_seeds;  // [2*b] state, [2*b+1] inc
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
   double epsilon;
@@ -47,8 +49,37 @@ struct RoundBufs {
   uint32_t* counts;   // per-cell histogram of this round
 };
 
-__global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t n_blocks, u128* seeds);
+// Global index (within the render_rays call) of the call's local ray i.
+// block_stride S > 1 interleaves 4096-ray blocks across shards: local block
+// lb is global block ray_offset/4096 + lb*S (ray_offset is block-aligned).
+__device__ __forceinline__ int64_t global_ray(const MarchParams& P, int64_t i) {
+  if (P.block_stride == 1) return P.ray_offset + i;
+  return P.ray_offset + (i / GF_RAY_BLOCK) * P.block_stride * GF_RAY_BLOCK + i % GF_RAY_BLOCK;
+}
+// slot of the ray's block in the per-call seed table
+__device__ __forceinline__ int64_t seed_slot(const MarchParams& P, int64_t g) {
+  return (g / GF_RAY_BLOCK - P.first_block) / P.block_stride;
+}
+
+__global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
+                              u128* seeds);
 __global__ void k_ray_init(MarchParams P, RayState R);
+__global__ void k_coarse_reduce(const uint8_t* occ_bits, int3 occ_res, int factor, int3 cres, uint8_t* coarse);
+__global__ void k_coarse_dilate(const uint8_t* coarse, int3 cres, int radius, uint32_t* bits);
+
+// Approximate (clamped) coarse cell of a float32 point; exactness is not
+// needed because the mip is dilated past the evaluation error.
+__device__ __forceinline__ uint32_t gf_coarse_cell(const GfGrid& g, float x, float y, float z) {
+  float v[3] = {x, y, z};
+  int idx[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float q = (v[a] - g.b_min_f[a]) * g.inv_cell_f[a];
+    q = fminf(fmaxf(q, 0.f), (float)(g.res[a] - 1));
+    idx[a] = __float_as_int(__fadd_rz(q, 8388608.0f)) - 0x4B000000;
+  }
+  return (uint32_t)(idx[0] + g.res[0] * (idx[1] + g.res[1] * idx[2]));
+}
 __global__ void k_march(MarchParams P, RayState R, RoundBufs B, int round);
 
 }  // namespace gf

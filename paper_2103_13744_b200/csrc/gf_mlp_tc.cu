@@ -44,11 +44,13 @@ struct TcShape {
   static constexpr int BB0 = 0, BB1 = N0, BB2 = N0 + N1, BB3 = N0 + N1 + N2, BB4 = N0 + N1 + N2 + N3;
   static constexpr int N_BIAS = N0 + N1 + N2 + N3 + N4;
   static constexpr int CELL_BYTES = ((BIAS + N_BIAS * 4) + 127) / 128 * 128;
-  // activations (A operands), 128 rows each
-  static constexpr int A0 = CELL_BYTES;                    // gamma(x)          128 x K0
-  static constexpr int A1 = A0 + 128 * K0 * 2;             // h0 / h1 / g       128 x W
-  static constexpr int A3 = A1 + 128 * W * 2;              // [feat, gamma(d)]  128 x K3
-  static constexpr int BAR = A3 + 128 * K3 * 2;            // 2 mbarriers + tmem base
+  // activations (A operands), 128 rows each.  A3 aliases A0: gamma(x) is dead
+  // once the trunk0 MMA has completed, which is before gamma(d) / feat land.
+  static constexpr int KA0 = K0 > K3 ? K0 : K3;
+  static constexpr int A0 = CELL_BYTES;                    // gamma(x) 128 x K0, later [feat, gamma(d)] 128 x K3
+  static constexpr int A3 = A0;
+  static constexpr int A1 = A0 + 128 * KA0 * 2;            // h0 / h1 / g       128 x W
+  static constexpr int BAR = A1 + 128 * W * 2;             // 2 mbarriers + tmem base
   static constexpr int SMEM = BAR + 32;
   static constexpr int TMEM_COLS = N2 <= 32 ? 32 : (N2 <= 64 ? 64 : (N2 <= 128 ? 128 : 256));
 };
@@ -156,6 +158,39 @@ __device__ __forceinline__ void sincos_scaled(float x, int k, float* s, float* c
   __sincosf(r, s, c);
 }
 
+// sin / cos of x * 2^k * pi for k < L: MUFU anchors every third octave,
+// double-angle steps in between (max abs error 2.6e-6, vs 4.9e-4 fp16
+// operand rounding).
+template <int L>
+__device__ __forceinline__ void encode_octaves(float x, float* s, float* c) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    if (k % 3 == 0) {
+      sincos_scaled(x, k, &s[k], &c[k]);
+    } else {
+      const float sp = s[k - 1], cp = c[k - 1];
+      s[k] = 2.0f * sp * cp;
+      c[k] = (cp - sp) * (cp + sp);
+    }
+  }
+}
+
+// row inputs of tile t for this thread (row = tid)
+template <class IO>
+__device__ __forceinline__ void prefetch_tile(const TileSched& S, const IO& io, uint32_t t, int tid, uint32_t& idx,
+                                              bool& valid, float* x, float* d) {
+  const uint2 tl = S.tiles[t];
+  const uint32_t seg0 = S.offsets[tl.x], seg_n = S.offsets[tl.x + 1] - seg0;
+  valid = tl.y + (uint32_t)tid < seg_n;
+  idx = 0;
+  x[0] = x[1] = x[2] = 0.f;
+  d[0] = d[1] = d[2] = 0.f;
+  if (valid) {
+    idx = S.sorted[seg0 + tl.y + tid];
+    io.load(idx, x, d);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
@@ -194,44 +229,38 @@ __global__ void __launch_bounds__(128) k_mlp_tc(const uint8_t* __restrict__ pack
   uint32_t ph_mma = 0, ph_w = 0;
   const uint32_t a0 = smem_u32(sA0), a1 = smem_u32(sA1), a3 = smem_u32(sA3), wb = smem_u32(smem);
 
+  // inputs of the next tile, prefetched while the current tile's MMAs run
+  uint32_t nidx = 0;
+  bool nvalid = false;
+  float nx[3] = {0.f, 0.f, 0.f}, nd[3] = {0.f, 0.f, 0.f};
+  if (t_begin < t_end) prefetch_tile(S, io, t_begin, tid, nidx, nvalid, nx, nd);
+
   for (uint32_t t = t_begin; t < t_end; ++t) {
     const uint2 tl = S.tiles[t];
     __syncthreads();  // previous tile fully retired (bias reads, output stores)
     const bool new_cell = (int)tl.x != cur;
     if (new_cell && tid == 0) bulk_load(wb, packed + (size_t)tl.x * T::CELL_BYTES, T::CELL_BYTES, bar_w);
     cur = (int)tl.x;
-    const uint32_t seg0 = S.offsets[tl.x], seg_n = S.offsets[tl.x + 1] - seg0;
-    const bool valid = tl.y + (uint32_t)tid < seg_n;
-    uint32_t idx = 0;
-    float x[3] = {0.f, 0.f, 0.f}, d[3] = {0.f, 0.f, 0.f};
-    if (valid) {
-      idx = S.sorted[seg0 + tl.y + tid];
-      io.load(idx, x, d);
-    }
+    const bool valid = nvalid;
+    const uint32_t idx = nidx;
+    float x[3] = {nx[0], nx[1], nx[2]}, d[3] = {nd[0], nd[1], nd[2]};
     // ---- gamma(x) -> A0 (63 features + 1 zero pad)
     {
       float e[64];
       e[0] = x[0]; e[1] = x[1]; e[2] = x[2];
 #pragma unroll
-      for (int k = 0; k < 10; ++k)
+      for (int a = 0; a < 3; ++a) {
+        float s[10], c[10];
+        encode_octaves<10>(x[a], s, c);
 #pragma unroll
-        for (int a = 0; a < 3; ++a) sincos_scaled(x[a], k, &e[3 + 6 * k + a], &e[6 + 6 * k + a]);
+        for (int k = 0; k < 10; ++k) {
+          e[3 + 6 * k + a] = s[k];
+          e[6 + 6 * k + a] = c[k];
+        }
+      }
       e[63] = 0.f;
 #pragma unroll
       for (int c = 0; c < 8; ++c) st_chunk(sA0, T::K0, tid, 8 * c, e + 8 * c);
-    }
-    // ---- gamma(d) -> A3 columns [W, W+27), zero pad to K3
-    {
-      float e[T::K3 - W];
-      e[0] = d[0]; e[1] = d[1]; e[2] = d[2];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int a = 0; a < 3; ++a) sincos_scaled(d[a], k, &e[3 + 6 * k + a], &e[6 + 6 * k + a]);
-#pragma unroll
-      for (int j = 27; j < T::K3 - W; ++j) e[j] = 0.f;
-#pragma unroll
-      for (int c = 0; c < (T::K3 - W) / 8; ++c) st_chunk(sA3, T::K3, tid, W + 8 * c, e + 8 * c);
     }
     fence_async_smem();
     fence_before();
@@ -243,15 +272,21 @@ __global__ void __launch_bounds__(128) k_mlp_tc(const uint8_t* __restrict__ pack
     fence_after();
 
     // ---- layer chain ------------------------------------------------------
-    auto run = [&](uint32_t a_addr, int K, uint32_t b_addr, uint32_t idesc) {
+    auto issue = [&](uint32_t a_addr, int K, uint32_t b_addr, uint32_t idesc) {
       if (tid == 0) {
         for (int ks = 0; ks < K / 16; ++ks)
           mma_f16(tmem, umma_desc(a_addr + ks * 256, K), umma_desc(b_addr + ks * 256, K), idesc, ks > 0 ? 1u : 0u);
         mma_commit(bar_mma);
       }
+    };
+    auto wait_mma = [&]() {
       mbar_wait(bar_mma, ph_mma);
       ph_mma ^= 1;
       fence_after();
+    };
+    auto run = [&](uint32_t a_addr, int K, uint32_t b_addr, uint32_t idesc) {
+      issue(a_addr, K, b_addr, idesc);
+      wait_mma();
     };
     auto sync_mma = [&]() {
       fence_async_smem();
@@ -260,8 +295,27 @@ __global__ void __launch_bounds__(128) k_mlp_tc(const uint8_t* __restrict__ pack
       fence_after();
     };
 
-    // trunk0: relu(gamma(x) W0^T + b0) -> A1
-    run(a0, T::K0, wb + T::B0, idesc_f16(128, T::N0));
+    // trunk0: relu(gamma(x) W0^T + b0) -> A1.  While the tensor core runs it,
+    // compute gamma(d) (registers) and prefetch the next tile's inputs.
+    issue(a0, T::K0, wb + T::B0, idesc_f16(128, T::N0));
+    float ed[T::K3 - W];
+    {
+      ed[0] = d[0]; ed[1] = d[1]; ed[2] = d[2];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        float s[4], c[4];
+        encode_octaves<4>(d[a], s, c);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          ed[3 + 6 * k + a] = s[k];
+          ed[6 + 6 * k + a] = c[k];
+        }
+      }
+#pragma unroll
+      for (int j = 27; j < T::K3 - W; ++j) ed[j] = 0.f;
+    }
+    if (t + 1 < t_end) prefetch_tile(S, io, t + 1, tid, nidx, nvalid, nx, nd);
+    wait_mma();
     {
       float h[W];
       tmem_load<W>(t_row, h);
@@ -269,6 +323,9 @@ __global__ void __launch_bounds__(128) k_mlp_tc(const uint8_t* __restrict__ pack
       for (int c = 0; c < W; ++c) h[c] = fmaxf(h[c] + sbias[T::BB0 + c], 0.f);
 #pragma unroll
       for (int c = 0; c < W / 8; ++c) st_chunk(sA1, W, tid, 8 * c, h + 8 * c);
+      // gamma(x) is dead: gamma(d) goes to A3 (== A0) columns [W, K3)
+#pragma unroll
+      for (int c = 0; c < (T::K3 - W) / 8; ++c) st_chunk(sA3, T::K3, tid, W + 8 * c, ed + 8 * c);
     }
     sync_mma();
     // trunk1: relu(h0 W1^T + b1) -> A1
@@ -411,12 +468,14 @@ template <int W, class IO>
 static void launch_tc_w(const void* packed, const TileSched& S, const IO& io, cudaStream_t st) {
   using T = TcShape<W>;
   auto k = k_mlp_tc<W, IO>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 128, T::SMEM);
-  if (per_sm < 1) per_sm = 1;
-  // TMEM: 512 columns per SM shared by the resident CTAs
-  per_sm = per_sm < 512 / T::TMEM_COLS ? per_sm : 512 / T::TMEM_COLS;
+  static thread_local int per_sm = 0;  // resident CTAs per SM for this instantiation
+  if (per_sm == 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 128, T::SMEM);
+    // TMEM: 512 columns per SM shared by the resident CTAs
+    per_sm = occ < 1 ? 1 : (occ < 512 / T::TMEM_COLS ? occ : 512 / T::TMEM_COLS);
+  }
   k<<<num_sms() * per_sm, 128, T::SMEM, st>>>((const uint8_t*)packed, S, io);
 }
 

@@ -253,13 +253,37 @@ def _field_grid(field):
     )
 
 
+def shard_rays(n_rays: int, rank: int, world: int) -> tuple[int, int, int]:
+    """Balanced multi-GPU partition of a ray set: rank r takes the 4096-ray
+    jitter blocks r, r+world, r+2*world, ... (image content is centre-heavy,
+    so contiguous bands would not balance).  Returns (ray_offset,
+    block_stride, n_local_rays) for ``render_rays_device``."""
+    if not (0 <= rank < world):
+        raise ValueError("rank must lie in [0, world)")
+    n_blocks = (n_rays + RAY_BLOCK - 1) // RAY_BLOCK
+    mine = list(range(rank, n_blocks, world))
+    n_local = sum(min(RAY_BLOCK, n_rays - b * RAY_BLOCK) for b in mine)
+    return rank * RAY_BLOCK, world, n_local
+
+
+def unshard_index(n_rays: int, world: int) -> np.ndarray:
+    """For the all-gathered, per-rank padded shard buffers (world, cap, 3)
+    flattened to (world*cap, 3), the row of each global ray in image order."""
+    n_blocks = (n_rays + RAY_BLOCK - 1) // RAY_BLOCK
+    cap = ((n_blocks + world - 1) // world) * RAY_BLOCK
+    g = np.arange(n_rays)
+    b, w = g // RAY_BLOCK, g % RAY_BLOCK
+    return (b % world) * cap + (b // world) * RAY_BLOCK + w
+
+
 def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camera | None = None, origins=None,
-                       directions=None, ray_offset: int = 0, n_rays: int | None = None, precision=None,
-                       out=None, stats=None, trace_capacity: int = 0):
+                       directions=None, ray_offset: int = 0, n_rays: int | None = None, block_stride: int = 1,
+                       precision=None, out=None, stats=None, trace_capacity: int = 0):
     """Device-resident core of render_rays / render_image.  Returns
     (rgb (n,3) float32 CUDA tensor, stats int64[4] CUDA tensor, trace or None).
     ``origins``/``directions`` may be CUDA tensors; ``cam`` generates rays
-    for pixels [ray_offset, ray_offset + n_rays)."""
+    for pixels [ray_offset, ray_offset + n_rays), or for the interleaved
+    blocks of ``shard_rays`` when ``block_stride`` > 1."""
     t = D.require_cuda()
     p = grid.resolved_precision(precision)
     packed = grid.device_params(p)
@@ -288,7 +312,7 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
     ws = D.workspace(N.lib().gf_render_workspace_bytes(arch, geom, ncfg, n))
     N.check(N.lib().gf_render_rays(
         arch, geom, N.ptr(packed), N.PRECISION[p], occ_geom, N.ptr(occ_bits), ncfg, ccam, N.ptr(o_d), N.ptr(d_d),
-        int(ray_offset), int(n), N.ptr(rgb), N.ptr(st), N.ptr(trace), int(trace_capacity), N.ptr(tcount),
+        int(ray_offset), int(block_stride), int(n), N.ptr(rgb), N.ptr(st), N.ptr(trace), int(trace_capacity), N.ptr(tcount),
         N.ptr(ws), ws.numel(), D.stream_handle()), "render_rays")
     tr = None
     if trace_capacity:
@@ -338,6 +362,36 @@ def render_image(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0
     stats = _stats_from(stats_h)
     stats.wall_ms = (time.perf_counter() - t_start) * 1000.0
     return host.numpy().reshape(cam.height, cam.width, 3), stats
+
+
+def render_image_distributed(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0, group=None,
+                             precision=None):
+    """Multi-GPU render_image (one process per GPU, torch.distributed/NCCL).
+
+    Each rank marches its interleaved 4096-ray blocks (``shard_rays``) with the
+    blocks' own jitter streams, so the assembled image is bit-identical to the
+    single-GPU render; the only exchange is one all-gather of the shards
+    (float32 RGB) plus a 4-counter all-reduce.  Returns the (H, W, 3) image
+    as a CUDA tensor on every rank and the global RenderStats."""
+    import torch.distributed as dist
+
+    t = D.require_cuda()
+    grid = _field_grid(field)
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = cam.width * cam.height
+    off, stride, n_local = shard_rays(n, rank, world)
+    n_blocks = (n + RAY_BLOCK - 1) // RAY_BLOCK
+    cap = ((n_blocks + world - 1) // world) * RAY_BLOCK
+    buf = t.zeros((cap, 3), dtype=t.float32, device=D.device())
+    st = t.zeros(4, dtype=t.int64, device=buf.device)
+    if n_local:
+        render_rays_device(grid, occupancy, cfg, seed, cam=cam, ray_offset=off, n_rays=n_local, block_stride=stride,
+                           precision=precision, out=buf[:n_local], stats=st)
+    gathered = t.empty((world * cap, 3), dtype=t.float32, device=buf.device)
+    dist.all_gather_into_tensor(gathered, buf, group=group)
+    dist.all_reduce(st, group=group)
+    idx = t.from_numpy(unshard_index(n, world)).to(buf.device)
+    return gathered.index_select(0, idx).view(cam.height, cam.width, 3), _stats_from(st)
 
 
 def compute_psnr(a, b) -> float:
