@@ -81,7 +81,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:  # noqa: BLE001
@@ -111,7 +111,8 @@ class ClockSampler:
         names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "window": "nvidia-smi every 100 ms over a pre-roll of the same load + the timed frames"}
 
 
 # ---------------------------------------------------------------------------
@@ -193,6 +194,7 @@ def main():
     ap.add_argument("--precision", default=None, choices=[None, "fp16", "fp32"])
     ap.add_argument("--cpu-block-stride", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--clock-preroll", type=float, default=0.6, help="seconds of untimed load before the timed frames")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -244,6 +246,12 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        # pre-roll under the same load so nvidia-smi (>=100 ms period) has
+        # samples spanning the timed window even when K frames take < 100 ms
+        t_pre = time.perf_counter()
+        while time.perf_counter() - t_pre < args.clock_preroll:
+            step()
+            torch.cuda.synchronize()
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             ev[i][0].record(stream)
