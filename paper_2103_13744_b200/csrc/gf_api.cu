@@ -277,6 +277,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->R.rng = c.take<u128>((size_t)n_rays);
   w->R.run = c.take<uint32_t>((size_t)n_rays);
   w->R.flags = c.take<uint8_t>((size_t)n_rays);
+  w->R.ivl = c.take<uint32_t>((size_t)n_rays * GF_MAX_IVL);
   w->RB.rec = c.take<float4>(cap);
   w->RB.res = c.take<float4>(cap);
   w->B.counts = c.take<uint32_t>((size_t)n_cells);
@@ -377,7 +378,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
     bool same_box = occ_bits != nullptr;
     for (int a = 0; a < 3 && same_box; ++a)
       same_box = occ->b_min[a] == grid->b_min[a] && occ->b_max[a] == grid->b_max[a];
-    if (same_box && !(no && no[0] == '1')) {
+    if (same_box && !(no && no[0] == '1') && cfg->ert_chunk <= 32 && cfg->k < 65535) {
       double diag2 = 0, maxabs = 0;
       for (int a = 0; a < 3; ++a) {
         double e = grid->b_max[a] - grid->b_min[a];
@@ -386,7 +387,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
       }
       const double reach = 0.5 * sqrt(diag2) / cfg->k * 1.0001 + 1e-5 * (1.0 + maxabs);
       const char* fenv = getenv("GF_COARSE_FACTOR");
-      const int want = fenv ? atoi(fenv) : 2;
+      const int want = fenv ? atoi(fenv) : 4;
       int f = 0, radius = 0;
       for (int cand : {want, 1, 2, 4, 8}) {
         if (cand < 1 || occ->res[0] % cand || occ->res[1] % cand || occ->res[2] % cand) continue;
@@ -406,6 +407,9 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
         cg.res[0] = cres.x; cg.res[1] = cres.y; cg.res[2] = cres.z;
         P.coarse = gf_make_grid(&cg);
         P.coarse_bits = w.coarse_bits;
+        double cmin = 1e300;
+        for (int a = 0; a < 3; ++a) cmin = fmin(cmin, (cg.b_max[a] - cg.b_min[a]) / cg.res[a]);
+        P.ivl_pad = (float)(0.05 * cmin + 1e-5 * (1.0 + maxabs));
         coarse_launches = 2;
       }
     }
@@ -418,10 +422,20 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   const unsigned ray_blocks = (unsigned)gf_div_up<int64_t>(n_rays, 128);
   k_ray_init<<<ray_blocks, 128, 0, st>>>(P, w.R);
   stage_mark(st, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
+  // whole-image camera calls: march warps over 8x4 pixel tiles
+  if (cam && ray_offset == 0 && ray_block_stride == 1 && n_rays == (int64_t)cam->width * cam->height &&
+      !getenv("GF_NO_TILE2D")) {
+    P.tile2d = 1;
+    P.tiles_x = (cam->width + 7) / 8;
+    P.march_threads = (int64_t)P.tiles_x * ((cam->height + 3) / 4) * 32;
+  } else {
+    P.march_threads = n_rays;
+  }
+  const unsigned march_blocks = (unsigned)gf_div_up<int64_t>(P.march_threads, 128);
   TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
   RenderIO io{w.RB.rec, w.RB.res, w.R.dir, (uint32_t)stride};
   for (int r = 0; r < P.n_rounds; ++r) {
-    k_march<<<ray_blocks, 128, 0, st>>>(P, w.R, w.RB, r);
+    k_march<<<march_blocks, 128, 0, st>>>(P, w.R, w.RB, r);
     stage_mark(st, GF_STAGE_MARCH, 1);
     launch_scan_cells(w.B, nc, st);
     stage_mark(st, GF_STAGE_SCAN, 1);
@@ -431,7 +445,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
       return fail(GF_ERR_UNSUPPORTED, "gf_render_rays: no MLP kernel for this architecture/precision");
     stage_mark(st, GF_STAGE_MLP, 1);
   }
-  k_march<<<ray_blocks, 128, 0, st>>>(P, w.R, w.RB, P.n_rounds);
+  k_march<<<march_blocks, 128, 0, st>>>(P, w.R, w.RB, P.n_rounds);
   stage_mark(st, GF_STAGE_MARCH, 1);
   return check_cuda("gf_render_rays");
 }

@@ -28,6 +28,80 @@ __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_
 }
 
 // -------------------------------------------------------------------------
+// Candidate slot ranges of one ray: a 3-D DDA (Amanatides-Woo) through the
+// dilated coarse mip collects the distance intervals [s_in, s_out] (from the
+// entry point) where the ray is inside a set coarse cell; slot j is a
+// candidate iff its nominal midpoint (j + 0.5) * seg lies in one (padded for
+// float32 error).  Because the mip is dilated by >= seg/2 + margin, a
+// non-candidate slot's sample provably lands in an empty fine cell.
+// -------------------------------------------------------------------------
+__device__ void coarse_intervals(const MarchParams& P, uint32_t* out, float ex, float ey, float ez, const float* d,
+                                 float smax, float seg) {
+  const GfGrid& g = P.coarse;
+  const float pos[3] = {ex, ey, ez};
+  int cell[3], step[3];
+  float snext[3], sdelta[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float q = (pos[a] - g.b_min_f[a]) * g.inv_cell_f[a];
+    q = fminf(fmaxf(q, 0.f), (float)g.res[a] - 1e-3f);
+    cell[a] = (int)floorf(q);
+    cell[a] = cell[a] < g.res[a] - 1 ? cell[a] : g.res[a] - 1;
+    const float v = d[a] * g.inv_cell_f[a];  // cells per unit distance
+    if (v > 0.f) {
+      step[a] = 1;
+      snext[a] = ((float)(cell[a] + 1) - q) / v;
+      sdelta[a] = 1.f / v;
+    } else if (v < 0.f) {
+      step[a] = -1;
+      snext[a] = ((float)cell[a] - q) / v;
+      sdelta[a] = -1.f / v;
+    } else {
+      step[a] = 0;
+      snext[a] = INFINITY;
+      sdelta[a] = INFINITY;
+    }
+  }
+  const float inv_seg = 1.f / seg;
+  const float kmax = (float)(P.k - 1);
+  int n = 0;
+  auto emit = [&](float sa, float sb) {
+    float lo = floorf((sa - P.ivl_pad) * inv_seg - 0.5f), hi = ceilf((sb + P.ivl_pad) * inv_seg - 0.5f);
+    lo = fmaxf(lo, 0.f);
+    hi = fminf(hi, kmax);
+    if (lo > hi) return;
+    const uint32_t v = (uint32_t)lo | ((uint32_t)hi << 16);
+    if (n < GF_MAX_IVL) {
+      out[n++] = v;
+    } else {  // out of room: widen the last range (conservative)
+      out[GF_MAX_IVL - 1] = (out[GF_MAX_IVL - 1] & 0xFFFFu) | ((uint32_t)hi << 16);
+    }
+  };
+  float s = 0.f, s_open = 0.f;
+  bool open = false;
+  for (int it = 0; it < 4096; ++it) {
+    const uint32_t c = (uint32_t)(cell[0] + g.res[0] * (cell[1] + g.res[1] * cell[2]));
+    const bool occ = (__ldg(P.coarse_bits + (c >> 5)) >> (c & 31)) & 1;
+    if (occ && !open) {
+      open = true;
+      s_open = s;
+    } else if (!occ && open) {
+      emit(s_open, s);
+      open = false;
+    }
+    const int ax = snext[0] < snext[1] ? (snext[0] < snext[2] ? 0 : 2) : (snext[1] < snext[2] ? 1 : 2);
+    const float sn = snext[ax];
+    if (!(sn < smax)) break;
+    s = sn;
+    cell[ax] += step[ax];
+    if (cell[ax] < 0 || cell[ax] >= g.res[ax]) break;
+    snext[ax] += sdelta[ax];
+  }
+  if (open) emit(s_open, smax);
+  for (int k = n; k < GF_MAX_IVL; ++k) out[k] = 0x0000FFFFu;  // empty (lo > hi)
+}
+
+// -------------------------------------------------------------------------
 // ray setup: render.py:333-342 generate_rays (if camera), 368-369 f64 upcast,
 // 486-500 slab test / seg / t0 in float32, and the ray's jitter stream
 // position.
@@ -86,6 +160,12 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
   R.acc[i] = make_float4(0.f, 0.f, 0.f, 1.f);
   R.run[i] = 0;
   R.flags[i] = hit ? (uint8_t)(GF_RAY_ALIVE | GF_RAY_HIT) : (uint8_t)0;
+  if (P.coarse_bits && hit) {
+    const float ex = __double2float_rn(__dadd_rn((double)o32[0], __dmul_rn(t0, (double)d32[0])));
+    const float ey = __double2float_rn(__dadd_rn((double)o32[1], __dmul_rn(t0, (double)d32[1])));
+    const float ez = __double2float_rn(__dadd_rn((double)o32[2], __dmul_rn(t0, (double)d32[2])));
+    coarse_intervals(P, R.ivl + i * GF_MAX_IVL, ex, ey, ez, d32, (float)(t1 - t0), seg);
+  }
   if (P.stratified) {
     const int64_t b = seed_slot(P, g);
     uint64_t draw0 = (uint64_t)(g % GF_RAY_BLOCK) * (uint64_t)P.k;  // float32 draw index of slot 0
@@ -153,7 +233,7 @@ __device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v)
 // At r == n_rounds: composite the last round and write the final colours.
 // -------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundBufs B, int round) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   bool in_range = i < P.n_rays;
   uint8_t flags = in_range ? R.flags[i] : 0;
   bool final_pass = round == P.n_rounds;
@@ -235,19 +315,27 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
   const double t0 = (double)o.w, sg64 = (double)d.w;
   const double ox = (double)o.x, oy = (double)o.y, oz = (double)o.z;
   const double dx = (double)d.x, dy = (double)d.y, dz = (double)d.z;
-  // entry point for the conservative coarse test (relative to it, the f32
-  // evaluation error stays ~1e-7 of the box size whatever the camera distance)
-  float ex = 0.f, ey = 0.f, ez = 0.f;
+  // candidate slots of this round from the ray's coarse-DDA ranges
+  uint32_t cmask = m >= 32 ? 0xFFFFFFFFu : ((1u << m) - 1u);
   if (P.coarse_bits && active) {
-    ex = __double2float_rn(__dadd_rn(ox, __dmul_rn(t0, dx)));
-    ey = __double2float_rn(__dadd_rn(oy, __dmul_rn(t0, dy)));
-    ez = __double2float_rn(__dadd_rn(oz, __dmul_rn(t0, dz)));
+    const uint4* iv = reinterpret_cast<const uint4*>(R.ivl + i * GF_MAX_IVL);
+    const uint4 q0 = iv[0], q1 = iv[1];
+    const uint32_t v[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+    uint32_t msk = 0;
+#pragma unroll
+    for (int k = 0; k < GF_MAX_IVL; ++k) {
+      const int lo = max((int)(v[k] & 0xFFFFu), s0), hi = min((int)(v[k] >> 16), s0 + m - 1);
+      if (lo <= hi) {
+        const int nb = hi - lo + 1;
+        msk |= (nb >= 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << (lo - s0);
+      }
+    }
+    cmask &= msk;
   }
   const bool fast_clip = P.grid.fast != 0;
   uint32_t kept = 0;
   double jd = (double)s0;
-  float jm = (float)s0 + 0.5f;
-  for (int j = 0; j < m; ++j, jd += 1.0, jm += 1.0f) {
+  for (int j = 0; j < m; ++j, jd += 1.0) {
     double jit = 0.5;
     if (P.stratified && active) {
       const uint32_t u = (draw & 1) ? (uint32_t)(outw >> 32) : (uint32_t)outw;
@@ -263,13 +351,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     // coarse test: the sample lies within seg/2 (+margin) of the segment
     // midpoint; the mip is dilated by that radius, so a clear bit proves the
     // exact sample is in an empty fine cell (skipped, counted in ess_skipped)
-    bool cand = active;
-    if (P.coarse_bits && cand) {
-      const float sm = jm * d.w;
-      const float cx = fmaf(sm, d.x, ex), cy = fmaf(sm, d.y, ey), cz = fmaf(sm, d.z, ez);
-      const uint32_t cf = gf_coarse_cell(P.coarse, cx, cy, cz);
-      cand = (__ldg(P.coarse_bits + (cf >> 5)) >> (cf & 31)) & 1;
-    }
+    const bool cand = active && (j >= 32 || ((cmask >> j) & 1u));
     bool keep = false;
     uint32_t cell = 0;
     if (__any_sync(0xffffffffu, cand) && cand) {

@@ -14,6 +14,7 @@ struct MarchParams {
   const uint8_t* occ_bits;
   GfGrid coarse;      // dilated coarse occupancy mip (empty-space pre-test)
   const uint32_t* coarse_bits;  // NULL: every candidate takes the exact path
+  float ivl_pad;      // world-distance padding of the DDA intervals (float32 error)
   gf_camera_t cam;
   int use_cam;
   const float* origins;
@@ -21,6 +22,8 @@ struct MarchParams {
   int64_t ray_offset, n_rays, first_block, block_stride;
   const u128* block_seeds;  // [2*b] state, [2*b+1] inc
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
+  int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
+  int64_t march_threads;
   double epsilon;
   float bg[3];
   float* rgb_out;
@@ -38,7 +41,11 @@ struct RayState {
   u128* rng;      // PCG64 state positioned at the ray's next float32 draw
   uint32_t* run;  // queried samples of the ray in the last marched round
   uint8_t* flags;
+  uint32_t* ivl;  // GF_MAX_IVL candidate slot ranges per ray (lo | hi << 16), from the coarse DDA
 };
+
+#define GF_MAX_IVL 8
+#define GF_IVL_ALL 0xFFFFFFFFu  // sentinel in ivl[0]: every slot is a candidate
 
 // Per-round buffers.  Staging is ray-major with a fixed stride (= chunk): the
 // kept samples of ray i in this round are rec[i*stride .. i*stride+run[i]),
@@ -55,6 +62,16 @@ struct RoundBufs {
 __device__ __forceinline__ int64_t global_ray(const MarchParams& P, int64_t i) {
   if (P.block_stride == 1) return P.ray_offset + i;
   return P.ray_offset + (i / GF_RAY_BLOCK) * P.block_stride * GF_RAY_BLOCK + i % GF_RAY_BLOCK;
+}
+// k_march thread -> call-local ray index; with tile2d a warp covers an 8x4
+// pixel tile so its rays cross the same cells at the same rounds (coherent
+// branches); out-of-image lanes get n_rays (inactive).
+__device__ __forceinline__ int64_t march_ray(const MarchParams& P, int64_t t) {
+  if (!P.tile2d) return t;
+  const int64_t warp = t >> 5;
+  const int lane = (int)(t & 31);
+  const int64_t x = (warp % P.tiles_x) * 8 + (lane & 7), y = (warp / P.tiles_x) * 4 + (lane >> 3);
+  return (x < P.cam.width && y < P.cam.height) ? y * P.cam.width + x : P.n_rays;
 }
 // slot of the ray's block in the per-call seed table
 __device__ __forceinline__ int64_t seed_slot(const MarchParams& P, int64_t g) {
