@@ -240,11 +240,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- device-timed region (value)
-    launches0 = N.lib().gf_launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         # pre-roll under the same load so nvidia-smi (>=100 ms period) has
         # samples spanning the timed window even when K frames take < 100 ms
@@ -252,15 +248,19 @@ def main():
         while time.perf_counter() - t_pre < args.clock_preroll:
             step()
             torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = N.lib().gf_launch_count()
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             ev[i][0].record(stream)
             step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = N.lib().gf_launch_count() - launches0
+        launches = N.lib().gf_launch_count() - launches0
+        if world > 1:
+            dist.barrier()
     per = [a.elapsed_time(b) for a, b in ev]
     ms = sum(per) / len(per)
     if world > 1:
