@@ -228,10 +228,12 @@ def main():
     gathered = torch.empty((world, SIZE * SIZE, 3), dtype=torch.float32, device="cuda") if world > 1 else None
     out = torch.empty((SIZE * SIZE, 3), dtype=torch.float32, device="cuda")
     stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    ws = torch.empty(N.lib().gf_render_workspace_bytes(grid.native_arch(), grid.native_geom(), cfg.native(0),
+                                                       SIZE * SIZE), dtype=torch.uint8, device="cuda")
 
     def step():
         stats.zero_()
-        gf.render.render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats)
+        gf.render.render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats, ws=ws)
         if gathered is not None:
             dist.all_gather_into_tensor(gathered, out)
 
@@ -276,7 +278,7 @@ def main():
     for _ in range(n_prof):
         flush.fill_(1)
         stats.zero_()
-        gf.render.render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats)
+        gf.render.render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats, ws=ws)
     torch.cuda.synchronize()
     st_ms, st_n = N.stage_times()
     N.lib().gf_stage_timing(0)

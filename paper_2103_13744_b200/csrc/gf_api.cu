@@ -42,6 +42,7 @@ int num_sms() {
 using namespace gf;
 
 #include <atomic>
+#include <mutex>
 #include <vector>
 
 static thread_local std::string g_err;
@@ -99,6 +100,75 @@ static int check_cuda(const char* where) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(GF_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
   return GF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-graph cache: a render call's ~55 launches are captured once per exact
+// argument set (all kernel parameters, workspace pointers, seed) and replayed
+// with one cudaGraphLaunch afterwards.
+// ---------------------------------------------------------------------------
+struct GraphKey {
+  std::vector<unsigned char> b;
+  template <class T>
+  void add(const T& v) {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&v);
+    b.insert(b.end(), p, p + sizeof(T));
+  }
+};
+
+struct GraphEntry {
+  std::vector<unsigned char> key;
+  int dev;
+  cudaGraphExec_t exec;
+  int64_t launches;
+  uint64_t last_use;
+};
+
+static std::mutex g_graph_mu;
+static std::vector<GraphEntry> g_graphs;
+static uint64_t g_graph_tick = 0;
+
+template <class F>
+static int run_graph(const GraphKey& k, cudaStream_t st, F&& enqueue) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (auto& e : g_graphs)
+      if (e.dev == dev && e.key == k.b) {
+        e.last_use = ++g_graph_tick;
+        g_launches += e.launches;
+        cudaGraphLaunch(e.exec, st);
+        return check_cuda("gf_render_rays (graph replay)");
+      }
+  }
+  const int64_t l0 = g_launches.load();
+  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();  // stream cannot be captured (e.g. legacy default stream): run eagerly
+    enqueue(st);
+    return check_cuda("gf_render_rays");
+  }
+  enqueue(st);
+  cudaGraph_t g = nullptr;
+  cudaError_t err = cudaStreamEndCapture(st, &g);
+  if (err != cudaSuccess) return fail(GF_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(err));
+  cudaGraphExec_t ex = nullptr;
+  err = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (err != cudaSuccess) return fail(GF_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(err));
+  cudaGraphLaunch(ex, st);
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (g_graphs.size() >= 8) {
+      auto lru = g_graphs.begin();
+      for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+        if (it->last_use < lru->last_use) lru = it;
+      cudaGraphExecDestroy(lru->exec);
+      g_graphs.erase(lru);
+    }
+    g_graphs.push_back(GraphEntry{k.b, dev, ex, g_launches.load() - l0, ++g_graph_tick});
+  }
+  return check_cuda("gf_render_rays (graph)");
 }
 
 // bump allocator over a caller-provided workspace
@@ -176,6 +246,7 @@ static size_t query_carve(Carve& c, int64_t n, int64_t n_cells, QueryWs* w) {
   w->B.tiles = c.take<uint2>((size_t)(n / GF_TILE_ROWS + n_cells + 1));
   w->B.n_tiles = c.take<uint32_t>(1);
   w->B.sorted = c.take<uint32_t>((size_t)n + 1);
+  w->B.tile_off = c.take<uint32_t>((size_t)n_cells + 1);
   return c.size();
 }
 
@@ -255,6 +326,7 @@ size_t gf_grouped_workspace_bytes(int64_t n_cells, int64_t n) {
 // ---------------------------------------------------------------------------
 struct RenderWs {
   u128* seeds;
+  u128* jump;
   RayState R;
   RoundBufs RB;
   BucketBufs B;
@@ -269,6 +341,7 @@ static const int64_t kMaxCoarseCells = 256ll * 256 * 256;
 static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int stride, int64_t n_cells, RenderWs* w) {
   const size_t cap = (size_t)n_rays * (size_t)stride;
   w->seeds = c.take<u128>((size_t)2 * n_blocks);
+  w->jump = c.take<u128>((size_t)2 * (GF_JUMP_MAX + 1));
   w->coarse_tmp = c.take<uint8_t>((size_t)kMaxCoarseCells);
   w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->R.org = c.take<float4>((size_t)n_rays);
@@ -280,13 +353,16 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->R.ivl = c.take<uint32_t>((size_t)n_rays * GF_MAX_IVL);
   w->RB.rec = c.take<float4>(cap);
   w->RB.res = c.take<float4>(cap);
-  w->B.counts = c.take<uint32_t>((size_t)n_cells);
+  w->B.counts = c.take<uint32_t>((size_t)2 * n_cells);  // two histograms, by round parity
   w->RB.counts = w->B.counts;
   w->B.offsets = c.take<uint32_t>((size_t)n_cells + 1);
   w->B.cursor = c.take<uint32_t>((size_t)n_cells);
   w->B.tiles = c.take<uint2>(cap / GF_TILE_ROWS + (size_t)n_cells + 1);
   w->B.n_tiles = c.take<uint32_t>(1);
   w->B.sorted = c.take<uint32_t>(cap + 1);
+  w->B.tile_off = c.take<uint32_t>((size_t)n_cells + 1);
+  w->RB.emit_list = c.take<uint32_t>((size_t)n_rays);
+  w->RB.emit_count = c.take<uint32_t>(2);
   return c.size();
 }
 
@@ -316,7 +392,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
                    const gf_camera_t* cam, const float* origins, const float* dirs, int64_t ray_offset,
                    int64_t ray_block_stride, int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace, int64_t trace_capacity,
                    int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
-  LayerTable t;
+  LayerTable t{};  // value-initialised: hashed into the graph key
   if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_render_rays: bad architecture");
   if (!valid_grid(grid)) return fail(GF_ERR_INVALID, "gf_render_rays: bad grid");
   if (!cfg || cfg->k < 1 || cfg->ert_chunk < 1 || !(cfg->epsilon >= 0.0 && cfg->epsilon < 1.0))
@@ -333,7 +409,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   int64_t first_block, n_blocks;
   block_range(ray_offset, ray_block_stride, n_rays, &first_block, &n_blocks);
   Carve c(ws);
-  RenderWs w;
+  RenderWs w{};
   if (render_carve(c, n_rays, n_blocks, stride, nc, &w) > ws_bytes)
     return fail(GF_ERR_WORKSPACE, "gf_render_rays: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
@@ -354,9 +430,11 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   P.n_rays = n_rays;
   P.first_block = first_block;
   P.block_seeds = w.seeds;
+  P.jump = w.jump;
   P.k = cfg->k;
   P.chunk = cfg->ert_chunk;
   P.n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
+  P.n_cells = nc;
   P.stride = stride;
   P.stratified = cfg->stratified ? 1 : 0;
   P.ert = cfg->epsilon > 0.0 ? 1 : 0;
@@ -373,6 +451,11 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   // grid dilated by the largest distance between a sample and the midpoint
   // of its nominal segment (seg/2) plus a float32 evaluation margin.
   int coarse_launches = 0;
+  struct {
+    bool on = false, word = false;
+    int f = 0, radius = 0;
+    int3 ores = {0, 0, 0}, cres = {0, 0, 0};
+  } cplan;
   {
     const char* no = getenv("GF_NO_COARSE");
     bool same_box = occ_bits != nullptr;
@@ -397,12 +480,14 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
         if (r <= 2) { f = cand; radius = r < 1 ? 1 : r; break; }
       }
       if (f) {
-        int3 ores = make_int3(occ->res[0], occ->res[1], occ->res[2]);
-        int3 cres = make_int3(ores.x / f, ores.y / f, ores.z / f);
-        const int64_t ncc = (int64_t)cres.x * cres.y * cres.z;
-        k_coarse_reduce<<<(unsigned)gf_div_up<int64_t>(ncc, 256), 256, 0, st>>>(occ_bits, ores, f, cres, w.coarse_tmp);
-        k_coarse_dilate<<<(unsigned)gf_div_up<int64_t>(gf_div_up<int64_t>(ncc, 32), 128), 128, 0, st>>>(
-            w.coarse_tmp, cres, radius, w.coarse_bits);
+        cplan.on = true;
+        cplan.f = f;
+        cplan.radius = radius;
+        cplan.ores = make_int3(occ->res[0], occ->res[1], occ->res[2]);
+        cplan.cres = make_int3(cplan.ores.x / f, cplan.ores.y / f, cplan.ores.z / f);
+        cplan.word = cplan.ores.x % (32 * f) == 0;  // word-parallel OR-reduce + separable dilation
+        coarse_launches = cplan.word ? 4 : 2;
+        const int3 cres = cplan.cres;
         gf_grid_geom_t cg = *occ;
         cg.res[0] = cres.x; cg.res[1] = cres.y; cg.res[2] = cres.z;
         P.coarse = gf_make_grid(&cg);
@@ -410,18 +495,31 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
         double cmin = 1e300;
         for (int a = 0; a < 3; ++a) cmin = fmin(cmin, (cg.b_max[a] - cg.b_min[a]) / cg.res[a]);
         P.ivl_pad = (float)(0.05 * cmin + 1e-5 * (1.0 + maxabs));
-        coarse_launches = 2;
       }
     }
   }
 
-  stage_open(st);
-  cudaMemsetAsync(w.B.counts, 0, (size_t)nc * 4, st);
-  if (P.stratified) k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(n_blocks, 64), 64, 0, st>>>(
-      cfg->seed, first_block, ray_block_stride, n_blocks, w.seeds);
-  const unsigned ray_blocks = (unsigned)gf_div_up<int64_t>(n_rays, 128);
-  k_ray_init<<<ray_blocks, 128, 0, st>>>(P, w.R);
-  stage_mark(st, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
+  auto enqueue_coarse = [&](cudaStream_t s) {
+    if (!cplan.on) return;
+    const int3 ores = cplan.ores, cres = cplan.cres;
+    const int64_t ncc = (int64_t)cres.x * cres.y * cres.z;
+    if (cplan.word) {
+      const int64_t nw = ncc / 32;
+      const unsigned gb = (unsigned)gf_div_up<int64_t>(nw, 128);
+      uint32_t* t0 = reinterpret_cast<uint32_t*>(w.coarse_tmp);
+      uint32_t* t1 = t0 + nw;
+      k_coarse_reduce_w<<<gb, 128, 0, s>>>(reinterpret_cast<const uint32_t*>(occ_bits), ores, cplan.f, cres, t0);
+      k_dilate_x<<<gb, 128, 0, s>>>(t0, t1, cres, cplan.radius);
+      k_dilate_yz<<<gb, 128, 0, s>>>(t1, t0, cres, cplan.radius, 1);
+      k_dilate_yz<<<gb, 128, 0, s>>>(t0, w.coarse_bits, cres, cplan.radius, 2);
+    } else {
+      k_coarse_reduce<<<(unsigned)gf_div_up<int64_t>(ncc, 256), 256, 0, s>>>(occ_bits, ores, cplan.f, cres,
+                                                                              w.coarse_tmp);
+      k_coarse_dilate<<<(unsigned)gf_div_up<int64_t>(gf_div_up<int64_t>(ncc, 32), 128), 128, 0, s>>>(
+          w.coarse_tmp, cres, cplan.radius, w.coarse_bits);
+    }
+  };
+
   // whole-image camera calls: march warps over 8x4 pixel tiles
   if (cam && ray_offset == 0 && ray_block_stride == 1 && n_rays == (int64_t)cam->width * cam->height &&
       !getenv("GF_NO_TILE2D")) {
@@ -432,22 +530,63 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
     P.march_threads = n_rays;
   }
   const unsigned march_blocks = (unsigned)gf_div_up<int64_t>(P.march_threads, 128);
+  const unsigned ray_blocks = (unsigned)gf_div_up<int64_t>(n_rays, 128);
   TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
   RenderIO io{w.RB.rec, w.RB.res, w.R.dir, (uint32_t)stride};
-  for (int r = 0; r < P.n_rounds; ++r) {
-    k_march<<<march_blocks, 128, 0, st>>>(P, w.R, w.RB, r);
-    stage_mark(st, GF_STAGE_MARCH, 1);
-    launch_scan_cells(w.B, nc, st);
-    stage_mark(st, GF_STAGE_SCAN, 1);
-    launch_scatter_render(w.RB.rec, w.R.run, n_rays, stride, w.B, st);
-    stage_mark(st, GF_STAGE_SCATTER, 1);
-    if (!run_mlp(t, packed, precision, S, &io, nullptr, st))
-      return fail(GF_ERR_UNSUPPORTED, "gf_render_rays: no MLP kernel for this architecture/precision");
-    stage_mark(st, GF_STAGE_MLP, 1);
+  const bool mlp_ok = precision == GF_PRECISION_FP16   ? prepare_mlp_tc(t)
+                      : precision == GF_PRECISION_FP32 ? prepare_mlp_fp32(t)
+                                                       : false;
+  if (!mlp_ok) return fail(GF_ERR_UNSUPPORTED, "gf_render_rays: no MLP kernel for this architecture/precision");
+
+  // the frame's launch sequence (captured once into a CUDA graph per
+  // argument set and replayed; eager when instrumented)
+  auto enqueue = [&](cudaStream_t s) {
+    enqueue_coarse(s);
+    stage_open(s);
+    cudaMemsetAsync(w.B.counts, 0, (size_t)2 * nc * 4, s);
+    cudaMemsetAsync(w.RB.emit_count, 0, 2 * sizeof(uint32_t), s);
+    if (P.stratified)
+      k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(n_blocks, 64), 64, 0, s>>>(cfg->seed, first_block, ray_block_stride,
+                                                                              n_blocks, w.seeds, w.jump);
+    k_ray_init<<<ray_blocks, 128, 0, s>>>(P, w.R);
+    stage_mark(s, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
+    for (int r = 0; r < P.n_rounds; ++r) {
+      k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r);
+      stage_mark(s, GF_STAGE_MARCH, 1);
+      launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, r, s);
+      stage_mark(s, GF_STAGE_SCATTER, nc <= 8192 ? 1 : 2);
+      run_mlp(t, packed, precision, S, &io, nullptr, s);
+      stage_mark(s, GF_STAGE_MLP, 1);
+    }
+    k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, P.n_rounds);
+    stage_mark(s, GF_STAGE_MARCH, 1);
+  };
+  // graphs for the production (tensor-core) path; the fp32 reference mode,
+  // traces and stage timing run eagerly
+  const bool use_graph = precision == GF_PRECISION_FP16 && !g_timer.on && !trace && !getenv("GF_NO_GRAPH");
+  if (!use_graph) {
+    enqueue(st);
+    return check_cuda("gf_render_rays");
   }
-  k_march<<<march_blocks, 128, 0, st>>>(P, w.R, w.RB, P.n_rounds);
-  stage_mark(st, GF_STAGE_MARCH, 1);
-  return check_cuda("gf_render_rays");
+  GraphKey key;  // every value a launch above reads on the host
+  key.add(P);
+  key.add(w);
+  key.add(packed);
+  key.add(precision);
+  key.add(nc);
+  key.add(cfg->seed);
+  key.add(n_blocks);
+  key.add(stride);
+  key.add(cplan.on);
+  key.add(cplan.word);
+  key.add(cplan.f);
+  key.add(cplan.radius);
+  key.add(cplan.ores);
+  key.add(cplan.cres);
+  key.add(march_blocks);
+  key.add(ray_blocks);
+  key.add(t);
+  return run_graph(key, st, enqueue);
 }
 
 // ---------------------------------------------------------------------------

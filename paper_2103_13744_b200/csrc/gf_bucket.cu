@@ -45,6 +45,9 @@ __device__ __forceinline__ uint2 block_exclusive_scan2(uint2 v, uint2* warp_tot,
 template <int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells) {
   __shared__ uint2 warp_tot[NT / 32];
+  extern __shared__ uint32_t s_toff[];  // per-cell first tile (n_cells + 1), when it fits
+  const bool in_smem = B.scan_smem_cells >= n_cells;
+  uint32_t* toff = in_smem ? s_toff : B.tile_off;
   uint2 carry = make_uint2(0, 0);
   for (int64_t chunk = 0; chunk < n_cells; chunk += (int64_t)NT * ITEMS) {
     uint32_t cnt[ITEMS];
@@ -66,11 +69,10 @@ __global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells
       if (c < n_cells) {
         B.offsets[c] = ex.x;
         B.cursor[c] = ex.x;
-        uint32_t nt = gf_div_up<uint32_t>(cnt[j], GF_TILE_ROWS);
-        for (uint32_t t = 0; t < nt; ++t) B.tiles[ex.y + t] = make_uint2((uint32_t)c, t * GF_TILE_ROWS);
+        toff[c] = ex.y;
         B.counts[c] = 0;
         ex.x += cnt[j];
-        ex.y += nt;
+        ex.y += gf_div_up<uint32_t>(cnt[j], GF_TILE_ROWS);
       }
     }
     carry.x += tot.x;
@@ -79,11 +81,29 @@ __global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells
   if (threadIdx.x == 0) {
     B.offsets[n_cells] = carry.x;
     *B.n_tiles = carry.y;
+    toff[n_cells] = carry.y;
+  }
+  __syncthreads();
+  // tile list, all threads in parallel: tile t belongs to the last cell whose
+  // first tile is <= t (binary search; empty cells share their successor's start)
+  const uint32_t nt = carry.y;
+  for (uint32_t t = threadIdx.x; t < nt; t += NT) {
+    int64_t lo = 0, hi = n_cells;  // invariant: toff[lo] <= t < toff[hi]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (toff[mid] <= t) lo = mid;
+      else hi = mid;
+    }
+    B.tiles[t] = make_uint2((uint32_t)lo, (t - toff[lo]) * GF_TILE_ROWS);
   }
 }
 
 void launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st) {
-  k_scan_cells<1024, 4><<<1, 1024, 0, st>>>(B, n_cells);
+  BucketBufs b = B;
+  const int64_t smem_cells = 48 * 1024 / 4 - 1;  // default dynamic smem budget
+  b.scan_smem_cells = n_cells <= smem_cells ? n_cells : 0;
+  const size_t smem = b.scan_smem_cells ? (size_t)(n_cells + 1) * 4 : 0;
+  k_scan_cells<1024, 4><<<1, 1024, smem, st>>>(b, n_cells);
 }
 
 // warp-aggregated cursor claim
@@ -101,24 +121,34 @@ __device__ __forceinline__ uint32_t claim_slot(uint32_t* cursor, bool pred, uint
   return pos;
 }
 
-// render path: records of ray i live at rec[i*stride .. +run[i])
-__global__ void __launch_bounds__(128) k_scatter_render(const float4* __restrict__ rec, const uint32_t* __restrict__ run,
-                                                        int64_t n_rays, int stride, BucketBufs B) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  uint32_t n = i < n_rays ? run[i] : 0u;
-  uint32_t nmax = __reduce_max_sync(0xffffffffu, n);
-  uint64_t base = (uint64_t)i * (uint64_t)stride;
-  for (uint32_t j = 0; j < nmax; ++j) {
-    bool p = j < n;
-    uint32_t key = p ? __float_as_uint(rec[base + j].w) : 0u;
-    uint32_t pos = claim_slot(B.cursor, p, key);
-    if (p) B.sorted[pos] = (uint32_t)(base + j);
+// render path: records of ray i live at rec[i*stride .. +run[i]); only the
+// rays the marcher listed (run > 0) are visited.  Persistent grid-stride;
+// also clears the other parity's list counter for the next round.
+__global__ void __launch_bounds__(256) k_scatter_render(const float4* __restrict__ rec, const uint32_t* __restrict__ run,
+                                                        const uint32_t* __restrict__ list, uint32_t* counts2,
+                                                        int round, int stride, BucketBufs B) {
+  const uint32_t n = counts2[round & 1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts2[(round + 1) & 1] = 0;
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t base_k = blockIdx.x * blockDim.x; base_k < n; base_k += step) {
+    const uint32_t k = base_k + threadIdx.x;
+    const bool ok = k < n;
+    const uint32_t i = ok ? list[k] : 0u;
+    const uint32_t cnt = ok ? run[i] : 0u;
+    const uint32_t nmax = __reduce_max_sync(0xffffffffu, cnt);
+    const uint64_t base = (uint64_t)i * (uint64_t)stride;
+    for (uint32_t j = 0; j < nmax; ++j) {
+      const bool p = j < cnt;
+      const uint32_t key = p ? __float_as_uint(rec[base + j].w) : 0u;
+      const uint32_t pos = claim_slot(B.cursor, p, key);
+      if (p) B.sorted[pos] = (uint32_t)(base + j);
+    }
   }
 }
 
-void launch_scatter_render(const float4* rec, const uint32_t* run, int64_t n_rays, int stride, const BucketBufs& B,
-                           cudaStream_t st) {
-  k_scatter_render<<<(unsigned)gf_div_up<int64_t>(n_rays, 128), 128, 0, st>>>(rec, run, n_rays, stride, B);
+void launch_scatter_render(const float4* rec, const uint32_t* run, const uint32_t* list, uint32_t* counts2, int round,
+                           int stride, const BucketBufs& B, cudaStream_t st) {
+  k_scatter_render<<<num_sms() * 8, 256, 0, st>>>(rec, run, list, counts2, round, stride, B);
 }
 
 // query path, pass 1: bounds check (core.py:92-101), network cell, histogram

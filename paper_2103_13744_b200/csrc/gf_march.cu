@@ -18,8 +18,18 @@ namespace gf {
 // per-block PCG64 seeds: SeedSequence([seed, 4096*b])   (render.py:569)
 // -------------------------------------------------------------------------
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
-                              u128* seeds) {
+                              u128* seeds, u128* jump) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) {
+    // LCG jump table: S_{n+d} = A^d S_n + (sum_{k<d} A^k) inc, d = 0..GF_JUMP_MAX
+    u128 a = 1, c = 0;
+    for (int d = 0; d <= GF_JUMP_MAX; ++d) {
+      jump[2 * d] = a;
+      jump[2 * d + 1] = c;
+      c = c * GF_PCG_MULT + 1;
+      a = a * GF_PCG_MULT;
+    }
+  }
   if (b >= n_blocks) return;
   u128 s, inc;
   gf_seed_block(seed, (uint64_t)((first_block + b * block_stride) * GF_RAY_BLOCK), &s, &inc);
@@ -213,13 +223,188 @@ __global__ void k_coarse_dilate(const uint8_t* __restrict__ coarse, int3 cres, i
   bits[w] = word;
 }
 
+// Word-parallel variants (fine rows 32-bit aligned: occ res.x % (32*factor) == 0).
+// One thread = 32 coarse cells along x.
+__global__ void k_coarse_reduce_w(const uint32_t* __restrict__ fine, int3 ores, int f, int3 cres, uint32_t* out) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int wpr = cres.x / 32;
+  if (w >= (int64_t)wpr * cres.y * cres.z) return;
+  const int wx = (int)(w % wpr), cy = (int)((w / wpr) % cres.y), cz = (int)(w / ((int64_t)wpr * cres.y));
+  uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int fz = cz * f; fz < cz * f + f; ++fz)
+    for (int fy = cy * f; fy < cy * f + f; ++fy) {
+      const int64_t row = ((int64_t)ores.x * (fy + (int64_t)ores.y * fz)) / 32 + (int64_t)wx * f;
+      for (int q = 0; q < f; ++q) acc[q] |= __ldg(fine + row + q);
+    }
+  const uint32_t lowf = (1u << f) - 1u;
+  uint32_t res = 0;
+  for (int b = 0; b < 32; ++b) {
+    const int bit = b * f;
+    if ((acc[bit >> 5] >> (bit & 31)) & lowf) res |= 1u << b;
+  }
+  out[w] = res;
+}
+
+__global__ void k_dilate_x(const uint32_t* __restrict__ in, uint32_t* out, int3 cres, int r) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int wpr = cres.x / 32;
+  if (w >= (int64_t)wpr * cres.y * cres.z) return;
+  const int wx = (int)(w % wpr);
+  const uint32_t v = in[w], prev = wx > 0 ? in[w - 1] : 0u, next = wx + 1 < wpr ? in[w + 1] : 0u;
+  uint32_t res = v;
+  for (int s = 1; s <= r; ++s) res |= (v << s) | (v >> s) | (prev >> (32 - s)) | (next << (32 - s));
+  out[w] = res;
+}
+
+// axis 1: y (stride = words per row), axis 2: z (stride = words per plane)
+__global__ void k_dilate_yz(const uint32_t* __restrict__ in, uint32_t* out, int3 cres, int r, int axis) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int wpr = cres.x / 32;
+  if (w >= (int64_t)wpr * cres.y * cres.z) return;
+  const int64_t stride = axis == 1 ? wpr : (int64_t)wpr * cres.y;
+  const int n = axis == 1 ? cres.y : cres.z;
+  const int c = axis == 1 ? (int)((w / wpr) % cres.y) : (int)(w / ((int64_t)wpr * cres.y));
+  uint32_t res = 0;
+  for (int o = max(c - r, 0); o <= min(c + r, n - 1); ++o) res |= in[w + (int64_t)(o - c) * stride];
+  out[w] = res;
+}
+
+// -------------------------------------------------------------------------
+// K2 placement (batched.py:60-85 group_by_network, as the MLP consumes it):
+// every record already carries its rank inside its cell (from the marcher's
+// histogram atomics), so its sorted slot is offsets[cell] + rank with no
+// atomics here.  SMEM: each CTA scans the per-cell counts into shared memory
+// itself (no separate scan launch); block 0 publishes offsets / n_tiles and
+// every thread writes part of the tile list.  !SMEM (very large grids):
+// offsets and tiles come from k_scan_cells.
+// -------------------------------------------------------------------------
+template <bool SMEM>
+__global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const uint32_t* __restrict__ run,
+                                               BucketBufs Bk, int64_t n_cells, int stride, int round) {
+  extern __shared__ uint32_t s_scan[];  // [n_cells+1] row offsets, [n_cells+1] tile offsets
+  const uint32_t* counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
+  const uint32_t* off = Bk.offsets;
+  const int tid = threadIdx.x;
+  const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + tid, gthreads = (uint64_t)gridDim.x * blockDim.x;
+  if (SMEM) {
+    __shared__ uint32_t wsum[2][16];
+    uint32_t* s_off = s_scan;
+    uint32_t* s_toff = s_scan + n_cells + 1;
+    const int per = (int)((n_cells + 511) / 512);
+    const int64_t c0 = (int64_t)tid * per;
+    uint32_t a = 0, b = 0;
+    for (int q = 0; q < per; ++q) {
+      const int64_t c = c0 + q;
+      if (c < n_cells) {
+        const uint32_t v = counts[c];
+        a += v;
+        b += (v + GF_TILE_ROWS - 1) / GF_TILE_ROWS;
+      }
+    }
+    // block exclusive scan of (a, b)
+    const int lane = tid & 31, wid = tid >> 5;
+    uint32_t xa = a, xb = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+      if (lane >= o) { xa += ya; xb += yb; }
+    }
+    if (lane == 31) { wsum[0][wid] = xa; wsum[1][wid] = xb; }
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t ta = lane < 16 ? wsum[0][lane] : 0, tb = lane < 16 ? wsum[1][lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        const uint32_t ya = __shfl_up_sync(0xffffffffu, ta, o), yb = __shfl_up_sync(0xffffffffu, tb, o);
+        if (lane >= o) { ta += ya; tb += yb; }
+      }
+      if (lane < 16) { wsum[0][lane] = ta; wsum[1][lane] = tb; }
+    }
+    __syncthreads();
+    uint32_t ea = (wid ? wsum[0][wid - 1] : 0) + xa - a, eb = (wid ? wsum[1][wid - 1] : 0) + xb - b;
+    for (int q = 0; q < per; ++q) {
+      const int64_t c = c0 + q;
+      if (c < n_cells) {
+        const uint32_t v = counts[c];
+        s_off[c] = ea;
+        s_toff[c] = eb;
+        ea += v;
+        eb += (v + GF_TILE_ROWS - 1) / GF_TILE_ROWS;
+      }
+    }
+    if (tid == 511) {
+      s_off[n_cells] = ea;
+      s_toff[n_cells] = eb;
+    }
+    __syncthreads();
+    const uint32_t n_tiles = s_toff[n_cells];
+    if (blockIdx.x == 0) {
+      for (int64_t c = tid; c <= n_cells; c += 512) Bk.offsets[c] = s_off[c];
+      if (tid == 0) {
+        *Bk.n_tiles = n_tiles;
+        RB.emit_count[(round + 1) & 1] = 0;
+      }
+    }
+    uint32_t* other = RB.counts + (size_t)((round + 1) & 1) * (size_t)n_cells;  // next round's histogram
+    for (uint64_t c = gtid; c < (uint64_t)n_cells; c += gthreads) {
+      other[c] = 0;
+      for (uint32_t t = s_toff[c]; t < s_toff[c + 1]; ++t)
+        Bk.tiles[t] = make_uint2((uint32_t)c, (t - s_toff[c]) * GF_TILE_ROWS);
+    }
+    off = s_off;
+  } else if (gtid == 0) {
+    RB.emit_count[(round + 1) & 1] = 0;
+  }
+  const uint32_t n_list = RB.emit_count[round & 1];
+  for (uint64_t k = gtid; k < n_list; k += gthreads) {
+    const uint32_t i = RB.emit_list[k];
+    const uint32_t nr = run[i];
+    const uint64_t base = (uint64_t)i * (uint64_t)stride;
+    for (uint32_t j = 0; j < nr; ++j) {
+      const float4 q = RB.rec[base + j];
+      const uint32_t cell = gf_flat_cell(grid, q.x, q.y, q.z);
+      Bk.sorted[off[cell] + __float_as_uint(q.w)] = (uint32_t)(base + j);
+    }
+  }
+}
+
+void launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
+                  int stride, int round, cudaStream_t st) {
+  const size_t smem = (size_t)2 * (n_cells + 1) * 4;
+  if (n_cells <= 8192) {
+    static thread_local bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_place<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8193 * 4);
+      attr = true;
+    }
+    k_place<true><<<num_sms() * 2, 512, smem, st>>>(grid, RB, run, Bk, n_cells, stride, round);
+  } else {
+    BucketBufs b = Bk;
+    b.counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
+    launch_scan_cells(b, n_cells, st);  // offsets + tiles; clears this round's counts after reading
+    k_place<false><<<num_sms() * 2, 512, 0, st>>>(grid, RB, run, Bk, n_cells, stride, round);
+  }
+}
+
+__device__ __forceinline__ u128 ldg_u128(const u128* p) {
+  const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(p));
+  return ((u128)v.y << 64) | v.x;
+}
+
 // warp-aggregated histogram increment: lanes with `pred` add 1 to hist[key]
-__device__ __forceinline__ void hist_add(uint32_t* hist, bool pred, uint32_t key) {
+// and receive their rank among all samples of that key this round (the
+// atomic's return value), i.e. their final row inside the cell's segment.
+__device__ __forceinline__ uint32_t hist_rank(uint32_t* hist, bool pred, uint32_t key) {
   unsigned act = __ballot_sync(0xffffffffu, pred);
+  uint32_t rank = 0;
   if (pred) {
     unsigned peers = __match_any_sync(act, key);
-    if ((unsigned)__ffs(peers) - 1 == gf_lane()) atomicAdd(&hist[key], (uint32_t)__popc(peers));
+    const int leader = __ffs(peers) - 1;
+    uint32_t b = 0;
+    if ((int)gf_lane() == leader) b = atomicAdd(&hist[key], (uint32_t)__popc(peers));
+    rank = __shfl_sync(peers, b, leader) + __popc(peers & ((1u << gf_lane()) - 1u));
   }
+  return rank;
 }
 
 __device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v) {
@@ -333,7 +518,111 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     cmask &= msk;
   }
   const bool fast_clip = P.grid.fast != 0;
+  uint32_t* counts_r = B.counts + (size_t)(round & 1) * (size_t)P.n_cells;  // this round's histogram
   uint32_t kept = 0;
+  if (m <= 32) {
+    // ---- warp-cooperative path: the warp's candidate (ray, slot) pairs are
+    // enumerated in (lane, slot) order and processed 32 at a time, one per
+    // lane, so the exact float64 placement never runs on idle lanes.
+    __shared__ uint32_t s_carry[4][32];  // kept samples so far, per ray (lane) of each warp
+    const int wib = threadIdx.x >> 5;
+    const unsigned lane = gf_lane();
+    if (!active) cmask = 0;
+    s_carry[wib][lane] = 0;
+    const uint32_t cnt = __popc(cmask);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o2);
+      if ((int)lane >= o2) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - cnt;
+    const uint32_t d0 = (uint32_t)draw;  // float32 draw index of slot s0 in the ray's block stream
+    const uint64_t S_lo = (uint64_t)S, S_hi = (uint64_t)(S >> 64), I_lo = (uint64_t)inc, I_hi = (uint64_t)(inc >> 64);
+    __syncwarp();
+    for (uint32_t b0 = 0; b0 < total; b0 += 32) {
+      const uint32_t k = b0 + lane;
+      const bool has = k < total;
+      int own = 0;  // smallest lane whose inclusive count exceeds k
+#pragma unroll
+      for (int st = 16; st; st >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, own + st - 1);
+        if (v <= k) own += st;
+      }
+      const uint32_t rank = k - __shfl_sync(0xffffffffu, excl, own);
+      const uint32_t cm_o = __shfl_sync(0xffffffffu, cmask, own);
+      const float ox_o = __shfl_sync(0xffffffffu, o.x, own), oy_o = __shfl_sync(0xffffffffu, o.y, own);
+      const float oz_o = __shfl_sync(0xffffffffu, o.z, own), t0_o = __shfl_sync(0xffffffffu, o.w, own);
+      const float dx_o = __shfl_sync(0xffffffffu, d.x, own), dy_o = __shfl_sync(0xffffffffu, d.y, own);
+      const float dz_o = __shfl_sync(0xffffffffu, d.z, own), sg_o = __shfl_sync(0xffffffffu, d.w, own);
+      const int64_t i_o = __shfl_sync(0xffffffffu, (long long)i, own);
+      double jit = 0.5;
+      int j = 0;
+      if (has) j = (int)__fns(cm_o, 0, (int)rank + 1);
+      if (P.stratified) {
+        const uint32_t d0_o = __shfl_sync(0xffffffffu, d0, own);
+        const u128 So = ((u128)__shfl_sync(0xffffffffu, S_hi, own) << 64) | __shfl_sync(0xffffffffu, S_lo, own);
+        const u128 Io = ((u128)__shfl_sync(0xffffffffu, I_hi, own) << 64) | __shfl_sync(0xffffffffu, I_lo, own);
+        if (has) {
+          const uint32_t dd = d0_o + (uint32_t)j;
+          const uint32_t delta = (dd >> 1) - (d0_o >> 1);
+          const u128 Sj = ldg_u128(&P.jump[2 * delta]) * So + ldg_u128(&P.jump[2 * delta + 1]) * Io;
+          const uint64_t w = gf_pcg_output(Sj);
+          const uint32_t u = (dd & 1) ? (uint32_t)(w >> 32) : (uint32_t)w;
+          jit = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, (int)(u >> 8)), 4503599627370496.0),
+                          5.9604644775390625e-8);
+        }
+      }
+      bool keep = false;
+      uint32_t cell = 0;
+      float px = 0.f, py = 0.f, pz = 0.f;
+      if (has) {
+        // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
+        const double t = __dadd_rn((double)t0_o, __dmul_rn(__dadd_rn((double)(s0 + j), jit), (double)sg_o));
+        px = __double2float_rn(__dadd_rn((double)ox_o, __dmul_rn(t, (double)dx_o)));
+        py = __double2float_rn(__dadd_rn((double)oy_o, __dmul_rn(t, (double)dy_o)));
+        pz = __double2float_rn(__dadd_rn((double)oz_o, __dmul_rn(t, (double)dz_o)));
+        if (fast_clip) {
+          px = gf_clip_fast(px, P.grid.b_min_f[0], P.grid.b_max_f[0]);
+          py = gf_clip_fast(py, P.grid.b_min_f[1], P.grid.b_max_f[1]);
+          pz = gf_clip_fast(pz, P.grid.b_min_f[2], P.grid.b_max_f[2]);
+        } else {
+          px = gf_clip_component(px, P.grid.b_min[0], P.grid.b_max[0]);
+          py = gf_clip_component(py, P.grid.b_min[1], P.grid.b_max[1]);
+          pz = gf_clip_component(pz, P.grid.b_min[2], P.grid.b_max[2]);
+        }
+        keep = true;
+        if (P.occ_bits) {
+          const uint32_t f = gf_flat_cell(P.occ, px, py, pz);
+          keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
+        }
+        if (keep) cell = gf_flat_cell(P.grid, px, py, pz);
+      }
+      // position of this sample in its ray's run: kept items of the same ray
+      // earlier in this batch + kept items of earlier batches
+      const unsigned kb = __ballot_sync(0xffffffffu, keep);
+      const unsigned same = __match_any_sync(0xffffffffu, has ? own : 32 + (int)lane);
+      const uint32_t pos = s_carry[wib][own] + __popc(kb & same & ((1u << lane) - 1u));
+      const uint32_t crank = hist_rank(counts_r, keep, cell);
+      if (keep) {
+        B.rec[(uint64_t)i_o * (uint64_t)P.stride + pos] = make_float4(px, py, pz, __uint_as_float(crank));
+        if (P.trace) {
+          unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
+          if ((int64_t)slotpos < P.trace_capacity)
+            P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, i_o), (uint32_t)(s0 + j), cell};
+        }
+      }
+      __syncwarp();
+      if (has && (int)lane == __ffs(same) - 1) s_carry[wib][own] += __popc(kb & same);
+      __syncwarp();
+    }
+    kept = s_carry[wib][lane];
+    if (P.stratified && active) {
+      const uint32_t delta = ((d0 + (uint32_t)m) >> 1) - (d0 >> 1);
+      S = ldg_u128(&P.jump[2 * delta]) * S + ldg_u128(&P.jump[2 * delta + 1]) * inc;
+    }
+  } else {
   double jd = (double)s0;
   for (int j = 0; j < m; ++j, jd += 1.0) {
     double jit = 0.5;
@@ -354,12 +643,13 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     const bool cand = active && (j >= 32 || ((cmask >> j) & 1u));
     bool keep = false;
     uint32_t cell = 0;
+    float px = 0.f, py = 0.f, pz = 0.f;
     if (__any_sync(0xffffffffu, cand) && cand) {
       // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
       const double t = __dadd_rn(t0, __dmul_rn(__dadd_rn(jd, jit), sg64));
-      float px = __double2float_rn(__dadd_rn(ox, __dmul_rn(t, dx)));
-      float py = __double2float_rn(__dadd_rn(oy, __dmul_rn(t, dy)));
-      float pz = __double2float_rn(__dadd_rn(oz, __dmul_rn(t, dz)));
+      px = __double2float_rn(__dadd_rn(ox, __dmul_rn(t, dx)));
+      py = __double2float_rn(__dadd_rn(oy, __dmul_rn(t, dy)));
+      pz = __double2float_rn(__dadd_rn(oz, __dmul_rn(t, dz)));
       if (fast_clip) {
         px = gf_clip_fast(px, P.grid.b_min_f[0], P.grid.b_max_f[0]);
         py = gf_clip_fast(py, P.grid.b_min_f[1], P.grid.b_max_f[1]);
@@ -374,22 +664,33 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
         const uint32_t f = gf_flat_cell(P.occ, px, py, pz);
         keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
       }
-      if (keep) {
-        cell = gf_flat_cell(P.grid, px, py, pz);
-        B.rec[base + kept] = make_float4(px, py, pz, __uint_as_float(cell));
-        if (P.trace) {
-          unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
-          if ((int64_t)slotpos < P.trace_capacity)
-            P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, i), (uint32_t)(s0 + j), cell};
-        }
-        ++kept;
-      }
+      if (keep) cell = gf_flat_cell(P.grid, px, py, pz);
     }
-    hist_add(B.counts, keep, cell);
+    const uint32_t rank = hist_rank(counts_r, keep, cell);
+    if (keep) {
+      B.rec[base + kept] = make_float4(px, py, pz, __uint_as_float(rank));
+      if (P.trace) {
+        unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
+        if ((int64_t)slotpos < P.trace_capacity)
+          P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, i), (uint32_t)(s0 + j), cell};
+      }
+      ++kept;
+    }
   }
+  }  // sequential path (ert_chunk > 32)
   if (active) {
     R.run[i] = kept;
     if (P.stratified) R.rng[i] = S;
+  }
+  {  // compact list of rays with queried samples, for the scatter kernel
+    const bool emit = active && kept > 0;
+    const unsigned em = __ballot_sync(0xffffffffu, emit);
+    if (em) {
+      uint32_t b = 0;
+      if (gf_lane() == 0) b = atomicAdd(&B.emit_count[round & 1], (uint32_t)__popc(em));
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (emit) B.emit_list[b + __popc(em & ((1u << gf_lane()) - 1u))] = (uint32_t)i;
+    }
   }
   warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], kept);
   warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], active ? (unsigned long long)(m - (int)kept) : 0ull);

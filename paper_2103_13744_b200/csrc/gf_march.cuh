@@ -1,6 +1,6 @@
 // Marcher data structures shared by gf_march.cu and gf_api.cu.
 #pragma once
-#include "gf_common.cuh"
+#include "gf_bucket.cuh"
 
 #define GF_RAY_ALIVE 1
 #define GF_RAY_HIT 2
@@ -21,8 +21,10 @@ struct MarchParams {
   const float* dirs;
   int64_t ray_offset, n_rays, first_block, block_stride;
   const u128* block_seeds;  // [2*b] state, [2*b+1] inc
+  const u128* jump;         // [2*d] A^d, [2*d+1] sum_{k<d} A^k  (d <= GF_JUMP_MAX)
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
   int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
+  int64_t n_cells;
   int64_t march_threads;
   double epsilon;
   float bg[3];
@@ -51,9 +53,11 @@ struct RayState {
 // kept samples of ray i in this round are rec[i*stride .. i*stride+run[i]),
 // in slot order, which is the order compositing consumes them.
 struct RoundBufs {
-  float4* rec;        // x, y, z, cell(bits)
+  float4* rec;        // x, y, z, rank of the sample inside its cell's segment (bits)
   float4* res;        // r, g, b, sigma written by the MLP
-  uint32_t* counts;   // per-cell histogram of this round
+  uint32_t* counts;   // [2][n_cells] per-cell histograms, by round parity
+  uint32_t* emit_list;   // rays that queried samples this round (for the scatter)
+  uint32_t* emit_count;  // [2], indexed by round parity
 };
 
 // Global index (within the render_rays call) of the call's local ray i.
@@ -78,11 +82,21 @@ __device__ __forceinline__ int64_t seed_slot(const MarchParams& P, int64_t g) {
   return (g / GF_RAY_BLOCK - P.first_block) / P.block_stride;
 }
 
+#define GF_JUMP_MAX 32  // largest PCG64 jump inside one round (chunk <= 32 -> <= 16 outputs)
+
+// K2 for the render path (fused scan + tile list + rank-based placement);
+// returns the number of launches it made
+void launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
+                  int stride, int round, cudaStream_t st);
+
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
-                              u128* seeds);
+                              u128* seeds, u128* jump);
 __global__ void k_ray_init(MarchParams P, RayState R);
 __global__ void k_coarse_reduce(const uint8_t* occ_bits, int3 occ_res, int factor, int3 cres, uint8_t* coarse);
 __global__ void k_coarse_dilate(const uint8_t* coarse, int3 cres, int radius, uint32_t* bits);
+__global__ void k_coarse_reduce_w(const uint32_t* fine, int3 ores, int f, int3 cres, uint32_t* out);
+__global__ void k_dilate_x(const uint32_t* in, uint32_t* out, int3 cres, int r);
+__global__ void k_dilate_yz(const uint32_t* in, uint32_t* out, int3 cres, int r, int axis);
 
 // Approximate (clamped) coarse cell of a float32 point; exactness is not
 // needed because the mip is dilated past the evaluation error.

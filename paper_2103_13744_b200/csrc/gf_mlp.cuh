@@ -125,4 +125,9 @@ bool launch_mlp_tc_query(const LayerTable& t, const void* packed, const TileSche
 
 int num_sms();
 
+// one-time per-process launch setup (smem attribute, residency) done outside
+// graph capture; return false if the architecture has no compiled variant
+bool prepare_mlp_fp32(const LayerTable& t);
+bool prepare_mlp_tc(const LayerTable& t);
+
 }  // namespace gf

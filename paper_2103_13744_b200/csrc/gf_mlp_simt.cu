@@ -15,6 +15,10 @@ static bool launch_fp32(const LayerTable& t, const float* packed, const TileSche
   return false;
 }
 
+bool prepare_mlp_fp32(const LayerTable& t) {
+  return t.pos_dim == 63 && t.dir_dim == 27 && t.view == t.width && t.trunk == 2 && (t.width == 32 || t.width == 64);
+}
+
 bool launch_mlp_fp32_render(const LayerTable& t, const float* packed, const TileSched& S, const RenderIO& io,
                             cudaStream_t st) {
   return launch_fp32(t, packed, S, io, st);

@@ -105,7 +105,11 @@ template <int W, class IO>
 void launch_fp32_width(const float* packed, const Fp32Layout& L, const TileSched& S, const IO& io, cudaStream_t st) {
   size_t smem = (size_t)L.cell_floats * sizeof(float);
   auto k = k_mlp_fp32<W, 2, 10, 4, IO>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static thread_local size_t smem_set = 0;  // attribute set once per thread (outside graph capture)
+  if (smem_set < smem) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_set = smem;
+  }
   k<<<num_sms() * 4, 128, smem, st>>>(packed, L, S, io);
 }
 

@@ -503,7 +503,7 @@ bool launch_pack_fp16(const LayerTable& t, int64_t n_cells, const float* const* 
 }
 
 template <int W, class IO>
-static void launch_tc_w(const void* packed, const TileSched& S, const IO& io, cudaStream_t st) {
+static int tc_resident() {
   using T = TcShape<W>;
   auto k = k_mlp_tc<W, IO>;
   static thread_local int per_sm = 0;  // resident CTAs per SM for this instantiation
@@ -528,7 +528,21 @@ static void launch_tc_w(const void* packed, const TileSched& S, const IO& io, cu
               T::SMEM, regs, per_sm, by_smem, by_regs, by_tmem);
     cudaGetLastError();
   }
-  k<<<num_sms() * per_sm, 128, T::SMEM, st>>>((const uint8_t*)packed, S, io);
+  return per_sm;
+}
+
+template <int W, class IO>
+static void launch_tc_w(const void* packed, const TileSched& S, const IO& io, cudaStream_t st) {
+  using T = TcShape<W>;
+  k_mlp_tc<W, IO><<<num_sms() * tc_resident<W, IO>(), 128, T::SMEM, st>>>((const uint8_t*)packed, S, io);
+}
+
+bool prepare_mlp_tc(const LayerTable& t) {
+  if (!tc_supported(t)) return false;
+  num_sms();
+  if (t.width == 32) tc_resident<32, RenderIO>();
+  else tc_resident<64, RenderIO>();
+  return true;
 }
 
 template <class IO>

@@ -11,6 +11,7 @@ host only transfers the camera in and the image + 4 counters out.
 
 from __future__ import annotations
 
+import threading
 import time
 from dataclasses import dataclass
 
@@ -276,9 +277,30 @@ def unshard_index(n_rays: int, world: int) -> np.ndarray:
     return (b % world) * cap + (b // world) * RAY_BLOCK + w
 
 
+_ctx = threading.local()
+
+
+def _render_context(n: int, ws_bytes: int):
+    """Per-thread persistent device buffers for a frame shape, so repeated
+    calls present identical pointers to the library (its CUDA-graph cache is
+    keyed on every kernel argument) and avoid allocator churn."""
+    t = D.require_cuda()
+    cache = getattr(_ctx, "bufs", None)
+    if cache is None:
+        cache = _ctx.bufs = {}
+    key = (t.cuda.current_device(), n)
+    c = cache.get(key)
+    if c is None or c["ws"].numel() < ws_bytes:
+        c = {"ws": D.workspace(ws_bytes), "rgb": D.empty((n, 3), t.float32),
+             "stats": t.zeros(4, dtype=t.int64, device=D.device()),
+             "host_stats": t.empty(4, dtype=t.int64, pin_memory=True)}
+        cache[key] = c
+    return c
+
+
 def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camera | None = None, origins=None,
                        directions=None, ray_offset: int = 0, n_rays: int | None = None, block_stride: int = 1,
-                       precision=None, out=None, stats=None, trace_capacity: int = 0):
+                       precision=None, out=None, stats=None, trace_capacity: int = 0, ws=None):
     """Device-resident core of render_rays / render_image.  Returns
     (rgb (n,3) float32 CUDA tensor, stats int64[4] CUDA tensor, trace or None).
     ``origins``/``directions`` may be CUDA tensors; ``cam`` generates rays
@@ -309,7 +331,8 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
     if trace_capacity:
         trace = D.empty((trace_capacity * N.TRACE_DTYPE.itemsize,), t.uint8)
         tcount = t.zeros(1, dtype=t.int64, device=rgb.device)
-    ws = D.workspace(N.lib().gf_render_workspace_bytes(arch, geom, ncfg, n))
+    if ws is None:
+        ws = D.workspace(N.lib().gf_render_workspace_bytes(arch, geom, ncfg, n))
     N.check(N.lib().gf_render_rays(
         arch, geom, N.ptr(packed), N.PRECISION[p], occ_geom, N.ptr(occ_bits), ncfg, ccam, N.ptr(o_d), N.ptr(d_d),
         int(ray_offset), int(block_stride), int(n), N.ptr(rgb), N.ptr(st), N.ptr(trace), int(trace_capacity), N.ptr(tcount),
@@ -353,13 +376,20 @@ def render_image(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0
     t_start = time.perf_counter()
     grid = _field_grid(field)
     t = D.require_cuda()
-    rgb, st, _ = render_rays_device(grid, occupancy, cfg, seed, cam=cam, precision=precision)
+    n = cam.width * cam.height
+    ncfg = cfg.native(seed)
+    ws_bytes = N.lib().gf_render_workspace_bytes(grid.native_arch(), grid.native_geom(), ncfg, n)
+    c = _render_context(n, ws_bytes)
+    c["stats"].zero_()
+    rgb, st, _ = render_rays_device(grid, occupancy, cfg, seed, cam=cam, precision=precision, out=c["rgb"],
+                                    stats=c["stats"], ws=c["ws"])
+    # fresh pinned block per call (torch's caching host allocator recycles it
+    # once the returned array is dropped), so the result needs no extra copy
     host = t.empty(rgb.shape, dtype=t.float32, pin_memory=True)
     host.copy_(rgb, non_blocking=True)
-    stats_h = t.empty(4, dtype=t.int64, pin_memory=True)
-    stats_h.copy_(st, non_blocking=True)
+    c["host_stats"].copy_(st, non_blocking=True)
     t.cuda.current_stream().synchronize()
-    stats = _stats_from(stats_h)
+    stats = _stats_from(c["host_stats"])
     stats.wall_ms = (time.perf_counter() - t_start) * 1000.0
     return host.numpy().reshape(cam.height, cam.width, 3), stats
 
