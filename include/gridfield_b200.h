@@ -61,7 +61,7 @@ typedef struct {
   int32_t res[3];
 } gf_grid_geom_t;
 
-/* render.py:368-390 RenderConfig plus the call's seed. */
+/* render.py:174-196 RenderConfig plus the call's seed. */
 typedef struct {
   int32_t k;               /* nominal samples per ray                         */
   int32_t ert_chunk;       /* samples per marching round                      */
@@ -73,14 +73,14 @@ typedef struct {
   uint64_t seed;           /* render_rays(seed=...)                           */
 } gf_march_cfg_t;
 
-/* render.py:219-251 Camera (pinhole, c2w row-major 3x4). */
+/* render.py:25-57 Camera (pinhole, c2w row-major 3x4). */
 typedef struct {
   int32_t width, height;
   double fx, fy, cx, cy;
   double c2w[12];
 } gf_camera_t;
 
-/* RenderStats counters (render.py:404-416), int64 on device, in this order. */
+/* RenderStats counters (render.py:210-222), int64 on device, in this order. */
 enum { GF_STAT_TOTAL_QUERIES = 0, GF_STAT_ESS_SKIPPED = 1, GF_STAT_ERT_TERMINATED = 2, GF_STAT_N_RAYS = 3, GF_STAT_COUNT = 4 };
 
 /* Optional per-sample trace of the marcher (test / debug only). */
@@ -94,7 +94,7 @@ typedef struct {
 GF_API int gf_abi_version(void);
 GF_API const char* gf_last_error(void);
 
-/* Number of float parameters per cell in manifest order (mlp.py:386-387). */
+/* Number of float parameters per cell in manifest order (mlp.py:86-87). */
 GF_API int64_t gf_param_count(const gf_arch_t* arch);
 
 /* --- weight packing ------------------------------------------------------
@@ -127,7 +127,7 @@ GF_API int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void
                               const int64_t* order_dev, float* rgb_dev, float* sigma_dev, void* ws_dev,
                               size_t ws_bytes, void* stream);
 
-/* --- render.render_rays / render_image (render.py:545-594) ---------------
+/* --- render.render_rays / render_image (render.py:351-400) ---------------
  * Rays come either from `cam` (pixel index = ray_offset + i, row-major) or
  * from float32 origins/directions (ray i of the call is global ray
  * ray_offset + i).  ray_offset selects the 4096-ray jitter blocks so shards of
@@ -170,12 +170,12 @@ GF_API int gf_positional_encode(const void* v_dev, int32_t v_f64, int64_t n, int
 /* core.py:187-194 density_to_alpha (elementwise, same length, same dtype). */
 GF_API int gf_density_to_alpha(const void* sigma_dev, const void* delta_dev, int32_t f64, int64_t n, void* out_dev,
                                void* stream);
-/* render.py:463-478 composite: n_rays x n_samples, float32.                */
+/* render.py:269-284 composite: n_rays x n_samples, float32.                */
 GF_API int gf_composite(const float* colors_dev, const float* alphas_dev, int64_t n_rays, int64_t n_samples,
                  float* rgb_dev, float* trans_dev, void* stream);
 GF_API int gf_composite_f64(const double* colors_dev, const double* alphas_dev, int64_t n_rays, int64_t n_samples,
                      double* rgb_dev, double* trans_dev, void* stream);
-/* render.py:333-342 generate_rays for a camera (float32 origins, dirs).    */
+/* render.py:139-148 generate_rays for a camera (float32 origins, dirs).    */
 GF_API int gf_generate_rays(const gf_camera_t* cam, float* origins_dev, float* dirs_dev, void* stream);
 
 /* --- instrumentation ------------------------------------------------------
@@ -192,7 +192,7 @@ GF_API int64_t gf_launch_count(void);
 
 /* --- host-side helpers (no device work) ---------------------------------- */
 /* PCG64(SeedSequence([seed, block_start])).state as {state_hi, state_lo,
- * inc_hi, inc_lo} (numpy semantics; render.py:569).                          */
+ * inc_hi, inc_lo} (numpy semantics; render.py:375).                          */
 GF_API int gf_pcg64_block_state(uint64_t seed, uint64_t block_start, uint64_t out4[4]);
 
 #ifdef __cplusplus

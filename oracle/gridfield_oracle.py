@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-RAY_BLOCK = 4096  # render.py:216
+RAY_BLOCK = 4096  # render.py:22
 
 LAYER_ORDER = ("trunk", "density", "feature", "direction", "color")
 
@@ -37,7 +37,7 @@ LAYER_ORDER = ("trunk", "density", "feature", "direction", "color")
 
 
 def layer_manifest(hidden_layers=4, width=32, pos_dim=63, dir_dim=27, view_width=None, skip_layer=None):
-    """(name, in, out) list; mlp.py:373-384."""
+    """(name, in, out) list; mlp.py:73-84."""
     v = view_width or width
     out = [("trunk0", pos_dim, width)]
     for k in range(1, hidden_layers - 2):
@@ -290,12 +290,12 @@ class Occupancy:
 
 
 # --------------------------------------------------------------------------
-# rays and marching (render.py:333-594)
+# rays and marching (render.py:139-400)
 # --------------------------------------------------------------------------
 
 
 def pixel_rays(width, height, fx, fy, cx, cy, c2w):
-    """render.py:333-342, restated per component: u,v in f64; world direction
+    """render.py:139-148, restated per component: u,v in f64; world direction
     R.[u,v,1] in f64; normalise by the f64 Euclidean norm; cast to float32."""
     c2w = np.asarray(c2w, np.float64)
     u = (np.arange(width) + 0.5 - cx) / fx
@@ -311,7 +311,7 @@ def pixel_rays(width, height, fx, fy, cx, cy, c2w):
 
 
 def slab(o, d, b_min, b_max):
-    """render.py:345-365 slab test in f64; parallel components use the inside test."""
+    """render.py:151-171 slab test in f64; parallel components use the inside test."""
     o = np.asarray(o, np.float64)
     d = np.asarray(d, np.float64)
     with np.errstate(divide="ignore", invalid="ignore"):
@@ -352,7 +352,7 @@ class Counters:
 
 
 def march_block(query, b_min, b_max, occ, o64, d64, cfg: MarchConfig, gen, ray_base=0, trace=False):
-    """render.py:481-542 for one ray block.  ``query(pos, dir) -> (rgb, sigma)``.
+    """render.py:287-348 for one ray block.  ``query(pos, dir) -> (rgb, sigma)``.
 
     Promotion rules reproduced: sample distance
     ``t = f64(t0_32) + (f64(j) + f64(jitter_32)) * f64(seg_32)``, position
@@ -414,7 +414,7 @@ def march_block(query, b_min, b_max, occ, o64, d64, cfg: MarchConfig, gen, ray_b
 
 
 def render_rays(query, b_min, b_max, occ, origins, directions, cfg: MarchConfig, seed=0, workers=1, trace=False):
-    """render.py:545-578: fixed 4096-ray blocks, jitter stream per block from
+    """render.py:351-384: fixed 4096-ray blocks, jitter stream per block from
     ``SeedSequence([seed, block_start])``, thread pool over blocks."""
     o = np.asarray(origins, np.float64).reshape(-1, 3)
     d = np.asarray(directions, np.float64).reshape(-1, 3)
@@ -440,7 +440,7 @@ def render_rays(query, b_min, b_max, occ, origins, directions, cfg: MarchConfig,
 
 
 def render_image(lat: Lattice, occ: Occupancy | None, cam, cfg: MarchConfig, seed=0, workers=1, trace=False):
-    """render.py:581-594 for a NetworkGrid field; ``cam`` has width, height,
+    """render.py:387-400 for a NetworkGrid field; ``cam`` has width, height,
     fx, fy, cx, cy, c2w."""
     o, d = pixel_rays(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, cam.c2w)
     q = lambda p, dd: query_points(lat, p, dd)
@@ -449,7 +449,7 @@ def render_image(lat: Lattice, occ: Occupancy | None, cam, cfg: MarchConfig, see
 
 
 def composite(colors, alphas):
-    """render.py:463-478 (front-to-back blending, batch dims allowed)."""
+    """render.py:269-284 (front-to-back blending, batch dims allowed)."""
     colors = np.asarray(colors)
     alphas = np.asarray(alphas)
     if colors.shape[-2] == 0:

@@ -4,9 +4,9 @@ float32 draw stream that the reference renderer consumes.
 TEST INFRASTRUCTURE ONLY.  This module is the checker for the C++ port in
 ``paper_2103_13744_b200/csrc/seedseq.cpp``; nothing in the product imports it.
 
-Reference call site: ``render.py:569``
+Reference call site: ``render.py:375``
     rng = np.random.default_rng(np.random.SeedSequence([seed, block_start]))
-and ``render.py:490`` ``rng.random((n, k), dtype=np.float32)``.
+and ``render.py:296`` ``rng.random((n, k), dtype=np.float32)``.
 numpy (pinned here at 2.3.5, third-party, not under /root/reference) defines
 the algorithm: SeedSequence pool mixing (pool size 4, 32-bit hashmix), PCG64
 ``set_seed`` from four generated 64-bit words, XSL-RR output, and float32

@@ -12,7 +12,7 @@
 
 #include "../../include/gridfield_b200.h"
 
-#define GF_RAY_BLOCK 4096  // render.py:216 RAY_BLOCK
+#define GF_RAY_BLOCK 4096  // render.py:22 RAY_BLOCK
 #define GF_TILE_ROWS 128   // MLP rows per tile (one TMEM lane per row)
 
 typedef unsigned __int128 u128;

@@ -2,20 +2,20 @@
 // placement, clip, empty-space skipping, per-round emission, compositing and
 // early ray termination.
 //
-// Reference: render.py:333-365 (rays, slab), render.py:481-542 (_march_block),
-// render.py:545-578 (4096-ray blocks + SeedSequence jitter streams),
+// Reference: render.py:139-171 (rays, slab), render.py:287-348 (_march_block),
+// render.py:351-384 (4096-ray blocks + SeedSequence jitter streams),
 // core.py:52-112 (clip / bin), occupancy.py:65-79 (bit lookup),
 // core.py:187-194 (alpha).
 //
 // One thread owns one ray for the whole frame.  Rounds (ert_chunk samples)
 // are separate launches because the next round's live set depends on the
-// MLP results of this round (chunk-granular ERT, render.py:532-537).
+// MLP results of this round (chunk-granular ERT, render.py:338-343).
 #include "gf_march.cuh"
 
 namespace gf {
 
 // -------------------------------------------------------------------------
-// per-block PCG64 seeds: SeedSequence([seed, 4096*b])   (render.py:569)
+// per-block PCG64 seeds: SeedSequence([seed, 4096*b])   (render.py:375)
 // -------------------------------------------------------------------------
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
                               u128* seeds, u128* jump) {
@@ -112,7 +112,7 @@ __device__ void coarse_intervals(const MarchParams& P, uint32_t* out, float ex, 
 }
 
 // -------------------------------------------------------------------------
-// ray setup: render.py:333-342 generate_rays (if camera), 368-369 f64 upcast,
+// ray setup: render.py:139-148 generate_rays (if camera), 368-369 f64 upcast,
 // 486-500 slab test / seg / t0 in float32, and the ray's jitter stream
 // position.
 // -------------------------------------------------------------------------
@@ -143,7 +143,7 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
       d32[a] = P.dirs[3 * i + a];
     }
   }
-  // slab test in f64 (render.py:345-365)
+  // slab test in f64 (render.py:151-171)
   double lo_max = -INFINITY, hi_min = INFINITY;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     acc = R.acc[i];
     seg = R.dir[i].w;
     if (round > 0) {
-      // ---- composite round r-1 (render.py:527-531), float32, no contraction
+      // ---- composite round r-1 (render.py:333-337), float32, no contraction
       uint32_t n = R.run[i];
       float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
       for (uint32_t j = 0; j < n; ++j) {
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       acc.y = __fadd_rn(acc.y, __fmul_rn(acc.w, sg));
       acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
       acc.w = __fmul_rn(acc.w, tr);
-      // ---- ERT after the round (render.py:532-537)
+      // ---- ERT after the round (render.py:338-343)
       if (P.ert) {
         bool dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
         if (dead) {
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
 
   if (final_pass) {
     if (in_range) {
-      // render.py:539-542: acc + trans*bg, clip to [0,1]
+      // render.py:345-348: acc + trans*bg, clip to [0,1]
       float c0 = __fadd_rn(acc.x, __fmul_rn(acc.w, P.bg[0]));
       float c1 = __fadd_rn(acc.y, __fmul_rn(acc.w, P.bg[1]));
       float c2 = __fadd_rn(acc.z, __fmul_rn(acc.w, P.bg[2]));
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
   }
   if (!__any_sync(0xffffffffu, active)) return;
 
-  // ---- sample round r (render.py:505-524)
+  // ---- sample round r (render.py:311-330)
   int s0 = round * P.chunk;
   int m = min(P.chunk, P.k - s0);
   float4 o = active ? R.org[i] : make_float4(0.f, 0.f, 0.f, 0.f);

@@ -10,7 +10,7 @@ namespace gf {
 #define GF_MAX_LAYERS 16
 
 // Layer table for one architecture; manifest order trunk0..trunk{T-1},
-// density, feature, direction, color (mlp.py:373-384).
+// density, feature, direction, color (mlp.py:73-84).
 struct LayerTable {
   int n_layers, trunk, width, view, pos_dim, dir_dim;
   int in[GF_MAX_LAYERS], out[GF_MAX_LAYERS];
@@ -59,7 +59,7 @@ __host__ inline Fp32Layout make_fp32_layout(const LayerTable& t) {
 
 // Sources / sinks of MLP rows ------------------------------------------------
 // Render: rows are kept samples in the ray-major staging buffer; the view
-// direction is the ray's (render.py:520).
+// direction is the ray's (render.py:326).
 struct RenderIO {
   const float4* rec;
   float4* res;

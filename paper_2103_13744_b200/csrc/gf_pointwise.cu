@@ -96,7 +96,7 @@ __global__ void k_alpha(const T* __restrict__ s, const T* __restrict__ d, int64_
   out[i] = -expm1_((-s[i]) * d[i]);
 }
 
-// render.py:463-478 composite (one thread per ray): sum_j (T_j * a_j) * c_j
+// render.py:269-284 composite (one thread per ray): sum_j (T_j * a_j) * c_j
 // accumulated in sample order, T by running product; float32 or float64 like
 // the numpy original (which computes in the input dtype).
 __device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
@@ -127,7 +127,7 @@ __global__ void k_composite(const T* __restrict__ col, const T* __restrict__ alp
   trans[r] = t;
 }
 
-// render.py:333-342 generate_rays
+// render.py:139-148 generate_rays
 __global__ void k_gen_rays(gf_camera_t c, float* o, float* dir) {
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (int64_t)c.width * c.height) return;

@@ -21,12 +21,12 @@ from . import _device as D
 from . import _native as N
 from .core import Aabb
 
-RAY_BLOCK = 4096  # render.py:216
+RAY_BLOCK = 4096  # render.py:22
 
 
 @dataclass(frozen=True)
 class Camera:
-    """render.py:219-270 (pinhole; +x right, +y down, +z forward)."""
+    """render.py:25-76 (pinhole; +x right, +y down, +z forward)."""
 
     width: int
     height: int
@@ -63,7 +63,7 @@ class Camera:
 
 
 def look_at_pose(eye, target, up=(0.0, 0.0, 1.0)) -> np.ndarray:
-    """render.py:273-294."""
+    """render.py:79-100."""
     eye = np.asarray(eye, dtype=np.float64)
     fwd = np.asarray(target, dtype=np.float64) - eye
     norm = np.linalg.norm(fwd)
@@ -82,7 +82,7 @@ def look_at_pose(eye, target, up=(0.0, 0.0, 1.0)) -> np.ndarray:
 
 @dataclass(frozen=True)
 class Ray:
-    """render.py:297-317."""
+    """render.py:103-123."""
 
     origin: np.ndarray
     direction: np.ndarray
@@ -103,14 +103,14 @@ class Ray:
 
 
 def generate_ray(cam: Camera, px) -> Ray:
-    """render.py:320-330 (single ray through continuous pixel coords)."""
+    """render.py:126-136 (single ray through continuous pixel coords)."""
     u, v = float(px[0]), float(px[1])
     d = cam.rotation @ np.array([(u - cam.cx) / cam.fx, (v - cam.cy) / cam.fy, 1.0])
     return Ray(cam.center, d / np.linalg.norm(d))
 
 
 def generate_rays(cam: Camera):
-    """render.py:333-342 on the device: float32 origins and unit directions,
+    """render.py:139-148 on the device: float32 origins and unit directions,
     row-major, bit-identical to the numpy reference."""
     t = D.require_cuda()
     n = cam.width * cam.height
@@ -121,7 +121,7 @@ def generate_rays(cam: Camera):
 
 
 def intersect_aabb(origins, directions, aabb: Aabb):
-    """render.py:345-365 slab test (float64).  Host helper for single rays and
+    """render.py:151-171 slab test (float64).  Host helper for single rays and
     tests; the marcher runs its own copy of this arithmetic on the device."""
     o = np.asarray(origins, dtype=np.float64)
     d = np.asarray(directions, dtype=np.float64)
@@ -138,7 +138,7 @@ def intersect_aabb(origins, directions, aabb: Aabb):
 
 @dataclass
 class RenderConfig:
-    """render.py:368-401."""
+    """render.py:174-207."""
 
     k: int = 384
     epsilon: float = 0.01
@@ -177,7 +177,7 @@ class RenderConfig:
 
 @dataclass
 class RenderStats:
-    """render.py:404-425."""
+    """render.py:210-231."""
 
     wall_ms: float = 0.0
     total_queries: int = 0
@@ -197,7 +197,7 @@ class RenderStats:
 
 
 def sample_ray(ray: Ray, aabb: Aabb, occ=None, cfg: RenderConfig | None = None, rng=None):
-    """render.py:428-460: single-ray sampler used by tests and tools (float64
+    """render.py:234-266: single-ray sampler used by tests and tools (float64
     jitter from the caller's Generator; not the marcher's path)."""
     from .core import clip_into
 
@@ -216,7 +216,7 @@ def sample_ray(ray: Ray, aabb: Aabb, occ=None, cfg: RenderConfig | None = None, 
 
 
 def composite(colors, alphas):
-    """render.py:463-478 on the device (float32 or float64, batch dims)."""
+    """render.py:269-284 on the device (float32 or float64, batch dims)."""
     colors = np.asarray(colors)
     alphas = np.asarray(alphas)
     dtype = np.result_type(colors.dtype, alphas.dtype)
@@ -353,13 +353,13 @@ def _stats_from(st) -> RenderStats:
 
 def render_rays(field, occupancy, origins, directions, cfg: RenderConfig, seed: int = 0, workers: int = 1,
                 precision=None):
-    """render.py:545-578.  ``workers`` is accepted for API compatibility; the
+    """render.py:351-384.  ``workers`` is accepted for API compatibility; the
     device result is identical for any value (ray blocks keep their own
     jitter streams)."""
     grid = _field_grid(field)
     o = np.asarray(origins, dtype=np.float64).reshape(-1, 3)
     d = np.asarray(directions, dtype=np.float64).reshape(-1, 3)
-    # render.py:562-563 upcasts to float64 and the slab test runs on those
+    # render.py:368-369 upcasts to float64 and the slab test runs on those
     # values; the device takes float32 rays, so float64 rays must round-trip
     if not (np.array_equal(o.astype(np.float32).astype(np.float64), o)
             and np.array_equal(d.astype(np.float32).astype(np.float64), d)):
@@ -371,7 +371,7 @@ def render_rays(field, occupancy, origins, directions, cfg: RenderConfig, seed: 
 
 def render_image(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0, workers: int = 1,
                  precision=None):
-    """render.py:581-594: full frame; stats.wall_ms covers ray generation
+    """render.py:387-400: full frame; stats.wall_ms covers ray generation
     through the image landing in host memory."""
     t_start = time.perf_counter()
     grid = _field_grid(field)
@@ -425,7 +425,7 @@ def render_image_distributed(field, occupancy, cam: Camera, cfg: RenderConfig, s
 
 
 def compute_psnr(a, b) -> float:
-    """render.py:597-607."""
+    """render.py:403-413."""
     a, b = np.asarray(a), np.asarray(b)
     if a.shape != b.shape:
         raise ValueError(f"image shapes differ: {a.shape} vs {b.shape}")
