@@ -351,6 +351,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->R.run = c.take<uint32_t>((size_t)n_rays);
   w->R.flags = c.take<uint8_t>((size_t)n_rays);
   w->R.ivl = c.take<uint32_t>((size_t)n_rays * GF_MAX_IVL);
+  w->R.denc = c.take<uint4>((size_t)n_rays * 4);
   w->RB.rec = c.take<float4>(cap);
   w->RB.res = c.take<float4>(cap);
   w->B.counts = c.take<uint32_t>((size_t)2 * n_cells);  // two histograms, by round parity
@@ -532,7 +533,11 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   const unsigned march_blocks = (unsigned)gf_div_up<int64_t>(P.march_threads, 128);
   const unsigned ray_blocks = (unsigned)gf_div_up<int64_t>(n_rays, 128);
   TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
-  RenderIO io{w.RB.rec, w.RB.res, w.R.dir, (uint32_t)stride};
+  int stride_shift = -1;
+  for (int b = 0; b < 31; ++b)
+    if ((1 << b) == stride) stride_shift = b;
+  if (precision != GF_PRECISION_FP16) w.R.denc = nullptr;  // only the tensor-core MLP reads gamma(d) per ray
+  RenderIO io{w.RB.rec, w.RB.res, w.R.dir, (uint32_t)stride, w.R.denc, stride_shift};
   const bool mlp_ok = precision == GF_PRECISION_FP16   ? prepare_mlp_tc(t)
                       : precision == GF_PRECISION_FP32 ? prepare_mlp_fp32(t)
                                                        : false;

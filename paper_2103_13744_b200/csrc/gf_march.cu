@@ -10,6 +10,7 @@
 // One thread owns one ray for the whole frame.  Rounds (ert_chunk samples)
 // are separate launches because the next round's live set depends on the
 // MLP results of this round (chunk-granular ERT, render.py:338-343).
+#include "gf_encode.cuh"
 #include "gf_march.cuh"
 
 namespace gf {
@@ -170,6 +171,12 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
   R.acc[i] = make_float4(0.f, 0.f, 0.f, 1.f);
   R.run[i] = 0;
   R.flags[i] = hit ? (uint8_t)(GF_RAY_ALIVE | GF_RAY_HIT) : (uint8_t)0;
+  if (R.denc && hit) {  // gamma(d) once per ray for every sample's direction layer (render.py:326)
+    uint4 de[4];
+    encode_direction_h(d32, de);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) R.denc[4 * i + q] = de[q];
+  }
   if (P.coarse_bits && hit) {
     const float ex = __double2float_rn(__dadd_rn((double)o32[0], __dmul_rn(t0, (double)d32[0])));
     const float ey = __double2float_rn(__dadd_rn((double)o32[1], __dmul_rn(t0, (double)d32[1])));

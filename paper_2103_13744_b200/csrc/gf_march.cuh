@@ -44,6 +44,7 @@ struct RayState {
   uint32_t* run;  // queried samples of the ray in the last marched round
   uint8_t* flags;
   uint32_t* ivl;  // GF_MAX_IVL candidate slot ranges per ray (lo | hi << 16), from the coarse DDA
+  uint4* denc;    // NULL, or 4 x uint4 per ray: gamma(d) as fp16 for the tensor-core MLP
 };
 
 #define GF_MAX_IVL 8

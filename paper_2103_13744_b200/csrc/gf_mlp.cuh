@@ -61,15 +61,30 @@ __host__ inline Fp32Layout make_fp32_layout(const LayerTable& t) {
 // Render: rows are kept samples in the ray-major staging buffer; the view
 // direction is the ray's (render.py:326).
 struct RenderIO {
+  static constexpr bool kDirEnc = true;  // tensor-core path reads the ray's pre-encoded gamma(d)
   const float4* rec;
   float4* res;
   const float4* ray_dir;
   uint32_t stride;
+  const uint4* denc;  // 4 x uint4 per ray (gf_encode.cuh encode_direction_h), from k_ray_init
+  int stride_shift;   // log2(stride) when stride is a power of two, else -1
+  __device__ __forceinline__ uint32_t ray_of(uint32_t idx) const {
+    return stride_shift >= 0 ? idx >> stride_shift : idx / stride;
+  }
   __device__ __forceinline__ void load(uint32_t idx, float* x, float* d) const {
     float4 r = rec[idx];
-    float4 dd = ray_dir[idx / stride];
+    float4 dd = ray_dir[ray_of(idx)];
     x[0] = r.x; x[1] = r.y; x[2] = r.z;
     d[0] = dd.x; d[1] = dd.y; d[2] = dd.z;
+  }
+  __device__ __forceinline__ void load_pos(uint32_t idx, float* x, float*) const {
+    float4 r = rec[idx];
+    x[0] = r.x; x[1] = r.y; x[2] = r.z;
+  }
+  __device__ __forceinline__ void load_denc(uint32_t idx, uint4* de) const {
+    const uint4* q = denc + 4ull * ray_of(idx);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) de[c] = q[c];
   }
   __device__ __forceinline__ void store(uint32_t idx, float r, float g, float b, float s) const {
     res[idx] = make_float4(r, g, b, s);
@@ -78,6 +93,7 @@ struct RenderIO {
 
 // Bulk query: caller's float32 (N,3) arrays, results in caller order.
 struct QueryIO {
+  static constexpr bool kDirEnc = false;
   const float* pos;
   const float* dir;
   float* rgb;
@@ -96,6 +112,8 @@ struct QueryIO {
     rgb[3ull * idx + 2] = b;
     sigma[idx] = s;
   }
+  __device__ __forceinline__ void load_pos(uint32_t idx, float* x, float* d) const { load(idx, x, d); }
+  __device__ __forceinline__ void load_denc(uint32_t, uint4*) const {}
 };
 
 struct TileSched {

@@ -3,12 +3,18 @@
 // Reference math: core.py:132-152 (encoding), mlp.py:222-266 (forward),
 // batched.py:120-151 (one network per segment).  Design:
 //
-//  * one CTA = 128 threads working on TWO 128-row tiles of the same cell at
-//    once (ping-pong): thread t owns row t of both tiles, which is TMEM lane
-//    t, so every epilogue is a private tcgen05.ld of the thread's own
-//    accumulator row; while the tensor core runs one tile's layer, the warps
-//    run the other tile's epilogue, hiding the MMA / commit / barrier latency
-//    of the 5-layer dependency chain;
+//  * one CTA = 256 threads = two warpgroups working on TWO 128-row tiles of
+//    the same cell at once: group g owns tile slot g (its A operands, its
+//    TMEM columns, its MMA commit barrier and its own elected issuing
+//    thread); thread gt of a group owns row gt, which is TMEM lane gt, so
+//    every epilogue is a private tcgen05.ld of the thread's own accumulator
+//    row.  While the tensor core runs one group's layer the other group runs
+//    its epilogue, hiding the MMA / commit / barrier latency of the 5-layer
+//    dependency chain; groups synchronise with named barriers, the CTA only
+//    at tile-pair boundaries (weight reuse);
+//  * epilogues: FADD2 bias adds, F2FP.RELU packs, 16-byte operand stores;
+//    the render path's direction chunk gamma(d) is encoded once per ray by
+//    k_ray_init and copied, not recomputed per sample;
 //  * the cell's weights are pre-packed on the device (gf_pack_weights) into
 //    the exact shared-memory image the MMAs consume (fp16, K-major,
 //    no-swizzle canonical layout, fp32 biases) and brought in with ONE 1-D
@@ -26,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "gf_encode.cuh"
 #include "gf_mlp.cuh"
 
 namespace gf {
@@ -144,61 +151,35 @@ __device__ __forceinline__ void tmem_load(uint32_t taddr, float* out) {
   for (int c = 0; c < N; ++c) out[c] = __uint_as_float(r[c]);
 }
 
-__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
-  uint32_t r;  // one F2FP.F16.F32.PACK_AB; low half = a
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
-  return r;
-}
-
-// write 8 consecutive features [k0, k0+8) of row r into a canonical operand
-__device__ __forceinline__ void st_chunk(uint8_t* A, int K, int r, int k0, const float* v) {
-  uint4 q = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
-  *reinterpret_cast<uint4*>(A + canon_off(r, k0, K)) = q;
-}
-
-// bias add (+ReLU) with 16-byte broadcast loads of the biases
+// bias add (+ReLU) and fp16 store of accumulator columns [0, N) of row r into
+// a canonical operand at K-offset k0: per 8 columns two 16-byte broadcast
+// bias loads, four FADD2, four F2FP(.RELU) packs and one 16-byte store.
 template <int N, bool RELU>
-__device__ __forceinline__ void add_bias(float* h, const float* __restrict__ b) {
+__device__ __forceinline__ void bias_pack_store(float* h, const float* __restrict__ b, uint8_t* A, int K, int r,
+                                                int k0) {
   const float4* b4 = reinterpret_cast<const float4*>(b);
 #pragma unroll
-  for (int c = 0; c < N / 4; ++c) {
-    const float4 q = b4[c];
-    h[4 * c + 0] += q.x; h[4 * c + 1] += q.y; h[4 * c + 2] += q.z; h[4 * c + 3] += q.w;
+  for (int c = 0; c < N / 8; ++c) {
+    const float4 p = b4[2 * c], q = b4[2 * c + 1];
+    float* v = h + 8 * c;
+    fadd2(v[0], v[1], p.x, p.y);
+    fadd2(v[2], v[3], p.z, p.w);
+    fadd2(v[4], v[5], q.x, q.y);
+    fadd2(v[6], v[7], q.z, q.w);
+    uint4 o;
     if (RELU) {
-      h[4 * c + 0] = fmaxf(h[4 * c + 0], 0.f); h[4 * c + 1] = fmaxf(h[4 * c + 1], 0.f);
-      h[4 * c + 2] = fmaxf(h[4 * c + 2], 0.f); h[4 * c + 3] = fmaxf(h[4 * c + 3], 0.f);
-    }
-  }
-}
-
-// sin / cos of x * 2^k * pi: the angle is formed exactly as numpy forms it
-// (fl32(x * fl32(2^k pi)) == 2^k fl32(x*pi)), reduced by 2pi with a two-term
-// Cody-Waite split, then MUFU sin/cos (~5e-7 abs).
-__device__ __forceinline__ void sincos_scaled(float x, int k, float* s, float* c) {
-  const float a = __fmul_rn(x, __int_as_float(0x40490FDB + (k << 23)));
-  const float n = rintf(a * 0.15915494309189535f);
-  float r = fmaf(-n, 6.28125f, a);          // 2pi_hi (exact times n <= 2^9)
-  r = fmaf(-n, 1.9353071795864769e-3f, r);  // 2pi_lo
-  __sincosf(r, s, c);
-}
-
-// octaves k < L: MUFU anchors every third octave, double-angle steps in
-// between (max abs error 2.6e-6 vs 4.9e-4 fp16 operand rounding)
-template <int L>
-__device__ __forceinline__ void encode_octaves(float x, float* s, float* c) {
-#pragma unroll
-  for (int k = 0; k < L; ++k) {
-    if (k % 3 == 0) {
-      sincos_scaled(x, k, &s[k], &c[k]);
+      o = make_uint4(pack_h2_relu(v[0], v[1]), pack_h2_relu(v[2], v[3]), pack_h2_relu(v[4], v[5]),
+                     pack_h2_relu(v[6], v[7]));
     } else {
-      const float sp = s[k - 1], cp = c[k - 1];
-      s[k] = 2.0f * sp * cp;
-      c[k] = (cp - sp) * (cp + sp);
+      o = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
     }
+    *reinterpret_cast<uint4*>(A + canon_off(r, k0 + 8 * c, K)) = o;
   }
 }
 
-// one row's inputs
+// one row's inputs (prefetched one pair ahead); the render path's direction
+// operand chunk (the ray's pre-encoded gamma(d), gf_encode.cuh) is fetched
+// separately while the trunk0 MMA runs
 struct RowIn {
   uint32_t idx;
   bool valid;
@@ -211,10 +192,10 @@ __device__ __forceinline__ void load_row(const TileSched& S, const IO& io, uint2
   r.valid = tl.y + (uint32_t)tid < seg_n;
   r.idx = 0;
   r.x[0] = r.x[1] = r.x[2] = 0.f;
-  r.d[0] = r.d[1] = r.d[2] = 0.f;
+  if (!IO::kDirEnc) r.d[0] = r.d[1] = r.d[2] = 0.f;
   if (r.valid) {
     r.idx = S.sorted[seg0 + tl.y + tid];
-    io.load(r.idx, r.x, r.d);
+    io.load_pos(r.idx, r.x, r.d);
   }
 }
 
@@ -224,58 +205,76 @@ __device__ __forceinline__ bool pair_second(const TileSched& S, uint32_t t, uint
   return t + 1 < t_end && S.tiles[t + 1].x == cell;
 }
 
+// gamma(x) (core.py:132-152 layout: raw xyz, then per octave k sin xyz, cos
+// xyz; column 63 zero) generated octave by octave and flushed to the K0
+// operand one 8-column chunk at a time, so only ~14 values are live
 template <int W>
 __device__ __forceinline__ void encode_position(uint8_t* A0, int tid, const float* x) {
   using T = TcShape<W>;
   float e[64];
   e[0] = x[0]; e[1] = x[1]; e[2] = x[2];
+  float sp[3], cp[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    float s[10], c[10];
-    encode_octaves<10>(x[a], s, c);
+  for (int k = 0; k < 10; ++k) {
 #pragma unroll
-    for (int k = 0; k < 10; ++k) {
-      e[3 + 6 * k + a] = s[k];
-      e[6 + 6 * k + a] = c[k];
+    for (int a = 0; a < 3; ++a) {
+      float sk, ck;
+      if (k % 3 == 0) {
+        sincos_scaled(x[a], k, &sk, &ck);
+      } else {
+        sk = 2.0f * sp[a] * cp[a];
+        ck = (cp[a] - sp[a]) * (cp[a] + sp[a]);
+      }
+      sp[a] = sk;
+      cp[a] = ck;
+      e[3 + 6 * k + a] = sk;
+      e[6 + 6 * k + a] = ck;
+    }
+    if (k == 9) e[63] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int last = 8 * c + 7, hi = k == 9 ? 63 : 8 + 6 * k, lo = 8 + 6 * (k - 1);
+      if (last <= hi && last > lo) {
+        const float* v = e + 8 * c;
+        *reinterpret_cast<uint4*>(A0 + canon_off(tid, 8 * c, T::K0)) =
+            make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
+      }
     }
   }
-  e[63] = 0.f;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) st_chunk(A0, T::K0, tid, 8 * c, e + 8 * c);
+}
+
+template <int W, class IO>
+__device__ __forceinline__ void fetch_direction(const IO& io, const RowIn& row, uint4* de) {
+  if (IO::kDirEnc) {
+    if (row.valid) io.load_denc(row.idx, de);
+    else de[0] = de[1] = de[2] = de[3] = make_uint4(0u, 0u, 0u, 0u);
+  } else {
+    encode_direction_h(row.d, de);
+  }
 }
 
 template <int W>
-__device__ __forceinline__ void encode_direction(uint8_t* A3, int tid, const float* d) {
+__device__ __forceinline__ void store_direction(uint8_t* A3, int tid, const uint4* de) {
   using T = TcShape<W>;
-  float e[T::K3 - W];
-  e[0] = d[0]; e[1] = d[1]; e[2] = d[2];
+  static_assert(T::K3 - W == 32, "direction operand chunk is 32 fp16 wide");
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    float s[4], c[4];
-    encode_octaves<4>(d[a], s, c);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      e[3 + 6 * k + a] = s[k];
-      e[6 + 6 * k + a] = c[k];
-    }
-  }
-#pragma unroll
-  for (int j = 27; j < T::K3 - W; ++j) e[j] = 0.f;
-#pragma unroll
-  for (int c = 0; c < (T::K3 - W) / 8; ++c) st_chunk(A3, T::K3, tid, W + 8 * c, e + 8 * c);
+  for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(A3 + canon_off(tid, W + 8 * q, T::K3)) = de[q];
 }
 
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
 template <int W, class IO>
-__global__ void __launch_bounds__(128) k_mlp_tc(const uint8_t* __restrict__ packed, TileSched S, IO io) {
+__global__ void __launch_bounds__(256, W == 32 ? 3 : 1) k_mlp_tc(const uint8_t* __restrict__ packed, TileSched S, IO io) {
   using T = TcShape<W>;
   extern __shared__ __align__(1024) uint8_t smem[];
   const float* sbias = reinterpret_cast<const float*>(smem + T::BIAS);
   const uint32_t bar0 = smem_u32(smem + T::BAR), bar_w = bar0 + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + T::BAR + 24);
   const int tid = threadIdx.x, warp = tid >> 5;
+  // two warpgroups: group g owns tile slot g (its A operands, its TMEM
+  // columns, its commit barrier); row gt of the tile is TMEM lane gt
+  const int g = tid >> 7, gt = tid & 127;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -292,19 +291,21 @@ __global__ void __launch_bounds__(128) k_mlp_tc(const uint8_t* __restrict__ pack
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;  // this warp's TMEM lane quarter
   const uint32_t wb = smem_u32(smem);
+  uint8_t* A0 = smem + T::A0(g);
+  uint8_t* A1 = smem + T::A1(g);
+  const uint32_t trow = tmem + g * T::NC + ((uint32_t)((warp & 3) * 32) << 16);  // lane quarter of this warp
 
   const uint32_t nt = *S.n_tiles;
   const uint32_t per = (nt + gridDim.x - 1) / gridDim.x;
   const uint32_t t_begin = blockIdx.x * per, t_end = min(nt, t_begin + per);
   int cur = -1;
-  uint32_t ph[2] = {0, 0}, ph_w = 0;
+  uint32_t ph = 0, ph_w = 0;
 
-  // MMA issue for layer L of slot s (one elected thread)
-  auto issue = [&](int L, int s) {
-    if (tid != 0) return;
-    const uint32_t a0 = wb + T::A0(s), a1 = wb + T::A1(s), d = tmem + s * T::NC;
+  // MMA issue for layer L of this group's slot (thread gt == 0 of the group)
+  auto issue = [&](int L) {
+    if (gt != 0) return;
+    const uint32_t a0 = wb + T::A0(g), a1 = wb + T::A1(g), d = tmem + g * T::NC;
     uint32_t a = a1, b = wb + T::B1, idesc = idesc_f16(128, T::N1);
     int K = T::K1;
     if (L == 0) { a = a0; b = wb + T::B0; K = T::K0; idesc = idesc_f16(128, T::N0); }
@@ -313,89 +314,89 @@ __global__ void __launch_bounds__(128) k_mlp_tc(const uint8_t* __restrict__ pack
     if (L == 4) { b = wb + T::B4; K = T::K4; idesc = idesc_f16(128, T::N4); }
     for (int ks = 0; ks < K / 16; ++ks)
       mma_f16(d, umma_desc(a + ks * 256, K), umma_desc(b + ks * 256, K), idesc, ks > 0 ? 1u : 0u);
-    mma_commit(bar0 + 8 * s);
+    mma_commit(bar0 + 8 * g);
   };
-  auto wait_mma = [&](int s) {
-    mbar_wait(bar0 + 8 * s, ph[s]);
-    ph[s] ^= 1;
+  auto wait_mma = [&]() {
+    mbar_wait(bar0 + 8 * g, ph);
+    ph ^= 1;
     fence_after();
   };
-  auto publish = [&]() {  // smem operand writes -> visible to the tensor core, TMEM reads retired
+  // this group's smem operand writes -> visible to the tensor core; its TMEM
+  // reads retired (named barrier over the group's 128 threads)
+  auto publish = [&]() {
     fence_async_smem();
     fence_before();
-    __syncthreads();
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
     fence_after();
   };
+  // tile of this group inside the pair starting at t (slot 1 only for a
+  // second tile of the same cell: both slots share the staged weights)
+  auto my_tile = [&](uint32_t t, uint2& tl) -> bool {
+    if (t >= t_end) return false;
+    tl = S.tiles[t];
+    if (g == 0) return true;
+    if (!pair_second(S, t, t_end, tl.x)) return false;
+    tl = S.tiles[t + 1];
+    return true;
+  };
 
-  RowIn nxt[2];
-  if (t_begin < t_end) {
-    const uint2 tl = S.tiles[t_begin];
-    load_row(S, io, tl, tid, nxt[0]);
-    if (pair_second(S, t_begin, t_end, tl.x)) load_row(S, io, S.tiles[t_begin + 1], tid, nxt[1]);
+  RowIn nxt;
+  {
+    uint2 tl;
+    if (my_tile(t_begin, tl)) load_row(S, io, tl, gt, nxt);
   }
 
   for (uint32_t t = t_begin; t < t_end;) {
     const uint2 tl = S.tiles[t];
     const bool two = pair_second(S, t, t_end, tl.x);
     const uint32_t t_next = t + (two ? 2 : 1);
-    __syncthreads();  // previous pair fully retired (bias reads, output stores)
+    const bool active = g == 0 || two;
+    __syncthreads();  // previous pair fully retired (bias reads, weight operands)
     const bool new_cell = (int)tl.x != cur;
     if (new_cell && tid == 0) bulk_load(wb, packed + (size_t)tl.x * T::CELL_BYTES, T::CELL_BYTES, bar_w);
     cur = (int)tl.x;
-    RowIn row[2] = {nxt[0], nxt[1]};
-
-    encode_position<W>(smem + T::A0(0), tid, row[0].x);
-    if (two) encode_position<W>(smem + T::A0(1), tid, row[1].x);
-    publish();
+    const RowIn row = nxt;
+    if (active) {
+      encode_position<W>(A0, gt, row.x);
+      publish();
+    }
     if (new_cell) {
       mbar_wait(bar_w, ph_w);
       ph_w ^= 1;
     }
-    issue(0, 0);
-    if (two) issue(0, 1);
-    // prefetch the next pair while trunk0 runs
-    if (t_next < t_end) {
-      const uint2 tn = S.tiles[t_next];
-      load_row(S, io, tn, tid, nxt[0]);
-      if (pair_second(S, t_next, t_end, tn.x)) load_row(S, io, S.tiles[t_next + 1], tid, nxt[1]);
+    if (active) issue(0);
+    uint4 de[4];  // direction operand chunk of this row, fetched while trunk0 runs
+    if (active && IO::kDirEnc) fetch_direction<W>(io, row, de);
+    {  // prefetch this group's row of the next pair while trunk0 runs
+      uint2 tn;
+      if (my_tile(t_next, tn)) load_row(S, io, tn, gt, nxt);
     }
-
-    float sigma[2] = {0.f, 0.f};
+    if (active) {
+      float sigma = 0.f;
 #pragma unroll
-    for (int L = 0; L < 5; ++L) {
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        if (s == 1 && !two) continue;
-        uint8_t* A0 = smem + T::A0(s);
-        uint8_t* A1 = smem + T::A1(s);
-        const uint32_t trow = tmem + s * T::NC + lane_base;
-        wait_mma(s);
+      for (int L = 0; L < 5; ++L) {
+        wait_mma();
         if (L == 0) {  // trunk0 -> A1; gamma(x) is dead, gamma(d) -> A0 as [., gamma(d)]
           float h[W];
           tmem_load<W>(trow, h);
-          add_bias<W, true>(h, sbias + T::BB0);
-#pragma unroll
-          for (int c = 0; c < W / 8; ++c) st_chunk(A1, W, tid, 8 * c, h + 8 * c);
-          encode_direction<W>(A0, tid, row[s].d);
+          bias_pack_store<W, true>(h, sbias + T::BB0, A1, W, gt, 0);
+          if (!IO::kDirEnc) fetch_direction<W>(io, row, de);
+          store_direction<W>(A0, gt, de);
         } else if (L == 1) {  // trunk1 -> A1
           float h[W];
           tmem_load<W>(trow, h);
-          add_bias<W, true>(h, sbias + T::BB1);
-#pragma unroll
-          for (int c = 0; c < W / 8; ++c) st_chunk(A1, W, tid, 8 * c, h + 8 * c);
+          bias_pack_store<W, true>(h, sbias + T::BB1, A1, W, gt, 0);
         } else if (L == 2) {  // feature (cols 0..W-1, unactivated) + density (col W)
-          float h[T::N2];
-          tmem_load<T::N2>(trow, h);
-          add_bias<T::N2, false>(h, sbias + T::BB2);
-          sigma[s] = fmaxf(h[W], 0.f);
-#pragma unroll
-          for (int c = 0; c < W / 8; ++c) st_chunk(A0, T::K3, tid, 8 * c, h + 8 * c);
+          float h[W];
+          tmem_load<W>(trow, h);
+          bias_pack_store<W, false>(h, sbias + T::BB2, A0, T::K3, gt, 0);
+          float z[16];
+          tmem_load<16>(trow + W, z);
+          sigma = fmaxf(z[0] + sbias[T::BB2 + W], 0.f);
         } else if (L == 3) {  // direction -> A1
           float h[W];
           tmem_load<W>(trow, h);
-          add_bias<W, true>(h, sbias + T::BB3);
-#pragma unroll
-          for (int c = 0; c < W / 8; ++c) st_chunk(A1, W, tid, 8 * c, h + 8 * c);
+          bias_pack_store<W, true>(h, sbias + T::BB3, A1, W, gt, 0);
         } else {  // color: sigmoid
           float z[16];
           tmem_load<16>(trow, z);
@@ -403,13 +404,14 @@ __global__ void __launch_bounds__(128) k_mlp_tc(const uint8_t* __restrict__ pack
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const float v = z[c] + sbias[T::BB4 + c];
-            rgb[c] = v >= 0.f ? __fdividef(1.f, 1.f + __expf(-v)) : __fdividef(__expf(v), 1.f + __expf(v));
+            const float e = __expf(-fabsf(v)), r = __fdividef(1.f, 1.f + e);  // sign-split sigmoid (mlp.py:228-235)
+            rgb[c] = v >= 0.f ? r : e * r;
           }
-          if (row[s].valid) io.store(row[s].idx, rgb[0], rgb[1], rgb[2], sigma[s]);
+          if (row.valid) io.store(row.idx, rgb[0], rgb[1], rgb[2], sigma);
         }
         if (L < 4) {
           publish();
-          issue(L + 1, s);
+          issue(L + 1);
         }
       }
     }
@@ -518,7 +520,7 @@ static int tc_resident() {
     int regs = 128;
     if (cudaFuncGetAttributes(&fa, k) == cudaSuccess && fa.numRegs > 0) regs = fa.numRegs;
     const int by_smem = smem_sm / (T::SMEM + 1024);
-    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * 128);
+    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * 256);
     const int by_tmem = 512 / T::TMEM_COLS;
     per_sm = by_smem < by_regs ? by_smem : by_regs;
     per_sm = per_sm < by_tmem ? per_sm : by_tmem;
@@ -534,7 +536,7 @@ static int tc_resident() {
 template <int W, class IO>
 static void launch_tc_w(const void* packed, const TileSched& S, const IO& io, cudaStream_t st) {
   using T = TcShape<W>;
-  k_mlp_tc<W, IO><<<num_sms() * tc_resident<W, IO>(), 128, T::SMEM, st>>>((const uint8_t*)packed, S, io);
+  k_mlp_tc<W, IO><<<num_sms() * tc_resident<W, IO>(), 256, T::SMEM, st>>>((const uint8_t*)packed, S, io);
 }
 
 bool prepare_mlp_tc(const LayerTable& t) {
