@@ -335,7 +335,7 @@ def main():
             torch.cuda.synchronize()
         if i:  # first call re-validates caches; not counted
             e2e_times.append(time.perf_counter() - t0)
-    e2e_s = statistics.mean(e2e_times)
+    e2e_s = statistics.median(e2e_times)  # host jitter (pinned-block reuse, GIL) skews the mean
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -190,7 +190,7 @@ static bool valid_grid(const gf_grid_geom_t* g) {
   if (!g) return false;
   for (int a = 0; a < 3; ++a)
     if (!(g->b_min[a] < g->b_max[a]) || g->res[a] < 1) return false;
-  return true;
+  return (int64_t)g->res[0] * g->res[1] * g->res[2] <= GF_MAX_CELLS;  // tile cell field width
 }
 
 static int64_t n_cells_of(const gf_grid_geom_t* g) { return (int64_t)g->res[0] * g->res[1] * g->res[2]; }
@@ -289,7 +289,7 @@ int gf_query_points(const gf_arch_t* arch, const gf_grid_geom_t* grid, const voi
   stage_mark(st, GF_STAGE_SCAN, 1);
   launch_scatter_query(w.keys, n, w.B, st);
   stage_mark(st, GF_STAGE_SCATTER, n > 0 ? 1 : 0);
-  TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
+  TileSched S{w.B.tiles, w.B.n_tiles, w.B.sorted, nullptr};
   QueryIO io{pos, dir, rgb, sigma, nullptr};
   if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_query_points: no MLP kernel for this architecture/precision");
@@ -308,7 +308,7 @@ int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packe
   if (query_carve(c, n, n_cells, &w) > ws_bytes) return fail(GF_ERR_WORKSPACE, "gf_grouped_forward: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   launch_segments_from_offsets(offsets, n_cells, n, w.B, st);
-  TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
+  TileSched S{w.B.tiles, w.B.n_tiles, w.B.sorted, nullptr};
   QueryIO io{pos, dir, rgb, sigma, order};
   if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_grouped_forward: no MLP kernel for this architecture/precision");
@@ -327,6 +327,7 @@ size_t gf_grouped_workspace_bytes(int64_t n_cells, int64_t n) {
 struct RenderWs {
   u128* seeds;
   u128* jump;
+  u128* start;
   RayState R;
   RoundBufs RB;
   BucketBufs B;
@@ -342,6 +343,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   const size_t cap = (size_t)n_rays * (size_t)stride;
   w->seeds = c.take<u128>((size_t)2 * n_blocks);
   w->jump = c.take<u128>((size_t)2 * (GF_JUMP_MAX + 1));
+  w->start = c.take<u128>((size_t)2 * GF_RAY_BLOCK);
   w->coarse_tmp = c.take<uint8_t>((size_t)kMaxCoarseCells);
   w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->R.org = c.take<float4>((size_t)n_rays);
@@ -360,7 +362,8 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->B.cursor = c.take<uint32_t>((size_t)n_cells);
   w->B.tiles = c.take<uint2>(cap / GF_TILE_ROWS + (size_t)n_cells + 1);
   w->B.n_tiles = c.take<uint32_t>(1);
-  w->B.sorted = c.take<uint32_t>(cap + 1);
+  w->B.sorted = nullptr;
+  w->B.srec = c.take<float4>(cap + 1);
   w->B.tile_off = c.take<uint32_t>((size_t)n_cells + 1);
   w->RB.emit_list = c.take<uint32_t>((size_t)n_rays);
   w->RB.emit_count = c.take<uint32_t>(2);
@@ -432,6 +435,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   P.first_block = first_block;
   P.block_seeds = w.seeds;
   P.jump = w.jump;
+  P.start = w.start;
   P.k = cfg->k;
   P.chunk = cfg->ert_chunk;
   P.n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
@@ -532,12 +536,12 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   }
   const unsigned march_blocks = (unsigned)gf_div_up<int64_t>(P.march_threads, 128);
   const unsigned ray_blocks = (unsigned)gf_div_up<int64_t>(n_rays, 128);
-  TileSched S{w.B.tiles, w.B.n_tiles, w.B.offsets, w.B.sorted};
+  TileSched S{w.B.tiles, w.B.n_tiles, nullptr, w.B.srec};
   int stride_shift = -1;
   for (int b = 0; b < 31; ++b)
     if ((1 << b) == stride) stride_shift = b;
   if (precision != GF_PRECISION_FP16) w.R.denc = nullptr;  // only the tensor-core MLP reads gamma(d) per ray
-  RenderIO io{w.RB.rec, w.RB.res, w.R.dir, (uint32_t)stride, w.R.denc, stride_shift};
+  RenderIO io{w.RB.res, w.R.dir, (uint32_t)stride, w.R.denc, stride_shift};
   const bool mlp_ok = precision == GF_PRECISION_FP16   ? prepare_mlp_tc(t)
                       : precision == GF_PRECISION_FP32 ? prepare_mlp_fp32(t)
                                                        : false;
@@ -551,8 +555,8 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
     cudaMemsetAsync(w.B.counts, 0, (size_t)2 * nc * 4, s);
     cudaMemsetAsync(w.RB.emit_count, 0, 2 * sizeof(uint32_t), s);
     if (P.stratified)
-      k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(n_blocks, 64), 64, 0, s>>>(cfg->seed, first_block, ray_block_stride,
-                                                                              n_blocks, w.seeds, w.jump);
+      k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(n_blocks > GF_RAY_BLOCK ? n_blocks : GF_RAY_BLOCK, 64), 64, 0, s>>>(
+          cfg->seed, first_block, ray_block_stride, n_blocks, cfg->k, w.seeds, w.jump, w.start);
     k_ray_init<<<ray_blocks, 128, 0, s>>>(P, w.R);
     stage_mark(s, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
     for (int r = 0; r < P.n_rounds; ++r) {

@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells
       if (toff[mid] <= t) lo = mid;
       else hi = mid;
     }
-    B.tiles[t] = make_uint2((uint32_t)lo, (t - toff[lo]) * GF_TILE_ROWS);
+    const uint32_t r0 = (t - toff[lo]) * GF_TILE_ROWS, n_seg = B.offsets[lo + 1] - B.offsets[lo];
+    B.tiles[t] = gf_make_tile((uint32_t)lo, B.offsets[lo] + r0, min(n_seg - r0, (uint32_t)GF_TILE_ROWS));
   }
 }
 

@@ -19,7 +19,7 @@ namespace gf {
 // per-block PCG64 seeds: SeedSequence([seed, 4096*b])   (render.py:375)
 // -------------------------------------------------------------------------
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
-                              u128* seeds, u128* jump) {
+                              int k, u128* seeds, u128* jump, u128* start) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b == 0) {
     // LCG jump table: S_{n+d} = A^d S_n + (sum_{k<d} A^k) inc, d = 0..GF_JUMP_MAX
@@ -30,6 +30,14 @@ __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_
       c = c * GF_PCG_MULT + 1;
       a = a * GF_PCG_MULT;
     }
+  }
+  if (b < GF_RAY_BLOCK) {
+    // row r of a block starts at float32 draw r*k, i.e. after (r*k >> 1) + 1
+    // PCG64 steps (each step yields two float32 draws): the same jump for
+    // every block, so it is tabulated once per call instead of per ray
+    const uint64_t d = (((uint64_t)b * (uint64_t)k) >> 1) + 1;
+    start[2 * b] = gf_pcg_advance(1, 0, d);      // A^d
+    start[2 * b + 1] = gf_pcg_advance(0, 1, d);  // sum_{j<d} A^j
   }
   if (b >= n_blocks) return;
   u128 s, inc;
@@ -88,25 +96,36 @@ __device__ void coarse_intervals(const MarchParams& P, uint32_t* out, float ex, 
       out[GF_MAX_IVL - 1] = (out[GF_MAX_IVL - 1] & 0xFFFFu) | ((uint32_t)hi << 16);
     }
   };
+  // per-axis state in scalars (no local-memory arrays): next crossing
+  // distance, crossing spacing, flat-index delta and steps left in the grid
+  const int rx = g.res[0], rxy = g.res[0] * g.res[1];
+  float n0 = snext[0], n1 = snext[1], n2 = snext[2];
+  const float e0 = sdelta[0], e1 = sdelta[1], e2 = sdelta[2];
+  const int f0 = step[0], f1 = step[1] * rx, f2 = step[2] * rxy;
+  int l0 = step[0] > 0 ? g.res[0] - 1 - cell[0] : cell[0];
+  int l1 = step[1] > 0 ? g.res[1] - 1 - cell[1] : cell[1];
+  int l2 = step[2] > 0 ? g.res[2] - 1 - cell[2] : cell[2];
+  int c = cell[0] + rx * cell[1] + rxy * cell[2];
   float s = 0.f, s_open = 0.f;
   bool open = false;
   for (int it = 0; it < 4096; ++it) {
-    const uint32_t c = (uint32_t)(cell[0] + g.res[0] * (cell[1] + g.res[1] * cell[2]));
     const bool occ = (__ldg(P.coarse_bits + (c >> 5)) >> (c & 31)) & 1;
-    if (occ && !open) {
-      open = true;
-      s_open = s;
-    } else if (!occ && open) {
-      emit(s_open, s);
-      open = false;
+    if (occ != open) {
+      if (occ) s_open = s;
+      else emit(s_open, s);
+      open = occ;
     }
-    const int ax = snext[0] < snext[1] ? (snext[0] < snext[2] ? 0 : 2) : (snext[1] < snext[2] ? 1 : 2);
-    const float sn = snext[ax];
+    const bool a0 = n0 < n1 && n0 < n2;
+    const bool a1 = !a0 && n1 < n2;
+    const float sn = a0 ? n0 : (a1 ? n1 : n2);
     if (!(sn < smax)) break;
+    const int left = a0 ? l0 : (a1 ? l1 : l2);
+    if (left == 0) break;  // the next crossing leaves the grid
     s = sn;
-    cell[ax] += step[ax];
-    if (cell[ax] < 0 || cell[ax] >= g.res[ax]) break;
-    snext[ax] += sdelta[ax];
+    c += a0 ? f0 : (a1 ? f1 : f2);
+    if (a0) { n0 += e0; --l0; }
+    else if (a1) { n1 += e1; --l1; }
+    else { n2 += e2; --l2; }
   }
   if (open) emit(s_open, smax);
   for (int k = n; k < GF_MAX_IVL; ++k) out[k] = 0x0000FFFFu;  // empty (lo > hi)
@@ -185,9 +204,8 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
   }
   if (P.stratified) {
     const int64_t b = seed_slot(P, g);
-    uint64_t draw0 = (uint64_t)(g % GF_RAY_BLOCK) * (uint64_t)P.k;  // float32 draw index of slot 0
-    u128 s = gf_pcg_advance(P.block_seeds[2 * b], P.block_seeds[2 * b + 1], (draw0 >> 1) + 1);
-    R.rng[i] = s;
+    const int r = (int)(g % GF_RAY_BLOCK);  // the ray's row in its block: slot 0 is float32 draw r*k
+    R.rng[i] = P.start[2 * r] * P.block_seeds[2 * b] + P.start[2 * r + 1] * P.block_seeds[2 * b + 1];
   }
   if (i == 0) atomicAdd((unsigned long long*)&P.stats[GF_STAT_N_RAYS], (unsigned long long)P.n_rays);
 }
@@ -280,7 +298,8 @@ __global__ void k_dilate_yz(const uint32_t* __restrict__ in, uint32_t* out, int3
 // K2 placement (batched.py:60-85 group_by_network, as the MLP consumes it):
 // every record already carries its rank inside its cell (from the marcher's
 // histogram atomics), so its sorted slot is offsets[cell] + rank with no
-// atomics here.  SMEM: each CTA scans the per-cell counts into shared memory
+// atomics here; the record itself (with its staging index in .w) moves to
+// its sorted slot, so the MLP streams its rows with no gather.  SMEM: each CTA scans the per-cell counts into shared memory
 // itself (no separate scan launch); block 0 publishes offsets / n_tiles and
 // every thread writes part of the tile list.  !SMEM (very large grids):
 // offsets and tiles come from k_scan_cells.
@@ -355,22 +374,49 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
     uint32_t* other = RB.counts + (size_t)((round + 1) & 1) * (size_t)n_cells;  // next round's histogram
     for (uint64_t c = gtid; c < (uint64_t)n_cells; c += gthreads) {
       other[c] = 0;
-      for (uint32_t t = s_toff[c]; t < s_toff[c + 1]; ++t)
-        Bk.tiles[t] = make_uint2((uint32_t)c, (t - s_toff[c]) * GF_TILE_ROWS);
+      const uint32_t n_seg = s_off[c + 1] - s_off[c];
+      for (uint32_t t = s_toff[c]; t < s_toff[c + 1]; ++t) {
+        const uint32_t r0 = (t - s_toff[c]) * GF_TILE_ROWS;
+        Bk.tiles[t] = gf_make_tile((uint32_t)c, s_off[c] + r0, min(n_seg - r0, (uint32_t)GF_TILE_ROWS));
+      }
     }
     off = s_off;
   } else if (gtid == 0) {
     RB.emit_count[(round + 1) & 1] = 0;
   }
+  // warp-cooperative record walk: a warp takes 32 listed rays, prefix-sums
+  // their runs and moves their records 32 at a time (one per lane), so every
+  // lane has an independent load -> cell -> store chain in flight
   const uint32_t n_list = RB.emit_count[round & 1];
-  for (uint64_t k = gtid; k < n_list; k += gthreads) {
-    const uint32_t i = RB.emit_list[k];
-    const uint32_t nr = run[i];
-    const uint64_t base = (uint64_t)i * (uint64_t)stride;
-    for (uint32_t j = 0; j < nr; ++j) {
-      const float4 q = RB.rec[base + j];
-      const uint32_t cell = gf_flat_cell(grid, q.x, q.y, q.z);
-      Bk.sorted[off[cell] + __float_as_uint(q.w)] = (uint32_t)(base + j);
+  const unsigned lane = gf_lane();
+  const uint64_t warp_g = gtid >> 5, n_warps = gthreads >> 5;
+  for (uint64_t k0 = warp_g * 32; k0 < n_list; k0 += n_warps * 32) {
+    const uint64_t k = k0 + lane;
+    const uint32_t i = k < n_list ? RB.emit_list[k] : 0u;
+    const uint32_t nr = k < n_list ? run[i] : 0u;
+    uint32_t incl = nr;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31), excl = incl - nr;
+    for (uint32_t b0 = 0; b0 < total; b0 += 32) {
+      const uint32_t q = b0 + lane;
+      int own = 0;  // smallest lane whose inclusive count exceeds q
+#pragma unroll
+      for (int st = 16; st; st >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, own + st - 1);
+        if (v <= q) own += st;
+      }
+      const uint32_t j = q - __shfl_sync(0xffffffffu, excl, own);
+      const uint32_t i_o = __shfl_sync(0xffffffffu, i, own);
+      if (q < total) {
+        const uint64_t src = (uint64_t)i_o * (uint64_t)stride + j;
+        const float4 r = RB.rec[src];
+        const uint32_t cell = gf_flat_cell(grid, r.x, r.y, r.z);
+        Bk.srec[off[cell] + __float_as_uint(r.w)] = make_float4(r.x, r.y, r.z, __uint_as_float((uint32_t)src));
+      }
     }
   }
 }

@@ -22,6 +22,7 @@ struct MarchParams {
   int64_t ray_offset, n_rays, first_block, block_stride;
   const u128* block_seeds;  // [2*b] state, [2*b+1] inc
   const u128* jump;         // [2*d] A^d, [2*d+1] sum_{k<d} A^k  (d <= GF_JUMP_MAX)
+  const u128* start;        // [2*r], [2*r+1]: the same pair for the jump to block row r's first draw
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
   int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
   int64_t n_cells;
@@ -91,7 +92,7 @@ void launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, 
                   int stride, int round, cudaStream_t st);
 
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
-                              u128* seeds, u128* jump);
+                              int k, u128* seeds, u128* jump, u128* start);
 __global__ void k_ray_init(MarchParams P, RayState R);
 __global__ void k_coarse_reduce(const uint8_t* occ_bits, int3 occ_res, int factor, int3 cres, uint8_t* coarse);
 __global__ void k_coarse_dilate(const uint8_t* coarse, int3 cres, int radius, uint32_t* bits);

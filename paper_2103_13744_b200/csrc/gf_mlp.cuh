@@ -60,9 +60,15 @@ __host__ inline Fp32Layout make_fp32_layout(const LayerTable& t) {
 // Sources / sinks of MLP rows ------------------------------------------------
 // Render: rows are kept samples in the ray-major staging buffer; the view
 // direction is the ray's (render.py:326).
+struct TileSched {
+  const uint2* tiles;       // gf_make_tile entries
+  const uint32_t* n_tiles;
+  const uint32_t* sorted;   // query paths: caller row per sorted row
+  const float4* srec;       // render path: sorted sample records
+};
+
 struct RenderIO {
   static constexpr bool kDirEnc = true;  // tensor-core path reads the ray's pre-encoded gamma(d)
-  const float4* rec;
   float4* res;
   const float4* ray_dir;
   uint32_t stride;
@@ -71,15 +77,16 @@ struct RenderIO {
   __device__ __forceinline__ uint32_t ray_of(uint32_t idx) const {
     return stride_shift >= 0 ? idx >> stride_shift : idx / stride;
   }
-  __device__ __forceinline__ void load(uint32_t idx, float* x, float* d) const {
-    float4 r = rec[idx];
-    float4 dd = ray_dir[ray_of(idx)];
+  // sorted row -> (staging index, position[, direction])
+  template <bool DIR>
+  __device__ __forceinline__ void fetch(const TileSched& S, uint32_t row, uint32_t& idx, float* x, float* d) const {
+    const float4 r = S.srec[row];
+    idx = __float_as_uint(r.w);
     x[0] = r.x; x[1] = r.y; x[2] = r.z;
-    d[0] = dd.x; d[1] = dd.y; d[2] = dd.z;
-  }
-  __device__ __forceinline__ void load_pos(uint32_t idx, float* x, float*) const {
-    float4 r = rec[idx];
-    x[0] = r.x; x[1] = r.y; x[2] = r.z;
+    if (DIR) {
+      const float4 dd = ray_dir[ray_of(idx)];
+      d[0] = dd.x; d[1] = dd.y; d[2] = dd.z;
+    }
   }
   __device__ __forceinline__ void load_denc(uint32_t idx, uint4* de) const {
     const uint4* q = denc + 4ull * ray_of(idx);
@@ -99,11 +106,15 @@ struct QueryIO {
   float* rgb;
   float* sigma;
   const int64_t* store_idx;  // optional: row idx is written to store_idx[idx] (grouped_forward)
-  __device__ __forceinline__ void load(uint32_t idx, float* x, float* d) const {
+  template <bool DIR>
+  __device__ __forceinline__ void fetch(const TileSched& S, uint32_t row, uint32_t& idx, float* x, float* d) const {
+    idx = S.sorted[row];
     const float* p = pos + 3ull * idx;
-    const float* q = dir + 3ull * idx;
     x[0] = p[0]; x[1] = p[1]; x[2] = p[2];
-    d[0] = q[0]; d[1] = q[1]; d[2] = q[2];
+    if (DIR) {
+      const float* q = dir + 3ull * idx;
+      d[0] = q[0]; d[1] = q[1]; d[2] = q[2];
+    }
   }
   __device__ __forceinline__ void store(uint32_t row, float r, float g, float b, float s) const {
     const uint64_t idx = store_idx ? (uint64_t)store_idx[row] : (uint64_t)row;
@@ -112,15 +123,7 @@ struct QueryIO {
     rgb[3ull * idx + 2] = b;
     sigma[idx] = s;
   }
-  __device__ __forceinline__ void load_pos(uint32_t idx, float* x, float* d) const { load(idx, x, d); }
   __device__ __forceinline__ void load_denc(uint32_t, uint4*) const {}
-};
-
-struct TileSched {
-  const uint2* tiles;
-  const uint32_t* n_tiles;
-  const uint32_t* offsets;
-  const uint32_t* sorted;
 };
 
 // launchers (gf_mlp_simt.cu / gf_mlp_tc.cu); return false if the architecture

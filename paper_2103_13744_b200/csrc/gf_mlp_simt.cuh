@@ -66,19 +66,18 @@ __global__ void __launch_bounds__(128) k_mlp_fp32(const float* __restrict__ pack
   int cur = -1;
   for (uint32_t t = t_begin; t < t_end; ++t) {
     const uint2 tl = S.tiles[t];
-    if ((int)tl.x != cur) {
+    const uint32_t cell = gf_tile_cell(tl);
+    if ((int)cell != cur) {
       __syncthreads();
-      const float4* src = reinterpret_cast<const float4*>(packed + (size_t)tl.x * L.cell_floats);
+      const float4* src = reinterpret_cast<const float4*>(packed + (size_t)cell * L.cell_floats);
       for (int j = threadIdx.x; j < L.cell_floats / 4; j += blockDim.x) smem4[j] = __ldg(src + j);
       __syncthreads();
-      cur = (int)tl.x;
+      cur = (int)cell;
     }
-    const uint32_t seg0 = S.offsets[tl.x], seg_n = S.offsets[tl.x + 1] - seg0;
-    const uint32_t r = tl.y + threadIdx.x;
-    if (r >= seg_n) continue;
-    const uint32_t idx = S.sorted[seg0 + r];
+    if (threadIdx.x >= gf_tile_rows(tl)) continue;
+    uint32_t idx;
     float x[3], d[3];
-    io.load(idx, x, d);
+    io.template fetch<true>(S, tl.y + threadIdx.x, idx, x, d);
     float xe[P];
     encode_f32<LX>(x, xe);
     float h[W], h2[W];

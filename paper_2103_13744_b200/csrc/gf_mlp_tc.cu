@@ -188,21 +188,17 @@ struct RowIn {
 
 template <class IO>
 __device__ __forceinline__ void load_row(const TileSched& S, const IO& io, uint2 tl, int tid, RowIn& r) {
-  const uint32_t seg0 = S.offsets[tl.x], seg_n = S.offsets[tl.x + 1] - seg0;
-  r.valid = tl.y + (uint32_t)tid < seg_n;
+  r.valid = (uint32_t)tid < gf_tile_rows(tl);
   r.idx = 0;
   r.x[0] = r.x[1] = r.x[2] = 0.f;
   if (!IO::kDirEnc) r.d[0] = r.d[1] = r.d[2] = 0.f;
-  if (r.valid) {
-    r.idx = S.sorted[seg0 + tl.y + tid];
-    io.load_pos(r.idx, r.x, r.d);
-  }
+  if (r.valid) io.template fetch<!IO::kDirEnc>(S, tl.y + (uint32_t)tid, r.idx, r.x, r.d);
 }
 
 // tiles [t, t+1) or [t, t+2): the second slot is used only for a tile of the
 // same cell (both slots share the staged weights)
 __device__ __forceinline__ bool pair_second(const TileSched& S, uint32_t t, uint32_t t_end, uint32_t cell) {
-  return t + 1 < t_end && S.tiles[t + 1].x == cell;
+  return t + 1 < t_end && gf_tile_cell(S.tiles[t + 1]) == cell;
 }
 
 // gamma(x) (core.py:132-152 layout: raw xyz, then per octave k sin xyz, cos
@@ -335,7 +331,7 @@ __global__ void __launch_bounds__(256, W == 32 ? 3 : 1) k_mlp_tc(const uint8_t* 
     if (t >= t_end) return false;
     tl = S.tiles[t];
     if (g == 0) return true;
-    if (!pair_second(S, t, t_end, tl.x)) return false;
+    if (!pair_second(S, t, t_end, gf_tile_cell(tl))) return false;
     tl = S.tiles[t + 1];
     return true;
   };
@@ -347,14 +343,14 @@ __global__ void __launch_bounds__(256, W == 32 ? 3 : 1) k_mlp_tc(const uint8_t* 
   }
 
   for (uint32_t t = t_begin; t < t_end;) {
-    const uint2 tl = S.tiles[t];
-    const bool two = pair_second(S, t, t_end, tl.x);
+    const uint32_t cell = gf_tile_cell(S.tiles[t]);
+    const bool two = pair_second(S, t, t_end, cell);
     const uint32_t t_next = t + (two ? 2 : 1);
     const bool active = g == 0 || two;
     __syncthreads();  // previous pair fully retired (bias reads, weight operands)
-    const bool new_cell = (int)tl.x != cur;
-    if (new_cell && tid == 0) bulk_load(wb, packed + (size_t)tl.x * T::CELL_BYTES, T::CELL_BYTES, bar_w);
-    cur = (int)tl.x;
+    const bool new_cell = (int)cell != cur;
+    if (new_cell && tid == 0) bulk_load(wb, packed + (size_t)cell * T::CELL_BYTES, T::CELL_BYTES, bar_w);
+    cur = (int)cell;
     const RowIn row = nxt;
     if (active) {
       encode_position<W>(A0, gt, row.x);
