@@ -451,6 +451,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   P.trace = trace;
   P.trace_capacity = trace ? trace_capacity : 0;
   P.trace_count = trace_count;
+  P.count_candidates = getenv("GF_COUNT_CANDIDATES") && getenv("GF_COUNT_CANDIDATES")[0] == '1';
 
   // ---- coarse empty-space pre-test: a mip of the occupancy
   // grid dilated by the largest distance between a sample and the midpoint

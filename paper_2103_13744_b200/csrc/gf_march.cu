@@ -575,14 +575,23 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
   uint32_t kept = 0;
   if (m <= 32) {
     // ---- warp-cooperative path: the warp's candidate (ray, slot) pairs are
-    // enumerated in (lane, slot) order and processed 32 at a time, one per
-    // lane, so the exact float64 placement never runs on idle lanes.
-    __shared__ uint32_t s_carry[4][32];  // kept samples so far, per ray (lane) of each warp
+    // compacted into a shared-memory list in (lane, slot) order and processed
+    // 32 at a time, one per lane, so the exact float64 placement never runs
+    // on idle lanes.  Each candidate lane reads its ray's parameters from
+    // shared memory (broadcast when several lanes share a ray).
+    struct RayPar {
+      float4 o, d;      // origin + t0, direction + seg
+      uint4 S, I;       // PCG64 state at draw d0 (rounded down to a word), increment
+      uint32_t i, d0;   // call-local ray index, float32 draw index of slot s0
+      uint32_t carry, pad;
+    };
+    __shared__ RayPar s_ray[4][32];
+    __shared__ uint16_t s_list[4][32 * 32];
     const int wib = threadIdx.x >> 5;
     const unsigned lane = gf_lane();
     if (!active) cmask = 0;
-    s_carry[wib][lane] = 0;
     const uint32_t cnt = __popc(cmask);
+    if (P.count_candidates) warp_add_u64(&P.stats[GF_STAT_N_RAYS], cnt);
     uint32_t incl = cnt;
 #pragma unroll
     for (int o2 = 1; o2 < 32; o2 <<= 1) {
@@ -590,34 +599,43 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       if ((int)lane >= o2) incl += v;
     }
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t excl = incl - cnt;
     const uint32_t d0 = (uint32_t)draw;  // float32 draw index of slot s0 in the ray's block stream
-    const uint64_t S_lo = (uint64_t)S, S_hi = (uint64_t)(S >> 64), I_lo = (uint64_t)inc, I_hi = (uint64_t)(inc >> 64);
+    {
+      RayPar& rp = s_ray[wib][lane];
+      rp.o = o;
+      rp.d = d;
+      rp.S = make_uint4((uint32_t)S, (uint32_t)(S >> 32), (uint32_t)(S >> 64), (uint32_t)(S >> 96));
+      rp.I = make_uint4((uint32_t)inc, (uint32_t)(inc >> 32), (uint32_t)(inc >> 64), (uint32_t)(inc >> 96));
+      rp.i = (uint32_t)i;
+      rp.d0 = d0;
+      rp.carry = 0;
+      uint32_t msk = cmask, pos = incl - cnt;
+      while (msk) {  // this lane's candidate slots, ascending
+        const int j = __ffs(msk) - 1;
+        s_list[wib][pos++] = (uint16_t)((lane << 5) | (uint32_t)j);
+        msk &= msk - 1u;
+      }
+    }
     __syncwarp();
     for (uint32_t b0 = 0; b0 < total; b0 += 32) {
       const uint32_t k = b0 + lane;
       const bool has = k < total;
-      int own = 0;  // smallest lane whose inclusive count exceeds k
-#pragma unroll
-      for (int st = 16; st; st >>= 1) {
-        const uint32_t v = __shfl_sync(0xffffffffu, incl, own + st - 1);
-        if (v <= k) own += st;
-      }
-      const uint32_t rank = k - __shfl_sync(0xffffffffu, excl, own);
-      const uint32_t cm_o = __shfl_sync(0xffffffffu, cmask, own);
-      const float ox_o = __shfl_sync(0xffffffffu, o.x, own), oy_o = __shfl_sync(0xffffffffu, o.y, own);
-      const float oz_o = __shfl_sync(0xffffffffu, o.z, own), t0_o = __shfl_sync(0xffffffffu, o.w, own);
-      const float dx_o = __shfl_sync(0xffffffffu, d.x, own), dy_o = __shfl_sync(0xffffffffu, d.y, own);
-      const float dz_o = __shfl_sync(0xffffffffu, d.z, own), sg_o = __shfl_sync(0xffffffffu, d.w, own);
-      const int64_t i_o = __shfl_sync(0xffffffffu, (long long)i, own);
+      const uint32_t e = has ? (uint32_t)s_list[wib][k] : (32u << 5);
+      const int own = (int)(e >> 5);  // 32 for idle lanes
+      const int j = (int)(e & 31u);
       double jit = 0.5;
-      int j = 0;
-      if (has) j = (int)__fns(cm_o, 0, (int)rank + 1);
-      if (P.stratified) {
-        const uint32_t d0_o = __shfl_sync(0xffffffffu, d0, own);
-        const u128 So = ((u128)__shfl_sync(0xffffffffu, S_hi, own) << 64) | __shfl_sync(0xffffffffu, S_lo, own);
-        const u128 Io = ((u128)__shfl_sync(0xffffffffu, I_hi, own) << 64) | __shfl_sync(0xffffffffu, I_lo, own);
-        if (has) {
+      float4 ro = make_float4(0.f, 0.f, 0.f, 0.f), rd = ro;
+      uint32_t i_o = 0;
+      if (has) {
+        const RayPar& rp = s_ray[wib][own];
+        ro = rp.o;
+        rd = rp.d;
+        i_o = rp.i;
+        if (P.stratified) {
+          const uint32_t d0_o = rp.d0;
+          const uint4 sv = rp.S, iv = rp.I;
+          const u128 So = ((u128)(((uint64_t)sv.w << 32) | sv.z) << 64) | (((uint64_t)sv.y << 32) | sv.x);
+          const u128 Io = ((u128)(((uint64_t)iv.w << 32) | iv.z) << 64) | (((uint64_t)iv.y << 32) | iv.x);
           const uint32_t dd = d0_o + (uint32_t)j;
           const uint32_t delta = (dd >> 1) - (d0_o >> 1);
           const u128 Sj = ldg_u128(&P.jump[2 * delta]) * So + ldg_u128(&P.jump[2 * delta + 1]) * Io;
@@ -632,10 +650,10 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       float px = 0.f, py = 0.f, pz = 0.f;
       if (has) {
         // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
-        const double t = __dadd_rn((double)t0_o, __dmul_rn(__dadd_rn((double)(s0 + j), jit), (double)sg_o));
-        px = __double2float_rn(__dadd_rn((double)ox_o, __dmul_rn(t, (double)dx_o)));
-        py = __double2float_rn(__dadd_rn((double)oy_o, __dmul_rn(t, (double)dy_o)));
-        pz = __double2float_rn(__dadd_rn((double)oz_o, __dmul_rn(t, (double)dz_o)));
+        const double t = __dadd_rn((double)ro.w, __dmul_rn(__dadd_rn((double)(s0 + j), jit), (double)rd.w));
+        px = __double2float_rn(__dadd_rn((double)ro.x, __dmul_rn(t, (double)rd.x)));
+        py = __double2float_rn(__dadd_rn((double)ro.y, __dmul_rn(t, (double)rd.y)));
+        pz = __double2float_rn(__dadd_rn((double)ro.z, __dmul_rn(t, (double)rd.z)));
         if (fast_clip) {
           px = gf_clip_fast(px, P.grid.b_min_f[0], P.grid.b_max_f[0]);
           py = gf_clip_fast(py, P.grid.b_min_f[1], P.grid.b_max_f[1]);
@@ -656,21 +674,21 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       // earlier in this batch + kept items of earlier batches
       const unsigned kb = __ballot_sync(0xffffffffu, keep);
       const unsigned same = __match_any_sync(0xffffffffu, has ? own : 32 + (int)lane);
-      const uint32_t pos = s_carry[wib][own] + __popc(kb & same & ((1u << lane) - 1u));
       const uint32_t crank = hist_rank(counts_r, keep, cell);
       if (keep) {
+        const uint32_t pos = s_ray[wib][own].carry + __popc(kb & same & ((1u << lane) - 1u));
         B.rec[(uint64_t)i_o * (uint64_t)P.stride + pos] = make_float4(px, py, pz, __uint_as_float(crank));
         if (P.trace) {
           unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
           if ((int64_t)slotpos < P.trace_capacity)
-            P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, i_o), (uint32_t)(s0 + j), cell};
+            P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, (int64_t)i_o), (uint32_t)(s0 + j), cell};
         }
       }
       __syncwarp();
-      if (has && (int)lane == __ffs(same) - 1) s_carry[wib][own] += __popc(kb & same);
+      if (has && (int)lane == 31 - __clz(same)) s_ray[wib][own].carry += __popc(kb & same);
       __syncwarp();
     }
-    kept = s_carry[wib][lane];
+    kept = s_ray[wib][lane].carry;
     if (P.stratified && active) {
       const uint32_t delta = ((d0 + (uint32_t)m) >> 1) - (d0 >> 1);
       S = ldg_u128(&P.jump[2 * delta]) * S + ldg_u128(&P.jump[2 * delta + 1]) * inc;

@@ -27,6 +27,7 @@ struct MarchParams {
   int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
   int64_t n_cells;
   int64_t march_threads;
+  int count_candidates;  // diagnostics (GF_COUNT_CANDIDATES=1): exact-path candidates added to stats[N_RAYS]
   double epsilon;
   float bg[3];
   float* rgb_out;
