@@ -2,6 +2,7 @@
 //
 // Host-side orchestration only: argument validation, workspace carving and
 // the launch sequence of the render / query pipelines on the caller's stream.
+#include <algorithm>
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
@@ -328,6 +329,7 @@ struct RenderWs {
   u128* seeds;
   u128* jump;
   u128* start;
+  u128* round_jump;
   RayState R;
   RoundBufs RB;
   BucketBufs B;
@@ -339,11 +341,13 @@ struct RenderWs {
 // exceeds that many cells
 static const int64_t kMaxCoarseCells = 256ll * 256 * 256;
 
-static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int stride, int64_t n_cells, RenderWs* w) {
+static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int stride, int64_t n_cells, int n_rounds,
+                           RenderWs* w) {
   const size_t cap = (size_t)n_rays * (size_t)stride;
   w->seeds = c.take<u128>((size_t)2 * n_blocks);
   w->jump = c.take<u128>((size_t)2 * (GF_JUMP_MAX + 1));
   w->start = c.take<u128>((size_t)2 * GF_RAY_BLOCK);
+  w->round_jump = c.take<u128>((size_t)4 * n_rounds);
   w->coarse_tmp = c.take<uint8_t>((size_t)kMaxCoarseCells);
   w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->R.org = c.take<float4>((size_t)n_rays);
@@ -351,7 +355,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->R.acc = c.take<float4>((size_t)n_rays);
   w->R.rng = c.take<u128>((size_t)n_rays);
   w->R.run = c.take<uint32_t>((size_t)n_rays);
-  w->R.flags = c.take<uint8_t>((size_t)n_rays);
+  w->R.flags = c.take<uint32_t>((size_t)n_rays);
   w->R.ivl = c.take<uint32_t>((size_t)n_rays * GF_MAX_IVL);
   w->R.denc = c.take<uint4>((size_t)n_rays * 4);
   w->RB.rec = c.take<float4>(cap);
@@ -388,7 +392,8 @@ size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* gr
   Carve c(nullptr);
   RenderWs w;
   // worst case: the call's rays straddle one more block boundary
-  return render_carve(c, n_rays, n_rays / GF_RAY_BLOCK + 2, stride, n_cells_of(grid), &w);
+  return render_carve(c, n_rays, n_rays / GF_RAY_BLOCK + 2, stride, n_cells_of(grid),
+                      (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk, &w);
 }
 
 int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed, int precision,
@@ -414,7 +419,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   block_range(ray_offset, ray_block_stride, n_rays, &first_block, &n_blocks);
   Carve c(ws);
   RenderWs w{};
-  if (render_carve(c, n_rays, n_blocks, stride, nc, &w) > ws_bytes)
+  if (render_carve(c, n_rays, n_blocks, stride, nc, (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk, &w) > ws_bytes)
     return fail(GF_ERR_WORKSPACE, "gf_render_rays: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
 
@@ -436,6 +441,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   P.block_seeds = w.seeds;
   P.jump = w.jump;
   P.start = w.start;
+  P.round_jump = w.round_jump;
   P.k = cfg->k;
   P.chunk = cfg->ert_chunk;
   P.n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
@@ -556,8 +562,9 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
     cudaMemsetAsync(w.B.counts, 0, (size_t)2 * nc * 4, s);
     cudaMemsetAsync(w.RB.emit_count, 0, 2 * sizeof(uint32_t), s);
     if (P.stratified)
-      k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(n_blocks > GF_RAY_BLOCK ? n_blocks : GF_RAY_BLOCK, 64), 64, 0, s>>>(
-          cfg->seed, first_block, ray_block_stride, n_blocks, cfg->k, w.seeds, w.jump, w.start);
+      k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(std::max<int64_t>({n_blocks, (int64_t)GF_RAY_BLOCK, 2ll * P.n_rounds}), 64),
+                      64, 0, s>>>(cfg->seed, first_block, ray_block_stride, n_blocks, cfg->k, cfg->ert_chunk, P.n_rounds,
+                                  w.seeds, w.jump, w.start, w.round_jump);
     k_ray_init<<<ray_blocks, 128, 0, s>>>(P, w.R);
     stage_mark(s, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
     for (int r = 0; r < P.n_rounds; ++r) {

@@ -19,7 +19,8 @@ namespace gf {
 // per-block PCG64 seeds: SeedSequence([seed, 4096*b])   (render.py:375)
 // -------------------------------------------------------------------------
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
-                              int k, u128* seeds, u128* jump, u128* start) {
+                              int k, int chunk, int n_rounds, u128* seeds, u128* jump, u128* start,
+                              u128* round_jump) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b == 0) {
     // LCG jump table: S_{n+d} = A^d S_n + (sum_{k<d} A^k) inc, d = 0..GF_JUMP_MAX
@@ -38,6 +39,13 @@ __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_
     const uint64_t d = (((uint64_t)b * (uint64_t)k) >> 1) + 1;
     start[2 * b] = gf_pcg_advance(1, 0, d);      // A^d
     start[2 * b + 1] = gf_pcg_advance(0, 1, d);  // sum_{j<d} A^j
+  }
+  if (b < 2 * n_rounds) {
+    // round r of a ray whose slot-0 draw has parity p starts (p + r*chunk) >> 1
+    // PCG64 words after the ray's slot-0 word
+    const uint64_t d = ((uint64_t)(b & 1) + (uint64_t)(b >> 1) * (uint64_t)chunk) >> 1;
+    round_jump[2 * b] = gf_pcg_advance(1, 0, d);
+    round_jump[2 * b + 1] = gf_pcg_advance(0, 1, d);
   }
   if (b >= n_blocks) return;
   u128 s, inc;
@@ -189,7 +197,7 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
   R.dir[i] = make_float4(d32[0], d32[1], d32[2], seg);
   R.acc[i] = make_float4(0.f, 0.f, 0.f, 1.f);
   R.run[i] = 0;
-  R.flags[i] = hit ? (uint8_t)(GF_RAY_ALIVE | GF_RAY_HIT) : (uint8_t)0;
+  uint32_t fw = hit ? (uint32_t)(GF_RAY_ALIVE | GF_RAY_HIT) : 0u;
   if (R.denc && hit) {  // gamma(d) once per ray for every sample's direction layer (render.py:326)
     uint4 de[4];
     encode_direction_h(d32, de);
@@ -201,7 +209,27 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
     const float ey = __double2float_rn(__dadd_rn((double)o32[1], __dmul_rn(t0, (double)d32[1])));
     const float ez = __double2float_rn(__dadd_rn((double)o32[2], __dmul_rn(t0, (double)d32[2])));
     coarse_intervals(P, R.ivl + i * GF_MAX_IVL, ex, ey, ez, d32, (float)(t1 - t0), seg);
+    if (P.n_rounds <= 24) {  // rounds holding at least one candidate slot
+      const uint4* iv = reinterpret_cast<const uint4*>(R.ivl + i * GF_MAX_IVL);
+      const uint4 q0 = iv[0], q1 = iv[1];
+      const uint32_t v[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      uint32_t rm = 0;
+#pragma unroll
+      for (int k = 0; k < GF_MAX_IVL; ++k) {
+        const int lo = (int)(v[k] & 0xFFFFu), hi = (int)(v[k] >> 16);
+        if (lo <= hi) {
+          const int r0 = lo / P.chunk, r1 = hi / P.chunk;
+          rm |= (r1 - r0 >= 31 ? 0xFFFFFFFFu : ((2u << (r1 - r0)) - 1u)) << r0;
+        }
+      }
+      fw |= (rm & 0xFFFFFFu) << 8;
+    } else {
+      fw |= GF_RAY_ALLROUNDS;
+    }
+  } else if (hit) {
+    fw |= GF_RAY_ALLROUNDS;
   }
+  R.flags[i] = fw;
   if (P.stratified) {
     const int64_t b = seed_slot(P, g);
     const int r = (int)(g % GF_RAY_BLOCK);  // the ray's row in its block: slot 0 is float32 draw r*k
@@ -472,50 +500,51 @@ __device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v)
 // -------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundBufs B, int round) {
   const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
-  bool in_range = i < P.n_rays;
-  uint8_t flags = in_range ? R.flags[i] : 0;
-  bool final_pass = round == P.n_rounds;
-  if (!final_pass && !__any_sync(0xffffffffu, flags & GF_RAY_ALIVE)) return;
+  const bool in_range = i < P.n_rays;
+  uint32_t fw = in_range ? R.flags[i] : 0u;  // flags | candidate-round mask << 8
+  const uint32_t fw0 = fw;
+  const bool final_pass = round == P.n_rounds;
+  if (!final_pass && !__any_sync(0xffffffffu, fw & GF_RAY_ALIVE)) return;
 
+  // ---- composite round r-1 (render.py:333-337), float32, no contraction;
+  // only rays that queried samples last round have anything to blend
   float4 acc = make_float4(0.f, 0.f, 0.f, 1.f);
-  float seg = 0.f;
-  uint64_t base = (uint64_t)i * (uint64_t)P.stride;
-  if (flags & GF_RAY_ALIVE) {
+  const bool had = (fw & GF_RAY_ALIVE) && (fw & GF_RAY_HAD);
+  if (had) {
     acc = R.acc[i];
-    seg = R.dir[i].w;
-    if (round > 0) {
-      // ---- composite round r-1 (render.py:333-337), float32, no contraction
-      uint32_t n = R.run[i];
-      float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
-      for (uint32_t j = 0; j < n; ++j) {
-        float4 q = B.res[base + j];
-        float a = -expm1f(__fmul_rn(-q.w, seg));
-        float w = __fmul_rn(tr, a);
-        tr = __fmul_rn(tr, __fsub_rn(1.0f, a));
-        sr = __fadd_rn(sr, __fmul_rn(w, q.x));
-        sg = __fadd_rn(sg, __fmul_rn(w, q.y));
-        sb = __fadd_rn(sb, __fmul_rn(w, q.z));
-      }
-      acc.x = __fadd_rn(acc.x, __fmul_rn(acc.w, sr));
-      acc.y = __fadd_rn(acc.y, __fmul_rn(acc.w, sg));
-      acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
-      acc.w = __fmul_rn(acc.w, tr);
-      // ---- ERT after the round (render.py:338-343)
-      if (P.ert) {
-        bool dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
-        if (dead) {
-          flags &= (uint8_t)~GF_RAY_ALIVE;
-          if ((int64_t)round * P.chunk < P.k) flags |= GF_RAY_TERMINATED;  // rounds remained
-        }
-      }
-      R.acc[i] = acc;
+    const float seg = R.dir[i].w;
+    const uint64_t base = (uint64_t)i * (uint64_t)P.stride;
+    const uint32_t n = R.run[i];
+    float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
+    for (uint32_t j = 0; j < n; ++j) {
+      float4 q = B.res[base + j];
+      float a = -expm1f(__fmul_rn(-q.w, seg));
+      float w = __fmul_rn(tr, a);
+      tr = __fmul_rn(tr, __fsub_rn(1.0f, a));
+      sr = __fadd_rn(sr, __fmul_rn(w, q.x));
+      sg = __fadd_rn(sg, __fmul_rn(w, q.y));
+      sb = __fadd_rn(sb, __fmul_rn(w, q.z));
     }
-  } else if (final_pass && in_range) {
-    acc = R.acc[i];
+    acc.x = __fadd_rn(acc.x, __fmul_rn(acc.w, sr));
+    acc.y = __fadd_rn(acc.y, __fmul_rn(acc.w, sg));
+    acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
+    acc.w = __fmul_rn(acc.w, tr);
+    // ---- ERT after the round (render.py:338-343); transmittance only moves
+    // in rounds with samples, so other rays cannot cross epsilon
+    if (P.ert) {
+      bool dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
+      if (dead) {
+        fw &= ~(uint32_t)GF_RAY_ALIVE;
+        if ((int64_t)round * P.chunk < P.k) fw |= GF_RAY_TERMINATED;  // rounds remained
+      }
+    }
+    R.acc[i] = acc;
   }
+  fw &= ~(uint32_t)GF_RAY_HAD;
 
   if (final_pass) {
     if (in_range) {
+      if (!had) acc = R.acc[i];
       // render.py:345-348: acc + trans*bg, clip to [0,1]
       float c0 = __fadd_rn(acc.x, __fmul_rn(acc.w, P.bg[0]));
       float c1 = __fadd_rn(acc.y, __fmul_rn(acc.w, P.bg[1]));
@@ -524,35 +553,41 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       P.rgb_out[3 * i + 1] = fminf(fmaxf(c1, 0.f), 1.f);
       P.rgb_out[3 * i + 2] = fminf(fmaxf(c2, 0.f), 1.f);
     }
-    warp_add_u64(&P.stats[GF_STAT_ERT_TERMINATED], (flags & GF_RAY_TERMINATED) ? 1ull : 0ull);
+    warp_add_u64(&P.stats[GF_STAT_ERT_TERMINATED], (fw & GF_RAY_TERMINATED) ? 1ull : 0ull);
     return;
   }
 
-  bool active = (flags & GF_RAY_ALIVE) != 0;
-  if (in_range) {
-    R.flags[i] = flags;
-    if (!active) R.run[i] = 0;  // a ray that stops here must not re-emit last round's samples
-  }
-  if (!__any_sync(0xffffffffu, active)) return;
-
   // ---- sample round r (render.py:311-330)
-  int s0 = round * P.chunk;
-  int m = min(P.chunk, P.k - s0);
+  const int s0 = round * P.chunk;
+  const int m = min(P.chunk, P.k - s0);
+  const bool alive = (fw & GF_RAY_ALIVE) != 0;
+  // rays whose coarse intervals have no slot in this round only add to ess_skipped
+  const bool active = alive && ((fw & GF_RAY_ALLROUNDS) || (round < 24 && ((fw >> (8 + round)) & 1u)));
+  warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (alive && !active) ? (unsigned long long)m : 0ull);
+  if (!__any_sync(0xffffffffu, active)) {
+    if (in_range && fw != fw0) R.flags[i] = fw;
+    return;
+  }
   float4 o = active ? R.org[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   float4 d = active ? R.dir[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   u128 S = 0, inc = 0;
   uint64_t outw = 0;
   uint64_t draw = 0;
   if (P.stratified && active) {
+    // state of the word holding this round's first draw: a tabulated jump
+    // from the ray's slot-0 state (R.rng stays read-only)
     const int64_t g = global_ray(P, i);
     inc = P.block_seeds[2 * seed_slot(P, g) + 1];
-    S = R.rng[i];
+    const uint64_t draw0 = (uint64_t)(g % GF_RAY_BLOCK) * (uint64_t)P.k;
+    const int jr = 2 * (2 * round + (int)(draw0 & 1));
+    S = ldg_u128(&P.round_jump[jr]) * R.rng[i] + ldg_u128(&P.round_jump[jr + 1]) * inc;
     outw = gf_pcg_output(S);
-    draw = (uint64_t)(g % GF_RAY_BLOCK) * (uint64_t)P.k + (uint64_t)s0;
+    draw = draw0 + (uint64_t)s0;
   }
   const double t0 = (double)o.w, sg64 = (double)d.w;
   const double ox = (double)o.x, oy = (double)o.y, oz = (double)o.z;
   const double dx = (double)d.x, dy = (double)d.y, dz = (double)d.z;
+  const uint64_t base = (uint64_t)i * (uint64_t)P.stride;
   // candidate slots of this round from the ray's coarse-DDA ranges
   uint32_t cmask = m >= 32 ? 0xFFFFFFFFu : ((1u << m) - 1u);
   if (P.coarse_bits && active) {
@@ -689,10 +724,6 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       __syncwarp();
     }
     kept = s_ray[wib][lane].carry;
-    if (P.stratified && active) {
-      const uint32_t delta = ((d0 + (uint32_t)m) >> 1) - (d0 >> 1);
-      S = ldg_u128(&P.jump[2 * delta]) * S + ldg_u128(&P.jump[2 * delta + 1]) * inc;
-    }
   } else {
   double jd = (double)s0;
   for (int j = 0; j < m; ++j, jd += 1.0) {
@@ -749,10 +780,11 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     }
   }
   }  // sequential path (ert_chunk > 32)
-  if (active) {
+  if (active && kept > 0) {
     R.run[i] = kept;
-    if (P.stratified) R.rng[i] = S;
+    fw |= GF_RAY_HAD;
   }
+  if (in_range && fw != fw0) R.flags[i] = fw;
   {  // compact list of rays with queried samples, for the scatter kernel
     const bool emit = active && kept > 0;
     const unsigned em = __ballot_sync(0xffffffffu, emit);

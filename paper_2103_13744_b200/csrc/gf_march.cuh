@@ -5,6 +5,8 @@
 #define GF_RAY_ALIVE 1
 #define GF_RAY_HIT 2
 #define GF_RAY_TERMINATED 4
+#define GF_RAY_HAD 8         // queried samples in the last marched round (composite them next pass)
+#define GF_RAY_ALLROUNDS 16  // no per-round candidate mask: every round is a candidate round
 
 namespace gf {
 
@@ -23,6 +25,7 @@ struct MarchParams {
   const u128* block_seeds;  // [2*b] state, [2*b+1] inc
   const u128* jump;         // [2*d] A^d, [2*d+1] sum_{k<d} A^k  (d <= GF_JUMP_MAX)
   const u128* start;        // [2*r], [2*r+1]: the same pair for the jump to block row r's first draw
+  const u128* round_jump;   // [2*(2*round+parity)], +1: jump from a ray's slot-0 word to round's first word
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
   int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
   int64_t n_cells;
@@ -42,9 +45,9 @@ struct RayState {
   float4* org;    // ox, oy, oz, t0_32
   float4* dir;    // dx, dy, dz, seg_32
   float4* acc;    // r, g, b, transmittance
-  u128* rng;      // PCG64 state positioned at the ray's next float32 draw
+  u128* rng;      // PCG64 state of the word holding the ray's slot-0 float32 draw
   uint32_t* run;  // queried samples of the ray in the last marched round
-  uint8_t* flags;
+  uint32_t* flags;  // GF_RAY_* bits | (rounds with candidate slots, bit r) << 8
   uint32_t* ivl;  // GF_MAX_IVL candidate slot ranges per ray (lo | hi << 16), from the coarse DDA
   uint4* denc;    // NULL, or 4 x uint4 per ray: gamma(d) as fp16 for the tensor-core MLP
 };
@@ -93,7 +96,8 @@ void launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, 
                   int stride, int round, cudaStream_t st);
 
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
-                              int k, u128* seeds, u128* jump, u128* start);
+                              int k, int chunk, int n_rounds, u128* seeds, u128* jump, u128* start,
+                              u128* round_jump);
 __global__ void k_ray_init(MarchParams P, RayState R);
 __global__ void k_coarse_reduce(const uint8_t* occ_bits, int3 occ_res, int factor, int3 cres, uint8_t* coarse);
 __global__ void k_coarse_dilate(const uint8_t* coarse, int3 cres, int radius, uint32_t* bits);
