@@ -64,6 +64,23 @@ def build_inputs(gf):
     return aabb, grid, occ, cams
 
 
+def c4_camera(gf, aabb):
+    """BASELINE config 4's 1920x1080 view: the focal length of
+    sphere_cameras(aabb, 1, 1080, seed=0) on a 16:9 sensor."""
+    c = gf.sphere_cameras(aabb, 1, 1080, seed=0)[0]
+    return gf.Camera(1920, 1080, c.fx, c.fy, 960.0, 540.0, c.c2w)
+
+
+def build_c4(gf):
+    """Config 4: 32^3 lattice of 64-wide tiny MLPs (random init, seed 0), the
+    toy-scene occupancy, one 1920x1080 view."""
+    aabb = gf.Aabb((-1.0,) * 3, (1.0,) * 3)
+    grid = gf.init_network_grid(aabb, (32, 32, 32), seed=0, arch=gf.MlpArchitecture(hidden_width=64))
+    z = np.load(ROOT / "tests" / "golden" / "toy_occupancy_256.npz")
+    occ = gf.OccupancyGrid(aabb, z["res"], z["bits"].copy())
+    return aabb, grid, occ, c4_camera(gf, aabb)
+
+
 # ---------------------------------------------------------------------------
 # clocks during the timed region
 # ---------------------------------------------------------------------------

@@ -265,6 +265,18 @@ def grouped_eval(lat: Lattice, pos_sorted, dir_sorted, groups: Groups):
     return rgb[groups.inverse], sig[groups.inverse]
 
 
+def bulk_query_inputs(b_min, b_max, n, seed=0):
+    """Reference bench.py:108-112 input recipe (BASELINE config 5): uniform
+    float32 positions in the box, normalised float32 normal directions."""
+    rng = np.random.default_rng(seed)
+    b_min = np.asarray(b_min, np.float64)
+    span = (np.asarray(b_max, np.float64) - b_min).astype(np.float32)
+    pts = b_min.astype(np.float32) + rng.random((n, 3), dtype=np.float32) * span
+    dirs = rng.normal(size=(n, 3)).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    return pts, dirs
+
+
 def query_points(lat: Lattice, positions, directions):
     """grid.py:50-56: bin at network resolution, group, evaluate."""
     keys = bin_cells(positions, lat.b_min, lat.b_max, lat.res)

@@ -24,7 +24,7 @@ OUT = Path(__file__).resolve().parent
 sys.path.insert(0, str(REF))
 
 import gridfield  # noqa: E402  (the reference)
-from gridfield import core, grid as ggrid, occupancy, render, scene, batched  # noqa: E402
+from gridfield import core, grid as ggrid, mlp, occupancy, render, scene, batched  # noqa: E402
 
 
 def save(name, **arrays):
@@ -200,8 +200,48 @@ def gen_render():
     render_case("render_two_blocks", gb, occ, cam80, render.RenderConfig(k=64), seed=11, keep_trace=False)
 
 
+def w64_grid(res=(8, 8, 8), seed=4):
+    """The C4 architecture (64-wide tiny MLPs) on a small lattice."""
+    return ggrid.init_network_grid(unit(), res, seed=seed, arch=mlp.MlpArchitecture(hidden_width=64))
+
+
+def gen_wide():
+    """64-wide networks (BASELINE config 4's architecture): a query and a
+    traced render on an 8^3 lattice."""
+    aabb = unit()
+    g = w64_grid()
+    rng = np.random.default_rng(2)
+    n = 8000
+    pts = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    dirs = rng.normal(size=(n, 3)).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    c, s = g.query_points(pts, dirs)
+    save("query_w64", pts=pts, dirs=dirs, rgb=c, sigma=s,
+         w0_checksum=np.float64(g.params.weights["trunk0"].astype(np.float64).sum()))
+    gb = w64_grid()
+    gb.params.biases["density"][:] = 20.0
+    occ = toy_occ(256)
+    cam = scene.sphere_cameras(aabb, 1, 40, seed=7)[0]
+    render_case("render_w64_bias20", gb, occ, cam, render.RenderConfig(k=128), seed=2)
+
+
+def gen_bulk():
+    """BASELINE config 5's input recipe (bench.py:108-112 of the reference:
+    uniform positions in the box, normalised normal directions, default_rng(0))
+    at 2^14 points through the 16^3 seed-0 lattice."""
+    g = ggrid.init_network_grid(unit(), (16, 16, 16), seed=0)
+    rng = np.random.default_rng(0)
+    n = 1 << 14
+    span = (g.aabb.b_max - g.aabb.b_min).astype(np.float32)
+    pts = g.aabb.b_min.astype(np.float32) + rng.random((n, 3), dtype=np.float32) * span
+    dirs = rng.normal(size=(n, 3)).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    c, s = g.query_points(pts, dirs)
+    save("query_c5", pts=pts, dirs=dirs, rgb=c, sigma=s, keys=g.cell_index(pts))
+
+
 def main():
-    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render"]
+    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk"]
     for w in what:
         t = time.time()
         globals()[f"gen_{w}"]()

@@ -38,6 +38,9 @@ def device_grid(gf, name):
     if gname == "g2":
         g = gf.init_network_grid(aabb, (2, 3, 4), seed=9)
         g.params.biases["density"][:] = 5.0
+    elif gname == "gw":
+        g = gf.init_network_grid(aabb, (8, 8, 8), seed=4, arch=gf.MlpArchitecture(hidden_width=64))
+        g.params.biases["density"][:] = 20.0
     else:
         g = gf.init_network_grid(aabb, (16, 16, 16), seed=0)
         if gname == "gb":
@@ -254,7 +257,7 @@ def test_render_matches_golden(gf, name, precision, tol):
 
 
 @pytest.mark.parametrize("name", ["render_s32_trace", "render_toy96_bias20", "render_inside_chunk7", "render_axis",
-                                  "render_s32_k50", "render_two_blocks"])
+                                  "render_s32_k50", "render_two_blocks", "render_w64_bias20"])
 def test_render_trace_bit_exact(gf, name):
     """Every queried sample: same ray, same slot, same float32 position, same
     network cell as the oracle (itself pinned to the reference's trace)."""

@@ -45,6 +45,29 @@ def test_bin_out_of_bounds_message():
         O.bin_cells(np.array([0.5, 1.5, 0.5]), UNIT_MIN, UNIT_MAX, np.array([16, 16, 16]))
 
 
+def test_query_64_wide():
+    """64-wide tiny networks (config 4's architecture) against the reference."""
+    z = golden("query_w64")
+    lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (8, 8, 8), seed=4, width=64)
+    assert lat.weights["trunk0"].astype(np.float64).sum() == float(z["w0_checksum"])
+    rgb, sig = O.query_points(lat, z["pts"], z["dirs"])
+    assert np.max(np.abs(rgb - z["rgb"])) <= 1e-6
+    assert np.max(np.abs(sig - z["sigma"])) <= 1e-6
+
+
+def test_bulk_query_recipe():
+    """Config 5's input recipe (reference bench.py:108-112) through the 16^3
+    seed-0 lattice."""
+    z = golden("query_c5")
+    lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (16, 16, 16), seed=0)
+    pts, dirs = O.bulk_query_inputs(lat.b_min, lat.b_max, len(z["pts"]), seed=0)
+    assert np.array_equal(pts, z["pts"]) and np.array_equal(dirs, z["dirs"])
+    assert np.array_equal(O.bin_cells(pts, UNIT_MIN, UNIT_MAX, lat.res), z["keys"])
+    rgb, sig = O.query_points(lat, pts, dirs)
+    assert np.max(np.abs(rgb - z["rgb"])) <= 1e-6
+    assert np.max(np.abs(sig - z["sigma"])) <= 1e-6
+
+
 def test_query_points_and_grouping():
     z = golden("query16")
     lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (16, 16, 16), seed=3)
@@ -64,7 +87,7 @@ def test_query_points_and_grouping():
 RENDER_CASES = [
     "render_c1", "render_c1_bias20", "render_toy96", "render_toy96_bias20", "render_s32_trace",
     "render_s32_k50", "render_s32_nostrat", "render_inside_chunk7", "render_axis", "render_empty",
-    "render_two_blocks",
+    "render_two_blocks", "render_w64_bias20",
 ]
 
 LATTICES = {
@@ -72,6 +95,7 @@ LATTICES = {
     "render_toy96_bias20": ("gb", "toy"), "render_s32_trace": ("gb", "toy"), "render_s32_k50": ("gb", "toy"),
     "render_s32_nostrat": ("gb", None), "render_inside_chunk7": ("g2", None), "render_axis": ("gb", "toy"),
     "render_empty": ("g0", "empty"), "render_two_blocks": ("gb", "toy"),
+    "render_w64_bias20": ("gw", "toy"),
 }
 
 
@@ -81,6 +105,9 @@ def case_inputs(name):
     if gname == "g2":
         lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (2, 3, 4), seed=9)
         lat.biases["density"][:] = 5.0
+    elif gname == "gw":  # BASELINE config 4's 64-wide architecture on an 8^3 lattice
+        lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (8, 8, 8), seed=4, width=64)
+        lat.biases["density"][:] = 20.0
     else:
         lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (16, 16, 16), seed=0)
         if gname == "gb":
