@@ -64,6 +64,89 @@ def build_inputs(gf):
     return aabb, grid, occ, cams
 
 
+def c4_desc(precision):
+    return {
+        "workload": "C4: 1920x1080 frame, 32^3 grid of 64-wide tiny MLPs (random init, seed 0), toy-scene occupancy "
+                    "256^3, K=384, eps=0.01, ert_chunk=32, stratified, seed 0 (extra measurement, not the BASELINE line)",
+        "image": [1920, 1080], "grid": [32, 32, 32], "width": 64, "k": 384, "mlp_precision": precision,
+        "l2": "flushed between timed frames (256 MiB write outside the timed window)",
+    }
+
+
+def run_bulk(args, rank, world, local):
+    """Config 5: 2^26 random points/directions (reference bench.py:108-112
+    recipe) through the 16^3 bank per step, no compositing.  Inputs resident
+    in HBM for `value`; e2e copies them from pinned host memory every step."""
+    import torch
+
+    import paper_2103_13744_b200 as gf
+    from oracle import gridfield_oracle as O
+    from paper_2103_13744_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    n = 1 << 26
+    grid = gf.init_network_grid(gf.Aabb((-1.0,) * 3, (1.0,) * 3), (16, 16, 16), seed=0)
+    precision = args.precision or "fp16"
+    grid.precision = precision
+    pts, dirs = O.bulk_query_inputs(np.full(3, -1.0), np.ones(3), n, seed=1 + rank)  # input generator only
+    p_h, d_h = torch.from_numpy(pts).pin_memory(), torch.from_numpy(dirs).pin_memory()
+    p_d, d_d = p_h.cuda(), d_h.cuda()
+    rgb_h = torch.empty((n, 3), dtype=torch.float32).pin_memory()
+    sig_h = torch.empty((n,), dtype=torch.float32).pin_memory()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        grid.query_points(p_d, d_d)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = N.lib().gf_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            grid.query_points(p_d, d_d)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = N.lib().gf_launch_count() - launches0
+    ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    N.lib().gf_stage_timing(1)
+    grid.query_points(p_d, d_d)
+    torch.cuda.synchronize()
+    st_ms, _ = N.stage_times()
+    N.lib().gf_stage_timing(0)
+    e2e_t = []
+    for _ in range(max(3, args.steps // 2)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pd, dd = p_h.cuda(non_blocking=True), d_h.cuda(non_blocking=True)
+        r, sg = grid.query_points(pd, dd)
+        rgb_h.copy_(r, non_blocking=True)
+        sig_h.copy_(sg, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = statistics.median(e2e_t)
+    peaks, peak_src = load_peaks()
+    flops = n * gf.count_flops(grid.arch)
+    tf = flops / (st_ms["mlp"] * 1e-3) / 1e12
+    line = {
+        "metric": "MLP samples/sec vs roofline (config 5 bulk query)", "value": world * n / (ms * 1e-3) / 1e6,
+        "unit": "Mquery/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16" if precision == "fp16" else "f32",
+        "data": "synthetic (reference bench.py recipe, random-init 16^3 lattice)",
+        "config": {"workload": "C5: 2^26 random points/dirs through the 16^3 bank of 32-wide MLPs, no compositing",
+                   "points": n, "l2": "flushed between timed steps; inputs 1.6 GB > L2"},
+        "e2e": {"value": world * n / e2e_s / 1e6, "unit": "Mquery/s", "h2d_bytes_per_step": int(2 * pts.nbytes),
+                "d2h_bytes_per_step": int(n * 16), "ms_per_step": e2e_s * 1e3},
+        "roofline": {"bound": "tensor", "achieved": tf, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": tf / peaks["bf16_tflops_sustained"], "traffic": None, "kernel": "mlp",
+                     "peak_source": peak_src},
+        "stage_ms": st_ms, "clocks": clk.summary(), "gpu_launches": int(launches),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def c4_camera(gf, aabb):
     """BASELINE config 4's 1920x1080 view: the focal length of
     sphere_cameras(aabb, 1, 1080, seed=0) on a 16:9 sensor."""
@@ -212,6 +295,9 @@ def main():
     ap.add_argument("--cpu-block-stride", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--clock-preroll", type=float, default=0.6, help="seconds of untimed load before the timed frames")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
+                    help="c2: the BASELINE metric's frame (default, the driver's line); c4: 32^3 lattice of "
+                         "64-wide MLPs at 1920x1080; c5: 2^26-point bulk query (extra measurements)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,6 +305,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.workload == "c5":
+        return run_bulk(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
@@ -229,8 +317,12 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    aabb, grid, occ, cams = build_inputs(gf)
-    cam = cams[rank % len(cams)]
+    if args.workload == "c4":
+        aabb, grid, occ, cam = build_c4(gf)
+    else:
+        aabb, grid, occ, cams = build_inputs(gf)
+        cam = cams[rank % len(cams)]
+    n_pix = cam.width * cam.height
     cfg = gf.RenderConfig()
     precision = args.precision
     if precision is None:
@@ -242,11 +334,11 @@ def main():
     grid.precision = precision
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    gathered = torch.empty((world, SIZE * SIZE, 3), dtype=torch.float32, device="cuda") if world > 1 else None
-    out = torch.empty((SIZE * SIZE, 3), dtype=torch.float32, device="cuda")
+    gathered = torch.empty((world, n_pix, 3), dtype=torch.float32, device="cuda") if world > 1 else None
+    out = torch.empty((n_pix, 3), dtype=torch.float32, device="cuda")
     stats = torch.zeros(4, dtype=torch.int64, device="cuda")
     ws = torch.empty(N.lib().gf_render_workspace_bytes(grid.native_arch(), grid.native_geom(), cfg.native(0),
-                                                       SIZE * SIZE), dtype=torch.uint8, device="cuda")
+                                                       n_pix), dtype=torch.uint8, device="cuda")
 
     def step():
         stats.zero_()
@@ -286,7 +378,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * SIZE * SIZE / (ms * 1e-3) / 1e6
+    value = world * n_pix / (ms * 1e-3) / 1e6
     queries = int(stats[0].item())
 
     # ---- stage breakdown + roofline (separate frames with stage events on)
@@ -303,12 +395,12 @@ def main():
     st_n = {k: v // n_prof for k, v in st_n.items()}
     peaks, peak_src = load_peaks()
     flops_per_q = gf.count_flops(grid.arch)
-    R, Q, rounds = SIZE * SIZE, queries, (cfg.k + cfg.ert_chunk - 1) // cfg.ert_chunk
+    R, Q, rounds = n_pix, queries, (cfg.k + cfg.ert_chunk - 1) // cfg.ert_chunk
     cell_bytes = 2 * grid.arch.parameter_count() if precision == "fp16" else 4 * grid.arch.parameter_count()
     algo = {  # SURVEY.md §8(d) per-unit figures x units per frame
         "mlp_flop": Q * flops_per_q,
-        "mlp_bytes": Q * 36 + 791 * cell_bytes,
-        "march_bytes": Q * 40 + R * 12 + R * 16 * rounds + (256 ** 3) // 8,
+        "mlp_bytes": Q * 36 + (791 if args.workload == "c2" else grid.n_cells) * cell_bytes,
+        "march_bytes": Q * 40 + R * 12 + R * 16 * rounds + int(np.prod(occ.resolution)) // 8,
         "scatter_bytes": Q * 20,
     }
     mlp_tflops = algo["mlp_flop"] / (st_ms["mlp"] * 1e-3) / 1e12 if st_ms["mlp"] > 0 else 0.0
@@ -357,13 +449,13 @@ def main():
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": world * SIZE * SIZE / e2e_s / 1e6, "unit": UNIT,
+    e2e = {"value": world * n_pix / e2e_s / 1e6, "unit": UNIT,
            "h2d_bytes_per_step": int(N.C.sizeof(N.CameraT) + N.C.sizeof(N.MarchCfg)),
            "d2h_bytes_per_step": int(img.nbytes + 32), "ms_per_frame": e2e_s * 1e3}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
         os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
         workers = cpu_workers()
         dt, rays, _ = cpu_render_sample(cam, args.cpu_block_stride, workers)
@@ -377,7 +469,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f16" if precision == "fp16" else "f32",
             "data": "synthetic (random-init 16^3 lattice, analytic toy-scene occupancy)",
-            "config": workload_desc(precision),
+            "config": workload_desc(precision) if args.workload == "c2" else c4_desc(precision),
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "queries_per_frame": queries, "mlp_samples_per_s": queries / (st_ms["mlp"] * 1e-3) if st_ms["mlp"] else None,
