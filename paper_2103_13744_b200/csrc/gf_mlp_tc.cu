@@ -48,26 +48,32 @@ struct TcShape {
   static constexpr int K2 = W, N2 = ((W + 1 + 15) / 16) * 16;  // feature (rows 0..W-1) + density (row W)
   static constexpr int K3 = ((W + D + 15) / 16) * 16, N3 = W;  // direction [feat, gamma(d)] -> W
   static constexpr int K4 = W, N4 = 16;                        // color W -> 3 (rows 0..2)
-  // operand byte offsets (fp16, canonical K-major no-swizzle)
+  // weight operand byte offsets (fp16, canonical K-major no-swizzle)
   static constexpr int B0 = 0;
   static constexpr int B1 = B0 + N0 * K0 * 2;
   static constexpr int B2 = B1 + N1 * K1 * 2;
   static constexpr int B3 = B2 + N2 * K2 * 2;
   static constexpr int B4 = B3 + N3 * K3 * 2;
-  static constexpr int BIAS = B4 + N4 * K4 * 2;  // fp32 biases
-  static constexpr int BB0 = 0, BB1 = N0, BB2 = N0 + N1, BB3 = N0 + N1 + N2, BB4 = N0 + N1 + N2 + N3;
-  static constexpr int N_BIAS = N0 + N1 + N2 + N3 + N4;
-  static constexpr int CELL_BYTES = ((BIAS + N_BIAS * 4) + 127) / 128 * 128;
-  // per tile slot: A0 holds gamma(x) (128 x K0), later [feat, gamma(d)]
-  // (128 x K3) once the trunk0 MMA has consumed gamma(x); A1 holds h0/h1/g.
-  static constexpr int KA0 = K0 > K3 ? K0 : K3;
-  static constexpr int SLOT_BYTES = 128 * KA0 * 2 + 128 * W * 2;
-  static constexpr int A0(int s) { return CELL_BYTES + s * SLOT_BYTES; }
-  static constexpr int A1(int s) { return CELL_BYTES + s * SLOT_BYTES + 128 * KA0 * 2; }
-  static constexpr int BAR = CELL_BYTES + 2 * SLOT_BYTES;  // mma[0], mma[1], weights, tmem base
+  // bias operands: one K=16 tile per layer, row n = [hi(b_n), lo(b_n), 0 ...]
+  // (fp16 hi + fp16 remainder: 22 significant bits); multiplied by the
+  // constant ONES tile (columns 0 and 1 = 1) they initialise the accumulator
+  static constexpr int BB0 = B4 + N4 * K4 * 2;
+  static constexpr int BB1 = BB0 + N0 * 32;
+  static constexpr int BB2 = BB1 + N1 * 32;
+  static constexpr int BB3 = BB2 + N2 * 32;
+  static constexpr int BB4 = BB3 + N3 * 32;
+  static constexpr int CELL_BYTES = ((BB4 + N4 * 32) + 1023) / 1024 * 1024;
+  static constexpr int ONES = CELL_BYTES;  // 128 x 16 fp16 constant A operand
+  // one A operand slot per tile, re-laid out in place layer by layer:
+  // gamma(x) (K0) -> h0 (K1) -> h1 (K2) -> [feat, gamma(d)] (K3) -> g (K4)
+  static constexpr int KA = K0 > K3 ? K0 : K3;
+  static constexpr int SLOT_BYTES = 128 * KA * 2;
+  static constexpr int A(int s) { return ONES + 4096 + s * SLOT_BYTES; }
+  static constexpr int BAR = A(2);  // mma[0], mma[1], weights, tmem base
   static constexpr int SMEM = BAR + 32;
   static constexpr int NC = N2 <= 32 ? 32 : (N2 <= 64 ? 64 : (N2 <= 128 ? 128 : 256));  // TMEM cols per slot
   static constexpr int TMEM_COLS = 2 * NC;
+  static constexpr int CTAS_PER_SM = W == 32 ? 4 : 2;
 };
 
 // byte offset of element (r, k) in a canonical K-major no-swizzle operand of
@@ -151,21 +157,14 @@ __device__ __forceinline__ void tmem_load(uint32_t taddr, float* out) {
   for (int c = 0; c < N; ++c) out[c] = __uint_as_float(r[c]);
 }
 
-// bias add (+ReLU) and fp16 store of accumulator columns [0, N) of row r into
-// a canonical operand at K-offset k0: per 8 columns two 16-byte broadcast
-// bias loads, four FADD2, four F2FP(.RELU) packs and one 16-byte store.
+// fp16 store (+ReLU) of accumulator columns [0, N) of row r into a
+// canonical operand of K columns: per 8 columns four F2FP(.RELU) packs and
+// one 16-byte store (the bias is already in the accumulator)
 template <int N, bool RELU>
-__device__ __forceinline__ void bias_pack_store(float* h, const float* __restrict__ b, uint8_t* A, int K, int r,
-                                                int k0) {
-  const float4* b4 = reinterpret_cast<const float4*>(b);
+__device__ __forceinline__ void pack_store(const float* h, uint8_t* A, int K, int r) {
 #pragma unroll
   for (int c = 0; c < N / 8; ++c) {
-    const float4 p = b4[2 * c], q = b4[2 * c + 1];
-    float* v = h + 8 * c;
-    fadd2(v[0], v[1], p.x, p.y);
-    fadd2(v[2], v[3], p.z, p.w);
-    fadd2(v[4], v[5], q.x, q.y);
-    fadd2(v[6], v[7], q.z, q.w);
+    const float* v = h + 8 * c;
     uint4 o;
     if (RELU) {
       o = make_uint4(pack_h2_relu(v[0], v[1]), pack_h2_relu(v[2], v[3]), pack_h2_relu(v[4], v[5]),
@@ -173,7 +172,7 @@ __device__ __forceinline__ void bias_pack_store(float* h, const float* __restric
     } else {
       o = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
     }
-    *reinterpret_cast<uint4*>(A + canon_off(r, k0 + 8 * c, K)) = o;
+    *reinterpret_cast<uint4*>(A + canon_off(r, 8 * c, K)) = o;
   }
 }
 
@@ -261,14 +260,14 @@ __device__ __forceinline__ void store_direction(uint8_t* A3, int tid, const uint
 // the kernel
 // ---------------------------------------------------------------------------
 template <int W, class IO>
-__global__ void __launch_bounds__(256, W == 32 ? 3 : 1) k_mlp_tc(const uint8_t* __restrict__ packed, TileSched S, IO io) {
+__global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const uint8_t* __restrict__ packed,
+                                                                         TileSched S, IO io) {
   using T = TcShape<W>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const float* sbias = reinterpret_cast<const float*>(smem + T::BIAS);
   const uint32_t bar0 = smem_u32(smem + T::BAR), bar_w = bar0 + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + T::BAR + 24);
   const int tid = threadIdx.x, warp = tid >> 5;
-  // two warpgroups: group g owns tile slot g (its A operands, its TMEM
+  // two warpgroups: group g owns tile slot g (its A operand, its TMEM
   // columns, its commit barrier); row gt of the tile is TMEM lane gt
   const int g = tid >> 7, gt = tid & 127;
 
@@ -283,13 +282,18 @@ __global__ void __launch_bounds__(256, W == 32 ? 3 : 1) k_mlp_tc(const uint8_t* 
     mbar_init(bar_w, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  {  // constant bias multiplier: row r = [1, 1, 0 ... 0]
+    const int r = tid >> 1, c = tid & 1;
+    *reinterpret_cast<uint4*>(smem + T::ONES + canon_off(r, 8 * c, 16)) =
+        c ? make_uint4(0u, 0u, 0u, 0u) : make_uint4(0x3C003C00u, 0u, 0u, 0u);
+  }
+  fence_async_smem();
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t wb = smem_u32(smem);
-  uint8_t* A0 = smem + T::A0(g);
-  uint8_t* A1 = smem + T::A1(g);
+  uint8_t* Ag = smem + T::A(g);
   const uint32_t trow = tmem + g * T::NC + ((uint32_t)((warp & 3) * 32) << 16);  // lane quarter of this warp
 
   const uint32_t nt = *S.n_tiles;
@@ -298,18 +302,19 @@ __global__ void __launch_bounds__(256, W == 32 ? 3 : 1) k_mlp_tc(const uint8_t* 
   int cur = -1;
   uint32_t ph = 0, ph_w = 0;
 
-  // MMA issue for layer L of this group's slot (thread gt == 0 of the group)
+  // MMA chain of layer L for this group's slot (thread gt == 0 of the group):
+  // bias tile first (accumulator := bias), then the K steps
   auto issue = [&](int L) {
     if (gt != 0) return;
-    const uint32_t a0 = wb + T::A0(g), a1 = wb + T::A1(g), d = tmem + g * T::NC;
-    uint32_t a = a1, b = wb + T::B1, idesc = idesc_f16(128, T::N1);
+    const uint32_t a = wb + T::A(g), d = tmem + g * T::NC;
+    uint32_t b = wb + T::B1, bb = wb + T::BB1, idesc = idesc_f16(128, T::N1);
     int K = T::K1;
-    if (L == 0) { a = a0; b = wb + T::B0; K = T::K0; idesc = idesc_f16(128, T::N0); }
-    if (L == 2) { b = wb + T::B2; K = T::K2; idesc = idesc_f16(128, T::N2); }
-    if (L == 3) { a = a0; b = wb + T::B3; K = T::K3; idesc = idesc_f16(128, T::N3); }
-    if (L == 4) { b = wb + T::B4; K = T::K4; idesc = idesc_f16(128, T::N4); }
-    for (int ks = 0; ks < K / 16; ++ks)
-      mma_f16(d, umma_desc(a + ks * 256, K), umma_desc(b + ks * 256, K), idesc, ks > 0 ? 1u : 0u);
+    if (L == 0) { b = wb + T::B0; bb = wb + T::BB0; K = T::K0; idesc = idesc_f16(128, T::N0); }
+    if (L == 2) { b = wb + T::B2; bb = wb + T::BB2; K = T::K2; idesc = idesc_f16(128, T::N2); }
+    if (L == 3) { b = wb + T::B3; bb = wb + T::BB3; K = T::K3; idesc = idesc_f16(128, T::N3); }
+    if (L == 4) { b = wb + T::B4; bb = wb + T::BB4; K = T::K4; idesc = idesc_f16(128, T::N4); }
+    mma_f16(d, umma_desc(wb + T::ONES, 16), umma_desc(bb, 16), idesc, 0u);
+    for (int ks = 0; ks < K / 16; ++ks) mma_f16(d, umma_desc(a + ks * 256, K), umma_desc(b + ks * 256, K), idesc, 1u);
     mma_commit(bar0 + 8 * g);
   };
   auto wait_mma = [&]() {
@@ -347,13 +352,13 @@ __global__ void __launch_bounds__(256, W == 32 ? 3 : 1) k_mlp_tc(const uint8_t* 
     const bool two = pair_second(S, t, t_end, cell);
     const uint32_t t_next = t + (two ? 2 : 1);
     const bool active = g == 0 || two;
-    __syncthreads();  // previous pair fully retired (bias reads, weight operands)
+    __syncthreads();  // previous pair fully retired (weight operands may be replaced)
     const bool new_cell = (int)cell != cur;
     if (new_cell && tid == 0) bulk_load(wb, packed + (size_t)cell * T::CELL_BYTES, T::CELL_BYTES, bar_w);
     cur = (int)cell;
     const RowIn row = nxt;
     if (active) {
-      encode_position<W>(A0, gt, row.x);
+      encode_position<W>(Ag, gt, row.x);
       publish();
     }
     if (new_cell) {
@@ -361,45 +366,44 @@ __global__ void __launch_bounds__(256, W == 32 ? 3 : 1) k_mlp_tc(const uint8_t* 
       ph_w ^= 1;
     }
     if (active) issue(0);
-    uint4 de[4];  // direction operand chunk of this row, fetched while trunk0 runs
-    if (active && IO::kDirEnc) fetch_direction<W>(io, row, de);
     {  // prefetch this group's row of the next pair while trunk0 runs
       uint2 tn;
       if (my_tile(t_next, tn)) load_row(S, io, tn, gt, nxt);
     }
     if (active) {
       float sigma = 0.f;
+      uint4 de[4];  // direction operand chunk, fetched one layer ahead of its use
 #pragma unroll
       for (int L = 0; L < 5; ++L) {
+        if (L == 1) fetch_direction<W>(io, row, de);
         wait_mma();
-        if (L == 0) {  // trunk0 -> A1; gamma(x) is dead, gamma(d) -> A0 as [., gamma(d)]
+        if (L == 0) {  // trunk0 -> h0 (K1 layout, over the dead gamma(x))
           float h[W];
           tmem_load<W>(trow, h);
-          bias_pack_store<W, true>(h, sbias + T::BB0, A1, W, gt, 0);
-          if (!IO::kDirEnc) fetch_direction<W>(io, row, de);
-          store_direction<W>(A0, gt, de);
-        } else if (L == 1) {  // trunk1 -> A1
+          pack_store<W, true>(h, Ag, T::K1, gt);
+        } else if (L == 1) {  // trunk1 -> h1 (K2 layout)
           float h[W];
           tmem_load<W>(trow, h);
-          bias_pack_store<W, true>(h, sbias + T::BB1, A1, W, gt, 0);
-        } else if (L == 2) {  // feature (cols 0..W-1, unactivated) + density (col W)
+          pack_store<W, true>(h, Ag, T::K2, gt);
+        } else if (L == 2) {  // feature (cols 0..W-1, unactivated) + density (col W) -> [feat, gamma(d)] (K3)
           float h[W];
           tmem_load<W>(trow, h);
-          bias_pack_store<W, false>(h, sbias + T::BB2, A0, T::K3, gt, 0);
+          pack_store<W, false>(h, Ag, T::K3, gt);
+          store_direction<W>(Ag, gt, de);
           float z[16];
           tmem_load<16>(trow + W, z);
-          sigma = fmaxf(z[0] + sbias[T::BB2 + W], 0.f);
-        } else if (L == 3) {  // direction -> A1
+          sigma = fmaxf(z[0], 0.f);
+        } else if (L == 3) {  // direction -> g (K4 layout)
           float h[W];
           tmem_load<W>(trow, h);
-          bias_pack_store<W, true>(h, sbias + T::BB3, A1, W, gt, 0);
+          pack_store<W, true>(h, Ag, T::K4, gt);
         } else {  // color: sigmoid
           float z[16];
           tmem_load<16>(trow, z);
           float rgb[3];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const float v = z[c] + sbias[T::BB4 + c];
+            const float v = z[c];
             const float e = __expf(-fabsf(v)), r = __fdividef(1.f, 1.f + e);  // sign-split sigmoid (mlp.py:228-235)
             rgb[c] = v >= 0.f ? r : e * r;
           }
@@ -462,22 +466,28 @@ __global__ void k_pack_tc(PackArgsTc A, int64_t n_cells, uint8_t* packed) {
     int n = j / T::K4, k = j % T::K4;
     put(T::B4, T::K4, n, k, n < 3 ? w(5, n, k, 3, W) : 0.f);
   }
-  float* bias = reinterpret_cast<float*>(dst + T::BIAS);
-  for (int j = threadIdx.x; j < T::N_BIAS; j += blockDim.x) {
-    float v = 0.f;
-    if (j < T::BB1) v = A.b[0][cell * W + j];
-    else if (j < T::BB2) v = A.b[1][cell * W + (j - T::BB1)];
-    else if (j < T::BB3) {
-      int c = j - T::BB2;
-      v = c < W ? A.b[3][cell * W + c] : (c == W ? A.b[2][cell] : 0.f);
-    } else if (j < T::BB4) v = A.b[4][cell * W + (j - T::BB3)];
-    else {
-      int c = j - T::BB4;
-      v = c < 3 ? A.b[5][cell * 3 + c] : 0.f;
+  // bias tiles: row n of layer L = [hi, lo, 0 ...] with hi = fp16(b), lo = fp16(b - hi)
+  auto bias_of = [&](int L, int n) -> float {
+    if (L == 0) return n < W ? A.b[0][cell * W + n] : 0.f;
+    if (L == 1) return n < W ? A.b[1][cell * W + n] : 0.f;
+    if (L == 2) return n < W ? A.b[3][cell * W + n] : (n == W ? A.b[2][cell] : 0.f);  // feature, then density
+    if (L == 3) return n < W ? A.b[4][cell * W + n] : 0.f;
+    return n < 3 ? A.b[5][cell * 3 + n] : 0.f;
+  };
+  const int bb[5] = {T::BB0, T::BB1, T::BB2, T::BB3, T::BB4}, nn[5] = {T::N0, T::N1, T::N2, T::N3, T::N4};
+  for (int L = 0; L < 5; ++L) {
+    for (int j = threadIdx.x; j < nn[L] * 16; j += blockDim.x) {
+      const int n = j / 16, k = j % 16;
+      float v = 0.f;
+      if (k < 2) {
+        const float b = bias_of(L, n);
+        const float hi = __half2float(__float2half_rn(b));
+        v = k == 0 ? hi : b - hi;
+      }
+      put(bb[L], 16, n, k, v);
     }
-    bias[j] = v;
   }
-  for (int j = T::BIAS + T::N_BIAS * 4 + threadIdx.x; j < T::CELL_BYTES; j += blockDim.x) dst[j] = 0;
+  for (int j = T::BB4 + T::N4 * 32 + threadIdx.x; j < T::CELL_BYTES; j += blockDim.x) dst[j] = 0;
 }
 
 static bool tc_supported(const LayerTable& t) {
