@@ -14,7 +14,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libgridfield_b200.so"
+LIB_PATH = Path(os.environ.get("GF_LIB_PATH") or Path(__file__).resolve().parent / "_lib" / "libgridfield_b200.so")
 
 GF_OK, GF_ERR_INVALID, GF_ERR_CUDA, GF_ERR_WORKSPACE, GF_ERR_UNSUPPORTED = range(5)
 PRECISION = {"fp32": 0, "fp16": 1}

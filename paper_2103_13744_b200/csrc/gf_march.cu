@@ -429,21 +429,33 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
       if ((int)lane >= o) incl += v;
     }
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31), excl = incl - nr;
-    for (uint32_t b0 = 0; b0 < total; b0 += 32) {
-      const uint32_t q = b0 + lane;
-      int own = 0;  // smallest lane whose inclusive count exceeds q
+    // U records per lane per pass: U independent loads in flight per lane
+    constexpr int U = 4;
+    for (uint32_t b0 = 0; b0 < total; b0 += 32 * U) {
+      float4 r[U];
+      uint32_t src[U];
+      bool ok[U];
 #pragma unroll
-      for (int st = 16; st; st >>= 1) {
-        const uint32_t v = __shfl_sync(0xffffffffu, incl, own + st - 1);
-        if (v <= q) own += st;
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = b0 + 32 * u + lane;
+        int own = 0;  // smallest lane whose inclusive count exceeds q
+#pragma unroll
+        for (int st = 16; st; st >>= 1) {
+          const uint32_t v = __shfl_sync(0xffffffffu, incl, own + st - 1);
+          if (v <= q) own += st;
+        }
+        const uint32_t j = q - __shfl_sync(0xffffffffu, excl, own);
+        const uint32_t i_o = __shfl_sync(0xffffffffu, i, own);
+        ok[u] = q < total;
+        src[u] = i_o * (uint32_t)stride + j;  // staging index (< 2^32, checked on the host)
+        if (ok[u]) r[u] = RB.rec[src[u]];
       }
-      const uint32_t j = q - __shfl_sync(0xffffffffu, excl, own);
-      const uint32_t i_o = __shfl_sync(0xffffffffu, i, own);
-      if (q < total) {
-        const uint64_t src = (uint64_t)i_o * (uint64_t)stride + j;
-        const float4 r = RB.rec[src];
-        const uint32_t cell = gf_flat_cell(grid, r.x, r.y, r.z);
-        Bk.srec[off[cell] + __float_as_uint(r.w)] = make_float4(r.x, r.y, r.z, __uint_as_float((uint32_t)src));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (ok[u]) {
+          const uint32_t cell = gf_flat_cell(grid, r[u].x, r[u].y, r[u].z);
+          Bk.srec[off[cell] + __float_as_uint(r[u].w)] = make_float4(r[u].x, r[u].y, r[u].z, __uint_as_float(src[u]));
+        }
       }
     }
   }

@@ -115,13 +115,15 @@ __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
 
+// parity wait with a suspend-time hint: the warp sleeps in the barrier unit
+// until the phase flips (or the hint expires) instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   uint32_t done;
   do {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(done)
-        : "r"(bar), "r"(phase)
+        : "r"(bar), "r"(phase), "r"(1000000u)
         : "memory");
   } while (!done);
 }
@@ -305,6 +307,10 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
   // MMA chain of layer L for this group's slot (thread gt == 0 of the group):
   // bias tile first (accumulator := bias), then the K steps
   auto issue = [&](int L) {
+#if GF_EXP == 3
+    if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar0 + 8 * g) : "memory");
+    return;
+#endif
     if (gt != 0) return;
     const uint32_t a = wb + T::A(g), d = tmem + g * T::NC;
     uint32_t b = wb + T::B1, bb = wb + T::BB1, idesc = idesc_f16(128, T::N1);
@@ -358,7 +364,11 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
     cur = (int)cell;
     const RowIn row = nxt;
     if (active) {
+#if GF_EXP == 1
+      for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(Ag + canon_off(gt, 8 * c, T::K0)) = make_uint4(__float_as_uint(row.x[0]), 0u, 0u, 0u);
+#else
       encode_position<W>(Ag, gt, row.x);
+#endif
       publish();
     }
     if (new_cell) {
@@ -375,7 +385,6 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
       uint4 de[4];  // direction operand chunk, fetched one layer ahead of its use
 #pragma unroll
       for (int L = 0; L < 5; ++L) {
-        if (L == 1) fetch_direction<W>(io, row, de);
         wait_mma();
         if (L == 0) {  // trunk0 -> h0 (K1 layout, over the dead gamma(x))
           float h[W];
@@ -385,11 +394,12 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
           float h[W];
           tmem_load<W>(trow, h);
           pack_store<W, true>(h, Ag, T::K2, gt);
+          fetch_direction<W>(io, row, de);  // in flight while the L2 MMA runs
         } else if (L == 2) {  // feature (cols 0..W-1, unactivated) + density (col W) -> [feat, gamma(d)] (K3)
+          store_direction<W>(Ag, gt, de);
           float h[W];
           tmem_load<W>(trow, h);
           pack_store<W, false>(h, Ag, T::K3, gt);
-          store_direction<W>(Ag, gt, de);
           float z[16];
           tmem_load<16>(trow + W, z);
           sigma = fmaxf(z[0], 0.f);
