@@ -330,6 +330,7 @@ struct RenderWs {
   u128* jump;
   u128* start;
   u128* round_jump;
+  u128* block_ci;
   RayState R;
   RoundBufs RB;
   BucketBufs B;
@@ -348,6 +349,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->jump = c.take<u128>((size_t)2 * (GF_JUMP_MAX + 1));
   w->start = c.take<u128>((size_t)2 * GF_RAY_BLOCK);
   w->round_jump = c.take<u128>((size_t)4 * n_rounds);
+  w->block_ci = c.take<u128>((size_t)GF_CI_N * n_blocks);
   w->coarse_tmp = c.take<uint8_t>((size_t)kMaxCoarseCells);
   w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->R.org = c.take<float4>((size_t)n_rays);
@@ -442,6 +444,21 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   P.jump = w.jump;
   P.start = w.start;
   P.round_jump = w.round_jump;
+  P.block_ci = w.block_ci;
+  // the network cell of a sample follows from its occupancy cell when both
+  // grids bin exactly in float32 over the same box and each network cell is
+  // 2^s occupancy cells per axis (power-of-two scaling keeps floor exact)
+  if (occ_bits && P.grid.fast && P.occ.fast) {
+    bool ok = true;
+    for (int a = 0; a < 3 && ok; ++a) {
+      ok = occ->b_min[a] == grid->b_min[a] && occ->b_max[a] == grid->b_max[a] && occ->res[a] % grid->res[a] == 0;
+      int q = ok ? occ->res[a] / grid->res[a] : 0, sh = 0;
+      while (ok && (1 << sh) < q) ++sh;
+      ok = ok && (1 << sh) == q;
+      P.net_shift[a] = sh;
+    }
+    P.net_from_occ = ok ? 1 : 0;
+  }
   P.k = cfg->k;
   P.chunk = cfg->ert_chunk;
   P.n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
@@ -564,7 +581,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
     if (P.stratified)
       k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(std::max<int64_t>({n_blocks, (int64_t)GF_RAY_BLOCK, 2ll * P.n_rounds}), 64),
                       64, 0, s>>>(cfg->seed, first_block, ray_block_stride, n_blocks, cfg->k, cfg->ert_chunk, P.n_rounds,
-                                  w.seeds, w.jump, w.start, w.round_jump);
+                                  w.seeds, w.jump, w.start, w.round_jump, w.block_ci);
     k_ray_init<<<ray_blocks, 128, 0, s>>>(P, w.R);
     stage_mark(s, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
     for (int r = 0; r < P.n_rounds; ++r) {

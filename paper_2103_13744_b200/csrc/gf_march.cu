@@ -20,7 +20,7 @@ namespace gf {
 // -------------------------------------------------------------------------
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
                               int k, int chunk, int n_rounds, u128* seeds, u128* jump, u128* start,
-                              u128* round_jump) {
+                              u128* round_jump, u128* block_ci) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b == 0) {
     // LCG jump table: S_{n+d} = A^d S_n + (sum_{k<d} A^k) inc, d = 0..GF_JUMP_MAX
@@ -52,6 +52,11 @@ __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_
   gf_seed_block(seed, (uint64_t)((first_block + b * block_stride) * GF_RAY_BLOCK), &s, &inc);
   seeds[2 * b] = s;
   seeds[2 * b + 1] = inc;
+  u128 c = 0;  // sum_{k<d} A^k
+  for (int d = 0; d < GF_CI_N; ++d) {
+    block_ci[b * GF_CI_N + d] = c * inc;
+    c = c * GF_PCG_MULT + 1;
+  }
 }
 
 // -------------------------------------------------------------------------
@@ -585,11 +590,13 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
   u128 S = 0, inc = 0;
   uint64_t outw = 0;
   uint64_t draw = 0;
+  uint32_t blk = 0;
   if (P.stratified && active) {
     // state of the word holding this round's first draw: a tabulated jump
     // from the ray's slot-0 state (R.rng stays read-only)
     const int64_t g = global_ray(P, i);
-    inc = P.block_seeds[2 * seed_slot(P, g) + 1];
+    blk = (uint32_t)seed_slot(P, g);
+    inc = P.block_seeds[2 * blk + 1];
     const uint64_t draw0 = (uint64_t)(g % GF_RAY_BLOCK) * (uint64_t)P.k;
     const int jr = 2 * (2 * round + (int)(draw0 & 1));
     S = ldg_u128(&P.round_jump[jr]) * R.rng[i] + ldg_u128(&P.round_jump[jr + 1]) * inc;
@@ -628,9 +635,10 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     // shared memory (broadcast when several lanes share a ray).
     struct RayPar {
       float4 o, d;      // origin + t0, direction + seg
-      uint4 S, I;       // PCG64 state at draw d0 (rounded down to a word), increment
+      uint4 S;          // PCG64 state at draw d0 (rounded down to a word)
       uint32_t i, d0;   // call-local ray index, float32 draw index of slot s0
-      uint32_t carry, pad;
+      uint32_t carry;   // kept samples so far this round
+      uint32_t blk;     // the ray's slot in the per-block tables (seeds, C^d * inc)
     };
     __shared__ RayPar s_ray[4][32];
     __shared__ uint16_t s_list[4][32 * 32];
@@ -652,7 +660,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       rp.o = o;
       rp.d = d;
       rp.S = make_uint4((uint32_t)S, (uint32_t)(S >> 32), (uint32_t)(S >> 64), (uint32_t)(S >> 96));
-      rp.I = make_uint4((uint32_t)inc, (uint32_t)(inc >> 32), (uint32_t)(inc >> 64), (uint32_t)(inc >> 96));
+      rp.blk = blk;
       rp.i = (uint32_t)i;
       rp.d0 = d0;
       rp.carry = 0;
@@ -680,12 +688,12 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
         i_o = rp.i;
         if (P.stratified) {
           const uint32_t d0_o = rp.d0;
-          const uint4 sv = rp.S, iv = rp.I;
+          const uint4 sv = rp.S;
           const u128 So = ((u128)(((uint64_t)sv.w << 32) | sv.z) << 64) | (((uint64_t)sv.y << 32) | sv.x);
-          const u128 Io = ((u128)(((uint64_t)iv.w << 32) | iv.z) << 64) | (((uint64_t)iv.y << 32) | iv.x);
           const uint32_t dd = d0_o + (uint32_t)j;
           const uint32_t delta = (dd >> 1) - (d0_o >> 1);
-          const u128 Sj = ldg_u128(&P.jump[2 * delta]) * So + ldg_u128(&P.jump[2 * delta + 1]) * Io;
+          // S_delta = A^delta S + (sum_{k<delta} A^k) inc; the second term is tabulated per block
+          const u128 Sj = ldg_u128(&P.jump[2 * delta]) * So + ldg_u128(&P.block_ci[(size_t)rp.blk * GF_CI_N + delta]);
           const uint64_t w = gf_pcg_output(Sj);
           const uint32_t u = (dd & 1) ? (uint32_t)(w >> 32) : (uint32_t)w;
           jit = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, (int)(u >> 8)), 4503599627370496.0),
@@ -711,11 +719,21 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
           pz = gf_clip_component(pz, P.grid.b_min[2], P.grid.b_max[2]);
         }
         keep = true;
-        if (P.occ_bits) {
-          const uint32_t f = gf_flat_cell(P.occ, px, py, pz);
+        if (P.net_from_occ) {  // both grids fast, same box, occupancy cells nest 2^s per network cell
+          const int ox = gf_bin_axis_fast(P.occ, 0, px), oy = gf_bin_axis_fast(P.occ, 1, py),
+                    oz = gf_bin_axis_fast(P.occ, 2, pz);
+          const uint32_t f = (uint32_t)(ox + P.occ.res[0] * (oy + P.occ.res[1] * oz));
           keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
+          cell = (uint32_t)((ox >> P.net_shift[0]) +
+                            P.grid.res[0] * ((oy >> P.net_shift[1]) + P.grid.res[1] * (oz >> P.net_shift[2])));
+        } else {
+          if (P.occ_bits) {
+            const uint32_t f = gf_flat_cell(P.occ, px, py, pz);
+            keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
+          }
+          if (keep) cell = gf_flat_cell(P.grid, px, py, pz);
         }
-        if (keep) cell = gf_flat_cell(P.grid, px, py, pz);
+        if (!keep) cell = 0;
       }
       // position of this sample in its ray's run: kept items of the same ray
       // earlier in this batch + kept items of earlier batches

@@ -26,6 +26,9 @@ struct MarchParams {
   const u128* jump;         // [2*d] A^d, [2*d+1] sum_{k<d} A^k  (d <= GF_JUMP_MAX)
   const u128* start;        // [2*r], [2*r+1]: the same pair for the jump to block row r's first draw
   const u128* round_jump;   // [2*(2*round+parity)], +1: jump from a ray's slot-0 word to round's first word
+  const u128* block_ci;     // [b*GF_CI_N + d] = (sum_{k<d} A^k) * inc_b: the increment part of a d-word jump
+  int net_from_occ;         // network cell = occupancy cell >> net_shift per axis (see gf_api.cu)
+  int net_shift[3];
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
   int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
   int64_t n_cells;
@@ -89,6 +92,7 @@ __device__ __forceinline__ int64_t seed_slot(const MarchParams& P, int64_t g) {
 }
 
 #define GF_JUMP_MAX 32  // largest PCG64 jump inside one round (chunk <= 32 -> <= 16 outputs)
+#define GF_CI_N 17      // per-block increment terms for jumps of 0..16 words
 
 // K2 for the render path (fused scan + tile list + rank-based placement);
 // returns the number of launches it made
@@ -97,7 +101,7 @@ void launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, 
 
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
                               int k, int chunk, int n_rounds, u128* seeds, u128* jump, u128* start,
-                              u128* round_jump);
+                              u128* round_jump, u128* block_ci);
 __global__ void k_ray_init(MarchParams P, RayState R);
 __global__ void k_coarse_reduce(const uint8_t* occ_bits, int3 occ_res, int factor, int3 cres, uint8_t* coarse);
 __global__ void k_coarse_dilate(const uint8_t* coarse, int3 cres, int radius, uint32_t* bits);
