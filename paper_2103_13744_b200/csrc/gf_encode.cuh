@@ -42,6 +42,63 @@ __device__ __forceinline__ void sincos_scaled(float x, int k, float* s, float* c
   __sincosf(r, s, c);
 }
 
+// ---- packed float32 pairs (FMUL2 / FADD2 / FFMA2 on sm_100): each lane of
+// the pair is the same IEEE round-to-nearest operation as the scalar form
+struct F2 {
+  unsigned long long v;
+};
+__device__ __forceinline__ F2 f2(float a, float b) {
+  F2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r.v) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_split(F2 p, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(p.v)); }
+__device__ __forceinline__ F2 f2_mul(F2 a, F2 b) {
+  F2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_add(F2 a, F2 b) {
+  F2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_sub(F2 a, F2 b) {
+  F2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) {
+  F2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+  return r;
+}
+
+// sincos_scaled for two independent (value, octave) pairs at once: the
+// angle products and the 2pi reduction run as f32x2 (identical roundings:
+// rint(-t) == -rint(t) and fma(n', hi, a) with n' = -n is fmaf(-n, hi, a))
+__device__ __forceinline__ void sincos_scaled2(float x0, int k0, float x1, int k1, float* s0, float* c0, float* s1,
+                                               float* c1) {
+  const F2 a = f2_mul(f2(x0, x1), f2(__int_as_float(0x40490FDB + (k0 << 23)), __int_as_float(0x40490FDB + (k1 << 23))));
+  float t0, t1;
+  f2_split(f2_mul(a, f2(-0.15915494309189535f, -0.15915494309189535f)), t0, t1);
+  const F2 n = f2(rintf(t0), rintf(t1));
+  F2 r = f2_fma(n, f2(6.28125f, 6.28125f), a);
+  r = f2_fma(n, f2(1.9353071795864769e-3f, 1.9353071795864769e-3f), r);
+  float r0, r1;
+  f2_split(r, r0, r1);
+  __sincosf(r0, s0, c0);
+  __sincosf(r1, s1, c1);
+}
+
+// one double-angle step for two independent chains: s' = (s + s) c,
+// c' = (c - s)(c + s)
+__device__ __forceinline__ void double_angle2(F2& s, F2& c) {
+  const F2 s2 = f2_mul(f2_add(s, s), c);
+  c = f2_mul(f2_sub(c, s), f2_add(c, s));
+  s = s2;
+}
+
 // octaves k < L: MUFU anchors every third octave, double-angle steps in
 // between (max abs error 2.6e-6 vs 4.9e-4 fp16 operand rounding)
 template <int L>

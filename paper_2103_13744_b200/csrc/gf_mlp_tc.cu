@@ -208,35 +208,51 @@ __device__ __forceinline__ bool pair_second(const TileSched& S, uint32_t t, uint
 template <int W>
 __device__ __forceinline__ void encode_position(uint8_t* A0, int tid, const float* x) {
   using T = TcShape<W>;
+  // S[k][a], C[k][a] for the 10 octaves of the 3 axes.  Anchors k = 0, 3, 6, 9
+  // (MUFU after exact reduction), two double-angle steps after each of the
+  // first three; the 12 anchors and 9 chains are processed in f32x2 pairs.
+  float S[10][3], C[10][3];
+  sincos_scaled2(x[0], 0, x[1], 0, &S[0][0], &C[0][0], &S[0][1], &C[0][1]);
+  sincos_scaled2(x[2], 0, x[2], 3, &S[0][2], &C[0][2], &S[3][2], &C[3][2]);
+  sincos_scaled2(x[0], 3, x[1], 3, &S[3][0], &C[3][0], &S[3][1], &C[3][1]);
+  sincos_scaled2(x[0], 6, x[1], 6, &S[6][0], &C[6][0], &S[6][1], &C[6][1]);
+  sincos_scaled2(x[2], 6, x[2], 9, &S[6][2], &C[6][2], &S[9][2], &C[9][2]);
+  sincos_scaled2(x[0], 9, x[1], 9, &S[9][0], &C[9][0], &S[9][1], &C[9][1]);
+  // chains (octave of the anchor, axis) paired: (0x,0y) (0z,3x) (3y,3z) (6x,6y); 6z alone
+  const int ck[4][2] = {{0, 0}, {0, 3}, {3, 3}, {6, 6}}, ca[4][2] = {{0, 1}, {2, 0}, {1, 2}, {0, 1}};
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int k0 = ck[p][0], a0 = ca[p][0], k1 = ck[p][1], a1 = ca[p][1];
+    F2 s = f2(S[k0][a0], S[k1][a1]), c = f2(C[k0][a0], C[k1][a1]);
+#pragma unroll
+    for (int st = 1; st <= 2; ++st) {
+      double_angle2(s, c);
+      f2_split(s, S[k0 + st][a0], S[k1 + st][a1]);
+      f2_split(c, C[k0 + st][a0], C[k1 + st][a1]);
+    }
+  }
+#pragma unroll
+  for (int st = 1; st <= 2; ++st) {
+    const float sp = S[5 + st][2], cp = C[5 + st][2];
+    S[6 + st][2] = 2.0f * sp * cp;
+    C[6 + st][2] = (cp - sp) * (cp + sp);
+  }
+  // core.py:132-152 layout: raw xyz, then per octave sin xyz, cos xyz; col 63 = 0
   float e[64];
   e[0] = x[0]; e[1] = x[1]; e[2] = x[2];
-  float sp[3], cp[3];
 #pragma unroll
-  for (int k = 0; k < 10; ++k) {
+  for (int k = 0; k < 10; ++k)
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      float sk, ck;
-      if (k % 3 == 0) {
-        sincos_scaled(x[a], k, &sk, &ck);
-      } else {
-        sk = 2.0f * sp[a] * cp[a];
-        ck = (cp[a] - sp[a]) * (cp[a] + sp[a]);
-      }
-      sp[a] = sk;
-      cp[a] = ck;
-      e[3 + 6 * k + a] = sk;
-      e[6 + 6 * k + a] = ck;
+      e[3 + 6 * k + a] = S[k][a];
+      e[6 + 6 * k + a] = C[k][a];
     }
-    if (k == 9) e[63] = 0.f;
+  e[63] = 0.f;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int last = 8 * c + 7, hi = k == 9 ? 63 : 8 + 6 * k, lo = 8 + 6 * (k - 1);
-      if (last <= hi && last > lo) {
-        const float* v = e + 8 * c;
-        *reinterpret_cast<uint4*>(A0 + canon_off(tid, 8 * c, T::K0)) =
-            make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
-      }
-    }
+  for (int c = 0; c < 8; ++c) {
+    const float* v = e + 8 * c;
+    *reinterpret_cast<uint4*>(A0 + canon_off(tid, 8 * c, T::K0)) =
+        make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
   }
 }
 
