@@ -73,7 +73,11 @@ struct TcShape {
   static constexpr int SMEM = BAR + 32;
   static constexpr int NC = N2 <= 32 ? 32 : (N2 <= 64 ? 64 : (N2 <= 128 ? 128 : 256));  // TMEM cols per slot
   static constexpr int TMEM_COLS = 2 * NC;
+#if GF_EXP == 10
+  static constexpr int CTAS_PER_SM = W == 32 ? 3 : 2;
+#else
   static constexpr int CTAS_PER_SM = W == 32 ? 4 : 2;
+#endif
 };
 
 // byte offset of element (r, k) in a canonical K-major no-swizzle operand of
@@ -159,6 +163,30 @@ __device__ __forceinline__ void tmem_load(uint32_t taddr, float* out) {
   for (int c = 0; c < N; ++c) out[c] = __uint_as_float(r[c]);
 }
 
+// accumulator columns [c0, c0 + N) of this thread's TMEM row -> fp16 (+ReLU)
+// into a canonical operand of K columns, 16 columns per TMEM load so only 16
+// accumulator registers are live
+template <int N, bool RELU>
+__device__ __forceinline__ void tmem_to_operand(uint32_t trow, uint8_t* A, int K, int r) {
+#pragma unroll
+  for (int c = 0; c < N; c += 16) {
+    float h[16];
+    tmem_load<16>(trow + c, h);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const float* v = h + 8 * q;
+      uint4 o;
+      if (RELU) {
+        o = make_uint4(pack_h2_relu(v[0], v[1]), pack_h2_relu(v[2], v[3]), pack_h2_relu(v[4], v[5]),
+                       pack_h2_relu(v[6], v[7]));
+      } else {
+        o = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
+      }
+      *reinterpret_cast<uint4*>(A + canon_off(r, c + 8 * q, K)) = o;
+    }
+  }
+}
+
 // fp16 store (+ReLU) of accumulator columns [0, N) of row r into a
 // canonical operand of K columns: per 8 columns four F2FP(.RELU) packs and
 // one 16-byte store (the bias is already in the accumulator)
@@ -205,55 +233,69 @@ __device__ __forceinline__ bool pair_second(const TileSched& S, uint32_t t, uint
 // gamma(x) (core.py:132-152 layout: raw xyz, then per octave k sin xyz, cos
 // xyz; column 63 zero) generated octave by octave and flushed to the K0
 // operand one 8-column chunk at a time, so only ~14 values are live
+// gamma(x) (core.py:132-152 layout: raw xyz, then per octave k sin xyz, cos
+// xyz; column 63 zero).  Anchors k = 0, 3, 6, 9 (MUFU after exact
+// reduction), two double-angle steps after each of the first three; anchors
+// and chains run as f32x2 pairs, in octave order, and every completed
+// 8-column chunk is flushed to the K0 operand at once (few live registers).
 template <int W>
 __device__ __forceinline__ void encode_position(uint8_t* A0, int tid, const float* x) {
   using T = TcShape<W>;
-  // S[k][a], C[k][a] for the 10 octaves of the 3 axes.  Anchors k = 0, 3, 6, 9
-  // (MUFU after exact reduction), two double-angle steps after each of the
-  // first three; the 12 anchors and 9 chains are processed in f32x2 pairs.
-  float S[10][3], C[10][3];
-  sincos_scaled2(x[0], 0, x[1], 0, &S[0][0], &C[0][0], &S[0][1], &C[0][1]);
-  sincos_scaled2(x[2], 0, x[2], 3, &S[0][2], &C[0][2], &S[3][2], &C[3][2]);
-  sincos_scaled2(x[0], 3, x[1], 3, &S[3][0], &C[3][0], &S[3][1], &C[3][1]);
-  sincos_scaled2(x[0], 6, x[1], 6, &S[6][0], &C[6][0], &S[6][1], &C[6][1]);
-  sincos_scaled2(x[2], 6, x[2], 9, &S[6][2], &C[6][2], &S[9][2], &C[9][2]);
-  sincos_scaled2(x[0], 9, x[1], 9, &S[9][0], &C[9][0], &S[9][1], &C[9][1]);
-  // chains (octave of the anchor, axis) paired: (0x,0y) (0z,3x) (3y,3z) (6x,6y); 6z alone
-  const int ck[4][2] = {{0, 0}, {0, 3}, {3, 3}, {6, 6}}, ca[4][2] = {{0, 1}, {2, 0}, {1, 2}, {0, 1}};
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int k0 = ck[p][0], a0 = ca[p][0], k1 = ck[p][1], a1 = ca[p][1];
-    F2 s = f2(S[k0][a0], S[k1][a1]), c = f2(C[k0][a0], C[k1][a1]);
-#pragma unroll
-    for (int st = 1; st <= 2; ++st) {
-      double_angle2(s, c);
-      f2_split(s, S[k0 + st][a0], S[k1 + st][a1]);
-      f2_split(c, C[k0 + st][a0], C[k1 + st][a1]);
-    }
-  }
-#pragma unroll
-  for (int st = 1; st <= 2; ++st) {
-    const float sp = S[5 + st][2], cp = C[5 + st][2];
-    S[6 + st][2] = 2.0f * sp * cp;
-    C[6 + st][2] = (cp - sp) * (cp + sp);
-  }
-  // core.py:132-152 layout: raw xyz, then per octave sin xyz, cos xyz; col 63 = 0
   float e[64];
   e[0] = x[0]; e[1] = x[1]; e[2] = x[2];
-#pragma unroll
-  for (int k = 0; k < 10; ++k)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      e[3 + 6 * k + a] = S[k][a];
-      e[6 + 6 * k + a] = C[k][a];
-    }
   e[63] = 0.f;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
+  auto put = [&](int k, int a, float sv, float cv) {
+    e[3 + 6 * k + a] = sv;
+    e[6 + 6 * k + a] = cv;
+  };
+  auto flush = [&](int c) {
     const float* v = e + 8 * c;
     *reinterpret_cast<uint4*>(A0 + canon_off(tid, 8 * c, T::K0)) =
         make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
+  };
+  // two chains of two double-angle steps from anchors (ka, aa), (kb, ab)
+  auto chains = [&](int ka, int aa, float sa, float ca, int kb, int ab, float sb, float cb) {
+    F2 sv = f2(sa, sb), cv = f2(ca, cb);
+#pragma unroll
+    for (int st = 1; st <= 2; ++st) {
+      double_angle2(sv, cv);
+      float s0, s1, c0, c1;
+      f2_split(sv, s0, s1);
+      f2_split(cv, c0, c1);
+      put(ka + st, aa, s0, c0);
+      put(kb + st, ab, s1, c1);
+    }
+  };
+  float s0, c0, s1, c1, s2, c2, s3, c3;
+  // octaves 0-2 (and z of 3-5)
+  sincos_scaled2(x[0], 0, x[1], 0, &s0, &c0, &s1, &c1);
+  sincos_scaled2(x[2], 0, x[2], 3, &s2, &c2, &s3, &c3);
+  put(0, 0, s0, c0); put(0, 1, s1, c1); put(0, 2, s2, c2); put(3, 2, s3, c3);
+  chains(0, 0, s0, c0, 0, 1, s1, c1);
+  chains(0, 2, s2, c2, 3, 2, s3, c3);
+  flush(0); flush(1);
+  // octaves 3-5
+  sincos_scaled2(x[0], 3, x[1], 3, &s0, &c0, &s1, &c1);
+  put(3, 0, s0, c0); put(3, 1, s1, c1);
+  chains(3, 0, s0, c0, 3, 1, s1, c1);
+  flush(2); flush(3);
+  // octaves 6-8 (and z of 9)
+  sincos_scaled2(x[0], 6, x[1], 6, &s0, &c0, &s1, &c1);
+  sincos_scaled2(x[2], 6, x[2], 9, &s2, &c2, &s3, &c3);
+  put(6, 0, s0, c0); put(6, 1, s1, c1); put(6, 2, s2, c2); put(9, 2, s3, c3);
+  chains(6, 0, s0, c0, 6, 1, s1, c1);
+#pragma unroll
+  for (int st = 1; st <= 2; ++st) {  // 6z alone (scalar, same roundings)
+    const float sp = s2, cp = c2;
+    s2 = 2.0f * sp * cp;
+    c2 = (cp - sp) * (cp + sp);
+    put(6 + st, 2, s2, c2);
   }
+  flush(4); flush(5); flush(6);
+  // octave 9
+  sincos_scaled2(x[0], 9, x[1], 9, &s0, &c0, &s1, &c1);
+  put(9, 0, s0, c0); put(9, 1, s1, c1);
+  flush(7);
 }
 
 template <int W, class IO>
@@ -403,26 +445,18 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
       for (int L = 0; L < 5; ++L) {
         wait_mma();
         if (L == 0) {  // trunk0 -> h0 (K1 layout, over the dead gamma(x))
-          float h[W];
-          tmem_load<W>(trow, h);
-          pack_store<W, true>(h, Ag, T::K1, gt);
+          tmem_to_operand<W, true>(trow, Ag, T::K1, gt);
         } else if (L == 1) {  // trunk1 -> h1 (K2 layout)
-          float h[W];
-          tmem_load<W>(trow, h);
-          pack_store<W, true>(h, Ag, T::K2, gt);
+          tmem_to_operand<W, true>(trow, Ag, T::K2, gt);
           fetch_direction<W>(io, row, de);  // in flight while the L2 MMA runs
         } else if (L == 2) {  // feature (cols 0..W-1, unactivated) + density (col W) -> [feat, gamma(d)] (K3)
           store_direction<W>(Ag, gt, de);
-          float h[W];
-          tmem_load<W>(trow, h);
-          pack_store<W, false>(h, Ag, T::K3, gt);
+          tmem_to_operand<W, false>(trow, Ag, T::K3, gt);
           float z[16];
           tmem_load<16>(trow + W, z);
           sigma = fmaxf(z[0], 0.f);
         } else if (L == 3) {  // direction -> g (K4 layout)
-          float h[W];
-          tmem_load<W>(trow, h);
-          pack_store<W, true>(h, Ag, T::K4, gt);
+          tmem_to_operand<W, true>(trow, Ag, T::K4, gt);
         } else {  // color: sigmoid
           float z[16];
           tmem_load<16>(trow, z);
