@@ -237,10 +237,23 @@ int gf_pack_weights(const gf_arch_t* arch, int64_t n_cells, const float* const* 
 struct QueryWs {
   uint32_t* keys;
   BucketBufs B;
+  uint32_t* cursor2;  // bulk path: super-cell run cursors
+  float4* trec;       // super-cell-ordered records
+  float4* tdir;
 };
 
 static size_t query_carve(Carve& c, int64_t n, int64_t n_cells, QueryWs* w) {
   w->keys = c.take<uint32_t>((size_t)n + 1);
+  if (query_bucket_fast_ok(n, n_cells)) {
+    w->cursor2 = c.take<uint32_t>((size_t)n_cells);
+    w->trec = c.take<float4>((size_t)n + 1);
+    w->tdir = c.take<float4>((size_t)n + 1);
+    w->B.srec = c.take<float4>((size_t)n + 1);
+    w->B.sdir = c.take<float4>((size_t)n + 1);
+  } else {
+    w->cursor2 = nullptr;
+    w->trec = w->tdir = w->B.srec = w->B.sdir = nullptr;
+  }
   w->B.counts = c.take<uint32_t>((size_t)n_cells);
   w->B.offsets = c.take<uint32_t>((size_t)n_cells + 1);
   w->B.cursor = c.take<uint32_t>((size_t)n_cells);
@@ -284,14 +297,24 @@ int gf_query_points(const gf_arch_t* arch, const gf_grid_geom_t* grid, const voi
   GfGrid g = gf_make_grid(grid);
   stage_open(st);
   cudaMemsetAsync(w.B.counts, 0, (size_t)nc * 4, st);
-  launch_query_keys(g, pos, n, w.keys, w.B.counts, err, st);
-  stage_mark(st, GF_STAGE_MARCH, n > 0 ? 1 : 0);
-  launch_scan_cells(w.B, nc, st);
-  stage_mark(st, GF_STAGE_SCAN, 1);
-  launch_scatter_query(w.keys, n, w.B, st);
-  stage_mark(st, GF_STAGE_SCATTER, n > 0 ? 1 : 0);
-  TileSched S{w.B.tiles, w.B.n_tiles, w.B.sorted, nullptr};
-  QueryIO io{pos, dir, rgb, sigma, nullptr};
+  const bool fast = w.cursor2 != nullptr;
+  if (fast) {
+    stage_mark(st, GF_STAGE_MARCH, launch_query_bucket(g, pos, dir, n, nc, w.keys, w.B, w.trec, w.tdir, w.cursor2,
+                                                       err, st, 1));
+  } else {
+    launch_query_keys(g, pos, n, w.keys, w.B.counts, err, st);
+    stage_mark(st, GF_STAGE_MARCH, n > 0 ? 1 : 0);
+  }
+  stage_mark(st, GF_STAGE_SCAN, launch_scan_cells(w.B, nc, st, n));
+  if (fast) {
+    stage_mark(st, GF_STAGE_SCATTER, launch_query_bucket(g, pos, dir, n, nc, w.keys, w.B, w.trec, w.tdir, w.cursor2,
+                                                         err, st, 2));
+  } else {
+    launch_scatter_query(w.keys, n, w.B, st);
+    stage_mark(st, GF_STAGE_SCATTER, n > 0 ? 1 : 0);
+  }
+  TileSched S{w.B.tiles, w.B.n_tiles, fast ? nullptr : w.B.sorted, w.B.srec, w.B.sdir};
+  QueryIO io{pos, dir, rgb, sigma, nullptr, fast ? w.B.sdir : nullptr};
   if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_query_points: no MLP kernel for this architecture/precision");
   stage_mark(st, GF_STAGE_MLP, 1);
@@ -309,8 +332,8 @@ int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packe
   if (query_carve(c, n, n_cells, &w) > ws_bytes) return fail(GF_ERR_WORKSPACE, "gf_grouped_forward: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   launch_segments_from_offsets(offsets, n_cells, n, w.B, st);
-  TileSched S{w.B.tiles, w.B.n_tiles, w.B.sorted, nullptr};
-  QueryIO io{pos, dir, rgb, sigma, order};
+  TileSched S{w.B.tiles, w.B.n_tiles, nullptr, nullptr, nullptr};  // rows already grouped: identity
+  QueryIO io{pos, dir, rgb, sigma, order, nullptr};
   if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_grouped_forward: no MLP kernel for this architecture/precision");
   return check_cuda("gf_grouped_forward");
@@ -560,7 +583,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   }
   const unsigned march_blocks = (unsigned)gf_div_up<int64_t>(P.march_threads, 128);
   const unsigned ray_blocks = (unsigned)gf_div_up<int64_t>(n_rays, 128);
-  TileSched S{w.B.tiles, w.B.n_tiles, nullptr, w.B.srec};
+  TileSched S{w.B.tiles, w.B.n_tiles, nullptr, w.B.srec, nullptr};
   int stride_shift = -1;
   for (int b = 0; b < 31; ++b)
     if ((1 << b) == stride) stride_shift = b;
@@ -587,8 +610,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
     for (int r = 0; r < P.n_rounds; ++r) {
       k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r);
       stage_mark(s, GF_STAGE_MARCH, 1);
-      launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, r, s);
-      stage_mark(s, GF_STAGE_SCATTER, nc <= 8192 ? 1 : 2);
+      stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, r, (int64_t)n_rays * stride, s));
       run_mlp(t, packed, precision, S, &io, nullptr, s);
       stage_mark(s, GF_STAGE_MLP, 1);
     }

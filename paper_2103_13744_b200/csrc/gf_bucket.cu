@@ -6,6 +6,8 @@
 // its own inputs and its cell's weights), so they use a warp-aggregated
 // atomic scatter; the public group_by_network entry point uses the stable
 // variant in gf_group.cu.
+#include <algorithm>
+
 #include "gf_bucket.cuh"
 
 namespace gf {
@@ -84,6 +86,7 @@ __global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells
     toff[n_cells] = carry.y;
   }
   __syncthreads();
+  if (!in_smem) return;  // tile list built by k_fill_tiles from B.tile_off
   // tile list, all threads in parallel: tile t belongs to the last cell whose
   // first tile is <= t (binary search; empty cells share their successor's start)
   const uint32_t nt = carry.y;
@@ -99,12 +102,257 @@ __global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells
   }
 }
 
-void launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st) {
+// tile list from the per-cell first-tile table, one thread per tile (binary
+// search over tile_off; empty cells share their successor's start)
+__global__ void __launch_bounds__(256) k_fill_tiles(BucketBufs B, int64_t n_cells) {
+  const uint32_t nt = *B.n_tiles;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n_cells;  // invariant: tile_off[lo] <= t < tile_off[hi]
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (B.tile_off[mid] <= t) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t r0 = (t - B.tile_off[lo]) * GF_TILE_ROWS, n_seg = B.offsets[lo + 1] - B.offsets[lo];
+    B.tiles[t] = gf_make_tile((uint32_t)lo, B.offsets[lo] + r0, min(n_seg - r0, (uint32_t)GF_TILE_ROWS));
+  }
+}
+
+// offsets + tile list.  Small grids: one CTA does both with the tile table in
+// shared memory.  Large grids / many tiles: the scan CTA writes the table to
+// global memory and a grid-wide kernel fills the tiles.
+int launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st, int64_t max_rows) {
   BucketBufs b = B;
   const int64_t smem_cells = 48 * 1024 / 4 - 1;  // default dynamic smem budget
-  b.scan_smem_cells = n_cells <= smem_cells ? n_cells : 0;
-  const size_t smem = b.scan_smem_cells ? (size_t)(n_cells + 1) * 4 : 0;
+  const bool one_cta = n_cells <= smem_cells && max_rows <= (int64_t)1 << 20;
+  b.scan_smem_cells = one_cta ? n_cells : 0;
+  const size_t smem = one_cta ? (size_t)(n_cells + 1) * 4 : 0;
   k_scan_cells<1024, 4><<<1, 1024, smem, st>>>(b, n_cells);
+  if (!one_cta) {
+    const int64_t max_tiles = max_rows / GF_TILE_ROWS + n_cells + 1;
+    k_fill_tiles<<<(unsigned)std::min<int64_t>(gf_div_up<int64_t>(max_tiles, 256), (int64_t)num_sms() * 8), 256, 0,
+                   st>>>(b, n_cells);
+    return 2;
+  }
+  return 1;
+}
+
+// ---------------------------------------------------------------------------
+// bulk query bucketing (NetworkGrid.query_points at scale, grid.py:50-56):
+// a two-level counting sort that MOVES the (position, index) and
+// (direction, key) records so the MLP streams its rows.
+//   pass 1: bin each point (bounds check core.py:92-101) -> key, per-cell
+//           counts (shared-memory histogram, one global atomic per bin);
+//   scan:   segment offsets; cursors start at them;
+//   pass 2: records -> super-cell order (key >> sb, <= 64 buckets);
+//   pass 3: super-cell order -> cell order (a chunk spans few super-cells).
+// Passes 2 and 3 stage GF_QB_TILE records per iteration in shared memory,
+// grouped by bucket (local counting sort), reserve each bucket's run with one
+// global atomic and write the runs out contiguously: scattering 16-byte
+// records one by one leaves partially written lines that cost DRAM
+// read-modify-writes.  Order inside a cell is arbitrary: each query's result
+// depends only on its own inputs and its cell's weights.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(GF_QB_THREADS) k_query_keys_hist(GfGrid g, const float* __restrict__ pos,
+                                                                   int64_t n, int64_t n_cells, uint32_t* keys,
+                                                                   uint32_t* counts, int64_t* err) {
+  extern __shared__ uint32_t hist[];
+  for (int64_t c = threadIdx.x; c < n_cells; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float x[3];
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      x[a] = pos[3 * i + a];
+      if (!((double)x[a] >= g.b_min[a] && (double)x[a] <= g.b_max[a])) {  // core.py:92-101 (NaN rejected)
+        atomicMin((unsigned long long*)err, (unsigned long long)(3 * i + a));
+        ok = false;
+      }
+    }
+    uint32_t key = 0xFFFFFFFFu;
+    if (ok) {
+      key = gf_flat_cell(g, x[0], x[1], x[2]);
+      atomicAdd(&hist[key], 1u);
+    }
+    keys[i] = key;
+  }
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < n_cells; c += blockDim.x)
+    if (hist[c]) atomicAdd(&counts[c], hist[c]);
+}
+
+// one staged scatter step: the block's GF_QB_TILE items (bucket bk[k] in
+// [0, nb), or nb for none) are grouped by bucket in shared memory and written
+// as contiguous runs at cursor[bucket] (+= run length).
+struct QbStage {
+  float4 rec[GF_QB_TILE];
+  float4 dir[GF_QB_TILE];
+  uint16_t bucket[GF_QB_TILE];
+};
+
+template <class Load>
+__device__ __forceinline__ void qb_stage_scatter(QbStage& st, uint32_t* hist, uint32_t* lbase, uint32_t* gbase,
+                                                 int nb, uint32_t* cursor, int cursor_shift, float4* orec,
+                                                 float4* odir, Load load) {
+  constexpr int PER = GF_QB_TILE / GF_QB_THREADS;
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) hist[c] = 0;
+  __syncthreads();
+  float4 r[PER], d[PER];
+  int bk[PER];
+  uint32_t rank[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    bk[q] = load(q * GF_QB_THREADS + threadIdx.x, r[q], d[q]);  // < 0: no item
+    if (bk[q] >= 0) rank[q] = atomicAdd(&hist[bk[q]], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of the bucket counts (nb <= blockDim) and global run reservation
+  if (threadIdx.x < nb) {
+    const uint32_t h = hist[threadIdx.x];
+    gbase[threadIdx.x] = h ? atomicAdd(&cursor[(uint32_t)threadIdx.x << cursor_shift], h) : 0u;
+  }
+  {
+    __shared__ uint32_t wsum[GF_QB_THREADS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t v = threadIdx.x < nb ? hist[threadIdx.x] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t t = lane < GF_QB_THREADS / 32 ? wsum[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      if (lane < GF_QB_THREADS / 32) wsum[lane] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < nb) lbase[threadIdx.x] = (wid ? wsum[wid - 1] : 0u) + x - v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (bk[q] >= 0) {
+      const uint32_t k = lbase[bk[q]] + rank[q];
+      st.rec[k] = r[q];
+      st.dir[k] = d[q];
+      st.bucket[k] = (uint16_t)bk[q];
+    }
+  }
+  __syncthreads();
+  const uint32_t total = lbase[nb - 1] + hist[nb - 1];
+  for (uint32_t k = threadIdx.x; k < total; k += blockDim.x) {  // consecutive k -> consecutive run slots
+    const int b = st.bucket[k];
+    const uint32_t dst = gbase[b] + (k - lbase[b]);
+    orec[dst] = st.rec[k];
+    odir[dst] = st.dir[k];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(GF_QB_THREADS, 1) k_query_move_super(const float* __restrict__ pos,
+                                                                       const float* __restrict__ dir, int64_t n,
+                                                                       int sb, const uint32_t* __restrict__ keys,
+                                                                       uint32_t* cursor, float4* trec, float4* tdir) {
+  extern __shared__ __align__(16) uint8_t qsm[];
+  QbStage& st = *reinterpret_cast<QbStage*>(qsm);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(qsm + sizeof(QbStage));
+  uint32_t* lbase = hist + GF_QB_SUPER;
+  uint32_t* gbase = lbase + GF_QB_SUPER;
+  for (int64_t t0 = (int64_t)blockIdx.x * GF_QB_TILE; t0 < n; t0 += (int64_t)gridDim.x * GF_QB_TILE) {
+    qb_stage_scatter(st, hist, lbase, gbase, GF_QB_SUPER, cursor, sb, trec, tdir,
+                     [&](int k, float4& r, float4& d) -> int {
+                       const int64_t i = t0 + k;
+                       if (i >= n) return -1;
+                       const uint32_t key = keys[i];
+                       if (key == 0xFFFFFFFFu) return -1;
+                       r = make_float4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], __uint_as_float((uint32_t)i));
+                       d = make_float4(dir[3 * i], dir[3 * i + 1], dir[3 * i + 2], __uint_as_float(key));
+                       return (int)(key >> sb);
+                     });
+  }
+}
+
+// pass 3: a CTA walks a contiguous range of the super-cell order; every tile
+// of it lies within one super-cell (tiles never straddle: ranges are cut at
+// super-cell starts), so its buckets are the <= 2^sb cells of that super-cell
+__global__ void __launch_bounds__(GF_QB_THREADS, 1) k_query_move_cell(const uint32_t* __restrict__ offsets,
+                                                                      int64_t n_cells, int sb,
+                                                                      const float4* __restrict__ trec,
+                                                                      const float4* __restrict__ tdir,
+                                                                      uint32_t* cursor, float4* srec, float4* sdir) {
+  extern __shared__ __align__(16) uint8_t qsm[];
+  QbStage& st = *reinterpret_cast<QbStage*>(qsm);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(qsm + sizeof(QbStage));
+  uint32_t* lbase = hist + (1 << GF_QB_SUB_BITS);
+  uint32_t* gbase = lbase + (1 << GF_QB_SUB_BITS);
+  const int s = blockIdx.y;                       // super-cell
+  const uint32_t s0 = offsets[(uint32_t)s << sb], s1 = offsets[min((uint32_t)(s + 1) << sb, (uint32_t)n_cells)];
+  const uint32_t nb = 1u << sb;
+  for (uint32_t t0 = s0 + blockIdx.x * GF_QB_TILE; t0 < s1; t0 += gridDim.x * GF_QB_TILE) {
+    qb_stage_scatter(st, hist, lbase, gbase, (int)nb, cursor + ((uint32_t)s << sb), 0, srec, sdir,
+                     [&](int k, float4& r, float4& d) -> int {
+                       const uint32_t row = t0 + (uint32_t)k;
+                       if (row >= s1) return -1;
+                       r = trec[row];
+                       d = tdir[row];
+                       return (int)(__float_as_uint(d.w) & (nb - 1u));
+                     });
+  }
+}
+
+bool query_bucket_fast_ok(int64_t n, int64_t n_cells) {
+  // super-cells x sub-cells must cover the grid; offsets[n_cells] is read at the last super-cell end
+  return n_cells <= ((int64_t)GF_QB_SUPER << GF_QB_SUB_BITS) && n < 0xFFFFFFF0ll && n_cells >= 1;
+}
+
+int query_super_shift(int64_t n_cells) {
+  int sb = 0;
+  while ((n_cells - 1) >> sb >= GF_QB_SUPER) ++sb;
+  return sb;
+}
+
+size_t query_stage_smem() { return sizeof(QbStage) + 3 * (size_t)(1 << GF_QB_SUB_BITS) * 4; }
+
+int launch_query_bucket(const GfGrid& g, const float* pos, const float* dir, int64_t n, int64_t n_cells,
+                        uint32_t* keys, const BucketBufs& B, float4* trec, float4* tdir, uint32_t* cursor2,
+                        int64_t* err, cudaStream_t st, int pass) {
+  if (n == 0) return 0;
+  const int sb = query_super_shift(n_cells);
+  if (pass == 1) {
+    const size_t smem = (size_t)n_cells * 4;
+    static thread_local size_t smem_set = 0;
+    if (smem > 48 * 1024 && smem_set < smem) {
+      cudaFuncSetAttribute(k_query_keys_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_set = smem;
+    }
+    const int64_t ctas = std::min<int64_t>(gf_div_up<int64_t>(n, GF_QB_THREADS), (int64_t)num_sms() * 2);
+    k_query_keys_hist<<<(unsigned)ctas, GF_QB_THREADS, smem, st>>>(g, pos, n, n_cells, keys, B.counts, err);
+    return 1;
+  }
+  const size_t smem = query_stage_smem();
+  static thread_local bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_query_move_super, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_query_move_cell, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  // cursors: B.cursor = offsets (set by k_scan_cells) serves pass 3; pass 2
+  // uses a copy (its super-cell runs start at the same offsets)
+  cudaMemcpyAsync(cursor2, B.cursor, (size_t)n_cells * 4, cudaMemcpyDeviceToDevice, st);
+  k_query_move_super<<<num_sms(), GF_QB_THREADS, smem, st>>>(pos, dir, n, sb, keys, cursor2, trec, tdir);
+  const int n_super = (int)((n_cells - 1) >> sb) + 1;
+  const unsigned per_super = (unsigned)std::max<int64_t>(1, (int64_t)num_sms() / n_super + 1);
+  k_query_move_cell<<<dim3(per_super, (unsigned)n_super), GF_QB_THREADS, smem, st>>>(B.offsets, n_cells, sb, trec, tdir,
+                                                                                      B.cursor, B.srec, B.sdir);
+  return 2;
 }
 
 // warp-aggregated cursor claim
@@ -201,8 +449,7 @@ __global__ void k_iota(uint32_t* out, int64_t n) {
 void launch_segments_from_offsets(const int64_t* offsets, int64_t n_cells, int64_t n, const BucketBufs& B,
                                   cudaStream_t st) {
   k_counts_from_offsets<<<(unsigned)gf_div_up<int64_t>(n_cells, 256), 256, 0, st>>>(offsets, n_cells, B.counts);
-  launch_scan_cells(B, n_cells, st);
-  if (n > 0) k_iota<<<(unsigned)gf_div_up<int64_t>(n, 256), 256, 0, st>>>(B.sorted, n);
+  launch_scan_cells(B, n_cells, st, n);  // rows are already in order: TileSched.sorted = NULL (identity)
 }
 
 void launch_query_keys(const GfGrid& g, const float* pos, int64_t n, uint32_t* keys, uint32_t* counts, int64_t* err,

@@ -20,14 +20,25 @@ struct BucketBufs {
   uint2* tiles;       // [max_tiles] gf_make_tile(cell, first row, rows)
   uint32_t* n_tiles;  // [1]
   uint32_t* sorted;   // [capacity]  item index per sorted slot (query paths)
-  float4* srec;       // [capacity]  render path: the sorted sample records themselves (x, y, z, staging index)
+  float4* srec;       // [capacity]  sorted records (x, y, z, staging / caller index): render and bulk query
+  float4* sdir;       // [capacity]  bulk query: sorted directions (x, y, z, cell bits)
   uint32_t* tile_off; // [n_cells+1] first tile of each cell (global fallback for large grids)
   int64_t scan_smem_cells;  // set by launch_scan_cells
 };
 
-void launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st);
-void launch_scatter_render(const float4* rec, const uint32_t* run, const uint32_t* list, uint32_t* counts2, int round,
-                           int stride, const BucketBufs& B, cudaStream_t st);
+// max_rows: upper bound on the rows to tile (sizes the tile-fill grid)
+int launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st, int64_t max_rows);  // -> launches
+
+// bulk-query bucketing (gf_bucket.cu): two-level record-moving counting sort
+#define GF_QB_THREADS 1024
+#define GF_QB_TILE 2048        // records staged in shared memory per step (2 x 16 B + 2 B each)
+#define GF_QB_SUPER 64         // first-level buckets (super-cell = key >> shift)
+#define GF_QB_SUB_BITS 10      // second level: <= 1024 cells per super-cell (grids <= 65536 cells)
+bool query_bucket_fast_ok(int64_t n, int64_t n_cells);
+// pass 1 -> 1 launch; pass 2 -> 2 launches (returned)
+int launch_query_bucket(const GfGrid& g, const float* pos, const float* dir, int64_t n, int64_t n_cells,
+                        uint32_t* keys, const BucketBufs& B, float4* trec, float4* tdir, uint32_t* cursor2,
+                        int64_t* err, cudaStream_t st, int pass);
 int num_sms();
 void launch_query_keys(const GfGrid& g, const float* pos, int64_t n, uint32_t* keys, uint32_t* counts, int64_t* err,
                        cudaStream_t st);

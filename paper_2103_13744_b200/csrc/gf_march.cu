@@ -466,8 +466,8 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
   }
 }
 
-void launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
-                  int stride, int round, cudaStream_t st) {
+int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
+                 int stride, int round, int64_t max_rows, cudaStream_t st) {
   const size_t smem = (size_t)2 * (n_cells + 1) * 4;
   if (n_cells <= 8192) {
     static thread_local bool attr = false;
@@ -476,12 +476,13 @@ void launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, 
       attr = true;
     }
     k_place<true><<<num_sms() * 2, 512, smem, st>>>(grid, RB, run, Bk, n_cells, stride, round);
-  } else {
-    BucketBufs b = Bk;
-    b.counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
-    launch_scan_cells(b, n_cells, st);  // offsets + tiles; clears this round's counts after reading
-    k_place<false><<<num_sms() * 2, 512, 0, st>>>(grid, RB, run, Bk, n_cells, stride, round);
+    return 1;
   }
+  BucketBufs b = Bk;
+  b.counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
+  const int n = launch_scan_cells(b, n_cells, st, max_rows);  // offsets + tiles; clears this round's counts
+  k_place<false><<<num_sms() * 2, 512, 0, st>>>(grid, RB, run, Bk, n_cells, stride, round);
+  return n + 1;
 }
 
 __device__ __forceinline__ u128 ldg_u128(const u128* p) {

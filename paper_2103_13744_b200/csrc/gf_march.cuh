@@ -96,8 +96,8 @@ __device__ __forceinline__ int64_t seed_slot(const MarchParams& P, int64_t g) {
 
 // K2 for the render path (fused scan + tile list + rank-based placement);
 // returns the number of launches it made
-void launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
-                  int stride, int round, cudaStream_t st);
+int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
+                 int stride, int round, int64_t max_rows, cudaStream_t st);
 
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
                               int k, int chunk, int n_rounds, u128* seeds, u128* jump, u128* start,

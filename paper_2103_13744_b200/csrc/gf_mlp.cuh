@@ -63,8 +63,9 @@ __host__ inline Fp32Layout make_fp32_layout(const LayerTable& t) {
 struct TileSched {
   const uint2* tiles;       // gf_make_tile entries
   const uint32_t* n_tiles;
-  const uint32_t* sorted;   // query paths: caller row per sorted row
-  const float4* srec;       // render path: sorted sample records
+  const uint32_t* sorted;   // query paths without moved records: caller row per sorted row (NULL: identity)
+  const float4* srec;       // sorted records (x, y, z, index bits): render path and bulk queries
+  const float4* sdir;       // bulk queries: sorted directions (x, y, z, 0)
 };
 
 struct RenderIO {
@@ -88,7 +89,7 @@ struct RenderIO {
       d[0] = dd.x; d[1] = dd.y; d[2] = dd.z;
     }
   }
-  __device__ __forceinline__ void load_denc(uint32_t idx, uint4* de) const {
+  __device__ __forceinline__ void load_denc(uint32_t idx, uint32_t, uint4* de) const {
     const uint4* q = denc + 4ull * ray_of(idx);
 #pragma unroll
     for (int c = 0; c < 4; ++c) de[c] = q[c];
@@ -100,15 +101,26 @@ struct RenderIO {
 
 // Bulk query: caller's float32 (N,3) arrays, results in caller order.
 struct QueryIO {
-  static constexpr bool kDirEnc = false;
+  static constexpr bool kDirEnc = true;  // direction gathered + encoded one layer ahead of its use (load_denc)
   const float* pos;
   const float* dir;
   float* rgb;
   float* sigma;
   const int64_t* store_idx;  // optional: row idx is written to store_idx[idx] (grouped_forward)
+  const float4* sdir;        // bulk path: directions in sorted order (read by sorted row)
   template <bool DIR>
   __device__ __forceinline__ void fetch(const TileSched& S, uint32_t row, uint32_t& idx, float* x, float* d) const {
-    idx = S.sorted[row];
+    if (S.srec) {  // records moved into sorted order by the bucketing pass
+      const float4 r = S.srec[row];
+      idx = __float_as_uint(r.w);
+      x[0] = r.x; x[1] = r.y; x[2] = r.z;
+      if (DIR) {
+        const float4 q = S.sdir[row];
+        d[0] = q.x; d[1] = q.y; d[2] = q.z;
+      }
+      return;
+    }
+    idx = S.sorted ? S.sorted[row] : row;
     const float* p = pos + 3ull * idx;
     x[0] = p[0]; x[1] = p[1]; x[2] = p[2];
     if (DIR) {
@@ -123,7 +135,7 @@ struct QueryIO {
     rgb[3ull * idx + 2] = b;
     sigma[idx] = s;
   }
-  __device__ __forceinline__ void load_denc(uint32_t, uint4*) const {}
+  __device__ __forceinline__ void load_denc(uint32_t idx, uint32_t row, uint4* de) const;  // gf_mlp_tc.cu
 };
 
 // launchers (gf_mlp_simt.cu / gf_mlp_tc.cu); return false if the architecture

@@ -210,7 +210,7 @@ __device__ __forceinline__ void pack_store(const float* h, uint8_t* A, int K, in
 // operand chunk (the ray's pre-encoded gamma(d), gf_encode.cuh) is fetched
 // separately while the trunk0 MMA runs
 struct RowIn {
-  uint32_t idx;
+  uint32_t idx, row;  // caller / staging index, sorted row
   bool valid;
   float x[3], d[3];
 };
@@ -219,6 +219,7 @@ template <class IO>
 __device__ __forceinline__ void load_row(const TileSched& S, const IO& io, uint2 tl, int tid, RowIn& r) {
   r.valid = (uint32_t)tid < gf_tile_rows(tl);
   r.idx = 0;
+  r.row = tl.y + (uint32_t)tid;
   r.x[0] = r.x[1] = r.x[2] = 0.f;
   if (!IO::kDirEnc) r.d[0] = r.d[1] = r.d[2] = 0.f;
   if (r.valid) io.template fetch<!IO::kDirEnc>(S, tl.y + (uint32_t)tid, r.idx, r.x, r.d);
@@ -301,7 +302,7 @@ __device__ __forceinline__ void encode_position(uint8_t* A0, int tid, const floa
 template <int W, class IO>
 __device__ __forceinline__ void fetch_direction(const IO& io, const RowIn& row, uint4* de) {
   if (IO::kDirEnc) {
-    if (row.valid) io.load_denc(row.idx, de);
+    if (row.valid) io.load_denc(row.idx, row.row, de);
     else de[0] = de[1] = de[2] = de[3] = make_uint4(0u, 0u, 0u, 0u);
   } else {
     encode_direction_h(row.d, de);
@@ -314,6 +315,18 @@ __device__ __forceinline__ void store_direction(uint8_t* A3, int tid, const uint
   static_assert(T::K3 - W == 32, "direction operand chunk is 32 fp16 wide");
 #pragma unroll
   for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(A3 + canon_off(tid, W + 8 * q, T::K3)) = de[q];
+}
+
+__device__ __forceinline__ void QueryIO::load_denc(uint32_t idx, uint32_t row, uint4* de) const {
+  float d[3];
+  if (sdir) {
+    const float4 q = sdir[row];
+    d[0] = q.x; d[1] = q.y; d[2] = q.z;
+  } else {
+    const float* q = dir + 3ull * idx;
+    d[0] = q[0]; d[1] = q[1]; d[2] = q[2];
+  }
+  encode_direction_h(d, de);
 }
 
 // ---------------------------------------------------------------------------
