@@ -257,7 +257,7 @@ __device__ __forceinline__ void qb_stage_scatter(QbStage& st, uint32_t* hist, ui
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(GF_QB_THREADS, 1) k_query_move_super(const float* __restrict__ pos,
+__global__ void __launch_bounds__(GF_QB_THREADS, 2) k_query_move_super(const float* __restrict__ pos,
                                                                        const float* __restrict__ dir, int64_t n,
                                                                        int sb, const uint32_t* __restrict__ keys,
                                                                        uint32_t* cursor, float4* trec, float4* tdir) {
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(GF_QB_THREADS, 1) k_query_move_super(const flo
 // pass 3: a CTA walks a contiguous range of the super-cell order; every tile
 // of it lies within one super-cell (tiles never straddle: ranges are cut at
 // super-cell starts), so its buckets are the <= 2^sb cells of that super-cell
-__global__ void __launch_bounds__(GF_QB_THREADS, 1) k_query_move_cell(const uint32_t* __restrict__ offsets,
+__global__ void __launch_bounds__(GF_QB_THREADS, 2) k_query_move_cell(const uint32_t* __restrict__ offsets,
                                                                       int64_t n_cells, int sb,
                                                                       const float4* __restrict__ trec,
                                                                       const float4* __restrict__ tdir,
@@ -347,9 +347,9 @@ int launch_query_bucket(const GfGrid& g, const float* pos, const float* dir, int
   // cursors: B.cursor = offsets (set by k_scan_cells) serves pass 3; pass 2
   // uses a copy (its super-cell runs start at the same offsets)
   cudaMemcpyAsync(cursor2, B.cursor, (size_t)n_cells * 4, cudaMemcpyDeviceToDevice, st);
-  k_query_move_super<<<num_sms(), GF_QB_THREADS, smem, st>>>(pos, dir, n, sb, keys, cursor2, trec, tdir);
+  k_query_move_super<<<num_sms() * 2, GF_QB_THREADS, smem, st>>>(pos, dir, n, sb, keys, cursor2, trec, tdir);
   const int n_super = (int)((n_cells - 1) >> sb) + 1;
-  const unsigned per_super = (unsigned)std::max<int64_t>(1, (int64_t)num_sms() / n_super + 1);
+  const unsigned per_super = (unsigned)std::max<int64_t>(1, (int64_t)num_sms() * 2 / n_super + 1);
   k_query_move_cell<<<dim3(per_super, (unsigned)n_super), GF_QB_THREADS, smem, st>>>(B.offsets, n_cells, sb, trec, tdir,
                                                                                       B.cursor, B.srec, B.sdir);
   return 2;

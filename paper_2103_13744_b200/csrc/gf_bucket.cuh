@@ -30,10 +30,10 @@ struct BucketBufs {
 int launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st, int64_t max_rows);  // -> launches
 
 // bulk-query bucketing (gf_bucket.cu): two-level record-moving counting sort
-#define GF_QB_THREADS 1024
+#define GF_QB_THREADS 512
 #define GF_QB_TILE 2048        // records staged in shared memory per step (2 x 16 B + 2 B each)
 #define GF_QB_SUPER 64         // first-level buckets (super-cell = key >> shift)
-#define GF_QB_SUB_BITS 10      // second level: <= 1024 cells per super-cell (grids <= 65536 cells)
+#define GF_QB_SUB_BITS 9       // second level: <= 512 cells per super-cell (grids <= 32768 cells)
 bool query_bucket_fast_ok(int64_t n, int64_t n_cells);
 // pass 1 -> 1 launch; pass 2 -> 2 launches (returned)
 int launch_query_bucket(const GfGrid& g, const float* pos, const float* dir, int64_t n, int64_t n_cells,
