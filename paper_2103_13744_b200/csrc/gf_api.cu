@@ -240,6 +240,9 @@ struct QueryWs {
   uint32_t* cursor2;  // bulk path: super-cell run cursors
   float4* trec;       // super-cell-ordered records
   float4* tdir;
+  uint32_t* dest2;    // point -> super-order row
+  uint32_t* dest3;    // super-order row -> sorted row
+  float4* sorted_out; // results in sorted order
 };
 
 static size_t query_carve(Carve& c, int64_t n, int64_t n_cells, QueryWs* w) {
@@ -250,9 +253,12 @@ static size_t query_carve(Carve& c, int64_t n, int64_t n_cells, QueryWs* w) {
     w->tdir = c.take<float4>((size_t)n + 1);
     w->B.srec = c.take<float4>((size_t)n + 1);
     w->B.sdir = c.take<float4>((size_t)n + 1);
+    w->dest2 = c.take<uint32_t>((size_t)n + 1);
+    w->dest3 = c.take<uint32_t>((size_t)n + 1);
+    w->sorted_out = c.take<float4>((size_t)n + 1);
   } else {
-    w->cursor2 = nullptr;
-    w->trec = w->tdir = w->B.srec = w->B.sdir = nullptr;
+    w->cursor2 = w->dest2 = w->dest3 = nullptr;
+    w->trec = w->tdir = w->B.srec = w->B.sdir = w->sorted_out = nullptr;
   }
   w->B.counts = c.take<uint32_t>((size_t)n_cells);
   w->B.offsets = c.take<uint32_t>((size_t)n_cells + 1);
@@ -300,7 +306,7 @@ int gf_query_points(const gf_arch_t* arch, const gf_grid_geom_t* grid, const voi
   const bool fast = w.cursor2 != nullptr;
   if (fast) {
     stage_mark(st, GF_STAGE_MARCH, launch_query_bucket(g, pos, dir, n, nc, w.keys, w.B, w.trec, w.tdir, w.cursor2,
-                                                       err, st, 1));
+                                                       w.dest2, w.dest3, err, st, 1));
   } else {
     launch_query_keys(g, pos, n, w.keys, w.B.counts, err, st);
     stage_mark(st, GF_STAGE_MARCH, n > 0 ? 1 : 0);
@@ -308,16 +314,21 @@ int gf_query_points(const gf_arch_t* arch, const gf_grid_geom_t* grid, const voi
   stage_mark(st, GF_STAGE_SCAN, launch_scan_cells(w.B, nc, st, n));
   if (fast) {
     stage_mark(st, GF_STAGE_SCATTER, launch_query_bucket(g, pos, dir, n, nc, w.keys, w.B, w.trec, w.tdir, w.cursor2,
-                                                         err, st, 2));
+                                                         w.dest2, w.dest3, err, st, 2));
   } else {
     launch_scatter_query(w.keys, n, w.B, st);
     stage_mark(st, GF_STAGE_SCATTER, n > 0 ? 1 : 0);
   }
   TileSched S{w.B.tiles, w.B.n_tiles, fast ? nullptr : w.B.sorted, w.B.srec, w.B.sdir};
-  QueryIO io{pos, dir, rgb, sigma, nullptr, fast ? w.B.sdir : nullptr};
+  QueryIO io{pos, dir, rgb, sigma, nullptr, fast ? w.B.sdir : nullptr, fast ? w.sorted_out : nullptr};
   if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_query_points: no MLP kernel for this architecture/precision");
   stage_mark(st, GF_STAGE_MLP, 1);
+  if (fast) {
+    // the super-order record buffer is dead after the sort: it holds the super-order results
+    stage_mark(st, GF_STAGE_SCATTER, launch_query_unpermute(n, w.B.offsets + nc, w.keys, w.dest2, w.dest3,
+                                                            w.sorted_out, w.trec, rgb, sigma, st));
+  }
   return check_cuda("gf_query_points");
 }
 
@@ -333,7 +344,7 @@ int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packe
   cudaStream_t st = (cudaStream_t)stream;
   launch_segments_from_offsets(offsets, n_cells, n, w.B, st);
   TileSched S{w.B.tiles, w.B.n_tiles, nullptr, nullptr, nullptr};  // rows already grouped: identity
-  QueryIO io{pos, dir, rgb, sigma, order, nullptr};
+  QueryIO io{pos, dir, rgb, sigma, order, nullptr, nullptr};
   if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_grouped_forward: no MLP kernel for this architecture/precision");
   return check_cuda("gf_grouped_forward");

@@ -191,10 +191,12 @@ struct QbStage {
   uint16_t bucket[GF_QB_TILE];
 };
 
+// dest_of (optional): dest_of[item0 + k] = the item's output row, written in
+// item order (coalesced); composing the two levels' maps un-permutes results.
 template <class Load>
 __device__ __forceinline__ void qb_stage_scatter(QbStage& st, uint32_t* hist, uint32_t* lbase, uint32_t* gbase,
                                                  int nb, uint32_t* cursor, int cursor_shift, float4* orec,
-                                                 float4* odir, Load load) {
+                                                 float4* odir, uint32_t* dest_of, int64_t item0, Load load) {
   constexpr int PER = GF_QB_TILE / GF_QB_THREADS;
   for (int c = threadIdx.x; c < nb; c += blockDim.x) hist[c] = 0;
   __syncthreads();
@@ -244,6 +246,7 @@ __device__ __forceinline__ void qb_stage_scatter(QbStage& st, uint32_t* hist, ui
       st.rec[k] = r[q];
       st.dir[k] = d[q];
       st.bucket[k] = (uint16_t)bk[q];
+      if (dest_of) dest_of[item0 + q * GF_QB_THREADS + threadIdx.x] = gbase[bk[q]] + rank[q];
     }
   }
   __syncthreads();
@@ -260,14 +263,15 @@ __device__ __forceinline__ void qb_stage_scatter(QbStage& st, uint32_t* hist, ui
 __global__ void __launch_bounds__(GF_QB_THREADS, 2) k_query_move_super(const float* __restrict__ pos,
                                                                        const float* __restrict__ dir, int64_t n,
                                                                        int sb, const uint32_t* __restrict__ keys,
-                                                                       uint32_t* cursor, float4* trec, float4* tdir) {
+                                                                       uint32_t* cursor, float4* trec, float4* tdir,
+                                                                       uint32_t* dest2) {
   extern __shared__ __align__(16) uint8_t qsm[];
   QbStage& st = *reinterpret_cast<QbStage*>(qsm);
   uint32_t* hist = reinterpret_cast<uint32_t*>(qsm + sizeof(QbStage));
   uint32_t* lbase = hist + GF_QB_SUPER;
   uint32_t* gbase = lbase + GF_QB_SUPER;
   for (int64_t t0 = (int64_t)blockIdx.x * GF_QB_TILE; t0 < n; t0 += (int64_t)gridDim.x * GF_QB_TILE) {
-    qb_stage_scatter(st, hist, lbase, gbase, GF_QB_SUPER, cursor, sb, trec, tdir,
+    qb_stage_scatter(st, hist, lbase, gbase, GF_QB_SUPER, cursor, sb, trec, tdir, dest2, t0,
                      [&](int k, float4& r, float4& d) -> int {
                        const int64_t i = t0 + k;
                        if (i >= n) return -1;
@@ -287,7 +291,8 @@ __global__ void __launch_bounds__(GF_QB_THREADS, 2) k_query_move_cell(const uint
                                                                       int64_t n_cells, int sb,
                                                                       const float4* __restrict__ trec,
                                                                       const float4* __restrict__ tdir,
-                                                                      uint32_t* cursor, float4* srec, float4* sdir) {
+                                                                      uint32_t* cursor, float4* srec, float4* sdir,
+                                                                      uint32_t* dest3) {
   extern __shared__ __align__(16) uint8_t qsm[];
   QbStage& st = *reinterpret_cast<QbStage*>(qsm);
   uint32_t* hist = reinterpret_cast<uint32_t*>(qsm + sizeof(QbStage));
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(GF_QB_THREADS, 2) k_query_move_cell(const uint
   const uint32_t s0 = offsets[(uint32_t)s << sb], s1 = offsets[min((uint32_t)(s + 1) << sb, (uint32_t)n_cells)];
   const uint32_t nb = 1u << sb;
   for (uint32_t t0 = s0 + blockIdx.x * GF_QB_TILE; t0 < s1; t0 += gridDim.x * GF_QB_TILE) {
-    qb_stage_scatter(st, hist, lbase, gbase, (int)nb, cursor + ((uint32_t)s << sb), 0, srec, sdir,
+    qb_stage_scatter(st, hist, lbase, gbase, (int)nb, cursor + ((uint32_t)s << sb), 0, srec, sdir, dest3, t0,
                      [&](int k, float4& r, float4& d) -> int {
                        const uint32_t row = t0 + (uint32_t)k;
                        if (row >= s1) return -1;
@@ -306,6 +311,41 @@ __global__ void __launch_bounds__(GF_QB_THREADS, 2) k_query_move_cell(const uint
                        return (int)(__float_as_uint(d.w) & (nb - 1u));
                      });
   }
+}
+
+// results back to caller order in two gathers that mirror the two sort
+// levels (each reads from <= 64 advancing runs, so the gathers stay local;
+// scattering results from the MLP would cost DRAM read-modify-writes):
+//   super order: so[t] = sorted_out[dest3[t]];   caller order: out[i] = so[dest2[i]]
+__global__ void __launch_bounds__(256) k_query_unperm_super(const uint32_t* __restrict__ n_valid,
+                                                            const uint32_t* __restrict__ dest3,
+                                                            const float4* __restrict__ sorted_out, float4* so) {
+  const uint32_t nv = *n_valid;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nv; t += gridDim.x * blockDim.x)
+    so[t] = sorted_out[dest3[t]];
+}
+
+__global__ void __launch_bounds__(256) k_query_unperm_caller(int64_t n, const uint32_t* __restrict__ keys,
+                                                             const uint32_t* __restrict__ dest2,
+                                                             const float4* __restrict__ so, float* rgb, float* sigma) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (keys[i] == 0xFFFFFFFFu) continue;  // out of bounds: the call reports an error
+    const float4 v = so[dest2[i]];
+    rgb[3 * i + 0] = v.x;
+    rgb[3 * i + 1] = v.y;
+    rgb[3 * i + 2] = v.z;
+    sigma[i] = v.w;
+  }
+}
+
+int launch_query_unpermute(int64_t n, const uint32_t* n_valid, const uint32_t* keys, const uint32_t* dest2,
+                           const uint32_t* dest3, const float4* sorted_out, float4* so, float* rgb, float* sigma,
+                           cudaStream_t st) {
+  if (n == 0) return 0;
+  const unsigned grid = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(n, 256), (int64_t)num_sms() * 16);
+  k_query_unperm_super<<<grid, 256, 0, st>>>(n_valid, dest3, sorted_out, so);
+  k_query_unperm_caller<<<grid, 256, 0, st>>>(n, keys, dest2, so, rgb, sigma);
+  return 2;
 }
 
 bool query_bucket_fast_ok(int64_t n, int64_t n_cells) {
@@ -323,7 +363,7 @@ size_t query_stage_smem() { return sizeof(QbStage) + 3 * (size_t)(1 << GF_QB_SUB
 
 int launch_query_bucket(const GfGrid& g, const float* pos, const float* dir, int64_t n, int64_t n_cells,
                         uint32_t* keys, const BucketBufs& B, float4* trec, float4* tdir, uint32_t* cursor2,
-                        int64_t* err, cudaStream_t st, int pass) {
+                        uint32_t* dest2, uint32_t* dest3, int64_t* err, cudaStream_t st, int pass) {
   if (n == 0) return 0;
   const int sb = query_super_shift(n_cells);
   if (pass == 1) {
@@ -347,11 +387,11 @@ int launch_query_bucket(const GfGrid& g, const float* pos, const float* dir, int
   // cursors: B.cursor = offsets (set by k_scan_cells) serves pass 3; pass 2
   // uses a copy (its super-cell runs start at the same offsets)
   cudaMemcpyAsync(cursor2, B.cursor, (size_t)n_cells * 4, cudaMemcpyDeviceToDevice, st);
-  k_query_move_super<<<num_sms() * 2, GF_QB_THREADS, smem, st>>>(pos, dir, n, sb, keys, cursor2, trec, tdir);
+  k_query_move_super<<<num_sms() * 2, GF_QB_THREADS, smem, st>>>(pos, dir, n, sb, keys, cursor2, trec, tdir, dest2);
   const int n_super = (int)((n_cells - 1) >> sb) + 1;
   const unsigned per_super = (unsigned)std::max<int64_t>(1, (int64_t)num_sms() * 2 / n_super + 1);
   k_query_move_cell<<<dim3(per_super, (unsigned)n_super), GF_QB_THREADS, smem, st>>>(B.offsets, n_cells, sb, trec, tdir,
-                                                                                      B.cursor, B.srec, B.sdir);
+                                                                                      B.cursor, B.srec, B.sdir, dest3);
   return 2;
 }
 

@@ -38,7 +38,10 @@ bool query_bucket_fast_ok(int64_t n, int64_t n_cells);
 // pass 1 -> 1 launch; pass 2 -> 2 launches (returned)
 int launch_query_bucket(const GfGrid& g, const float* pos, const float* dir, int64_t n, int64_t n_cells,
                         uint32_t* keys, const BucketBufs& B, float4* trec, float4* tdir, uint32_t* cursor2,
-                        int64_t* err, cudaStream_t st, int pass);
+                        uint32_t* dest2, uint32_t* dest3, int64_t* err, cudaStream_t st, int pass);
+int launch_query_unpermute(int64_t n, const uint32_t* n_valid, const uint32_t* keys, const uint32_t* dest2,
+                           const uint32_t* dest3, const float4* sorted_out, float4* so, float* rgb, float* sigma,
+                           cudaStream_t st);
 int num_sms();
 void launch_query_keys(const GfGrid& g, const float* pos, int64_t n, uint32_t* keys, uint32_t* counts, int64_t* err,
                        cudaStream_t st);

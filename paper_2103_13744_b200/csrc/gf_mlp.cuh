@@ -94,7 +94,7 @@ struct RenderIO {
 #pragma unroll
     for (int c = 0; c < 4; ++c) de[c] = q[c];
   }
-  __device__ __forceinline__ void store(uint32_t idx, float r, float g, float b, float s) const {
+  __device__ __forceinline__ void store(uint32_t idx, uint32_t, float r, float g, float b, float s) const {
     res[idx] = make_float4(r, g, b, s);
   }
 };
@@ -128,7 +128,12 @@ struct QueryIO {
       d[0] = q[0]; d[1] = q[1]; d[2] = q[2];
     }
   }
-  __device__ __forceinline__ void store(uint32_t row, float r, float g, float b, float s) const {
+  float4* sorted_out;        // bulk path: results in sorted-row order (un-permuted by a coalesced gather pass)
+  __device__ __forceinline__ void store(uint32_t row, uint32_t srow, float r, float g, float b, float s) const {
+    if (sorted_out) {
+      sorted_out[srow] = make_float4(r, g, b, s);
+      return;
+    }
     const uint64_t idx = store_idx ? (uint64_t)store_idx[row] : (uint64_t)row;
     rgb[3ull * idx + 0] = r;
     rgb[3ull * idx + 1] = g;

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(128) k_mlp_fp32(const float* __restrict__ pack
     dense_f32<W + D, DP, W, true>(sw + L.w_off[T + 2], sw + L.b_off[T + 2], cat, h2);
     float z[3];
     dense_f32<W, WP, 3, false>(sw + L.w_off[T + 3], sw + L.b_off[T + 3], h2, z);
-    io.store(idx, sigmoid_split(z[0]), sigmoid_split(z[1]), sigmoid_split(z[2]), sig[0]);
+    io.store(idx, tl.y + threadIdx.x, sigmoid_split(z[0]), sigmoid_split(z[1]), sigmoid_split(z[2]), sig[0]);
   }
 }
 

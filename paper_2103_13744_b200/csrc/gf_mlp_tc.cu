@@ -480,7 +480,7 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
             const float e = __expf(-fabsf(v)), r = __fdividef(1.f, 1.f + e);  // sign-split sigmoid (mlp.py:228-235)
             rgb[c] = v >= 0.f ? r : e * r;
           }
-          if (row.valid) io.store(row.idx, rgb[0], rgb[1], rgb[2], sigma);
+          if (row.valid) io.store(row.idx, row.row, rgb[0], rgb[1], rgb[2], sigma);
         }
         if (L < 4) {
           publish();
