@@ -119,6 +119,7 @@ struct GraphKey {
 
 struct GraphEntry {
   std::vector<unsigned char> key;
+  std::vector<unsigned char> topo;  // launch structure only (no per-view values)
   int dev;
   cudaGraphExec_t exec;
   int64_t launches;
@@ -129,8 +130,11 @@ static std::mutex g_graph_mu;
 static std::vector<GraphEntry> g_graphs;
 static uint64_t g_graph_tick = 0;
 
+// A new argument set with the launch structure of a cached graph (a new
+// camera, seed or output buffer) is captured and applied to that graph with
+// cudaGraphExecUpdate, which costs far less than a fresh instantiation.
 template <class F>
-static int run_graph(const GraphKey& k, cudaStream_t st, F&& enqueue) {
+static int run_graph(const GraphKey& k, const GraphKey& topo, cudaStream_t st, F&& enqueue) {
   int dev = 0;
   cudaGetDevice(&dev);
   {
@@ -153,6 +157,23 @@ static int run_graph(const GraphKey& k, cudaStream_t st, F&& enqueue) {
   cudaGraph_t g = nullptr;
   cudaError_t err = cudaStreamEndCapture(st, &g);
   if (err != cudaSuccess) return fail(GF_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(err));
+  {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (auto& e : g_graphs) {
+      if (e.dev != dev || e.topo != topo.b) continue;
+      cudaGraphExecUpdateResultInfo info;
+      if (cudaGraphExecUpdate(e.exec, g, &info) == cudaSuccess) {
+        cudaGraphDestroy(g);
+        e.key = k.b;
+        e.last_use = ++g_graph_tick;
+        g_launches += e.launches;
+        cudaGraphLaunch(e.exec, st);
+        return check_cuda("gf_render_rays (graph update)");
+      }
+      cudaGetLastError();  // structure differs after all: instantiate below
+      break;
+    }
+  }
   cudaGraphExec_t ex = nullptr;
   err = cudaGraphInstantiate(&ex, g, 0);
   cudaGraphDestroy(g);
@@ -167,7 +188,7 @@ static int run_graph(const GraphKey& k, cudaStream_t st, F&& enqueue) {
       cudaGraphExecDestroy(lru->exec);
       g_graphs.erase(lru);
     }
-    g_graphs.push_back(GraphEntry{k.b, dev, ex, g_launches.load() - l0, ++g_graph_tick});
+    g_graphs.push_back(GraphEntry{k.b, topo.b, dev, ex, g_launches.load() - l0, ++g_graph_tick});
   }
   return check_cuda("gf_render_rays (graph)");
 }
@@ -641,7 +662,6 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   key.add(packed);
   key.add(precision);
   key.add(nc);
-  key.add(cfg->seed);
   key.add(n_blocks);
   key.add(stride);
   key.add(cplan.on);
@@ -653,7 +673,19 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   key.add(march_blocks);
   key.add(ray_blocks);
   key.add(t);
-  return run_graph(key, st, enqueue);
+  const size_t n_shared = key.b.size() - sizeof(P);
+  key.add(cfg->seed);
+  // structure key: the same launches with per-view values (camera, rays, seed, outputs) cleared
+  MarchParams Pt = P;
+  memset(&Pt.cam, 0, sizeof(Pt.cam));
+  Pt.origins = Pt.dirs = nullptr;
+  Pt.ray_offset = Pt.first_block = 0;
+  Pt.rgb_out = nullptr;
+  Pt.stats = nullptr;
+  GraphKey topo;
+  topo.add(Pt);
+  topo.b.insert(topo.b.end(), key.b.begin() + sizeof(P), key.b.begin() + sizeof(P) + n_shared);
+  return run_graph(key, topo, st, enqueue);
 }
 
 // ---------------------------------------------------------------------------

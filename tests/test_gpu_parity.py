@@ -329,3 +329,24 @@ def test_deterministic_across_runs(gf):
     assert np.array_equal(a, b) and sa.total_queries == sb.total_queries
     c, _ = gf.render_image(g, occ, cam, gf.RenderConfig(), seed=8)
     assert not np.array_equal(a, c)
+
+
+def test_graph_reuse_across_views_bit_identical(gf, monkeypatch):
+    """Views, seeds and output buffers change between calls while the cached
+    CUDA graph is updated in place (cudaGraphExecUpdate): every frame must be
+    bit-identical to an eager (uncaptured) render of the same call."""
+    aabb = unit(gf)
+    g = gf.init_network_grid(aabb, (16, 16, 16), seed=0)
+    g.params.biases["density"][:] = 20.0
+    from conftest import toy_occupancy_bits
+
+    res, bits = toy_occupancy_bits()
+    occ = gf.OccupancyGrid(aabb, res, bits.copy())
+    cams = gf.sphere_cameras(aabb, 3, 40, seed=4)
+    cfg = gf.RenderConfig(k=96)
+    got = [gf.render_image(g, occ, cams[i % 3], cfg, seed=i, precision="fp16") for i in range(6)]
+    monkeypatch.setenv("GF_NO_GRAPH", "1")
+    for i in range(6):
+        img, st = gf.render_image(g, occ, cams[i % 3], cfg, seed=i, precision="fp16")
+        assert np.array_equal(img, got[i][0])
+        assert st.to_dict() | {"wall_ms": 0} == got[i][1].to_dict() | {"wall_ms": 0}
