@@ -452,6 +452,18 @@ def main():
     e2e = {"value": world * n_pix / e2e_s / 1e6, "unit": UNIT,
            "h2d_bytes_per_step": int(N.C.sizeof(N.CameraT) + N.C.sizeof(N.MarchCfg)),
            "d2h_bytes_per_step": int(img.nbytes + 32), "ms_per_frame": e2e_s * 1e3}
+    if args.workload == "c2":
+        # the C3 view batch through the same API, a different camera every frame
+        # (each new view updates the cached frame graph in place)
+        views = gf.sphere_cameras(aabb, 64, SIZE, seed=0)
+        vt = []
+        for v in views[rank::world] if world > 1 else views:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            gf.render_image(grid, occ, v, cfg, seed=0)
+            vt.append(time.perf_counter() - t0)
+        e2e["views"] = {"n": len(vt), "median_ms_per_frame": statistics.median(vt) * 1e3,
+                        "max_ms_per_frame": max(vt) * 1e3}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
