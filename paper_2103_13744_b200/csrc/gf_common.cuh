@@ -197,6 +197,34 @@ __device__ __forceinline__ float gf_clip_component(float p, double lo, double hi
 __device__ __forceinline__ float gf_clip_fast(float p, float lo, float hi) { return fminf(fmaxf(p, lo), hi); }
 
 // ---------------------------------------------------------------------------
+// L2 residency hints for the per-round staging buffers: records written by
+// one kernel and read once by the next are stored evict_last and loaded
+// evict_first, so they survive the streaming traffic in between.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t gf_pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t gf_pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float4 gf_ld_hint(const float4* a, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void gf_st_hint(float4* a, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w), "l"(pol)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // misc
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned gf_lane() { return threadIdx.x & 31u; }

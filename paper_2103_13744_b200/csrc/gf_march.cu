@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
   // lane has an independent load -> cell -> store chain in flight
   const uint32_t n_list = RB.emit_count[round & 1];
   const unsigned lane = gf_lane();
+  const uint64_t pol_first = gf_pol_first(), pol_last = gf_pol_last();
   const uint64_t warp_g = gtid >> 5, n_warps = gthreads >> 5;
   for (uint64_t k0 = warp_g * 32; k0 < n_list; k0 += n_warps * 32) {
     const uint64_t k = k0 + lane;
@@ -453,13 +454,14 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
         const uint32_t i_o = __shfl_sync(0xffffffffu, i, own);
         ok[u] = q < total;
         src[u] = i_o * (uint32_t)stride + j;  // staging index (< 2^32, checked on the host)
-        if (ok[u]) r[u] = RB.rec[src[u]];
+        if (ok[u]) r[u] = gf_ld_hint(RB.rec + src[u], pol_first);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (ok[u]) {
           const uint32_t cell = gf_flat_cell(grid, r[u].x, r[u].y, r[u].z);
-          Bk.srec[off[cell] + __float_as_uint(r[u].w)] = make_float4(r[u].x, r[u].y, r[u].z, __uint_as_float(src[u]));
+          gf_st_hint(Bk.srec + off[cell] + __float_as_uint(r[u].w),
+                     make_float4(r[u].x, r[u].y, r[u].z, __uint_as_float(src[u])), pol_last);
         }
       }
     }
@@ -534,8 +536,9 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     const uint64_t base = (uint64_t)i * (uint64_t)P.stride;
     const uint32_t n = R.run[i];
     float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
+    const uint64_t pol_first = gf_pol_first();
     for (uint32_t j = 0; j < n; ++j) {
-      float4 q = B.res[base + j];
+      float4 q = gf_ld_hint(B.res + base + j, pol_first);
       float a = -expm1f(__fmul_rn(-q.w, seg));
       float w = __fmul_rn(tr, a);
       tr = __fmul_rn(tr, __fsub_rn(1.0f, a));
@@ -743,7 +746,8 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       const uint32_t crank = hist_rank(counts_r, keep, cell);
       if (keep) {
         const uint32_t pos = s_ray[wib][own].carry + __popc(kb & same & ((1u << lane) - 1u));
-        B.rec[(uint64_t)i_o * (uint64_t)P.stride + pos] = make_float4(px, py, pz, __uint_as_float(crank));
+        gf_st_hint(B.rec + (uint64_t)i_o * (uint64_t)P.stride + pos, make_float4(px, py, pz, __uint_as_float(crank)),
+                   gf_pol_last());
         if (P.trace) {
           unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
           if ((int64_t)slotpos < P.trace_capacity)

@@ -81,7 +81,7 @@ struct RenderIO {
   // sorted row -> (staging index, position[, direction])
   template <bool DIR>
   __device__ __forceinline__ void fetch(const TileSched& S, uint32_t row, uint32_t& idx, float* x, float* d) const {
-    const float4 r = S.srec[row];
+    const float4 r = gf_ld_hint(S.srec + row, gf_pol_first());
     idx = __float_as_uint(r.w);
     x[0] = r.x; x[1] = r.y; x[2] = r.z;
     if (DIR) {
@@ -95,7 +95,7 @@ struct RenderIO {
     for (int c = 0; c < 4; ++c) de[c] = q[c];
   }
   __device__ __forceinline__ void store(uint32_t idx, uint32_t, float r, float g, float b, float s) const {
-    res[idx] = make_float4(r, g, b, s);
+    gf_st_hint(res + idx, make_float4(r, g, b, s), gf_pol_last());  // read by the next march pass
   }
 };
 
