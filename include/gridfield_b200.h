@@ -178,6 +178,43 @@ GF_API int gf_composite_f64(const double* colors_dev, const double* alphas_dev, 
 /* render.py:139-148 generate_rays for a camera (float32 origins, dirs).    */
 GF_API int gf_generate_rays(const gf_camera_t* cam, float* origins_dev, float* dirs_dev, void* stream);
 
+/* --- analytic test scenes (scene.py:27-135) ---------------
+ * The closed-form AnalyticScene field (spheres, then boxes, in the
+ * reference's iteration order) evaluated on the device in place of the MLPs,
+ * so scene renders (the reference's ERT-bound / ESS-exactness acceptance
+ * checks, render_image(scene, ...)) run through the same marcher.          */
+#define GF_MAX_PRIMS 16
+typedef struct {
+  int32_t kind;            /* 0 Sphere(center=a, radius), 1 Box(lo=a, hi=b)  */
+  int32_t _pad;
+  double a[3], b[3];
+  double color[3];
+  double radius, density, feather;
+} gf_prim_t;
+
+typedef struct {
+  double b_min[3], b_max[3];  /* scene.aabb                                  */
+  int32_t n_prims;
+  int32_t _pad;
+  gf_prim_t prims[GF_MAX_PRIMS];
+  double texture_freq, texture_amp, view_tint;
+  double tint_axis[3];
+} gf_analytic_t;
+
+/* AnalyticScene.query_points (scene.py:115-135) for n float32 points.      */
+GF_API int gf_query_analytic(const gf_analytic_t* scene, const float* pos_dev, const float* dir_dev, int64_t n,
+                             float* rgb_dev, float* sigma_dev, void* stream);
+/* render.render_rays / render_image with an AnalyticScene field: arguments as
+ * gf_render_rays minus the network (the scene box is the march box).       */
+GF_API size_t gf_render_analytic_workspace_bytes(const gf_analytic_t* scene, const gf_march_cfg_t* cfg,
+                                                 int64_t n_rays);
+GF_API int gf_render_rays_analytic(const gf_analytic_t* scene, const gf_grid_geom_t* occ, const uint8_t* occ_bits_dev,
+                                   const gf_march_cfg_t* cfg, const gf_camera_t* cam, const float* origins_dev,
+                                   const float* dirs_dev, int64_t ray_offset, int64_t ray_block_stride, int64_t n_rays,
+                                   float* rgb_dev, int64_t* stats_dev, gf_trace_rec_t* trace_dev,
+                                   int64_t trace_capacity, int64_t* trace_count_dev, void* ws_dev, size_t ws_bytes,
+                                   void* stream);
+
 /* --- instrumentation ------------------------------------------------------
  * Stage timing: while enabled, gf_render_rays / gf_query_points record CUDA
  * events on their stream between stages; gf_stage_times() synchronises and

@@ -41,6 +41,10 @@ def stream_handle() -> int:
     return torch().cuda.current_stream().cuda_stream
 
 
+def is_tensor(a) -> bool:
+    return isinstance(a, torch().Tensor)
+
+
 def to_device(a, dtype) -> "object":
     """numpy array (or torch tensor) -> contiguous device tensor of ``dtype``."""
     t = require_cuda()

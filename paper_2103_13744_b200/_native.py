@@ -47,6 +47,20 @@ class CameraT(C.Structure):
     ]
 
 
+MAX_PRIMS = 16
+
+
+class Prim(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("_pad", C.c_int32), ("a", C.c_double * 3), ("b", C.c_double * 3),
+                ("color", C.c_double * 3), ("radius", C.c_double), ("density", C.c_double), ("feather", C.c_double)]
+
+
+class Analytic(C.Structure):
+    _fields_ = [("b_min", C.c_double * 3), ("b_max", C.c_double * 3), ("n_prims", C.c_int32), ("_pad", C.c_int32),
+                ("prims", Prim * MAX_PRIMS), ("texture_freq", C.c_double), ("texture_amp", C.c_double),
+                ("view_tint", C.c_double), ("tint_axis", C.c_double * 3)]
+
+
 TRACE_DTYPE = np.dtype([("x", "<f4"), ("y", "<f4"), ("z", "<f4"), ("ray", "<u4"), ("slot", "<u4"), ("cell", "<u4")])
 
 _P = C.c_void_p
@@ -78,6 +92,11 @@ _SIGS = {
     "gf_composite_f64": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P, _P]),
     "gf_generate_rays": (C.c_int, [C.POINTER(CameraT), _P, _P, _P]),
     "gf_pcg64_block_state": (C.c_int, [C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]),
+    "gf_query_analytic": (C.c_int, [C.POINTER(Analytic), _P, _P, C.c_int64, _P, _P, _P]),
+    "gf_render_analytic_workspace_bytes": (C.c_size_t, [C.POINTER(Analytic), C.POINTER(MarchCfg), C.c_int64]),
+    "gf_render_rays_analytic": (C.c_int, [C.POINTER(Analytic), C.POINTER(GridGeom), _P, C.POINTER(MarchCfg),
+                                          C.POINTER(CameraT), _P, _P, C.c_int64, C.c_int64, C.c_int64, _P, _P, _P,
+                                          C.c_int64, _P, _P, C.c_size_t, _P]),
     "gf_stage_timing": (C.c_int, [C.c_int32]),
     "gf_stage_times": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "gf_launch_count": (C.c_int64, []),

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <string>
 
+#include "gf_analytic.cuh"
 #include "gf_march.cuh"
 #include "gf_mlp.cuh"
 
@@ -453,13 +454,17 @@ size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* gr
                       (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk, &w);
 }
 
-int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed, int precision,
-                   const gf_grid_geom_t* occ, const uint8_t* occ_bits, const gf_march_cfg_t* cfg,
-                   const gf_camera_t* cam, const float* origins, const float* dirs, int64_t ray_offset,
-                   int64_t ray_block_stride, int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace, int64_t trace_capacity,
-                   int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
+// The render pipeline for a NetworkGrid field (an == NULL: bucketed
+// per-cell MLPs) or an analytic scene (an != NULL: one bucket, closed-form
+// field).  Everything else (rays, sampling, ESS, compositing, ERT, graphs)
+// is shared.
+static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_grid_geom_t* grid, const void* packed,
+                       int precision, const gf_grid_geom_t* occ, const uint8_t* occ_bits, const gf_march_cfg_t* cfg,
+                       const gf_camera_t* cam, const float* origins, const float* dirs, int64_t ray_offset,
+                       int64_t ray_block_stride, int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace,
+                       int64_t trace_capacity, int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
   LayerTable t{};  // value-initialised: hashed into the graph key
-  if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_render_rays: bad architecture");
+  if (!an && (!arch || !make_layer_table(arch, &t))) return fail(GF_ERR_INVALID, "gf_render_rays: bad architecture");
   if (!valid_grid(grid)) return fail(GF_ERR_INVALID, "gf_render_rays: bad grid");
   if (!cfg || cfg->k < 1 || cfg->ert_chunk < 1 || !(cfg->epsilon >= 0.0 && cfg->epsilon < 1.0))
     return fail(GF_ERR_INVALID, "gf_render_rays: bad march config");
@@ -619,9 +624,10 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   int stride_shift = -1;
   for (int b = 0; b < 31; ++b)
     if ((1 << b) == stride) stride_shift = b;
-  if (precision != GF_PRECISION_FP16) w.R.denc = nullptr;  // only the tensor-core MLP reads gamma(d) per ray
+  if (an || precision != GF_PRECISION_FP16) w.R.denc = nullptr;  // only the tensor-core MLP reads gamma(d) per ray
   RenderIO io{w.RB.res, w.R.dir, (uint32_t)stride, w.R.denc, stride_shift};
-  const bool mlp_ok = precision == GF_PRECISION_FP16   ? prepare_mlp_tc(t)
+  const bool mlp_ok = an                                 ? true
+                      : precision == GF_PRECISION_FP16   ? prepare_mlp_tc(t)
                       : precision == GF_PRECISION_FP32 ? prepare_mlp_fp32(t)
                                                        : false;
   if (!mlp_ok) return fail(GF_ERR_UNSUPPORTED, "gf_render_rays: no MLP kernel for this architecture/precision");
@@ -643,7 +649,11 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
       k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r);
       stage_mark(s, GF_STAGE_MARCH, 1);
       stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, r, (int64_t)n_rays * stride, s));
-      run_mlp(t, packed, precision, S, &io, nullptr, s);
+      if (an)
+        launch_field_analytic(*an, w.B.offsets, w.B.srec, w.R.dir, stride_shift, (uint32_t)stride, w.RB.res,
+                              (int64_t)n_rays * stride, s);
+      else
+        run_mlp(t, packed, precision, S, &io, nullptr, s);
       stage_mark(s, GF_STAGE_MLP, 1);
     }
     k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, P.n_rounds);
@@ -651,7 +661,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   };
   // graphs for the production (tensor-core) path; the fp32 reference mode,
   // traces and stage timing run eagerly
-  const bool use_graph = precision == GF_PRECISION_FP16 && !g_timer.on && !trace && !getenv("GF_NO_GRAPH");
+  const bool use_graph = (an || precision == GF_PRECISION_FP16) && !g_timer.on && !trace && !getenv("GF_NO_GRAPH");
   if (!use_graph) {
     enqueue(st);
     return check_cuda("gf_render_rays");
@@ -673,6 +683,8 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   key.add(march_blocks);
   key.add(ray_blocks);
   key.add(t);
+  key.add(an != nullptr);
+  if (an) key.add(*an);
   const size_t n_shared = key.b.size() - sizeof(P);
   key.add(cfg->seed);
   // structure key: the same launches with per-view values (camera, rays, seed, outputs) cleared
@@ -686,6 +698,56 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
   topo.add(Pt);
   topo.b.insert(topo.b.end(), key.b.begin() + sizeof(P), key.b.begin() + sizeof(P) + n_shared);
   return run_graph(key, topo, st, enqueue);
+}
+
+int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void* packed, int precision,
+                   const gf_grid_geom_t* occ, const uint8_t* occ_bits, const gf_march_cfg_t* cfg,
+                   const gf_camera_t* cam, const float* origins, const float* dirs, int64_t ray_offset,
+                   int64_t ray_block_stride, int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace,
+                   int64_t trace_capacity, int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
+  return render_impl(arch, nullptr, grid, packed, precision, occ, occ_bits, cfg, cam, origins, dirs, ray_offset,
+                     ray_block_stride, n_rays, rgb, stats, trace, trace_capacity, trace_count, ws, ws_bytes, stream);
+}
+
+// ---------------------------------------------------------------------------
+// analytic scenes (scene.py:77-135)
+// ---------------------------------------------------------------------------
+static gf_grid_geom_t analytic_box(const gf_analytic_t* s) {
+  gf_grid_geom_t g;
+  for (int a = 0; a < 3; ++a) {
+    g.b_min[a] = s->b_min[a];
+    g.b_max[a] = s->b_max[a];
+    g.res[a] = 1;  // one bucket: the field has no cells
+  }
+  return g;
+}
+
+size_t gf_render_analytic_workspace_bytes(const gf_analytic_t* scene, const gf_march_cfg_t* cfg, int64_t n_rays) {
+  if (!scene) return 0;
+  const gf_grid_geom_t g = analytic_box(scene);
+  return gf_render_workspace_bytes(nullptr, &g, cfg, n_rays);
+}
+
+int gf_render_rays_analytic(const gf_analytic_t* scene, const gf_grid_geom_t* occ, const uint8_t* occ_bits,
+                            const gf_march_cfg_t* cfg, const gf_camera_t* cam, const float* origins, const float* dirs,
+                            int64_t ray_offset, int64_t ray_block_stride, int64_t n_rays, float* rgb, int64_t* stats,
+                            gf_trace_rec_t* trace, int64_t trace_capacity, int64_t* trace_count, void* ws,
+                            size_t ws_bytes, void* stream) {
+  AnalyticDev A;
+  memset(&A, 0, sizeof(A));
+  if (!make_analytic(scene, &A)) return fail(GF_ERR_INVALID, "gf_render_rays_analytic: bad scene");
+  const gf_grid_geom_t g = analytic_box(scene);
+  return render_impl(nullptr, &A, &g, nullptr, GF_PRECISION_FP32, occ, occ_bits, cfg, cam, origins, dirs, ray_offset,
+                     ray_block_stride, n_rays, rgb, stats, trace, trace_capacity, trace_count, ws, ws_bytes, stream);
+}
+
+int gf_query_analytic(const gf_analytic_t* scene, const float* pos, const float* dir, int64_t n, float* rgb,
+                      float* sigma, void* stream) {
+  AnalyticDev A;
+  memset(&A, 0, sizeof(A));
+  if (!make_analytic(scene, &A) || n < 0) return fail(GF_ERR_INVALID, "gf_query_analytic: bad scene or size");
+  launch_query_analytic(A, pos, dir, n, rgb, sigma, (cudaStream_t)stream);
+  return check_cuda("gf_query_analytic");
 }
 
 // ---------------------------------------------------------------------------

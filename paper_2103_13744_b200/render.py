@@ -244,14 +244,28 @@ def composite(colors, alphas):
 # the marcher
 # ---------------------------------------------------------------------------
 def _field_grid(field):
+    """render.py:361-364 field protocol: NetworkGrid (per-cell MLPs) and
+    AnalyticScene (closed-form field) both march on the device."""
     from .grid import NetworkGrid
+    from .scene import AnalyticScene
 
-    if isinstance(field, NetworkGrid):
+    if isinstance(field, (NetworkGrid, AnalyticScene)):
         return field
     raise NotImplementedError(
-        f"the device marcher evaluates NetworkGrid fields; got {type(field).__name__} "
-        "(analytic fields are not on the B200 hot path yet)"
+        f"the device marcher evaluates NetworkGrid and AnalyticScene fields; got {type(field).__name__}"
     )
+
+
+def _is_analytic(field) -> bool:
+    from .scene import AnalyticScene
+
+    return isinstance(field, AnalyticScene)
+
+
+def _render_ws_bytes(field, ncfg, n: int) -> int:
+    if _is_analytic(field):
+        return N.lib().gf_render_analytic_workspace_bytes(field.native(), ncfg, n)
+    return N.lib().gf_render_workspace_bytes(field.native_arch(), field.native_geom(), ncfg, n)
 
 
 def shard_rays(n_rays: int, rank: int, world: int) -> tuple[int, int, int]:
@@ -307,8 +321,10 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
     for pixels [ray_offset, ray_offset + n_rays), or for the interleaved
     blocks of ``shard_rays`` when ``block_stride`` > 1."""
     t = D.require_cuda()
-    p = grid.resolved_precision(precision)
-    packed = grid.device_params(p)
+    analytic = _is_analytic(grid)
+    if not analytic:
+        p = grid.resolved_precision(precision)
+        packed = grid.device_params(p)
     if cam is not None:
         total = cam.width * cam.height
         n = total - ray_offset if n_rays is None else int(n_rays)
@@ -320,7 +336,6 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
         n = o_d.shape[0]
         ccam = None
     ncfg = cfg.native(seed)
-    arch, geom = grid.native_arch(), grid.native_geom()
     if occupancy is not None:
         occ_geom, occ_bits = occupancy.native_geom(), occupancy.device_bits()
     else:
@@ -332,11 +347,17 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
         trace = D.empty((trace_capacity * N.TRACE_DTYPE.itemsize,), t.uint8)
         tcount = t.zeros(1, dtype=t.int64, device=rgb.device)
     if ws is None:
-        ws = D.workspace(N.lib().gf_render_workspace_bytes(arch, geom, ncfg, n))
-    N.check(N.lib().gf_render_rays(
-        arch, geom, N.ptr(packed), N.PRECISION[p], occ_geom, N.ptr(occ_bits), ncfg, ccam, N.ptr(o_d), N.ptr(d_d),
-        int(ray_offset), int(block_stride), int(n), N.ptr(rgb), N.ptr(st), N.ptr(trace), int(trace_capacity), N.ptr(tcount),
-        N.ptr(ws), ws.numel(), D.stream_handle()), "render_rays")
+        ws = D.workspace(_render_ws_bytes(grid, ncfg, n))
+    if analytic:
+        N.check(N.lib().gf_render_rays_analytic(
+            grid.native(), occ_geom, N.ptr(occ_bits), ncfg, ccam, N.ptr(o_d), N.ptr(d_d), int(ray_offset),
+            int(block_stride), int(n), N.ptr(rgb), N.ptr(st), N.ptr(trace), int(trace_capacity), N.ptr(tcount),
+            N.ptr(ws), ws.numel(), D.stream_handle()), "render_rays")
+    else:
+        N.check(N.lib().gf_render_rays(
+            grid.native_arch(), grid.native_geom(), N.ptr(packed), N.PRECISION[p], occ_geom, N.ptr(occ_bits), ncfg,
+            ccam, N.ptr(o_d), N.ptr(d_d), int(ray_offset), int(block_stride), int(n), N.ptr(rgb), N.ptr(st),
+            N.ptr(trace), int(trace_capacity), N.ptr(tcount), N.ptr(ws), ws.numel(), D.stream_handle()), "render_rays")
     tr = None
     if trace_capacity:
         cnt = int(tcount.item())
@@ -378,7 +399,7 @@ def render_image(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0
     t = D.require_cuda()
     n = cam.width * cam.height
     ncfg = cfg.native(seed)
-    ws_bytes = N.lib().gf_render_workspace_bytes(grid.native_arch(), grid.native_geom(), ncfg, n)
+    ws_bytes = _render_ws_bytes(grid, ncfg, n)
     c = _render_context(n, ws_bytes)
     c["stats"].zero_()
     rgb, st, _ = render_rays_device(grid, occupancy, cfg, seed, cam=cam, precision=precision, out=c["rgb"],

@@ -240,8 +240,51 @@ def gen_bulk():
     save("query_c5", pts=pts, dirs=dirs, rgb=c, sigma=s, keys=g.cell_index(pts))
 
 
+def gen_scene():
+    """Analytic scenes (scene.py) through the reference's
+    render_image: dense / ESS / ERT renders and field queries."""
+    sc = scene.standard_toy_scene()
+    aabb = sc.aabb
+    cam48 = scene.sphere_cameras(aabb, 1, 48, seed=3)[0]
+    cfg = render.RenderConfig(k=128, stratified=False)
+    for name, c, occ in (("render_scene_ert", cfg, None), ("render_scene_dense", cfg.replace(epsilon=0.0), None)):
+        img, st = render.render_image(sc, occ, cam48, c, seed=0)
+        save(name, image=img, total_queries=np.int64(st.total_queries), ess_skipped=np.int64(st.ess_skipped),
+             ert_terminated_rays=np.int64(st.ert_terminated_rays), n_rays=np.int64(st.n_rays), k=np.int64(c.k),
+             epsilon=np.float64(c.epsilon), background=np.array(c.background, np.float64),
+             ert_chunk=np.int64(c.ert_chunk), stratified=np.bool_(c.stratified), seed=np.int64(0), **cam_arrays(cam48))
+    occ = occupancy.extract_occupancy(sc.density_at, aabb, (32, 32, 32), tau=0.0)
+    cam_b = scene.sphere_cameras(aabb, 1, 48, seed=4)[0]
+    c = cfg.replace(epsilon=0.0)
+    img, st = render.render_image(sc, occ, cam_b, c, seed=0)
+    save("render_scene_ess", image=img, total_queries=np.int64(st.total_queries), ess_skipped=np.int64(st.ess_skipped),
+         ert_terminated_rays=np.int64(st.ert_terminated_rays), n_rays=np.int64(st.n_rays), k=np.int64(c.k),
+         epsilon=np.float64(c.epsilon), background=np.array(c.background, np.float64), ert_chunk=np.int64(c.ert_chunk),
+         stratified=np.bool_(c.stratified), seed=np.int64(0), occ_res=occ.resolution, occ_bits=occ.bits,
+         **cam_arrays(cam_b))
+    sp = scene.specular_toy_scene()
+    cam32 = scene.sphere_cameras(aabb, 1, 32, seed=5)[0]
+    c = render.RenderConfig(k=96)
+    img, st = render.render_image(sp, None, cam32, c, seed=5)
+    save("render_scene_specular", image=img, total_queries=np.int64(st.total_queries),
+         ess_skipped=np.int64(st.ess_skipped), ert_terminated_rays=np.int64(st.ert_terminated_rays),
+         n_rays=np.int64(st.n_rays), k=np.int64(c.k), epsilon=np.float64(c.epsilon),
+         background=np.array(c.background, np.float64), ert_chunk=np.int64(c.ert_chunk),
+         stratified=np.bool_(c.stratified), seed=np.int64(5), **cam_arrays(cam32))
+    rng = np.random.default_rng(8)
+    n = 8192
+    pts = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+    dirs = rng.normal(size=(n, 3)).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    out = {}
+    for tag, s_ in (("std", sc), ("spec", sp), ("rand", scene.random_toy_scene(4, 7))):
+        c_, s2 = s_.query_points(pts, dirs)
+        out[f"{tag}_rgb"], out[f"{tag}_sigma"] = c_, s2
+    save("query_scene", pts=pts, dirs=dirs, **out)
+
+
 def main():
-    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk"]
+    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene"]
     for w in what:
         t = time.time()
         globals()[f"gen_{w}"]()

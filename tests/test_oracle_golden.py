@@ -148,3 +148,32 @@ def test_render_matches_reference(name):
     cells = O.bin_cells(pos, lat.b_min, lat.b_max, lat.res) if len(pos) else np.zeros(0, np.int64)
     assert np.array_equal(np.bincount(cells, minlength=lat.n_cells), z["cell_hist"])
     assert np.max(np.abs(img - z["image"])) <= 1e-6
+
+
+# ---------------------------------------------------------------------------
+# analytic scenes (scene.py)
+# ---------------------------------------------------------------------------
+def test_analytic_scene_oracle_pinned():
+    from oracle import analytic as A
+
+    z = golden("query_scene")
+    for tag, sc in (("std", A.standard_scene()), ("spec", A.specular_scene()), ("rand", A.random_scene(4, 7))):
+        rgb, sig = A.scene_query(sc, z["pts"], z["dirs"])
+        assert np.array_equal(sig, z[f"{tag}_sigma"]), tag
+        assert np.array_equal(rgb, z[f"{tag}_rgb"]), tag
+
+
+@pytest.mark.parametrize("name", ["render_scene_ert", "render_scene_dense", "render_scene_ess", "render_scene_specular"])
+def test_analytic_scene_renders_pinned(name):
+    from oracle import analytic as A
+
+    z = golden(name)
+    sc = A.specular_scene() if "specular" in name else A.standard_scene()
+    occ = O.Occupancy(UNIT_MIN, UNIT_MAX, z["occ_res"], z["occ_bits"]) if "occ_bits" in z else None
+    cam = golden_camera(z)
+    o, d = O.pixel_rays(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, cam.c2w)
+    img, ctr = O.render_rays(lambda p, dd: A.scene_query(sc, p, dd), UNIT_MIN, UNIT_MAX, occ, o, d, case_config(z),
+                             seed=int(z["seed"]))
+    assert ctr.total_queries == int(z["total_queries"]) and ctr.ess_skipped == int(z["ess_skipped"])
+    assert ctr.ert_terminated_rays == int(z["ert_terminated_rays"])
+    assert np.max(np.abs(img.reshape(z["image"].shape) - z["image"])) <= 1e-6
