@@ -107,6 +107,13 @@ GF_API size_t gf_packed_bytes(const gf_arch_t* arch, int64_t n_cells, int precis
 GF_API int gf_pack_weights(const gf_arch_t* arch, int64_t n_cells, const float* const* layer_w_dev,
                     const float* const* layer_b_dev, void* packed_dev, int precision, void* stream);
 
+/* The same from a checkpoint payload (io.py:162-175 / 204-214): flat_dev is
+ * the float32 parameter block of a gridfield checkpoint, layer by layer in
+ * manifest order, each layer's weights (n_cells,out,in) then biases
+ * (n_cells,out) -- one host-to-device copy of the file's payload feeds K3. */
+GF_API int gf_pack_weights_flat(const gf_arch_t* arch, int64_t n_cells, const float* flat_dev, void* packed_dev,
+                                int precision, void* stream);
+
 /* --- NetworkGrid.query_points (grid.py:50-56) -----------------------------
  * Bin at network resolution, bucket by cell, fused encode + tiny MLP,
  * results written in the caller's query order.  err_dev (int64, device) must

@@ -70,6 +70,7 @@ _SIGS = {
     "gf_param_count": (C.c_int64, [C.POINTER(Arch)]),
     "gf_packed_bytes": (C.c_size_t, [C.POINTER(Arch), C.c_int64, C.c_int]),
     "gf_pack_weights": (C.c_int, [C.POINTER(Arch), C.c_int64, C.POINTER(_P), C.POINTER(_P), _P, C.c_int, _P]),
+    "gf_pack_weights_flat": (C.c_int, [C.POINTER(Arch), C.c_int64, _P, _P, C.c_int, _P]),
     "gf_query_workspace_bytes": (C.c_size_t, [C.POINTER(Arch), C.POINTER(GridGeom), C.c_int64]),
     "gf_query_points": (C.c_int, [C.POINTER(Arch), C.POINTER(GridGeom), _P, C.c_int, _P, _P, C.c_int64, _P, _P, _P,
                                   _P, C.c_size_t, _P]),

@@ -253,6 +253,23 @@ int gf_pack_weights(const gf_arch_t* arch, int64_t n_cells, const float* const* 
   return check_cuda("gf_pack_weights");
 }
 
+int gf_pack_weights_flat(const gf_arch_t* arch, int64_t n_cells, const float* flat, void* packed, int precision,
+                         void* stream) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t) || n_cells < 1 || !flat)
+    return fail(GF_ERR_INVALID, "gf_pack_weights_flat: bad architecture or payload");
+  const float* w[GF_MAX_LAYERS];
+  const float* b[GF_MAX_LAYERS];
+  size_t cursor = 0;
+  for (int l = 0; l < t.n_layers; ++l) {  // io.py:204-214 layout
+    w[l] = flat + cursor;
+    cursor += (size_t)n_cells * t.out[l] * t.in[l];
+    b[l] = flat + cursor;
+    cursor += (size_t)n_cells * t.out[l];
+  }
+  return gf_pack_weights(arch, n_cells, w, b, packed, precision, stream);
+}
+
 // ---------------------------------------------------------------------------
 // query path
 // ---------------------------------------------------------------------------

@@ -87,15 +87,23 @@ class NetworkGrid:
             nbytes = N.lib().gf_packed_bytes(arch, self.n_cells, N.PRECISION[p])
             if nbytes == 0:
                 raise N.NativeError(f"architecture {self.arch} has no {p} device layout")
-            w_dev = [D.to_device(np.asarray(self.params.weights[s.name], np.float32), t.float32)
-                     for s in self.arch.layers()]
-            b_dev = [D.to_device(np.asarray(self.params.biases[s.name], np.float32), t.float32)
-                     for s in self.arch.layers()]
-            wp = (N.C.c_void_p * len(w_dev))(*[x.data_ptr() for x in w_dev])
-            bp = (N.C.c_void_p * len(b_dev))(*[x.data_ptr() for x in b_dev])
             packed = D.workspace(nbytes)
-            N.check(N.lib().gf_pack_weights(arch, self.n_cells, wp, bp, N.ptr(packed), N.PRECISION[p],
-                                            D.stream_handle()), "pack weights")
+            flat = getattr(self, "_payload", None)
+            if flat is not None and flat[0] == fp:
+                # loaded from a checkpoint and unmodified since: one copy of the
+                # file's payload, packed on the device (io.load_checkpoint)
+                f_dev = D.to_device(flat[1], t.float32)
+                N.check(N.lib().gf_pack_weights_flat(arch, self.n_cells, N.ptr(f_dev), N.ptr(packed), N.PRECISION[p],
+                                                     D.stream_handle()), "pack weights (checkpoint payload)")
+            else:
+                w_dev = [D.to_device(np.asarray(self.params.weights[s.name], np.float32), t.float32)
+                         for s in self.arch.layers()]
+                b_dev = [D.to_device(np.asarray(self.params.biases[s.name], np.float32), t.float32)
+                         for s in self.arch.layers()]
+                wp = (N.C.c_void_p * len(w_dev))(*[x.data_ptr() for x in w_dev])
+                bp = (N.C.c_void_p * len(b_dev))(*[x.data_ptr() for x in b_dev])
+                N.check(N.lib().gf_pack_weights(arch, self.n_cells, wp, bp, N.ptr(packed), N.PRECISION[p],
+                                                D.stream_handle()), "pack weights")
             t.cuda.current_stream().synchronize()
             self._cache[key] = (fp, packed)
             return packed

@@ -283,8 +283,21 @@ def gen_scene():
     save("query_scene", pts=pts, dirs=dirs, **out)
 
 
+def gen_ckpt():
+    """A checkpoint written by the reference's io.save_checkpoint (io.py:150-175):
+    (2,3,4) lattice, seed 9, density bias 5, with a 8^3 occupancy bitmap."""
+    from gridfield import io as gio
+
+    aabb = unit()
+    g = ggrid.init_network_grid(aabb, (2, 3, 4), seed=9)
+    g.params.biases["density"][:] = 5.0
+    occ = occupancy.OccupancyGrid.from_bool_array(aabb, (8, 8, 8), np.arange(512) % 3 != 0)
+    gio.save_checkpoint(OUT / "ckpt_small.gfckpt", g, occ)
+    print("wrote ckpt_small.gfckpt", (OUT / "ckpt_small.gfckpt").stat().st_size)
+
+
 def main():
-    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene"]
+    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt"]
     for w in what:
         t = time.time()
         globals()[f"gen_{w}"]()
