@@ -222,6 +222,28 @@ GF_API int gf_render_rays_analytic(const gf_analytic_t* scene, const gf_grid_geo
                                    int64_t trace_capacity, int64_t* trace_count_dev, void* ws_dev, size_t ws_bytes,
                                    void* stream);
 
+/* --- occupancy.extract_occupancy (occupancy.py:94-128) ---------------------
+ * Probe every cell of `occ` (box + resolution of the extraction) on its 3x3x3
+ * lattice, clip into the box, threshold f64(density) > tau, and write the
+ * packed little-endian bitmap (ceil(n_cells/8) bytes) to bits_dev.  `tau` is
+ * the effective threshold: float32(tau) for a Python scalar (numpy's NEP 50
+ * float32 compare), tau itself for a float64 scalar.
+ * _analytic: field = AnalyticScene.density_at (scene.py:107-113), bit-exact.
+ * _network:  field = train.density_probe(model, direction) (train.py:577-586),
+ *   i.e. NetworkGrid.query_points at a fixed direction; probes are queried in
+ *   chunks of chunk_cells cells (0 = default) through gf_query_points.  err_dev
+ *   (init INT64_MAX) receives the first out-of-bounds probe component
+ *   (probe*3 + axis) when the extraction box leaves the network's box, and no
+ *   bit is written then.                                                    */
+GF_API int gf_extract_occupancy_analytic(const gf_analytic_t* scene, const gf_grid_geom_t* occ, double tau,
+                                         uint8_t* bits_dev, void* stream);
+GF_API size_t gf_extract_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* net, const gf_grid_geom_t* occ,
+                                         int64_t chunk_cells);
+GF_API int gf_extract_occupancy_network(const gf_arch_t* arch, const gf_grid_geom_t* net, const void* packed_dev,
+                                        int precision, const float* direction, const gf_grid_geom_t* occ, double tau,
+                                        int64_t chunk_cells, uint8_t* bits_dev, int64_t* err_dev, void* ws_dev,
+                                        size_t ws_bytes, void* stream);
+
 /* --- instrumentation ------------------------------------------------------
  * Stage timing: while enabled, gf_render_rays / gf_query_points record CUDA
  * events on their stream between stages; gf_stage_times() synchronises and

@@ -301,6 +301,39 @@ class Occupancy:
         return ((self.bits[f >> 3] >> (f & 7)) & 1).astype(bool)
 
 
+def probe_points(b_min, b_max, res):
+    """occupancy.py:112-123: every cell's 3x3x3 probe lattice in float64
+    (lo = b_min + i*cell, then lo + offset*cell), cast to float32 and clipped
+    into the box.  Returns (n_cells*27, 3) float32, cell-major, probes in
+    meshgrid 'ij' order."""
+    b_min = np.asarray(b_min, np.float64)
+    b_max = np.asarray(b_max, np.float64)
+    res = np.asarray(res, np.int64)
+    n = int(np.prod(res))
+    cell = (b_max - b_min) / res
+    flat = np.arange(n)
+    i3 = np.stack([flat % res[0], (flat // res[0]) % res[1], flat // (res[0] * res[1])], axis=-1)
+    lo = b_min + i3 * cell
+    offs = np.stack(np.meshgrid(*([np.array([0.0, 0.5, 1.0])] * 3), indexing="ij"), axis=-1).reshape(-1, 3)
+    pts = (lo[:, None, :] + offs[None, :, :] * cell).astype(np.float32).reshape(-1, 3)
+    return clamp_into_box(pts, b_min, b_max)
+
+
+def extract_occupancy(density, b_min, b_max, res, tau, chunk_cells=16384):
+    """occupancy.py:94-128: occupied iff any probe density > tau (numpy's
+    comparison semantics: float32 densities against a Python scalar compare in
+    float32).  Returns the packed little-endian bitmap."""
+    res = np.asarray(res, np.int64)
+    n = int(np.prod(res))
+    pts = probe_points(b_min, b_max, res)
+    occ = np.zeros(n, bool)
+    for s in range(0, n, chunk_cells):
+        e = min(n, s + chunk_cells)
+        sigma = np.asarray(density(pts[27 * s : 27 * e]))
+        occ[s:e] = (sigma.reshape(e - s, 27) > tau).any(axis=1)
+    return np.packbits(occ, bitorder="little")
+
+
 # --------------------------------------------------------------------------
 # rays and marching (render.py:139-400)
 # --------------------------------------------------------------------------

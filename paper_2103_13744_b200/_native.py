@@ -98,6 +98,12 @@ _SIGS = {
     "gf_render_rays_analytic": (C.c_int, [C.POINTER(Analytic), C.POINTER(GridGeom), _P, C.POINTER(MarchCfg),
                                           C.POINTER(CameraT), _P, _P, C.c_int64, C.c_int64, C.c_int64, _P, _P, _P,
                                           C.c_int64, _P, _P, C.c_size_t, _P]),
+    "gf_extract_occupancy_analytic": (C.c_int, [C.POINTER(Analytic), C.POINTER(GridGeom), C.c_double, _P, _P]),
+    "gf_extract_workspace_bytes": (C.c_size_t, [C.POINTER(Arch), C.POINTER(GridGeom), C.POINTER(GridGeom),
+                                                C.c_int64]),
+    "gf_extract_occupancy_network": (C.c_int, [C.POINTER(Arch), C.POINTER(GridGeom), _P, C.c_int,
+                                               C.POINTER(C.c_float), C.POINTER(GridGeom), C.c_double, C.c_int64, _P,
+                                               _P, _P, C.c_size_t, _P]),
     "gf_stage_timing": (C.c_int, [C.c_int32]),
     "gf_stage_times": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "gf_launch_count": (C.c_int64, []),

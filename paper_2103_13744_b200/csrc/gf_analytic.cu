@@ -14,32 +14,6 @@
 
 namespace gf {
 
-__device__ __forceinline__ float smoothstep32(float u) {
-  u = fminf(fmaxf(u, 0.f), 1.f);  // np.clip(u, 0.0, 1.0)
-  return __fmul_rn(__fmul_rn(u, u), __fsub_rn(3.0f, __fmul_rn(2.0f, u)));
-}
-
-__device__ __forceinline__ float prim_density(const AnalyticPrim& p, float x, float y, float z) {
-  if (p.kind == 0) {  // Sphere.density_at (scene.py:40-53)
-    const float tx = __fsub_rn(x, p.a[0]), ty = __fsub_rn(y, p.a[1]), tz = __fsub_rn(z, p.a[2]);
-    float d2 = __fmul_rn(tx, tx);
-    d2 = __fadd_rn(d2, __fmul_rn(ty, ty));
-    d2 = __fadd_rn(d2, __fmul_rn(tz, tz));
-    if (!(d2 < p.r2)) return 0.f;
-    if (!(p.feather > 0.f)) return p.density;
-    const float dist = __fsqrt_rn(d2);
-    return __fmul_rn(p.density, smoothstep32(__fdiv_rn(__fsub_rn(p.radius, dist), p.feather)));
-  }
-  // Box.density_at (scene.py:65-74)
-  const float dx = fminf(__fsub_rn(x, p.a[0]), __fsub_rn(p.b[0], x));
-  const float dy = fminf(__fsub_rn(y, p.a[1]), __fsub_rn(p.b[1], y));
-  const float dz = fminf(__fsub_rn(z, p.a[2]), __fsub_rn(p.b[2], z));
-  const float depth = fminf(fminf(dx, dy), dz);
-  if (!(depth > 0.f)) return 0.f;
-  if (!(p.feather > 0.f)) return p.density;
-  return __fmul_rn(p.density, smoothstep32(__fdiv_rn(depth, p.feather)));
-}
-
 // AnalyticScene.query_points (scene.py:115-135) for one point
 __device__ __forceinline__ void analytic_eval(const AnalyticDev& A, float x, float y, float z, float dx, float dy,
                                               float dz, float* rgb, float* sigma) {

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "gf_analytic.cuh"
+#include "gf_extract.cuh"
 #include "gf_march.cuh"
 #include "gf_mlp.cuh"
 
@@ -765,6 +766,85 @@ int gf_query_analytic(const gf_analytic_t* scene, const float* pos, const float*
   if (!make_analytic(scene, &A) || n < 0) return fail(GF_ERR_INVALID, "gf_query_analytic: bad scene or size");
   launch_query_analytic(A, pos, dir, n, rgb, sigma, (cudaStream_t)stream);
   return check_cuda("gf_query_analytic");
+}
+
+// ---------------------------------------------------------------------------
+// occupancy extraction (occupancy.py:94-128)
+// ---------------------------------------------------------------------------
+int gf_extract_occupancy_analytic(const gf_analytic_t* scene, const gf_grid_geom_t* occ, double tau, uint8_t* bits,
+                                  void* stream) {
+  AnalyticDev A;
+  memset(&A, 0, sizeof(A));
+  if (!make_analytic(scene, &A)) return fail(GF_ERR_INVALID, "gf_extract_occupancy_analytic: bad scene");
+  if (!valid_grid(occ)) return fail(GF_ERR_INVALID, "gf_extract_occupancy_analytic: bad occupancy grid");
+  launch_extract_analytic(A, gf_make_grid(occ), n_cells_of(occ), tau, bits, (cudaStream_t)stream);
+  return check_cuda("gf_extract_occupancy_analytic");
+}
+
+struct ExtractWs {
+  float *pos, *dir, *rgb, *sigma;
+  void* qws;
+  size_t qbytes;
+};
+
+static int64_t extract_chunk(int64_t n_cells, int64_t chunk_cells) {
+  int64_t c = chunk_cells > 0 ? chunk_cells : (1 << 19);
+  c = std::min<int64_t>(c, n_cells);
+  c = std::min<int64_t>(c, ((int64_t)0xFFFFFFF0ll / 27) & ~31ll);  // query row-index width
+  return std::max<int64_t>(32, (c + 31) & ~31ll);                    // bitmap chunks start on 32-cell words
+}
+
+static size_t extract_carve(Carve& c, const gf_arch_t* arch, const gf_grid_geom_t* net, int64_t chunk, ExtractWs* w) {
+  const size_t q = (size_t)chunk * 27;
+  w->pos = c.take<float>(3 * q);
+  w->dir = c.take<float>(3 * q);
+  w->rgb = c.take<float>(3 * q);
+  w->sigma = c.take<float>(q);
+  w->qbytes = gf_query_workspace_bytes(arch, net, (int64_t)q);
+  w->qws = c.take<char>(w->qbytes);
+  return c.size();
+}
+
+size_t gf_extract_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* net, const gf_grid_geom_t* occ,
+                                  int64_t chunk_cells) {
+  if (!valid_grid(net) || !valid_grid(occ)) return 0;
+  Carve c(nullptr);
+  ExtractWs w;
+  return extract_carve(c, arch, net, extract_chunk(n_cells_of(occ), chunk_cells), &w);
+}
+
+int gf_extract_occupancy_network(const gf_arch_t* arch, const gf_grid_geom_t* net, const void* packed, int precision,
+                                 const float* direction, const gf_grid_geom_t* occ, double tau, int64_t chunk_cells,
+                                 uint8_t* bits, int64_t* err, void* ws, size_t ws_bytes, void* stream) {
+  if (!valid_grid(net) || !valid_grid(occ) || !direction)
+    return fail(GF_ERR_INVALID, "gf_extract_occupancy_network: bad grid or direction");
+  const int64_t n = n_cells_of(occ), chunk = extract_chunk(n, chunk_cells);
+  Carve c(ws);
+  ExtractWs w;
+  if (extract_carve(c, arch, net, chunk, &w) > ws_bytes)
+    return fail(GF_ERR_WORKSPACE, "gf_extract_occupancy_network: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const GfGrid g = gf_make_grid(occ), gn = gf_make_grid(net);
+  bool inside = true;
+  for (int a = 0; a < 3; ++a) inside = inside && occ->b_min[a] >= net->b_min[a] && occ->b_max[a] <= net->b_max[a];
+  if (!inside) {
+    // probes clipped into the extraction box can leave the field's box: find the
+    // first offending component (the reference raises before any bit is set)
+    launch_probe_oob(g, gn, n, err, st);
+    int64_t h = 0;
+    cudaMemcpyAsync(&h, err, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return check_cuda("gf_extract_occupancy_network");
+    if (h != INT64_MAX) return GF_OK;
+  }
+  for (int64_t first = 0; first < n; first += chunk) {
+    const int64_t cnt = std::min<int64_t>(chunk, n - first);
+    launch_probe_points(g, first, cnt, direction, w.pos, w.dir, st);
+    const int rc = gf_query_points(arch, net, packed, precision, w.pos, w.dir, cnt * 27, w.rgb, w.sigma, err, w.qws,
+                                   w.qbytes, stream);
+    if (rc != GF_OK) return rc;
+    launch_probe_any(w.sigma, first, cnt, n, tau, bits, st);
+  }
+  return check_cuda("gf_extract_occupancy_network");
 }
 
 // ---------------------------------------------------------------------------

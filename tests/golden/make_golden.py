@@ -283,6 +283,63 @@ def gen_scene():
     save("query_scene", pts=pts, dirs=dirs, **out)
 
 
+def gen_extract():
+    """occupancy.extract_occupancy (occupancy.py:94-128) through
+    the reference: analytic scenes (bit-exact targets) at cubic, ragged and
+    non-power-of-two boxes, and a density_probe of a random-init lattice
+    (tolerance target: cells with a probe within `margin` of tau are marked)."""
+    from gridfield import train
+
+    out = {}
+    sc, sp, rnd = scene.standard_toy_scene(), scene.specular_toy_scene(), scene.random_toy_scene(11, 6)
+    cases = [
+        ("toy64", sc, sc.aabb, (64, 64, 64), 10.0),
+        ("rand48", rnd, rnd.aabb, (48, 40, 36), 10.0),
+        ("spec_box", sp, core.Aabb((-0.9, -1.0, -0.7), (1.0, 0.8, 1.0)), (40, 24, 33), 0.0),
+        ("toy_tau_f64", sc, sc.aabb, (30, 30, 30), np.float64(20.000001)),
+    ]
+    for tag, s_, box, res, tau in cases:
+        occ = occupancy.extract_occupancy(s_.density_at, box, res, tau=tau)
+        out[f"{tag}_bits"] = occ.bits
+        out[f"{tag}_res"] = np.asarray(res, np.int64)
+        out[f"{tag}_box"] = np.stack([box.b_min, box.b_max])
+        out[f"{tag}_tau"] = np.float64(tau)
+        out[f"{tag}_tau_is_f64"] = np.bool_(isinstance(tau, np.float64))
+        print(tag, occ.occupied_fraction())
+    print("random scene boxes:", len(rnd.boxes), "spheres:", len(rnd.spheres))
+    # network density probe: random-init 4^3 lattice with per-cell density biases
+    aabb = unit()
+    g = ggrid.init_network_grid(aabb, (4, 4, 4), seed=3)
+    rng = np.random.default_rng(21)
+    g.params.biases["density"][:] = rng.uniform(-0.5, 2.0, g.params.biases["density"].shape).astype(np.float32)
+    field = train.density_probe(g)
+    res = (24, 20, 16)
+    box = core.Aabb((-1.0, -0.75, -1.0), (0.9, 1.0, 0.6))
+    lo = occupancy.extract_occupancy(field, box, res, tau=0.0)
+    # tau at the median per-cell max density, and a margin mask for the tolerance check
+    n = int(np.prod(res))
+    cell = box.cell_size(res)
+    flat = np.arange(n)
+    lows = box.b_min + np.stack([flat % res[0], (flat // res[0]) % res[1], flat // (res[0] * res[1])], -1) * cell
+    pts = (lows[:, None, :] + occupancy._PROBE_OFFSETS[None] * cell).astype(np.float32)
+    sig = field(core.clip_into(pts.reshape(-1, 3), box)).reshape(n, 27)
+    tau = float(np.round(np.median(sig.max(1)), 4))
+    occ = occupancy.extract_occupancy(field, box, res, tau=tau)
+    near = (np.abs(sig - np.float32(tau)) < 5e-3).any(1)
+    out.update(net_bits=occ.bits, net_res=np.asarray(res, np.int64), net_box=np.stack([box.b_min, box.b_max]),
+               net_tau=np.float64(tau), net_near=np.packbits(near, bitorder="little"), net_tau0_bits=lo.bits,
+               net_near0=np.packbits((np.abs(sig) < 5e-3).any(1), bitorder="little"),
+               net_bias=np.asarray(g.params.biases["density"]), net_seed=np.int64(3), net_grid_res=np.array([4, 4, 4]))
+    print("net", occ.occupied_fraction(), "near", near.mean(), "tau", tau)
+    try:  # extraction box leaving the network's box: the reference's message
+        occupancy.extract_occupancy(field, core.Aabb((-1.0, -1.0, -1.0), (1.0, 1.25, 1.0)), (8, 8, 8), tau=1.0)
+        raise AssertionError("expected an out-of-bounds error")
+    except ValueError as e:
+        out["net_oob_message"] = np.array(str(e))
+        print("oob:", e)
+    save("extract", **out)
+
+
 def gen_ckpt():
     """A checkpoint written by the reference's io.save_checkpoint (io.py:150-175):
     (2,3,4) lattice, seed 9, density bias 5, with a 8^3 occupancy bitmap."""
@@ -297,7 +354,7 @@ def gen_ckpt():
 
 
 def main():
-    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt"]
+    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt", "extract"]
     for w in what:
         t = time.time()
         globals()[f"gen_{w}"]()
