@@ -244,6 +244,48 @@ GF_API int gf_extract_occupancy_network(const gf_arch_t* arch, const gf_grid_geo
                                         int64_t chunk_cells, uint8_t* bits_dev, int64_t* err_dev, void* ws_dev,
                                         size_t ws_bytes, void* stream);
 
+/* --- training ----------------------------------------------
+ * batched.grouped_backward (batched.py:154-187) + mlp.backward (mlp.py:269-316):
+ * parameter gradients of sum(d_color*color + d_sigma*sigma) per cell.  Rows
+ * pos/dir are grouped (cell c owns rows offsets[c]..offsets[c+1]); row j's
+ * upstream gradient is d_color[order[j]] / d_sigma[order[j]] (order NULL =
+ * identity).  packed_dev is the GF_PRECISION_FP32 packing.  gw[l] / gb[l]
+ * receive layer l's gradients in the reference layout (n_cells, out, in) /
+ * (n_cells, out), manifest order; cells without rows get zeros.         */
+GF_API int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* packed_dev, const float* pos_dev,
+                               const float* dir_dev, int64_t n, const int64_t* offsets_dev, const int64_t* order_dev,
+                               const float* d_color_dev, const float* d_sigma_dev, float* const* gw_dev,
+                               float* const* gb_dev, void* stream);
+/* train.photometric_loss_and_grads compositing (train.py:243-288): queries
+ * (ray_index, slot) of B rays x k slots with colours and densities (noise:
+ * optional density perturbation, train.py:245-249), per-ray deltas, ground
+ * truth gt (B,3), host background[3], two_over_b = float32(2/B).  Writes the
+ * float64 sum over rays of ||pred - gt||^2 to loss_sum_dev and, when
+ * d_color_q_dev is not NULL, the per-query upstream gradients.            */
+GF_API size_t gf_photometric_workspace_bytes(int64_t n_rays, int32_t k, int64_t n_queries);
+GF_API int gf_photometric_loss(int64_t n_rays, int32_t k, int64_t n_queries, const int64_t* ray_index_dev,
+                               const int64_t* slot_dev, const float* color_dev, const float* sigma_dev,
+                               const float* noise_dev, const float* deltas_dev, const float* gt_dev,
+                               const float* background, float two_over_b, float* d_color_q_dev, float* d_sigma_q_dev,
+                               double* loss_sum_dev, void* ws_dev, size_t ws_bytes, void* stream);
+/* train.adam_update (train.py:130-143) over one flat float32 array, in place.
+ * coef (host) = float32 {b1, 1-b1, b2, 1-b2, 1-b1^t, 1-b2^t, lr, eps}.    */
+GF_API int gf_adam_update(float* p_dev, const float* g_dev, float* m_dev, float* v_dev, int64_t n, const float* coef,
+                          void* stream);
+/* train.regularization_term (train.py:146-160) helpers: float64 sum of
+ * squares (fixed order), and out = y + float32(f) * x (y NULL: f * x).      */
+GF_API size_t gf_sum_squares_workspace_bytes(void);
+GF_API int gf_sum_squares(const float* x_dev, int64_t n, double* out_dev, void* ws_dev, size_t ws_bytes, void* stream);
+GF_API int gf_axpy(const float* x_dev, const float* y_dev, int64_t n, float f, float* out_dev, void* stream);
+/* train.distill_step loss terms (train.py:369-385): student / teacher colours
+ * and densities of n queries, delta = float32(delta_ref), c_sigma =
+ * float32(2*w_a/m), c_color = float32(2/m).  sums_dev[0] = sum(d_alpha^2),
+ * sums_dev[1] = sum(d_color^2) in float64; d_color / d_sigma = upstream.   */
+GF_API size_t gf_distill_workspace_bytes(int64_t n);
+GF_API int gf_distill_loss(int64_t n, const float* s_color_dev, const float* s_sigma_dev, const float* t_color_dev,
+                           const float* t_sigma_dev, float delta, float c_sigma, float c_color, float* d_color_dev,
+                           float* d_sigma_dev, double* sums_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
 /* --- instrumentation ------------------------------------------------------
  * Stage timing: while enabled, gf_render_rays / gf_query_points record CUDA
  * events on their stream between stages; gf_stage_times() synchronises and

@@ -104,6 +104,18 @@ _SIGS = {
     "gf_extract_occupancy_network": (C.c_int, [C.POINTER(Arch), C.POINTER(GridGeom), _P, C.c_int,
                                                C.POINTER(C.c_float), C.POINTER(GridGeom), C.c_double, C.c_int64, _P,
                                                _P, _P, C.c_size_t, _P]),
+    "gf_grouped_backward": (C.c_int, [C.POINTER(Arch), C.c_int64, _P, _P, _P, C.c_int64, _P, _P, _P, _P,
+                                      C.POINTER(_P), C.POINTER(_P), _P]),
+    "gf_photometric_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int64]),
+    "gf_photometric_loss": (C.c_int, [C.c_int64, C.c_int32, C.c_int64, _P, _P, _P, _P, _P, _P, _P,
+                                      C.POINTER(C.c_float), C.c_float, _P, _P, _P, _P, C.c_size_t, _P]),
+    "gf_adam_update": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(C.c_float), _P]),
+    "gf_sum_squares_workspace_bytes": (C.c_size_t, []),
+    "gf_sum_squares": (C.c_int, [_P, C.c_int64, _P, _P, C.c_size_t, _P]),
+    "gf_axpy": (C.c_int, [_P, _P, C.c_int64, C.c_float, _P, _P]),
+    "gf_distill_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "gf_distill_loss": (C.c_int, [C.c_int64, _P, _P, _P, _P, C.c_float, C.c_float, C.c_float, _P, _P, _P, _P,
+                                  C.c_size_t, _P]),
     "gf_stage_timing": (C.c_int, [C.c_int32]),
     "gf_stage_times": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "gf_launch_count": (C.c_int64, []),

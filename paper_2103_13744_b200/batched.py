@@ -80,28 +80,94 @@ def group_by_network(batch: QueryBatch, n_networks: int) -> GroupedLayout:
     )
 
 
-def grouped_forward(grid, layout: GroupedLayout, caches: list | None = None, precision=None):
-    """batched.py:120-151: evaluate each segment with its cell's network; the
-    kernel writes row j's result to original index order[j], so the output is
-    already in input order.  ``caches`` (training backward) is out of scope."""
-    if caches is not None:
-        raise NotImplementedError("grouped_backward caches belong to training, which this build does not cover")
+def grouped_forward_device(grid, layout: GroupedLayout, pos=None, dirs=None, precision="fp32") -> "GroupedCache":
+    """The fused grouped forward on device tensors (results in query order);
+    ``pos``/``dirs`` may be given as device tensors already in grouped order."""
     t = D.require_cuda()
     n = layout.n_queries
-    p = grid.resolved_precision(precision)
-    packed = grid.device_params(p)
-    pos = D.to_device(np.asarray(layout.positions, np.float32).reshape(-1, 3), t.float32)
-    dirs = D.to_device(np.asarray(layout.directions, np.float32).reshape(-1, 3), t.float32)
+    packed = grid.device_params(precision)
+    if pos is None:
+        pos = D.to_device(np.asarray(layout.positions, np.float32).reshape(-1, 3), t.float32)
+    if dirs is None:
+        dirs = D.to_device(np.asarray(layout.directions, np.float32).reshape(-1, 3), t.float32)
     offs = D.to_device(np.asarray(layout.offsets, np.int64), t.int64)
     order = D.to_device(np.asarray(layout.order, np.int64), t.int64)
     rgb = D.empty((n, 3), t.float32)
     sigma = D.empty((n,), t.float32)
     ws = D.workspace(N.lib().gf_grouped_workspace_bytes(grid.n_cells, n))
-    N.check(N.lib().gf_grouped_forward(grid.native_arch(), grid.n_cells, N.ptr(packed), N.PRECISION[p], N.ptr(pos),
-                                       N.ptr(dirs), n, N.ptr(offs), N.ptr(order), N.ptr(rgb), N.ptr(sigma), N.ptr(ws),
-                                       ws.numel(), D.stream_handle()), "grouped_forward")
+    N.check(N.lib().gf_grouped_forward(grid.native_arch(), grid.n_cells, N.ptr(packed), N.PRECISION[precision],
+                                       N.ptr(pos), N.ptr(dirs), n, N.ptr(offs), N.ptr(order), N.ptr(rgb),
+                                       N.ptr(sigma), N.ptr(ws), ws.numel(), D.stream_handle()), "grouped_forward")
+    return GroupedCache(packed, pos, dirs, offs, order, rgb, sigma)
+
+
+def grouped_forward(grid, layout: GroupedLayout, caches: list | None = None, precision=None):
+    """batched.py:120-151: evaluate each segment with its cell's network; the
+    kernel writes row j's result to original index order[j], so the output is
+    already in input order.
+
+    With ``caches`` (training) the pass runs in fp32 and appends one
+    ``GroupedCache`` holding the device-resident grouped rows and the packed
+    parameters it used; ``grouped_backward`` recomputes the activations from
+    them in its fused kernel instead of keeping (n, width) activation arrays."""
+    p = "fp32" if caches is not None else grid.resolved_precision(precision)
+    c = grouped_forward_device(grid, layout, precision=p)
+    if caches is not None:
+        caches.append(c)
     dtype = grid.params.dtype
-    return rgb.cpu().numpy().astype(dtype, copy=False), sigma.cpu().numpy().astype(dtype, copy=False)
+    return c.rgb.cpu().numpy().astype(dtype, copy=False), c.sigma.cpu().numpy().astype(dtype, copy=False)
+
+
+@dataclass
+class GroupedCache:
+    """What grouped_backward needs from its forward pass (the reference keeps
+    per-bucket activations, batched.py:143-150): the fp32 parameter packing
+    the forward used and the grouped rows, all on the device."""
+
+    packed: object
+    pos: object
+    dirs: object
+    offsets: object
+    order: object
+    rgb: object
+    sigma: object
+
+
+def grouped_backward_device(grid, layout: GroupedLayout, cache: GroupedCache, d_color, d_sigma):
+    """gf_grouped_backward on device tensors -> per-layer (gw, gb) device lists
+    in the reference layout (n_cells, out, in) / (n_cells, out)."""
+    t = D.require_cuda()
+    n = layout.n_queries
+    dc = D.to_device(d_color, t.float32).reshape(-1, 3).contiguous()
+    ds = D.to_device(d_sigma, t.float32).reshape(-1).contiguous()
+    if dc.shape[0] != n or ds.shape[0] != n:
+        raise ValueError("upstream gradients do not match the layout's query count")
+    specs = grid.arch.layers()
+    gw = [D.empty((grid.n_cells, s.out_dim, s.in_dim), t.float32) for s in specs]
+    gb = [D.empty((grid.n_cells, s.out_dim), t.float32) for s in specs]
+    wp = (N.C.c_void_p * len(gw))(*[x.data_ptr() for x in gw])
+    bp = (N.C.c_void_p * len(gb))(*[x.data_ptr() for x in gb])
+    N.check(N.lib().gf_grouped_backward(grid.native_arch(), grid.n_cells, N.ptr(cache.packed), N.ptr(cache.pos),
+                                        N.ptr(cache.dirs), n, N.ptr(cache.offsets), N.ptr(cache.order), N.ptr(dc),
+                                        N.ptr(ds), wp, bp, D.stream_handle()), "grouped_backward")
+    return gw, gb
+
+
+def grouped_backward(grid, layout: GroupedLayout, caches: list, d_color, d_sigma):
+    """batched.py:154-187: parameter gradients of sum(d_color*color +
+    d_sigma*sigma) stacked over all cells (zeros for unqueried networks), in
+    one device pass (gf_grouped_backward: one CTA per cell, fused forward
+    recompute + backward, fixed-order per-parameter sums).  Upstream
+    gradients arrive in original query order (numpy or CUDA tensors)."""
+    from . import mlp
+
+    if not caches or not isinstance(caches[-1], GroupedCache):
+        raise ValueError("grouped_backward needs the caches list filled by grouped_forward")
+    gw, gb = grouped_backward_device(grid, layout, caches[-1], d_color, d_sigma)
+    specs = grid.arch.layers()
+    dtype = grid.params.dtype
+    return mlp.MlpParams(grid.arch, {s.name: w.cpu().numpy().astype(dtype, copy=False) for s, w in zip(specs, gw)},
+                         {s.name: b.cpu().numpy().astype(dtype, copy=False) for s, b in zip(specs, gb)})
 
 
 def parallel_map(fn, items, workers: int = 1) -> list:

@@ -11,6 +11,7 @@
 
 #include "gf_analytic.cuh"
 #include "gf_extract.cuh"
+#include "gf_train.cuh"
 #include "gf_march.cuh"
 #include "gf_mlp.cuh"
 
@@ -845,6 +846,98 @@ int gf_extract_occupancy_network(const gf_arch_t* arch, const gf_grid_geom_t* ne
     launch_probe_any(w.sigma, first, cnt, n, tau, bits, st);
   }
   return check_cuda("gf_extract_occupancy_network");
+}
+
+// ---------------------------------------------------------------------------
+// training: batched.py:154-187, train.py:130-160, 212-288
+// ---------------------------------------------------------------------------
+int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* packed, const float* pos, const float* dir,
+                        int64_t n, const int64_t* offsets, const int64_t* order, const float* d_color,
+                        const float* d_sigma, float* const* gw, float* const* gb, void* stream) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_grouped_backward: bad architecture");
+  if (n_cells < 1 || n < 0 || !gw || !gb) return fail(GF_ERR_INVALID, "gf_grouped_backward: bad sizes");
+  BwdArgs A;
+  memset(&A, 0, sizeof(A));
+  A.pos = pos;
+  A.dir = dir;
+  A.offsets = offsets;
+  A.order = order;
+  A.d_color = d_color;
+  A.d_sigma = d_sigma;
+  for (int l = 0; l < t.n_layers; ++l) {
+    A.gw[l] = gw[l];
+    A.gb[l] = gb[l];
+  }
+  if (!launch_grouped_backward(t, (const float*)packed, A, n_cells, (cudaStream_t)stream))
+    return fail(GF_ERR_UNSUPPORTED, "gf_grouped_backward: no backward kernel for this architecture");
+  return check_cuda("gf_grouped_backward");
+}
+
+size_t gf_photometric_workspace_bytes(int64_t n_rays, int32_t k, int64_t n_queries) {
+  if (n_rays < 0 || k < 1 || n_queries < 0) return 0;
+  return photo_workspace(n_rays, k, n_queries);
+}
+
+int gf_photometric_loss(int64_t n_rays, int32_t k, int64_t n_queries, const int64_t* ray_index, const int64_t* slot,
+                        const float* color, const float* sigma, const float* noise, const float* deltas,
+                        const float* gt, const float* background, float two_over_b, float* d_color_q,
+                        float* d_sigma_q, double* loss_sum, void* ws, size_t ws_bytes, void* stream) {
+  if (n_rays < 0 || k < 1 || n_queries < 0 || n_queries >= (int64_t)INT32_MAX || !background)
+    return fail(GF_ERR_INVALID, "gf_photometric_loss: bad sizes");
+  if (photo_workspace(n_rays, k, n_queries) > ws_bytes)
+    return fail(GF_ERR_WORKSPACE, "gf_photometric_loss: workspace too small");
+  PhotoArgs A;
+  A.n_rays = n_rays;
+  A.n_queries = n_queries;
+  A.k = k;
+  A.ray_index = ray_index;
+  A.slot = slot;
+  A.color = color;
+  A.sigma = sigma;
+  A.noise = noise;
+  A.deltas = deltas;
+  A.gt = gt;
+  for (int c = 0; c < 3; ++c) A.bg[c] = background[c];
+  A.two_over_b = two_over_b;
+  A.d_color_q = d_color_q;
+  A.d_sigma_q = d_sigma_q;
+  launch_photometric(A, ws, loss_sum, (cudaStream_t)stream);
+  return check_cuda("gf_photometric_loss");
+}
+
+int gf_adam_update(float* p, const float* g, float* m, float* v, int64_t n, const float* coef, void* stream) {
+  if (n < 0 || !coef) return fail(GF_ERR_INVALID, "gf_adam_update: bad arguments");
+  AdamCoef c{coef[0], coef[1], coef[2], coef[3], coef[4], coef[5], coef[6], coef[7]};
+  launch_adam(p, g, m, v, n, c, (cudaStream_t)stream);
+  return check_cuda("gf_adam_update");
+}
+
+static const int kSumsqParts = 1024;
+
+size_t gf_sum_squares_workspace_bytes(void) { return kSumsqParts * sizeof(double); }
+
+int gf_sum_squares(const float* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || ws_bytes < kSumsqParts * sizeof(double)) return fail(GF_ERR_INVALID, "gf_sum_squares: bad arguments");
+  launch_sumsq(x, n, (double*)ws, kSumsqParts, out, (cudaStream_t)stream);
+  return check_cuda("gf_sum_squares");
+}
+
+int gf_axpy(const float* x, const float* y, int64_t n, float f, float* out, void* stream) {
+  if (n < 0 || !x || !out) return fail(GF_ERR_INVALID, "gf_axpy: bad arguments");
+  launch_axpy(x, y, n, f, out, (cudaStream_t)stream);
+  return check_cuda("gf_axpy");
+}
+
+size_t gf_distill_workspace_bytes(int64_t n) { return n < 0 ? 0 : gf_align((size_t)(n + 1) * 16); }
+
+int gf_distill_loss(int64_t n, const float* s_color, const float* s_sigma, const float* t_color, const float* t_sigma,
+                    float delta, float c_sigma, float c_color, float* d_color, float* d_sigma, double* sums,
+                    void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || ws_bytes < gf_distill_workspace_bytes(n)) return fail(GF_ERR_INVALID, "gf_distill_loss: bad arguments");
+  DistillArgs A{n, s_color, s_sigma, t_color, t_sigma, delta, c_sigma, c_color, d_color, d_sigma};
+  launch_distill(A, (double*)ws, sums, (cudaStream_t)stream);
+  return check_cuda("gf_distill_loss");
 }
 
 // ---------------------------------------------------------------------------

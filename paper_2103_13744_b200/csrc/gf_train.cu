@@ -1,0 +1,480 @@
+// Training kernels: the grouped backward pass of the
+// per-cell tiny MLPs, the photometric loss with its compositing gradients,
+// and the optimizer step.
+//
+// Reference:
+//   batched.py:154-187  grouped_backward (per-cell parameter gradients)
+//   mlp.py:269-316      backward (exact gradients of sum(dc*color + ds*sigma))
+//   train.py:212-288    photometric_loss_and_grads (dense compositing, the
+//                       rest-of-ray recurrence for d alpha, loss in float64)
+//   train.py:130-143    adam_update;  train.py:146-160 regularization_term
+//
+// Everything is float32 SIMT (the reference's arithmetic type); results match
+// the reference within a stated tolerance, not bit for bit, because numpy's
+// sgemm and pairwise sums associate differently.  Every reduction here has a
+// fixed order (one owner thread per parameter, one thread per ray), so the
+// device results are deterministic run to run.
+#include "gf_mlp_simt.cuh"
+#include "gf_train.cuh"
+
+namespace gf {
+
+// ---------------------------------------------------------------------------
+// grouped backward: one CTA per cell, TR rows per tile, one thread per row in
+// phase A (forward recompute + backward data in fp32, activations and deltas
+// stored to shared memory), all threads in phase B (each owns a fixed set of
+// parameters and sums dz[o] * in[i] over the tile's rows in row order).
+// ---------------------------------------------------------------------------
+template <int W>
+struct BwdShape {
+  static constexpr int P = 63, D = 27;
+  // per-row shared-memory vectors (floats)
+  static constexpr int X = 0;             // gamma(x)            P
+  static constexpr int H0 = X + P;        // h0                  W
+  static constexpr int H1 = H0 + W;       // h1                  W
+  static constexpr int CAT = H1 + W;      // [feat, gamma(d)]    W + D
+  static constexpr int G = CAT + W + D;   // g                   W
+  static constexpr int DZ0 = G + W;       // dz trunk0           W
+  static constexpr int DZ1 = DZ0 + W;     // dz trunk1           W
+  static constexpr int DZS = DZ1 + W;     // dz density          1
+  static constexpr int DZF = DZS + 1;     // dz feature          W
+  static constexpr int DZD = DZF + W;     // dz direction        W
+  static constexpr int DZC = DZD + W;     // dz color            3
+  static constexpr int END = DZC + 3;
+  static constexpr int LD = END | 1;      // odd row stride: conflict-free per-row access
+  static constexpr int TR = W == 32 ? 64 : 32;  // rows per tile (smem: TR * LD floats + weights)
+  static constexpr int N_LAYERS = 6;
+  // manifest order (mlp.py:73-84): trunk0, trunk1, density, feature, direction, color
+  __host__ __device__ static constexpr int in_dim(int l) { return l == 0 ? P : (l == 4 ? W + D : W); }
+  __host__ __device__ static constexpr int out_dim(int l) { return l == 2 ? 1 : (l == 5 ? 3 : W); }
+  __host__ __device__ static constexpr int in_off(int l) {
+    return l == 0 ? X : (l == 1 ? H0 : (l == 2 || l == 3 ? H1 : (l == 4 ? CAT : G)));
+  }
+  __host__ __device__ static constexpr int dz_off(int l) {
+    return l == 0 ? DZ0 : (l == 1 ? DZ1 : (l == 2 ? DZS : (l == 3 ? DZF : (l == 4 ? DZD : DZC))));
+  }
+  __host__ __device__ static constexpr int count(int l) { return out_dim(l) * in_dim(l) + out_dim(l); }
+  static constexpr int TOTAL = count(0) + count(1) + count(2) + count(3) + count(4) + count(5);
+};
+
+// out[o] = (relu)(sum_i in[i] * W[o][i] + b[o]); input vector in registers
+template <int IN, int INP, int OUT, bool RELU>
+__device__ __forceinline__ void dense_row(const float* __restrict__ w, const float* __restrict__ b, const float* in,
+                                          float* out_row) {
+#pragma unroll 4
+  for (int o = 0; o < OUT; ++o) {
+    const float4* wr = reinterpret_cast<const float4*>(w + o * INP);
+    float acc = 0.f;
+#pragma unroll
+    for (int i4 = 0; i4 < INP / 4; ++i4) {
+      const float4 q = wr[i4];
+      if (4 * i4 + 0 < IN) acc = fmaf(in[4 * i4 + 0], q.x, acc);
+      if (4 * i4 + 1 < IN) acc = fmaf(in[4 * i4 + 1], q.y, acc);
+      if (4 * i4 + 2 < IN) acc = fmaf(in[4 * i4 + 2], q.z, acc);
+      if (4 * i4 + 3 < IN) acc = fmaf(in[4 * i4 + 3], q.w, acc);
+    }
+    const float z = __fadd_rn(acc, b[o]);
+    out_row[o] = RELU ? fmaxf(z, 0.f) : z;
+  }
+}
+
+// dx[i] = sum_o dz[o] * W[o][i]  (matmul(dz, W), mlp.py:294-297)
+template <int NI, int INP, int OUT>
+__device__ __forceinline__ void dense_t_row(const float* __restrict__ w, const float* dz, float* dx) {
+#pragma unroll
+  for (int i = 0; i < NI; ++i) dx[i] = 0.f;
+#pragma unroll 2
+  for (int o = 0; o < OUT; ++o) {
+    const float g = dz[o];
+    const float* wr = w + o * INP;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) dx[i] = fmaf(g, wr[i], dx[i]);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(BwdShape<W>::TR) k_grouped_backward(const float* __restrict__ packed, Fp32Layout L,
+                                                                      BwdArgs A) {
+  using S = BwdShape<W>;
+  constexpr int P = S::P, D = S::D, TR = S::TR, LD = S::LD;
+  constexpr int PP = (P + 3) & ~3, WP = (W + 3) & ~3, DP = (W + D + 3) & ~3;
+  extern __shared__ float4 smem4[];
+  float* sw = reinterpret_cast<float*>(smem4);
+  float* srow = sw + L.cell_floats;  // TR rows x LD floats
+  const int64_t cell = blockIdx.x;
+  const int tid = threadIdx.x;
+  {
+    const float4* src = reinterpret_cast<const float4*>(packed + (size_t)cell * L.cell_floats);
+    for (int j = tid; j < L.cell_floats / 4; j += TR) smem4[j] = __ldg(src + j);
+  }
+  const int64_t r0 = A.offsets[cell], r1 = A.offsets[cell + 1];
+  const int64_t rows = r1 - r0;
+  const int n_tiles = rows > 0 ? (int)((rows + TR - 1) / TR) : 1;
+  for (int t = 0; t < n_tiles; ++t) {
+    const int64_t first = r0 + (int64_t)t * TR;
+    const int n_in = (int)(r1 - first < (int64_t)TR ? r1 - first : (int64_t)TR);  // <= 0 for an empty cell
+    __syncthreads();
+    if (tid < n_in) {
+      float* s = srow + tid * LD;
+      const int64_t row = first + tid;
+      const int64_t src = A.order ? A.order[row] : row;  // upstream gradients arrive in query order
+      float x[3], d[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        x[a] = A.pos[3 * row + a];
+        d[a] = A.dir[3 * row + a];
+      }
+      // ---- forward (mlp.py:238-266), activations to shared memory
+      float xe[P];
+      encode_f32<10>(x, xe);
+#pragma unroll
+      for (int i = 0; i < P; ++i) s[S::X + i] = xe[i];
+      dense_row<P, PP, W, true>(sw + L.w_off[0], sw + L.b_off[0], xe, s + S::H0);
+      float hv[W];
+#pragma unroll
+      for (int i = 0; i < W; ++i) hv[i] = s[S::H0 + i];
+      dense_row<W, WP, W, true>(sw + L.w_off[1], sw + L.b_off[1], hv, s + S::H1);
+#pragma unroll
+      for (int i = 0; i < W; ++i) hv[i] = s[S::H1 + i];
+      float sig;
+      dense_row<W, WP, 1, true>(sw + L.w_off[2], sw + L.b_off[2], hv, &sig);
+      dense_row<W, WP, W, false>(sw + L.w_off[3], sw + L.b_off[3], hv, s + S::CAT);
+      {
+        float de[D];
+        encode_f32<4>(d, de);
+#pragma unroll
+        for (int i = 0; i < D; ++i) s[S::CAT + W + i] = de[i];
+      }
+      {
+        float cat[W + D];
+#pragma unroll
+        for (int i = 0; i < W + D; ++i) cat[i] = s[S::CAT + i];
+        dense_row<W + D, DP, W, true>(sw + L.w_off[4], sw + L.b_off[4], cat, s + S::G);
+      }
+      float gv[W];
+#pragma unroll
+      for (int i = 0; i < W; ++i) gv[i] = s[S::G + i];
+      float z[3];
+      dense_row<W, WP, 3, false>(sw + L.w_off[5], sw + L.b_off[5], gv, z);
+      // ---- backward (mlp.py:291-316)
+      float dzc[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float col = sigmoid_split(z[c]);
+        dzc[c] = __fmul_rn(__fmul_rn(A.d_color[3 * src + c], col), __fsub_rn(1.0f, col));
+        s[S::DZC + c] = dzc[c];
+      }
+      float dv[W];
+      dense_t_row<W, WP, 3>(sw + L.w_off[5], dzc, dv);  // dg
+#pragma unroll
+      for (int i = 0; i < W; ++i) {
+        dv[i] = gv[i] > 0.f ? dv[i] : 0.f;  // dz_dir = dg * (g > 0)
+        s[S::DZD + i] = dv[i];
+      }
+      float dfeat[W];
+      dense_t_row<W, DP, W>(sw + L.w_off[4], dv, dfeat);  // first W columns of d_dir_in
+#pragma unroll
+      for (int i = 0; i < W; ++i) s[S::DZF + i] = dfeat[i];
+      const float dzs = sig > 0.f ? A.d_sigma[src] : 0.f;  // d_sigma * (sigma > 0)
+      s[S::DZS] = dzs;
+      float dh[W];
+      dense_t_row<W, WP, W>(sw + L.w_off[3], dfeat, dh);
+      {
+        const float* wd = sw + L.w_off[2];
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+          dh[i] = __fadd_rn(dh[i], __fmul_rn(dzs, wd[i]));  // dh + matmul(dz_density, W_density)
+          dh[i] = s[S::H1 + i] > 0.f ? dh[i] : 0.f;         // dz trunk1
+          s[S::DZ1 + i] = dh[i];
+        }
+      }
+      float dh0[W];
+      dense_t_row<W, WP, W>(sw + L.w_off[1], dh, dh0);
+#pragma unroll
+      for (int i = 0; i < W; ++i) s[S::DZ0 + i] = s[S::H0 + i] > 0.f ? dh0[i] : 0.f;
+    }
+    __syncthreads();
+    // ---- phase B: parameter sums over this tile's rows (gw = dz^T in, gb = sum dz)
+    for (int p = tid; p < S::TOTAL; p += TR) {
+      int l = 0, q = p;
+      while (q >= S::count(l)) q -= S::count(l++);
+      const int in = S::in_dim(l), out = S::out_dim(l);
+      const bool bias = q >= out * in;
+      const int o = bias ? q - out * in : q / in, i = bias ? 0 : q % in;
+      const float* dzp = srow + S::dz_off(l) + o;
+      const float* inp = srow + S::in_off(l) + i;
+      float acc = 0.f;
+      if (bias) {
+        for (int r = 0; r < n_in; ++r) acc = __fadd_rn(acc, dzp[r * LD]);
+      } else {
+        for (int r = 0; r < n_in; ++r) acc = fmaf(dzp[r * LD], inp[r * LD], acc);
+      }
+      float* dst = bias ? A.gb[l] + cell * out + o : A.gw[l] + (cell * out + o) * in + i;
+      *dst = t == 0 ? acc : __fadd_rn(*dst, acc);
+    }
+  }
+}
+
+template <int W>
+static bool launch_bwd_width(const float* packed, const Fp32Layout& L, const BwdArgs& A, int64_t n_cells,
+                             cudaStream_t st) {
+  using S = BwdShape<W>;
+  const size_t smem = (size_t)L.cell_floats * 4 + (size_t)S::TR * S::LD * 4;
+  static thread_local size_t set = 0;
+  if (set < smem) {
+    if (cudaFuncSetAttribute(k_grouped_backward<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return false;
+    set = smem;
+  }
+  if (n_cells > 0) k_grouped_backward<W><<<(unsigned)n_cells, S::TR, smem, st>>>(packed, L, A);
+  return true;
+}
+
+bool launch_grouped_backward(const LayerTable& t, const float* packed, const BwdArgs& A, int64_t n_cells,
+                             cudaStream_t st) {
+  if (!prepare_mlp_fp32(t)) return false;
+  const Fp32Layout L = make_fp32_layout(t);
+  return t.width == 32 ? launch_bwd_width<32>(packed, L, A, n_cells, st)
+                       : launch_bwd_width<64>(packed, L, A, n_cells, st);
+}
+
+// ---------------------------------------------------------------------------
+// photometric loss (train.py:243-288): dense (ray, slot) compositing of the
+// queried samples, float64 loss, and the per-query upstream gradients.
+// ---------------------------------------------------------------------------
+// scatter queried samples into the dense (B, k) grid: (r, g, b, alpha) and the
+// query index per slot; the density is perturbed / rectified first when a
+// noise vector is given (train.py:245-249)
+__global__ void k_photo_scatter(PhotoArgs A, float4* dense, int32_t* qidx, uint8_t* nmask) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < A.n_queries;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ray = A.ray_index[q], slot = A.slot[q];
+    float s = A.sigma[q];
+    if (A.noise) {
+      const float sh = __fadd_rn(s, A.noise[q]);
+      nmask[q] = sh > 0.f;
+      s = fmaxf(sh, 0.f);
+    }
+    const float a = -expm1f(__fmul_rn(-s, A.deltas[ray]));  // density_to_alpha (core.py:187-194)
+    const int64_t j = ray * A.k + slot;
+    dense[j] = make_float4(A.color[3 * q], A.color[3 * q + 1], A.color[3 * q + 2], a);
+    qidx[j] = (int32_t)q;
+  }
+}
+
+// one thread per ray: forward composite (cumprod transmittance, weights,
+// prediction + background), squared error in float64, then the backward
+// rest-of-ray recurrence from the last slot down (no division by 1 - alpha)
+__global__ void k_photo_ray(PhotoArgs A, const float4* __restrict__ dense, const int32_t* __restrict__ qidx,
+                            const uint8_t* __restrict__ nmask, float* tb, double* loss_parts) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= A.n_rays) return;
+  const int k = A.k;
+  const float4* dr = dense + b * k;
+  float* tbr = tb + b * k;
+  float tr = 1.0f, p0 = 0.f, p1 = 0.f, p2 = 0.f;
+  for (int i = 0; i < k; ++i) {
+    const float4 v = dr[i];
+    tbr[i] = tr;                          // t_before
+    const float w = __fmul_rn(tr, v.w);   // weights = t_before * alpha
+    p0 = __fadd_rn(p0, __fmul_rn(w, v.x));
+    p1 = __fadd_rn(p1, __fmul_rn(w, v.y));
+    p2 = __fadd_rn(p2, __fmul_rn(w, v.z));
+    tr = __fmul_rn(tr, __fsub_rn(1.0f, v.w));  // cumprod(1 - alpha)
+  }
+  const float r0 = __fsub_rn(__fadd_rn(p0, __fmul_rn(tr, A.bg[0])), A.gt[3 * b + 0]);
+  const float r1 = __fsub_rn(__fadd_rn(p1, __fmul_rn(tr, A.bg[1])), A.gt[3 * b + 1]);
+  const float r2 = __fsub_rn(__fadd_rn(p2, __fmul_rn(tr, A.bg[2])), A.gt[3 * b + 2]);
+  loss_parts[b] = __dadd_rn(__dadd_rn(__dmul_rn((double)r0, (double)r0), __dmul_rn((double)r1, (double)r1)),
+                            __dmul_rn((double)r2, (double)r2));
+  if (!A.d_color_q) return;
+  const float d0 = __fmul_rn(A.two_over_b, r0), d1 = __fmul_rn(A.two_over_b, r1), d2 = __fmul_rn(A.two_over_b, r2);
+  const float delta = A.deltas[b];
+  float re0 = A.bg[0], re1 = A.bg[1], re2 = A.bg[2];  // rest[:, k-1] = bg
+  for (int i = k - 1; i >= 0; --i) {
+    const float4 v = dr[i];
+    const int32_t q = qidx[b * k + i];
+    if (q >= 0) {
+      const float t = tbr[i];
+      // d_alpha = sum_c (dpred_c * t_before) * (color_c - rest_c)
+      const float e0 = __fmul_rn(__fmul_rn(d0, t), __fsub_rn(v.x, re0));
+      const float e1 = __fmul_rn(__fmul_rn(d1, t), __fsub_rn(v.y, re1));
+      const float e2 = __fmul_rn(__fmul_rn(d2, t), __fsub_rn(v.z, re2));
+      const float da = __fadd_rn(__fadd_rn(e0, e1), e2);
+      const float w = __fmul_rn(t, v.w);
+      A.d_color_q[3 * q + 0] = __fmul_rn(w, d0);
+      A.d_color_q[3 * q + 1] = __fmul_rn(w, d1);
+      A.d_color_q[3 * q + 2] = __fmul_rn(w, d2);
+      float ds = __fmul_rn(__fmul_rn(da, delta), __fsub_rn(1.0f, v.w));
+      if (A.noise && !nmask[q]) ds = __fmul_rn(ds, 0.f);  // d_sigma_q * noise_mask
+      A.d_sigma_q[q] = ds;
+    }
+    // rest[:, i-1] = alpha_i * color_i + (1 - alpha_i) * rest[:, i]
+    const float om = __fsub_rn(1.0f, v.w);
+    re0 = __fadd_rn(__fmul_rn(v.w, v.x), __fmul_rn(om, re0));
+    re1 = __fadd_rn(__fmul_rn(v.w, v.y), __fmul_rn(om, re1));
+    re2 = __fadd_rn(__fmul_rn(v.w, v.z), __fmul_rn(om, re2));
+  }
+}
+
+// fixed-order float64 sum of n values (one CTA): deterministic loss reduction
+__global__ void __launch_bounds__(1024) k_sum_f64(const double* v, int64_t n, double* out) {
+  __shared__ double s[1024];
+  double acc = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += 1024) acc = __dadd_rn(acc, v[j]);
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 512; w; w >>= 1) {
+    if ((int)threadIdx.x < w) s[threadIdx.x] = __dadd_rn(s[threadIdx.x], s[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+size_t photo_workspace(int64_t n_rays, int k, int64_t n_queries) {
+  const size_t cells = (size_t)n_rays * (size_t)k;
+  return gf_align(cells * 16) + gf_align(cells * 4) * 2 + gf_align((size_t)n_queries + 1) +
+         gf_align((size_t)n_rays * 8 + 8) + gf_align(8);
+}
+
+void launch_photometric(const PhotoArgs& A, void* ws, double* loss_sum, cudaStream_t st) {
+  char* p = (char*)ws;
+  const size_t cells = (size_t)A.n_rays * (size_t)A.k;
+  float4* dense = (float4*)p;
+  p += gf_align(cells * 16);
+  int32_t* qidx = (int32_t*)p;
+  p += gf_align(cells * 4);
+  float* tb = (float*)p;
+  p += gf_align(cells * 4);
+  uint8_t* nmask = (uint8_t*)p;
+  p += gf_align((size_t)A.n_queries + 1);
+  double* parts = (double*)p;
+  cudaMemsetAsync(dense, 0, cells * 16, st);
+  cudaMemsetAsync(qidx, 0xFF, cells * 4, st);
+  if (A.n_queries > 0) {
+    const unsigned g = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(A.n_queries, 256), (int64_t)num_sms() * 8);
+    k_photo_scatter<<<g, 256, 0, st>>>(A, dense, qidx, nmask);
+  }
+  if (A.n_rays > 0) k_photo_ray<<<(unsigned)gf_div_up<int64_t>(A.n_rays, 128), 128, 0, st>>>(A, dense, qidx, nmask, tb,
+                                                                                            parts);
+  k_sum_f64<<<1, 1024, 0, st>>>(parts, A.n_rays, loss_sum);
+}
+
+// ---------------------------------------------------------------------------
+// optimizer (train.py:130-160): Adam in place over one flat parameter array,
+// float32 with numpy's operation order (NEP 50: Python-float coefficients are
+// rounded to float32 before use); L2 term sum(x^2) in float64.
+// ---------------------------------------------------------------------------
+__global__ void k_adam(float* p, const float* g, float* m, float* v, int64_t n, AdamCoef c) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const float gj = g[j];
+    float mj = __fmul_rn(m[j], c.b1);                          // m *= b1
+    mj = __fadd_rn(mj, __fmul_rn(c.one_minus_b1, gj));         // m += (1 - b1) * g
+    float vj = __fmul_rn(v[j], c.b2);                          // v *= b2
+    vj = __fadd_rn(vj, __fmul_rn(__fmul_rn(c.one_minus_b2, gj), gj));  // v += (1 - b2) * g * g
+    // p -= lr * (m / bc1) / (sqrt(v / bc2) + eps)
+    const float num = __fmul_rn(c.lr, __fdiv_rn(mj, c.bc1));
+    const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(vj, c.bc2)), c.eps);
+    p[j] = __fsub_rn(p[j], __fdiv_rn(num, den));
+    m[j] = mj;
+    v[j] = vj;
+  }
+}
+
+void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, const AdamCoef& c, cudaStream_t st) {
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(n, 256), (int64_t)num_sms() * 16);
+  k_adam<<<grid, 256, 0, st>>>(p, g, m, v, n, c);
+}
+
+// partial sums of squares in float64, then one fixed-order CTA sum
+__global__ void __launch_bounds__(256) k_sumsq(const float* x, int64_t n, double* parts) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x; j < n; j += (int64_t)gridDim.x * 256) {
+    const double d = (double)x[j];
+    acc = __dadd_rn(acc, __dmul_rn(d, d));
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w; w >>= 1) {
+    if ((int)threadIdx.x < w) s[threadIdx.x] = __dadd_rn(s[threadIdx.x], s[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) parts[blockIdx.x] = s[0];
+}
+
+// out = y + f * x (two roundings, as numpy's g + (2*weight) * w); y NULL: f * x
+__global__ void k_axpy(const float* x, const float* y, int64_t n, float f, float* out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const float r = __fmul_rn(f, x[j]);
+    out[j] = y ? __fadd_rn(y[j], r) : r;
+  }
+}
+
+// distill_step's loss and upstream gradients (train.py:369-385) per query:
+// alphas at the reference segment, L2 on alpha (weight w_a) and colour
+__global__ void k_distill(DistillArgs A, double* parts) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < A.n; q += (int64_t)gridDim.x * blockDim.x) {
+    const float ta = -expm1f(__fmul_rn(-A.t_sigma[q], A.delta));
+    const float sa = -expm1f(__fmul_rn(-A.s_sigma[q], A.delta));
+    const float da = __fsub_rn(sa, ta);
+    double col = 0.0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float dc = __fsub_rn(A.s_color[3 * q + c], A.t_color[3 * q + c]);
+      col = __dadd_rn(col, __dmul_rn((double)dc, (double)dc));
+      A.d_color[3 * q + c] = __fmul_rn(A.c_color, dc);
+    }
+    // (2 w_a / m) * d_alpha * delta * (1 - s_alpha)
+    A.d_sigma[q] = __fmul_rn(__fmul_rn(__fmul_rn(A.c_sigma, da), A.delta), __fsub_rn(1.0f, sa));
+    parts[2 * q] = __dmul_rn((double)da, (double)da);
+    parts[2 * q + 1] = col;
+  }
+}
+
+// per-term fixed-order float64 sums of the (alpha, colour) parts
+__global__ void __launch_bounds__(1024) k_sum_pairs_f64(const double* v, int64_t n, double* out) {
+  __shared__ double s[2][1024];
+  double a = 0.0, b = 0.0;
+  for (int64_t j = threadIdx.x; j < n; j += 1024) {
+    a = __dadd_rn(a, v[2 * j]);
+    b = __dadd_rn(b, v[2 * j + 1]);
+  }
+  s[0][threadIdx.x] = a;
+  s[1][threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 512; w; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      s[0][threadIdx.x] = __dadd_rn(s[0][threadIdx.x], s[0][threadIdx.x + w]);
+      s[1][threadIdx.x] = __dadd_rn(s[1][threadIdx.x], s[1][threadIdx.x + w]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s[0][0];
+    out[1] = s[1][0];
+  }
+}
+
+void launch_distill(const DistillArgs& A, double* parts, double* sums, cudaStream_t st) {
+  if (A.n > 0) {
+    const unsigned grid = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(A.n, 256), (int64_t)num_sms() * 16);
+    k_distill<<<grid, 256, 0, st>>>(A, parts);
+  }
+  k_sum_pairs_f64<<<1, 1024, 0, st>>>(parts, A.n, sums);
+}
+
+void launch_sumsq(const float* x, int64_t n, double* parts, int n_parts, double* out, cudaStream_t st) {
+  k_sumsq<<<n_parts, 256, 0, st>>>(x, n, parts);
+  k_sum_f64<<<1, 1024, 0, st>>>(parts, n_parts, out);
+}
+
+void launch_axpy(const float* x, const float* y, int64_t n, float f, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(n, 256), (int64_t)num_sms() * 16);
+  k_axpy<<<grid, 256, 0, st>>>(x, y, n, f, out);
+}
+
+}  // namespace gf

@@ -1,16 +1,313 @@
-"""The piece of gridfield.train the hot path needs (mirror of
-/root/reference/pkg/src/gridfield/train.py:577-586).
+"""Training-loop pieces of gridfield.train on the device (mirror of
+/root/reference/pkg/src/gridfield/train.py).
 
-``density_probe(model)`` is the density field occupancy extraction probes
-(cli.py:155-160).  It is a plain callable, as in the reference; because it is
-recognisable, ``extract_occupancy`` runs it on the device in one library call
-(gf_extract_occupancy_network) instead of one host round trip per chunk.
-Training itself (photometric fine-tuning, distillation) is out of scope.
+What runs where:
+* ``photometric_loss_and_grads`` (train.py:212-288): grouping, the fp32
+  grouped forward, dense compositing + float64 loss + the rest-of-ray
+  gradient recurrence (gf_photometric_loss), and the fused per-cell backward
+  (gf_grouped_backward) all run on the device; the regularisation gradient is
+  folded in on the device (gf_axpy) before one download of the gradients.
+* ``distill_step`` (train.py:341-390): the teacher query, the student's
+  grouped forward / backward, the loss terms (gf_distill_loss) and Adam run
+  on the device.  The in-cell sample draws use the caller's numpy Generator,
+  as in the reference, so the stream of random numbers is the same.
+* ``adam_update`` (train.py:130-143) and ``regularization_term``
+  (train.py:146-160): one kernel per parameter array (gf_adam_update,
+  gf_sum_squares, gf_axpy).  Parameters stay numpy arrays in place, as the
+  reference API requires; each step uploads them and writes them back.
+* ``prepare_ray_samples`` (train.py:175-209): numpy sample placement with the
+  caller's Generator, with the occupancy test and the clip on the device.
+* ``density_probe`` (train.py:577-586): recognised by ``extract_occupancy``,
+  which then runs the probe lattice on the device in one call.
+
+The device path computes in float32, the reference's parameter dtype; float64
+parameter stacks are rejected.  The data loaders, the pipeline driver, and the
+CLI reporting (``photometric_step``, ``run_pipeline`` and the rest) are out of
+scope.
 """
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
+
+from . import _device as D
+from . import _native as N
+from . import mlp
+from .batched import GroupedLayout, QueryBatch, group_by_network, grouped_backward_device, grouped_forward_device
+from .core import Aabb, clip_into
+from .render import intersect_aabb
+
+REGULARIZED_LAYERS = ("direction", "color")  # train.py:33
+
+
+@dataclass
+class TrainConfig:
+    """train.py:36-110 (the fields the device steps read, same defaults)."""
+
+    batch_size_pixels: int = 8192
+    learning_rate: float = 5e-4
+    lr_final_fraction: float = 0.1
+    l2_reg_weight: float = 1e-6
+    teacher_steps: int = 600_000
+    distill_steps: int = 150_000
+    finetune_steps: int = 1_000_000
+    distill_points_per_cell: int = 32
+    distill_alpha_weight: float = 1.0
+    distill_delta: float | None = None
+    k_train: int = 384
+    density_noise_std: float = 0.0
+    seed: int = 0
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
+    grid_max_dim: int = 16
+    occupancy_factor: int = 16
+    occupancy_tau: float = 10.0
+    teacher_hidden_layers: int = 10
+    teacher_hidden_width: int = 256
+    teacher_direction_width: int = 128
+    teacher_skip_layer: int | None = 5
+    student_hidden_layers: int = 4
+    student_hidden_width: int = 32
+    background: tuple = (1.0, 1.0, 1.0)
+    log_every: int = 100
+
+    def teacher_architecture(self, encoding) -> mlp.MlpArchitecture:
+        return mlp.teacher_architecture(hidden_layers=self.teacher_hidden_layers,
+                                        hidden_width=self.teacher_hidden_width,
+                                        direction_layer_width=self.teacher_direction_width,
+                                        skip_layer=self.teacher_skip_layer,
+                                        position_input_dim=encoding.position_dim,
+                                        direction_input_dim=encoding.direction_dim)
+
+    def student_architecture(self, encoding) -> mlp.MlpArchitecture:
+        return mlp.MlpArchitecture(hidden_layers=self.student_hidden_layers, hidden_width=self.student_hidden_width,
+                                   position_input_dim=encoding.position_dim,
+                                   direction_input_dim=encoding.direction_dim)
+
+
+def lr_schedule(step: int, base_lr: float, horizon: int, final_fraction: float = 0.1) -> float:
+    """train.py:112-116."""
+    if horizon <= 0:
+        return base_lr
+    return float(base_lr * final_fraction ** (step / horizon))
+
+
+@dataclass
+class AdamState:
+    """train.py:119-127."""
+
+    m: mlp.MlpParams
+    v: mlp.MlpParams
+    step: int = 0
+
+    @classmethod
+    def for_params(cls, params: mlp.MlpParams) -> "AdamState":
+        return cls(m=mlp.map_params(np.zeros_like, params), v=mlp.map_params(np.zeros_like, params))
+
+
+def _f32(x) -> float:
+    """A Python scalar as numpy's NEP 50 rule applies it to a float32 array."""
+    return float(np.float32(x))
+
+
+def _require_f32(params: mlp.MlpParams):
+    if params.dtype != np.float32:
+        raise N.NativeError(f"the device training path computes in float32, got {params.dtype} parameters")
+
+
+def adam_update(params: mlp.MlpParams, grads: mlp.MlpParams, state: AdamState, lr: float, cfg: TrainConfig):
+    """train.py:130-143: one Adam step, in place, on the device (gf_adam_update
+    per parameter array, float32 in numpy's operation order)."""
+    _require_f32(params)
+    t = D.require_cuda()
+    state.step += 1
+    b1, b2, eps = cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps
+    bc1 = 1.0 - b1**state.step
+    bc2 = 1.0 - b2**state.step
+    coef = (N.C.c_float * 8)(*[_f32(v) for v in (b1, 1.0 - b1, b2, 1.0 - b2, bc1, bc2, lr, eps)])
+    for (_, p), (_, g), (_, m), (_, v) in zip(params.arrays(), grads.arrays(), state.m.arrays(), state.v.arrays()):
+        pd, gd = D.to_device(p, t.float32), D.to_device(g, t.float32)
+        md, vd = D.to_device(m, t.float32), D.to_device(v, t.float32)
+        N.check(N.lib().gf_adam_update(N.ptr(pd), N.ptr(gd), N.ptr(md), N.ptr(vd), pd.numel(), coef,
+                                       D.stream_handle()), "adam_update")
+        p[...] = pd.cpu().numpy().reshape(p.shape)
+        m[...] = md.cpu().numpy().reshape(m.shape)
+        v[...] = vd.cpu().numpy().reshape(v.shape)
+
+
+def _sum_squares(x_dev) -> "object":
+    t = D.require_cuda()
+    out = D.empty((1,), t.float64)
+    ws = D.workspace(N.lib().gf_sum_squares_workspace_bytes())
+    N.check(N.lib().gf_sum_squares(N.ptr(x_dev), x_dev.numel(), N.ptr(out), N.ptr(ws), ws.numel(), D.stream_handle()),
+            "sum_squares")
+    return out
+
+
+def _axpy(x_dev, y_dev, f: float, out_dev):
+    N.check(N.lib().gf_axpy(N.ptr(x_dev), N.ptr(y_dev), x_dev.numel(), _f32(f), N.ptr(out_dev), D.stream_handle()),
+            "axpy")
+
+
+def _regularization_device(params: mlp.MlpParams, weight: float):
+    """(value, {layer: (w_dev, b_dev)}) of the L2 term; device sums / scales."""
+    t = D.require_cuda()
+    value = 0.0
+    dev = {}
+    for name in REGULARIZED_LAYERS:
+        w = D.to_device(params.weights[name], t.float32)
+        b = D.to_device(params.biases[name], t.float32)
+        value += float(_sum_squares(w).item() + _sum_squares(b).item())
+        dev[name] = (w, b)
+    return weight * value, dev
+
+
+def regularization_term(params: mlp.MlpParams, weight: float):
+    """train.py:146-160: L2 penalty on the view-dependent tail; gradient zero
+    everywhere except those layers (2 * weight * x)."""
+    _require_f32(params)
+    t = D.require_cuda()
+    value, dev = _regularization_device(params, weight)
+    grads = mlp.map_params(np.zeros_like, params)
+    for name, (w, b) in dev.items():
+        gw, gb = D.empty(w.shape, t.float32), D.empty(b.shape, t.float32)
+        _axpy(w, None, 2.0 * weight, gw)
+        _axpy(b, None, 2.0 * weight, gb)
+        grads.weights[name][...] = gw.cpu().numpy()
+        grads.biases[name][...] = gb.cpu().numpy()
+    return value, grads
+
+
+@dataclass
+class RaySamples:
+    """train.py:163-172: retained quadrature points of a ray batch."""
+
+    positions: np.ndarray
+    directions: np.ndarray
+    ray_index: np.ndarray
+    slot: np.ndarray
+    deltas: np.ndarray
+    n_rays: int
+    k: int
+
+
+def prepare_ray_samples(origins, directions, aabb: Aabb, k: int, stratified: bool, rng, occ=None) -> RaySamples:
+    """train.py:175-209: stratified equidistant samples, ESS-filtered.  The
+    jitter comes from the caller's Generator (same draws as the reference);
+    the clip and the occupancy test run on the device."""
+    n = len(origins)
+    t0, t1 = intersect_aabb(origins, directions, aabb)
+    hit = t1 > t0
+    seg = np.where(hit, (t1 - t0) / k, 0.0).astype(np.float32)
+    jitter = rng.random((n, k), dtype=np.float32) if stratified else np.full((n, k), 0.5, np.float32)
+    ts = t0[:, None].astype(np.float32) + (np.arange(k)[None, :] + jitter) * seg[:, None]
+    pts = origins[:, None, :].astype(np.float32) + ts[..., None] * directions[:, None, :].astype(np.float32)
+    pts = clip_into(pts, aabb)
+    keep = np.repeat(hit[:, None], k, axis=1)
+    if occ is not None:
+        keep &= occ.occupied_at(pts.reshape(-1, 3)).reshape(n, k)
+    ray_index, slot = np.nonzero(keep)
+    return RaySamples(positions=pts[ray_index, slot], directions=np.asarray(directions, dtype=np.float32)[ray_index],
+                      ray_index=ray_index, slot=slot, deltas=seg, n_rays=n, k=k)
+
+
+def _grads_to_host(grid, gw, gb) -> mlp.MlpParams:
+    specs = grid.arch.layers()
+    return mlp.MlpParams(grid.arch, {s.name: w.cpu().numpy() for s, w in zip(specs, gw)},
+                         {s.name: b.cpu().numpy() for s, b in zip(specs, gb)})
+
+
+def photometric_loss_and_grads(model, samples: RaySamples, gt: np.ndarray, background, reg_weight: float = 0.0,
+                               want_grads: bool = True, sigma_noise: np.ndarray | None = None):
+    """train.py:212-288 on the device: mean squared pixel error of the
+    composited batch (float64), plus parameter gradients (MlpParams)."""
+    _require_f32(model.params)
+    t = D.require_cuda()
+    b, k = samples.n_rays, samples.k
+    layout = group_by_network(QueryBatch(samples.positions, samples.directions, model.cell_index(samples.positions)),
+                              model.n_cells)
+    cache = grouped_forward_device(model, layout)
+    q = layout.n_queries
+    ri = D.to_device(np.asarray(samples.ray_index, np.int64), t.int64)
+    sl = D.to_device(np.asarray(samples.slot, np.int64), t.int64)
+    noise = None if sigma_noise is None else D.to_device(np.asarray(sigma_noise).astype(np.float32), t.float32)
+    deltas = D.to_device(np.asarray(samples.deltas).astype(np.float32), t.float32)
+    gtd = D.to_device(np.asarray(gt).astype(np.float32).reshape(-1, 3), t.float32)
+    bg = (N.C.c_float * 3)(*[float(v) for v in np.asarray(background, dtype=np.float32).reshape(3)])
+    dcq = D.empty((q, 3), t.float32) if want_grads else None
+    dsq = D.empty((q,), t.float32) if want_grads else None
+    loss_sum = D.empty((1,), t.float64)
+    ws = D.workspace(N.lib().gf_photometric_workspace_bytes(b, k, q))
+    N.check(N.lib().gf_photometric_loss(b, k, q, N.ptr(ri), N.ptr(sl), N.ptr(cache.rgb), N.ptr(cache.sigma),
+                                        N.ptr(noise), N.ptr(deltas), N.ptr(gtd), bg, _f32(2.0 / b) if b else 0.0,
+                                        N.ptr(dcq), N.ptr(dsq), N.ptr(loss_sum), N.ptr(ws), ws.numel(),
+                                        D.stream_handle()), "photometric_loss")
+    loss = float(loss_sum.item() / b) if b else float("nan")
+    reg_dev = None
+    if reg_weight > 0.0:
+        reg_value, reg_dev = _regularization_device(model.params, reg_weight)
+        loss += reg_value
+    if not want_grads:
+        return loss, None
+    gw, gb = grouped_backward_device(model, layout, cache, dcq, dsq)
+    if reg_dev is not None:
+        names = [s.name for s in model.arch.layers()]
+        for name, (w, bias) in reg_dev.items():
+            li = names.index(name)
+            _axpy(w, gw[li], 2.0 * reg_weight, gw[li])  # g + (2 * weight) * w
+            _axpy(bias, gb[li], 2.0 * reg_weight, gb[li])
+    return loss, _grads_to_host(model, gw, gb)
+
+
+def _unit_sphere(rng, shape) -> np.ndarray:
+    """train.py:335-338."""
+    v = rng.normal(size=(*shape, 3)).astype(np.float32)
+    v /= np.linalg.norm(v, axis=-1, keepdims=True)
+    return v
+
+
+def distill_step(student, teacher, cfg: TrainConfig, state: AdamState, rng, delta_ref: float) -> float:
+    """train.py:341-390: regress every cell network onto the teacher at
+    random in-cell points; loss terms, gradients and the update on the device."""
+    _require_f32(student.params)
+    t = D.require_cuda()
+    n, p = student.n_cells, cfg.distill_points_per_cell
+    res = student.resolution
+    cell = student.aabb.cell_size(res).astype(np.float32)
+    flat = np.arange(n)
+    idx3 = np.stack([flat % res[0], (flat // res[0]) % res[1], flat // (res[0] * res[1])], axis=-1)
+    lows = (student.aabb.b_min + idx3 * student.aabb.cell_size(res)).astype(np.float32)
+    u = rng.random((n, p, 3), dtype=np.float32) * np.float32(1.0 - 2e-5) + np.float32(1e-5)
+    positions = clip_into(lows[:, None, :] + u * cell[None, None, :], student.aabb).reshape(-1, 3)
+    directions = _unit_sphere(rng, (n, p)).reshape(-1, 3)
+
+    pos_d = D.to_device(positions, t.float32)
+    dir_d = D.to_device(directions, t.float32)
+    t_color, t_sigma = teacher.query_points(pos_d, dir_d)
+    # the student lattice: cell c owns rows [c*p, (c+1)*p), identity order
+    m = n * p
+    layout = GroupedLayout(positions=positions, directions=directions, order=np.arange(m, dtype=np.int64),
+                           inverse=np.arange(m, dtype=np.int64), offsets=np.arange(0, m + 1, p, dtype=np.int64),
+                           n_networks=n)
+    cache = grouped_forward_device(student, layout, pos_d, dir_d)
+    w_a = cfg.distill_alpha_weight
+    dc = D.empty((m, 3), t.float32)
+    ds = D.empty((m,), t.float32)
+    sums = D.empty((2,), t.float64)
+    ws = D.workspace(N.lib().gf_distill_workspace_bytes(m))
+    N.check(N.lib().gf_distill_loss(m, N.ptr(cache.rgb), N.ptr(cache.sigma), N.ptr(t_color), N.ptr(t_sigma),
+                                    _f32(delta_ref), _f32(2.0 * w_a / m), _f32(2.0 / m), N.ptr(dc), N.ptr(ds),
+                                    N.ptr(sums), N.ptr(ws), ws.numel(), D.stream_handle()), "distill_loss")
+    s_a, s_c = sums.cpu().numpy()
+    loss = float(w_a * s_a + s_c) / m
+    gw, gb = grouped_backward_device(student, layout, cache, dc, ds)
+    grads = _grads_to_host(student, gw, gb)
+    lr = lr_schedule(state.step, cfg.learning_rate, cfg.distill_steps, cfg.lr_final_fraction)
+    adam_update(student.params, grads, state, lr, cfg)
+    return loss
 
 
 class DensityProbe:

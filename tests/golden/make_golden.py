@@ -340,6 +340,93 @@ def gen_extract():
     save("extract", **out)
 
 
+def _fixed_batch(grid, n_rays, k, seed, occ=None):
+    """test_train.py:92-103 fixed_batch."""
+    from gridfield import train
+
+    rng = np.random.default_rng(seed)
+    origins = np.tile(np.array([[-2.0, 0.0, 0.0]], np.float32), (n_rays, 1))
+    offsets = rng.uniform(-0.6, 0.6, (n_rays, 2)).astype(np.float32)
+    targets = np.concatenate([np.zeros((n_rays, 1), np.float32), offsets], axis=1)
+    dirs = targets - origins
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    samples = train.prepare_ray_samples(origins, dirs, grid.aabb, k, True, rng, occ=occ)
+    gt = rng.random((n_rays, 3)).astype(np.float32)
+    return origins, dirs, samples, gt
+
+
+def _grads_dict(prefix, g):
+    out = {}
+    for k_, v in g.weights.items():
+        out[f"{prefix}w_{k_}"] = np.asarray(v)
+    for k_, v in g.biases.items():
+        out[f"{prefix}b_{k_}"] = np.asarray(v)
+    return out
+
+
+def gen_train():
+    """Training kernels through the reference: grouped_backward
+    on random upstream gradients (32- and 64-wide), photometric_loss_and_grads
+    on test_train.py's fixed batch (with and without regularisation / density
+    noise), adam_update, and one distill_step."""
+    from gridfield import train
+
+    out = {}
+    aabb = core.Aabb((0.0, 0.0, 0.0), (1.0, 1.0, 1.0))
+    # grouped_backward, 32-wide (3,2,2) lattice with density biases around 0
+    for tag, res, arch, n in (("g32", (3, 2, 2), None, 3000), ("g64", (2, 1, 1), mlp.MlpArchitecture(hidden_width=64), 700)):
+        g = ggrid.init_network_grid(aabb, res, seed=11, arch=arch)
+        rng = np.random.default_rng(12)
+        for k_ in g.params.biases:
+            g.params.biases[k_][:] = rng.normal(0, 0.3, g.params.biases[k_].shape).astype(np.float32)
+        pts = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+        pts[:7] = np.float32(1.0)  # upper faces
+        dirs = rng.normal(size=(n, 3)).astype(np.float32)
+        dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+        dcol = rng.normal(size=(n, 3)).astype(np.float32)
+        dsig = rng.normal(size=n).astype(np.float32)
+        layout = batched.group_by_network(batched.QueryBatch(pts, dirs, g.cell_index(pts)), g.n_cells)
+        caches = []
+        batched.grouped_forward(g, layout, caches=caches)
+        grads = batched.grouped_backward(g, layout, caches, dcol, dsig)
+        out.update({f"{tag}_pts": pts, f"{tag}_dirs": dirs, f"{tag}_dcol": dcol, f"{tag}_dsig": dsig,
+                    f"{tag}_res": np.array(res), f"{tag}_biases": np.concatenate([np.asarray(v).ravel() for v in g.params.biases.values()])})
+        out.update(_grads_dict(f"{tag}_", grads))
+    # photometric loss + grads on the reference test's fixed batch
+    g = ggrid.init_network_grid(aabb, (2, 2, 2), seed=5)
+    g.params.biases["density"][:] = 1.5
+    _, _, smp, gt = _fixed_batch(g, 64, 32, 1)
+    noise = np.random.default_rng(13).normal(0, 0.5, len(smp.positions)).astype(np.float32)
+    out.update(ph_pos=smp.positions, ph_dirs=smp.directions, ph_ray=smp.ray_index, ph_slot=smp.slot,
+               ph_deltas=smp.deltas, ph_nrays=np.int64(smp.n_rays), ph_k=np.int64(smp.k), ph_gt=gt, ph_noise=noise)
+    for tag, kw in (("ph0", {}), ("ph_reg", {"reg_weight": 1e-3}), ("ph_noise", {"sigma_noise": noise})):
+        loss, grads = train.photometric_loss_and_grads(g, smp, gt, (1.0, 1.0, 1.0), **kw)
+        out[f"{tag}_loss"] = np.float64(loss)
+        out.update(_grads_dict(f"{tag}_", grads))
+    # adam: two steps with the ph0 gradients
+    cfg = train.TrainConfig()
+    _, grads = train.photometric_loss_and_grads(g, smp, gt, (1.0, 1.0, 1.0))
+    st = train.AdamState.for_params(g.params)
+    p = g.params.copy()
+    train.adam_update(p, grads, st, 5e-4, cfg)
+    train.adam_update(p, grads, st, 3e-4, cfg)
+    out.update(_grads_dict("adam_p_", p))
+    out.update(_grads_dict("adam_m_", st.m))
+    out.update(_grads_dict("adam_v_", st.v))
+    # one distill step (test_train.py:255-270 setup)
+    enc = core.PositionalEncoding()
+    dcfg = train.TrainConfig(distill_points_per_cell=8, teacher_hidden_layers=4, teacher_hidden_width=32,
+                             teacher_direction_width=32, teacher_skip_layer=None)
+    teacher = ggrid.init_network_grid(aabb, (1, 1, 1), seed=6, arch=dcfg.teacher_architecture(enc), encoding=enc)
+    student = ggrid.init_network_grid(aabb, (2, 2, 2), seed=7)
+    st = train.AdamState.for_params(student.params)
+    losses = [train.distill_step(student, teacher, dcfg, st, np.random.default_rng(3), delta_ref=0.01)]
+    out["ds_loss"] = np.array(losses)
+    out.update(_grads_dict("ds_p_", student.params))
+    save("train", **out)
+    print("ph0 loss", out["ph0_loss"], "distill", losses)
+
+
 def gen_ckpt():
     """A checkpoint written by the reference's io.save_checkpoint (io.py:150-175):
     (2,3,4) lattice, seed 9, density bias 5, with a 8^3 occupancy bitmap."""
@@ -354,7 +441,7 @@ def gen_ckpt():
 
 
 def main():
-    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt", "extract"]
+    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt", "extract", "train"]
     for w in what:
         t = time.time()
         globals()[f"gen_{w}"]()

@@ -1,0 +1,175 @@
+"""Training kernels on the device against the reference.
+
+Fixtures: tests/golden/train.npz, written by the reference itself
+(tests/golden/make_golden.py gen_train): batched.grouped_backward on random
+upstream gradients (32- and 64-wide lattices), train.photometric_loss_and_grads
+on the reference test's fixed batch (plain / L2-regularised / density noise),
+two adam_update steps, and one distill_step.
+
+Tolerances (float32 throughout; numpy's sgemm and pairwise sums associate
+differently from the device's fixed-order sums):
+* gradients: |got - ref| <= 2e-4 * max|ref| + 1e-4 * |ref|, per layer;
+* losses: relative 1e-5;
+* Adam on the reference's own gradients: bit-exact (elementwise float32 in
+  numpy's operation order);
+* one distill step: parameters within 2e-6 absolute (lr = 5e-4 moves each by
+  at most ~lr).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, have_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs CUDA")]
+
+LAYERS = ("trunk0", "trunk1", "density", "feature", "direction", "color")
+
+
+def _gf():
+    import paper_2103_13744_b200 as gf
+
+    return gf
+
+
+def _close(got, ref, what, rel=1e-4, scale=2e-4):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    tol = scale * max(float(np.abs(ref).max()), 1e-30) + rel * np.abs(ref)
+    err = np.abs(got - ref)
+    assert np.all(err <= tol), f"{what}: max err {err.max():.3e}, max |ref| {np.abs(ref).max():.3e}"
+
+
+def _check_grads(grads, z, prefix):
+    for name in LAYERS:
+        _close(grads.weights[name], z[f"{prefix}w_{name}"], f"{prefix}w_{name}")
+        _close(grads.biases[name], z[f"{prefix}b_{name}"], f"{prefix}b_{name}")
+
+
+@pytest.mark.parametrize("tag,width", [("g32", 32), ("g64", 64)])
+def test_grouped_backward_matches_reference(tag, width):
+    gf = _gf()
+    z = golden("train")
+    aabb = gf.Aabb((0.0,) * 3, (1.0,) * 3)
+    arch = None if width == 32 else gf.MlpArchitecture(hidden_width=64)
+    g = gf.init_network_grid(aabb, tuple(z[f"{tag}_res"]), seed=11, arch=arch)
+    flat = z[f"{tag}_biases"]
+    o = 0
+    for k in g.params.biases:
+        n = g.params.biases[k].size
+        g.params.biases[k][...] = flat[o : o + n].reshape(g.params.biases[k].shape)
+        o += n
+    pts, dirs = z[f"{tag}_pts"], z[f"{tag}_dirs"]
+    layout = gf.group_by_network(gf.QueryBatch(pts, dirs, g.cell_index(pts)), g.n_cells)
+    caches = []
+    gf.grouped_forward(g, layout, caches=caches)
+    grads = gf.batched.grouped_backward(g, layout, caches, z[f"{tag}_dcol"], z[f"{tag}_dsig"])
+    _check_grads(grads, z, f"{tag}_")
+
+
+def _photo_setup(gf, z):
+    from paper_2103_13744_b200 import train
+
+    aabb = gf.Aabb((0.0,) * 3, (1.0,) * 3)
+    g = gf.init_network_grid(aabb, (2, 2, 2), seed=5)
+    g.params.biases["density"][:] = 1.5
+    smp = train.RaySamples(z["ph_pos"], z["ph_dirs"], z["ph_ray"], z["ph_slot"], z["ph_deltas"], int(z["ph_nrays"]),
+                           int(z["ph_k"]))
+    return train, g, smp
+
+
+@pytest.mark.parametrize("tag", ["ph0", "ph_reg", "ph_noise"])
+def test_photometric_loss_and_grads_match_reference(tag):
+    gf = _gf()
+    z = golden("train")
+    train, g, smp = _photo_setup(gf, z)
+    kw = {"ph_reg": {"reg_weight": 1e-3}, "ph_noise": {"sigma_noise": z["ph_noise"]}}.get(tag, {})
+    loss, grads = train.photometric_loss_and_grads(g, smp, z["ph_gt"], (1.0, 1.0, 1.0), **kw)
+    assert abs(loss - float(z[f"{tag}_loss"])) <= 1e-5 * abs(float(z[f"{tag}_loss"]))
+    _check_grads(grads, z, f"{tag}_")
+    loss2, none = train.photometric_loss_and_grads(g, smp, z["ph_gt"], (1.0, 1.0, 1.0), want_grads=False, **kw)
+    assert none is None and loss2 == loss
+
+
+def test_adam_update_bit_exact_on_reference_gradients():
+    gf = _gf()
+    z = golden("train")
+    train, g, _ = _photo_setup(gf, z)
+    grads = gf.mlp.MlpParams(g.arch, {k: z[f"ph0_w_{k}"] for k in LAYERS}, {k: z[f"ph0_b_{k}"] for k in LAYERS})
+    st = train.AdamState.for_params(g.params)
+    p = g.params.copy()
+    cfg = train.TrainConfig()
+    train.adam_update(p, grads, st, 5e-4, cfg)
+    train.adam_update(p, grads, st, 3e-4, cfg)
+    for name in LAYERS:
+        for pre, obj in (("adam_p_", p), ("adam_m_", st.m), ("adam_v_", st.v)):
+            assert np.array_equal(obj.weights[name], z[f"{pre}w_{name}"]), (pre, name)
+            assert np.array_equal(obj.biases[name], z[f"{pre}b_{name}"]), (pre, name)
+
+
+def test_distill_step_matches_reference():
+    gf = _gf()
+    from paper_2103_13744_b200 import train
+
+    z = golden("train")
+    aabb = gf.Aabb((0.0,) * 3, (1.0,) * 3)
+    enc = gf.PositionalEncoding()
+    cfg = train.TrainConfig(distill_points_per_cell=8, teacher_hidden_layers=4, teacher_hidden_width=32,
+                            teacher_direction_width=32, teacher_skip_layer=None)
+    teacher = gf.init_network_grid(aabb, (1, 1, 1), seed=6, arch=cfg.teacher_architecture(enc), encoding=enc)
+    student = gf.init_network_grid(aabb, (2, 2, 2), seed=7)
+    st = train.AdamState.for_params(student.params)
+    loss = train.distill_step(student, teacher, cfg, st, np.random.default_rng(3), delta_ref=0.01)
+    assert abs(loss - float(z["ds_loss"][0])) <= 1e-5 * float(z["ds_loss"][0])
+    for name in LAYERS:
+        assert np.abs(student.params.weights[name] - z[f"ds_p_w_{name}"]).max() <= 2e-6, name
+        assert np.abs(student.params.biases[name] - z[f"ds_p_b_{name}"]).max() <= 2e-6, name
+
+
+def test_reference_training_semantics():
+    """test_train.py: zero model -> loss 0 on background ground truth; the
+    regulariser alone; gradients only reach cells that were sampled; the
+    device path is deterministic."""
+    gf = _gf()
+    from paper_2103_13744_b200 import train
+
+    z = golden("train")
+    _, g, smp = _photo_setup(gf, z)
+    for k in g.params.weights:
+        g.params.weights[k][:] = 0
+        g.params.biases[k][:] = 0
+    gt = np.ones((int(z["ph_nrays"]), 3), np.float32)
+    loss, grads = train.photometric_loss_and_grads(g, smp, gt, (1.0, 1.0, 1.0))
+    assert loss == 0.0
+    g.params.weights["color"][:] = 0.01
+    reg, _ = train.regularization_term(g.params, 1e-6)
+    loss2, _ = train.photometric_loss_and_grads(g, smp, gt, (1.0, 1.0, 1.0), reg_weight=1e-6)
+    assert loss2 == pytest.approx(reg)
+    # gradients land only in sampled cells
+    _, g2, smp2 = _photo_setup(gf, z)
+    cells = set(np.unique(g2.cell_index(smp2.positions)).tolist())
+    _, gr = train.photometric_loss_and_grads(g2, smp2, z["ph_gt"], (1.0, 1.0, 1.0))
+    for c in range(g2.n_cells):
+        if c not in cells:
+            assert not np.any(gr.weights["trunk0"][c])
+    _, gr2 = train.photometric_loss_and_grads(g2, smp2, z["ph_gt"], (1.0, 1.0, 1.0))
+    for name in LAYERS:
+        assert np.array_equal(gr.weights[name], gr2.weights[name])
+
+
+def test_overfit_fixed_batch_loss_drops():
+    """test_train.py:123-135 on the device path."""
+    gf = _gf()
+    from paper_2103_13744_b200 import train
+
+    z = golden("train")
+    _, g, smp = _photo_setup(gf, z)
+    state = train.AdamState.for_params(g.params)
+    cfg = train.TrainConfig()
+    losses = []
+    for _ in range(50):
+        loss, grads = train.photometric_loss_and_grads(g, smp, z["ph_gt"], (1, 1, 1))
+        train.adam_update(g.params, grads, state, 5e-4, cfg)
+        losses.append(loss)
+    assert losses[-1] < losses[0]
+    for i in range(0, 40, 10):
+        assert losses[i + 10] < losses[i]
