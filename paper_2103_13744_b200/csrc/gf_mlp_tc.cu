@@ -391,7 +391,10 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
     if (L == 3) { b = wb + T::B3; bb = wb + T::BB3; K = T::K3; idesc = idesc_f16(128, T::N3); }
     if (L == 4) { b = wb + T::B4; bb = wb + T::BB4; K = T::K4; idesc = idesc_f16(128, T::N4); }
     mma_f16(d, umma_desc(wb + T::ONES, 16), umma_desc(bb, 16), idesc, 0u);
-    for (int ks = 0; ks < K / 16; ++ks) mma_f16(d, umma_desc(a + ks * 256, K), umma_desc(b + ks * 256, K), idesc, 1u);
+    // a K step of 16 columns is 256 B further in both operands: +16 in the
+    // descriptors' start-address field (>> 4), no carry out of 14 bits
+    const uint64_t da = umma_desc(a, K), db = umma_desc(b, K);
+    for (int ks = 0; ks < K / 16; ++ks) mma_f16(d, da + (uint64_t)(ks * 16), db + (uint64_t)(ks * 16), idesc, 1u);
     mma_commit(bar0 + 8 * g);
   };
   auto wait_mma = [&]() {
