@@ -307,6 +307,67 @@ def measure_extract(gf, torch, aabb, occ, reps=5):
                     "bitmap D2H; the reference takes 6.7 s on 8 host cores for the same bitmap"}
 
 
+def measure_train(gf, torch, aabb, occ, cam, reps=3, cpu=True):
+    """one photometric training step at the reference's default
+    batch (TrainConfig(): 8192 pixels of one 800x800 view, k_train=384, ESS on
+    the toy occupancy, 16^3 random-init lattice): device time of the kernels
+    (group + forward + loss + backward) by CUDA events, the step through the
+    public API (photometric_loss_and_grads + adam_update, numpy parameters in
+    and out as the reference's API requires), and the numpy oracle of the
+    reference's math on the same batch (one host thread)."""
+    from paper_2103_13744_b200 import train
+    from paper_2103_13744_b200.batched import grouped_backward_device, grouped_forward_device
+
+    grid = gf.init_network_grid(aabb, (16, 16, 16), seed=0)
+    cfg = train.TrainConfig()
+    o, d = gf.render.generate_rays(cam)
+    rng = np.random.default_rng(0)
+    pix = rng.choice(len(o), size=cfg.batch_size_pixels, replace=False)
+    smp = train.prepare_ray_samples(o[pix], d[pix], aabb, cfg.k_train, True, rng, occ=occ)
+    gt = rng.random((len(pix), 3)).astype(np.float32)
+    q = len(smp.positions)
+    state = train.AdamState.for_params(grid.params)
+    train.photometric_loss_and_grads(grid, smp, gt, cfg.background)  # warm-up (packing, workspaces)
+    # kernels only: grouped forward + backward on device-resident rows
+    layout = gf.group_by_network(gf.QueryBatch(smp.positions, smp.directions, grid.cell_index(smp.positions)),
+                                 grid.n_cells)
+    dc = torch.full((q, 3), 1e-3, device="cuda")
+    ds = torch.full((q,), 1e-3, device="cuda")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(reps):
+        cache = grouped_forward_device(grid, layout)
+    ev[1].record()
+    for _ in range(reps):
+        grouped_backward_device(grid, layout, cache, dc, ds)
+    ev[2].record()
+    torch.cuda.synchronize()
+    fwd_ms, bwd_ms = ev[0].elapsed_time(ev[1]) / reps, ev[1].elapsed_time(ev[2]) / reps
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        loss, grads = train.photometric_loss_and_grads(grid, smp, gt, cfg.background)
+        train.adam_update(grid.params, grads, state, cfg.learning_rate, cfg)
+    api_ms = (time.perf_counter() - t0) / reps * 1e3
+    flop = 3 * 12392 * q  # forward + backward data + parameter gradients, count_flops units
+    out = {"samples": q, "rays": len(pix), "k_train": cfg.k_train, "forward_kernel_ms": fwd_ms,
+           "backward_kernel_ms": bwd_ms, "backward_tflops": flop * 2 / 3 / (bwd_ms * 1e-3) / 1e12,
+           "api_step_ms": api_ms, "loss": loss,
+           "note": "api_step_ms = photometric_loss_and_grads + adam_update with host numpy parameters "
+                   "(101.8 MB of gradients and 3 parameter-sized arrays cross PCIe each step)"}
+    if cpu:
+        from oracle import gridfield_oracle as O
+        from oracle import train_oracle as T
+
+        lat = O.lattice_from_grid(grid)
+        t0 = time.perf_counter()
+        T.photometric_loss_and_grads(lat, smp.positions, smp.directions, smp.ray_index, smp.slot, smp.deltas,
+                                     smp.n_rays, smp.k, gt, cfg.background)
+        out["cpu_oracle_s"] = time.perf_counter() - t0
+        out["cpu_note"] = "numpy oracle of train.photometric_loss_and_grads on the same batch, 1 host thread"
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -487,9 +548,10 @@ def main():
         e2e["views"] = {"n": len(vt), "median_ms_per_frame": statistics.median(vt) * 1e3,
                         "max_ms_per_frame": max(vt) * 1e3}
 
-    extract = None
+    extract = train_step = None
     if args.workload == "c2" and rank == 0:
         extract = measure_extract(gf, torch, aabb, occ)
+        train_step = measure_train(gf, torch, aabb, occ, cam, cpu=world == 1 and not args.no_cpu_baseline)
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -512,7 +574,7 @@ def main():
             "gpu_launches": int(launches),
             "queries_per_frame": queries, "mlp_samples_per_s": queries / (st_ms["mlp"] * 1e-3) if st_ms["mlp"] else None,
             "stage_roofline": stage_roof, "paper_1080ti_mpix_s_context": PAPER_1080TI_MPIX_S,
-            "occupancy_extract": extract,
+            "occupancy_extract": extract, "training_step": train_step,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -252,10 +252,11 @@ GF_API int gf_extract_occupancy_network(const gf_arch_t* arch, const gf_grid_geo
  * identity).  packed_dev is the GF_PRECISION_FP32 packing.  gw[l] / gb[l]
  * receive layer l's gradients in the reference layout (n_cells, out, in) /
  * (n_cells, out), manifest order; cells without rows get zeros.         */
+GF_API size_t gf_grouped_backward_workspace_bytes(const gf_arch_t* arch, int64_t n_cells, int64_t n);
 GF_API int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* packed_dev, const float* pos_dev,
                                const float* dir_dev, int64_t n, const int64_t* offsets_dev, const int64_t* order_dev,
                                const float* d_color_dev, const float* d_sigma_dev, float* const* gw_dev,
-                               float* const* gb_dev, void* stream);
+                               float* const* gb_dev, void* ws_dev, size_t ws_bytes, void* stream);
 /* train.photometric_loss_and_grads compositing (train.py:243-288): queries
  * (ray_index, slot) of B rays x k slots with colours and densities (noise:
  * optional density perturbation, train.py:245-249), per-ray deltas, ground

@@ -147,9 +147,11 @@ def grouped_backward_device(grid, layout: GroupedLayout, cache: GroupedCache, d_
     gb = [D.empty((grid.n_cells, s.out_dim), t.float32) for s in specs]
     wp = (N.C.c_void_p * len(gw))(*[x.data_ptr() for x in gw])
     bp = (N.C.c_void_p * len(gb))(*[x.data_ptr() for x in gb])
-    N.check(N.lib().gf_grouped_backward(grid.native_arch(), grid.n_cells, N.ptr(cache.packed), N.ptr(cache.pos),
-                                        N.ptr(cache.dirs), n, N.ptr(cache.offsets), N.ptr(cache.order), N.ptr(dc),
-                                        N.ptr(ds), wp, bp, D.stream_handle()), "grouped_backward")
+    arch = grid.native_arch()
+    ws = D.workspace(N.lib().gf_grouped_backward_workspace_bytes(arch, grid.n_cells, n))
+    N.check(N.lib().gf_grouped_backward(arch, grid.n_cells, N.ptr(cache.packed), N.ptr(cache.pos), N.ptr(cache.dirs),
+                                        n, N.ptr(cache.offsets), N.ptr(cache.order), N.ptr(dc), N.ptr(ds), wp, bp,
+                                        N.ptr(ws), ws.numel(), D.stream_handle()), "grouped_backward")
     return gw, gb
 
 

@@ -851,12 +851,20 @@ int gf_extract_occupancy_network(const gf_arch_t* arch, const gf_grid_geom_t* ne
 // ---------------------------------------------------------------------------
 // training: batched.py:154-187, train.py:130-160, 212-288
 // ---------------------------------------------------------------------------
+size_t gf_grouped_backward_workspace_bytes(const gf_arch_t* arch, int64_t n_cells, int64_t n) {
+  LayerTable t;
+  if (!arch || !make_layer_table(arch, &t) || n_cells < 1 || n < 0) return 0;
+  return bwd_workspace(t, n_cells, n);
+}
+
 int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* packed, const float* pos, const float* dir,
                         int64_t n, const int64_t* offsets, const int64_t* order, const float* d_color,
-                        const float* d_sigma, float* const* gw, float* const* gb, void* stream) {
+                        const float* d_sigma, float* const* gw, float* const* gb, void* ws, size_t ws_bytes,
+                        void* stream) {
   LayerTable t;
   if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_grouped_backward: bad architecture");
   if (n_cells < 1 || n < 0 || !gw || !gb) return fail(GF_ERR_INVALID, "gf_grouped_backward: bad sizes");
+  if (bwd_workspace(t, n_cells, n) > ws_bytes) return fail(GF_ERR_WORKSPACE, "gf_grouped_backward: workspace too small");
   BwdArgs A;
   memset(&A, 0, sizeof(A));
   A.pos = pos;
@@ -869,7 +877,7 @@ int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* pack
     A.gw[l] = gw[l];
     A.gb[l] = gb[l];
   }
-  if (!launch_grouped_backward(t, (const float*)packed, A, n_cells, (cudaStream_t)stream))
+  if (!launch_grouped_backward(t, (const float*)packed, A, n_cells, n, ws, (cudaStream_t)stream))
     return fail(GF_ERR_UNSUPPORTED, "gf_grouped_backward: no backward kernel for this architecture");
   return check_cuda("gf_grouped_backward");
 }

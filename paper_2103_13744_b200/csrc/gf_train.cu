@@ -20,10 +20,14 @@
 namespace gf {
 
 // ---------------------------------------------------------------------------
-// grouped backward: one CTA per cell, TR rows per tile, one thread per row in
-// phase A (forward recompute + backward data in fp32, activations and deltas
-// stored to shared memory), all threads in phase B (each owns a fixed set of
-// parameters and sums dz[o] * in[i] over the tile's rows in row order).
+// grouped backward: one CTA per cell, TR rows per tile.  Phase A: four lanes
+// per row (a row's lanes are adjacent in one warp and sync with __syncwarp)
+// recompute the fp32 forward and run the backward data pass, each lane owning
+// a quarter of every layer's outputs (or, for the transposed products, of the
+// inputs); activations and deltas go to shared memory.  Phase B: every thread
+// owns a fixed set of parameters and sums dz[o] * in[i] over the tile's rows
+// in row order.  Each value is produced by one thread in a fixed order, so
+// the result is deterministic.
 // ---------------------------------------------------------------------------
 template <int W>
 struct BwdShape {
@@ -40,9 +44,13 @@ struct BwdShape {
   static constexpr int DZF = DZS + 1;     // dz feature          W
   static constexpr int DZD = DZF + W;     // dz direction        W
   static constexpr int DZC = DZD + W;     // dz color            3
-  static constexpr int END = DZC + 3;
+  static constexpr int SIG = DZC + 3;     // sigma               1
+  static constexpr int ZC = SIG + 1;      // color logits        3
+  static constexpr int END = ZC + 3;
   static constexpr int LD = END | 1;      // odd row stride: conflict-free per-row access
-  static constexpr int TR = W == 32 ? 64 : 32;  // rows per tile (smem: TR * LD floats + weights)
+  static constexpr int LANES = 4;         // threads per row in phase A
+  static constexpr int TR = 32;           // rows per tile
+  static constexpr int THREADS = TR * LANES;
   static constexpr int N_LAYERS = 6;
   // manifest order (mlp.py:73-84): trunk0, trunk1, density, feature, direction, color
   __host__ __device__ static constexpr int in_dim(int l) { return l == 0 ? P : (l == 4 ? W + D : W); }
@@ -57,12 +65,17 @@ struct BwdShape {
   static constexpr int TOTAL = count(0) + count(1) + count(2) + count(3) + count(4) + count(5);
 };
 
-// out[o] = (relu)(sum_i in[i] * W[o][i] + b[o]); input vector in registers
-template <int IN, int INP, int OUT, bool RELU>
-__device__ __forceinline__ void dense_row(const float* __restrict__ w, const float* __restrict__ b, const float* in,
-                                          float* out_row) {
-#pragma unroll 4
-  for (int o = 0; o < OUT; ++o) {
+// outputs [o0, o0 + NO) of relu?(W in + b) for one row; input vector read
+// from shared memory into registers once
+template <int IN, int INP, int NO, bool RELU>
+__device__ __forceinline__ void dense_part(const float* __restrict__ w, const float* __restrict__ b,
+                                           const float* in_s, int o0, float* out_s) {
+  float in[IN];
+#pragma unroll
+  for (int i = 0; i < IN; ++i) in[i] = in_s[i];
+#pragma unroll 2
+  for (int oo = 0; oo < NO; ++oo) {
+    const int o = o0 + oo;
     const float4* wr = reinterpret_cast<const float4*>(w + o * INP);
     float acc = 0.f;
 #pragma unroll
@@ -74,150 +87,240 @@ __device__ __forceinline__ void dense_row(const float* __restrict__ w, const flo
       if (4 * i4 + 3 < IN) acc = fmaf(in[4 * i4 + 3], q.w, acc);
     }
     const float z = __fadd_rn(acc, b[o]);
-    out_row[o] = RELU ? fmaxf(z, 0.f) : z;
+    out_s[o] = RELU ? fmaxf(z, 0.f) : z;
   }
 }
 
-// dx[i] = sum_o dz[o] * W[o][i]  (matmul(dz, W), mlp.py:294-297)
+// dx[i] = sum_o dz[o] * W[o][i] for i in [i0, i0 + NI)  (matmul(dz, W), mlp.py:294-297)
 template <int NI, int INP, int OUT>
-__device__ __forceinline__ void dense_t_row(const float* __restrict__ w, const float* dz, float* dx) {
+__device__ __forceinline__ void dense_t_part(const float* __restrict__ w, const float* dz_s, int i0, float* dx) {
 #pragma unroll
   for (int i = 0; i < NI; ++i) dx[i] = 0.f;
-#pragma unroll 2
+#pragma unroll 4
   for (int o = 0; o < OUT; ++o) {
-    const float g = dz[o];
-    const float* wr = w + o * INP;
+    const float g = dz_s[o];
+    const float* wr = w + o * INP + i0;
 #pragma unroll
     for (int i = 0; i < NI; ++i) dx[i] = fmaf(g, wr[i], dx[i]);
   }
 }
 
+// work plan: every cell's rows split into chunks of GF_BWD_CHUNK rows (one CTA
+// each, so a crowded cell does not serialise the kernel); chunk k's partial
+// sums land in scratch row k and k_bwd_reduce adds a cell's chunks in order
+#define GF_BWD_CHUNK 256
+
+__global__ void __launch_bounds__(1024) k_bwd_plan(const int64_t* __restrict__ offsets, int64_t n_cells, uint2* chunks,
+                                                   uint32_t* chunk_off, uint32_t* n_chunks) {
+  __shared__ uint32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t per = (n_cells + 1023) / 1024, c0 = (int64_t)tid * per;
+  uint32_t local = 0;
+  for (int64_t c = c0; c < c0 + per && c < n_cells; ++c)
+    local += (uint32_t)((offsets[c + 1] - offsets[c] + GF_BWD_CHUNK - 1) / GF_BWD_CHUNK);
+  uint32_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    wsum[lane] = t;
+  }
+  __syncthreads();
+  uint32_t base = (wid ? wsum[wid - 1] : 0u) + x - local;
+  for (int64_t c = c0; c < c0 + per && c < n_cells; ++c) {
+    chunk_off[c] = base;
+    const uint32_t nch = (uint32_t)((offsets[c + 1] - offsets[c] + GF_BWD_CHUNK - 1) / GF_BWD_CHUNK);
+    for (uint32_t j = 0; j < nch; ++j) chunks[base + j] = make_uint2((uint32_t)c, j);
+    base += nch;
+  }
+  if (tid == 1023) {
+    chunk_off[n_cells] = base;
+    *n_chunks = base;
+  }
+}
+
+// chunk sums -> reference-layout gradients; cells without rows get zeros
 template <int W>
-__global__ void __launch_bounds__(BwdShape<W>::TR) k_grouped_backward(const float* __restrict__ packed, Fp32Layout L,
-                                                                      BwdArgs A) {
+__global__ void __launch_bounds__(256) k_bwd_reduce(const float* __restrict__ scratch,
+                                                    const uint32_t* __restrict__ chunk_off, int64_t n_cells,
+                                                    BwdArgs A) {
   using S = BwdShape<W>;
-  constexpr int P = S::P, D = S::D, TR = S::TR, LD = S::LD;
+  const int64_t n = n_cells * S::TOTAL;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = e / S::TOTAL;
+    const int p = (int)(e % S::TOTAL);
+    float acc = 0.f;
+    const uint32_t k0 = chunk_off[cell], k1 = chunk_off[cell + 1];
+    for (uint32_t k = k0; k < k1; ++k) acc = k == k0 ? scratch[(size_t)k * S::TOTAL + p]
+                                                    : __fadd_rn(acc, scratch[(size_t)k * S::TOTAL + p]);
+    int l = 0, qq = p;
+    while (qq >= S::count(l)) qq -= S::count(l++);
+    const int in = S::in_dim(l), out = S::out_dim(l);
+    if (qq >= out * in) A.gb[l][cell * out + (qq - out * in)] = acc;
+    else A.gw[l][(cell * out + qq / in) * in + qq % in] = acc;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const float* __restrict__ packed,
+                                                                           Fp32Layout L, BwdArgs A,
+                                                                           const uint2* __restrict__ chunks,
+                                                                           const uint32_t* __restrict__ n_chunks,
+                                                                           float* scratch) {
+  using S = BwdShape<W>;
+  constexpr int P = S::P, D = S::D, TR = S::TR, LD = S::LD, NT = S::THREADS, Q = W / S::LANES;
   constexpr int PP = (P + 3) & ~3, WP = (W + 3) & ~3, DP = (W + D + 3) & ~3;
   extern __shared__ float4 smem4[];
   float* sw = reinterpret_cast<float*>(smem4);
   float* srow = sw + L.cell_floats;  // TR rows x LD floats
-  const int64_t cell = blockIdx.x;
+  if (blockIdx.x >= *n_chunks) return;
+  const uint2 ch = chunks[blockIdx.x];
+  const int64_t cell = ch.x;
   const int tid = threadIdx.x;
+  const int r = tid / S::LANES, q = tid % S::LANES;  // row of the tile, lane within the row
   {
     const float4* src = reinterpret_cast<const float4*>(packed + (size_t)cell * L.cell_floats);
-    for (int j = tid; j < L.cell_floats / 4; j += TR) smem4[j] = __ldg(src + j);
+    for (int j = tid; j < L.cell_floats / 4; j += NT) smem4[j] = __ldg(src + j);
   }
-  const int64_t r0 = A.offsets[cell], r1 = A.offsets[cell + 1];
-  const int64_t rows = r1 - r0;
-  const int n_tiles = rows > 0 ? (int)((rows + TR - 1) / TR) : 1;
+  const int64_t r0 = A.offsets[cell] + (int64_t)ch.y * GF_BWD_CHUNK;
+  const int64_t r1 = min(A.offsets[cell + 1], r0 + (int64_t)GF_BWD_CHUNK);
+  const int n_tiles = (int)((r1 - r0 + TR - 1) / TR);  // >= 1: chunks hold rows
+  float* part = scratch + (size_t)blockIdx.x * S::TOTAL;
   for (int t = 0; t < n_tiles; ++t) {
     const int64_t first = r0 + (int64_t)t * TR;
     const int n_in = (int)(r1 - first < (int64_t)TR ? r1 - first : (int64_t)TR);  // <= 0 for an empty cell
     __syncthreads();
-    if (tid < n_in) {
-      float* s = srow + tid * LD;
-      const int64_t row = first + tid;
-      const int64_t src = A.order ? A.order[row] : row;  // upstream gradients arrive in query order
+    // ---------------- phase A (every lane reaches every __syncwarp)
+    const bool on = r < n_in;
+    float* s = srow + r * LD;
+    const int64_t row = first + r;
+    const int64_t src = on ? (A.order ? A.order[row] : row) : 0;  // upstream gradients arrive in query order
+    if (on) {
+      // gamma(x): lane q encodes octaves q, q+4, q+8; gamma(d): octave q (core.py:132-152)
       float x[3], d[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         x[a] = A.pos[3 * row + a];
         d[a] = A.dir[3 * row + a];
       }
-      // ---- forward (mlp.py:238-266), activations to shared memory
-      float xe[P];
-      encode_f32<10>(x, xe);
+      if (q == 0) {
 #pragma unroll
-      for (int i = 0; i < P; ++i) s[S::X + i] = xe[i];
-      dense_row<P, PP, W, true>(sw + L.w_off[0], sw + L.b_off[0], xe, s + S::H0);
-      float hv[W];
-#pragma unroll
-      for (int i = 0; i < W; ++i) hv[i] = s[S::H0 + i];
-      dense_row<W, WP, W, true>(sw + L.w_off[1], sw + L.b_off[1], hv, s + S::H1);
-#pragma unroll
-      for (int i = 0; i < W; ++i) hv[i] = s[S::H1 + i];
-      float sig;
-      dense_row<W, WP, 1, true>(sw + L.w_off[2], sw + L.b_off[2], hv, &sig);
-      dense_row<W, WP, W, false>(sw + L.w_off[3], sw + L.b_off[3], hv, s + S::CAT);
-      {
-        float de[D];
-        encode_f32<4>(d, de);
-#pragma unroll
-        for (int i = 0; i < D; ++i) s[S::CAT + W + i] = de[i];
-      }
-      {
-        float cat[W + D];
-#pragma unroll
-        for (int i = 0; i < W + D; ++i) cat[i] = s[S::CAT + i];
-        dense_row<W + D, DP, W, true>(sw + L.w_off[4], sw + L.b_off[4], cat, s + S::G);
-      }
-      float gv[W];
-#pragma unroll
-      for (int i = 0; i < W; ++i) gv[i] = s[S::G + i];
-      float z[3];
-      dense_row<W, WP, 3, false>(sw + L.w_off[5], sw + L.b_off[5], gv, z);
-      // ---- backward (mlp.py:291-316)
-      float dzc[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float col = sigmoid_split(z[c]);
-        dzc[c] = __fmul_rn(__fmul_rn(A.d_color[3 * src + c], col), __fsub_rn(1.0f, col));
-        s[S::DZC + c] = dzc[c];
-      }
-      float dv[W];
-      dense_t_row<W, WP, 3>(sw + L.w_off[5], dzc, dv);  // dg
-#pragma unroll
-      for (int i = 0; i < W; ++i) {
-        dv[i] = gv[i] > 0.f ? dv[i] : 0.f;  // dz_dir = dg * (g > 0)
-        s[S::DZD + i] = dv[i];
-      }
-      float dfeat[W];
-      dense_t_row<W, DP, W>(sw + L.w_off[4], dv, dfeat);  // first W columns of d_dir_in
-#pragma unroll
-      for (int i = 0; i < W; ++i) s[S::DZF + i] = dfeat[i];
-      const float dzs = sig > 0.f ? A.d_sigma[src] : 0.f;  // d_sigma * (sigma > 0)
-      s[S::DZS] = dzs;
-      float dh[W];
-      dense_t_row<W, WP, W>(sw + L.w_off[3], dfeat, dh);
-      {
-        const float* wd = sw + L.w_off[2];
-#pragma unroll
-        for (int i = 0; i < W; ++i) {
-          dh[i] = __fadd_rn(dh[i], __fmul_rn(dzs, wd[i]));  // dh + matmul(dz_density, W_density)
-          dh[i] = s[S::H1 + i] > 0.f ? dh[i] : 0.f;         // dz trunk1
-          s[S::DZ1 + i] = dh[i];
+        for (int a = 0; a < 3; ++a) {
+          s[S::X + a] = x[a];
+          s[S::CAT + W + a] = d[a];
         }
       }
-      float dh0[W];
-      dense_t_row<W, WP, W>(sw + L.w_off[1], dh, dh0);
+      for (int k = q; k < 10; k += S::LANES) {
+        const float f = __int_as_float(0x40490FDB + (k << 23));  // fl32(pi) * 2^k == fl32(2^k pi)
 #pragma unroll
-      for (int i = 0; i < W; ++i) s[S::DZ0 + i] = s[S::H0 + i] > 0.f ? dh0[i] : 0.f;
+        for (int a = 0; a < 3; ++a) {
+          float sv, cv;
+          sincosf(__fmul_rn(x[a], f), &sv, &cv);
+          s[S::X + 3 + 6 * k + a] = sv;
+          s[S::X + 6 + 6 * k + a] = cv;
+        }
+      }
+      {
+        const int k = q;  // 4 direction octaves, one per lane
+        const float f = __int_as_float(0x40490FDB + (k << 23));
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          float sv, cv;
+          sincosf(__fmul_rn(d[a], f), &sv, &cv);
+          s[S::CAT + W + 3 + 6 * k + a] = sv;
+          s[S::CAT + W + 6 + 6 * k + a] = cv;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- forward (mlp.py:238-266)
+    if (on) dense_part<P, PP, Q, true>(sw + L.w_off[0], sw + L.b_off[0], s + S::X, q * Q, s + S::H0);
+    __syncwarp();
+    if (on) dense_part<W, WP, Q, true>(sw + L.w_off[1], sw + L.b_off[1], s + S::H0, q * Q, s + S::H1);
+    __syncwarp();
+    if (on) {
+      dense_part<W, WP, Q, false>(sw + L.w_off[3], sw + L.b_off[3], s + S::H1, q * Q, s + S::CAT);  // feature
+      if (q == 0) dense_part<W, WP, 1, true>(sw + L.w_off[2], sw + L.b_off[2], s + S::H1, 0, s + S::SIG);
+    }
+    __syncwarp();
+    if (on) dense_part<W + D, DP, Q, true>(sw + L.w_off[4], sw + L.b_off[4], s + S::CAT, q * Q, s + S::G);
+    __syncwarp();
+    // ---- backward (mlp.py:291-316)
+    if (on && q < 3) {
+      dense_part<W, WP, 1, false>(sw + L.w_off[5], sw + L.b_off[5], s + S::G, q, s + S::ZC);  // logit q
+      const float col = sigmoid_split(s[S::ZC + q]);
+      s[S::DZC + q] = __fmul_rn(__fmul_rn(A.d_color[3 * src + q], col), __fsub_rn(1.0f, col));
+    }
+    if (on && q == 3) s[S::DZS] = s[S::SIG] > 0.f ? A.d_sigma[src] : 0.f;  // d_sigma * (sigma > 0)
+    __syncwarp();
+    if (on) {  // dz_dir = (dz_color W_color) * (g > 0)
+      float dv[Q];
+      dense_t_part<Q, WP, 3>(sw + L.w_off[5], s + S::DZC, q * Q, dv);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) s[S::DZD + q * Q + i] = s[S::G + q * Q + i] > 0.f ? dv[i] : 0.f;
+    }
+    __syncwarp();
+    if (on) {  // dfeat = first W columns of dz_dir W_direction
+      float dv[Q];
+      dense_t_part<Q, DP, W>(sw + L.w_off[4], s + S::DZD, q * Q, dv);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) s[S::DZF + q * Q + i] = dv[i];
+    }
+    __syncwarp();
+    if (on) {  // dz trunk1 = (dfeat W_feature + dz_density W_density) * (h1 > 0)
+      float dv[Q];
+      dense_t_part<Q, WP, W>(sw + L.w_off[3], s + S::DZF, q * Q, dv);
+      const float dzs = s[S::DZS];
+      const float* wd = sw + L.w_off[2] + q * Q;
+#pragma unroll
+      for (int i = 0; i < Q; ++i) {
+        const float h = __fadd_rn(dv[i], __fmul_rn(dzs, wd[i]));
+        s[S::DZ1 + q * Q + i] = s[S::H1 + q * Q + i] > 0.f ? h : 0.f;
+      }
+    }
+    __syncwarp();
+    if (on) {  // dz trunk0 = (dz1 W_trunk1) * (h0 > 0)
+      float dv[Q];
+      dense_t_part<Q, WP, W>(sw + L.w_off[1], s + S::DZ1, q * Q, dv);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) s[S::DZ0 + q * Q + i] = s[S::H0 + q * Q + i] > 0.f ? dv[i] : 0.f;
     }
     __syncthreads();
-    // ---- phase B: parameter sums over this tile's rows (gw = dz^T in, gb = sum dz)
-    for (int p = tid; p < S::TOTAL; p += TR) {
-      int l = 0, q = p;
-      while (q >= S::count(l)) q -= S::count(l++);
+    // ---------------- phase B: parameter sums over this tile's rows (gw = dz^T in, gb = sum dz)
+    for (int p = tid; p < S::TOTAL; p += NT) {
+      int l = 0, qq = p;
+      while (qq >= S::count(l)) qq -= S::count(l++);
       const int in = S::in_dim(l), out = S::out_dim(l);
-      const bool bias = q >= out * in;
-      const int o = bias ? q - out * in : q / in, i = bias ? 0 : q % in;
+      const bool bias = qq >= out * in;
+      const int o = bias ? qq - out * in : qq / in, i = bias ? 0 : qq % in;
       const float* dzp = srow + S::dz_off(l) + o;
       const float* inp = srow + S::in_off(l) + i;
       float acc = 0.f;
       if (bias) {
-        for (int r = 0; r < n_in; ++r) acc = __fadd_rn(acc, dzp[r * LD]);
+        for (int rr = 0; rr < n_in; ++rr) acc = __fadd_rn(acc, dzp[rr * LD]);
       } else {
-        for (int r = 0; r < n_in; ++r) acc = fmaf(dzp[r * LD], inp[r * LD], acc);
+        for (int rr = 0; rr < n_in; ++rr) acc = fmaf(dzp[rr * LD], inp[rr * LD], acc);
       }
-      float* dst = bias ? A.gb[l] + cell * out + o : A.gw[l] + (cell * out + o) * in + i;
-      *dst = t == 0 ? acc : __fadd_rn(*dst, acc);
+      part[p] = t == 0 ? acc : __fadd_rn(part[p], acc);
     }
   }
 }
 
+int64_t bwd_max_chunks(int64_t n_cells, int64_t n);
+
 template <int W>
-static bool launch_bwd_width(const float* packed, const Fp32Layout& L, const BwdArgs& A, int64_t n_cells,
-                             cudaStream_t st) {
+static bool launch_bwd_width(const float* packed, const Fp32Layout& L, const BwdArgs& A, int64_t n_cells, int64_t n,
+                             void* ws, cudaStream_t st) {
   using S = BwdShape<W>;
   const size_t smem = (size_t)L.cell_floats * 4 + (size_t)S::TR * S::LD * 4;
   static thread_local size_t set = 0;
@@ -227,16 +330,41 @@ static bool launch_bwd_width(const float* packed, const Fp32Layout& L, const Bwd
       return false;
     set = smem;
   }
-  if (n_cells > 0) k_grouped_backward<W><<<(unsigned)n_cells, S::TR, smem, st>>>(packed, L, A);
+  if (n_cells <= 0) return true;
+  const int64_t max_chunks = bwd_max_chunks(n_cells, n);
+  char* p = (char*)ws;
+  uint2* chunks = (uint2*)p;
+  p += gf_align((size_t)max_chunks * 8);
+  uint32_t* chunk_off = (uint32_t*)p;
+  p += gf_align((size_t)(n_cells + 1) * 4);
+  uint32_t* n_chunks = (uint32_t*)p;
+  p += gf_align(4);
+  float* scratch = (float*)p;
+  k_bwd_plan<<<1, 1024, 0, st>>>(A.offsets, n_cells, chunks, chunk_off, n_chunks);
+  if (max_chunks > 0)
+    k_grouped_backward<W><<<(unsigned)max_chunks, S::THREADS, smem, st>>>(packed, L, A, chunks, n_chunks, scratch);
+  const int64_t elems = n_cells * S::TOTAL;
+  k_bwd_reduce<W><<<(unsigned)std::min<int64_t>(gf_div_up<int64_t>(elems, 256), (int64_t)num_sms() * 16), 256, 0, st>>>(
+      scratch, chunk_off, n_cells, A);
   return true;
 }
 
-bool launch_grouped_backward(const LayerTable& t, const float* packed, const BwdArgs& A, int64_t n_cells,
-                             cudaStream_t st) {
+int64_t bwd_max_chunks(int64_t n_cells, int64_t n) { return n / GF_BWD_CHUNK + std::min<int64_t>(n_cells, n) + 1; }
+
+size_t bwd_workspace(const LayerTable& t, int64_t n_cells, int64_t n) {
+  if (!prepare_mlp_fp32(t)) return 0;
+  const int total = t.width == 32 ? BwdShape<32>::TOTAL : BwdShape<64>::TOTAL;
+  const int64_t mc = bwd_max_chunks(n_cells, n);
+  return gf_align((size_t)mc * 8) + gf_align((size_t)(n_cells + 1) * 4) + gf_align(4) +
+         gf_align((size_t)mc * total * 4);
+}
+
+bool launch_grouped_backward(const LayerTable& t, const float* packed, const BwdArgs& A, int64_t n_cells, int64_t n,
+                             void* ws, cudaStream_t st) {
   if (!prepare_mlp_fp32(t)) return false;
   const Fp32Layout L = make_fp32_layout(t);
-  return t.width == 32 ? launch_bwd_width<32>(packed, L, A, n_cells, st)
-                       : launch_bwd_width<64>(packed, L, A, n_cells, st);
+  return t.width == 32 ? launch_bwd_width<32>(packed, L, A, n_cells, n, ws, st)
+                       : launch_bwd_width<64>(packed, L, A, n_cells, n, ws, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -48,8 +48,9 @@ struct DistillArgs {
   float* d_sigma;           // (n,) out
 };
 
-bool launch_grouped_backward(const LayerTable& t, const float* packed, const BwdArgs& A, int64_t n_cells,
-                             cudaStream_t st);
+size_t bwd_workspace(const LayerTable& t, int64_t n_cells, int64_t n);
+bool launch_grouped_backward(const LayerTable& t, const float* packed, const BwdArgs& A, int64_t n_cells, int64_t n,
+                             void* ws, cudaStream_t st);
 size_t photo_workspace(int64_t n_rays, int k, int64_t n_queries);
 void launch_photometric(const PhotoArgs& A, void* ws, double* loss_sum, cudaStream_t st);
 void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, const AdamCoef& c, cudaStream_t st);
