@@ -54,6 +54,17 @@ def to_device(a, dtype) -> "object":
     return t.from_numpy(arr).to(device=device(), dtype=dtype, non_blocking=False).contiguous()
 
 
+def to_host(x) -> np.ndarray:
+    """Device tensor -> numpy array through page-locked memory (one DMA at
+    full PCIe rate; torch's caching host allocator recycles the buffers).  The
+    returned array views the pinned buffer and keeps it alive."""
+    t = require_cuda()
+    h = t.empty(tuple(x.shape), dtype=x.dtype, pin_memory=True)
+    h.copy_(x, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    return h.numpy()
+
+
 def empty(shape, dtype):
     t = require_cuda()
     return t.empty(shape, dtype=dtype, device=device())

@@ -143,8 +143,16 @@ def grouped_backward_device(grid, layout: GroupedLayout, cache: GroupedCache, d_
     if dc.shape[0] != n or ds.shape[0] != n:
         raise ValueError("upstream gradients do not match the layout's query count")
     specs = grid.arch.layers()
-    gw = [D.empty((grid.n_cells, s.out_dim, s.in_dim), t.float32) for s in specs]
-    gb = [D.empty((grid.n_cells, s.out_dim), t.float32) for s in specs]
+    # one flat buffer in MlpParams.arrays() order (w, b per layer): the views
+    # below are the per-layer outputs, the buffer feeds the optimizer directly
+    nc = grid.n_cells
+    flat = D.empty((nc * sum(s.out_dim * s.in_dim + s.out_dim for s in specs),), t.float32)
+    gw, gb, off = [], [], 0
+    for s in specs:
+        gw.append(flat[off : off + nc * s.out_dim * s.in_dim].view(nc, s.out_dim, s.in_dim))
+        off += nc * s.out_dim * s.in_dim
+        gb.append(flat[off : off + nc * s.out_dim].view(nc, s.out_dim))
+        off += nc * s.out_dim
     wp = (N.C.c_void_p * len(gw))(*[x.data_ptr() for x in gw])
     bp = (N.C.c_void_p * len(gb))(*[x.data_ptr() for x in gb])
     arch = grid.native_arch()
@@ -152,7 +160,7 @@ def grouped_backward_device(grid, layout: GroupedLayout, cache: GroupedCache, d_
     N.check(N.lib().gf_grouped_backward(arch, grid.n_cells, N.ptr(cache.packed), N.ptr(cache.pos), N.ptr(cache.dirs),
                                         n, N.ptr(cache.offsets), N.ptr(cache.order), N.ptr(dc), N.ptr(ds), wp, bp,
                                         N.ptr(ws), ws.numel(), D.stream_handle()), "grouped_backward")
-    return gw, gb
+    return gw, gb, flat
 
 
 def grouped_backward(grid, layout: GroupedLayout, caches: list, d_color, d_sigma):
@@ -165,7 +173,7 @@ def grouped_backward(grid, layout: GroupedLayout, caches: list, d_color, d_sigma
 
     if not caches or not isinstance(caches[-1], GroupedCache):
         raise ValueError("grouped_backward needs the caches list filled by grouped_forward")
-    gw, gb = grouped_backward_device(grid, layout, caches[-1], d_color, d_sigma)
+    gw, gb, _ = grouped_backward_device(grid, layout, caches[-1], d_color, d_sigma)
     specs = grid.arch.layers()
     dtype = grid.params.dtype
     return mlp.MlpParams(grid.arch, {s.name: w.cpu().numpy().astype(dtype, copy=False) for s, w in zip(specs, gw)},

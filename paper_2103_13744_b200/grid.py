@@ -89,7 +89,19 @@ class NetworkGrid:
                 raise N.NativeError(f"architecture {self.arch} has no {p} device layout")
             packed = D.workspace(nbytes)
             flat = getattr(self, "_payload", None)
-            if flat is not None and flat[0] == fp:
+            dev = getattr(self.params, "_dev_flat", None)
+            if dev is not None and dev[0] == fp:
+                # the optimizer's device copy of exactly these host arrays
+                # (train.adam_update): pack from it, no upload
+                ptrs, off, base, item = [], 0, dev[1].data_ptr(), dev[1].element_size()
+                for _, a in self.params.arrays():
+                    ptrs.append(base + off * item)
+                    off += a.size
+                wp = (N.C.c_void_p * (len(ptrs) // 2))(*ptrs[0::2])
+                bp = (N.C.c_void_p * (len(ptrs) // 2))(*ptrs[1::2])
+                N.check(N.lib().gf_pack_weights(arch, self.n_cells, wp, bp, N.ptr(packed), N.PRECISION[p],
+                                                D.stream_handle()), "pack weights (device copy)")
+            elif flat is not None and flat[0] == fp:
                 # loaded from a checkpoint and unmodified since: one copy of the
                 # file's payload, packed on the device (io.load_checkpoint)
                 f_dev = D.to_device(flat[1], t.float32)

@@ -95,17 +95,60 @@ def lr_schedule(step: int, base_lr: float, horizon: int, final_fraction: float =
     return float(base_lr * final_fraction ** (step / horizon))
 
 
-@dataclass
 class AdamState:
-    """train.py:119-127."""
+    """train.py:119-127.  The moments live on the device between steps
+    (flat float32, MlpParams.arrays() order); ``m`` / ``v`` read them back
+    into the host containers on access."""
 
-    m: mlp.MlpParams
-    v: mlp.MlpParams
-    step: int = 0
+    def __init__(self, m: mlp.MlpParams, v: mlp.MlpParams, step: int = 0):
+        self._m, self._v = m, v
+        self.step = step
+        self._dev = None  # (m_flat, v_flat) on the device once adam_update ran
 
     @classmethod
     def for_params(cls, params: mlp.MlpParams) -> "AdamState":
         return cls(m=mlp.map_params(np.zeros_like, params), v=mlp.map_params(np.zeros_like, params))
+
+    def _sync(self):
+        if self._dev is not None:
+            _scatter_flat(D.to_host(self._dev[0]), self._m)
+            _scatter_flat(D.to_host(self._dev[1]), self._v)
+
+    @property
+    def m(self) -> mlp.MlpParams:
+        self._sync()
+        return self._m
+
+    @property
+    def v(self) -> mlp.MlpParams:
+        self._sync()
+        return self._v
+
+
+def _flat_size(params: mlp.MlpParams) -> int:
+    return sum(int(a.size) for _, a in params.arrays())
+
+
+def _scatter_flat(flat: np.ndarray, params: mlp.MlpParams):
+    off = 0
+    for _, a in params.arrays():
+        a[...] = flat[off : off + a.size].reshape(a.shape)
+        off += a.size
+
+
+def device_flat(params: mlp.MlpParams):
+    """Flat float32 device copy of ``params`` (arrays() order): the cached one
+    when the host arrays are unchanged since it was made, else an upload."""
+    hit = getattr(params, "_dev_flat", None)
+    if hit is not None and hit[0] == params.fingerprint():
+        return hit[1]
+    t = D.require_cuda()
+    flat = D.empty((_flat_size(params),), t.float32)
+    off = 0
+    for _, a in params.arrays():
+        flat[off : off + a.size].copy_(t.from_numpy(np.ascontiguousarray(a, dtype=np.float32).reshape(-1)))
+        off += a.size
+    return flat
 
 
 def _f32(x) -> float:
@@ -119,23 +162,26 @@ def _require_f32(params: mlp.MlpParams):
 
 
 def adam_update(params: mlp.MlpParams, grads: mlp.MlpParams, state: AdamState, lr: float, cfg: TrainConfig):
-    """train.py:130-143: one Adam step, in place, on the device (gf_adam_update
-    per parameter array, float32 in numpy's operation order)."""
+    """train.py:130-143: one Adam step, in place.  One gf_adam_update launch
+    over the flat parameter vector (float32, numpy's operation order); the
+    moments stay on the device, gradients from this package's device passes
+    are used without re-upload, and the updated parameters are written back
+    into the host arrays (the reference API) with their device copy kept for
+    the next forward pass."""
     _require_f32(params)
-    t = D.require_cuda()
     state.step += 1
     b1, b2, eps = cfg.adam_beta1, cfg.adam_beta2, cfg.adam_eps
     bc1 = 1.0 - b1**state.step
     bc2 = 1.0 - b2**state.step
     coef = (N.C.c_float * 8)(*[_f32(v) for v in (b1, 1.0 - b1, b2, 1.0 - b2, bc1, bc2, lr, eps)])
-    for (_, p), (_, g), (_, m), (_, v) in zip(params.arrays(), grads.arrays(), state.m.arrays(), state.v.arrays()):
-        pd, gd = D.to_device(p, t.float32), D.to_device(g, t.float32)
-        md, vd = D.to_device(m, t.float32), D.to_device(v, t.float32)
-        N.check(N.lib().gf_adam_update(N.ptr(pd), N.ptr(gd), N.ptr(md), N.ptr(vd), pd.numel(), coef,
-                                       D.stream_handle()), "adam_update")
-        p[...] = pd.cpu().numpy().reshape(p.shape)
-        m[...] = md.cpu().numpy().reshape(m.shape)
-        v[...] = vd.cpu().numpy().reshape(v.shape)
+    if state._dev is None:
+        state._dev = (device_flat(state._m).clone(), device_flat(state._v).clone())
+    p = device_flat(params)
+    g = device_flat(grads)
+    N.check(N.lib().gf_adam_update(N.ptr(p), N.ptr(g), N.ptr(state._dev[0]), N.ptr(state._dev[1]), p.numel(), coef,
+                                   D.stream_handle()), "adam_update")
+    _scatter_flat(D.to_host(p), params)
+    params._dev_flat = (params.fingerprint(), p)
 
 
 def _sum_squares(x_dev) -> "object":
@@ -214,10 +260,20 @@ def prepare_ray_samples(origins, directions, aabb: Aabb, k: int, stratified: boo
                       ray_index=ray_index, slot=slot, deltas=seg, n_rays=n, k=k)
 
 
-def _grads_to_host(grid, gw, gb) -> mlp.MlpParams:
+def _grads_to_host(grid, gw, gb, flat) -> mlp.MlpParams:
+    """Host MlpParams of the gradients (one download); the device buffer rides
+    along for adam_update while the host arrays stay unmodified."""
     specs = grid.arch.layers()
-    return mlp.MlpParams(grid.arch, {s.name: w.cpu().numpy() for s, w in zip(specs, gw)},
-                         {s.name: b.cpu().numpy() for s, b in zip(specs, gb)})
+    host = D.to_host(flat)  # the gradient arrays view this pinned buffer
+    w, b, off = {}, {}, 0
+    for s, gwl, gbl in zip(specs, gw, gb):
+        w[s.name] = host[off : off + gwl.numel()].reshape(tuple(gwl.shape))
+        off += gwl.numel()
+        b[s.name] = host[off : off + gbl.numel()].reshape(tuple(gbl.shape))
+        off += gbl.numel()
+    out = mlp.MlpParams(grid.arch, w, b)
+    out._dev_flat = (out.fingerprint(), flat)
+    return out
 
 
 def photometric_loss_and_grads(model, samples: RaySamples, gt: np.ndarray, background, reg_weight: float = 0.0,
@@ -252,14 +308,14 @@ def photometric_loss_and_grads(model, samples: RaySamples, gt: np.ndarray, backg
         loss += reg_value
     if not want_grads:
         return loss, None
-    gw, gb = grouped_backward_device(model, layout, cache, dcq, dsq)
+    gw, gb, flat = grouped_backward_device(model, layout, cache, dcq, dsq)
     if reg_dev is not None:
         names = [s.name for s in model.arch.layers()]
         for name, (w, bias) in reg_dev.items():
             li = names.index(name)
             _axpy(w, gw[li], 2.0 * reg_weight, gw[li])  # g + (2 * weight) * w
             _axpy(bias, gb[li], 2.0 * reg_weight, gb[li])
-    return loss, _grads_to_host(model, gw, gb)
+    return loss, _grads_to_host(model, gw, gb, flat)
 
 
 def _unit_sphere(rng, shape) -> np.ndarray:
@@ -303,8 +359,8 @@ def distill_step(student, teacher, cfg: TrainConfig, state: AdamState, rng, delt
                                     N.ptr(sums), N.ptr(ws), ws.numel(), D.stream_handle()), "distill_loss")
     s_a, s_c = sums.cpu().numpy()
     loss = float(w_a * s_a + s_c) / m
-    gw, gb = grouped_backward_device(student, layout, cache, dc, ds)
-    grads = _grads_to_host(student, gw, gb)
+    gw, gb, flat = grouped_backward_device(student, layout, cache, dc, ds)
+    grads = _grads_to_host(student, gw, gb, flat)
     lr = lr_schedule(state.step, cfg.learning_rate, cfg.distill_steps, cfg.lr_final_fraction)
     adam_update(student.params, grads, state, lr, cfg)
     return loss
