@@ -287,6 +287,24 @@ GF_API int gf_distill_loss(int64_t n, const float* s_color_dev, const float* s_s
                            const float* t_sigma_dev, float delta, float c_sigma, float c_color, float* d_color_dev,
                            float* d_sigma_dev, double* sums_dev, void* ws_dev, size_t ws_bytes, void* stream);
 
+/* train.prepare_ray_samples (train.py:175-209): n float32 rays, k slots,
+ * box = {b_min[3], b_max[3]}, the caller Generator's PCG64 state pcg =
+ * {state_hi, state_lo, inc_hi, inc_lo} with its buffered half (has_uint32,
+ * uinteger) -- only read when stratified.  _count writes per-ray kept counts
+ * turned into exclusive offsets (offsets_dev[n] = Q); _write fills deltas
+ * (n,), float64 positions (Q,3), float32 directions (Q,3), ray_index and
+ * slot (Q,) in np.nonzero order.  The caller advances its Generator by n*k
+ * float32 draws afterwards.                                               */
+GF_API int gf_prepare_samples_count(const float* origins_dev, const float* dirs_dev, int64_t n, int32_t k,
+                                    int32_t stratified, const double* box, const uint64_t* pcg, int32_t has_uint32,
+                                    uint32_t uinteger, const gf_grid_geom_t* occ, const uint8_t* occ_bits_dev,
+                                    int64_t* offsets_dev, void* stream);
+GF_API int gf_prepare_samples_write(const float* origins_dev, const float* dirs_dev, int64_t n, int32_t k,
+                                    int32_t stratified, const double* box, const uint64_t* pcg, int32_t has_uint32,
+                                    uint32_t uinteger, const gf_grid_geom_t* occ, const uint8_t* occ_bits_dev,
+                                    const int64_t* offsets_dev, float* deltas_dev, double* pos_dev, float* dirs_out_dev,
+                                    int64_t* ray_index_dev, int64_t* slot_dev, void* stream);
+
 /* --- instrumentation ------------------------------------------------------
  * Stage timing: while enabled, gf_render_rays / gf_query_points record CUDA
  * events on their stream between stages; gf_stage_times() synchronises and

@@ -117,6 +117,12 @@ _SIGS = {
     "gf_distill_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "gf_distill_loss": (C.c_int, [C.c_int64, _P, _P, _P, _P, C.c_float, C.c_float, C.c_float, _P, _P, _P, _P,
                                   C.c_size_t, _P]),
+    "gf_prepare_samples_count": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_uint64), C.c_int32, C.c_uint32, C.POINTER(GridGeom), _P, _P,
+                                           _P]),
+    "gf_prepare_samples_write": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                           C.POINTER(C.c_uint64), C.c_int32, C.c_uint32, C.POINTER(GridGeom), _P, _P,
+                                           _P, _P, _P, _P, _P, _P]),
     "gf_stage_timing": (C.c_int, [C.c_int32]),
     "gf_stage_times": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "gf_launch_count": (C.c_int64, []),

@@ -12,6 +12,7 @@
 #include "gf_analytic.cuh"
 #include "gf_extract.cuh"
 #include "gf_train.cuh"
+#include "gf_samples.cuh"
 #include "gf_march.cuh"
 #include "gf_mlp.cuh"
 
@@ -946,6 +947,60 @@ int gf_distill_loss(int64_t n, const float* s_color, const float* s_sigma, const
   DistillArgs A{n, s_color, s_sigma, t_color, t_sigma, delta, c_sigma, c_color, d_color, d_sigma};
   launch_distill(A, (double*)ws, sums, (cudaStream_t)stream);
   return check_cuda("gf_distill_loss");
+}
+
+static bool prep_args(const float* o, const float* d, int64_t n, int32_t k, int32_t stratified, const double* box,
+                      const uint64_t* pcg, int32_t has_uint32, uint32_t uinteger, const gf_grid_geom_t* occ,
+                      const uint8_t* occ_bits, int64_t* offsets, PrepArgs* A) {
+  if (n < 0 || k < 1 || !box || !offsets || (n > 0 && (!o || !d)) || (stratified && !pcg) || (occ_bits && !valid_grid(occ)))
+    return false;
+  memset(A, 0, sizeof(*A));
+  A->origins = o;
+  A->dirs = d;
+  A->n = n;
+  A->k = k;
+  A->stratified = stratified ? 1 : 0;
+  for (int a = 0; a < 3; ++a) {
+    A->b_min[a] = box[a];
+    A->b_max[a] = box[3 + a];
+  }
+  if (stratified) {
+    A->state = ((u128)pcg[0] << 64) | pcg[1];
+    A->inc = ((u128)pcg[2] << 64) | pcg[3];
+  }
+  A->has_uint32 = has_uint32 ? 1 : 0;
+  A->uinteger = uinteger;
+  if (occ_bits) A->occ = gf_make_grid(occ);
+  A->occ_bits = occ_bits;
+  A->offsets = offsets;
+  return true;
+}
+
+int gf_prepare_samples_count(const float* o, const float* d, int64_t n, int32_t k, int32_t stratified, const double* box,
+                             const uint64_t* pcg, int32_t has_uint32, uint32_t uinteger, const gf_grid_geom_t* occ,
+                             const uint8_t* occ_bits, int64_t* offsets, void* stream) {
+  PrepArgs A;
+  if (!prep_args(o, d, n, k, stratified, box, pcg, has_uint32, uinteger, occ, occ_bits, offsets, &A))
+    return fail(GF_ERR_INVALID, "gf_prepare_samples_count: bad arguments");
+  launch_prepare_count(A, (cudaStream_t)stream);
+  return check_cuda("gf_prepare_samples_count");
+}
+
+int gf_prepare_samples_write(const float* o, const float* d, int64_t n, int32_t k, int32_t stratified, const double* box,
+                             const uint64_t* pcg, int32_t has_uint32, uint32_t uinteger, const gf_grid_geom_t* occ,
+                             const uint8_t* occ_bits, const int64_t* offsets, float* deltas, double* pos,
+                             float* dir_out, int64_t* ray_index, int64_t* slot, void* stream) {
+  PrepArgs A;
+  if (!prep_args(o, d, n, k, stratified, box, pcg, has_uint32, uinteger, occ, occ_bits, (int64_t*)offsets, &A) ||
+      !deltas)
+    return fail(GF_ERR_INVALID, "gf_prepare_samples_write: bad arguments");
+  A.deltas = deltas;
+  A.pos = pos;
+  A.dir_out = dir_out;
+  A.ray_index = ray_index;
+  A.slot = slot;
+  launch_prepare_write(A, (cudaStream_t)stream);
+  return check_cuda("gf_prepare_samples_write");
 }
 
 // ---------------------------------------------------------------------------

@@ -15,8 +15,9 @@ What runs where:
   (train.py:146-160): one kernel per parameter array (gf_adam_update,
   gf_sum_squares, gf_axpy).  Parameters stay numpy arrays in place, as the
   reference API requires; each step uploads them and writes them back.
-* ``prepare_ray_samples`` (train.py:175-209): numpy sample placement with the
-  caller's Generator, with the occupancy test and the clip on the device.
+* ``prepare_ray_samples`` (train.py:175-209): on the device; the caller's
+  numpy Generator stream (PCG64) is reproduced there and the Generator is
+  advanced exactly as rng.random((n, k), float32) would.
 * ``density_probe`` (train.py:577-586): recognised by ``extract_occupancy``,
   which then runs the probe lattice on the device in one call.
 
@@ -37,7 +38,6 @@ from . import _native as N
 from . import mlp
 from .batched import GroupedLayout, QueryBatch, group_by_network, grouped_backward_device, grouped_forward_device
 from .core import Aabb, clip_into
-from .render import intersect_aabb
 
 REGULARIZED_LAYERS = ("direction", "color")  # train.py:33
 
@@ -240,24 +240,84 @@ class RaySamples:
     k: int
 
 
+_M64 = (1 << 64) - 1
+
+
+def _xsl_rr(state: int) -> int:
+    """PCG64's output function (numpy pcg64.h pcg_output_xsl_rr_128_64)."""
+    x = ((state >> 64) ^ state) & _M64
+    rot = state >> 122
+    return ((x >> rot) | (x << ((64 - rot) & 63))) & _M64
+
+
+def _pcg_state(rng):
+    bg = getattr(rng, "bit_generator", None)
+    if bg is None or type(bg).__name__ != "PCG64":
+        raise N.NativeError("prepare_ray_samples reproduces numpy's PCG64 Generator stream on the device; "
+                            f"got {type(bg).__name__ if bg is not None else type(rng).__name__}")
+    st = bg.state
+    return bg, st
+
+
+def _advance_float32_draws(bg, st, draws: int):
+    """Leave the Generator exactly where rng.random((n, k), float32) would:
+    each float32 takes one 32-bit half of a 64-bit output, low half first,
+    after the buffered half if there is one (numpy pcg64_next32)."""
+    if draws <= 0:
+        return
+    rem = draws - (1 if st["has_uint32"] else 0)
+    words = (rem + 1) // 2
+    if words:
+        bg.advance(words)  # also clears the buffered half
+    new = bg.state
+    if rem % 2:
+        new["has_uint32"], new["uinteger"] = 1, _xsl_rr(new["state"]["state"]) >> 32
+    else:
+        new["has_uint32"], new["uinteger"] = 0, 0
+    bg.state = new
+
+
 def prepare_ray_samples(origins, directions, aabb: Aabb, k: int, stratified: bool, rng, occ=None) -> RaySamples:
-    """train.py:175-209: stratified equidistant samples, ESS-filtered.  The
-    jitter comes from the caller's Generator (same draws as the reference);
-    the clip and the occupancy test run on the device."""
-    n = len(origins)
-    t0, t1 = intersect_aabb(origins, directions, aabb)
-    hit = t1 > t0
-    seg = np.where(hit, (t1 - t0) / k, 0.0).astype(np.float32)
-    jitter = rng.random((n, k), dtype=np.float32) if stratified else np.full((n, k), 0.5, np.float32)
-    ts = t0[:, None].astype(np.float32) + (np.arange(k)[None, :] + jitter) * seg[:, None]
-    pts = origins[:, None, :].astype(np.float32) + ts[..., None] * directions[:, None, :].astype(np.float32)
-    pts = clip_into(pts, aabb)
-    keep = np.repeat(hit[:, None], k, axis=1)
+    """train.py:175-209 on the device (gf_prepare_samples_*): slab test,
+    stratified jitter from the caller's Generator (its PCG64 stream is
+    reproduced on the device and the Generator is advanced by the same n*k
+    draws), float64 sample positions clamped into the box, the occupancy
+    test, and np.nonzero's ordering.  Rays are float32 (generate_rays)."""
+    t = D.require_cuda()
+    o_h, d_h = np.asarray(origins), np.asarray(directions)
+    if o_h.dtype != np.float32 or d_h.dtype != np.float32:
+        raise N.NativeError("the device sample preparation takes float32 rays (as generate_rays returns)")
+    n = len(o_h)
+    o = D.to_device(o_h.reshape(-1, 3), t.float32)
+    d = D.to_device(d_h.reshape(-1, 3), t.float32)
+    box = (N.C.c_double * 6)(*[float(v) for v in aabb.b_min], *[float(v) for v in aabb.b_max])
+    pcg = (N.C.c_uint64 * 4)()
+    has, uint = 0, 0
+    if stratified:
+        bg, st = _pcg_state(rng)
+        s, inc = st["state"]["state"], st["state"]["inc"]
+        pcg[0], pcg[1], pcg[2], pcg[3] = s >> 64, s & _M64, inc >> 64, inc & _M64
+        has, uint = int(st["has_uint32"]), int(st["uinteger"])
+    geom, bits = None, None
     if occ is not None:
-        keep &= occ.occupied_at(pts.reshape(-1, 3)).reshape(n, k)
-    ray_index, slot = np.nonzero(keep)
-    return RaySamples(positions=pts[ray_index, slot], directions=np.asarray(directions, dtype=np.float32)[ray_index],
-                      ray_index=ray_index, slot=slot, deltas=seg, n_rays=n, k=k)
+        if np.any(aabb.b_min < occ.aabb.b_min) or np.any(aabb.b_max > occ.aabb.b_max):
+            raise N.NativeError("sample box must lie inside the occupancy grid's box")
+        geom, bits = occ.native_geom(), occ.device_bits()
+    offs = D.empty((n + 1,), t.int64)
+    args = (N.ptr(o), N.ptr(d), n, int(k), int(bool(stratified)), box, pcg, has, uint, geom, N.ptr(bits))
+    N.check(N.lib().gf_prepare_samples_count(*args, N.ptr(offs), D.stream_handle()), "prepare_ray_samples")
+    q = int(offs[n].item()) if n else 0
+    deltas = D.empty((n,), t.float32)
+    pos = D.empty((q, 3), t.float64)
+    dirs = D.empty((q, 3), t.float32)
+    ri = D.empty((q,), t.int64)
+    sl = D.empty((q,), t.int64)
+    N.check(N.lib().gf_prepare_samples_write(*args, N.ptr(offs), N.ptr(deltas), N.ptr(pos), N.ptr(dirs), N.ptr(ri),
+                                             N.ptr(sl), D.stream_handle()), "prepare_ray_samples")
+    if stratified:
+        _advance_float32_draws(bg, st, n * int(k))
+    return RaySamples(positions=D.to_host(pos), directions=D.to_host(dirs), ray_index=D.to_host(ri),
+                      slot=D.to_host(sl), deltas=D.to_host(deltas), n_rays=n, k=int(k))
 
 
 def _grads_to_host(grid, gw, gb, flat) -> mlp.MlpParams:

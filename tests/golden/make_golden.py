@@ -423,6 +423,23 @@ def gen_train():
     losses = [train.distill_step(student, teacher, dcfg, st, np.random.default_rng(3), delta_ref=0.01)]
     out["ds_loss"] = np.array(losses)
     out.update(_grads_dict("ds_p_", student.params))
+    # prepare_ray_samples: occupancy-filtered, a Generator holding a buffered
+    # half (odd number of float32 draws before), and non-stratified
+    occ4 = occupancy.OccupancyGrid.from_bool_array(aabb, (4, 1, 1), np.array([False, False, False, True]))
+    for tag, pre, strat, occ_ in (("prep_occ", 0, True, occ4), ("prep_odd", 3, True, None), ("prep_mid", 0, False, None)):
+        rng = np.random.default_rng(17)
+        if pre:
+            rng.random(pre, dtype=np.float32)
+        n_r, k_ = 24, 40
+        origins = np.tile(np.array([[-2.0, 0.0, 0.0]], np.float32), (n_r, 1))
+        offs = rng.uniform(-0.6, 0.6, (n_r, 2)).astype(np.float32)
+        dirs = np.concatenate([np.zeros((n_r, 1), np.float32), offs], axis=1) - origins
+        dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+        smp = train.prepare_ray_samples(origins, dirs, aabb, k_, strat, rng, occ=occ_)
+        after = rng.random(5, dtype=np.float32)  # pins the Generator state left behind
+        out.update({f"{tag}_o": origins, f"{tag}_d": dirs, f"{tag}_pos": smp.positions, f"{tag}_dirs": smp.directions,
+                    f"{tag}_ray": smp.ray_index, f"{tag}_slot": smp.slot, f"{tag}_deltas": smp.deltas,
+                    f"{tag}_after": after, f"{tag}_k": np.int64(k_), f"{tag}_pre": np.int64(pre)})
     save("train", **out)
     print("ph0 loss", out["ph0_loss"], "distill", losses)
 

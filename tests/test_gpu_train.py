@@ -173,3 +173,40 @@ def test_overfit_fixed_batch_loss_drops():
     assert losses[-1] < losses[0]
     for i in range(0, 40, 10):
         assert losses[i + 10] < losses[i]
+
+
+@pytest.mark.parametrize("tag", ["ph", "prep_occ", "prep_odd", "prep_mid"])
+def test_prepare_ray_samples_bit_exact(tag):
+    """train.prepare_ray_samples on the device: samples, order, deltas and the
+    Generator state left behind are the reference's exactly."""
+    gf = _gf()
+    from paper_2103_13744_b200 import train
+
+    z = golden("train")
+    aabb = gf.Aabb((0.0,) * 3, (1.0,) * 3)
+    if tag == "ph":  # test_train.py fixed_batch: rng draws the ray offsets, the jitter, then gt
+        rng = np.random.default_rng(1)
+        n = int(z["ph_nrays"])
+        origins = np.tile(np.array([[-2.0, 0.0, 0.0]], np.float32), (n, 1))
+        offs = rng.uniform(-0.6, 0.6, (n, 2)).astype(np.float32)
+        dirs = np.concatenate([np.zeros((n, 1), np.float32), offs], axis=1) - origins
+        dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+        smp = train.prepare_ray_samples(origins, dirs, aabb, int(z["ph_k"]), True, rng)
+        assert np.array_equal(rng.random((n, 3)).astype(np.float32), z["ph_gt"])
+        ref = dict(pos=z["ph_pos"], dirs=z["ph_dirs"], ray=z["ph_ray"], slot=z["ph_slot"], deltas=z["ph_deltas"])
+    else:
+        rng = np.random.default_rng(17)
+        if int(z[f"{tag}_pre"]):
+            rng.random(int(z[f"{tag}_pre"]), dtype=np.float32)
+        rng.uniform(-0.6, 0.6, (len(z[f"{tag}_o"]), 2))  # the offsets the fixture drew
+        occ = None
+        if tag == "prep_occ":
+            occ = gf.OccupancyGrid.from_bool_array(aabb, (4, 1, 1), np.array([False, False, False, True]))
+        smp = train.prepare_ray_samples(z[f"{tag}_o"], z[f"{tag}_d"], aabb, int(z[f"{tag}_k"]), tag != "prep_mid",
+                                        rng, occ=occ)
+        assert np.array_equal(rng.random(5, dtype=np.float32), z[f"{tag}_after"])
+        ref = {key: z[f"{tag}_{key}"] for key in ("pos", "dirs", "ray", "slot", "deltas")}
+    assert smp.positions.dtype == np.float64 and np.array_equal(smp.positions, ref["pos"])
+    assert np.array_equal(smp.directions, ref["dirs"])
+    assert np.array_equal(smp.ray_index, ref["ray"]) and np.array_equal(smp.slot, ref["slot"])
+    assert np.array_equal(smp.deltas, ref["deltas"])
