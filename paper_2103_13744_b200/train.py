@@ -21,10 +21,13 @@ What runs where:
 * ``density_probe`` (train.py:577-586): recognised by ``extract_occupancy``,
   which then runs the probe lattice on the device in one call.
 
-The device path computes in float32, the reference's parameter dtype; float64
-parameter stacks are rejected.  The data loaders, the pipeline driver, and the
-CLI reporting (``photometric_step``, ``run_pipeline`` and the rest) are out of
-scope.
+``photometric_step``, ``train_photometric_loop``, ``run_distill_loop``,
+``evaluate_psnr`` and ``mean_free_space_density`` are the reference's drivers
+over these device steps (any dataset object with the reference dataset's
+``indices`` / ``cameras`` / ``images`` / ``aabb`` works).  The device path
+computes in float32, the reference's parameter dtype; float64 parameter stacks
+are rejected.  Dataset generation, the pipeline driver (``run_pipeline``) and
+CLI reporting are out of scope.
 """
 
 from __future__ import annotations
@@ -424,6 +427,83 @@ def distill_step(student, teacher, cfg: TrainConfig, state: AdamState, rng, delt
     lr = lr_schedule(state.step, cfg.learning_rate, cfg.distill_steps, cfg.lr_final_fraction)
     adam_update(student.params, grads, state, lr, cfg)
     return loss
+
+
+def photometric_step(model, dataset, cfg: TrainConfig, state: AdamState, rng, occ=None, apply_reg: bool = False,
+                     lr: float | None = None, train_indices: list | None = None, noise_std: float = 0.0) -> float:
+    """train.py:291-332: one training image and pixel batch (the caller's
+    Generator draws the view, the pixels, the jitter and the density noise in
+    the reference's order), device rays / samples / loss / gradients / Adam.
+    ``dataset`` is any object with the reference dataset's ``indices(split)``,
+    ``cameras``, ``images`` and ``aabb``."""
+    from .render import generate_rays
+
+    idx = train_indices if train_indices is not None else dataset.indices("train")
+    view = int(rng.choice(np.asarray(idx)))
+    cam = dataset.cameras[view]
+    n_px = cam.width * cam.height
+    bsz = min(cfg.batch_size_pixels, n_px)
+    pixels = rng.choice(n_px, size=bsz, replace=bsz > n_px)
+    origins, dirs = generate_rays(cam)
+    gt = dataset.images[view].reshape(-1, 3)[pixels]
+    samples = prepare_ray_samples(origins[pixels], dirs[pixels], dataset.aabb, cfg.k_train, True, rng, occ=occ)
+    noise = None
+    if noise_std > 0.0:
+        noise = rng.normal(0.0, noise_std, size=len(samples.positions)).astype(np.float32)
+    loss, grads = photometric_loss_and_grads(model, samples, gt, cfg.background,
+                                             reg_weight=cfg.l2_reg_weight if apply_reg else 0.0, sigma_noise=noise)
+    adam_update(model.params, grads, state, cfg.learning_rate if lr is None else lr, cfg)
+    return loss
+
+
+def train_photometric_loop(model, dataset, cfg: TrainConfig, steps: int, rng, occ, apply_reg: bool, stage: str,
+                           curve: list | None = None, noise_std: float = 0.0) -> None:
+    """train.py:418-441: ``steps`` photometric updates with a fresh optimizer."""
+    state = AdamState.for_params(model.params)
+    for step in range(steps):
+        lr = lr_schedule(step, cfg.learning_rate, steps, cfg.lr_final_fraction)
+        loss = photometric_step(model, dataset, cfg, state, rng, occ=occ, apply_reg=apply_reg, lr=lr,
+                                noise_std=noise_std)
+        if curve is not None and (step % cfg.log_every == 0 or step == steps - 1):
+            curve.append({"stage": stage, "step": step, "loss": loss})
+
+
+def run_distill_loop(student, teacher, cfg: TrainConfig, delta_ref: float, rng, curve: list | None = None):
+    """train.py:444-463: the distillation stage; returns (first, last) loss."""
+    state = AdamState.for_params(student.params)
+    first = last = float("nan")
+    for step in range(cfg.distill_steps):
+        last = distill_step(student, teacher, cfg, state, rng, delta_ref)
+        if step == 0:
+            first = last
+        if curve is not None and (step % cfg.log_every == 0 or step == cfg.distill_steps - 1):
+            curve.append({"stage": "distill", "step": step, "loss": last})
+    return first, last
+
+
+def evaluate_psnr(model, dataset, render_cfg, occ=None, split: str = "test", seed: int = 0, workers: int = 1) -> float:
+    """train.py:393-407: mean PSNR over a split, rendered on the device."""
+    from .render import compute_psnr, render_image
+
+    psnrs = []
+    for i in dataset.indices(split):
+        img, _ = render_image(model, occ, dataset.cameras[i], render_cfg, seed=seed, workers=workers)
+        psnrs.append(compute_psnr(img, dataset.images[i]))
+    return float(np.mean(psnrs))
+
+
+def mean_free_space_density(model, empty_cell_flat) -> float:
+    """train.py:589-602: mean density over a fixed probe lattice of known-empty cells."""
+    if len(empty_cell_flat) == 0:
+        return 0.0
+    res = model.resolution
+    cell = model.aabb.cell_size(res)
+    flat = np.asarray(empty_cell_flat)
+    idx3 = np.stack([flat % res[0], (flat // res[0]) % res[1], flat // (res[0] * res[1])], axis=-1)
+    lows = model.aabb.b_min + idx3 * cell
+    offsets = np.stack(np.meshgrid(*([np.array([0.25, 0.5, 0.75])] * 3), indexing="ij"), axis=-1).reshape(-1, 3)
+    pts = (lows[:, None, :] + offsets[None, :, :] * cell).reshape(-1, 3).astype(np.float32)
+    return float(density_probe(model)(pts).mean())
 
 
 class DensityProbe:

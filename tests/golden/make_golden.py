@@ -440,8 +440,30 @@ def gen_train():
         out.update({f"{tag}_o": origins, f"{tag}_d": dirs, f"{tag}_pos": smp.positions, f"{tag}_dirs": smp.directions,
                     f"{tag}_ray": smp.ray_index, f"{tag}_slot": smp.slot, f"{tag}_deltas": smp.deltas,
                     f"{tag}_after": after, f"{tag}_k": np.int64(k_), f"{tag}_pre": np.int64(pre)})
+    # three photometric_step calls on a tiny duck-typed dataset (test_train.py:183-197 shape)
+    class DS:
+        def __init__(self, aabb, cams, images):
+            self.aabb, self.cameras, self.images = aabb, cams, images
+
+        def indices(self, split):
+            return [0, 1, 2] if split == "train" else [1]
+
+    cams = scene.sphere_cameras(aabb, 3, 16, seed=1)
+    imgs = np.random.default_rng(31).random((3, 16, 16, 3)).astype(np.float32)
+    ds = DS(aabb, cams, imgs)
+    g = ggrid.init_network_grid(aabb, (2, 2, 2), seed=8)
+    g.params.biases["density"][:] = 0.8
+    pcfg = train.TrainConfig(batch_size_pixels=32, k_train=16)
+    st = train.AdamState.for_params(g.params)
+    rng = np.random.default_rng(9)
+    out["step_losses"] = np.array([train.photometric_step(g, ds, pcfg, st, rng, lr=5e-4, noise_std=0.1 * i)
+                                   for i in range(3)])
+    out["step_after"] = rng.random(4)
+    out["step_images"] = imgs
+    out.update(_grads_dict("step_p_", g.params))
+    out["free_space"] = np.float64(train.mean_free_space_density(g, np.arange(0, 8, 3)))
     save("train", **out)
-    print("ph0 loss", out["ph0_loss"], "distill", losses)
+    print("ph0 loss", out["ph0_loss"], "distill", losses, "steps", out["step_losses"])
 
 
 def gen_ckpt():

@@ -210,3 +210,33 @@ def test_prepare_ray_samples_bit_exact(tag):
     assert np.array_equal(smp.directions, ref["dirs"])
     assert np.array_equal(smp.ray_index, ref["ray"]) and np.array_equal(smp.slot, ref["slot"])
     assert np.array_equal(smp.deltas, ref["deltas"])
+
+
+def test_photometric_step_matches_reference():
+    """train.py:291-332 through the device: three steps on a tiny dataset with
+    the caller's Generator driving view, pixels, jitter and density noise."""
+    gf = _gf()
+    from paper_2103_13744_b200 import train
+
+    z = golden("train")
+    aabb = gf.Aabb((0.0,) * 3, (1.0,) * 3)
+
+    class DS:
+        def __init__(self):
+            self.aabb, self.cameras, self.images = aabb, gf.sphere_cameras(aabb, 3, 16, seed=1), z["step_images"]
+
+        def indices(self, split):
+            return [0, 1, 2] if split == "train" else [1]
+
+    g = gf.init_network_grid(aabb, (2, 2, 2), seed=8)
+    g.params.biases["density"][:] = 0.8
+    cfg = train.TrainConfig(batch_size_pixels=32, k_train=16)
+    st = train.AdamState.for_params(g.params)
+    rng = np.random.default_rng(9)
+    losses = [train.photometric_step(g, DS(), cfg, st, rng, lr=5e-4, noise_std=0.1 * i) for i in range(3)]
+    np.testing.assert_allclose(losses, z["step_losses"], rtol=1e-5)
+    assert np.array_equal(rng.random(4), z["step_after"])  # same draws consumed as the reference
+    for name in LAYERS:
+        assert np.abs(g.params.weights[name] - z[f"step_p_w_{name}"]).max() <= 5e-6, name
+        assert np.abs(g.params.biases[name] - z[f"step_p_b_{name}"]).max() <= 5e-6, name
+    assert train.mean_free_space_density(g, np.arange(0, 8, 3)) == pytest.approx(float(z["free_space"]), rel=1e-5)
