@@ -70,7 +70,11 @@ struct TcShape {
   static constexpr int SLOT_BYTES = 128 * KA * 2;
   static constexpr int A(int s) { return ONES + 4096 + s * SLOT_BYTES; }
   static constexpr int BAR = A(2);  // mma[0], mma[1], weights, tmem base
-  static constexpr int SMEM = BAR + 32;
+  // window of the CTA's tile descriptors (refilled at pair boundaries): tile
+  // reads at the top of each pair are shared-memory loads, not global ones
+  static constexpr int TILEBUF = BAR + 32;
+  static constexpr int TB = 64;
+  static constexpr int SMEM = TILEBUF + TB * 8;
   static constexpr int NC = N2 <= 32 ? 32 : (N2 <= 64 ? 64 : (N2 <= 128 ? 128 : 256));  // TMEM cols per slot
   static constexpr int TMEM_COLS = 2 * NC;
 #if GF_EXP == 10
@@ -225,11 +229,6 @@ __device__ __forceinline__ void load_row(const TileSched& S, const IO& io, uint2
   if (r.valid) io.template fetch<!IO::kDirEnc>(S, tl.y + (uint32_t)tid, r.idx, r.x, r.d);
 }
 
-// tiles [t, t+1) or [t, t+2): the second slot is used only for a tile of the
-// same cell (both slots share the staged weights)
-__device__ __forceinline__ bool pair_second(const TileSched& S, uint32_t t, uint32_t t_end, uint32_t cell) {
-  return t + 1 < t_end && gf_tile_cell(S.tiles[t + 1]) == cell;
-}
 
 // gamma(x) (core.py:132-152 layout: raw xyz, then per octave k sin xyz, cos
 // xyz; column 63 zero) generated octave by octave and flushed to the K0
@@ -372,6 +371,15 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
   const uint32_t nt = *S.n_tiles;
   const uint32_t per = (nt + gridDim.x - 1) / gridDim.x;
   const uint32_t t_begin = blockIdx.x * per, t_end = min(nt, t_begin + per);
+  uint2* s_tiles = reinterpret_cast<uint2*>(smem + T::TILEBUF);
+  uint32_t tbase = t_begin;
+  auto fill_tiles = [&](uint32_t from) {  // all threads, then a CTA barrier
+    tbase = from;
+    for (uint32_t j = tid; j < (uint32_t)T::TB && from + j < t_end; j += blockDim.x) s_tiles[j] = S.tiles[from + j];
+    __syncthreads();
+  };
+  fill_tiles(t_begin);
+  auto tile_at = [&](uint32_t u) -> uint2 { return s_tiles[u - tbase]; };
   int cur = -1;
   uint32_t ph = 0, ph_w = 0;
 
@@ -412,12 +420,15 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
   };
   // tile of this group inside the pair starting at t (slot 1 only for a
   // second tile of the same cell: both slots share the staged weights)
+  auto second = [&](uint32_t t, uint32_t cell) -> bool {
+    return t + 1 < t_end && gf_tile_cell(tile_at(t + 1)) == cell;
+  };
   auto my_tile = [&](uint32_t t, uint2& tl) -> bool {
     if (t >= t_end) return false;
-    tl = S.tiles[t];
+    tl = tile_at(t);
     if (g == 0) return true;
-    if (!pair_second(S, t, t_end, gf_tile_cell(tl))) return false;
-    tl = S.tiles[t + 1];
+    if (!second(t, gf_tile_cell(tl))) return false;
+    tl = tile_at(t + 1);
     return true;
   };
 
@@ -428,11 +439,12 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
   }
 
   for (uint32_t t = t_begin; t < t_end;) {
-    const uint32_t cell = gf_tile_cell(S.tiles[t]);
-    const bool two = pair_second(S, t, t_end, cell);
+    __syncthreads();  // previous pair fully retired (weight operands and the tile window may be replaced)
+    if (t + 4 > tbase + (uint32_t)T::TB && tbase + (uint32_t)T::TB < t_end) fill_tiles(t);  // CTA-uniform
+    const uint32_t cell = gf_tile_cell(tile_at(t));
+    const bool two = second(t, cell);
     const uint32_t t_next = t + (two ? 2 : 1);
     const bool active = g == 0 || two;
-    __syncthreads();  // previous pair fully retired (weight operands may be replaced)
     const bool new_cell = (int)cell != cur;
     if (new_cell && tid == 0) bulk_load(wb, packed + (size_t)cell * T::CELL_BYTES, T::CELL_BYTES, bar_w);
     cur = (int)cell;
