@@ -433,6 +433,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->R.acc = c.take<float4>((size_t)n_rays);
   w->R.rng = c.take<u128>((size_t)n_rays);
   w->R.run = c.take<uint32_t>((size_t)n_rays);
+  w->R.pend = c.take<uint32_t>((size_t)n_rays);
   w->R.flags = c.take<uint32_t>((size_t)n_rays);
   w->R.ivl = c.take<uint32_t>((size_t)n_rays * GF_MAX_IVL);
   w->R.denc = c.take<uint4>((size_t)n_rays * 4);
@@ -462,11 +463,21 @@ static void block_range(int64_t ray_offset, int64_t block_stride, int64_t n_rays
   *count = last - *first + 1;
 }
 
+// Rounds run in pairs when the warp-cooperative marcher applies (chunk <= 32)
+// and there are at least two rounds: both rounds are placed and evaluated by
+// one K2 + MLP pass and composited in order with the ERT check between them,
+// halving the per-round launches (GF_NO_PAIRS=1 disables it).
+static bool pairs_ok(const gf_march_cfg_t* cfg, int64_t n_rays) {
+  const int n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
+  return cfg->ert_chunk <= 32 && n_rounds >= 2 && (double)n_rays * 2.0 * cfg->ert_chunk < 4.0e9;
+}
+
 size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* grid, const gf_march_cfg_t* cfg,
                                  int64_t n_rays) {
   (void)arch;
   if (!valid_grid(grid) || !cfg || cfg->k < 1 || cfg->ert_chunk < 1 || n_rays < 0) return 0;
   int stride = cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k;
+  if (pairs_ok(cfg, n_rays)) stride = 2 * cfg->ert_chunk;
   Carve c(nullptr);
   RenderWs w;
   // worst case: the call's rays straddle one more block boundary
@@ -493,7 +504,10 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
   if (ray_offset < 0 || n_rays < 0 || ray_block_stride < 1) return fail(GF_ERR_INVALID, "gf_render_rays: bad ray range");
   if (ray_block_stride > 1 && ray_offset % GF_RAY_BLOCK)
     return fail(GF_ERR_INVALID, "gf_render_rays: interleaved shards need a block-aligned ray_offset");
-  const int stride = cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k;
+  const char* no_pairs = getenv("GF_NO_PAIRS");
+  // traces list exactly the reference's samples: no speculative second rounds
+  const bool pair = pairs_ok(cfg, n_rays) && !trace && !(no_pairs && no_pairs[0] == '1');
+  const int stride = pair ? 2 * cfg->ert_chunk : (cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k);
   if ((double)n_rays * stride >= 4.0e9) return fail(GF_ERR_INVALID, "gf_render_rays: too many rays per call");
   if (n_rays == 0) return GF_OK;
   const int64_t nc = n_cells_of(grid);
@@ -544,6 +558,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
   P.n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
   P.n_cells = nc;
   P.stride = stride;
+  P.pair = pair ? 1 : 0;
   P.stratified = cfg->stratified ? 1 : 0;
   P.ert = cfg->epsilon > 0.0 ? 1 : 0;
   P.eps_f64 = cfg->eps_compare_f64 ? 1 : 0;
@@ -665,10 +680,13 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
                                   w.seeds, w.jump, w.start, w.round_jump, w.block_ci);
     k_ray_init<<<ray_blocks, 128, 0, s>>>(P, w.R);
     stage_mark(s, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
-    for (int r = 0; r < P.n_rounds; ++r) {
-      k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r);
-      stage_mark(s, GF_STAGE_MARCH, 1);
-      stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, r, (int64_t)n_rays * stride, s));
+    const int step = P.pair ? 2 : 1;
+    for (int r = 0; r < P.n_rounds; r += step) {
+      k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r, 0);
+      if (P.pair && r + 1 < P.n_rounds) k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r + 1, 1);
+      stage_mark(s, GF_STAGE_MARCH, P.pair && r + 1 < P.n_rounds ? 2 : 1);
+      stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, P.pair ? P.chunk : 0,
+                                                   r / step, (int64_t)n_rays * stride, s));
       if (an)
         launch_field_analytic(*an, w.B.offsets, w.B.srec, w.R.dir, stride_shift, (uint32_t)stride, w.RB.res,
                               (int64_t)n_rays * stride, s);
@@ -676,7 +694,8 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
         run_mlp(t, packed, precision, S, &io, nullptr, s);
       stage_mark(s, GF_STAGE_MLP, 1);
     }
-    k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, P.n_rounds);
+    // final pass: composite the last (pair of) round(s) and write the colours
+    k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, (P.n_rounds + step - 1) / step * step, 0);
     stage_mark(s, GF_STAGE_MARCH, 1);
   };
   // graphs for the production (tensor-core) path; the fp32 reference mode,

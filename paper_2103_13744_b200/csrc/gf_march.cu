@@ -339,7 +339,7 @@ __global__ void k_dilate_yz(const uint32_t* __restrict__ in, uint32_t* out, int3
 // -------------------------------------------------------------------------
 template <bool SMEM>
 __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const uint32_t* __restrict__ run,
-                                               BucketBufs Bk, int64_t n_cells, int stride, int round) {
+                                               BucketBufs Bk, int64_t n_cells, int stride, int half, int round) {
   extern __shared__ uint32_t s_scan[];  // [n_cells+1] row offsets, [n_cells+1] tile offsets
   const uint32_t* counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
   const uint32_t* off = Bk.offsets;
@@ -427,7 +427,8 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
   for (uint64_t k0 = warp_g * 32; k0 < n_list; k0 += n_warps * 32) {
     const uint64_t k = k0 + lane;
     const uint32_t i = k < n_list ? RB.emit_list[k] : 0u;
-    const uint32_t nr = k < n_list ? run[i] : 0u;
+    const uint32_t rv = k < n_list ? run[i] : 0u;
+    const uint32_t na = rv & 0xFFFFu, nr = na + (rv >> 16);  // paired rounds: both rounds' records
     uint32_t incl = nr;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -452,8 +453,10 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
         }
         const uint32_t j = q - __shfl_sync(0xffffffffu, excl, own);
         const uint32_t i_o = __shfl_sync(0xffffffffu, i, own);
+        const uint32_t na_o = __shfl_sync(0xffffffffu, na, own);
         ok[u] = q < total;
-        src[u] = i_o * (uint32_t)stride + j;  // staging index (< 2^32, checked on the host)
+        // staging index (< 2^32, checked on the host); a pair's second round sits `half` further
+        src[u] = i_o * (uint32_t)stride + (j < na_o ? j : (uint32_t)half + (j - na_o));
         if (ok[u]) r[u] = gf_ld_hint(RB.rec + src[u], pol_first);
       }
 #pragma unroll
@@ -469,7 +472,7 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
 }
 
 int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
-                 int stride, int round, int64_t max_rows, cudaStream_t st) {
+                 int stride, int half, int round, int64_t max_rows, cudaStream_t st) {
   const size_t smem = (size_t)2 * (n_cells + 1) * 4;
   if (n_cells <= 8192) {
     static thread_local bool attr = false;
@@ -477,13 +480,13 @@ int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, c
       cudaFuncSetAttribute(k_place<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8193 * 4);
       attr = true;
     }
-    k_place<true><<<num_sms() * 2, 512, smem, st>>>(grid, RB, run, Bk, n_cells, stride, round);
+    k_place<true><<<num_sms() * 2, 512, smem, st>>>(grid, RB, run, Bk, n_cells, stride, half, round);
     return 1;
   }
   BucketBufs b = Bk;
   b.counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
   const int n = launch_scan_cells(b, n_cells, st, max_rows);  // offsets + tiles; clears this round's counts
-  k_place<false><<<num_sms() * 2, 512, 0, st>>>(grid, RB, run, Bk, n_cells, stride, round);
+  k_place<false><<<num_sms() * 2, 512, 0, st>>>(grid, RB, run, Bk, n_cells, stride, half, round);
   return n + 1;
 }
 
@@ -518,50 +521,85 @@ __device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v)
 // march pass r: composite round r-1 (+ERT), then place / skip / emit round r.
 // At r == n_rounds: composite the last round and write the final colours.
 // -------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundBufs B, int round) {
+__global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
   const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   const bool in_range = i < P.n_rays;
   uint32_t fw = in_range ? R.flags[i] : 0u;  // flags | candidate-round mask << 8
   const uint32_t fw0 = fw;
-  const bool final_pass = round == P.n_rounds;
+  const bool final_pass = round >= P.n_rounds;
   if (!final_pass && !__any_sync(0xffffffffu, fw & GF_RAY_ALIVE)) return;
 
-  // ---- composite round r-1 (render.py:333-337), float32, no contraction;
-  // only rays that queried samples last round have anything to blend
+  // ---- composite the previous round (render.py:333-337), float32, no
+  // contraction; only rays that queried samples then have anything to blend.
+  // Paired rounds (P.pair): chunks 2s and 2s+1 are placed and evaluated
+  // together and composited here one after the other, with the ERT check
+  // between them; a ray that dies after the first drops the second's samples
+  // and its deferred counters, exactly as if that round had never run.
   float4 acc = make_float4(0.f, 0.f, 0.f, 1.f);
-  const bool had = (fw & GF_RAY_ALIVE) && (fw & GF_RAY_HAD);
+  const bool hadA = (fw & GF_RAY_ALIVE) && (fw & GF_RAY_HAD);
+  const bool hadB = P.pair && (fw & GF_RAY_ALIVE) && (fw & GF_RAY_HAD2);
+  const bool had = phase == 0 && (hadA || hadB);
+  unsigned long long commit_q = 0, commit_s = 0;
   if (had) {
     acc = R.acc[i];
     const float seg = R.dir[i].w;
     const uint64_t base = (uint64_t)i * (uint64_t)P.stride;
-    const uint32_t n = R.run[i];
-    float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
+    const uint32_t run = R.run[i];
     const uint64_t pol_first = gf_pol_first();
-    for (uint32_t j = 0; j < n; ++j) {
-      float4 q = gf_ld_hint(B.res + base + j, pol_first);
-      float a = -expm1f(__fmul_rn(-q.w, seg));
-      float w = __fmul_rn(tr, a);
-      tr = __fmul_rn(tr, __fsub_rn(1.0f, a));
-      sr = __fadd_rn(sr, __fmul_rn(w, q.x));
-      sg = __fadd_rn(sg, __fmul_rn(w, q.y));
-      sb = __fadd_rn(sb, __fmul_rn(w, q.z));
-    }
-    acc.x = __fadd_rn(acc.x, __fmul_rn(acc.w, sr));
-    acc.y = __fadd_rn(acc.y, __fmul_rn(acc.w, sg));
-    acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
-    acc.w = __fmul_rn(acc.w, tr);
-    // ---- ERT after the round (render.py:338-343); transmittance only moves
-    // in rounds with samples, so other rays cannot cross epsilon
-    if (P.ert) {
-      bool dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
+    auto blend = [&](uint64_t b0, uint32_t n) {
+      float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
+      for (uint32_t j = 0; j < n; ++j) {
+        float4 q = gf_ld_hint(B.res + b0 + j, pol_first);
+        float a = -expm1f(__fmul_rn(-q.w, seg));
+        float w = __fmul_rn(tr, a);
+        tr = __fmul_rn(tr, __fsub_rn(1.0f, a));
+        sr = __fadd_rn(sr, __fmul_rn(w, q.x));
+        sg = __fadd_rn(sg, __fmul_rn(w, q.y));
+        sb = __fadd_rn(sb, __fmul_rn(w, q.z));
+      }
+      acc.x = __fadd_rn(acc.x, __fmul_rn(acc.w, sr));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(acc.w, sg));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
+      acc.w = __fmul_rn(acc.w, tr);
+    };
+    // ERT after a round (render.py:338-343); transmittance only moves in
+    // rounds with samples, so other rays cannot cross epsilon.  `next` is the
+    // first round after the composited one: termination counts if it exists.
+    auto ert = [&](int next) -> bool {
+      if (!P.ert) return false;
+      const bool dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
       if (dead) {
         fw &= ~(uint32_t)GF_RAY_ALIVE;
-        if ((int64_t)round * P.chunk < P.k) fw |= GF_RAY_TERMINATED;  // rounds remained
+        if ((int64_t)next * P.chunk < P.k) fw |= GF_RAY_TERMINATED;  // rounds remained
+      }
+      return dead;
+    };
+    if (!P.pair) {
+      blend(base, run);
+      ert(round);
+    } else {
+      bool dead = false;
+      if (hadA) {
+        blend(base, run & 0xFFFFu);
+        dead = ert(round - 1);
+        if (!dead && round - 1 < P.n_rounds) {  // the second round really ran for this ray: its counters stand
+          const uint32_t pend = R.pend[i];
+          commit_q = pend & 0xFFFFu;
+          commit_s = pend >> 16;
+        }
+      }
+      if (!dead && hadB) {
+        blend(base + (uint64_t)P.chunk, run >> 16);
+        ert(round);
       }
     }
     R.acc[i] = acc;
   }
-  fw &= ~(uint32_t)GF_RAY_HAD;
+  if (P.pair) {
+    warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], commit_q);
+    warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], commit_s);
+  }
+  if (phase == 0) fw &= ~(uint32_t)(GF_RAY_HAD | GF_RAY_HAD2);
 
   if (final_pass) {
     if (in_range) {
@@ -584,7 +622,13 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
   const bool alive = (fw & GF_RAY_ALIVE) != 0;
   // rays whose coarse intervals have no slot in this round only add to ess_skipped
   const bool active = alive && ((fw & GF_RAY_ALLROUNDS) || (round < 24 && ((fw >> (8 + round)) & 1u)));
-  warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (alive && !active) ? (unsigned long long)m : 0ull);
+  // second round of a pair: a ray whose first round queried samples may still
+  // die at that round's ERT check, so its counters wait in R.pend until then
+  const bool defer = phase == 1 && alive && (fw & GF_RAY_HAD);
+  const int par = P.pair ? ((round >> 1) & 1) : (round & 1);  // histogram / emit-list parity
+  const uint32_t half = phase == 1 ? (uint32_t)P.chunk : 0u;  // staging offset of the pair's second round
+  warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (alive && !active && !defer) ? (unsigned long long)m : 0ull);
+  if (defer && !active) R.pend[i] = (uint32_t)m << 16;
   if (!__any_sync(0xffffffffu, active)) {
     if (in_range && fw != fw0) R.flags[i] = fw;
     return;
@@ -629,7 +673,7 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     cmask &= msk;
   }
   const bool fast_clip = P.grid.fast != 0;
-  uint32_t* counts_r = B.counts + (size_t)(round & 1) * (size_t)P.n_cells;  // this round's histogram
+  uint32_t* counts_r = B.counts + (size_t)par * (size_t)P.n_cells;  // this round's histogram
   uint32_t kept = 0;
   if (m <= 32) {
     // ---- warp-cooperative path: the warp's candidate (ray, slot) pairs are
@@ -746,8 +790,8 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       const uint32_t crank = hist_rank(counts_r, keep, cell);
       if (keep) {
         const uint32_t pos = s_ray[wib][own].carry + __popc(kb & same & ((1u << lane) - 1u));
-        gf_st_hint(B.rec + (uint64_t)i_o * (uint64_t)P.stride + pos, make_float4(px, py, pz, __uint_as_float(crank)),
-                   gf_pol_last());
+        gf_st_hint(B.rec + (uint64_t)i_o * (uint64_t)P.stride + half + pos,
+                   make_float4(px, py, pz, __uint_as_float(crank)), gf_pol_last());
         if (P.trace) {
           unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
           if ((int64_t)slotpos < P.trace_capacity)
@@ -815,23 +859,26 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
     }
   }
   }  // sequential path (ert_chunk > 32)
+  const bool hadA_now = phase == 1 && (fw & GF_RAY_HAD);  // the pair's first round queried samples
   if (active && kept > 0) {
-    R.run[i] = kept;
-    fw |= GF_RAY_HAD;
+    // run = first round's count | second round's count << 16
+    R.run[i] = phase == 0 ? kept : ((hadA_now ? (R.run[i] & 0xFFFFu) : 0u) | (kept << 16));
+    fw |= phase == 0 ? GF_RAY_HAD : GF_RAY_HAD2;
   }
+  if (defer && active) R.pend[i] = kept | ((uint32_t)(m - (int)kept) << 16);
   if (in_range && fw != fw0) R.flags[i] = fw;
-  {  // compact list of rays with queried samples, for the scatter kernel
-    const bool emit = active && kept > 0;
+  {  // compact list of rays with queried samples (once per pair), for the scatter kernel
+    const bool emit = active && kept > 0 && !hadA_now;
     const unsigned em = __ballot_sync(0xffffffffu, emit);
     if (em) {
       uint32_t b = 0;
-      if (gf_lane() == 0) b = atomicAdd(&B.emit_count[round & 1], (uint32_t)__popc(em));
+      if (gf_lane() == 0) b = atomicAdd(&B.emit_count[par], (uint32_t)__popc(em));
       b = __shfl_sync(0xffffffffu, b, 0);
       if (emit) B.emit_list[b + __popc(em & ((1u << gf_lane()) - 1u))] = (uint32_t)i;
     }
   }
-  warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], kept);
-  warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], active ? (unsigned long long)(m - (int)kept) : 0ull);
+  warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], defer ? 0ull : (unsigned long long)kept);
+  warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (active && !defer) ? (unsigned long long)(m - (int)kept) : 0ull);
 }
 
 }  // namespace gf

@@ -7,6 +7,7 @@
 #define GF_RAY_TERMINATED 4
 #define GF_RAY_HAD 8         // queried samples in the last marched round (composite them next pass)
 #define GF_RAY_ALLROUNDS 16  // no per-round candidate mask: every round is a candidate round
+#define GF_RAY_HAD2 32       // paired rounds: the pair's second round queried samples
 
 namespace gf {
 
@@ -30,6 +31,7 @@ struct MarchParams {
   int net_from_occ;         // network cell = occupancy cell >> net_shift per axis (see gf_api.cu)
   int net_shift[3];
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
+  int pair;           // rounds run in pairs (2s, 2s+1): placed and evaluated together, composited in order
   int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
   int64_t n_cells;
   int64_t march_threads;
@@ -49,7 +51,8 @@ struct RayState {
   float4* dir;    // dx, dy, dz, seg_32
   float4* acc;    // r, g, b, transmittance
   u128* rng;      // PCG64 state of the word holding the ray's slot-0 float32 draw
-  uint32_t* run;  // queried samples of the ray in the last marched round
+  uint32_t* run;  // queried samples of the ray in the last marched round (pairs: first | second << 16)
+  uint32_t* pend; // pairs: the second round's (queries | ess_skipped << 16), committed if the ray survives the first
   uint32_t* flags;  // GF_RAY_* bits | (rounds with candidate slots, bit r) << 8
   uint32_t* ivl;  // GF_MAX_IVL candidate slot ranges per ray (lo | hi << 16), from the coarse DDA
   uint4* denc;    // NULL, or 4 x uint4 per ray: gamma(d) as fp16 for the tensor-core MLP
@@ -97,7 +100,7 @@ __device__ __forceinline__ int64_t seed_slot(const MarchParams& P, int64_t g) {
 // K2 for the render path (fused scan + tile list + rank-based placement);
 // returns the number of launches it made
 int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
-                 int stride, int round, int64_t max_rows, cudaStream_t st);
+                 int stride, int half, int round, int64_t max_rows, cudaStream_t st);
 
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
                               int k, int chunk, int n_rounds, u128* seeds, u128* jump, u128* start,
@@ -122,6 +125,6 @@ __device__ __forceinline__ uint32_t gf_coarse_cell(const GfGrid& g, float x, flo
   }
   return (uint32_t)(idx[0] + g.res[0] * (idx[1] + g.res[1] * idx[2]));
 }
-__global__ void k_march(MarchParams P, RayState R, RoundBufs B, int round);
+__global__ void k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase);
 
 }  // namespace gf
