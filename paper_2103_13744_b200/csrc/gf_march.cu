@@ -521,7 +521,9 @@ __device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v)
 // march pass r: composite round r-1 (+ERT), then place / skip / emit round r.
 // At r == n_rounds: composite the last round and write the final colours.
 // -------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
+// 7 CTAs/SM (<= 72 registers): measured faster than the unconstrained 85
+// registers despite a few spilled bytes
+__global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
   const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   const bool in_range = i < P.n_rays;
   uint32_t fw = in_range ? R.flags[i] : 0u;  // flags | candidate-round mask << 8
@@ -574,23 +576,21 @@ __global__ void __launch_bounds__(128) k_march(MarchParams P, RayState R, RoundB
       }
       return dead;
     };
-    if (!P.pair) {
-      blend(base, run);
-      ert(round);
-    } else {
-      bool dead = false;
-      if (hadA) {
-        blend(base, run & 0xFFFFu);
-        dead = ert(round - 1);
-        if (!dead && round - 1 < P.n_rounds) {  // the second round really ran for this ray: its counters stand
-          const uint32_t pend = R.pend[i];
-          commit_q = pend & 0xFFFFu;
-          commit_s = pend >> 16;
-        }
-      }
-      if (!dead && hadB) {
-        blend(base + (uint64_t)P.chunk, run >> 16);
-        ert(round);
+    // one blend site (keeps the marcher's registers down): part 0 is the
+    // round (or a pair's first round), part 1 a pair's second round
+    bool dead = false;
+#pragma unroll 1
+    for (int part = 0; part < (P.pair ? 2 : 1); ++part) {
+      const bool use = !P.pair || (part == 0 ? hadA : (hadB && !dead));
+      if (!use) continue;
+      const uint32_t n = !P.pair ? run : (part == 0 ? (run & 0xFFFFu) : (run >> 16));
+      blend(base + (part ? (uint64_t)P.chunk : 0ull), n);
+      dead = ert(P.pair && part == 0 ? round - 1 : round);
+      if (P.pair && part == 0 && !dead && round - 1 < P.n_rounds) {
+        // the pair's second round really ran for this ray: its counters stand
+        const uint32_t pend = R.pend[i];
+        commit_q = pend & 0xFFFFu;
+        commit_s = pend >> 16;
       }
     }
     R.acc[i] = acc;
