@@ -433,7 +433,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->R.acc = c.take<float4>((size_t)n_rays);
   w->R.rng = c.take<u128>((size_t)n_rays);
   w->R.run = c.take<uint32_t>((size_t)n_rays);
-  w->R.pend = c.take<uint32_t>((size_t)n_rays);
+  w->R.pend = c.take<uint32_t>((size_t)n_rays * 4);
   w->R.flags = c.take<uint32_t>((size_t)n_rays);
   w->R.ivl = c.take<uint32_t>((size_t)n_rays * GF_MAX_IVL);
   w->R.denc = c.take<uint4>((size_t)n_rays * 4);
@@ -463,13 +463,24 @@ static void block_range(int64_t ray_offset, int64_t block_stride, int64_t n_rays
   *count = last - *first + 1;
 }
 
-// Rounds run in pairs when the warp-cooperative marcher applies (chunk <= 32)
-// and there are at least two rounds: both rounds are placed and evaluated by
-// one K2 + MLP pass and composited in order with the ERT check between them,
-// halving the per-round launches (GF_NO_PAIRS=1 disables it).
-static bool pairs_ok(const gf_march_cfg_t* cfg, int64_t n_rays) {
+// Rounds run in groups of G (2 by default; 4 available) when the
+// warp-cooperative marcher applies (chunk <= 32): the G rounds are placed by G
+// marcher passes and evaluated by one K2 + MLP pass, then composited in order
+// with the ERT check after each, cutting the per-round launches by G.
+// GF_GROUP=1|2|4 overrides (1 = one round at a time).
+static int group_size(const gf_march_cfg_t* cfg, int64_t n_rays, bool allow_env = true) {
   const int n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
-  return cfg->ert_chunk <= 32 && n_rounds >= 2 && (double)n_rays * 2.0 * cfg->ert_chunk < 4.0e9;
+  // default 2: equal frame time to 4 on C2 and half the speculative work
+  // when rays terminate early
+  int g = n_rounds >= 2 ? 2 : 1;
+  if (allow_env) {
+    const char* e = getenv("GF_GROUP");
+    if (e && (e[0] == '1' || e[0] == '2' || e[0] == '4')) g = e[0] - '0';
+    while (g > n_rounds && g > 1) g /= 2;
+  }
+  if (cfg->ert_chunk > 32) g = 1;
+  while (g > 1 && (double)n_rays * g * cfg->ert_chunk >= 4.0e9) g /= 2;
+  return g;
 }
 
 size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* grid, const gf_march_cfg_t* cfg,
@@ -477,7 +488,8 @@ size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* gr
   (void)arch;
   if (!valid_grid(grid) || !cfg || cfg->k < 1 || cfg->ert_chunk < 1 || n_rays < 0) return 0;
   int stride = cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k;
-  if (pairs_ok(cfg, n_rays)) stride = 2 * cfg->ert_chunk;
+  const int g = group_size(cfg, n_rays, true);
+  if (g > 1) stride = g * cfg->ert_chunk;
   Carve c(nullptr);
   RenderWs w;
   // worst case: the call's rays straddle one more block boundary
@@ -504,10 +516,9 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
   if (ray_offset < 0 || n_rays < 0 || ray_block_stride < 1) return fail(GF_ERR_INVALID, "gf_render_rays: bad ray range");
   if (ray_block_stride > 1 && ray_offset % GF_RAY_BLOCK)
     return fail(GF_ERR_INVALID, "gf_render_rays: interleaved shards need a block-aligned ray_offset");
-  const char* no_pairs = getenv("GF_NO_PAIRS");
-  // traces list exactly the reference's samples: no speculative second rounds
-  const bool pair = pairs_ok(cfg, n_rays) && !trace && !(no_pairs && no_pairs[0] == '1');
-  const int stride = pair ? 2 * cfg->ert_chunk : (cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k);
+  // traces list exactly the reference's samples: no speculative later rounds
+  const int group = trace ? 1 : group_size(cfg, n_rays, true);
+  const int stride = group > 1 ? group * cfg->ert_chunk : (cfg->ert_chunk < cfg->k ? cfg->ert_chunk : cfg->k);
   if ((double)n_rays * stride >= 4.0e9) return fail(GF_ERR_INVALID, "gf_render_rays: too many rays per call");
   if (n_rays == 0) return GF_OK;
   const int64_t nc = n_cells_of(grid);
@@ -558,7 +569,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
   P.n_rounds = (cfg->k + cfg->ert_chunk - 1) / cfg->ert_chunk;
   P.n_cells = nc;
   P.stride = stride;
-  P.pair = pair ? 1 : 0;
+  P.group = group;
   P.stratified = cfg->stratified ? 1 : 0;
   P.ert = cfg->epsilon > 0.0 ? 1 : 0;
   P.eps_f64 = cfg->eps_compare_f64 ? 1 : 0;
@@ -680,12 +691,13 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
                                   w.seeds, w.jump, w.start, w.round_jump, w.block_ci);
     k_ray_init<<<ray_blocks, 128, 0, s>>>(P, w.R);
     stage_mark(s, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
-    const int step = P.pair ? 2 : 1;
+    const int step = P.group;
     for (int r = 0; r < P.n_rounds; r += step) {
-      k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r, 0);
-      if (P.pair && r + 1 < P.n_rounds) k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r + 1, 1);
-      stage_mark(s, GF_STAGE_MARCH, P.pair && r + 1 < P.n_rounds ? 2 : 1);
-      stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, P.pair ? P.chunk : 0,
+      int passes = 0;
+      for (int p = 0; p < step && r + p < P.n_rounds; ++p, ++passes)
+        k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r + p, p);
+      stage_mark(s, GF_STAGE_MARCH, passes);
+      stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, step > 1 ? P.chunk : 0,
                                                    r / step, (int64_t)n_rays * stride, s));
       if (an)
         launch_field_analytic(*an, w.B.offsets, w.B.srec, w.R.dir, stride_shift, (uint32_t)stride, w.RB.res,
@@ -694,7 +706,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
         run_mlp(t, packed, precision, S, &io, nullptr, s);
       stage_mark(s, GF_STAGE_MLP, 1);
     }
-    // final pass: composite the last (pair of) round(s) and write the colours
+    // final pass: composite the last group of rounds and write the colours
     k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, (P.n_rounds + step - 1) / step * step, 0);
     stage_mark(s, GF_STAGE_MARCH, 1);
   };

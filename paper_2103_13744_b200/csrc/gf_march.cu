@@ -337,7 +337,7 @@ __global__ void k_dilate_yz(const uint32_t* __restrict__ in, uint32_t* out, int3
 // every thread writes part of the tile list.  !SMEM (very large grids):
 // offsets and tiles come from k_scan_cells.
 // -------------------------------------------------------------------------
-template <bool SMEM>
+template <bool SMEM, int GR>
 __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const uint32_t* __restrict__ run,
                                                BucketBufs Bk, int64_t n_cells, int stride, int half, int round) {
   extern __shared__ uint32_t s_scan[];  // [n_cells+1] row offsets, [n_cells+1] tile offsets
@@ -428,7 +428,13 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
     const uint64_t k = k0 + lane;
     const uint32_t i = k < n_list ? RB.emit_list[k] : 0u;
     const uint32_t rv = k < n_list ? run[i] : 0u;
-    const uint32_t na = rv & 0xFFFFu, nr = na + (rv >> 16);  // paired rounds: both rounds' records
+    // grouped rounds: one count byte per round of the group, records of round
+    // p at staging offset p * half
+    // GR rounds per group (one count byte each); cum = prefix counts after
+    // rounds 0, 1, 2 of the group, one byte each
+    const uint32_t c1 = rv & 0xFFu, c2 = c1 + ((rv >> 8) & 0xFFu), c3 = c2 + ((rv >> 16) & 0xFFu);
+    const uint32_t nr = GR == 1 ? rv : (GR == 2 ? c2 : c3 + (rv >> 24));
+    const uint32_t cum = GR == 2 ? c1 : (c1 | (c2 << 8) | (c3 << 16));
     uint32_t incl = nr;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -453,10 +459,20 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
         }
         const uint32_t j = q - __shfl_sync(0xffffffffu, excl, own);
         const uint32_t i_o = __shfl_sync(0xffffffffu, i, own);
-        const uint32_t na_o = __shfl_sync(0xffffffffu, na, own);
         ok[u] = q < total;
-        // staging index (< 2^32, checked on the host); a pair's second round sits `half` further
-        src[u] = i_o * (uint32_t)stride + (j < na_o ? j : (uint32_t)half + (j - na_o));
+        // staging index (< 2^32, checked on the host): j-th record of the ray
+        // over its group's rounds, round p's records `p * half` further
+        uint32_t off = j;
+        if (GR == 2) {
+          const uint32_t a1 = __shfl_sync(0xffffffffu, cum, own);
+          off = j < a1 ? j : (uint32_t)half + j - a1;
+        } else if (GR == 4) {
+          const uint32_t cu = __shfl_sync(0xffffffffu, cum, own);
+          const uint32_t a1 = cu & 0xFFu, a2 = (cu >> 8) & 0xFFu, a3 = cu >> 16;
+          off = j < a1 ? j
+                       : (j < a2 ? (uint32_t)half + j - a1 : (j < a3 ? 2u * half + j - a2 : 3u * half + j - a3));
+        }
+        src[u] = i_o * (uint32_t)stride + off;
         if (ok[u]) r[u] = gf_ld_hint(RB.rec + src[u], pol_first);
       }
 #pragma unroll
@@ -471,23 +487,32 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
   }
 }
 
-int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
-                 int stride, int half, int round, int64_t max_rows, cudaStream_t st) {
+template <int GR>
+static int launch_place_g(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk,
+                          int64_t n_cells, int stride, int half, int round, int64_t max_rows, cudaStream_t st) {
   const size_t smem = (size_t)2 * (n_cells + 1) * 4;
   if (n_cells <= 8192) {
     static thread_local bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_place<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8193 * 4);
+      cudaFuncSetAttribute(k_place<true, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8193 * 4);
       attr = true;
     }
-    k_place<true><<<num_sms() * 2, 512, smem, st>>>(grid, RB, run, Bk, n_cells, stride, half, round);
+    k_place<true, GR><<<num_sms() * 2, 512, smem, st>>>(grid, RB, run, Bk, n_cells, stride, half, round);
     return 1;
   }
   BucketBufs b = Bk;
   b.counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
   const int n = launch_scan_cells(b, n_cells, st, max_rows);  // offsets + tiles; clears this round's counts
-  k_place<false><<<num_sms() * 2, 512, 0, st>>>(grid, RB, run, Bk, n_cells, stride, half, round);
+  k_place<false, GR><<<num_sms() * 2, 512, 0, st>>>(grid, RB, run, Bk, n_cells, stride, half, round);
   return n + 1;
+}
+
+int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
+                 int stride, int half, int round, int64_t max_rows, cudaStream_t st) {
+  const int group = half > 0 ? stride / half : 1;  // rounds per group (1, 2 or 4)
+  if (group == 4) return launch_place_g<4>(grid, RB, run, Bk, n_cells, stride, half, round, max_rows, st);
+  if (group == 2) return launch_place_g<2>(grid, RB, run, Bk, n_cells, stride, half, round, max_rows, st);
+  return launch_place_g<1>(grid, RB, run, Bk, n_cells, stride, 0, round, max_rows, st);
 }
 
 __device__ __forceinline__ u128 ldg_u128(const u128* p) {
@@ -533,14 +558,14 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
 
   // ---- composite the previous round (render.py:333-337), float32, no
   // contraction; only rays that queried samples then have anything to blend.
-  // Paired rounds (P.pair): chunks 2s and 2s+1 are placed and evaluated
-  // together and composited here one after the other, with the ERT check
-  // between them; a ray that dies after the first drops the second's samples
-  // and its deferred counters, exactly as if that round had never run.
+  // Grouped rounds (P.group = G > 1): rounds G*s .. G*s+G-1 are placed by G
+  // marcher passes and evaluated by one K2 + MLP pass, then composited here
+  // in order with the ERT check after each; a ray that dies inside the group
+  // drops the later rounds' samples and their deferred counters, exactly as
+  // if those rounds had never run.
   float4 acc = make_float4(0.f, 0.f, 0.f, 1.f);
-  const bool hadA = (fw & GF_RAY_ALIVE) && (fw & GF_RAY_HAD);
-  const bool hadB = P.pair && (fw & GF_RAY_ALIVE) && (fw & GF_RAY_HAD2);
-  const bool had = phase == 0 && (hadA || hadB);
+  const uint32_t had_bits = (fw & GF_RAY_ALIVE) ? (fw & GF_RAY_HAD_ALL) : 0u;
+  const bool had = phase == 0 && had_bits != 0;
   unsigned long long commit_q = 0, commit_s = 0;
   if (had) {
     acc = R.acc[i];
@@ -564,42 +589,38 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
       acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
       acc.w = __fmul_rn(acc.w, tr);
     };
-    // ERT after a round (render.py:338-343); transmittance only moves in
-    // rounds with samples, so other rays cannot cross epsilon.  `next` is the
-    // first round after the composited one: termination counts if it exists.
-    auto ert = [&](int next) -> bool {
-      if (!P.ert) return false;
-      const bool dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
-      if (dead) {
-        fw &= ~(uint32_t)GF_RAY_ALIVE;
-        if ((int64_t)next * P.chunk < P.k) fw |= GF_RAY_TERMINATED;  // rounds remained
-      }
-      return dead;
-    };
-    // one blend site (keeps the marcher's registers down): part 0 is the
-    // round (or a pair's first round), part 1 a pair's second round
+    // one blend site (keeps the marcher's registers down).  Part p is round
+    // round - G + p; the ERT check after it counts a termination if round
+    // p + 1 exists (render.py:338-343).  Transmittance only moves in rounds
+    // with samples, so other rays cannot cross epsilon.
+    const int G = P.group;
     bool dead = false;
 #pragma unroll 1
-    for (int part = 0; part < (P.pair ? 2 : 1); ++part) {
-      const bool use = !P.pair || (part == 0 ? hadA : (hadB && !dead));
-      if (!use) continue;
-      const uint32_t n = !P.pair ? run : (part == 0 ? (run & 0xFFFFu) : (run >> 16));
-      blend(base + (part ? (uint64_t)P.chunk : 0ull), n);
-      dead = ert(P.pair && part == 0 ? round - 1 : round);
-      if (P.pair && part == 0 && !dead && round - 1 < P.n_rounds) {
-        // the pair's second round really ran for this ray: its counters stand
-        const uint32_t pend = R.pend[i];
-        commit_q = pend & 0xFFFFu;
-        commit_s = pend >> 16;
+    for (int part = 0; part < G && !dead; ++part) {
+      const int c = round - G + part;  // the composited round
+      if (part > 0 && c < P.n_rounds && (had_bits & gf_had_below(part))) {
+        // the round really ran for this ray: its deferred counters stand
+        const uint32_t pend = R.pend[4 * (uint64_t)i + part];
+        commit_q += pend & 0xFFFFu;
+        commit_s += pend >> 16;
+      }
+      if (!(had_bits & gf_had_bit(part))) continue;
+      blend(base + (uint64_t)part * (uint64_t)P.chunk, G == 1 ? run : ((run >> (8 * part)) & 0xFFu));
+      if (P.ert) {
+        dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
+        if (dead) {
+          fw &= ~(uint32_t)GF_RAY_ALIVE;
+          if ((int64_t)(c + 1) * P.chunk < P.k) fw |= GF_RAY_TERMINATED;  // rounds remained
+        }
       }
     }
     R.acc[i] = acc;
   }
-  if (P.pair) {
+  if (P.group > 1) {
     warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], commit_q);
     warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], commit_s);
   }
-  if (phase == 0) fw &= ~(uint32_t)(GF_RAY_HAD | GF_RAY_HAD2);
+  if (phase == 0) fw &= ~(uint32_t)GF_RAY_HAD_ALL;
 
   if (final_pass) {
     if (in_range) {
@@ -622,13 +643,14 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
   const bool alive = (fw & GF_RAY_ALIVE) != 0;
   // rays whose coarse intervals have no slot in this round only add to ess_skipped
   const bool active = alive && ((fw & GF_RAY_ALLROUNDS) || (round < 24 && ((fw >> (8 + round)) & 1u)));
-  // second round of a pair: a ray whose first round queried samples may still
-  // die at that round's ERT check, so its counters wait in R.pend until then
-  const bool defer = phase == 1 && alive && (fw & GF_RAY_HAD);
-  const int par = P.pair ? ((round >> 1) & 1) : (round & 1);  // histogram / emit-list parity
-  const uint32_t half = phase == 1 ? (uint32_t)P.chunk : 0u;  // staging offset of the pair's second round
+  // later round of a group: a ray whose earlier rounds in the group queried
+  // samples may still die at their ERT checks, so its counters wait in R.pend
+  const bool earlier = phase > 0 && (fw & gf_had_below(phase));
+  const bool defer = alive && earlier;
+  const int par = (round / P.group) & 1;                       // histogram / emit-list parity
+  const uint32_t half = (uint32_t)phase * (uint32_t)P.chunk;   // staging offset of the group's round
   warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (alive && !active && !defer) ? (unsigned long long)m : 0ull);
-  if (defer && !active) R.pend[i] = (uint32_t)m << 16;
+  if (defer && !active) R.pend[4 * (uint64_t)i + phase] = (uint32_t)m << 16;
   if (!__any_sync(0xffffffffu, active)) {
     if (in_range && fw != fw0) R.flags[i] = fw;
     return;
@@ -859,16 +881,16 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
     }
   }
   }  // sequential path (ert_chunk > 32)
-  const bool hadA_now = phase == 1 && (fw & GF_RAY_HAD);  // the pair's first round queried samples
   if (active && kept > 0) {
-    // run = first round's count | second round's count << 16
-    R.run[i] = phase == 0 ? kept : ((hadA_now ? (R.run[i] & 0xFFFFu) : 0u) | (kept << 16));
-    fw |= phase == 0 ? GF_RAY_HAD : GF_RAY_HAD2;
+    // groups: one byte per round of the group (the first writer of a group
+    // clears the others); single rounds: the whole word
+    R.run[i] = P.group == 1 ? kept : ((earlier ? R.run[i] : 0u) | (kept << (8 * phase)));
+    fw |= gf_had_bit(phase);
   }
-  if (defer && active) R.pend[i] = kept | ((uint32_t)(m - (int)kept) << 16);
+  if (defer && active) R.pend[4 * (uint64_t)i + phase] = kept | ((uint32_t)(m - (int)kept) << 16);
   if (in_range && fw != fw0) R.flags[i] = fw;
-  {  // compact list of rays with queried samples (once per pair), for the scatter kernel
-    const bool emit = active && kept > 0 && !hadA_now;
+  {  // compact list of rays with queried samples (once per group), for the scatter kernel
+    const bool emit = active && kept > 0 && !earlier;
     const unsigned em = __ballot_sync(0xffffffffu, emit);
     if (em) {
       uint32_t b = 0;

@@ -7,7 +7,12 @@
 #define GF_RAY_TERMINATED 4
 #define GF_RAY_HAD 8         // queried samples in the last marched round (composite them next pass)
 #define GF_RAY_ALLROUNDS 16  // no per-round candidate mask: every round is a candidate round
-#define GF_RAY_HAD2 32       // paired rounds: the pair's second round queried samples
+#define GF_RAY_HAD_ALL (8u | 32u | 64u | 128u)  // grouped rounds: round p of the group queried samples
+// flag bit of round p of a group (p = 0 is GF_RAY_HAD), and of rounds < p
+__host__ __device__ __forceinline__ uint32_t gf_had_bit(int p) { return p == 0 ? 8u : (16u << p); }
+__host__ __device__ __forceinline__ uint32_t gf_had_below(int p) {
+  return p <= 0 ? 0u : (p == 1 ? 8u : (p == 2 ? 40u : 104u));
+}
 
 namespace gf {
 
@@ -31,7 +36,7 @@ struct MarchParams {
   int net_from_occ;         // network cell = occupancy cell >> net_shift per axis (see gf_api.cu)
   int net_shift[3];
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
-  int pair;           // rounds run in pairs (2s, 2s+1): placed and evaluated together, composited in order
+  int group;          // rounds per group (1, 2 or 4): placed by G passes, evaluated together, composited in order
   int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
   int64_t n_cells;
   int64_t march_threads;
@@ -51,8 +56,8 @@ struct RayState {
   float4* dir;    // dx, dy, dz, seg_32
   float4* acc;    // r, g, b, transmittance
   u128* rng;      // PCG64 state of the word holding the ray's slot-0 float32 draw
-  uint32_t* run;  // queried samples of the ray in the last marched round (pairs: first | second << 16)
-  uint32_t* pend; // pairs: the second round's (queries | ess_skipped << 16), committed if the ray survives the first
+  uint32_t* run;  // queried samples of the ray in the last marched round (groups: one byte per round)
+  uint32_t* pend; // groups: [4] per ray, round p's (queries | ess_skipped << 16), committed if the ray survives rounds < p
   uint32_t* flags;  // GF_RAY_* bits | (rounds with candidate slots, bit r) << 8
   uint32_t* ivl;  // GF_MAX_IVL candidate slot ranges per ray (lo | hi << 16), from the coarse DDA
   uint4* denc;    // NULL, or 4 x uint4 per ray: gamma(d) as fp16 for the tensor-core MLP
