@@ -570,6 +570,10 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
   P.n_cells = nc;
   P.stride = stride;
   P.group = group;
+  {
+    const char* nf = getenv("GF_NO_FUSE");
+    P.fuse = group > 1 && !(nf && nf[0] == '1');
+  }
   P.stratified = cfg->stratified ? 1 : 0;
   P.ert = cfg->epsilon > 0.0 ? 1 : 0;
   P.eps_f64 = cfg->eps_compare_f64 ? 1 : 0;
@@ -694,7 +698,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
     const int step = P.group;
     for (int r = 0; r < P.n_rounds; r += step) {
       int passes = 0;
-      for (int p = 0; p < step && r + p < P.n_rounds; ++p, ++passes)
+      for (int p = 0; p < step && r + p < P.n_rounds; p += P.fuse ? step : 1, ++passes)
         k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r + p, p);
       stage_mark(s, GF_STAGE_MARCH, passes);
       stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, step > 1 ? P.chunk : 0,

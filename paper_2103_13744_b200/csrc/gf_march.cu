@@ -546,97 +546,10 @@ __device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v)
 // march pass r: composite round r-1 (+ERT), then place / skip / emit round r.
 // At r == n_rounds: composite the last round and write the final colours.
 // -------------------------------------------------------------------------
-// 7 CTAs/SM (<= 72 registers): measured faster than the unconstrained 85
-// registers despite a few spilled bytes
-__global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
-  const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
-  const bool in_range = i < P.n_rays;
-  uint32_t fw = in_range ? R.flags[i] : 0u;  // flags | candidate-round mask << 8
-  const uint32_t fw0 = fw;
-  const bool final_pass = round >= P.n_rounds;
-  if (!final_pass && !__any_sync(0xffffffffu, fw & GF_RAY_ALIVE)) return;
-
-  // ---- composite the previous round (render.py:333-337), float32, no
-  // contraction; only rays that queried samples then have anything to blend.
-  // Grouped rounds (P.group = G > 1): rounds G*s .. G*s+G-1 are placed by G
-  // marcher passes and evaluated by one K2 + MLP pass, then composited here
-  // in order with the ERT check after each; a ray that dies inside the group
-  // drops the later rounds' samples and their deferred counters, exactly as
-  // if those rounds had never run.
-  float4 acc = make_float4(0.f, 0.f, 0.f, 1.f);
-  const uint32_t had_bits = (fw & GF_RAY_ALIVE) ? (fw & GF_RAY_HAD_ALL) : 0u;
-  const bool had = phase == 0 && had_bits != 0;
-  unsigned long long commit_q = 0, commit_s = 0;
-  if (had) {
-    acc = R.acc[i];
-    const float seg = R.dir[i].w;
-    const uint64_t base = (uint64_t)i * (uint64_t)P.stride;
-    const uint32_t run = R.run[i];
-    const uint64_t pol_first = gf_pol_first();
-    auto blend = [&](uint64_t b0, uint32_t n) {
-      float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
-      for (uint32_t j = 0; j < n; ++j) {
-        float4 q = gf_ld_hint(B.res + b0 + j, pol_first);
-        float a = -expm1f(__fmul_rn(-q.w, seg));
-        float w = __fmul_rn(tr, a);
-        tr = __fmul_rn(tr, __fsub_rn(1.0f, a));
-        sr = __fadd_rn(sr, __fmul_rn(w, q.x));
-        sg = __fadd_rn(sg, __fmul_rn(w, q.y));
-        sb = __fadd_rn(sb, __fmul_rn(w, q.z));
-      }
-      acc.x = __fadd_rn(acc.x, __fmul_rn(acc.w, sr));
-      acc.y = __fadd_rn(acc.y, __fmul_rn(acc.w, sg));
-      acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
-      acc.w = __fmul_rn(acc.w, tr);
-    };
-    // one blend site (keeps the marcher's registers down).  Part p is round
-    // round - G + p; the ERT check after it counts a termination if round
-    // p + 1 exists (render.py:338-343).  Transmittance only moves in rounds
-    // with samples, so other rays cannot cross epsilon.
-    const int G = P.group;
-    bool dead = false;
-#pragma unroll 1
-    for (int part = 0; part < G && !dead; ++part) {
-      const int c = round - G + part;  // the composited round
-      if (part > 0 && c < P.n_rounds && (had_bits & gf_had_below(part))) {
-        // the round really ran for this ray: its deferred counters stand
-        const uint32_t pend = R.pend[4 * (uint64_t)i + part];
-        commit_q += pend & 0xFFFFu;
-        commit_s += pend >> 16;
-      }
-      if (!(had_bits & gf_had_bit(part))) continue;
-      blend(base + (uint64_t)part * (uint64_t)P.chunk, G == 1 ? run : ((run >> (8 * part)) & 0xFFu));
-      if (P.ert) {
-        dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
-        if (dead) {
-          fw &= ~(uint32_t)GF_RAY_ALIVE;
-          if ((int64_t)(c + 1) * P.chunk < P.k) fw |= GF_RAY_TERMINATED;  // rounds remained
-        }
-      }
-    }
-    R.acc[i] = acc;
-  }
-  if (P.group > 1) {
-    warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], commit_q);
-    warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], commit_s);
-  }
-  if (phase == 0) fw &= ~(uint32_t)GF_RAY_HAD_ALL;
-
-  if (final_pass) {
-    if (in_range) {
-      if (!had) acc = R.acc[i];
-      // render.py:345-348: acc + trans*bg, clip to [0,1]
-      float c0 = __fadd_rn(acc.x, __fmul_rn(acc.w, P.bg[0]));
-      float c1 = __fadd_rn(acc.y, __fmul_rn(acc.w, P.bg[1]));
-      float c2 = __fadd_rn(acc.z, __fmul_rn(acc.w, P.bg[2]));
-      P.rgb_out[3 * i + 0] = fminf(fmaxf(c0, 0.f), 1.f);
-      P.rgb_out[3 * i + 1] = fminf(fmaxf(c1, 0.f), 1.f);
-      P.rgb_out[3 * i + 2] = fminf(fmaxf(c2, 0.f), 1.f);
-    }
-    warp_add_u64(&P.stats[GF_STAT_ERT_TERMINATED], (fw & GF_RAY_TERMINATED) ? 1ull : 0ull);
-    return;
-  }
-
+// one round's sampling for the marcher's ray i (render.py:311-330): placement,
+// ESS, histogram ranks, staging records, counters; `fw` is the ray's flag word
+__device__ __forceinline__ void march_sample(const MarchParams& P, const RayState& R, const RoundBufs& B, int64_t i,
+                                             uint32_t& fw, int round, int phase) {
   // ---- sample round r (render.py:311-330)
   const int s0 = round * P.chunk;
   const int m = min(P.chunk, P.k - s0);
@@ -651,10 +564,7 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
   const uint32_t half = (uint32_t)phase * (uint32_t)P.chunk;   // staging offset of the group's round
   warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (alive && !active && !defer) ? (unsigned long long)m : 0ull);
   if (defer && !active) R.pend[4 * (uint64_t)i + phase] = (uint32_t)m << 16;
-  if (!__any_sync(0xffffffffu, active)) {
-    if (in_range && fw != fw0) R.flags[i] = fw;
-    return;
-  }
+  if (!__any_sync(0xffffffffu, active)) return;
   float4 o = active ? R.org[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   float4 d = active ? R.dir[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   u128 S = 0, inc = 0;
@@ -888,7 +798,6 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
     fw |= gf_had_bit(phase);
   }
   if (defer && active) R.pend[4 * (uint64_t)i + phase] = kept | ((uint32_t)(m - (int)kept) << 16);
-  if (in_range && fw != fw0) R.flags[i] = fw;
   {  // compact list of rays with queried samples (once per group), for the scatter kernel
     const bool emit = active && kept > 0 && !earlier;
     const unsigned em = __ballot_sync(0xffffffffu, emit);
@@ -901,6 +810,105 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
   }
   warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], defer ? 0ull : (unsigned long long)kept);
   warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (active && !defer) ? (unsigned long long)(m - (int)kept) : 0ull);
+}
+
+// 7 CTAs/SM (<= 72 registers): measured faster than the unconstrained 85
+// registers despite a few spilled bytes
+__global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
+  const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const bool in_range = i < P.n_rays;
+  uint32_t fw = in_range ? R.flags[i] : 0u;  // flags | candidate-round mask << 8
+  const uint32_t fw0 = fw;
+  const bool final_pass = round >= P.n_rounds;
+  if (!final_pass && !__any_sync(0xffffffffu, fw & GF_RAY_ALIVE)) return;
+
+  // ---- composite the previous round (render.py:333-337), float32, no
+  // contraction; only rays that queried samples then have anything to blend.
+  // Grouped rounds (P.group = G > 1): rounds G*s .. G*s+G-1 are placed by G
+  // marcher passes and evaluated by one K2 + MLP pass, then composited here
+  // in order with the ERT check after each; a ray that dies inside the group
+  // drops the later rounds' samples and their deferred counters, exactly as
+  // if those rounds had never run.
+  float4 acc = make_float4(0.f, 0.f, 0.f, 1.f);
+  const uint32_t had_bits = (fw & GF_RAY_ALIVE) ? (fw & GF_RAY_HAD_ALL) : 0u;
+  const bool had = phase == 0 && had_bits != 0;
+  unsigned long long commit_q = 0, commit_s = 0;
+  if (had) {
+    acc = R.acc[i];
+    const float seg = R.dir[i].w;
+    const uint64_t base = (uint64_t)i * (uint64_t)P.stride;
+    const uint32_t run = R.run[i];
+    const uint64_t pol_first = gf_pol_first();
+    auto blend = [&](uint64_t b0, uint32_t n) {
+      float tr = 1.0f, sr = 0.f, sg = 0.f, sb = 0.f;
+      for (uint32_t j = 0; j < n; ++j) {
+        float4 q = gf_ld_hint(B.res + b0 + j, pol_first);
+        float a = -expm1f(__fmul_rn(-q.w, seg));
+        float w = __fmul_rn(tr, a);
+        tr = __fmul_rn(tr, __fsub_rn(1.0f, a));
+        sr = __fadd_rn(sr, __fmul_rn(w, q.x));
+        sg = __fadd_rn(sg, __fmul_rn(w, q.y));
+        sb = __fadd_rn(sb, __fmul_rn(w, q.z));
+      }
+      acc.x = __fadd_rn(acc.x, __fmul_rn(acc.w, sr));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(acc.w, sg));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(acc.w, sb));
+      acc.w = __fmul_rn(acc.w, tr);
+    };
+    // one blend site (keeps the marcher's registers down).  Part p is round
+    // round - G + p; the ERT check after it counts a termination if round
+    // p + 1 exists (render.py:338-343).  Transmittance only moves in rounds
+    // with samples, so other rays cannot cross epsilon.
+    const int G = P.group;
+    bool dead = false;
+#pragma unroll 1
+    for (int part = 0; part < G && !dead; ++part) {
+      const int c = round - G + part;  // the composited round
+      if (part > 0 && c < P.n_rounds && (had_bits & gf_had_below(part))) {
+        // the round really ran for this ray: its deferred counters stand
+        const uint32_t pend = R.pend[4 * (uint64_t)i + part];
+        commit_q += pend & 0xFFFFu;
+        commit_s += pend >> 16;
+      }
+      if (!(had_bits & gf_had_bit(part))) continue;
+      blend(base + (uint64_t)part * (uint64_t)P.chunk, G == 1 ? run : ((run >> (8 * part)) & 0xFFu));
+      if (P.ert) {
+        dead = P.eps_f64 ? ((double)acc.w < P.epsilon) : (acc.w < (float)P.epsilon);
+        if (dead) {
+          fw &= ~(uint32_t)GF_RAY_ALIVE;
+          if ((int64_t)(c + 1) * P.chunk < P.k) fw |= GF_RAY_TERMINATED;  // rounds remained
+        }
+      }
+    }
+    R.acc[i] = acc;
+  }
+  if (P.group > 1) {
+    warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], commit_q);
+    warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], commit_s);
+  }
+  if (phase == 0) fw &= ~(uint32_t)GF_RAY_HAD_ALL;
+
+  if (final_pass) {
+    if (in_range) {
+      if (!had) acc = R.acc[i];
+      // render.py:345-348: acc + trans*bg, clip to [0,1]
+      float c0 = __fadd_rn(acc.x, __fmul_rn(acc.w, P.bg[0]));
+      float c1 = __fadd_rn(acc.y, __fmul_rn(acc.w, P.bg[1]));
+      float c2 = __fadd_rn(acc.z, __fmul_rn(acc.w, P.bg[2]));
+      P.rgb_out[3 * i + 0] = fminf(fmaxf(c0, 0.f), 1.f);
+      P.rgb_out[3 * i + 1] = fminf(fmaxf(c1, 0.f), 1.f);
+      P.rgb_out[3 * i + 2] = fminf(fmaxf(c2, 0.f), 1.f);
+    }
+    warp_add_u64(&P.stats[GF_STAT_ERT_TERMINATED], (fw & GF_RAY_TERMINATED) ? 1ull : 0ull);
+    return;
+  }
+
+  // ---- sample this pass's round(s): with P.fuse the whole group of rounds
+  // is placed by this one pass, else one round per launch (phase)
+  const int nsub = P.fuse ? min(P.group, P.n_rounds - round) : 1;
+#pragma unroll 1
+  for (int sub = 0; sub < nsub; ++sub) march_sample(P, R, B, i, fw, round + sub, phase + sub);
+  if (in_range && fw != fw0) R.flags[i] = fw;
 }
 
 }  // namespace gf

@@ -37,6 +37,7 @@ struct MarchParams {
   int net_shift[3];
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
   int group;          // rounds per group (1, 2 or 4): placed by G passes, evaluated together, composited in order
+  int fuse;           // one marcher launch places all of a group's rounds
   int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
   int64_t n_cells;
   int64_t march_threads;
