@@ -475,11 +475,11 @@ static int group_size(const gf_march_cfg_t* cfg, int64_t n_rays, bool allow_env 
   int g = n_rounds >= 2 ? 2 : 1;
   if (allow_env) {
     const char* e = getenv("GF_GROUP");
-    if (e && (e[0] == '1' || e[0] == '2' || e[0] == '4')) g = e[0] - '0';
-    while (g > n_rounds && g > 1) g /= 2;
+    if (e && e[0] >= '1' && e[0] <= '4') g = e[0] - '0';
+    if (g > n_rounds) g = n_rounds;
   }
   if (cfg->ert_chunk > 32) g = 1;
-  while (g > 1 && (double)n_rays * g * cfg->ert_chunk >= 4.0e9) g /= 2;
+  while (g > 1 && (double)n_rays * g * cfg->ert_chunk >= 4.0e9) --g;
   return g;
 }
 

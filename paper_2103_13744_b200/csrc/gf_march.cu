@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
     // GR rounds per group (one count byte each); cum = prefix counts after
     // rounds 0, 1, 2 of the group, one byte each
     const uint32_t c1 = rv & 0xFFu, c2 = c1 + ((rv >> 8) & 0xFFu), c3 = c2 + ((rv >> 16) & 0xFFu);
-    const uint32_t nr = GR == 1 ? rv : (GR == 2 ? c2 : c3 + (rv >> 24));
+    const uint32_t nr = GR == 1 ? rv : (GR == 2 ? c2 : (GR == 3 ? c3 : c3 + (rv >> 24)));
     const uint32_t cum = GR == 2 ? c1 : (c1 | (c2 << 8) | (c3 << 16));
     uint32_t incl = nr;
 #pragma unroll
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
         if (GR == 2) {
           const uint32_t a1 = __shfl_sync(0xffffffffu, cum, own);
           off = j < a1 ? j : (uint32_t)half + j - a1;
-        } else if (GR == 4) {
+        } else if (GR >= 3) {
           const uint32_t cu = __shfl_sync(0xffffffffu, cum, own);
           const uint32_t a1 = cu & 0xFFu, a2 = (cu >> 8) & 0xFFu, a3 = cu >> 16;
           off = j < a1 ? j
@@ -509,8 +509,9 @@ static int launch_place_g(const GfGrid& grid, const RoundBufs& RB, const uint32_
 
 int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
                  int stride, int half, int round, int64_t max_rows, cudaStream_t st) {
-  const int group = half > 0 ? stride / half : 1;  // rounds per group (1, 2 or 4)
+  const int group = half > 0 ? stride / half : 1;  // rounds per group (1 to 4)
   if (group == 4) return launch_place_g<4>(grid, RB, run, Bk, n_cells, stride, half, round, max_rows, st);
+  if (group == 3) return launch_place_g<3>(grid, RB, run, Bk, n_cells, stride, half, round, max_rows, st);
   if (group == 2) return launch_place_g<2>(grid, RB, run, Bk, n_cells, stride, half, round, max_rows, st);
   return launch_place_g<1>(grid, RB, run, Bk, n_cells, stride, 0, round, max_rows, st);
 }
