@@ -653,6 +653,19 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       }
     }
     __syncwarp();
+    // the record of the previous batch waiting for its cell rank
+    bool pend_ok = false;
+    uint32_t pend_raw = 0, pend_peers = 0;
+    int pend_leader = (int)lane;
+    uint64_t pend_addr = 0;
+    float pend_x = 0.f, pend_y = 0.f, pend_z = 0.f;
+    auto resolve = [&]() {  // warp-uniform
+      const uint32_t b = __shfl_sync(0xffffffffu, pend_raw, pend_leader);
+      if (pend_ok) {
+        const uint32_t crank = b + __popc(pend_peers & ((1u << lane) - 1u));
+        gf_st_hint(B.rec + pend_addr, make_float4(pend_x, pend_y, pend_z, __uint_as_float(crank)), gf_pol_last());
+      }
+    };
     for (uint32_t b0 = 0; b0 < total; b0 += 32) {
       const uint32_t k = b0 + lane;
       const bool has = k < total;
@@ -720,11 +733,29 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       // earlier in this batch + kept items of earlier batches
       const unsigned kb = __ballot_sync(0xffffffffu, keep);
       const unsigned same = __match_any_sync(0xffffffffu, has ? own : 32 + (int)lane);
-      const uint32_t crank = hist_rank(counts_r, keep, cell);
+      // issue this batch's warp-aggregated rank atomic now, consume it one
+      // batch later: the previous batch's records are stored meanwhile
+      uint32_t peers = 0, raw = 0;
+      int leader = (int)lane;
+      {
+        const unsigned act = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          peers = __match_any_sync(act, cell);
+          leader = __ffs(peers) - 1;
+          if ((int)lane == leader) raw = atomicAdd(&counts_r[cell], (uint32_t)__popc(peers));
+        }
+      }
+      resolve();
+      pend_ok = keep;
+      pend_raw = raw;
+      pend_peers = peers;
+      pend_leader = leader;
       if (keep) {
         const uint32_t pos = s_ray[wib][own].carry + __popc(kb & same & ((1u << lane) - 1u));
-        gf_st_hint(B.rec + (uint64_t)i_o * (uint64_t)P.stride + half + pos,
-                   make_float4(px, py, pz, __uint_as_float(crank)), gf_pol_last());
+        pend_addr = (uint64_t)i_o * (uint64_t)P.stride + half + pos;
+        pend_x = px;
+        pend_y = py;
+        pend_z = pz;
         if (P.trace) {
           unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
           if ((int64_t)slotpos < P.trace_capacity)
@@ -735,6 +766,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       if (has && (int)lane == 31 - __clz(same)) s_ray[wib][own].carry += __popc(kb & same);
       __syncwarp();
     }
+    resolve();  // the last batch's records
     kept = s_ray[wib][lane].carry;
   } else {
   double jd = (double)s0;
