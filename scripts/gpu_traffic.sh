@@ -4,7 +4,7 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 export PYTHONDONTWRITEBYTECODE=1
 TAG=${TAG:-traffic}
-for k in k_mlp_tc:12:12 k_march:13:13 k_place:12:12; do
+for k in k_mlp_tc:6:6 k_march:7:7 k_place:6:6; do  # launches per C2 frame with grouped rounds (G=2)
   IFS=: read name skip count <<< "$k"
   timeout 900 ncu --set full --clock-control none -k regex:$name -s $skip -c $count \
     -o gpurun_out/${TAG}_$name -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --clock-preroll 0 \
