@@ -350,3 +350,33 @@ def test_graph_reuse_across_views_bit_identical(gf, monkeypatch):
         img, st = gf.render_image(g, occ, cams[i % 3], cfg, seed=i, precision="fp16")
         assert np.array_equal(img, got[i][0])
         assert st.to_dict() | {"wall_ms": 0} == got[i][1].to_dict() | {"wall_ms": 0}
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not have_gpu(), reason="needs CUDA")
+@pytest.mark.parametrize("precision", ["fp16", "fp32"])
+def test_grouped_rounds_bit_identical(precision, monkeypatch):
+    """Rounds run in groups (GF_GROUP, default 2) with speculative placement
+    and per-round ERT at compositing: images and every RenderStats counter
+    must be bit-identical to one round at a time, on an ERT-heavy frame."""
+    import paper_2103_13744_b200 as gf
+
+    aabb = gf.Aabb((-1.0,) * 3, (1.0,) * 3)
+    grid = gf.init_network_grid(aabb, (16, 16, 16), seed=0, precision=precision)
+    grid.params.biases["density"][:] = 20.0
+    res, bits = toy_occupancy_bits()
+    occ = gf.OccupancyGrid(aabb, res, bits.copy())
+    cam = gf.sphere_cameras(aabb, 1, 96, seed=3)[0]
+    out = {}
+    for mode in ("1", "2", "3", "4", "2-nofuse"):
+        monkeypatch.setenv("GF_GROUP", mode[0])
+        monkeypatch.setenv("GF_NO_FUSE", "1" if mode.endswith("nofuse") else "0")
+        for cfg in (gf.RenderConfig(), gf.RenderConfig(k=200, ert_chunk=24)):
+            img, st = gf.render_image(grid, occ, cam, cfg, seed=7)
+            out.setdefault(cfg.k, []).append((mode, img, (st.total_queries, st.ess_skipped, st.ert_terminated_rays)))
+    for k, runs in out.items():
+        _, img0, st0 = runs[0]
+        assert st0[2] > 0  # the frame really terminates rays early
+        for mode, img, st in runs[1:]:
+            assert st == st0, (k, mode, st, st0)
+            assert np.array_equal(img, img0), (k, mode)
