@@ -147,3 +147,33 @@ def test_no_oracle_import_in_product():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "import oracle" not in text and "from oracle" not in text, f
+
+
+@pytest.mark.parametrize("pre,draws", [(0, 0), (0, 1), (0, 7), (1, 6), (3, 1000), (2, 3073)])
+def test_generator_advance_matches_numpy(pre, draws):
+    """train._advance_float32_draws leaves a numpy PCG64 Generator exactly
+    where rng.random(draws, float32) would (buffered 32-bit half included):
+    the host half of the device sample preparation (train.py:186)."""
+    from paper_2103_13744_b200 import train
+
+    a, b = np.random.default_rng(5), np.random.default_rng(5)
+    for r in (a, b):
+        r.random(pre, dtype=np.float32)
+    a.random(draws, dtype=np.float32)
+    bg, st = train._pcg_state(b)
+    train._advance_float32_draws(bg, st, draws)
+    assert a.bit_generator.state == b.bit_generator.state
+    assert np.array_equal(a.random(9, dtype=np.float32), b.random(9, dtype=np.float32))
+    assert a.random() == b.random()
+
+
+def test_pcg_output_function_matches_numpy():
+    """train._xsl_rr is numpy's PCG64 output: one raw 64-bit draw."""
+    from paper_2103_13744_b200 import train
+
+    rng = np.random.default_rng(11)
+    st = rng.bit_generator.state["state"]
+    s, inc = st["state"], st["inc"]
+    mult = 0x2360ED051FC65DA44385DF649FCCF645
+    s1 = (s * mult + inc) % (1 << 128)
+    assert train._xsl_rr(s1) == int(rng.integers(0, 2**64, dtype=np.uint64, endpoint=False))
