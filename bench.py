@@ -73,6 +73,17 @@ def c4_desc(precision):
     }
 
 
+def bulk_inputs(n, seed):
+    """Reference bench.py:108-112 input recipe (BASELINE config 5): uniform
+    float32 positions in [-1, 1]^3, normalised float32 normal directions."""
+    rng = np.random.default_rng(seed)
+    span = np.float32(2.0)
+    pts = np.float32(-1.0) + rng.random((n, 3), dtype=np.float32) * span
+    dirs = rng.normal(size=(n, 3)).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    return pts, dirs
+
+
 def run_bulk(args, rank, world, local):
     """Config 5: 2^26 random points/directions (reference bench.py:108-112
     recipe) through the 16^3 bank per step, no compositing.  Inputs resident
@@ -80,7 +91,6 @@ def run_bulk(args, rank, world, local):
     import torch
 
     import paper_2103_13744_b200 as gf
-    from oracle import gridfield_oracle as O
     from paper_2103_13744_b200 import _native as N
 
     torch.cuda.set_device(local)
@@ -88,7 +98,7 @@ def run_bulk(args, rank, world, local):
     grid = gf.init_network_grid(gf.Aabb((-1.0,) * 3, (1.0,) * 3), (16, 16, 16), seed=0)
     precision = args.precision or "fp16"
     grid.precision = precision
-    pts, dirs = O.bulk_query_inputs(np.full(3, -1.0), np.ones(3), n, seed=1 + rank)  # input generator only
+    pts, dirs = bulk_inputs(n, seed=1 + rank)
     p_h, d_h = torch.from_numpy(pts).pin_memory(), torch.from_numpy(dirs).pin_memory()
     p_d, d_d = p_h.cuda(), d_h.cuda()
     rgb_h = torch.empty((n, 3), dtype=torch.float32).pin_memory()
