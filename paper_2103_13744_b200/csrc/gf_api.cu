@@ -46,6 +46,16 @@ int num_sms() {
 
 using namespace gf;
 
+// programmatic dependent launch between the frame's kernels (gf_common.cuh)
+bool gf_pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GF_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -699,7 +709,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
     for (int r = 0; r < P.n_rounds; r += step) {
       int passes = 0;
       for (int p = 0; p < step && r + p < P.n_rounds; p += P.fuse ? step : 1, ++passes)
-        k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, r + p, p);
+        gf_launch_pdl(k_march, dim3(march_blocks), dim3(128), 0, s, P, w.R, w.RB, r + p, p);
       stage_mark(s, GF_STAGE_MARCH, passes);
       stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, step > 1 ? P.chunk : 0,
                                                    r / step, (int64_t)n_rays * stride, s));
@@ -711,7 +721,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
       stage_mark(s, GF_STAGE_MLP, 1);
     }
     // final pass: composite the last group of rounds and write the colours
-    k_march<<<march_blocks, 128, 0, s>>>(P, w.R, w.RB, (P.n_rounds + step - 1) / step * step, 0);
+    gf_launch_pdl(k_march, dim3(march_blocks), dim3(128), 0, s, P, w.R, w.RB, (P.n_rounds + step - 1) / step * step, 0);
     stage_mark(s, GF_STAGE_MARCH, 1);
   };
   // graphs for the production (tensor-core) path; the fp32 reference mode,

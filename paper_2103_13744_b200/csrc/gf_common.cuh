@@ -233,3 +233,31 @@ template <typename T>
 __host__ __device__ __forceinline__ T gf_div_up(T a, T b) { return (a + b - 1) / b; }
 
 __host__ __device__ __forceinline__ size_t gf_align(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL) between the frame's kernels: the next
+// kernel of the round chain is launched early and its CTAs run their
+// independent setup while the previous kernel drains; gf_pdl_wait() (before
+// any read of the previous kernel's results) blocks until that kernel has
+// completed and its writes are visible.  Outside a PDL launch both are no-ops.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void gf_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void gf_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool gf_pdl_enabled();  // gf_api.cu: on unless GF_NO_PDL=1
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t gf_launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = gf_pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}

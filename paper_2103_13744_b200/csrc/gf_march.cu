@@ -341,6 +341,7 @@ template <bool SMEM, int GR>
 __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const uint32_t* __restrict__ run,
                                                BucketBufs Bk, int64_t n_cells, int stride, int half, int round) {
   extern __shared__ uint32_t s_scan[];  // [n_cells+1] row offsets, [n_cells+1] tile offsets
+  gf_pdl_wait();     // the marcher's histogram and records
   const uint32_t* counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
   const uint32_t* off = Bk.offsets;
   const int tid = threadIdx.x;
@@ -497,13 +498,15 @@ static int launch_place_g(const GfGrid& grid, const RoundBufs& RB, const uint32_
       cudaFuncSetAttribute(k_place<true, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 8193 * 4);
       attr = true;
     }
-    k_place<true, GR><<<num_sms() * 2, 512, smem, st>>>(grid, RB, run, Bk, n_cells, stride, half, round);
+    gf_launch_pdl(k_place<true, GR>, dim3(num_sms() * 2), dim3(512), smem, st, grid, RB, run, Bk, n_cells, stride, half,
+                  round);
     return 1;
   }
   BucketBufs b = Bk;
   b.counts = RB.counts + (size_t)(round & 1) * (size_t)n_cells;
   const int n = launch_scan_cells(b, n_cells, st, max_rows);  // offsets + tiles; clears this round's counts
-  k_place<false, GR><<<num_sms() * 2, 512, 0, st>>>(grid, RB, run, Bk, n_cells, stride, half, round);
+  gf_launch_pdl(k_place<false, GR>, dim3(num_sms() * 2), dim3(512), 0, st, grid, RB, run, Bk, n_cells, stride, half,
+                round);
   return n + 1;
 }
 
@@ -848,6 +851,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
 // 7 CTAs/SM (<= 72 registers): measured faster than the unconstrained 85
 // registers despite a few spilled bytes
 __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
+  gf_pdl_wait();     // the previous MLP / marcher pass
   const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   const bool in_range = i < P.n_rays;
   uint32_t fw = in_range ? R.flags[i] : 0u;  // flags | candidate-round mask << 8

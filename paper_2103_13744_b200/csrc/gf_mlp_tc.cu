@@ -363,6 +363,9 @@ __global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const u
   fence_before();
   __syncthreads();
   fence_after();
+  // setup above is private to this CTA (TMEM, barriers, constant tile): it
+  // overlaps the previous kernel's tail under PDL; its results are read below
+  gf_pdl_wait();
   const uint32_t tmem = *tmem_slot;
   const uint32_t wb = smem_u32(smem);
   uint8_t* Ag = smem + T::A(g);
@@ -630,7 +633,8 @@ static int tc_resident() {
 template <int W, class IO>
 static void launch_tc_w(const void* packed, const TileSched& S, const IO& io, cudaStream_t st) {
   using T = TcShape<W>;
-  k_mlp_tc<W, IO><<<num_sms() * tc_resident<W, IO>(), 256, T::SMEM, st>>>((const uint8_t*)packed, S, io);
+  gf_launch_pdl(k_mlp_tc<W, IO>, dim3(num_sms() * tc_resident<W, IO>()), dim3(256), (size_t)T::SMEM, st,
+                (const uint8_t*)packed, S, io);
 }
 
 bool prepare_mlp_tc(const LayerTable& t) {
