@@ -657,10 +657,11 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
       const unsigned gb = (unsigned)gf_div_up<int64_t>(nw, 128);
       uint32_t* t0 = reinterpret_cast<uint32_t*>(w.coarse_tmp);
       uint32_t* t1 = t0 + nw;
-      k_coarse_reduce_w<<<gb, 128, 0, s>>>(reinterpret_cast<const uint32_t*>(occ_bits), ores, cplan.f, cres, t0);
-      k_dilate_x<<<gb, 128, 0, s>>>(t0, t1, cres, cplan.radius);
-      k_dilate_yz<<<gb, 128, 0, s>>>(t1, t0, cres, cplan.radius, 1);
-      k_dilate_yz<<<gb, 128, 0, s>>>(t0, w.coarse_bits, cres, cplan.radius, 2);
+      gf_launch_pdl(k_coarse_reduce_w, dim3(gb), dim3(128), 0, s, reinterpret_cast<const uint32_t*>(occ_bits), ores,
+                    cplan.f, cres, t0);
+      gf_launch_pdl(k_dilate_x, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, t1, cres, cplan.radius);
+      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t1, t0, cres, cplan.radius, 1);
+      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, w.coarse_bits, cres, cplan.radius, 2);
     } else {
       k_coarse_reduce<<<(unsigned)gf_div_up<int64_t>(ncc, 256), 256, 0, s>>>(occ_bits, ores, cplan.f, cres,
                                                                               w.coarse_tmp);
@@ -695,15 +696,19 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
   // the frame's launch sequence (captured once into a CUDA graph per
   // argument set and replayed; eager when instrumented)
   auto enqueue = [&](cudaStream_t s) {
-    enqueue_coarse(s);
-    stage_open(s);
+    // memsets first, so the setup kernels and the round chain form one
+    // uninterrupted run of programmatic dependent launches
     cudaMemsetAsync(w.B.counts, 0, (size_t)2 * nc * 4, s);
     cudaMemsetAsync(w.RB.emit_count, 0, 2 * sizeof(uint32_t), s);
+    enqueue_coarse(s);
+    stage_open(s);
     if (P.stratified)
-      k_seed_blocks<<<(unsigned)gf_div_up<int64_t>(std::max<int64_t>({n_blocks, (int64_t)GF_RAY_BLOCK, 2ll * P.n_rounds}), 64),
-                      64, 0, s>>>(cfg->seed, first_block, ray_block_stride, n_blocks, cfg->k, cfg->ert_chunk, P.n_rounds,
-                                  w.seeds, w.jump, w.start, w.round_jump, w.block_ci);
-    k_ray_init<<<ray_blocks, 128, 0, s>>>(P, w.R);
+      gf_launch_pdl(k_seed_blocks,
+                    dim3((unsigned)gf_div_up<int64_t>(
+                        std::max<int64_t>({n_blocks, (int64_t)GF_RAY_BLOCK, 2ll * P.n_rounds}), 64)),
+                    dim3(64), 0, s, (uint64_t)cfg->seed, first_block, ray_block_stride, n_blocks, (int)cfg->k,
+                    (int)cfg->ert_chunk, (int)P.n_rounds, w.seeds, w.jump, w.start, w.round_jump, w.block_ci);
+    gf_launch_pdl(k_ray_init, dim3(ray_blocks), dim3(128), 0, s, P, w.R);
     stage_mark(s, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
     const int step = P.group;
     for (int r = 0; r < P.n_rounds; r += step) {

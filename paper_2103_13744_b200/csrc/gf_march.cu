@@ -21,6 +21,7 @@ namespace gf {
 __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_stride, int64_t n_blocks,
                               int k, int chunk, int n_rounds, u128* seeds, u128* jump, u128* start,
                               u128* round_jump, u128* block_ci) {
+  gf_pdl_wait();
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b == 0) {
     // LCG jump table: S_{n+d} = A^d S_n + (sum_{k<d} A^k) inc, d = 0..GF_JUMP_MAX
@@ -150,6 +151,7 @@ __device__ void coarse_intervals(const MarchParams& P, uint32_t* out, float ex, 
 // position.
 // -------------------------------------------------------------------------
 __global__ void k_ray_init(MarchParams P, RayState R) {
+  gf_pdl_wait();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P.n_rays) return;
   const int64_t g = global_ray(P, i);  // ray index within the render_rays call
@@ -248,6 +250,7 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
 // `radius` coarse cells (Chebyshev), stored as bits.
 // -------------------------------------------------------------------------
 __global__ void k_coarse_reduce(const uint8_t* __restrict__ occ_bits, int3 ores, int f, int3 cres, uint8_t* coarse) {
+  gf_pdl_wait();
   int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)cres.x * cres.y * cres.z;
   if (c >= n) return;
@@ -263,6 +266,7 @@ __global__ void k_coarse_reduce(const uint8_t* __restrict__ occ_bits, int3 ores,
 }
 
 __global__ void k_coarse_dilate(const uint8_t* __restrict__ coarse, int3 cres, int r, uint32_t* bits) {
+  gf_pdl_wait();
   int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one 32-bit word per thread
   const int64_t n = (int64_t)cres.x * cres.y * cres.z;
   if (w * 32 >= n) return;
@@ -284,6 +288,7 @@ __global__ void k_coarse_dilate(const uint8_t* __restrict__ coarse, int3 cres, i
 // Word-parallel variants (fine rows 32-bit aligned: occ res.x % (32*factor) == 0).
 // One thread = 32 coarse cells along x.
 __global__ void k_coarse_reduce_w(const uint32_t* __restrict__ fine, int3 ores, int f, int3 cres, uint32_t* out) {
+  gf_pdl_wait();
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int wpr = cres.x / 32;
   if (w >= (int64_t)wpr * cres.y * cres.z) return;
@@ -304,6 +309,7 @@ __global__ void k_coarse_reduce_w(const uint32_t* __restrict__ fine, int3 ores, 
 }
 
 __global__ void k_dilate_x(const uint32_t* __restrict__ in, uint32_t* out, int3 cres, int r) {
+  gf_pdl_wait();
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int wpr = cres.x / 32;
   if (w >= (int64_t)wpr * cres.y * cres.z) return;
@@ -316,6 +322,7 @@ __global__ void k_dilate_x(const uint32_t* __restrict__ in, uint32_t* out, int3 
 
 // axis 1: y (stride = words per row), axis 2: z (stride = words per plane)
 __global__ void k_dilate_yz(const uint32_t* __restrict__ in, uint32_t* out, int3 cres, int r, int axis) {
+  gf_pdl_wait();
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int wpr = cres.x / 32;
   if (w >= (int64_t)wpr * cres.y * cres.z) return;
