@@ -46,6 +46,7 @@ __device__ __forceinline__ uint2 block_exclusive_scan2(uint2 v, uint2* warp_tot,
 
 template <int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells) {
+  gf_pdl_wait();  // counts from the preceding pass (no-op outside a PDL launch)
   __shared__ uint2 warp_tot[NT / 32];
   extern __shared__ uint32_t s_toff[];  // per-cell first tile (n_cells + 1), when it fits
   const bool in_smem = B.scan_smem_cells >= n_cells;
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(NT) k_scan_cells(BucketBufs B, int64_t n_cells
 // tile list from the per-cell first-tile table, one thread per tile (binary
 // search over tile_off; empty cells share their successor's start)
 __global__ void __launch_bounds__(256) k_fill_tiles(BucketBufs B, int64_t n_cells) {
+  gf_pdl_wait();  // counts from the preceding pass (no-op outside a PDL launch)
   const uint32_t nt = *B.n_tiles;
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
     int64_t lo = 0, hi = n_cells;  // invariant: tile_off[lo] <= t < tile_off[hi]
@@ -127,11 +129,11 @@ int launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st, int
   const bool one_cta = n_cells <= smem_cells && max_rows <= (int64_t)1 << 20;
   b.scan_smem_cells = one_cta ? n_cells : 0;
   const size_t smem = one_cta ? (size_t)(n_cells + 1) * 4 : 0;
-  k_scan_cells<1024, 4><<<1, 1024, smem, st>>>(b, n_cells);
+  gf_launch_pdl(k_scan_cells<1024, 4>, dim3(1), dim3(1024), smem, st, b, n_cells);
   if (!one_cta) {
     const int64_t max_tiles = max_rows / GF_TILE_ROWS + n_cells + 1;
-    k_fill_tiles<<<(unsigned)std::min<int64_t>(gf_div_up<int64_t>(max_tiles, 256), (int64_t)num_sms() * 8), 256, 0,
-                   st>>>(b, n_cells);
+    gf_launch_pdl(k_fill_tiles, dim3((unsigned)std::min<int64_t>(gf_div_up<int64_t>(max_tiles, 256), (int64_t)num_sms() * 8)),
+                  dim3(256), 0, st, b, n_cells);
     return 2;
   }
   return 1;
