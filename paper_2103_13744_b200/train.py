@@ -139,9 +139,58 @@ def _scatter_flat(flat: np.ndarray, params: mlp.MlpParams):
         off += a.size
 
 
+class DeviceGrads(mlp.MlpParams):
+    """Parameter gradients resident on the device (one flat buffer in
+    MlpParams.arrays() order).  ``weights`` / ``biases`` are the reference's
+    host arrays, downloaded on first access; ``adam_update`` consumes the
+    device buffer directly, so a training step that never looks at the
+    gradients on the host moves none of them over PCIe."""
+
+    def __init__(self, arch, flat, shapes):
+        self.arch = arch
+        self._flat = flat
+        self._shapes = shapes  # [(kind, name, shape)] in arrays() order
+        self._w = self._b = None
+
+    @property
+    def materialized(self) -> bool:
+        return self._w is not None
+
+    def _materialize(self):
+        if self._w is None:
+            host = D.to_host(self._flat)  # the arrays view this pinned buffer
+            w, b, off = {}, {}, 0
+            for kind, name, shape in self._shapes:
+                n = int(np.prod(shape))
+                (w if kind == "w" else b)[name] = D.tracked(host[off : off + n].reshape(shape))
+                off += n
+            self._w, self._b = w, b
+            self._dev_flat = (mlp.MlpParams.fingerprint(self), self._flat)
+
+    @property
+    def weights(self):
+        self._materialize()
+        return self._w
+
+    @weights.setter
+    def weights(self, v):
+        self._w = v
+
+    @property
+    def biases(self):
+        self._materialize()
+        return self._b
+
+    @biases.setter
+    def biases(self, v):
+        self._b = v
+
+
 def device_flat(params: mlp.MlpParams):
     """Flat float32 device copy of ``params`` (arrays() order): the cached one
     when the host arrays are unchanged since it was made, else an upload."""
+    if isinstance(params, DeviceGrads) and not params.materialized:
+        return params._flat
     hit = getattr(params, "_dev_flat", None)
     if hit is not None and hit[0] == params.fingerprint():
         return hit[1]
@@ -179,12 +228,42 @@ def adam_update(params: mlp.MlpParams, grads: mlp.MlpParams, state: AdamState, l
     coef = (N.C.c_float * 8)(*[_f32(v) for v in (b1, 1.0 - b1, b2, 1.0 - b2, bc1, bc2, lr, eps)])
     if state._dev is None:
         state._dev = (device_flat(state._m).clone(), device_flat(state._v).clone())
+    buf, views = _pinned_home(params)
     p = device_flat(params)
     g = device_flat(grads)
     N.check(N.lib().gf_adam_update(N.ptr(p), N.ptr(g), N.ptr(state._dev[0]), N.ptr(state._dev[1]), p.numel(), coef,
                                    D.stream_handle()), "adam_update")
-    _scatter_flat(D.to_host(p), params)
+    # one DMA of the updated parameters straight into their (page-locked) host arrays
+    t = D.require_cuda()
+    buf.copy_(p, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    for v in views:
+        v._bump()  # written behind numpy's back: device caches must see a new version
     params._dev_flat = (params.fingerprint(), p)
+
+
+def _pinned_home(params: mlp.MlpParams):
+    """The parameter arrays, re-homed once into one page-locked flat buffer in
+    arrays() order (values preserved), so the optimizer's result lands in them
+    with a single DMA.  Re-homed again if the caller replaces an array."""
+    home = getattr(params, "_pinned_home", None)
+    if home is not None:
+        buf, views = home
+        cur = [a for _, a in params.arrays()]
+        if len(cur) == len(views) and all(a is v for a, v in zip(cur, views)):
+            return buf, views
+    t = D.require_cuda()
+    buf = t.empty((_flat_size(params),), dtype=t.float32, pin_memory=True)
+    host = buf.numpy()
+    views, off = [], 0
+    for (kind, name), a in list(params.arrays()):
+        v = D.TrackedArray(host[off : off + a.size].reshape(a.shape))
+        v[...] = a
+        (params.weights if kind == "w" else params.biases)[name] = v
+        views.append(v)
+        off += a.size
+    params._pinned_home = (buf, views)
+    return buf, views
 
 
 def _sum_squares(x_dev) -> "object":
@@ -324,19 +403,12 @@ def prepare_ray_samples(origins, directions, aabb: Aabb, k: int, stratified: boo
 
 
 def _grads_to_host(grid, gw, gb, flat) -> mlp.MlpParams:
-    """Host MlpParams of the gradients (one download); the device buffer rides
-    along for adam_update while the host arrays stay unmodified."""
-    specs = grid.arch.layers()
-    host = D.to_host(flat)  # the gradient arrays view this pinned buffer
-    w, b, off = {}, {}, 0
-    for s, gwl, gbl in zip(specs, gw, gb):
-        w[s.name] = host[off : off + gwl.numel()].reshape(tuple(gwl.shape))
-        off += gwl.numel()
-        b[s.name] = host[off : off + gbl.numel()].reshape(tuple(gbl.shape))
-        off += gbl.numel()
-    out = mlp.MlpParams(grid.arch, w, b)
-    out._dev_flat = (out.fingerprint(), flat)
-    return out
+    """The gradients as an MlpParams whose host arrays are downloaded only if
+    the caller reads them (DeviceGrads)."""
+    shapes = []
+    for s, gwl, gbl in zip(grid.arch.layers(), gw, gb):
+        shapes += [("w", s.name, tuple(gwl.shape)), ("b", s.name, tuple(gbl.shape))]
+    return DeviceGrads(grid.arch, flat, shapes)
 
 
 def photometric_loss_and_grads(model, samples: RaySamples, gt: np.ndarray, background, reg_weight: float = 0.0,
