@@ -368,9 +368,9 @@ def measure_train(gf, torch, aabb, occ, cam, reps=5, cpu=True):
     out = {"samples": q, "rays": len(pix), "k_train": cfg.k_train, "forward_kernel_ms": fwd_ms,
            "backward_kernel_ms": bwd_ms, "backward_tflops": flop * 2 / 3 / (bwd_ms * 1e-3) / 1e12,
            "api_step_ms": api_ms, "loss": loss,
-           "note": "api_step_ms = photometric_loss_and_grads + adam_update through the reference API: numpy "
-                   "gradients out and numpy parameters written back each step (2 x 101.8 MB over PCIe, pinned); "
-                   "Adam moments stay on the device"}
+           "note": "api_step_ms = photometric_loss_and_grads + adam_update through the reference API: the "
+                   "gradients stay on the device unless read (DeviceGrads); the numpy parameters are updated in "
+                   "place by one DMA into their page-locked storage; Adam moments stay on the device"}
     if cpu:
         from oracle import gridfield_oracle as O
         from oracle import train_oracle as T
