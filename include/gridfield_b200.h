@@ -222,6 +222,11 @@ GF_API int gf_render_rays_analytic(const gf_analytic_t* scene, const gf_grid_geo
                                    int64_t trace_capacity, int64_t* trace_count_dev, void* ws_dev, size_t ws_bytes,
                                    void* stream);
 
+/* Grouped-order rows of a query batch (batched.py:73-78 positions[order]):
+ * out[j] = float32(x[idx[j]]) for (n, 3) rows, x float32 or float64.       */
+GF_API int gf_gather_rows3(const void* x_dev, int32_t x_f64, const int64_t* idx_dev, int64_t n, float* out_dev,
+                           void* stream);
+
 /* --- occupancy.extract_occupancy (occupancy.py:94-128) ---------------------
  * Probe every cell of `occ` (box + resolution of the extraction) on its 3x3x3
  * lattice, clip into the box, threshold f64(density) > tau, and write the

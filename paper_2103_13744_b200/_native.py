@@ -123,6 +123,7 @@ _SIGS = {
     "gf_prepare_samples_write": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                            C.POINTER(C.c_uint64), C.c_int32, C.c_uint32, C.POINTER(GridGeom), _P, _P,
                                            _P, _P, _P, _P, _P, _P]),
+    "gf_gather_rows3": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, _P]),
     "gf_stage_timing": (C.c_int, [C.c_int32]),
     "gf_stage_times": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "gf_launch_count": (C.c_int64, []),

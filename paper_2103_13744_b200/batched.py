@@ -90,8 +90,9 @@ def grouped_forward_device(grid, layout: GroupedLayout, pos=None, dirs=None, pre
         pos = D.to_device(np.asarray(layout.positions, np.float32).reshape(-1, 3), t.float32)
     if dirs is None:
         dirs = D.to_device(np.asarray(layout.directions, np.float32).reshape(-1, 3), t.float32)
-    offs = D.to_device(np.asarray(layout.offsets, np.int64), t.int64)
-    order = D.to_device(np.asarray(layout.order, np.int64), t.int64)
+    offs = D.to_device(layout.offsets if D.is_tensor(layout.offsets) else np.asarray(layout.offsets, np.int64),
+                       t.int64)
+    order = D.to_device(layout.order if D.is_tensor(layout.order) else np.asarray(layout.order, np.int64), t.int64)
     rgb = D.empty((n, 3), t.float32)
     sigma = D.empty((n,), t.float32)
     ws = D.workspace(N.lib().gf_grouped_workspace_bytes(grid.n_cells, n))

@@ -22,6 +22,7 @@ void launch_group(const int64_t* keys, int64_t n, int64_t n_keys, int64_t* order
                   int64_t* err, void* ws, cudaStream_t st);
 void launch_bin_points(const GfGrid& g, const void* x, int f64, int64_t n, int64_t* flat, int64_t* err,
                        cudaStream_t st);
+void launch_gather_rows3(const void* x, int f64, const int64_t* idx, int64_t n, float* out, cudaStream_t st);
 void launch_occupied_at(const GfGrid& g, const uint8_t* bits, const void* x, int f64, int64_t n, uint8_t* out,
                         int64_t* err, cudaStream_t st);
 void launch_clip(const double* lo, const double* hi, const float* x, int64_t n, float* out, cudaStream_t st);
@@ -1071,6 +1072,12 @@ int gf_bin_points(const gf_grid_geom_t* grid, const void* x, int32_t x_f64, int6
   if (!valid_grid(grid) || n < 0) return fail(GF_ERR_INVALID, "gf_bin_points: bad grid");
   launch_bin_points(gf_make_grid(grid), x, x_f64, n, flat, err, (cudaStream_t)stream);
   return check_cuda("gf_bin_points");
+}
+
+int gf_gather_rows3(const void* x, int32_t x_f64, const int64_t* idx, int64_t n, float* out, void* stream) {
+  if (n < 0 || (n > 0 && (!x || !idx || !out))) return fail(GF_ERR_INVALID, "gf_gather_rows3: bad arguments");
+  launch_gather_rows3(x, x_f64, idx, n, out, (cudaStream_t)stream);
+  return check_cuda("gf_gather_rows3");
 }
 
 int gf_occupied_at(const gf_grid_geom_t* occ, const uint8_t* bits, const void* x, int32_t x_f64, int64_t n,

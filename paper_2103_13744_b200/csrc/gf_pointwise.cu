@@ -148,6 +148,23 @@ __global__ void k_gen_rays(gf_camera_t c, float* o, float* dir) {
 
 static unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// out[j] = float32(x[idx[j]]) for (n, 3) rows; x float32 or float64 (the
+// grouped layout of a query batch, batched.py:73-78, straight on the device)
+template <typename T>
+__global__ void k_gather_rows3(const T* __restrict__ x, const int64_t* __restrict__ idx, int64_t n, float* out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = idx[j];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out[3 * j + a] = (float)x[3 * s + a];
+  }
+}
+
+void launch_gather_rows3(const void* x, int f64, const int64_t* idx, int64_t n, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  if (f64) k_gather_rows3<double><<<blocks(n, 256), 256, 0, st>>>((const double*)x, idx, n, out);
+  else k_gather_rows3<float><<<blocks(n, 256), 256, 0, st>>>((const float*)x, idx, n, out);
+}
+
 void launch_bin_points(const GfGrid& g, const void* x, int f64, int64_t n, int64_t* flat, int64_t* err,
                        cudaStream_t st) {
   if (n <= 0) return;

@@ -411,6 +411,47 @@ def _grads_to_host(grid, gw, gb, flat) -> mlp.MlpParams:
     return DeviceGrads(grid.arch, flat, shapes)
 
 
+@dataclass
+class _DeviceLayout:
+    """GroupedLayout (batched.py:36-57) of a training batch, kept on the device."""
+
+    n_queries: int
+    order: object
+    offsets: object
+    pos: object   # (Q, 3) float32 rows in grouped order
+    dirs: object  # (Q, 3) float32
+
+
+def _device_layout(model, positions, directions) -> _DeviceLayout:
+    """group_by_network(QueryBatch(x, d, model.cell_index(x)), n_cells)
+    (batched.py:60-85, grid.py:44-45) without leaving the device: float64
+    binning, stable grouping, rows gathered in grouped order."""
+    from .core import raise_if_out_of_bounds
+
+    t = D.require_cuda()
+    x = np.asarray(positions)
+    f64 = x.dtype != np.float32
+    xd = D.to_device(x.reshape(-1, 3), t.float64 if f64 else t.float32)
+    q = int(xd.shape[0])
+    keys = D.empty((q,), t.int64)
+    err = D.err_slot()
+    N.check(N.lib().gf_bin_points(model.native_geom(), N.ptr(xd), int(f64), q, N.ptr(keys), N.ptr(err),
+                                  D.stream_handle()), "cell_index")
+    raise_if_out_of_bounds(err, x.reshape(-1, 3), model.aabb)
+    order = D.empty((q,), t.int64)
+    inverse = D.empty((q,), t.int64)
+    offsets = D.empty((model.n_cells + 1,), t.int64)
+    ws = D.workspace(N.lib().gf_group_workspace_bytes(q, model.n_cells))
+    N.check(N.lib().gf_group_by_key(N.ptr(keys), q, model.n_cells, N.ptr(order), N.ptr(inverse), N.ptr(offsets),
+                                    N.ptr(err), N.ptr(ws), ws.numel(), D.stream_handle()), "group_by_network")
+    dd = D.to_device(np.asarray(directions, np.float32).reshape(-1, 3), t.float32)
+    pos = D.empty((q, 3), t.float32)
+    dirs = D.empty((q, 3), t.float32)
+    N.check(N.lib().gf_gather_rows3(N.ptr(xd), int(f64), N.ptr(order), q, N.ptr(pos), D.stream_handle()), "gather")
+    N.check(N.lib().gf_gather_rows3(N.ptr(dd), 0, N.ptr(order), q, N.ptr(dirs), D.stream_handle()), "gather")
+    return _DeviceLayout(q, order, offsets, pos, dirs)
+
+
 def photometric_loss_and_grads(model, samples: RaySamples, gt: np.ndarray, background, reg_weight: float = 0.0,
                                want_grads: bool = True, sigma_noise: np.ndarray | None = None):
     """train.py:212-288 on the device: mean squared pixel error of the
@@ -418,9 +459,8 @@ def photometric_loss_and_grads(model, samples: RaySamples, gt: np.ndarray, backg
     _require_f32(model.params)
     t = D.require_cuda()
     b, k = samples.n_rays, samples.k
-    layout = group_by_network(QueryBatch(samples.positions, samples.directions, model.cell_index(samples.positions)),
-                              model.n_cells)
-    cache = grouped_forward_device(model, layout)
+    layout = _device_layout(model, samples.positions, samples.directions)
+    cache = grouped_forward_device(model, layout, layout.pos, layout.dirs)
     q = layout.n_queries
     ri = D.to_device(np.asarray(samples.ray_index, np.int64), t.int64)
     sl = D.to_device(np.asarray(samples.slot, np.int64), t.int64)
