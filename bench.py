@@ -15,9 +15,17 @@ Prints ONE JSON line on rank 0.
 
 from __future__ import annotations
 
+import os
+
+# The CPU legs (reference arm, cpu_baseline) run numpy/OpenBLAS on a thread
+# pool of host workers, as the reference's parallel_map does: one BLAS thread
+# per worker.  OpenBLAS sizes its pool when numpy is first imported, so this
+# must precede every numpy import (the GPU arm does no BLAS work).
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ[_v] = "1"
+
 import argparse
 import json
-import os
 import statistics
 import subprocess
 import sys
@@ -37,12 +45,16 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 PAPER_1080TI_MPIX_S = 800 * 800 / 26e-3 / 1e6  # PAPER.md:166 (26 ms/frame, GTX 1080 Ti), context only
 
 
-def workload_desc(precision):
+def workload_desc():
+    """The C2 frame (identical for both arms; at N>1 the frame is split
+    across the ranks by interleaved 4096-ray blocks and NCCL-gathered, C3)."""
     return {
         "workload": "C2: 800x800 frame, 16^3 grid of 32-wide tiny MLPs (random init, seed 0), toy-scene "
                     "occupancy 256^3 (tau=10, 10.81% occupied), K=384, eps=0.01, ert_chunk=32, stratified, seed 0",
-        "image": [SIZE, SIZE], "grid": [16, 16, 16], "k": 384, "mlp_precision": precision,
-        "views": "sphere_cameras(aabb, 64, 800, seed=0)[rank]",
+        "image": [SIZE, SIZE], "grid": [16, 16, 16], "k": 384,
+        "view": "sphere_cameras(aabb, 64, 800, seed=0)[0]",
+        "multi_gpu": "N>1: the frame's 4096-ray blocks interleaved across ranks (shard_rays), NCCL all-gather of "
+                     "the shards + unshard + 4-counter all-reduce inside the step (render_image_distributed)",
         "l2": "flushed between timed frames (256 MiB write outside the timed window)",
     }
 
@@ -229,9 +241,10 @@ class ClockSampler:
 # reference arm / CPU baseline: the oracle port of the reference algorithm
 # ---------------------------------------------------------------------------
 def cpu_render_sample(cam, block_stride: int, workers: int):
-    """Render every `block_stride`-th 4096-ray block of the frame with the
-    reference algorithm (oracle port, numpy) on `workers` threads.
-    Returns (seconds, rays, queries)."""
+    """Render every `block_stride`-th 4096-ray block of the frame (1 = the
+    whole frame) with the reference algorithm (oracle port of render.py:
+    287-400, numpy, one OpenBLAS thread per worker as SURVEY §8d
+    prescribes) on `workers` threads.  Returns (seconds, rays, queries)."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import gridfield_oracle as O
@@ -263,28 +276,37 @@ def cpu_workers():
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port, pinned
+    bit-identical to the reference by tests/test_oracle_golden.py) renders
+    the WHOLE C2 frame (157 blocks) per step on every host core.  Warm-up
+    steps render one block per worker (they only warm the thread pool and
+    caches).  Timed steps stop early once --ref-budget-s is spent; `steps`
+    then reports the frames actually timed."""
     if rank != 0:
         return 0
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     import paper_2103_13744_b200 as gf
 
     _, _, _, cams = build_inputs(gf)
     workers = cpu_workers()
-    stride = args.cpu_block_stride
+    n_blocks = (SIZE * SIZE + 4095) // 4096
     for _ in range(args.warmup):
-        cpu_render_sample(cams[0], stride * 4, workers)
-    times, rays = [], 0
+        cpu_render_sample(cams[0], max(1, n_blocks // workers), workers)
+    times, rays, t_start = [], 0, time.perf_counter()
     for _ in range(args.steps):
-        dt, r, _ = cpu_render_sample(cams[0], stride, workers)
+        dt, r, _ = cpu_render_sample(cams[0], 1, workers)
         times.append(dt)
         rays = r
-    mpix = rays / statistics.median(times) / 1e6
-    sample = f"every {stride}th 4096-ray block of the C2 frame ({rays} rays), numpy oracle port, {workers} threads"
+        if time.perf_counter() - t_start > args.ref_budget_s:
+            break
+    ms = 1e3 * statistics.mean(times)
+    mpix = rays / (ms * 1e-3) / 1e6
+    sample = (f"the whole C2 frame per step ({rays} rays, {n_blocks} blocks of 4096), numpy oracle port of the "
+              f"reference algorithm, {workers} worker threads x 1 OpenBLAS thread; {len(times)} timed frames")
     line = {
-        "impl": "reference", "metric": METRIC, "value": mpix, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * SIZE * SIZE / (mpix * 1e6),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 sample placement / f32 MLP",
-        "data": "synthetic", "config": workload_desc("fp32 numpy"),
+        "impl": "reference", "metric": METRIC, "value": mpix, "unit": UNIT, "n_gpus": world, "steps": len(times),
+        "steps_requested": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 sample placement / f32 MLP",
+        "data": "synthetic", "config": workload_desc(),
         "cpu_baseline": {"value": mpix, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": mpix, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -390,10 +412,13 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default=None, choices=[None, "fp16", "fp32"])
-    ap.add_argument("--cpu-block-stride", type=int, default=8)
+    ap.add_argument("--precision", default=None, choices=[None, "fp16", "fp32"],
+                    help="MLP precision (default: the library default render_image uses)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="reference arm: stop timing whole frames after this many seconds")
     ap.add_argument("--clock-preroll", type=float, default=0.6, help="seconds of untimed load before the timed frames")
+    ap.add_argument("--no-extras", action="store_true", help="skip the extract / training side measurements")
     ap.add_argument("--workload", default="c2", choices=["c2", "c4", "c5"],
                     help="c2: the BASELINE metric's frame (default, the driver's line); c4: 32^3 lattice of "
                          "64-wide MLPs at 1920x1080; c5: 2^26-point bulk query (extra measurements)")
@@ -412,45 +437,51 @@ def main():
 
     import paper_2103_13744_b200 as gf
     from paper_2103_13744_b200 import _native as N
+    from paper_2103_13744_b200.render import ShardedFrame, render_image_distributed, render_rays_device
 
     torch.cuda.set_device(local)
     if world > 1:
+        if rank == 0:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator log: N ranks, NVLS/P2P transport
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.workload == "c4":
         aabb, grid, occ, cam = build_c4(gf)
     else:
         aabb, grid, occ, cams = build_inputs(gf)
-        cam = cams[rank % len(cams)]
+        cam = cams[0]
     n_pix = cam.width * cam.height
     cfg = gf.RenderConfig()
-    precision = args.precision
-    if precision is None:
-        try:
-            grid.device_params("fp16")
-            precision = "fp16"
-        except Exception:  # noqa: BLE001 -- tensor-core path not built: report the fp32 kernel instead
-            precision = "fp32"
-    grid.precision = precision
+    if args.precision:
+        grid.precision = args.precision
+    precision = grid.resolved_precision(render=True)  # what render_image(grid, occ, cam, cfg) runs
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    gathered = torch.empty((world, n_pix, 3), dtype=torch.float32, device="cuda") if world > 1 else None
-    out = torch.empty((n_pix, 3), dtype=torch.float32, device="cuda")
-    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    frame = ShardedFrame(n_pix, rank, world, torch.device("cuda", local)) if world > 1 else None
+    n_local = frame.n_local if frame else n_pix
+    out = torch.empty((n_pix, 3), dtype=torch.float32, device="cuda") if frame is None else None
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda") if frame is None else frame.stats
     ws = torch.empty(N.lib().gf_render_workspace_bytes(grid.native_arch(), grid.native_geom(), cfg.native(0),
-                                                       n_pix), dtype=torch.uint8, device="cuda")
+                                                       n_local), dtype=torch.uint8, device="cuda")
 
     def step():
-        stats.zero_()
-        gf.render.render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats, ws=ws)
-        if gathered is not None:
-            dist.all_gather_into_tensor(gathered, out)
+        """One frame: the whole view at N=1; at N>1 this rank's interleaved
+        blocks of the view, then the NCCL gather (render_image_distributed's
+        device path with preallocated buffers)."""
+        if frame is None:
+            stats.zero_()
+            render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats, ws=ws)
+        else:
+            render_image_distributed(grid, occ, cam, cfg, 0, frame=frame, ws=ws)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if world > 1:
+        os.environ["NCCL_DEBUG"] = "WARN"
 
     # ---- device-timed region (value)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    g0 = N.graph_counters()
     with ClockSampler(local) as clk:
         # pre-roll under the same load so nvidia-smi (>=100 ms period) has
         # samples spanning the timed window even when K frames take < 100 ms
@@ -462,6 +493,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = N.lib().gf_launch_count()
+        g0 = N.graph_counters()
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             ev[i][0].record(stream)
@@ -469,6 +501,7 @@ def main():
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         launches = N.lib().gf_launch_count() - launches0
+        g1 = N.graph_counters()
         if world > 1:
             dist.barrier()
     per = [a.elapsed_time(b) for a, b in ev]
@@ -477,16 +510,23 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = world * n_pix / (ms * 1e-3) / 1e6
-    queries = int(stats[0].item())
+    value = n_pix / (ms * 1e-3) / 1e6
+    queries = int(stats[0].item())  # global after the gather at N>1
+    graphs = {k: g1[k] - g0[k] for k in g1}
 
-    # ---- stage breakdown + roofline (separate frames with stage events on)
+    # ---- stage breakdown + roofline (separate frames with stage events on;
+    # this rank's share of the frame at N>1)
     N.lib().gf_stage_timing(1)
     n_prof = max(3, min(args.steps, 5))
+    st_local = torch.zeros(4, dtype=torch.int64, device="cuda")
     for _ in range(n_prof):
         flush.fill_(1)
-        stats.zero_()
-        gf.render.render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=stats, ws=ws)
+        st_local.zero_()
+        if frame is None:
+            render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=st_local, ws=ws)
+        else:
+            render_rays_device(grid, occ, cfg, 0, cam=cam, ray_offset=frame.offset, n_rays=frame.n_local,
+                               block_stride=frame.stride, out=frame.local[: frame.n_local], stats=st_local, ws=ws)
     torch.cuda.synchronize()
     st_ms, st_n = N.stage_times()
     N.lib().gf_stage_timing(0)
@@ -494,18 +534,20 @@ def main():
     st_n = {k: v // n_prof for k, v in st_n.items()}
     peaks, peak_src = load_peaks()
     flops_per_q = gf.count_flops(grid.arch)
-    R, Q, rounds = n_pix, queries, (cfg.k + cfg.ert_chunk - 1) // cfg.ert_chunk
+    R, Q, rounds = n_local, int(st_local[0].item()), (cfg.k + cfg.ert_chunk - 1) // cfg.ert_chunk
     cell_bytes = 2 * grid.arch.parameter_count() if precision == "fp16" else 4 * grid.arch.parameter_count()
-    algo = {  # SURVEY.md §8(d) per-unit figures x units per frame (DESIGN.md §roofline)
+    algo = {  # SURVEY.md §8(d) per-unit figures x units per frame (DESIGN.md §5)
         "mlp_flop": Q * flops_per_q,
         "mlp_bytes": Q * 36 + (791 if args.workload == "c2" else grid.n_cells) * cell_bytes,
         "march_bytes": Q * 40 + R * 12 + R * 16 * rounds + int(np.prod(occ.resolution)) // 8,
-        "scatter_bytes": Q * 20,
+        "scatter_bytes": Q * 48,
     }
     mlp_tflops = algo["mlp_flop"] / (st_ms["mlp"] * 1e-3) / 1e12 if st_ms["mlp"] > 0 else 0.0
     march_gbs = algo["march_bytes"] / (st_ms["march"] * 1e-3) / 1e9 if st_ms["march"] > 0 else 0.0
     scatter_gbs = algo["scatter_bytes"] / (st_ms["scatter"] * 1e-3) / 1e9 if st_ms["scatter"] > 0 else 0.0
-    peak_t = peaks["bf16_tflops_sustained"]
+    # the frame's kernels run for ~1 ms at max clock: the burst tensor peak is
+    # the denominator (the sustained figure is for seconds-long GEMM runs)
+    peak_t = peaks["bf16_tflops"]
     stage_roof = {
         "mlp": {"bound": "tensor", "achieved": mlp_tflops, "peak": peak_t, "unit": "TFLOP/s",
                 "frac": mlp_tflops / peak_t, "ms_per_frame": st_ms["mlp"], "launches_per_frame": st_n["mlp"]},
@@ -517,29 +559,33 @@ def main():
                     "launches_per_frame": st_n["scatter"]},
         "scan": {"ms_per_frame": st_ms["scan"], "launches_per_frame": st_n["scan"]},
         "setup": {"ms_per_frame": st_ms["setup"], "launches_per_frame": st_n["setup"]},
+        "queries_this_rank": Q, "rays_this_rank": R,
     }
     dominant = max(("mlp", "march", "scatter"), key=lambda k: st_ms[k])
     traffic = None
     tfile = ROOT / "profiles" / "ncu_traffic.json"
-    if tfile.exists():
+    if tfile.exists() and world == 1:
         try:
-            traffic = json.loads(tfile.read_text()).get(f"{dominant}_{precision}")
+            traffic = json.loads(tfile.read_text()).get(f"{args.workload}_{dominant}_{precision}")
         except Exception:  # noqa: BLE001
             traffic = None
     d = stage_roof[dominant]
     roofline = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"],
-                "frac": d["frac"], "traffic": traffic, "kernel": dominant, "peak_source": peak_src}
+                "frac": d["frac"], "traffic": traffic, "kernel": dominant,
+                "peak_source": f"{peak_src} ({'bf16_tflops burst' if d['bound'] == 'tensor' else 'hbm_gbs'})"}
 
-    # ---- end-to-end through the public API (numpy camera in, numpy image out)
+    # ---- end-to-end through the public API (camera in, numpy image out)
     e2e_times = []
     for i in range(args.steps + 1):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        img, st = gf.render_image(grid, occ, cam, cfg, seed=0)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, torch.from_numpy(img.reshape(-1, 3)).cuda(non_blocking=True))
+        if world == 1:
+            img, st = gf.render_image(grid, occ, cam, cfg, seed=0)
+        else:
+            img_d, st = render_image_distributed(grid, occ, cam, cfg, seed=0)
+            img = img_d.cpu().numpy() if rank == 0 else None
             torch.cuda.synchronize()
         if i:  # first call re-validates caches; not counted
             e2e_times.append(time.perf_counter() - t0)
@@ -548,15 +594,17 @@ def main():
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": world * n_pix / e2e_s / 1e6, "unit": UNIT,
+    e2e = {"value": n_pix / e2e_s / 1e6, "unit": UNIT,
            "h2d_bytes_per_step": int(N.C.sizeof(N.CameraT) + N.C.sizeof(N.MarchCfg)),
-           "d2h_bytes_per_step": int(img.nbytes + 32), "ms_per_frame": e2e_s * 1e3}
-    if args.workload == "c2":
+           "d2h_bytes_per_step": int(n_pix * 12 + 32), "ms_per_frame": e2e_s * 1e3,
+           "api": "render_image(grid, occ, cam, RenderConfig(), seed=0)" if world == 1 else
+                  "render_image_distributed(...) + image to host on rank 0"}
+    if args.workload == "c2" and world == 1:
         # the C3 view batch through the same API, a different camera every frame
         # (each new view updates the cached frame graph in place)
         views = gf.sphere_cameras(aabb, 64, SIZE, seed=0)
         vt = []
-        for v in views[rank::world] if world > 1 else views:
+        for v in views:
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             gf.render_image(grid, occ, v, cfg, seed=0)
@@ -565,30 +613,30 @@ def main():
                         "max_ms_per_frame": max(vt) * 1e3}
 
     extract = train_step = None
-    if args.workload == "c2" and rank == 0:
+    if args.workload == "c2" and rank == 0 and world == 1 and not args.no_extras:
         extract = measure_extract(gf, torch, aabb, occ)
-        train_step = measure_train(gf, torch, aabb, occ, cam, cpu=world == 1 and not args.no_cpu_baseline)
+        train_step = measure_train(gf, torch, aabb, occ, cam, cpu=not args.no_cpu_baseline)
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, N=1 only): the whole frame, all host cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "c2":
-        os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
         workers = cpu_workers()
-        dt, rays, _ = cpu_render_sample(cam, args.cpu_block_stride, workers)
+        dt, rays, _ = cpu_render_sample(cam, 1, workers)
         cpu = {"value": rays / dt / 1e6, "unit": UNIT, "cores": workers, "kind": "port",
-               "sample": f"every {args.cpu_block_stride}th 4096-ray block of the same frame ({rays} rays), "
-                         f"numpy oracle port of the reference algorithm, {workers} threads, {dt:.1f}s"}
+               "sample": f"the whole C2 frame ({rays} rays), numpy oracle port of the reference algorithm, "
+                         f"{workers} worker threads x 1 OpenBLAS thread, {dt:.1f} s"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f16" if precision == "fp16" else "f32",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f16" if precision == "fp16" else "f32", "mlp_precision": precision,
             "data": "synthetic (random-init 16^3 lattice, analytic toy-scene occupancy)",
-            "config": workload_desc(precision) if args.workload == "c2" else c4_desc(precision),
+            "config": workload_desc() if args.workload == "c2" else c4_desc(precision),
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
-            "gpu_launches": int(launches),
-            "queries_per_frame": queries, "mlp_samples_per_s": queries / (st_ms["mlp"] * 1e-3) if st_ms["mlp"] else None,
+            "gpu_launches": int(launches), "graphs_in_timed_region": graphs,
+            "queries_per_frame": queries, "mlp_samples_per_s": Q / (st_ms["mlp"] * 1e-3) if st_ms["mlp"] else None,
             "stage_roofline": stage_roof, "paper_1080ti_mpix_s_context": PAPER_1080TI_MPIX_S,
             "occupancy_extract": extract, "training_step": train_step,
         }

@@ -321,6 +321,12 @@ enum { GF_STAGE_SETUP = 0, GF_STAGE_MARCH = 1, GF_STAGE_SCAN = 2, GF_STAGE_SCATT
 GF_API int gf_stage_timing(int32_t enable);
 GF_API int gf_stage_times(double* ms_out, int64_t* launches_out);
 GF_API int64_t gf_launch_count(void);
+/* CUDA-graph activity of gf_render_rays since process start: {replays of a
+ * cached graph, in-place exec updates (new camera/seed/buffers), fresh
+ * instantiations, eager runs because the stream could not be captured}.
+ * Calls on the legacy default stream (0) run their graph on a per-thread
+ * side stream ordered by events.                                           */
+GF_API int gf_graph_counters(int64_t out4[4]);
 
 /* --- host-side helpers (no device work) ---------------------------------- */
 /* PCG64(SeedSequence([seed, block_start])).state as {state_hi, state_lo,

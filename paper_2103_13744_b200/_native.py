@@ -127,9 +127,17 @@ _SIGS = {
     "gf_stage_timing": (C.c_int, [C.c_int32]),
     "gf_stage_times": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "gf_launch_count": (C.c_int64, []),
+    "gf_graph_counters": (C.c_int, [_P]),
 }
 
 STAGES = ("setup", "march", "scan", "scatter", "mlp")
+
+
+def graph_counters() -> dict:
+    """CUDA-graph activity of gf_render_rays since process start."""
+    out = (C.c_int64 * 4)()
+    check(lib().gf_graph_counters(C.addressof(out)), "gf_graph_counters")
+    return dict(zip(("replays", "updates", "instantiations", "eager"), (int(v) for v in out)))
 
 
 def stage_times() -> tuple[dict, dict]:

@@ -148,23 +148,69 @@ static uint64_t g_graph_tick = 0;
 // A new argument set with the launch structure of a cached graph (a new
 // camera, seed or output buffer) is captured and applied to that graph with
 // cudaGraphExecUpdate, which costs far less than a fresh instantiation.
+// graph activity (gf_graph_counters): replays of a cached exec, in-place
+// updates of a cached exec, fresh instantiations, eager fallbacks
+static std::atomic<int64_t> g_graph_replays{0}, g_graph_updates{0}, g_graph_instantiations{0}, g_graph_eager{0};
+
+// The legacy default stream (handle 0, what torch's default stream is)
+// cannot be captured.  Calls on it run their graph on a per-thread,
+// per-device side stream instead, ordered after the caller's earlier work
+// and before its later work by two events.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t in = nullptr, out = nullptr;
+};
+
+struct StreamScope {
+  cudaStream_t user, run;
+  SideStream* side = nullptr;
+  StreamScope(cudaStream_t st, int dev) : user(st), run(st) {
+    if (st != nullptr && st != cudaStreamLegacy) return;
+    static thread_local std::vector<SideStream> per_dev;
+    if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1);
+    SideStream& ss = per_dev[dev];
+    if (!ss.s) {
+      if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ss.in, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ss.out, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        ss = SideStream{};
+        return;  // no side stream: the caller's stream is used (eager)
+      }
+    }
+    side = &ss;
+    cudaEventRecord(ss.in, st);
+    cudaStreamWaitEvent(ss.s, ss.in, 0);
+    run = ss.s;
+  }
+  ~StreamScope() {
+    if (!side) return;
+    cudaEventRecord(side->out, run);
+    cudaStreamWaitEvent(user, side->out, 0);
+  }
+};
+
 template <class F>
-static int run_graph(const GraphKey& k, const GraphKey& topo, cudaStream_t st, F&& enqueue) {
+static int run_graph(const GraphKey& k, const GraphKey& topo, cudaStream_t user_st, F&& enqueue) {
   int dev = 0;
   cudaGetDevice(&dev);
+  StreamScope scope(user_st, dev);
+  cudaStream_t st = scope.run;
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
     for (auto& e : g_graphs)
       if (e.dev == dev && e.key == k.b) {
         e.last_use = ++g_graph_tick;
         g_launches += e.launches;
+        ++g_graph_replays;
         cudaGraphLaunch(e.exec, st);
         return check_cuda("gf_render_rays (graph replay)");
       }
   }
   const int64_t l0 = g_launches.load();
   if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-    cudaGetLastError();  // stream cannot be captured (e.g. legacy default stream): run eagerly
+    cudaGetLastError();  // stream cannot be captured: run eagerly
+    ++g_graph_eager;
     enqueue(st);
     return check_cuda("gf_render_rays");
   }
@@ -182,6 +228,7 @@ static int run_graph(const GraphKey& k, const GraphKey& topo, cudaStream_t st, F
         e.key = k.b;
         e.last_use = ++g_graph_tick;
         g_launches += e.launches;
+        ++g_graph_updates;
         cudaGraphLaunch(e.exec, st);
         return check_cuda("gf_render_rays (graph update)");
       }
@@ -194,6 +241,7 @@ static int run_graph(const GraphKey& k, const GraphKey& topo, cudaStream_t st, F
   cudaGraphDestroy(g);
   if (err != cudaSuccess) return fail(GF_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(err));
   cudaGraphLaunch(ex, st);
+  ++g_graph_instantiations;
   {
     std::lock_guard<std::mutex> lk(g_graph_mu);
     if (g_graphs.size() >= 8) {
@@ -730,9 +778,8 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
     gf_launch_pdl(k_march, dim3(march_blocks), dim3(128), 0, s, P, w.R, w.RB, (P.n_rounds + step - 1) / step * step, 0);
     stage_mark(s, GF_STAGE_MARCH, 1);
   };
-  // graphs for the production (tensor-core) path; the fp32 reference mode,
-  // traces and stage timing run eagerly
-  const bool use_graph = (an || precision == GF_PRECISION_FP16) && !g_timer.on && !trace && !getenv("GF_NO_GRAPH");
+  // every precision replays a cached graph; traces and stage timing run eagerly
+  const bool use_graph = !g_timer.on && !trace && !getenv("GF_NO_GRAPH");
   if (!use_graph) {
     enqueue(st);
     return check_cuda("gf_render_rays");
@@ -1157,6 +1204,15 @@ int gf_stage_times(double* ms_out, int64_t* launches_out) {
 }
 
 int64_t gf_launch_count(void) { return g_launches.load(); }
+
+int gf_graph_counters(int64_t out4[4]) {
+  if (!out4) return fail(GF_ERR_INVALID, "gf_graph_counters: null output");
+  out4[0] = g_graph_replays.load();
+  out4[1] = g_graph_updates.load();
+  out4[2] = g_graph_instantiations.load();
+  out4[3] = g_graph_eager.load();
+  return GF_OK;
+}
 
 int gf_pcg64_block_state(uint64_t seed, uint64_t block_start, uint64_t out4[4]) {
   u128 s, inc;

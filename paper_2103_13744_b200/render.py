@@ -323,7 +323,7 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
     t = D.require_cuda()
     analytic = _is_analytic(grid)
     if not analytic:
-        p = grid.resolved_precision(precision)
+        p = grid.resolved_precision(precision, render=True)
         packed = grid.device_params(p)
     if cam is not None:
         total = cam.width * cam.height
@@ -415,34 +415,89 @@ def render_image(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0
     return host.numpy().reshape(cam.height, cam.width, 3), stats
 
 
+def shard_capacity(n_rays: int, world: int) -> int:
+    """Rows of each rank's padded shard buffer (whole 4096-ray blocks)."""
+    n_blocks = (n_rays + RAY_BLOCK - 1) // RAY_BLOCK
+    return ((n_blocks + world - 1) // world) * RAY_BLOCK
+
+
+class ShardedFrame:
+    """Buffers of one rank's part of a multi-GPU frame of ``n_rays`` rays.
+
+    Rank r renders the interleaved 4096-ray blocks of ``shard_rays`` into
+    ``local[:n_local]`` (each block keeps its own jitter stream, render.py:
+    371-375, so any split reproduces the single-GPU image bit for bit);
+    ``gather`` all-gathers the padded shards, restores image order
+    (``unshard_index``) into ``image`` and sums the 4 ``RenderStats``
+    counters across ranks.  The collective is the only exchange (SURVEY
+    §8e).  Works on CUDA tensors over NCCL and on CPU tensors over gloo."""
+
+    def __init__(self, n_rays: int, rank: int, world: int, device=None, channels: int = 3):
+        import torch
+
+        self.n_rays, self.rank, self.world = int(n_rays), int(rank), int(world)
+        self.offset, self.stride, self.n_local = shard_rays(self.n_rays, self.rank, self.world)
+        self.cap = shard_capacity(self.n_rays, self.world)
+        dev = device if device is not None else torch.device("cpu")
+        self.local = torch.zeros((self.cap, channels), dtype=torch.float32, device=dev)
+        self.gathered = torch.empty((self.world * self.cap, channels), dtype=torch.float32, device=dev)
+        self.image = torch.empty((self.n_rays, channels), dtype=torch.float32, device=dev)
+        self.index = torch.from_numpy(unshard_index(self.n_rays, self.world)).to(dev)
+        self.stats = torch.zeros(4, dtype=torch.int64, device=dev)
+
+    def gather(self, group=None):
+        """All-gather the shards and assemble the frame (``image``, ``stats``)."""
+        import torch
+        import torch.distributed as dist
+
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(self.gathered, self.local, group=group)
+        else:
+            dist.all_gather(list(self.gathered.view(self.world, self.cap, -1).unbind(0)), self.local, group=group)
+        torch.index_select(self.gathered, 0, self.index, out=self.image)
+        dist.all_reduce(self.stats, group=group)
+        return self.image, self.stats
+
+
+_dist_ctx = threading.local()
+
+
 def render_image_distributed(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0, group=None,
-                             precision=None):
+                             precision=None, frame: ShardedFrame | None = None, ws=None):
     """Multi-GPU render_image (one process per GPU, torch.distributed/NCCL).
 
     Each rank marches its interleaved 4096-ray blocks (``shard_rays``) with the
     blocks' own jitter streams, so the assembled image is bit-identical to the
     single-GPU render; the only exchange is one all-gather of the shards
-    (float32 RGB) plus a 4-counter all-reduce.  Returns the (H, W, 3) image
-    as a CUDA tensor on every rank and the global RenderStats."""
+    (float32 RGB) plus a 4-counter all-reduce (``ShardedFrame.gather``).
+    Returns the (H, W, 3) image as a CUDA tensor on every rank and the global
+    RenderStats."""
     import torch.distributed as dist
 
-    t = D.require_cuda()
+    D.require_cuda()
     grid = _field_grid(field)
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     n = cam.width * cam.height
-    off, stride, n_local = shard_rays(n, rank, world)
-    n_blocks = (n + RAY_BLOCK - 1) // RAY_BLOCK
-    cap = ((n_blocks + world - 1) // world) * RAY_BLOCK
-    buf = t.zeros((cap, 3), dtype=t.float32, device=D.device())
-    st = t.zeros(4, dtype=t.int64, device=buf.device)
-    if n_local:
-        render_rays_device(grid, occupancy, cfg, seed, cam=cam, ray_offset=off, n_rays=n_local, block_stride=stride,
-                           precision=precision, out=buf[:n_local], stats=st)
-    gathered = t.empty((world * cap, 3), dtype=t.float32, device=buf.device)
-    dist.all_gather_into_tensor(gathered, buf, group=group)
-    dist.all_reduce(st, group=group)
-    idx = t.from_numpy(unshard_index(n, world)).to(buf.device)
-    return gathered.index_select(0, idx).view(cam.height, cam.width, 3), _stats_from(st)
+    if frame is None:
+        cache = getattr(_dist_ctx, "frames", None)
+        if cache is None:
+            cache = _dist_ctx.frames = {}
+        key = (D.torch().cuda.current_device(), n, rank, world)
+        frame = cache.get(key)
+        if frame is None:
+            frame = cache[key] = ShardedFrame(n, rank, world, D.device())
+    frame.stats.zero_()
+    if frame.n_local:
+        if ws is None:
+            ws_bytes = _render_ws_bytes(grid, cfg.native(seed), frame.n_local)
+            ws = getattr(frame, "ws", None)
+            if ws is None or ws.numel() < ws_bytes:
+                ws = frame.ws = D.workspace(ws_bytes)
+        render_rays_device(grid, occupancy, cfg, seed, cam=cam, ray_offset=frame.offset, n_rays=frame.n_local,
+                           block_stride=frame.stride, precision=precision, out=frame.local[: frame.n_local],
+                           stats=frame.stats, ws=ws)
+    img, st = frame.gather(group)
+    return img.view(cam.height, cam.width, 3), _stats_from(st)
 
 
 def compute_psnr(a, b) -> float:

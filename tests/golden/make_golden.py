@@ -479,8 +479,48 @@ def gen_ckpt():
     print("wrote ckpt_small.gfckpt", (OUT / "ckpt_small.gfckpt").stat().st_size)
 
 
+C2_BLOCKS = (0, 40, 62, 70, 74, 76, 77, 78, 79, 80, 82, 84, 88, 96, 120, 156)
+
+
+def gen_c2():
+    """The benchmarked C2 frame (800x800, 16^3 random init seed 0, toy
+    occupancy 256^3, RenderConfig() defaults, seed 0), as random init and
+    with density bias 20 (ERT-heavy): full-frame RenderStats from
+    render_image, and colours + counters of sampled 4096-ray blocks (centre
+    blocks plus the ragged last one) from the reference's own _march_block
+    with the block's SeedSequence([seed, block_start]) stream."""
+    aabb = unit()
+    cam = scene.sphere_cameras(aabb, 64, 800, seed=0)[0]
+    occ = toy_occ(256)
+    cfg = render.RenderConfig()
+    o, d = render.generate_rays(cam)
+    o64, d64 = o.astype(np.float64), d.astype(np.float64)
+    out = dict(blocks=np.array(C2_BLOCKS, np.int64), **cam_arrays(cam))
+    for tag, bias in (("rand", None), ("bias20", 20.0)):
+        g = ggrid.init_network_grid(aabb, (16, 16, 16), seed=0)
+        if bias is not None:
+            g.params.biases["density"][:] = bias
+        t = time.time()
+        _, st = render.render_image(g, occ, cam, cfg, seed=0, workers=os.cpu_count())
+        print(f"  c2 {tag}: full frame {time.time() - t:.1f}s Q={st.total_queries} ess={st.ess_skipped} "
+              f"ert={st.ert_terminated_rays}")
+        out[f"{tag}_stats"] = np.array([st.total_queries, st.ess_skipped, st.ert_terminated_rays, st.n_rays], np.int64)
+        cols, bst = [], []
+        for b in C2_BLOCKS:
+            s0 = b * render.RAY_BLOCK
+            sl = slice(s0, min(s0 + render.RAY_BLOCK, len(o)))
+            rng = np.random.default_rng(np.random.SeedSequence([0, s0]))
+            c, _, bs = render._march_block(g, occ, o64[sl], d64[sl], cfg, rng)
+            cols.append(c.astype(np.float32))
+            bst.append([bs.total_queries, bs.ess_skipped, bs.ert_terminated_rays, bs.n_rays])
+        out[f"{tag}_block_rgb"] = np.concatenate(cols)
+        out[f"{tag}_block_stats"] = np.array(bst, np.int64)
+    save("render_c2", **out)
+
+
 def main():
-    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt", "extract", "train"]
+    what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt", "extract",
+                            "train", "c2"]
     for w in what:
         t = time.time()
         globals()[f"gen_{w}"]()

@@ -1,6 +1,7 @@
-"""Multi-process (world_size 2, gloo, CPU) checks of the sharding host logic:
-the interleaved block partition covers every ray exactly once, and the
-all-gather + unshard permutation reassembles image order."""
+"""Multi-process (world_size 2-3, gloo, CPU) checks of the sharding host
+logic: the interleaved block partition covers every ray exactly once, and
+ShardedFrame (render_image_distributed's all-gather + unshard + counter
+all-reduce) reassembles image order on every rank."""
 
 import os
 import socket
@@ -11,7 +12,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2103_13744_b200.render import RAY_BLOCK, shard_rays, unshard_index
+from paper_2103_13744_b200.render import RAY_BLOCK, ShardedFrame, shard_rays, unshard_index
 
 
 def _free_port():
@@ -39,37 +40,36 @@ def test_partition_covers_every_ray_once(n_rays, world):
 
 
 def _worker(rank, world, port, n_rays, out):
+    """Runs the product's ShardedFrame (the gather / unshard / counter
+    all-reduce of render_image_distributed) on gloo; the "render" of each
+    shard writes the global ray id of every local row (the map
+    global_ray() in gf_march.cuh implements on the device)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    off, stride, n_local = shard_rays(n_rays, rank, world)
-    n_blocks = (n_rays + RAY_BLOCK - 1) // RAY_BLOCK
-    cap = ((n_blocks + world - 1) // world) * RAY_BLOCK
-    buf = torch.full((cap, 3), -1.0, dtype=torch.float64)
-    i = torch.arange(n_local, dtype=torch.int64)
-    g = off + (i // RAY_BLOCK) * stride * RAY_BLOCK + i % RAY_BLOCK
-    buf[:n_local] = g.to(torch.float64)[:, None]  # "render" = global ray id
-    gathered = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(gathered, buf)
-    stats = torch.tensor([n_local], dtype=torch.int64)
-    dist.all_reduce(stats)
-    if rank == 0:
-        flat = torch.cat(gathered)
-        img = flat[torch.from_numpy(unshard_index(n_rays, world))][:, 0]
-        out.put((img.numpy(), int(stats.item())))
+    fr = ShardedFrame(n_rays, rank, world)
+    fr.local.fill_(-1.0)
+    i = torch.arange(fr.n_local, dtype=torch.int64)
+    g = fr.offset + (i // RAY_BLOCK) * fr.stride * RAY_BLOCK + i % RAY_BLOCK
+    fr.local[: fr.n_local] = g.to(torch.float32)[:, None] * torch.tensor([1.0, 2.0, 3.0])
+    fr.stats.copy_(torch.tensor([fr.n_local, 2 * fr.n_local, rank, 1]))
+    img, stats = fr.gather()
+    out.put((rank, img.numpy().copy(), stats.tolist()))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_rays,world", [(20_000, 2), (6400, 2)])
-def test_gloo_gather_reassembles_image_order(n_rays, world):
+@pytest.mark.parametrize("n_rays,world", [(20_000, 2), (6400, 2), (4096, 2), (13_000, 3)])
+def test_gloo_sharded_frame_reassembles_image_order(n_rays, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, n_rays, q)) for r in range(world)]
     for p in procs:
         p.start()
-    img, total = q.get(timeout=120)
+    res = [q.get(timeout=120) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert total == n_rays
-    assert np.array_equal(img, np.arange(n_rays, dtype=np.float64))
+    want = np.arange(n_rays, dtype=np.float32)[:, None] * np.array([1.0, 2.0, 3.0], np.float32)
+    for rank, img, stats in res:  # every rank holds the assembled frame and the global counters
+        assert np.array_equal(img, want), rank
+        assert stats == [n_rays, 2 * n_rays, sum(range(world)), world]
