@@ -203,12 +203,12 @@ __device__ __forceinline__ float gf_clip_fast(float p, float lo, float hi) { ret
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t gf_pol_last() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));  // pure: hoisted out of loops
   return p;
 }
 __device__ __forceinline__ uint64_t gf_pol_first() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ float4 gf_ld_hint(const float4* a, uint64_t pol) {

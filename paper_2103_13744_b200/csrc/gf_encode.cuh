@@ -80,9 +80,10 @@ __device__ __forceinline__ F2 f2_fma(F2 a, F2 b, F2 c) {
 __device__ __forceinline__ void sincos_scaled2(float x0, int k0, float x1, int k1, float* s0, float* c0, float* s1,
                                                float* c1) {
   const F2 a = f2_mul(f2(x0, x1), f2(__int_as_float(0x40490FDB + (k0 << 23)), __int_as_float(0x40490FDB + (k1 << 23))));
-  float t0, t1;
-  f2_split(f2_mul(a, f2(-0.15915494309189535f, -0.15915494309189535f)), t0, t1);
-  const F2 n = f2(rintf(t0), rintf(t1));
+  // n = -rint(a / 2pi): round to nearest even by the 1.5 * 2^23 shifter
+  // (|a / 2pi| <= 2^9 here), on the FMA pipe instead of two FRND on XU
+  const F2 M = f2(12582912.0f, 12582912.0f);
+  const F2 n = f2_sub(f2_add(f2_mul(a, f2(-0.15915494309189535f, -0.15915494309189535f)), M), M);
   F2 r = f2_fma(n, f2(6.28125f, 6.28125f), a);
   r = f2_fma(n, f2(1.9353071795864769e-3f, 1.9353071795864769e-3f), r);
   float r0, r1;
@@ -96,6 +97,17 @@ __device__ __forceinline__ void sincos_scaled2(float x0, int k0, float x1, int k
 __device__ __forceinline__ void double_angle2(F2& s, F2& c) {
   const F2 s2 = f2_mul(f2_add(s, s), c);
   c = f2_mul(f2_sub(c, s), f2_add(c, s));
+  s = s2;
+}
+
+// the same step in 4 paired ops: s' = (s + s) c, c' = fma(c, c, -s s).  An
+// error delta in (s, c) grows to at most ~2 delta per step, as above.
+__device__ __forceinline__ void double_angle2_fma(F2& s, F2& c) {
+  const F2 s2 = f2_mul(f2_add(s, s), c);
+  const F2 ss = f2_mul(s, s);
+  F2 nss;
+  asm("{\n\t.reg .b64 t;\n\tmov.b64 t, %1;\n\txor.b64 %0, t, 0x8000000080000000;\n\t}" : "=l"(nss.v) : "l"(ss.v));
+  c = f2_fma(c, c, nss);
   s = s2;
 }
 

@@ -3,30 +3,32 @@
 // Reference math: core.py:132-152 (encoding), mlp.py:222-266 (forward),
 // batched.py:120-151 (one network per segment).  Design:
 //
-//  * one CTA = 256 threads = two warpgroups working on TWO 128-row tiles of
-//    the same cell at once: group g owns tile slot g (its A operands, its
-//    TMEM columns, its MMA commit barrier and its own elected issuing
-//    thread); thread gt of a group owns row gt, which is TMEM lane gt, so
-//    every epilogue is a private tcgen05.ld of the thread's own accumulator
-//    row.  While the tensor core runs one group's layer the other group runs
-//    its epilogue, hiding the MMA / commit / barrier latency of the 5-layer
-//    dependency chain; groups synchronise with named barriers, the CTA only
-//    at tile-pair boundaries (weight reuse);
-//  * epilogues: FADD2 bias adds, F2FP.RELU packs, 16-byte operand stores;
-//    the render path's direction chunk gamma(d) is encoded once per ray by
-//    k_ray_init and copied, not recomputed per sample;
-//  * the cell's weights are pre-packed on the device (gf_pack_weights) into
-//    the exact shared-memory image the MMAs consume (fp16, K-major,
-//    no-swizzle canonical layout, fp32 biases) and brought in with ONE 1-D
-//    bulk TMA copy (cp.async.bulk + mbarrier complete_tx) only when the
-//    cell changes;
-//  * the 6 affine layers run as 5 chains of tcgen05.mma.kind::f16
-//    (M=128, N=32/32/48/32/16, K=64/32/32/64/32; density and feature share
-//    one N=48 MMA), fp32 accumulators in TMEM, activations round-trip only
-//    through shared memory (never HBM);
-//  * persistent CTAs walk contiguous tile ranges so consecutive tiles of the
-//    same cell reuse the staged weights; the next pair's row inputs are
-//    prefetched while the current pair's first MMAs run.
+//  * activations live in TENSOR MEMORY: every layer is a chain of
+//    tcgen05.mma.kind::f16 with the A operand (128 rows x K, fp16) read from
+//    TMEM and the B operand (the cell's weights) from shared memory.  With A
+//    in shared memory an M=128 x K=16 MMA moves 4 KB through the 128 B/clk
+//    shared-memory port (~51 cycles at N=32, measured: scripts/ubench_tmem.cu);
+//    from TMEM it runs at ~18 cycles, close to the N=32 floor of 16;
+//  * one CTA = NS warpgroups + 1 loader warp.  Warpgroup g owns TMEM slot g
+//    (SLOT columns: the accumulator D_L at [0, N_L), the A operand of layer L
+//    at ACOL_L) and runs its own stream of 128-row tiles; thread gt of a
+//    group owns row gt == TMEM lane gt, so every epilogue is a private
+//    tcgen05.ld of the thread's accumulator row, fp32 -> fp16 (+ReLU) packs
+//    and one tcgen05.st of the next layer's A row.  Groups never wait for
+//    each other: while one group's MMAs run the others run epilogues;
+//  * the CTA's contiguous tile range is cut into runs of one cell; the
+//    loader warp finds the runs and brings each run's packed weights (the
+//    exact shared-memory image of the B operands + bias tiles, k_pack_tc) into
+//    one of two buffers with one bulk TMA copy, so the next cell's weights
+//    arrive while the current run is evaluated.  Within a run group g takes
+//    tiles g, g+NS, ...; a per-buffer mbarrier (count NS) frees the buffer;
+//  * biases enter the accumulator through one K=16 MMA against a constant
+//    TMEM operand of ones (bias tile row n = [hi(b_n), lo(b_n), 0...], 22
+//    significant bits); density and feature share one N=W+16 MMA;
+//  * gamma(x) (core.py layout) is generated octave by octave (exactly
+//    reduced MUFU anchors + f32x2 double-angle steps) and flushed to TMEM
+//    4 columns (8 fp16) at a time; the render path's gamma(d) is encoded
+//    once per ray by k_ray_init and fetched while the first layers run.
 #include <cuda_fp16.h>
 
 #include <cstdio>
@@ -56,32 +58,47 @@ struct TcShape {
   static constexpr int B4 = B3 + N3 * K3 * 2;
   // bias operands: one K=16 tile per layer, row n = [hi(b_n), lo(b_n), 0 ...]
   // (fp16 hi + fp16 remainder: 22 significant bits); multiplied by the
-  // constant ONES tile (columns 0 and 1 = 1) they initialise the accumulator
+  // constant ONES operand (columns 0 and 1 = 1) they initialise the accumulator
   static constexpr int BB0 = B4 + N4 * K4 * 2;
   static constexpr int BB1 = BB0 + N0 * 32;
   static constexpr int BB2 = BB1 + N1 * 32;
   static constexpr int BB3 = BB2 + N2 * 32;
   static constexpr int BB4 = BB3 + N3 * 32;
   static constexpr int CELL_BYTES = ((BB4 + N4 * 32) + 1023) / 1024 * 1024;
-  static constexpr int ONES = CELL_BYTES;  // 128 x 16 fp16 constant A operand
-  // one A operand slot per tile, re-laid out in place layer by layer:
-  // gamma(x) (K0) -> h0 (K1) -> h1 (K2) -> [feat, gamma(d)] (K3) -> g (K4)
-  static constexpr int KA = K0 > K3 ? K0 : K3;
-  static constexpr int SLOT_BYTES = 128 * KA * 2;
-  static constexpr int A(int s) { return ONES + 4096 + s * SLOT_BYTES; }
-  static constexpr int BAR = A(2);  // mma[0], mma[1], weights, tmem base
-  // window of the CTA's tile descriptors (refilled at pair boundaries): tile
-  // reads at the top of each pair are shared-memory loads, not global ones
-  static constexpr int TILEBUF = BAR + 32;
-  static constexpr int TB = 64;
-  static constexpr int SMEM = TILEBUF + TB * 8;
-  static constexpr int NC = N2 <= 32 ? 32 : (N2 <= 64 ? 64 : (N2 <= 128 ? 128 : 256));  // TMEM cols per slot
-  static constexpr int TMEM_COLS = 2 * NC;
-#if GF_EXP == 10
-  static constexpr int CTAS_PER_SM = W == 32 ? 3 : 2;
-#else
-  static constexpr int CTAS_PER_SM = W == 32 ? 4 : 2;
+
+  // ---- TMEM slot of one tile (32-bit columns; fp16 A operands pack two
+  // K values per column, low half = even k).  Layer L reads A_L at ACOL_L
+  // and writes D_L at [0, N_L); the epilogue of L reads D_L completely before
+  // it writes A_{L+1}, so A_{L+1} may overlap D_L.
+  static constexpr int A0C = W, A1C = W, A2C = N2, A3C = W, A4C = W;
+  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+  static constexpr int SLOT =
+      cmax(cmax(A0C + K0 / 2, A1C + K1 / 2), cmax(cmax(A2C + K2 / 2, A3C + K3 / 2), A4C + K4 / 2));
+  static_assert(A0C >= N0 && A1C >= N1 && A2C >= N2 && A3C >= N3 && A4C >= N4, "A operand overlaps its layer's D");
+  static_assert(SLOT % 16 == 0, "slot columns");
+};
+
+// launch shape per width: warpgroups per CTA (TMEM slots), CTAs per SM
+#ifndef GF_TC_NS32
+#define GF_TC_NS32 3
 #endif
+#ifndef GF_TC_CTAS32
+#define GF_TC_CTAS32 2
+#endif
+template <int W>
+struct TcCfg {
+  static constexpr int NS = W == 32 ? GF_TC_NS32 : 2;
+  static constexpr int CTAS = W == 32 ? GF_TC_CTAS32 : 2;
+  static constexpr int THREADS = NS * 128 + 32;
+  static constexpr int ONES = NS * TcShape<W>::SLOT;  // 8 columns: [1, 1, 0 ...] fp16 per row
+  static constexpr int tmem_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
+  static constexpr int TMEM_COLS = tmem_cols(ONES + 8);
+  static_assert(ONES + 8 <= 512 && TMEM_COLS * CTAS <= 512, "TMEM budget");
+  // shared memory: two weight buffers, then barriers and the run table
+  static constexpr int BAR = 2 * TcShape<W>::CELL_BYTES;   // full[2], free[2], mma[NS]
+  static constexpr int TSLOT = BAR + 32 + 8 * NS;          // TMEM base address
+  static constexpr int RUNS = (TSLOT + 4 + 15) / 16 * 16;  // uint4 runs[2]: (cell, first tile, end tile, 0)
+  static constexpr int SMEM = RUNS + 32;
 };
 
 // byte offset of element (r, k) in a canonical K-major no-swizzle operand of
@@ -108,19 +125,30 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);   // M
 }
 
-__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+// D[tmem] (+)= A[tmem] . B[smem]
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n" : "+r"(pred));
+  return pred;
+}
+
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
 // parity wait with a suspend-time hint: the warp sleeps in the barrier unit
@@ -145,8 +173,8 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
 
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 #define GF_LD16(taddr, r)                                                                                      \
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
@@ -155,64 +183,40 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
                  "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),       \
                  "=r"(r[14]), "=r"(r[15])                                                                      \
                : "r"(taddr))
+#define GF_LD4(taddr, r)                                                   \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])             \
+               : "r"(taddr))
+#define GF_LD1(taddr, r) asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr))
+#define GF_ST4(taddr, a, b, c, d)                                                                       \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(a), "r"(b), \
+               "r"(c), "r"(d)                                                                           \
+               : "memory")
+#define GF_ST8(taddr, r)                                                                                        \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]), \
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])                       \
+               : "memory")
 
-// load N accumulator columns (multiple of 16) of this thread's row
-template <int N>
-__device__ __forceinline__ void tmem_load(uint32_t taddr, float* out) {
-  uint32_t r[N];
-#pragma unroll
-  for (int c = 0; c < N; c += 16) GF_LD16(taddr + c, (r + c));
-  tmem_wait_ld();
-#pragma unroll
-  for (int c = 0; c < N; ++c) out[c] = __uint_as_float(r[c]);
-}
-
-// accumulator columns [c0, c0 + N) of this thread's TMEM row -> fp16 (+ReLU)
-// into a canonical operand of K columns, 16 columns per TMEM load so only 16
-// accumulator registers are live
+// accumulator columns [0, N) of this thread's TMEM row -> fp16 (+ReLU) ->
+// the next layer's A row at column `acol` (two K values per column); 16
+// accumulator columns per load so only 16 fp32 values are live
 template <int N, bool RELU>
-__device__ __forceinline__ void tmem_to_operand(uint32_t trow, uint8_t* A, int K, int r) {
+__device__ __forceinline__ void epilogue_to_a(uint32_t trow, uint32_t acol) {
 #pragma unroll
   for (int c = 0; c < N; c += 16) {
-    float h[16];
-    tmem_load<16>(trow + c, h);
+    uint32_t r[16], o[8];
+    GF_LD16(trow + c, r);
+    tmem_wait_ld();
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const float* v = h + 8 * q;
-      uint4 o;
-      if (RELU) {
-        o = make_uint4(pack_h2_relu(v[0], v[1]), pack_h2_relu(v[2], v[3]), pack_h2_relu(v[4], v[5]),
-                       pack_h2_relu(v[6], v[7]));
-      } else {
-        o = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
-      }
-      *reinterpret_cast<uint4*>(A + canon_off(r, c + 8 * q, K)) = o;
+    for (int q = 0; q < 8; ++q) {
+      const float a = __uint_as_float(r[2 * q]), b = __uint_as_float(r[2 * q + 1]);
+      o[q] = RELU ? pack_h2_relu(a, b) : pack_h2(a, b);
     }
+    GF_ST8(trow + acol + c / 2, o);
   }
 }
 
-// fp16 store (+ReLU) of accumulator columns [0, N) of row r into a
-// canonical operand of K columns: per 8 columns four F2FP(.RELU) packs and
-// one 16-byte store (the bias is already in the accumulator)
-template <int N, bool RELU>
-__device__ __forceinline__ void pack_store(const float* h, uint8_t* A, int K, int r) {
-#pragma unroll
-  for (int c = 0; c < N / 8; ++c) {
-    const float* v = h + 8 * c;
-    uint4 o;
-    if (RELU) {
-      o = make_uint4(pack_h2_relu(v[0], v[1]), pack_h2_relu(v[2], v[3]), pack_h2_relu(v[4], v[5]),
-                     pack_h2_relu(v[6], v[7]));
-    } else {
-      o = make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
-    }
-    *reinterpret_cast<uint4*>(A + canon_off(r, 8 * c, K)) = o;
-  }
-}
-
-// one row's inputs (prefetched one pair ahead); the render path's direction
-// operand chunk (the ray's pre-encoded gamma(d), gf_encode.cuh) is fetched
-// separately while the trunk0 MMA runs
+// one row's inputs (prefetched one tile ahead within a run)
 struct RowIn {
   uint32_t idx, row;  // caller / staging index, sorted row
   bool valid;
@@ -229,18 +233,15 @@ __device__ __forceinline__ void load_row(const TileSched& S, const IO& io, uint2
   if (r.valid) io.template fetch<!IO::kDirEnc>(S, tl.y + (uint32_t)tid, r.idx, r.x, r.d);
 }
 
-
 // gamma(x) (core.py:132-152 layout: raw xyz, then per octave k sin xyz, cos
-// xyz; column 63 zero) generated octave by octave and flushed to the K0
-// operand one 8-column chunk at a time, so only ~14 values are live
-// gamma(x) (core.py:132-152 layout: raw xyz, then per octave k sin xyz, cos
-// xyz; column 63 zero).  Anchors k = 0, 3, 6, 9 (MUFU after exact
-// reduction), two double-angle steps after each of the first three; anchors
-// and chains run as f32x2 pairs, in octave order, and every completed
-// 8-column chunk is flushed to the K0 operand at once (few live registers).
+// xyz; column 63 zero).  Anchors at octaves 0 and 5 (MUFU after an exact
+// 2pi reduction, abs error <= 3.6e-7), four double-angle steps after each
+// (error at most doubles per step: <= 6e-6, against the 2.4e-4 fp16 operand
+// rounding), all as f32x2 pairs.  Octaves 0-4 are flushed to the A0 operand
+// in TMEM first (4 columns = 8 fp16 per store), then octaves 5-9, so few
+// values are live at once.
 template <int W>
-__device__ __forceinline__ void encode_position(uint8_t* A0, int tid, const float* x) {
-  using T = TcShape<W>;
+__device__ __forceinline__ void encode_position(uint32_t ta0, const float* x) {
   float e[64];
   e[0] = x[0]; e[1] = x[1]; e[2] = x[2];
   e[63] = 0.f;
@@ -250,15 +251,14 @@ __device__ __forceinline__ void encode_position(uint8_t* A0, int tid, const floa
   };
   auto flush = [&](int c) {
     const float* v = e + 8 * c;
-    *reinterpret_cast<uint4*>(A0 + canon_off(tid, 8 * c, T::K0)) =
-        make_uint4(pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
+    GF_ST4(ta0 + 4 * c, pack_h2(v[0], v[1]), pack_h2(v[2], v[3]), pack_h2(v[4], v[5]), pack_h2(v[6], v[7]));
   };
-  // two chains of two double-angle steps from anchors (ka, aa), (kb, ab)
+  // four double-angle steps of two chains from anchors (ka, aa), (kb, ab)
   auto chains = [&](int ka, int aa, float sa, float ca, int kb, int ab, float sb, float cb) {
     F2 sv = f2(sa, sb), cv = f2(ca, cb);
 #pragma unroll
-    for (int st = 1; st <= 2; ++st) {
-      double_angle2(sv, cv);
+    for (int st = 1; st <= 4; ++st) {
+      double_angle2_fma(sv, cv);
       float s0, s1, c0, c1;
       f2_split(sv, s0, s1);
       f2_split(cv, c0, c1);
@@ -267,35 +267,18 @@ __device__ __forceinline__ void encode_position(uint8_t* A0, int tid, const floa
     }
   };
   float s0, c0, s1, c1, s2, c2, s3, c3;
-  // octaves 0-2 (and z of 3-5)
+  // octaves 0-4 of x, y, z (and 5-9 of z)
   sincos_scaled2(x[0], 0, x[1], 0, &s0, &c0, &s1, &c1);
-  sincos_scaled2(x[2], 0, x[2], 3, &s2, &c2, &s3, &c3);
-  put(0, 0, s0, c0); put(0, 1, s1, c1); put(0, 2, s2, c2); put(3, 2, s3, c3);
+  sincos_scaled2(x[2], 0, x[2], 5, &s2, &c2, &s3, &c3);
+  put(0, 0, s0, c0); put(0, 1, s1, c1); put(0, 2, s2, c2); put(5, 2, s3, c3);
   chains(0, 0, s0, c0, 0, 1, s1, c1);
-  chains(0, 2, s2, c2, 3, 2, s3, c3);
-  flush(0); flush(1);
-  // octaves 3-5
-  sincos_scaled2(x[0], 3, x[1], 3, &s0, &c0, &s1, &c1);
-  put(3, 0, s0, c0); put(3, 1, s1, c1);
-  chains(3, 0, s0, c0, 3, 1, s1, c1);
-  flush(2); flush(3);
-  // octaves 6-8 (and z of 9)
-  sincos_scaled2(x[0], 6, x[1], 6, &s0, &c0, &s1, &c1);
-  sincos_scaled2(x[2], 6, x[2], 9, &s2, &c2, &s3, &c3);
-  put(6, 0, s0, c0); put(6, 1, s1, c1); put(6, 2, s2, c2); put(9, 2, s3, c3);
-  chains(6, 0, s0, c0, 6, 1, s1, c1);
-#pragma unroll
-  for (int st = 1; st <= 2; ++st) {  // 6z alone (scalar, same roundings)
-    const float sp = s2, cp = c2;
-    s2 = 2.0f * sp * cp;
-    c2 = (cp - sp) * (cp + sp);
-    put(6 + st, 2, s2, c2);
-  }
-  flush(4); flush(5); flush(6);
-  // octave 9
-  sincos_scaled2(x[0], 9, x[1], 9, &s0, &c0, &s1, &c1);
-  put(9, 0, s0, c0); put(9, 1, s1, c1);
-  flush(7);
+  chains(0, 2, s2, c2, 5, 2, s3, c3);
+  flush(0); flush(1); flush(2); flush(3);
+  // octaves 5-9 of x, y
+  sincos_scaled2(x[0], 5, x[1], 5, &s0, &c0, &s1, &c1);
+  put(5, 0, s0, c0); put(5, 1, s1, c1);
+  chains(5, 0, s0, c0, 5, 1, s1, c1);
+  flush(4); flush(5); flush(6); flush(7);
 }
 
 template <int W, class IO>
@@ -306,14 +289,6 @@ __device__ __forceinline__ void fetch_direction(const IO& io, const RowIn& row, 
   } else {
     encode_direction_h(row.d, de);
   }
-}
-
-template <int W>
-__device__ __forceinline__ void store_direction(uint8_t* A3, int tid, const uint4* de) {
-  using T = TcShape<W>;
-  static_assert(T::K3 - W == 32, "direction operand chunk is 32 fp16 wide");
-#pragma unroll
-  for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(A3 + canon_off(tid, W + 8 * q, T::K3)) = de[q];
 }
 
 __device__ __forceinline__ void QueryIO::load_denc(uint32_t idx, uint32_t row, uint4* de) const {
@@ -332,187 +307,191 @@ __device__ __forceinline__ void QueryIO::load_denc(uint32_t idx, uint32_t row, u
 // the kernel
 // ---------------------------------------------------------------------------
 template <int W, class IO>
-__global__ void __launch_bounds__(256, TcShape<W>::CTAS_PER_SM) k_mlp_tc(const uint8_t* __restrict__ packed,
-                                                                         TileSched S, IO io) {
+__global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(const uint8_t* __restrict__ packed,
+                                                                              TileSched S, IO io) {
   using T = TcShape<W>;
+  using C = TcCfg<W>;
+  constexpr int NS = C::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
-  const uint32_t bar0 = smem_u32(smem + T::BAR), bar_w = bar0 + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + T::BAR + 24);
-  const int tid = threadIdx.x, warp = tid >> 5;
-  // two warpgroups: group g owns tile slot g (its A operand, its TMEM
-  // columns, its commit barrier); row gt of the tile is TMEM lane gt
-  const int g = tid >> 7, gt = tid & 127;
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t bar_full = sb + C::BAR, bar_free = bar_full + 16, bar_mma = bar_full + 32;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::TSLOT);
+  uint4* runs = reinterpret_cast<uint4*>(smem + C::RUNS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = warp >> 2;  // warpgroup (TMEM slot); g == NS: the loader warp
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"((uint32_t)T::TMEM_COLS));
+                 "r"((uint32_t)C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(bar0, 1);
-    mbar_init(bar0 + 8, 1);
-    mbar_init(bar_w, 1);
+    mbar_init(bar_full, 1);
+    mbar_init(bar_full + 8, 1);
+    mbar_init(bar_free, NS);
+    mbar_init(bar_free + 8, NS);
+    for (int i = 0; i < NS; ++i) mbar_init(bar_mma + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  {  // constant bias multiplier: row r = [1, 1, 0 ... 0]
-    const int r = tid >> 1, c = tid & 1;
-    *reinterpret_cast<uint4*>(smem + T::ONES + canon_off(r, 8 * c, 16)) =
-        c ? make_uint4(0u, 0u, 0u, 0u) : make_uint4(0x3C003C00u, 0u, 0u, 0u);
-  }
-  fence_async_smem();
   fence_before();
   __syncthreads();
   fence_after();
-  // setup above is private to this CTA (TMEM, barriers, constant tile): it
-  // overlaps the previous kernel's tail under PDL; its results are read below
-  gf_pdl_wait();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t wb = smem_u32(smem);
-  uint8_t* Ag = smem + T::A(g);
-  const uint32_t trow = tmem + g * T::NC + ((uint32_t)((warp & 3) * 32) << 16);  // lane quarter of this warp
+  if (warp < 4) {  // constant bias multiplier, row r = [1, 1, 0 ... 0] (fp16), lane quarter of this warp
+    const uint32_t ta = tmem + C::ONES + ((uint32_t)(warp * 32) << 16);
+    uint32_t o[8] = {0x3C003C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    GF_ST8(ta, o);
+    tmem_wait_st();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  // setup above is private to this CTA (TMEM, barriers, constant operand):
+  // it overlaps the previous kernel's tail under PDL
+  gf_pdl_wait();
 
   const uint32_t nt = *S.n_tiles;
   const uint32_t per = (nt + gridDim.x - 1) / gridDim.x;
-  const uint32_t t_begin = blockIdx.x * per, t_end = min(nt, t_begin + per);
-  uint2* s_tiles = reinterpret_cast<uint2*>(smem + T::TILEBUF);
-  uint32_t tbase = t_begin;
-  auto fill_tiles = [&](uint32_t from) {  // all threads, then a CTA barrier
-    tbase = from;
-    for (uint32_t j = tid; j < (uint32_t)T::TB && from + j < t_end; j += blockDim.x) s_tiles[j] = S.tiles[from + j];
-    __syncthreads();
-  };
-  fill_tiles(t_begin);
-  auto tile_at = [&](uint32_t u) -> uint2 { return s_tiles[u - tbase]; };
-  int cur = -1;
-  uint32_t ph = 0, ph_w = 0;
+  const uint32_t t_begin = min(nt, blockIdx.x * per), t_end = min(nt, t_begin + per);
 
-  // MMA chain of layer L for this group's slot (thread gt == 0 of the group):
-  // bias tile first (accumulator := bias), then the K steps
-  auto issue = [&](int L) {
-#if GF_EXP == 3
-    if (gt == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar0 + 8 * g) : "memory");
-    return;
-#endif
-    if (gt != 0) return;
-    const uint32_t a = wb + T::A(g), d = tmem + g * T::NC;
-    uint32_t b = wb + T::B1, bb = wb + T::BB1, idesc = idesc_f16(128, T::N1);
-    int K = T::K1;
-    if (L == 0) { b = wb + T::B0; bb = wb + T::BB0; K = T::K0; idesc = idesc_f16(128, T::N0); }
-    if (L == 2) { b = wb + T::B2; bb = wb + T::BB2; K = T::K2; idesc = idesc_f16(128, T::N2); }
-    if (L == 3) { b = wb + T::B3; bb = wb + T::BB3; K = T::K3; idesc = idesc_f16(128, T::N3); }
-    if (L == 4) { b = wb + T::B4; bb = wb + T::BB4; K = T::K4; idesc = idesc_f16(128, T::N4); }
-    mma_f16(d, umma_desc(wb + T::ONES, 16), umma_desc(bb, 16), idesc, 0u);
-    // a K step of 16 columns is 256 B further in both operands: +16 in the
-    // descriptors' start-address field (>> 4), no carry out of 14 bits
-    const uint64_t da = umma_desc(a, K), db = umma_desc(b, K);
-    for (int ks = 0; ks < K / 16; ++ks) mma_f16(d, da + (uint64_t)(ks * 16), db + (uint64_t)(ks * 16), idesc, 1u);
-    mma_commit(bar0 + 8 * g);
-  };
-  auto wait_mma = [&]() {
-    mbar_wait(bar0 + 8 * g, ph);
-    ph ^= 1;
-    fence_after();
-  };
-  // this group's smem operand writes -> visible to the tensor core; its TMEM
-  // reads retired (named barrier over the group's 128 threads)
-  auto publish = [&]() {
-    fence_async_smem();
-    fence_before();
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
-    fence_after();
-  };
-  // tile of this group inside the pair starting at t (slot 1 only for a
-  // second tile of the same cell: both slots share the staged weights)
-  auto second = [&](uint32_t t, uint32_t cell) -> bool {
-    return t + 1 < t_end && gf_tile_cell(tile_at(t + 1)) == cell;
-  };
-  auto my_tile = [&](uint32_t t, uint2& tl) -> bool {
-    if (t >= t_end) return false;
-    tl = tile_at(t);
-    if (g == 0) return true;
-    if (!second(t, gf_tile_cell(tl))) return false;
-    tl = tile_at(t + 1);
-    return true;
-  };
-
-  RowIn nxt;
-  {
-    uint2 tl;
-    if (my_tile(t_begin, tl)) load_row(S, io, tl, gt, nxt);
-  }
-
-  for (uint32_t t = t_begin; t < t_end;) {
-    __syncthreads();  // previous pair fully retired (weight operands and the tile window may be replaced)
-    if (t + 4 > tbase + (uint32_t)T::TB && tbase + (uint32_t)T::TB < t_end) fill_tiles(t);  // CTA-uniform
-    const uint32_t cell = gf_tile_cell(tile_at(t));
-    const bool two = second(t, cell);
-    const uint32_t t_next = t + (two ? 2 : 1);
-    const bool active = g == 0 || two;
-    const bool new_cell = (int)cell != cur;
-    if (new_cell && tid == 0) bulk_load(wb, packed + (size_t)cell * T::CELL_BYTES, T::CELL_BYTES, bar_w);
-    cur = (int)cell;
-    const RowIn row = nxt;
-    if (active) {
-#if GF_EXP == 1
-      for (int c = 0; c < 8; ++c) *reinterpret_cast<uint4*>(Ag + canon_off(gt, 8 * c, T::K0)) = make_uint4(__float_as_uint(row.x[0]), 0u, 0u, 0u);
-#else
-      encode_position<W>(Ag, gt, row.x);
-#endif
-      publish();
-    }
-    if (new_cell) {
-      mbar_wait(bar_w, ph_w);
-      ph_w ^= 1;
-    }
-    if (active) issue(0);
-    {  // prefetch this group's row of the next pair while trunk0 runs
-      uint2 tn;
-      if (my_tile(t_next, tn)) load_row(S, io, tn, gt, nxt);
-    }
-    if (active) {
-      float sigma = 0.f;
-      uint4 de[4];  // direction operand chunk, fetched one layer ahead of its use
-#pragma unroll
-      for (int L = 0; L < 5; ++L) {
-        wait_mma();
-        if (L == 0) {  // trunk0 -> h0 (K1 layout, over the dead gamma(x))
-          tmem_to_operand<W, true>(trow, Ag, T::K1, gt);
-        } else if (L == 1) {  // trunk1 -> h1 (K2 layout)
-          tmem_to_operand<W, true>(trow, Ag, T::K2, gt);
-          fetch_direction<W>(io, row, de);  // in flight while the L2 MMA runs
-        } else if (L == 2) {  // feature (cols 0..W-1, unactivated) + density (col W) -> [feat, gamma(d)] (K3)
-          store_direction<W>(Ag, gt, de);
-          tmem_to_operand<W, false>(trow, Ag, T::K3, gt);
-          float z[16];
-          tmem_load<16>(trow + W, z);
-          sigma = fmaxf(z[0], 0.f);
-        } else if (L == 3) {  // direction -> g (K4 layout)
-          tmem_to_operand<W, true>(trow, Ag, T::K4, gt);
-        } else {  // color: sigmoid
-          float z[16];
-          tmem_load<16>(trow, z);
-          float rgb[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const float v = z[c];
-            const float e = __expf(-fabsf(v)), r = __fdividef(1.f, 1.f + e);  // sign-split sigmoid (mlp.py:228-235)
-            rgb[c] = v >= 0.f ? r : e * r;
-          }
-          if (row.valid) io.store(row.idx, row.row, rgb[0], rgb[1], rgb[2], sigma);
-        }
-        if (L < 4) {
-          publish();
-          issue(L + 1);
+  if (g == NS) {
+    // ---- loader warp: cut [t_begin, t_end) into runs of one cell; run r's
+    // weights go to buffer r & 1 once every group has released run r - 2
+    uint32_t s = t_begin;
+    for (uint32_t r = 0;; ++r) {
+      const uint32_t k = r & 1;
+      uint32_t cell = 0, e = s;
+      if (s < t_end) {
+        cell = gf_tile_cell(S.tiles[s]);
+        e = s + 1;
+        for (;;) {
+          if (e >= t_end) { e = t_end; break; }
+          const uint32_t t = e + (uint32_t)lane;
+          const bool diff = t >= t_end || gf_tile_cell(S.tiles[t]) != cell;
+          const uint32_t m = __ballot_sync(0xffffffffu, diff);
+          if (m) { e += (uint32_t)(__ffs(m) - 1); break; }
+          e += 32;
         }
       }
+      if (r >= 2) mbar_wait(bar_free + 8 * k, ((r - 2) >> 1) & 1);
+      if (lane == 0) {
+        runs[k] = make_uint4(cell, s, e, 0u);
+        if (s < t_end) bulk_load(sb + k * T::CELL_BYTES, packed + (size_t)cell * T::CELL_BYTES, T::CELL_BYTES,
+                                 bar_full + 8 * k);
+        else mbar_arrive(bar_full + 8 * k);  // end of the range
+      }
+      __syncwarp();
+      if (s >= t_end) break;
+      s = e;
     }
-    fence_before();
-    t = t_next;
+  } else {
+    // ---- warpgroup g: tiles g, g + NS, ... of every run
+    const int gt = tid & 127;
+    const uint32_t slot = tmem + (uint32_t)(g * T::SLOT);                // lane 0 of this group's slot
+    const uint32_t trow = slot + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lane quarter
+    const uint32_t ones = tmem + C::ONES;
+    const uint32_t mbar = bar_mma + 8 * g;
+    uint32_t ph = 0;
+    // layer L's MMA chain, issued by warp L % 4 of the group (one elected lane):
+    // bias tile against the ones operand first (accumulator := bias), then the K steps
+    auto issue = [&](int L, uint32_t wb) {
+      if ((warp & 3) != (L & 3)) return;
+      fence_after();
+      uint32_t b = wb + T::B1, bb = wb + T::BB1, idesc = idesc_f16(128, T::N1), acol = T::A1C;
+      int K = T::K1;
+      if (L == 0) { b = wb + T::B0; bb = wb + T::BB0; K = T::K0; idesc = idesc_f16(128, T::N0); acol = T::A0C; }
+      if (L == 2) { b = wb + T::B2; bb = wb + T::BB2; K = T::K2; idesc = idesc_f16(128, T::N2); acol = T::A2C; }
+      if (L == 3) { b = wb + T::B3; bb = wb + T::BB3; K = T::K3; idesc = idesc_f16(128, T::N3); acol = T::A3C; }
+      if (L == 4) { b = wb + T::B4; bb = wb + T::BB4; K = T::K4; idesc = idesc_f16(128, T::N4); acol = T::A4C; }
+      if (elect_one()) {
+        mma_ts(slot, ones, umma_desc(bb, 16), idesc, 0u);
+        // a K step of 16 columns: +8 TMEM columns of A, +256 B of B (+16 in
+        // the descriptor's start-address field, no carry out of 14 bits)
+        const uint64_t db = umma_desc(b, K);
+#pragma unroll
+        for (int ks = 0; ks < K / 16; ++ks) mma_ts(slot, slot + acol + 8 * ks, db + (uint64_t)(ks * 16), idesc, 1u);
+        mma_commit(mbar);
+      }
+      __syncwarp();
+    };
+    auto wait_mma = [&]() {
+      mbar_wait(mbar, ph);
+      ph ^= 1;
+      fence_after();
+    };
+    // this group's TMEM stores done and its TMEM loads retired -> the MMA
+    // issuer (named barrier over the group's 128 threads)
+    auto publish = [&]() {
+      tmem_wait_st();
+      fence_before();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+    };
+
+    for (uint32_t r = 0;; ++r) {
+      const uint32_t k = r & 1;
+      mbar_wait(bar_full + 8 * k, (r >> 1) & 1);
+      const uint4 run = runs[k];
+      if (run.y >= run.z) break;
+      const uint32_t wb = sb + k * T::CELL_BYTES;
+      RowIn nxt;
+      uint32_t t = run.y + (uint32_t)g;
+      if (t < run.z) load_row(S, io, S.tiles[t], gt, nxt);
+      for (; t < run.z; t += NS) {
+        const RowIn row = nxt;
+        encode_position<W>(trow + T::A0C, row.x);
+        publish();
+        issue(0, wb);
+        if (t + NS < run.z) load_row(S, io, S.tiles[t + NS], gt, nxt);  // next tile's rows while this one runs
+        uint4 de[4];  // direction operand chunk, fetched one layer ahead of its use
+        float sigma = 0.f;
+#pragma unroll
+        for (int L = 0; L < 5; ++L) {
+          wait_mma();
+          if (L == 0) {  // trunk0 -> h0
+            epilogue_to_a<W, true>(trow, T::A1C);
+          } else if (L == 1) {  // trunk1 -> h1
+            epilogue_to_a<W, true>(trow, T::A2C);
+            fetch_direction<W>(io, row, de);  // in flight while the L2 MMA runs
+          } else if (L == 2) {  // feature (cols 0..W-1, unactivated) + density (col W) -> [feat, gamma(d)]
+            uint32_t z;
+            GF_LD1(trow + W, z);
+            epilogue_to_a<W, false>(trow, T::A3C);  // its first wait covers the density load too
+            sigma = fmaxf(__uint_as_float(z), 0.f);
+            uint32_t o[8] = {de[0].x, de[0].y, de[0].z, de[0].w, de[1].x, de[1].y, de[1].z, de[1].w};
+            GF_ST8(trow + T::A3C + W / 2, o);
+            uint32_t o2[8] = {de[2].x, de[2].y, de[2].z, de[2].w, de[3].x, de[3].y, de[3].z, de[3].w};
+            GF_ST8(trow + T::A3C + W / 2 + 8, o2);
+          } else if (L == 3) {  // direction -> g
+            epilogue_to_a<W, true>(trow, T::A4C);
+          } else {  // color: sigmoid
+            uint32_t z[4];
+            GF_LD4(trow, z);
+            tmem_wait_ld();
+            float rgb[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {  // sign-split sigmoid (mlp.py:228-235): e = exp(-|v|), 1/(1+e) or e/(1+e)
+              const float v = __uint_as_float(z[c]);
+              float e, q;
+              asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * fabsf(v)));
+              asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(q) : "f"(1.f + e));
+              rgb[c] = v >= 0.f ? q : e * q;
+            }
+            if (row.valid) io.store(row.idx, row.row, rgb[0], rgb[1], rgb[2], sigma);
+          }
+          if (L < 4) {
+            publish();
+            issue(L + 1, wb);
+          }
+        }
+      }
+      if (gt == 0) mbar_arrive(bar_free + 8 * k);  // this group is done with buffer k
+    }
   }
+  fence_before();
   __syncthreads();
   fence_after();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)T::TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)C::TMEM_COLS));
 }
 
 // ---------------------------------------------------------------------------
@@ -602,46 +581,51 @@ bool launch_pack_fp16(const LayerTable& t, int64_t n_cells, const float* const* 
 }
 
 template <int W, class IO>
-static int tc_resident() {
-  using T = TcShape<W>;
+static int tc_grid() {
+  using C = TcCfg<W>;
   auto k = k_mlp_tc<W, IO>;
-  static thread_local int per_sm = 0;  // resident CTAs per SM for this instantiation
-  if (per_sm == 0) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-    // residency from first principles (the occupancy API proved unreliable
-    // here): shared memory (+1 KiB reserved per CTA), registers, TMEM columns
+  static thread_local int grid = 0;
+  if (grid == 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    // residency from first principles (the occupancy API reports 1 CTA/SM
+    // here, apparently counting all 16 named barriers per CTA): shared
+    // memory (+1 KiB reserved per CTA), registers, TMEM columns
     int dev = 0, smem_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaFuncAttributes fa;
     int regs = 128;
     if (cudaFuncGetAttributes(&fa, k) == cudaSuccess && fa.numRegs > 0) regs = fa.numRegs;
-    const int by_smem = smem_sm / (T::SMEM + 1024);
-    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * 256);
-    const int by_tmem = 512 / T::TMEM_COLS;
-    per_sm = by_smem < by_regs ? by_smem : by_regs;
-    per_sm = per_sm < by_tmem ? per_sm : by_tmem;
+    const int warps = (C::THREADS + 31) / 32;
+    const int by_smem = smem_sm / (C::SMEM + 1024);
+    const int by_regs = 65536 / (((regs + 7) / 8 * 8) * 32 * warps);
+    const int by_warps = 64 / warps;
+    int per_sm = by_smem < by_regs ? by_smem : by_regs;
+    per_sm = per_sm < by_warps ? per_sm : by_warps;
+    per_sm = per_sm < C::CTAS ? per_sm : C::CTAS;  // TMEM: CTAS x TMEM_COLS <= 512
     if (per_sm < 1) per_sm = 1;
-    if (getenv("GF_DEBUG"))
-      fprintf(stderr, "[gf] k_mlp_tc<%d>: smem %d B, regs %d -> %d CTAs/SM (smem %d, regs %d, tmem %d)\n", W,
-              T::SMEM, regs, per_sm, by_smem, by_regs, by_tmem);
+    grid = num_sms() * per_sm;
+    if (getenv("GF_DEBUG")) {
+      fprintf(stderr, "[gf] k_mlp_tc<%d>: %d warpgroups + loader, smem %d B, regs %d, TMEM %d cols -> %d CTAs/SM\n", W,
+              C::NS, C::SMEM, fa.numRegs, C::TMEM_COLS, per_sm);
+    }
     cudaGetLastError();
   }
-  return per_sm;
+  return grid;
 }
 
 template <int W, class IO>
 static void launch_tc_w(const void* packed, const TileSched& S, const IO& io, cudaStream_t st) {
-  using T = TcShape<W>;
-  gf_launch_pdl(k_mlp_tc<W, IO>, dim3(num_sms() * tc_resident<W, IO>()), dim3(256), (size_t)T::SMEM, st,
+  using C = TcCfg<W>;
+  gf_launch_pdl(k_mlp_tc<W, IO>, dim3(tc_grid<W, IO>()), dim3(C::THREADS), (size_t)C::SMEM, st,
                 (const uint8_t*)packed, S, io);
 }
 
 bool prepare_mlp_tc(const LayerTable& t) {
   if (!tc_supported(t)) return false;
   num_sms();
-  if (t.width == 32) tc_resident<32, RenderIO>();
-  else tc_resident<64, RenderIO>();
+  if (t.width == 32) { tc_grid<32, RenderIO>(); tc_grid<32, QueryIO>(); }
+  else { tc_grid<64, RenderIO>(); tc_grid<64, QueryIO>(); }
   return true;
 }
 

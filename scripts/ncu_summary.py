@@ -60,10 +60,12 @@ def launches_table(path):
     return "\n".join(lines)
 
 
-def report_summary(path, top=12):
-    rows = ncu_csv(path, "--page", "raw")
+def report_summary(path, top=12, launch=None):
+    sel = [] if launch is None else ["--launch-skip", str(launch), "--launch-count", "1"]
+    rows = ncu_csv(path, "--page", "raw", *sel)
     h, units, d = rows[0], rows[1], rows[2]
-    out = [f"### `{path.split('/')[-1]}` — `{d[h.index('Kernel Name')][:90]}`", "", "| counter | value |", "|---|---|"]
+    tag = "" if launch is None else f" (launch {launch} of the capture)"
+    out = [f"### `{path.split('/')[-1]}`{tag} — `{d[h.index('Kernel Name')][:90]}`", "", "| counter | value |", "|---|---|"]
     for k, label in KEYS:
         if k in h:
             out.append(f"| {label} (`{k}`) | {d[h.index(k)]} {units[h.index(k)]} |")
@@ -78,7 +80,7 @@ def report_summary(path, top=12):
 
     st = sorted(st, key=lambda x: -f(x[1]))[:6]
     out += ["", "stall samples: " + ", ".join(f"{k} {v}" for k, v in st), ""]
-    src = ncu_csv(path, "--page", "source", "--print-source", "cuda,sass")
+    src = ncu_csv(path, "--page", "source", "--print-source", "cuda,sass", *sel)
     agg, text, cur = collections.defaultdict(lambda: [0, 0]), {}, None
     for r in src:
         if len(r) == 2 and r[0] == "File Path":
@@ -106,6 +108,8 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--reports", nargs="*", default=[])
     ap.add_argument("--title", default="ncu summary")
+    ap.add_argument("--launch", type=int, default=None, help="which launch of a multi-launch capture")
+    ap.add_argument("--top", type=int, default=12)
     a = ap.parse_args()
     print(f"# {a.title}\n")
     if a.launches:
@@ -113,7 +117,7 @@ def main():
         print(launches_table(a.launches))
         print()
     for r in a.reports:
-        print(report_summary(r))
+        print(report_summary(r, a.top, a.launch))
         print()
 
 
