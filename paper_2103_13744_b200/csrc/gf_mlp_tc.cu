@@ -78,27 +78,37 @@ struct TcShape {
   static_assert(SLOT % 16 == 0, "slot columns");
 };
 
-// launch shape per width: warpgroups per CTA (TMEM slots), CTAs per SM
+// launch shape per width: warpgroups per CTA, tiles per warpgroup (TMEM
+// slots each), CTAs per SM.  Measured on the C2 frame (MLP ms/frame,
+// 2026-10-17): 3 groups x 1 tile x 2 CTAs 0.376; 6 x 1 x 1 0.373; 2 x 1 x 2
+// 0.457; 3 x 1 x 1 0.550; 3 x 2 x 1 0.414; 2 x 3 x 1 0.497 -- tiles in flight
+// per SM, each with its own warps, is what counts (latency-bound), and TMEM
+// (64 columns per W=32 tile) caps them at 7.
 #ifndef GF_TC_NS32
 #define GF_TC_NS32 3
 #endif
 #ifndef GF_TC_CTAS32
 #define GF_TC_CTAS32 2
 #endif
+#ifndef GF_TC_R32
+#define GF_TC_R32 1
+#endif
 template <int W>
 struct TcCfg {
   static constexpr int NS = W == 32 ? GF_TC_NS32 : 2;
   static constexpr int CTAS = W == 32 ? GF_TC_CTAS32 : 2;
+  static constexpr int R = W == 32 ? GF_TC_R32 : 1;        // tiles in flight per warpgroup (TMEM slots each)
   static constexpr int THREADS = NS * 128 + 32;
-  static constexpr int ONES = NS * TcShape<W>::SLOT;  // 8 columns: [1, 1, 0 ...] fp16 per row
+  static constexpr int ONES = NS * R * TcShape<W>::SLOT;  // 8 columns: [1, 1, 0 ...] fp16 per row
   static constexpr int tmem_cols(int c) { return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512; }
   static constexpr int TMEM_COLS = tmem_cols(ONES + 8);
   static_assert(ONES + 8 <= 512 && TMEM_COLS * CTAS <= 512, "TMEM budget");
-  // shared memory: two weight buffers, then barriers and the run table
-  static constexpr int BAR = 2 * TcShape<W>::CELL_BYTES;   // full[2], free[2], mma[NS]
-  static constexpr int TSLOT = BAR + 32 + 8 * NS;          // TMEM base address
-  static constexpr int RUNS = (TSLOT + 4 + 15) / 16 * 16;  // uint4 runs[2]: (cell, first tile, end tile, 0)
-  static constexpr int SMEM = RUNS + 32;
+  // shared memory: NBUF weight buffers, then barriers and the run table
+  static constexpr int NBUF = W == 32 ? 3 : 2;
+  static constexpr int BAR = NBUF * TcShape<W>::CELL_BYTES;      // full[NBUF], free[NBUF], mma[NS]
+  static constexpr int TSLOT = BAR + 16 * NBUF + 8 * NS;         // TMEM base address
+  static constexpr int RUNS = (TSLOT + 4 + 15) / 16 * 16;        // uint4 runs[NBUF]: (cell, first tile, end tile, 0)
+  static constexpr int SMEM = RUNS + 16 * NBUF;
 };
 
 // byte offset of element (r, k) in a canonical K-major no-swizzle operand of
@@ -314,7 +324,8 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
   constexpr int NS = C::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sb = smem_u32(smem);
-  const uint32_t bar_full = sb + C::BAR, bar_free = bar_full + 16, bar_mma = bar_full + 32;
+  constexpr int NB = C::NBUF;
+  const uint32_t bar_full = sb + C::BAR, bar_free = bar_full + 8 * NB, bar_mma = bar_free + 8 * NB;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::TSLOT);
   uint4* runs = reinterpret_cast<uint4*>(smem + C::RUNS);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -326,10 +337,10 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(bar_full, 1);
-    mbar_init(bar_full + 8, 1);
-    mbar_init(bar_free, NS);
-    mbar_init(bar_free + 8, NS);
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(bar_full + 8 * i, 1);
+      mbar_init(bar_free + 8 * i, NS);
+    }
     for (int i = 0; i < NS; ++i) mbar_init(bar_mma + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -356,10 +367,9 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
 
   if (g == NS) {
     // ---- loader warp: cut [t_begin, t_end) into runs of one cell; run r's
-    // weights go to buffer r & 1 once every group has released run r - 2
+    // weights go to buffer r % NB once every group has released run r - NB
     uint32_t s = t_begin;
-    for (uint32_t r = 0;; ++r) {
-      const uint32_t k = r & 1;
+    for (uint32_t r = 0, k = 0;; ++r, k = k + 1 == NB ? 0 : k + 1) {
       uint32_t cell = 0, e = s;
       if (s < t_end) {
         cell = gf_tile_cell(S.tiles[s]);
@@ -373,7 +383,7 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
           e += 32;
         }
       }
-      if (r >= 2) mbar_wait(bar_free + 8 * k, ((r - 2) >> 1) & 1);
+      if (r >= NB) mbar_wait(bar_free + 8 * k, ((r - NB) / NB) & 1);
       if (lane == 0) {
         runs[k] = make_uint4(cell, s, e, 0u);
         if (s < t_end) bulk_load(sb + k * T::CELL_BYTES, packed + (size_t)cell * T::CELL_BYTES, T::CELL_BYTES,
@@ -385,16 +395,22 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
       s = e;
     }
   } else {
-    // ---- warpgroup g: tiles g, g + NS, ... of every run
+    // ---- warpgroup g: tiles t_begin + g, t_begin + g + NS, ... of the CTA's
+    // range, up to R consecutive ones of the same run per pass (TMEM slots
+    // g*R .. g*R + R-1): each thread owns row gt of every tile in flight, so
+    // one barrier, one MMA commit and one wait per layer serve R tiles and
+    // the R epilogues interleave
+    constexpr int R = C::R;
     const int gt = tid & 127;
-    const uint32_t slot = tmem + (uint32_t)(g * T::SLOT);                // lane 0 of this group's slot
-    const uint32_t trow = slot + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's lane quarter
+    const uint32_t lq = (uint32_t)((warp & 3) * 32) << 16;  // this warp's lane quarter
+    const uint32_t slot0 = tmem + (uint32_t)(g * R * T::SLOT);
     const uint32_t ones = tmem + C::ONES;
     const uint32_t mbar = bar_mma + 8 * g;
     uint32_t ph = 0;
-    // layer L's MMA chain, issued by warp L % 4 of the group (one elected lane):
-    // bias tile against the ones operand first (accumulator := bias), then the K steps
-    auto issue = [&](int L, uint32_t wb) {
+    // layer L's MMA chains for n tiles, issued by warp L % 4 of the group (one
+    // elected lane): bias tile against the ones operand first (accumulator :=
+    // bias), then the K steps; one commit for all of them
+    auto issue = [&](int L, uint32_t wb, int n) {
       if ((warp & 3) != (L & 3)) return;
       fence_after();
       uint32_t b = wb + T::B1, bb = wb + T::BB1, idesc = idesc_f16(128, T::N1), acol = T::A1C;
@@ -403,13 +419,24 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
       if (L == 2) { b = wb + T::B2; bb = wb + T::BB2; K = T::K2; idesc = idesc_f16(128, T::N2); acol = T::A2C; }
       if (L == 3) { b = wb + T::B3; bb = wb + T::BB3; K = T::K3; idesc = idesc_f16(128, T::N3); acol = T::A3C; }
       if (L == 4) { b = wb + T::B4; bb = wb + T::BB4; K = T::K4; idesc = idesc_f16(128, T::N4); acol = T::A4C; }
+#if (GF_EXP & 2)  // diagnostic: no tensor-core work, the commit barrier is arrived directly
+      if (elect_one()) mbar_arrive(mbar);
+      __syncwarp();
+      return;
+#endif
       if (elect_one()) {
-        mma_ts(slot, ones, umma_desc(bb, 16), idesc, 0u);
-        // a K step of 16 columns: +8 TMEM columns of A, +256 B of B (+16 in
-        // the descriptor's start-address field, no carry out of 14 bits)
-        const uint64_t db = umma_desc(b, K);
+        const uint64_t dbb = umma_desc(bb, 16), db = umma_desc(b, K);
 #pragma unroll
-        for (int ks = 0; ks < K / 16; ++ks) mma_ts(slot, slot + acol + 8 * ks, db + (uint64_t)(ks * 16), idesc, 1u);
+        for (int j = 0; j < R; ++j) {
+          if (j < n) {
+            const uint32_t sl = slot0 + (uint32_t)(j * T::SLOT);
+            mma_ts(sl, ones, dbb, idesc, 0u);
+            // a K step of 16 columns: +8 TMEM columns of A, +256 B of B (+16 in
+            // the descriptor's start-address field, no carry out of 14 bits)
+#pragma unroll
+            for (int ks = 0; ks < K / 16; ++ks) mma_ts(sl, sl + acol + 8 * ks, db + (uint64_t)(ks * 16), idesc, 1u);
+          }
+        }
         mma_commit(mbar);
       }
       __syncwarp();
@@ -426,65 +453,119 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
       fence_before();
       asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
     };
+    auto trow = [&](int j) { return slot0 + (uint32_t)(j * T::SLOT) + lq; };
 
-    for (uint32_t r = 0;; ++r) {
-      const uint32_t k = r & 1;
-      mbar_wait(bar_full + 8 * k, (r >> 1) & 1);
-      const uint4 run = runs[k];
-      if (run.y >= run.z) break;
-      const uint32_t wb = sb + k * T::CELL_BYTES;
-      RowIn nxt;
-      uint32_t t = run.y + (uint32_t)g;
-      if (t < run.z) load_row(S, io, S.tiles[t], gt, nxt);
-      for (; t < run.z; t += NS) {
-        const RowIn row = nxt;
-        encode_position<W>(trow + T::A0C, row.x);
-        publish();
-        issue(0, wb);
-        if (t + NS < run.z) load_row(S, io, S.tiles[t + NS], gt, nxt);  // next tile's rows while this one runs
-        uint4 de[4];  // direction operand chunk, fetched one layer ahead of its use
-        float sigma = 0.f;
+    // before tile t the group releases every run ending at or before t (a
+    // short run may hold none of its tiles) and waits for the weights of the
+    // run holding t; rows are prefetched R tiles ahead, across runs
+    uint32_t r = 0, k = 0, wb = sb, run_end = 0;
+    mbar_wait(bar_full, 0);
+    run_end = runs[0].z;
+    RowIn q[R];  // rows of this group's next R tiles
+    uint32_t t = t_begin + (uint32_t)g;
 #pragma unroll
-        for (int L = 0; L < 5; ++L) {
-          wait_mma();
+    for (int j = 0; j < R; ++j)
+      if (t + (uint32_t)(j * NS) < t_end) load_row(S, io, S.tiles[t + (uint32_t)(j * NS)], gt, q[j]);
+    while (t < t_end) {
+      while (t >= run_end) {
+        if (gt == 0) mbar_arrive(bar_free + 8 * k);  // this group is done with run r
+        ++r;
+        k = k + 1 == NB ? 0 : k + 1;
+        mbar_wait(bar_full + 8 * k, (r / NB) & 1);
+        run_end = runs[k].z;
+        wb = sb + k * T::CELL_BYTES;
+      }
+      // tiles of this pass: t, t + NS, ... while they stay in this run
+      int n = 1;
+#pragma unroll
+      for (int j = 1; j < R; ++j)
+        if (n == j && t + (uint32_t)(j * NS) < run_end && t + (uint32_t)(j * NS) < t_end) n = j + 1;
+      RowIn row[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) row[j] = q[j];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (j < n) {
+#if (GF_EXP & 1)  // diagnostic: no encoding arithmetic, the operand gets the raw position
+          const uint32_t xv = __float_as_uint(row[j].x[0]);
+          GF_ST4(trow(j) + T::A0C, xv, xv, xv, xv);
+#else
+          encode_position<W>(trow(j) + T::A0C, row[j].x);
+#endif
+        }
+      }
+      publish();
+      issue(0, wb, n);
+      // refill the prefetch queue: the rows not consumed move up, the rest
+      // load while this pass runs
+      const uint32_t tn = t + (uint32_t)(n * NS);
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (j + n < R) {
+          q[j] = row[j + n];
+        } else if (tn + (uint32_t)(j * NS) < t_end) {
+          load_row(S, io, S.tiles[tn + (uint32_t)(j * NS)], gt, q[j]);
+        }
+      }
+      uint4 de[R][4];  // direction operand chunks, fetched one layer ahead of their use
+      float sigma[R];
+#pragma unroll
+      for (int L = 0; L < 5; ++L) {
+        wait_mma();
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          if (j >= n) continue;
+          const uint32_t tr = trow(j);
           if (L == 0) {  // trunk0 -> h0
-            epilogue_to_a<W, true>(trow, T::A1C);
+            epilogue_to_a<W, true>(tr, T::A1C);
           } else if (L == 1) {  // trunk1 -> h1
-            epilogue_to_a<W, true>(trow, T::A2C);
-            fetch_direction<W>(io, row, de);  // in flight while the L2 MMA runs
+            epilogue_to_a<W, true>(tr, T::A2C);
+            fetch_direction<W>(io, row[j], de[j]);  // in flight while the L2 MMA runs
           } else if (L == 2) {  // feature (cols 0..W-1, unactivated) + density (col W) -> [feat, gamma(d)]
             uint32_t z;
-            GF_LD1(trow + W, z);
-            epilogue_to_a<W, false>(trow, T::A3C);  // its first wait covers the density load too
-            sigma = fmaxf(__uint_as_float(z), 0.f);
-            uint32_t o[8] = {de[0].x, de[0].y, de[0].z, de[0].w, de[1].x, de[1].y, de[1].z, de[1].w};
-            GF_ST8(trow + T::A3C + W / 2, o);
-            uint32_t o2[8] = {de[2].x, de[2].y, de[2].z, de[2].w, de[3].x, de[3].y, de[3].z, de[3].w};
-            GF_ST8(trow + T::A3C + W / 2 + 8, o2);
+            GF_LD1(tr + W, z);
+            epilogue_to_a<W, false>(tr, T::A3C);  // its first wait covers the density load too
+            sigma[j] = fmaxf(__uint_as_float(z), 0.f);
+            uint32_t o[8] = {de[j][0].x, de[j][0].y, de[j][0].z, de[j][0].w,
+                             de[j][1].x, de[j][1].y, de[j][1].z, de[j][1].w};
+            GF_ST8(tr + T::A3C + W / 2, o);
+            uint32_t o2[8] = {de[j][2].x, de[j][2].y, de[j][2].z, de[j][2].w,
+                              de[j][3].x, de[j][3].y, de[j][3].z, de[j][3].w};
+            GF_ST8(tr + T::A3C + W / 2 + 8, o2);
           } else if (L == 3) {  // direction -> g
-            epilogue_to_a<W, true>(trow, T::A4C);
+            epilogue_to_a<W, true>(tr, T::A4C);
           } else {  // color: sigmoid
             uint32_t z[4];
-            GF_LD4(trow, z);
+            GF_LD4(tr, z);
             tmem_wait_ld();
             float rgb[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {  // sign-split sigmoid (mlp.py:228-235): e = exp(-|v|), 1/(1+e) or e/(1+e)
               const float v = __uint_as_float(z[c]);
-              float e, q;
+              float e, qv;
               asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * fabsf(v)));
-              asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(q) : "f"(1.f + e));
-              rgb[c] = v >= 0.f ? q : e * q;
+              asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(qv) : "f"(1.f + e));
+              rgb[c] = v >= 0.f ? qv : e * qv;
             }
-            if (row.valid) io.store(row.idx, row.row, rgb[0], rgb[1], rgb[2], sigma);
-          }
-          if (L < 4) {
-            publish();
-            issue(L + 1, wb);
+            if (row[j].valid) io.store(row[j].idx, row[j].row, rgb[0], rgb[1], rgb[2], sigma[j]);
           }
         }
+        if (L < 4) {
+          publish();
+          issue(L + 1, wb, n);
+        }
       }
-      if (gt == 0) mbar_arrive(bar_free + 8 * k);  // this group is done with buffer k
+      t = tn;
+    }
+    // release the current and any later runs (the loader waits on them
+    // before it reuses their buffers; the end sentinel needs no release)
+    for (;;) {
+      if (gt == 0) mbar_arrive(bar_free + 8 * k);
+      if (run_end >= t_end) break;
+      ++r;
+      k = k + 1 == NB ? 0 : k + 1;
+      mbar_wait(bar_full + 8 * k, (r / NB) & 1);
+      run_end = runs[k].z;
     }
   }
   fence_before();
