@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define GF_ABI_VERSION 1
+#define GF_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define GF_API __attribute__((visibility("default")))
@@ -52,6 +52,7 @@ typedef struct {
   int32_t pos_freqs;       /* 10 -> 63-wide position encoding                 */
   int32_t dir_freqs;       /* 4  -> 27-wide direction encoding                */
   int32_t include_raw;     /* 1: raw coordinates prepended                    */
+  int32_t skip_layer;      /* trunk layer fed [gamma(x), h] (mlp.py:79-81); 0: none */
 } gf_arch_t;
 
 /* grid.py:19-45 NetworkGrid geometry, occupancy.py:29-79 OccupancyGrid. */

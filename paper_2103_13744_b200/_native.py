@@ -17,6 +17,7 @@ import numpy as np
 LIB_PATH = Path(os.environ.get("GF_LIB_PATH") or Path(__file__).resolve().parent / "_lib" / "libgridfield_b200.so")
 
 GF_OK, GF_ERR_INVALID, GF_ERR_CUDA, GF_ERR_WORKSPACE, GF_ERR_UNSUPPORTED = range(5)
+ABI_VERSION = 2  # include/gridfield_b200.h GF_ABI_VERSION
 PRECISION = {"fp32": 0, "fp16": 1}
 STAT_FIELDS = ("total_queries", "ess_skipped", "ert_terminated_rays", "n_rays")
 INT64_MAX = np.iinfo(np.int64).max
@@ -26,6 +27,7 @@ class Arch(C.Structure):
     _fields_ = [
         ("hidden_layers", C.c_int32), ("width", C.c_int32), ("view_width", C.c_int32),
         ("pos_freqs", C.c_int32), ("dir_freqs", C.c_int32), ("include_raw", C.c_int32),
+        ("skip_layer", C.c_int32),
     ]
 
 
@@ -173,6 +175,9 @@ def lib():
                     fn = getattr(h, name)
                     fn.restype = res
                     fn.argtypes = args
+                if h.gf_abi_version() != ABI_VERSION:  # struct layouts below must match the library's
+                    raise NativeError(f"{LIB_PATH} has ABI {h.gf_abi_version()}, this binding expects {ABI_VERSION}; "
+                                      "rebuild it")
                 _lib = h
     return _lib
 
@@ -192,6 +197,7 @@ def make_arch(arch, encoding) -> Arch:
     return Arch(
         int(arch.hidden_layers), int(arch.hidden_width), int(arch.view_width),
         int(encoding.num_freqs_position), int(encoding.num_freqs_direction), int(bool(encoding.include_raw_input)),
+        int(arch.skip_layer or 0),
     )
 
 

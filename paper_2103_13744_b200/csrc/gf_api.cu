@@ -379,11 +379,16 @@ size_t gf_query_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* gri
   return query_carve(c, n, n_cells_of(grid), &w);
 }
 
-static bool run_mlp(const LayerTable& t, const void* packed, int precision, const TileSched& S, const RenderIO* rio,
-                    const QueryIO* qio, cudaStream_t st) {
-  if (precision == GF_PRECISION_FP32)
-    return rio ? launch_mlp_fp32_render(t, (const float*)packed, S, *rio, st)
-               : launch_mlp_fp32_query(t, (const float*)packed, S, *qio, st);
+static bool run_mlp(const LayerTable& t, const gf_arch_t* arch, const void* packed, int precision, const TileSched& S,
+                    const RenderIO* rio, const QueryIO* qio, cudaStream_t st) {
+  if (precision == GF_PRECISION_FP32) {
+    // the fused tiny-MLP kernel when it covers the manifest, else the generic one
+    if (rio ? launch_mlp_fp32_render(t, (const float*)packed, S, *rio, st)
+            : launch_mlp_fp32_query(t, (const float*)packed, S, *qio, st))
+      return true;
+    return rio ? launch_mlp_generic_render(t, arch, (const float*)packed, S, *rio, st)
+               : launch_mlp_generic_query(t, arch, (const float*)packed, S, *qio, st);
+  }
   if (precision == GF_PRECISION_FP16)
     return rio ? launch_mlp_tc_render(t, packed, S, *rio, st) : launch_mlp_tc_query(t, packed, S, *qio, st);
   return false;
@@ -422,7 +427,7 @@ int gf_query_points(const gf_arch_t* arch, const gf_grid_geom_t* grid, const voi
   }
   TileSched S{w.B.tiles, w.B.n_tiles, fast ? nullptr : w.B.sorted, w.B.srec, w.B.sdir};
   QueryIO io{pos, dir, rgb, sigma, nullptr, fast ? w.B.sdir : nullptr, fast ? w.sorted_out : nullptr};
-  if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
+  if (!run_mlp(t, arch, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_query_points: no MLP kernel for this architecture/precision");
   stage_mark(st, GF_STAGE_MLP, 1);
   if (fast) {
@@ -446,7 +451,7 @@ int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packe
   launch_segments_from_offsets(offsets, n_cells, n, w.B, st);
   TileSched S{w.B.tiles, w.B.n_tiles, nullptr, nullptr, nullptr};  // rows already grouped: identity
   QueryIO io{pos, dir, rgb, sigma, order, nullptr, nullptr};
-  if (!run_mlp(t, packed, precision, S, nullptr, &io, st))
+  if (!run_mlp(t, arch, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_grouped_forward: no MLP kernel for this architecture/precision");
   return check_cuda("gf_grouped_forward");
 }
@@ -738,7 +743,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
   RenderIO io{w.RB.res, w.R.dir, (uint32_t)stride, w.R.denc, stride_shift};
   const bool mlp_ok = an                                 ? true
                       : precision == GF_PRECISION_FP16   ? prepare_mlp_tc(t)
-                      : precision == GF_PRECISION_FP32 ? prepare_mlp_fp32(t)
+                      : precision == GF_PRECISION_FP32 ? (prepare_mlp_fp32(t) || prepare_mlp_generic(t, arch))
                                                        : false;
   if (!mlp_ok) return fail(GF_ERR_UNSUPPORTED, "gf_render_rays: no MLP kernel for this architecture/precision");
 
@@ -771,7 +776,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
         launch_field_analytic(*an, w.B.offsets, w.B.srec, w.R.dir, stride_shift, (uint32_t)stride, w.RB.res,
                               (int64_t)n_rays * stride, s);
       else
-        run_mlp(t, packed, precision, S, &io, nullptr, s);
+        run_mlp(t, arch, packed, precision, S, &io, nullptr, s);
       stage_mark(s, GF_STAGE_MLP, 1);
     }
     // final pass: composite the last group of rounds and write the colours

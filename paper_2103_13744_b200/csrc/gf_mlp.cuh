@@ -13,6 +13,7 @@ namespace gf {
 // density, feature, direction, color (mlp.py:73-84).
 struct LayerTable {
   int n_layers, trunk, width, view, pos_dim, dir_dim;
+  int skip;  // trunk layer whose input is [gamma(x), h] (mlp.py:79-81), -1: none
   int in[GF_MAX_LAYERS], out[GF_MAX_LAYERS];
 };
 
@@ -23,9 +24,14 @@ __host__ inline bool make_layer_table(const gf_arch_t* a, LayerTable* t) {
   t->view = a->view_width > 0 ? a->view_width : a->width;
   t->pos_dim = 3 * ((a->include_raw ? 1 : 0) + 2 * a->pos_freqs);
   t->dir_dim = 3 * ((a->include_raw ? 1 : 0) + 2 * a->dir_freqs);
+  t->skip = a->skip_layer > 0 ? a->skip_layer : -1;
+  if (t->skip >= t->trunk) return false;  // mlp.py:63-64: 1 <= skip_layer < trunk layers
   int l = 0;
   t->in[l] = t->pos_dim; t->out[l++] = t->width;
-  for (int k = 1; k < t->trunk; ++k) { t->in[l] = t->width; t->out[l++] = t->width; }
+  for (int k = 1; k < t->trunk; ++k) {
+    t->in[l] = k == t->skip ? t->width + t->pos_dim : t->width;
+    t->out[l++] = t->width;
+  }
   t->in[l] = t->width; t->out[l++] = 1;                      // density
   t->in[l] = t->width; t->out[l++] = t->width;               // feature
   t->in[l] = t->width + t->dir_dim; t->out[l++] = t->view;   // direction
@@ -160,6 +166,14 @@ bool launch_mlp_tc_render(const LayerTable& t, const void* packed, const TileSch
                           cudaStream_t st);
 bool launch_mlp_tc_query(const LayerTable& t, const void* packed, const TileSched& S, const QueryIO& io,
                          cudaStream_t st);
+
+// any manifest (depth, widths, skip layer, octaves): fp32 SIMT, gf_mlp_generic.cu
+bool generic_mlp_supported(const LayerTable& t);
+bool launch_mlp_generic_render(const LayerTable& t, const gf_arch_t* arch, const float* packed, const TileSched& S,
+                               const RenderIO& io, cudaStream_t st);
+bool launch_mlp_generic_query(const LayerTable& t, const gf_arch_t* arch, const float* packed, const TileSched& S,
+                              const QueryIO& io, cudaStream_t st);
+bool prepare_mlp_generic(const LayerTable& t, const gf_arch_t* arch);
 
 int num_sms();
 

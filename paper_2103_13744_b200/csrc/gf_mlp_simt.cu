@@ -8,7 +8,7 @@ namespace gf {
 template <class IO>
 static bool launch_fp32(const LayerTable& t, const float* packed, const TileSched& S, const IO& io, cudaStream_t st) {
   Fp32Layout L = make_fp32_layout(t);
-  const bool tiny = t.pos_dim == 63 && t.dir_dim == 27 && t.view == t.width && t.trunk == 2;
+  const bool tiny = t.pos_dim == 63 && t.dir_dim == 27 && t.view == t.width && t.trunk == 2 && t.skip < 0;
   if (!tiny) return false;
   if (t.width == 32) { launch_fp32_w32(packed, L, S, io, st); return true; }
   if (t.width == 64) { launch_fp32_w64(packed, L, S, io, st); return true; }
@@ -16,7 +16,8 @@ static bool launch_fp32(const LayerTable& t, const float* packed, const TileSche
 }
 
 bool prepare_mlp_fp32(const LayerTable& t) {
-  return t.pos_dim == 63 && t.dir_dim == 27 && t.view == t.width && t.trunk == 2 && (t.width == 32 || t.width == 64);
+  return t.pos_dim == 63 && t.dir_dim == 27 && t.view == t.width && t.trunk == 2 && t.skip < 0 &&
+         (t.width == 32 || t.width == 64);
 }
 
 bool launch_mlp_fp32_render(const LayerTable& t, const float* packed, const TileSched& S, const RenderIO& io,

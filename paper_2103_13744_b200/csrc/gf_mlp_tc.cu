@@ -642,7 +642,8 @@ __global__ void k_pack_tc(PackArgsTc A, int64_t n_cells, uint8_t* packed) {
 }
 
 static bool tc_supported(const LayerTable& t) {
-  return t.pos_dim == 63 && t.dir_dim == 27 && t.view == t.width && t.trunk == 2 && (t.width == 32 || t.width == 64);
+  return t.pos_dim == 63 && t.dir_dim == 27 && t.view == t.width && t.trunk == 2 && t.skip < 0 &&
+         (t.width == 32 || t.width == 64);
 }
 
 size_t fp16_cell_bytes(const LayerTable& t) {

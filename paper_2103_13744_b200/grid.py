@@ -14,6 +14,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _device as D
+import ctypes as C
+
 from . import _native as N
 from . import batched, mlp
 from .core import Aabb, PositionalEncoding, bin_point, flatten_cell_index, raise_if_out_of_bounds, validate_resolution
@@ -63,10 +65,19 @@ class NetworkGrid:
 
     # ---- device side -------------------------------------------------------
     def resolved_precision(self, precision=None, render: bool = False) -> str:
-        p = precision or self.precision or (RENDER_DEFAULT_PRECISION if render else DEFAULT_PRECISION)
+        p = precision or self.precision
+        if p is None:
+            p = RENDER_DEFAULT_PRECISION if render else DEFAULT_PRECISION
+            if p == "fp16" and not self.tensor_core_arch():
+                p = "fp32"  # manifests the tcgen05 kernel does not cover run the generic fp32 kernel
         if p not in N.PRECISION:
             raise ValueError(f"unknown precision {p!r}; expected one of {sorted(N.PRECISION)}")
         return p
+
+    def tensor_core_arch(self) -> bool:
+        """True if the fused tcgen05 kernel covers this manifest (4 hidden
+        layers of width 32 or 64, no skip layer, 10/4 octaves with raw input)."""
+        return N.lib().gf_packed_bytes(C.byref(self.native_arch()), 1, N.PRECISION["fp16"]) > 0
 
     def native_arch(self) -> N.Arch:
         return N.make_arch(self.arch, self.encoding)

@@ -77,6 +77,14 @@ class TrainConfig:
     background: tuple = (1.0, 1.0, 1.0)
     log_every: int = 100
 
+    @classmethod
+    def desk_preset(cls, seed: int = 0) -> "TrainConfig":
+        """train.py:75-91: the scaled-down schedule (128x128 toy scenes); its
+        6 x 96 skip-2 teacher runs on the generic device MLP."""
+        return cls(batch_size_pixels=640, teacher_steps=3200, distill_steps=1200, finetune_steps=2600,
+                   distill_points_per_cell=24, k_train=128, occupancy_factor=4, teacher_hidden_layers=6,
+                   teacher_hidden_width=96, teacher_direction_width=64, teacher_skip_layer=2, seed=seed)
+
     def teacher_architecture(self, encoding) -> mlp.MlpArchitecture:
         return mlp.teacher_architecture(hidden_layers=self.teacher_hidden_layers,
                                         hidden_width=self.teacher_hidden_width,

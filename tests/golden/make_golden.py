@@ -518,9 +518,55 @@ def gen_c2():
     save("render_c2", **out)
 
 
+def gen_generic():
+    """Manifests the fused tiny-MLP kernels do not cover (mlp.py:30-109),
+    through the reference: the default teacher (10 x 256, skip 5, view 128)
+    and the desk preset's teacher (6 x 96, skip 2, view 64) queried on random
+    points; a traced render of a (2,2,2) lattice of 5 x 48 skip-2 networks
+    with 6/3 octaves; and one distill_step with TrainConfig's default
+    teacher (train.py:341-390)."""
+    from gridfield import train
+
+    out = {}
+    aabb = unit()
+    enc = core.PositionalEncoding()
+    rng = np.random.default_rng(21)
+    for tag, arch, res, n in (("teach", mlp.teacher_architecture(), (1, 1, 1), 384),
+                              ("desk", train.TrainConfig.desk_preset().teacher_architecture(enc), (2, 1, 1), 300)):
+        g = ggrid.init_network_grid(aabb, res, seed=23, arch=arch, encoding=enc)
+        for k_ in g.params.biases:
+            g.params.biases[k_][:] = rng.normal(0, 0.2, g.params.biases[k_].shape).astype(np.float32)
+        pts = rng.uniform(-1, 1, (n, 3)).astype(np.float32)
+        dirs = rng.normal(size=(n, 3)).astype(np.float32)
+        dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+        rgb, sig = g.query_points(pts, dirs)
+        out.update({f"{tag}_pts": pts, f"{tag}_dirs": dirs, f"{tag}_rgb": rgb, f"{tag}_sigma": sig,
+                    f"{tag}_res": np.array(res), f"{tag}_biases": np.concatenate([np.asarray(v).ravel() for v in g.params.biases.values()])})
+    # traced render through a skip-layer lattice with non-default octaves
+    enc63 = core.PositionalEncoding(num_freqs_position=6, num_freqs_direction=3)
+    arch = mlp.MlpArchitecture(hidden_layers=5, hidden_width=48, position_input_dim=enc63.position_dim,
+                               direction_input_dim=enc63.direction_dim, direction_layer_width=40, skip_layer=2)
+    g = ggrid.init_network_grid(aabb, (2, 2, 2), seed=24, arch=arch, encoding=enc63)
+    g.params.biases["density"][:] = 4.0
+    cam = scene.sphere_cameras(aabb, 1, 24, seed=2)[0]
+    cfg = render.RenderConfig(k=64)
+    img, st = render.render_image(g, None, cam, cfg, seed=0)
+    out.update(rimg=img, rstats=np.array([st.total_queries, st.ess_skipped, st.ert_terminated_rays, st.n_rays], np.int64))
+    out.update(cam_arrays(cam))
+    # one distill_step with the default teacher
+    dcfg = train.TrainConfig(distill_points_per_cell=4)
+    teacher = ggrid.init_network_grid(aabb, (1, 1, 1), seed=25, arch=dcfg.teacher_architecture(enc), encoding=enc)
+    student = ggrid.init_network_grid(aabb, (2, 2, 2), seed=26)
+    stt = train.AdamState.for_params(student.params)
+    out["ds_loss"] = np.array([train.distill_step(student, teacher, dcfg, stt, np.random.default_rng(27), delta_ref=0.01)])
+    out.update(_grads_dict("ds_p_", student.params))
+    save("generic", **out)
+    print("  distill loss", out["ds_loss"], "render Q", st.total_queries)
+
+
 def main():
     what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt", "extract",
-                            "train", "c2"]
+                            "train", "c2", "generic"]
     for w in what:
         t = time.time()
         globals()[f"gen_{w}"]()

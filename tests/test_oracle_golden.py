@@ -222,3 +222,27 @@ def test_c2_sampled_blocks_match_reference(tag, bias):
     assert np.array_equal(st, z[f"{tag}_block_stats"][pick])
     assert np.max(np.abs(rgb - z[f"{tag}_block_rgb"][rows])) <= 1e-6
     assert z[f"{tag}_stats"][0] == (11_795_580 if bias is None else 6_481_005)  # SURVEY §8 probe
+
+
+@pytest.mark.parametrize("tag", ["teach", "desk"])
+def test_generic_manifest_oracle_pinned(tag):
+    """The oracle's forward with a skip layer and a separate direction width
+    (mlp.py:236-251) reproduces the reference's teacher queries
+    (tests/golden/generic.npz) -- the checker the device tests lean on."""
+    import paper_2103_13744_b200 as gf
+    from paper_2103_13744_b200 import train
+
+    z = golden("generic")
+    enc = gf.PositionalEncoding()
+    arch = gf.teacher_architecture() if tag == "teach" else train.TrainConfig.desk_preset().teacher_architecture(enc)
+    g = gf.init_network_grid(gf.Aabb((-1.0,) * 3, (1.0,) * 3), tuple(int(v) for v in z[f"{tag}_res"]), seed=23,
+                             arch=arch, encoding=enc)
+    flat, o = z[f"{tag}_biases"], 0
+    for k in g.params.biases:
+        n = g.params.biases[k].size
+        g.params.biases[k][...] = flat[o : o + n].reshape(g.params.biases[k].shape)
+        o += n
+    lat = O.lattice_from_grid(g)
+    rgb, sig = O.query_points(lat, z[f"{tag}_pts"], z[f"{tag}_dirs"])
+    assert np.abs(rgb - z[f"{tag}_rgb"]).max() <= 1e-6
+    assert np.abs(sig - z[f"{tag}_sigma"]).max() <= 1e-5 * max(1.0, float(np.abs(z[f"{tag}_sigma"]).max()))
