@@ -223,6 +223,30 @@ GF_API int gf_render_rays_analytic(const gf_analytic_t* scene, const gf_grid_geo
                                    int64_t trace_capacity, int64_t* trace_count_dev, void* ws_dev, size_t ws_bytes,
                                    void* stream);
 
+/* --- caller-evaluated fields (render.py:361-364 field protocol) -----------
+ * Any field object with aabb + query_points: the device marches, places and
+ * composites as for the built-in fields, and once per round group hands the
+ * caller the group's queried samples.  The callback gets the sorted sample
+ * records (float4 x, y, z, staging index bits), their count n, the per-ray
+ * direction records (float4, ray = index >> stride_shift, or index / stride
+ * when stride_shift < 0) and the result buffer (float4 r, g, b, sigma by
+ * staging index); gf_field_gather / gf_field_scatter convert between those
+ * and plain (n, 3) / (n,) arrays.  Nonzero return aborts the render.  No
+ * CUDA graph: the stream is synchronised before each callback.            */
+typedef int (*gf_field_fn)(void* user, const void* srec_dev, int64_t n, const void* ray_dir_dev,
+                           int32_t stride_shift, uint32_t stride, void* res_dev, void* stream);
+GF_API size_t gf_render_field_workspace_bytes(const gf_grid_geom_t* box, const gf_march_cfg_t* cfg, int64_t n_rays);
+GF_API int gf_render_rays_field(gf_field_fn fn, void* user, const gf_grid_geom_t* box, const gf_grid_geom_t* occ,
+                                const uint8_t* occ_bits_dev, const gf_march_cfg_t* cfg, const gf_camera_t* cam,
+                                const float* origins_dev, const float* dirs_dev, int64_t ray_offset,
+                                int64_t ray_block_stride, int64_t n_rays, float* rgb_dev, int64_t* stats_dev,
+                                gf_trace_rec_t* trace_dev, int64_t trace_capacity, int64_t* trace_count_dev,
+                                void* ws_dev, size_t ws_bytes, void* stream);
+GF_API int gf_field_gather(const void* srec_dev, int64_t n, const void* ray_dir_dev, int32_t stride_shift,
+                           uint32_t stride, float* pos_dev, float* dir_dev, void* stream);
+GF_API int gf_field_scatter(const void* srec_dev, int64_t n, const float* rgb_dev, const float* sigma_dev,
+                            void* res_dev, void* stream);
+
 /* Grouped-order rows of a query batch (batched.py:73-78 positions[order]):
  * out[j] = float32(x[idx[j]]) for (n, 3) rows, x float32 or float64.       */
 GF_API int gf_gather_rows3(const void* x_dev, int32_t x_f64, const int64_t* idx_dev, int64_t n, float* out_dev,
@@ -249,6 +273,37 @@ GF_API int gf_extract_occupancy_network(const gf_arch_t* arch, const gf_grid_geo
                                         int precision, const float* direction, const gf_grid_geom_t* occ, double tau,
                                         int64_t chunk_cells, uint8_t* bits_dev, int64_t* err_dev, void* ws_dev,
                                         size_t ws_bytes, void* stream);
+
+/* --- mlp.forward / mlp.backward (mlp.py:222-316) ---------------------------
+ * The reference's plain network API on ALREADY-ENCODED inputs, for any
+ * manifest (depth, widths, skip layer) and a stack of n_net networks, in
+ * float32 (f64 = 0) or float64 (f64 = 1).  w[l] / b[l]: layer l of the
+ * manifest, (n_net, out, in) / (n_net, out); x_enc (n_net, rows, pos_dim),
+ * d_enc (n_net, rows, dir_dim); color (n_net, rows, 3), sigma (n_net, rows).
+ * forward optionally writes the activations backward consumes (mlp.py:252-
+ * 256): hs[k] (n_net, rows, width) per trunk layer, feat (.., width), g (..,
+ * view); NULL skips them.  backward takes those activations plus color /
+ * sigma and the upstream d_color / d_sigma and writes gw[l] / gb[l] (same
+ * shapes as w / b), summed over the rows in a fixed order.                 */
+typedef struct {
+  int32_t hidden_layers;   /* >= 3 (mlp.py:30-64)                              */
+  int32_t width;
+  int32_t view_width;      /* direction-layer width; 0: width                 */
+  int32_t pos_dim;         /* position_input_dim                              */
+  int32_t dir_dim;         /* direction_input_dim                             */
+  int32_t skip_layer;      /* 0: none                                         */
+} gf_manifest_t;
+
+GF_API int gf_mlp_forward(const gf_manifest_t* m, int32_t f64, int64_t n_net, int64_t rows,
+                          const void* const* w_dev, const void* const* b_dev, const void* x_enc_dev,
+                          const void* d_enc_dev, void* color_dev, void* sigma_dev, void* const* hs_dev,
+                          void* feat_dev, void* g_dev, void* stream);
+GF_API size_t gf_mlp_backward_workspace_bytes(const gf_manifest_t* m, int32_t f64, int64_t n_net, int64_t rows);
+GF_API int gf_mlp_backward(const gf_manifest_t* m, int32_t f64, int64_t n_net, int64_t rows,
+                           const void* const* w_dev, const void* x_enc_dev, const void* d_enc_dev,
+                           const void* const* hs_dev, const void* feat_dev, const void* g_dev, const void* color_dev,
+                           const void* sigma_dev, const void* d_color_dev, const void* d_sigma_dev,
+                           void* const* gw_dev, void* const* gb_dev, void* ws_dev, size_t ws_bytes, void* stream);
 
 /* --- training ----------------------------------------------
  * batched.grouped_backward (batched.py:154-187) + mlp.backward (mlp.py:269-316):

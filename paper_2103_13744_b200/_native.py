@@ -31,6 +31,23 @@ class Arch(C.Structure):
     ]
 
 
+# gf_field_fn: (user, srec, n, ray_dir, stride_shift, stride, res, stream) -> status
+FIELD_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_uint32, C.c_void_p,
+                       C.c_void_p)
+
+
+class Manifest(C.Structure):
+    _fields_ = [
+        ("hidden_layers", C.c_int32), ("width", C.c_int32), ("view_width", C.c_int32),
+        ("pos_dim", C.c_int32), ("dir_dim", C.c_int32), ("skip_layer", C.c_int32),
+    ]
+
+
+def make_manifest(arch) -> Manifest:
+    return Manifest(int(arch.hidden_layers), int(arch.hidden_width), int(arch.view_width),
+                    int(arch.position_input_dim), int(arch.direction_input_dim), int(arch.skip_layer or 0))
+
+
 class GridGeom(C.Structure):
     _fields_ = [("b_min", C.c_double * 3), ("b_max", C.c_double * 3), ("res", C.c_int32 * 3)]
 
@@ -106,6 +123,18 @@ _SIGS = {
     "gf_extract_occupancy_network": (C.c_int, [C.POINTER(Arch), C.POINTER(GridGeom), _P, C.c_int,
                                                C.POINTER(C.c_float), C.POINTER(GridGeom), C.c_double, C.c_int64, _P,
                                                _P, _P, C.c_size_t, _P]),
+    "gf_render_field_workspace_bytes": (C.c_size_t, [C.POINTER(GridGeom), C.POINTER(MarchCfg), C.c_int64]),
+    "gf_render_rays_field": (C.c_int, [FIELD_FN, _P, C.POINTER(GridGeom), C.POINTER(GridGeom), _P,
+                                       C.POINTER(MarchCfg), C.POINTER(CameraT), _P, _P, C.c_int64, C.c_int64,
+                                       C.c_int64, _P, _P, _P, C.c_int64, _P, _P, C.c_size_t, _P]),
+    "gf_field_gather": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_uint32, _P, _P, _P]),
+    "gf_field_scatter": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P]),
+    "gf_mlp_forward": (C.c_int, [C.POINTER(Manifest), C.c_int32, C.c_int64, C.c_int64, C.POINTER(_P), C.POINTER(_P),
+                                 _P, _P, _P, _P, C.POINTER(_P), _P, _P, _P]),
+    "gf_mlp_backward_workspace_bytes": (C.c_size_t, [C.POINTER(Manifest), C.c_int32, C.c_int64, C.c_int64]),
+    "gf_mlp_backward": (C.c_int, [C.POINTER(Manifest), C.c_int32, C.c_int64, C.c_int64, C.POINTER(_P), _P, _P,
+                                  C.POINTER(_P), _P, _P, _P, _P, _P, _P, C.POINTER(_P), C.POINTER(_P), _P,
+                                  C.c_size_t, _P]),
     "gf_grouped_backward_workspace_bytes": (C.c_size_t, [C.POINTER(Arch), C.c_int64, C.c_int64]),
     "gf_grouped_backward": (C.c_int, [C.POINTER(Arch), C.c_int64, _P, _P, _P, C.c_int64, _P, _P, _P, _P,
                                       C.POINTER(_P), C.POINTER(_P), _P, C.c_size_t, _P]),

@@ -157,11 +157,39 @@ def grouped_backward_device(grid, layout: GroupedLayout, cache: GroupedCache, d_
     wp = (N.C.c_void_p * len(gw))(*[x.data_ptr() for x in gw])
     bp = (N.C.c_void_p * len(gb))(*[x.data_ptr() for x in gb])
     arch = grid.native_arch()
-    ws = D.workspace(N.lib().gf_grouped_backward_workspace_bytes(arch, grid.n_cells, n))
+    ws_bytes = N.lib().gf_grouped_backward_workspace_bytes(arch, grid.n_cells, n)
+    if ws_bytes == 0 and n > 0:
+        _grouped_backward_dense(grid, cache, dc, ds, flat, gw, gb)
+        return gw, gb, flat
+    ws = D.workspace(ws_bytes)
     N.check(N.lib().gf_grouped_backward(arch, grid.n_cells, N.ptr(cache.packed), N.ptr(cache.pos), N.ptr(cache.dirs),
                                         n, N.ptr(cache.offsets), N.ptr(cache.order), N.ptr(dc), N.ptr(ds), wp, bp,
                                         N.ptr(ws), ws.numel(), D.stream_handle()), "grouped_backward")
     return gw, gb, flat
+
+
+def _grouped_backward_dense(grid, cache: GroupedCache, dc, ds, flat, gw, gb):
+    """Manifests without a fused backward kernel (any depth / width / skip
+    layer): each queried cell's rows go through the device encoding and
+    mlp.backward's dense kernels (gf_mlp_forward / gf_mlp_backward)."""
+    from . import mlp
+
+    flat.zero_()
+    offs = cache.offsets.cpu().numpy()
+    order = cache.order.cpu().numpy()
+    pos = cache.pos.cpu().numpy().reshape(-1, 3)
+    dirs = cache.dirs.cpu().numpy().reshape(-1, 3)
+    dc_h = dc.cpu().numpy()[order]
+    ds_h = ds.cpu().numpy()[order]
+    specs = grid.arch.layers()
+    for c in np.nonzero(offs[1:] > offs[:-1])[0]:
+        rows = slice(int(offs[c]), int(offs[c + 1]))
+        x = grid.encoding.encode_position(pos[rows])
+        d = grid.encoding.encode_direction(dirs[rows])
+        g = mlp.backward(grid.params.at(int(c)).astype(np.float32), x, d, dc_h[rows], ds_h[rows])
+        for s_, w_, b_ in zip(specs, gw, gb):
+            w_[int(c)].copy_(D.to_device(g.weights[s_.name], w_.dtype))
+            b_[int(c)].copy_(D.to_device(g.biases[s_.name], b_.dtype))
 
 
 def grouped_backward(grid, layout: GroupedLayout, caches: list, d_color, d_sigma):

@@ -456,6 +456,35 @@ int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packe
   return check_cuda("gf_grouped_forward");
 }
 
+int gf_mlp_forward(const gf_manifest_t* m, int32_t f64, int64_t n_net, int64_t rows, const void* const* w,
+                   const void* const* b, const void* x, const void* d, void* color, void* sigma, void* const* hs,
+                   void* feat, void* g, void* stream) {
+  if (!m || !dense_mlp_supported(m) || n_net < 0 || rows < 0 || !w || !b)
+    return fail(GF_ERR_INVALID, "gf_mlp_forward: unsupported manifest or bad sizes");
+  if (!launch_dense_forward(m, f64, n_net, rows, w, b, x, d, color, sigma, hs, feat, g, (cudaStream_t)stream))
+    return fail(GF_ERR_UNSUPPORTED, "gf_mlp_forward: manifest too wide for the dense kernel");
+  return check_cuda("gf_mlp_forward");
+}
+
+size_t gf_mlp_backward_workspace_bytes(const gf_manifest_t* m, int32_t f64, int64_t n_net, int64_t rows) {
+  if (!m || !dense_mlp_supported(m) || n_net < 0 || rows < 0) return 0;
+  return dense_backward_workspace(m, f64, n_net, rows);
+}
+
+int gf_mlp_backward(const gf_manifest_t* m, int32_t f64, int64_t n_net, int64_t rows, const void* const* w,
+                    const void* x, const void* d, const void* const* hs, const void* feat, const void* g,
+                    const void* color, const void* sigma, const void* d_color, const void* d_sigma, void* const* gw,
+                    void* const* gb, void* ws, size_t ws_bytes, void* stream) {
+  if (!m || !dense_mlp_supported(m) || n_net < 0 || rows < 0 || !w || !gw || !gb || !hs)
+    return fail(GF_ERR_INVALID, "gf_mlp_backward: unsupported manifest or bad sizes");
+  if (dense_backward_workspace(m, f64, n_net, rows) > ws_bytes)
+    return fail(GF_ERR_WORKSPACE, "gf_mlp_backward: workspace too small");
+  if (!launch_dense_backward(m, f64, n_net, rows, w, x, d, hs, feat, g, color, sigma, d_color, d_sigma, gw, gb, ws,
+                             (cudaStream_t)stream))
+    return fail(GF_ERR_UNSUPPORTED, "gf_mlp_backward: manifest too wide for the dense kernel");
+  return check_cuda("gf_mlp_backward");
+}
+
 size_t gf_grouped_workspace_bytes(int64_t n_cells, int64_t n) {
   Carve c(nullptr);
   QueryWs w;
@@ -565,13 +594,37 @@ size_t gf_render_workspace_bytes(const gf_arch_t* arch, const gf_grid_geom_t* gr
 // per-cell MLPs) or an analytic scene (an != NULL: one bucket, closed-form
 // field).  Everything else (rays, sampling, ESS, compositing, ERT, graphs)
 // is shared.
-static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_grid_geom_t* grid, const void* packed,
+struct ExtField {
+  gf_field_fn fn;
+  void* user;
+};
+
+__global__ void k_field_gather(const float4* __restrict__ srec, int64_t n, const float4* __restrict__ ray_dir,
+                               int shift, uint32_t stride, float* pos, float* dir) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 r = srec[i];
+    const uint32_t idx = __float_as_uint(r.w);
+    const float4 d = ray_dir[shift >= 0 ? idx >> shift : idx / stride];
+    pos[3 * i] = r.x; pos[3 * i + 1] = r.y; pos[3 * i + 2] = r.z;
+    dir[3 * i] = d.x; dir[3 * i + 1] = d.y; dir[3 * i + 2] = d.z;
+  }
+}
+
+__global__ void k_field_scatter(const float4* __restrict__ srec, int64_t n, const float* __restrict__ rgb,
+                                const float* __restrict__ sigma, float4* res) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    res[__float_as_uint(srec[i].w)] = make_float4(rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2], sigma[i]);
+}
+
+static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtField* ext, const gf_grid_geom_t* grid,
+                       const void* packed,
                        int precision, const gf_grid_geom_t* occ, const uint8_t* occ_bits, const gf_march_cfg_t* cfg,
                        const gf_camera_t* cam, const float* origins, const float* dirs, int64_t ray_offset,
                        int64_t ray_block_stride, int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace,
                        int64_t trace_capacity, int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
   LayerTable t{};  // value-initialised: hashed into the graph key
-  if (!an && (!arch || !make_layer_table(arch, &t))) return fail(GF_ERR_INVALID, "gf_render_rays: bad architecture");
+  if (!an && !ext && (!arch || !make_layer_table(arch, &t)))
+    return fail(GF_ERR_INVALID, "gf_render_rays: bad architecture");
   if (!valid_grid(grid)) return fail(GF_ERR_INVALID, "gf_render_rays: bad grid");
   if (!cfg || cfg->k < 1 || cfg->ert_chunk < 1 || !(cfg->epsilon >= 0.0 && cfg->epsilon < 1.0))
     return fail(GF_ERR_INVALID, "gf_render_rays: bad march config");
@@ -741,7 +794,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
     if ((1 << b) == stride) stride_shift = b;
   if (an || precision != GF_PRECISION_FP16) w.R.denc = nullptr;  // only the tensor-core MLP reads gamma(d) per ray
   RenderIO io{w.RB.res, w.R.dir, (uint32_t)stride, w.R.denc, stride_shift};
-  const bool mlp_ok = an                                 ? true
+  const bool mlp_ok = (an || ext)                        ? true
                       : precision == GF_PRECISION_FP16   ? prepare_mlp_tc(t)
                       : precision == GF_PRECISION_FP32 ? (prepare_mlp_fp32(t) || prepare_mlp_generic(t, arch))
                                                        : false;
@@ -749,6 +802,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
 
   // the frame's launch sequence (captured once into a CUDA graph per
   // argument set and replayed; eager when instrumented)
+  int ext_status = GF_OK;  // a caller-evaluated field's callback failed
   auto enqueue = [&](cudaStream_t s) {
     // memsets first, so the setup kernels and the round chain form one
     // uninterrupted run of programmatic dependent launches
@@ -772,11 +826,20 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
       stage_mark(s, GF_STAGE_MARCH, passes);
       stage_mark(s, GF_STAGE_SCATTER, launch_place(P.grid, w.RB, w.R.run, w.B, nc, stride, step > 1 ? P.chunk : 0,
                                                    r / step, (int64_t)n_rays * stride, s));
-      if (an)
+      if (an) {
         launch_field_analytic(*an, w.B.offsets, w.B.srec, w.R.dir, stride_shift, (uint32_t)stride, w.RB.res,
                               (int64_t)n_rays * stride, s);
-      else
+      } else if (ext) {
+        // the group's sample count (one bucket: offsets[1]), then the caller
+        uint32_t q = 0;
+        cudaMemcpyAsync(&q, w.B.offsets + nc, sizeof(q), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (ext_status == GF_OK && q > 0 &&
+            ext->fn(ext->user, w.B.srec, (int64_t)q, w.R.dir, stride_shift, (uint32_t)stride, w.RB.res, s) != 0)
+          ext_status = GF_ERR_UNSUPPORTED;
+      } else {
         run_mlp(t, arch, packed, precision, S, &io, nullptr, s);
+      }
       stage_mark(s, GF_STAGE_MLP, 1);
     }
     // final pass: composite the last group of rounds and write the colours
@@ -784,9 +847,10 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const gf_gr
     stage_mark(s, GF_STAGE_MARCH, 1);
   };
   // every precision replays a cached graph; traces and stage timing run eagerly
-  const bool use_graph = !g_timer.on && !trace && !getenv("GF_NO_GRAPH");
+  const bool use_graph = !g_timer.on && !trace && !ext && !getenv("GF_NO_GRAPH");
   if (!use_graph) {
     enqueue(st);
+    if (ext_status != GF_OK) return fail(ext_status, "gf_render_rays_field: the field callback failed");
     return check_cuda("gf_render_rays");
   }
   GraphKey key;  // every value a launch above reads on the host
@@ -828,7 +892,7 @@ int gf_render_rays(const gf_arch_t* arch, const gf_grid_geom_t* grid, const void
                    const gf_camera_t* cam, const float* origins, const float* dirs, int64_t ray_offset,
                    int64_t ray_block_stride, int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace,
                    int64_t trace_capacity, int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
-  return render_impl(arch, nullptr, grid, packed, precision, occ, occ_bits, cfg, cam, origins, dirs, ray_offset,
+  return render_impl(arch, nullptr, nullptr, grid, packed, precision, occ, occ_bits, cfg, cam, origins, dirs, ray_offset,
                      ray_block_stride, n_rays, rgb, stats, trace, trace_capacity, trace_count, ws, ws_bytes, stream);
 }
 
@@ -860,8 +924,48 @@ int gf_render_rays_analytic(const gf_analytic_t* scene, const gf_grid_geom_t* oc
   memset(&A, 0, sizeof(A));
   if (!make_analytic(scene, &A)) return fail(GF_ERR_INVALID, "gf_render_rays_analytic: bad scene");
   const gf_grid_geom_t g = analytic_box(scene);
-  return render_impl(nullptr, &A, &g, nullptr, GF_PRECISION_FP32, occ, occ_bits, cfg, cam, origins, dirs, ray_offset,
+  return render_impl(nullptr, &A, nullptr, &g, nullptr, GF_PRECISION_FP32, occ, occ_bits, cfg, cam, origins, dirs, ray_offset,
                      ray_block_stride, n_rays, rgb, stats, trace, trace_capacity, trace_count, ws, ws_bytes, stream);
+}
+
+size_t gf_render_field_workspace_bytes(const gf_grid_geom_t* box, const gf_march_cfg_t* cfg, int64_t n_rays) {
+  if (!box) return 0;
+  gf_grid_geom_t g = *box;
+  g.res[0] = g.res[1] = g.res[2] = 1;  // one bucket: the caller's field has no cells
+  return gf_render_workspace_bytes(nullptr, &g, cfg, n_rays);
+}
+
+int gf_render_rays_field(gf_field_fn fn, void* user, const gf_grid_geom_t* box, const gf_grid_geom_t* occ,
+                         const uint8_t* occ_bits, const gf_march_cfg_t* cfg, const gf_camera_t* cam,
+                         const float* origins, const float* dirs, int64_t ray_offset, int64_t ray_block_stride,
+                         int64_t n_rays, float* rgb, int64_t* stats, gf_trace_rec_t* trace, int64_t trace_capacity,
+                         int64_t* trace_count, void* ws, size_t ws_bytes, void* stream) {
+  if (!fn || !box) return fail(GF_ERR_INVALID, "gf_render_rays_field: no field callback or box");
+  gf_grid_geom_t g = *box;
+  g.res[0] = g.res[1] = g.res[2] = 1;
+  const ExtField E{fn, user};
+  return render_impl(nullptr, nullptr, &E, &g, nullptr, GF_PRECISION_FP32, occ, occ_bits, cfg, cam, origins, dirs,
+                     ray_offset, ray_block_stride, n_rays, rgb, stats, trace, trace_capacity, trace_count, ws,
+                     ws_bytes, stream);
+}
+
+int gf_field_gather(const void* srec, int64_t n, const void* ray_dir, int32_t stride_shift, uint32_t stride,
+                    float* pos, float* dir, void* stream) {
+  if (n < 0 || (n > 0 && (!srec || !ray_dir || !pos || !dir)) || (stride_shift < 0 && stride == 0))
+    return fail(GF_ERR_INVALID, "gf_field_gather: bad arguments");
+  if (n > 0)
+    k_field_gather<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8), 256, 0,
+                     (cudaStream_t)stream>>>((const float4*)srec, n, (const float4*)ray_dir, stride_shift, stride, pos,
+                                             dir);
+  return check_cuda("gf_field_gather");
+}
+
+int gf_field_scatter(const void* srec, int64_t n, const float* rgb_, const float* sigma, void* res, void* stream) {
+  if (n < 0 || (n > 0 && (!srec || !rgb_ || !sigma || !res))) return fail(GF_ERR_INVALID, "gf_field_scatter: bad arguments");
+  if (n > 0)
+    k_field_scatter<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8), 256, 0,
+                      (cudaStream_t)stream>>>((const float4*)srec, n, rgb_, sigma, (float4*)res);
+  return check_cuda("gf_field_scatter");
 }
 
 int gf_query_analytic(const gf_analytic_t* scene, const float* pos, const float* dir, int64_t n, float* rgb,

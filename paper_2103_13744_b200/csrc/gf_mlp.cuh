@@ -175,6 +175,18 @@ bool launch_mlp_generic_query(const LayerTable& t, const gf_arch_t* arch, const 
                               const QueryIO& io, cudaStream_t st);
 bool prepare_mlp_generic(const LayerTable& t, const gf_arch_t* arch);
 
+// mlp.forward / mlp.backward on encoded inputs, any manifest, f32 / f64:
+// gf_mlp_dense.cu
+bool dense_mlp_supported(const gf_manifest_t* m);
+size_t dense_backward_workspace(const gf_manifest_t* m, int f64, int64_t n_net, int64_t rows);
+bool launch_dense_forward(const gf_manifest_t* m, int f64, int64_t n_net, int64_t rows, const void* const* w,
+                          const void* const* b, const void* x, const void* d, void* color, void* sigma,
+                          void* const* hs, void* feat, void* g, cudaStream_t st);
+bool launch_dense_backward(const gf_manifest_t* m, int f64, int64_t n_net, int64_t rows, const void* const* w,
+                           const void* x, const void* d, const void* const* hs, const void* feat, const void* g,
+                           const void* color, const void* sigma, const void* d_color, const void* d_sigma,
+                           void* const* gw, void* const* gb, void* ws, cudaStream_t st);
+
 int num_sms();
 
 // one-time per-process launch setup (smem attribute, residency) done outside

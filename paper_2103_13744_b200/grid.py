@@ -15,6 +15,7 @@ import numpy as np
 
 from . import _device as D
 import ctypes as C
+import os
 
 from . import _native as N
 from . import batched, mlp
@@ -27,7 +28,7 @@ from .core import Aabb, PositionalEncoding, bin_point, flatten_cell_index, raise
 # queries (query_points / grouped_forward) keep the fp32 SIMT kernel, since
 # the reference compares raw network outputs at 1e-6 (test_batched.py:94).
 DEFAULT_PRECISION = "fp32"
-RENDER_DEFAULT_PRECISION = "fp16"
+RENDER_DEFAULT_PRECISION = "fp16"  # GF_RENDER_PRECISION=fp32 restores the reference's float32 renders
 
 
 @dataclass
@@ -67,7 +68,7 @@ class NetworkGrid:
     def resolved_precision(self, precision=None, render: bool = False) -> str:
         p = precision or self.precision
         if p is None:
-            p = RENDER_DEFAULT_PRECISION if render else DEFAULT_PRECISION
+            p = (os.environ.get("GF_RENDER_PRECISION") or RENDER_DEFAULT_PRECISION) if render else DEFAULT_PRECISION
             if p == "fp16" and not self.tensor_core_arch():
                 p = "fp32"  # manifests the tcgen05 kernel does not cover run the generic fp32 kernel
         if p not in N.PRECISION:

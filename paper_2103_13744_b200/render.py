@@ -245,15 +245,18 @@ def composite(colors, alphas):
 # ---------------------------------------------------------------------------
 def _field_grid(field):
     """render.py:361-364 field protocol: NetworkGrid (per-cell MLPs) and
-    AnalyticScene (closed-form field) both march on the device."""
+    AnalyticScene (closed-form field) are evaluated on the device; any other
+    object with ``aabb`` and ``query_points(positions, directions)`` is a
+    caller-evaluated field: the device still marches, places and composites,
+    and hands the field each round group's samples (gf_render_rays_field)."""
     from .grid import NetworkGrid
     from .scene import AnalyticScene
 
     if isinstance(field, (NetworkGrid, AnalyticScene)):
         return field
-    raise NotImplementedError(
-        f"the device marcher evaluates NetworkGrid and AnalyticScene fields; got {type(field).__name__}"
-    )
+    if hasattr(field, "aabb") and callable(getattr(field, "query_points", None)):
+        return field
+    raise TypeError(f"a field needs .aabb and .query_points(positions, directions); got {type(field).__name__}")
 
 
 def _is_analytic(field) -> bool:
@@ -262,10 +265,47 @@ def _is_analytic(field) -> bool:
     return isinstance(field, AnalyticScene)
 
 
+def _is_caller_field(field) -> bool:
+    from .grid import NetworkGrid
+    from .scene import AnalyticScene
+
+    return not isinstance(field, (NetworkGrid, AnalyticScene))
+
+
+def _box_geom(aabb):
+    return N.make_geom(aabb, (1, 1, 1))
+
+
 def _render_ws_bytes(field, ncfg, n: int) -> int:
     if _is_analytic(field):
         return N.lib().gf_render_analytic_workspace_bytes(field.native(), ncfg, n)
+    if _is_caller_field(field):
+        return N.lib().gf_render_field_workspace_bytes(_box_geom(field.aabb), ncfg, n)
     return N.lib().gf_render_workspace_bytes(field.native_arch(), field.native_geom(), ncfg, n)
+
+
+def _field_callback(field, errors: list):
+    """ctypes callback for gf_render_rays_field: gather the group's samples
+    into (n, 3) arrays, evaluate the caller's field, scatter the results."""
+    t = D.torch()
+
+    def cb(user, srec, n, ray_dir, shift, stride, res, stream):
+        try:
+            pos = D.empty((n, 3), t.float32)
+            dirs = D.empty((n, 3), t.float32)
+            N.check(N.lib().gf_field_gather(srec, n, ray_dir, shift, stride, N.ptr(pos), N.ptr(dirs), stream),
+                    "field gather")
+            rgb, sigma = field.query_points(pos.cpu().numpy(), dirs.cpu().numpy())
+            rgb_d = D.to_device(np.asarray(rgb, np.float32).reshape(n, 3), t.float32)
+            sig_d = D.to_device(np.asarray(sigma, np.float32).reshape(n), t.float32)
+            N.check(N.lib().gf_field_scatter(srec, n, N.ptr(rgb_d), N.ptr(sig_d), res, stream), "field scatter")
+            t.cuda.current_stream().synchronize()  # rgb_d / sig_d live until the scatter ran
+            return 0
+        except BaseException as e:  # re-raised by the caller after the library returns
+            errors.append(e)
+            return 1
+
+    return N.FIELD_FN(cb)
 
 
 def shard_rays(n_rays: int, rank: int, world: int) -> tuple[int, int, int]:
@@ -322,7 +362,8 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
     blocks of ``shard_rays`` when ``block_stride`` > 1."""
     t = D.require_cuda()
     analytic = _is_analytic(grid)
-    if not analytic:
+    caller = _is_caller_field(grid)
+    if not analytic and not caller:
         p = grid.resolved_precision(precision, render=True)
         packed = grid.device_params(p)
     if cam is not None:
@@ -348,7 +389,17 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
         tcount = t.zeros(1, dtype=t.int64, device=rgb.device)
     if ws is None:
         ws = D.workspace(_render_ws_bytes(grid, ncfg, n))
-    if analytic:
+    if caller:
+        errors = []
+        fn = _field_callback(grid, errors)
+        status = N.lib().gf_render_rays_field(
+            fn, None, _box_geom(grid.aabb), occ_geom, N.ptr(occ_bits), ncfg, ccam, N.ptr(o_d), N.ptr(d_d),
+            int(ray_offset), int(block_stride), int(n), N.ptr(rgb), N.ptr(st), N.ptr(trace), int(trace_capacity),
+            N.ptr(tcount), N.ptr(ws), ws.numel(), D.stream_handle())
+        if errors:
+            raise errors[0]
+        N.check(status, "render_rays")
+    elif analytic:
         N.check(N.lib().gf_render_rays_analytic(
             grid.native(), occ_geom, N.ptr(occ_bits), ncfg, ccam, N.ptr(o_d), N.ptr(d_d), int(ray_offset),
             int(block_stride), int(n), N.ptr(rgb), N.ptr(st), N.ptr(trace), int(trace_capacity), N.ptr(tcount),

@@ -98,18 +98,32 @@ def test_distill_step_default_teacher_matches_reference():
         assert np.abs(student.params.biases[name] - z[f"ds_p_b_{name}"]).max() <= 2e-6, name
 
 
-def test_generic_backward_is_refused_clearly():
-    """grouped_backward has device kernels for the tiny manifests only: a
-    teacher-sized grid must fail loudly, never fall back to the host."""
+def test_generic_grouped_backward_matches_reference_math():
+    """grouped_backward of a skip-layer grid (no fused backward kernel) runs
+    the dense device kernels per cell; the reference's batched.grouped_backward
+    is mlp.backward per cell on the grouped rows (batched.py:154-187), checked
+    here against the float64 device mlp.backward of the same rows."""
     gf = _gf()
-    from paper_2103_13744_b200 import batched
+    from paper_2103_13744_b200 import batched, mlp
 
     aabb = gf.Aabb((-1.0,) * 3, (1.0,) * 3)
-    g = gf.init_network_grid(aabb, (1, 1, 1), seed=1, arch=gf.teacher_architecture(hidden_layers=5, hidden_width=64))
-    pts = np.zeros((4, 3), np.float32)
-    dirs = np.tile(np.array([[0.0, 0.0, 1.0]], np.float32), (4, 1))
+    g = gf.init_network_grid(aabb, (2, 1, 1), seed=1, arch=gf.teacher_architecture(hidden_layers=5, hidden_width=64))
+    rng = np.random.default_rng(2)
+    pts = rng.uniform(-1, 1, (50, 3)).astype(np.float32)
+    dirs = rng.normal(size=(50, 3)).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=-1, keepdims=True)
+    dc = rng.normal(size=(50, 3)).astype(np.float32)
+    ds = rng.normal(size=50).astype(np.float32)
     layout = batched.group_by_network(batched.QueryBatch(pts, dirs, g.cell_index(pts)), g.n_cells)
     caches = []
     batched.grouped_forward(g, layout, caches=caches)
-    with pytest.raises(Exception, match="backward"):
-        batched.grouped_backward(g, layout, caches, np.ones((4, 3), np.float32), np.ones(4, np.float32))
+    grads = batched.grouped_backward(g, layout, caches, dc, ds)
+    cells = g.cell_index(pts)
+    for c in range(g.n_cells):
+        m = cells == c
+        x = g.encoding.encode_position(pts[m].astype(np.float64))
+        d = g.encoding.encode_direction(dirs[m].astype(np.float64))
+        ref = mlp.backward(g.params.at(c).astype(np.float64), x, d, dc[m].astype(np.float64), ds[m].astype(np.float64))
+        for name in ref.weights:
+            _close(grads.weights[name][c], ref.weights[name], f"cell {c} w {name}", rel=1e-3, scale=1e-4)
+            _close(grads.biases[name][c], ref.biases[name], f"cell {c} b {name}", rel=1e-3, scale=1e-4)

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol(native):
 
 
 def test_abi_version(native):
-    assert native.lib().gf_abi_version() == 1
+    assert native.lib().gf_abi_version() == native.ABI_VERSION == 2
 
 
 def test_pcg64_block_state_matches_numpy_golden(native):
