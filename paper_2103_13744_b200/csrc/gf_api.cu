@@ -505,6 +505,7 @@ struct RenderWs {
   BucketBufs B;
   uint8_t* coarse_tmp;
   uint32_t* coarse_bits;
+  uint32_t* fine_bits;
 };
 
 // occupancy grids are capped at 256^3 (occupancy.py:21); the coarse mip never
@@ -521,6 +522,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->block_ci = c.take<u128>((size_t)GF_CI_N * n_blocks);
   w->coarse_tmp = c.take<uint8_t>((size_t)kMaxCoarseCells);
   w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
+  w->fine_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->R.org = c.take<float4>((size_t)n_rays);
   w->R.dir = c.take<float4>((size_t)n_rays);
   w->R.acc = c.take<float4>((size_t)n_rays);
@@ -708,8 +710,8 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
   // of its nominal segment (seg/2) plus a float32 evaluation margin.
   int coarse_launches = 0;
   struct {
-    bool on = false, word = false;
-    int f = 0, radius = 0;
+    bool on = false, word = false, fine = false;
+    int f = 0, radius = 0, fine_radius = 0;
     int3 ores = {0, 0, 0}, cres = {0, 0, 0};
   } cplan;
   {
@@ -751,6 +753,22 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
         double cmin = 1e300;
         for (int a = 0; a < 3; ++a) cmin = fmin(cmin, (cg.b_max[a] - cg.b_min[a]) / cg.res[a]);
         P.ivl_pad = (float)(0.05 * cmin + 1e-5 * (1.0 + maxabs));
+        // per-candidate pre-test on the occupancy grid itself, dilated by
+        // ceil(reach / fine cell) <= 2 cells: word-parallel dilation of the
+        // fine bitmap (x rows of whole 32-bit words), exact float32 binning
+        // opt-in (GF_FINE=1): exact, but measured slower on C2 (march 0.613 ->
+        // 0.633 ms): the filter pass costs more than the skipped placements
+        const char* nfine = getenv("GF_FINE");
+        double fmin = 1e300;
+        for (int a = 0; a < 3; ++a) fmin = fmin < (occ->b_max[a] - occ->b_min[a]) / occ->res[a]
+                                               ? fmin : (occ->b_max[a] - occ->b_min[a]) / occ->res[a];
+        const int rf = (int)ceil(reach / fmin);
+        if (nfine && nfine[0] == '1' && P.occ.fast && occ->res[0] % 32 == 0 && rf <= 2) {
+          cplan.fine = true;
+          cplan.fine_radius = rf < 1 ? 1 : rf;
+          P.fine_bits = w.fine_bits;
+          coarse_launches += 3;
+        }
       }
     }
   }
@@ -774,6 +792,17 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
                                                                               w.coarse_tmp);
       k_coarse_dilate<<<(unsigned)gf_div_up<int64_t>(gf_div_up<int64_t>(ncc, 32), 128), 128, 0, s>>>(
           w.coarse_tmp, cres, cplan.radius, w.coarse_bits);
+    }
+    if (cplan.fine) {  // the fine pre-test bitmap: occupancy dilated per axis (x, y, z)
+      const int64_t nw = (int64_t)ores.x * ores.y * ores.z / 32;
+      const unsigned gb = (unsigned)gf_div_up<int64_t>(nw, 128);
+      uint32_t* t0 = reinterpret_cast<uint32_t*>(w.coarse_tmp);
+      uint32_t* t1 = t0 + nw;
+      gf_launch_pdl(k_dilate_x, dim3(gb), dim3(128), 0, s, reinterpret_cast<const uint32_t*>(occ_bits), t1, ores,
+                    cplan.fine_radius);
+      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t1, t0, ores, cplan.fine_radius, 1);
+      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, w.fine_bits, ores,
+                    cplan.fine_radius, 2);
     }
   };
 
@@ -865,6 +894,8 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
   key.add(cplan.word);
   key.add(cplan.f);
   key.add(cplan.radius);
+  key.add(cplan.fine);
+  key.add(cplan.fine_radius);
   key.add(cplan.ores);
   key.add(cplan.cres);
   key.add(march_blocks);

@@ -644,7 +644,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o2);
       if ((int)lane >= o2) incl += v;
     }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t total_c = __shfl_sync(0xffffffffu, incl, 31);
     const uint32_t d0 = (uint32_t)draw;  // float32 draw index of slot s0 in the ray's block stream
     {
       RayPar& rp = s_ray[wib][lane];
@@ -655,7 +655,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       rp.i = (uint32_t)i;
       rp.d0 = d0;
       rp.carry = 0;
-      uint32_t msk = cmask, pos = incl - cnt;
+      uint32_t msk = cmask, pos = incl - cnt;  // candidate list in (lane, slot) order
       while (msk) {  // this lane's candidate slots, ascending
         const int j = __ffs(msk) - 1;
         s_list[wib][pos++] = (uint16_t)((lane << 5) | (uint32_t)j);
@@ -663,6 +663,45 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       }
     }
     __syncwarp();
+    uint32_t total = total_c;
+    if (P.fine_bits) {
+      // pre-test at the segment midpoint against the dilated fine bitmap:
+      // the exact sample lies within seg/2 (+ float32 margin) of it, so a
+      // clear bit proves an ESS skip; survivors are compacted in place
+      // (writes never pass the batch being read)
+      constexpr int FU = 4;  // batches in flight: FU bitmap loads per lane before the first ballot
+      uint32_t kept_n = 0;
+      for (uint32_t b0 = 0; b0 < total_c; b0 += 32 * FU) {
+        uint32_t e[FU], word[FU], bit[FU];
+#pragma unroll
+        for (int u = 0; u < FU; ++u) {
+          const uint32_t k = b0 + 32 * u + lane;
+          e[u] = k < total_c ? (uint32_t)s_list[wib][k] : 0xFFFFFFFFu;
+          word[u] = 0u;
+          bit[u] = 0u;
+          if (e[u] != 0xFFFFFFFFu) {
+            const RayPar& rp = s_ray[wib][e[u] >> 5];
+            const float tm = fmaf((float)(s0 + (int)(e[u] & 31u)) + 0.5f, rp.d.w, rp.o.w);
+            const float px = fmaf(tm, rp.d.x, rp.o.x), py = fmaf(tm, rp.d.y, rp.o.y), pz = fmaf(tm, rp.d.z, rp.o.z);
+            const uint32_t f = (uint32_t)(gf_bin_axis_fast(P.occ, 0, px) +
+                                          P.occ.res[0] * (gf_bin_axis_fast(P.occ, 1, py) +
+                                                          P.occ.res[1] * gf_bin_axis_fast(P.occ, 2, pz)));
+            word[u] = __ldg(P.fine_bits + (f >> 5));
+            bit[u] = f & 31u;
+          }
+        }
+        __syncwarp();  // every lane has read its FU entries before any is overwritten
+#pragma unroll
+        for (int u = 0; u < FU; ++u) {
+          const bool pass = e[u] != 0xFFFFFFFFu && ((word[u] >> bit[u]) & 1u);
+          const unsigned pm = __ballot_sync(0xffffffffu, pass);
+          if (pass) s_list[wib][kept_n + __popc(pm & ((1u << lane) - 1u))] = (uint16_t)e[u];
+          kept_n += __popc(pm);
+        }
+        __syncwarp();
+      }
+      total = kept_n;
+    }
     // the record of the previous batch waiting for its cell rank
     bool pend_ok = false;
     uint32_t pend_raw = 0, pend_peers = 0;

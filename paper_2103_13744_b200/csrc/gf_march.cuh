@@ -23,6 +23,8 @@ struct MarchParams {
   GfGrid coarse;      // dilated coarse occupancy mip (empty-space pre-test)
   const uint32_t* coarse_bits;  // NULL: every candidate takes the exact path
   float ivl_pad;      // world-distance padding of the DDA intervals (float32 error)
+  const uint32_t* fine_bits;  // occupancy dilated by >= seg/2 + margin (occupancy geometry): per-candidate
+                              // pre-test at the segment midpoint, before the jitter and the exact placement
   gf_camera_t cam;
   int use_cam;
   const float* origins;
