@@ -506,6 +506,7 @@ struct RenderWs {
   uint8_t* coarse_tmp;
   uint32_t* coarse_bits;
   uint32_t* fine_bits;
+  unsigned long long* stats_part;
 };
 
 // occupancy grids are capped at 256^3 (occupancy.py:21); the coarse mip never
@@ -523,6 +524,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->coarse_tmp = c.take<uint8_t>((size_t)kMaxCoarseCells);
   w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->fine_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
+  w->stats_part = c.take<unsigned long long>((size_t)GF_STAT_SLOTS * GF_STAT_COUNT);
   w->R.org = c.take<float4>((size_t)n_rays);
   w->R.dir = c.take<float4>((size_t)n_rays);
   w->R.acc = c.take<float4>((size_t)n_rays);
@@ -700,6 +702,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
   for (int a = 0; a < 3; ++a) P.bg[a] = cfg->background[a];
   P.rgb_out = rgb;
   P.stats = stats;
+  P.stats_part = w.stats_part;
   P.trace = trace;
   P.trace_capacity = trace ? trace_capacity : 0;
   P.trace_count = trace_count;
@@ -837,6 +840,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
     // uninterrupted run of programmatic dependent launches
     cudaMemsetAsync(w.B.counts, 0, (size_t)2 * nc * 4, s);
     cudaMemsetAsync(w.RB.emit_count, 0, 2 * sizeof(uint32_t), s);
+    cudaMemsetAsync(w.stats_part, 0, (size_t)GF_STAT_SLOTS * GF_STAT_COUNT * 8, s);
     enqueue_coarse(s);
     stage_open(s);
     if (P.stratified)
@@ -873,7 +877,8 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
     }
     // final pass: composite the last group of rounds and write the colours
     gf_launch_pdl(k_march, dim3(march_blocks), dim3(128), 0, s, P, w.R, w.RB, (P.n_rounds + step - 1) / step * step, 0);
-    stage_mark(s, GF_STAGE_MARCH, 1);
+    launch_stats_fold(w.stats_part, stats, s);  // the warps' spread counters -> the caller's RenderStats
+    stage_mark(s, GF_STAGE_MARCH, 2);
   };
   // every precision replays a cached graph; traces and stage timing run eagerly
   const bool use_graph = !g_timer.on && !trace && !ext && !getenv("GF_NO_GRAPH");

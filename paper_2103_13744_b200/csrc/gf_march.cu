@@ -553,6 +553,48 @@ __device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v)
   if (gf_lane() == 0 && v) atomicAdd((unsigned long long*)dst, v);
 }
 
+// RenderStats counters of one marcher thread, flushed once per warp per pass
+// into a spread slot (one global counter per stat serialised ~10^5 atomics
+// per pass); k_stats_fold sums the slots into the caller's stats at the end
+struct MarchStats {
+  unsigned long long v[GF_STAT_COUNT] = {0ull, 0ull, 0ull, 0ull};
+};
+
+__device__ __forceinline__ void flush_stats(const MarchParams& P, MarchStats& S) {  // warp-uniform
+  const uint32_t slot = ((blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5)) & (GF_STAT_SLOTS - 1);
+#pragma unroll
+  for (int c = 0; c < GF_STAT_COUNT; ++c) {
+    unsigned long long v = S.v[c];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (gf_lane() == 0 && v) atomicAdd(P.stats_part + slot * GF_STAT_COUNT + c, v);
+  }
+}
+
+__global__ void k_stats_fold(const unsigned long long* __restrict__ part, int64_t* stats) {
+  gf_pdl_wait();
+  __shared__ unsigned long long acc[GF_STAT_COUNT];
+  if (threadIdx.x < GF_STAT_COUNT) acc[threadIdx.x] = 0ull;
+  __syncthreads();
+  unsigned long long v[GF_STAT_COUNT] = {0ull, 0ull, 0ull, 0ull};
+  for (int s = threadIdx.x; s < GF_STAT_SLOTS; s += blockDim.x)
+#pragma unroll
+    for (int c = 0; c < GF_STAT_COUNT; ++c) v[c] += part[s * GF_STAT_COUNT + c];
+#pragma unroll
+  for (int c = 0; c < GF_STAT_COUNT; ++c) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&acc[c], v[c]);
+  }
+  __syncthreads();
+  if (threadIdx.x < GF_STAT_COUNT && acc[threadIdx.x])
+    atomicAdd((unsigned long long*)&stats[threadIdx.x], acc[threadIdx.x]);
+}
+
+void launch_stats_fold(const unsigned long long* part, int64_t* stats, cudaStream_t st) {
+  gf_launch_pdl(k_stats_fold, dim3(1), dim3(256), 0, st, part, stats);
+}
+
 // -------------------------------------------------------------------------
 // march pass r: composite round r-1 (+ERT), then place / skip / emit round r.
 // At r == n_rounds: composite the last round and write the final colours.
@@ -560,7 +602,7 @@ __device__ __forceinline__ void warp_add_u64(int64_t* dst, unsigned long long v)
 // one round's sampling for the marcher's ray i (render.py:311-330): placement,
 // ESS, histogram ranks, staging records, counters; `fw` is the ray's flag word
 __device__ __forceinline__ void march_sample(const MarchParams& P, const RayState& R, const RoundBufs& B, int64_t i,
-                                             uint32_t& fw, int round, int phase) {
+                                             uint32_t& fw, int round, int phase, MarchStats& ST) {
   // ---- sample round r (render.py:311-330)
   const int s0 = round * P.chunk;
   const int m = min(P.chunk, P.k - s0);
@@ -573,7 +615,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
   const bool defer = alive && earlier;
   const int par = (round / P.group) & 1;                       // histogram / emit-list parity
   const uint32_t half = (uint32_t)phase * (uint32_t)P.chunk;   // staging offset of the group's round
-  warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (alive && !active && !defer) ? (unsigned long long)m : 0ull);
+  ST.v[GF_STAT_ESS_SKIPPED] += (alive && !active && !defer) ? (unsigned long long)m : 0ull;
   if (defer && !active) R.pend[4 * (uint64_t)i + phase] = (uint32_t)m << 16;
   if (!__any_sync(0xffffffffu, active)) return;
   float4 o = active ? R.org[i] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -637,7 +679,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
     const unsigned lane = gf_lane();
     if (!active) cmask = 0;
     const uint32_t cnt = __popc(cmask);
-    if (P.count_candidates) warp_add_u64(&P.stats[GF_STAT_N_RAYS], cnt);
+    if (P.count_candidates) ST.v[GF_STAT_N_RAYS] += cnt;
     uint32_t incl = cnt;
 #pragma unroll
     for (int o2 = 1; o2 < 32; o2 <<= 1) {
@@ -890,8 +932,8 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       if (emit) B.emit_list[b + __popc(em & ((1u << gf_lane()) - 1u))] = (uint32_t)i;
     }
   }
-  warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], defer ? 0ull : (unsigned long long)kept);
-  warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], (active && !defer) ? (unsigned long long)(m - (int)kept) : 0ull);
+  ST.v[GF_STAT_TOTAL_QUERIES] += defer ? 0ull : (unsigned long long)kept;
+  ST.v[GF_STAT_ESS_SKIPPED] += (active && !defer) ? (unsigned long long)(m - (int)kept) : 0ull;
 }
 
 // 7 CTAs/SM (<= 72 registers): measured faster than the unconstrained 85
@@ -965,10 +1007,9 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
     }
     R.acc[i] = acc;
   }
-  if (P.group > 1) {
-    warp_add_u64(&P.stats[GF_STAT_TOTAL_QUERIES], commit_q);
-    warp_add_u64(&P.stats[GF_STAT_ESS_SKIPPED], commit_s);
-  }
+  MarchStats ST;
+  ST.v[GF_STAT_TOTAL_QUERIES] = commit_q;
+  ST.v[GF_STAT_ESS_SKIPPED] = commit_s;
   if (phase == 0) fw &= ~(uint32_t)GF_RAY_HAD_ALL;
 
   if (final_pass) {
@@ -982,7 +1023,8 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
       P.rgb_out[3 * i + 1] = fminf(fmaxf(c1, 0.f), 1.f);
       P.rgb_out[3 * i + 2] = fminf(fmaxf(c2, 0.f), 1.f);
     }
-    warp_add_u64(&P.stats[GF_STAT_ERT_TERMINATED], (fw & GF_RAY_TERMINATED) ? 1ull : 0ull);
+    ST.v[GF_STAT_ERT_TERMINATED] += (fw & GF_RAY_TERMINATED) ? 1ull : 0ull;
+    flush_stats(P, ST);
     return;
   }
 
@@ -990,8 +1032,9 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
   // is placed by this one pass, else one round per launch (phase)
   const int nsub = P.fuse ? min(P.group, P.n_rounds - round) : 1;
 #pragma unroll 1
-  for (int sub = 0; sub < nsub; ++sub) march_sample(P, R, B, i, fw, round + sub, phase + sub);
+  for (int sub = 0; sub < nsub; ++sub) march_sample(P, R, B, i, fw, round + sub, phase + sub, ST);
   if (in_range && fw != fw0) R.flags[i] = fw;
+  flush_stats(P, ST);
 }
 
 }  // namespace gf

@@ -16,6 +16,8 @@ __host__ __device__ __forceinline__ uint32_t gf_had_below(int p) {
 
 namespace gf {
 
+#define GF_STAT_SLOTS 1024  // warps flush their counters into slot (warp id mod 1024)
+
 struct MarchParams {
   GfGrid grid;        // network lattice geometry (cell keys)
   GfGrid occ;         // occupancy geometry
@@ -23,6 +25,7 @@ struct MarchParams {
   GfGrid coarse;      // dilated coarse occupancy mip (empty-space pre-test)
   const uint32_t* coarse_bits;  // NULL: every candidate takes the exact path
   float ivl_pad;      // world-distance padding of the DDA intervals (float32 error)
+  unsigned long long* stats_part;  // GF_STAT_SLOTS x GF_STAT_COUNT partial counters (spread: no hot address)
   const uint32_t* fine_bits;  // occupancy dilated by >= seg/2 + margin (occupancy geometry): per-candidate
                               // pre-test at the segment midpoint, before the jitter and the exact placement
   gf_camera_t cam;
@@ -107,6 +110,7 @@ __device__ __forceinline__ int64_t seed_slot(const MarchParams& P, int64_t g) {
 
 // K2 for the render path (fused scan + tile list + rank-based placement);
 // returns the number of launches it made
+void launch_stats_fold(const unsigned long long* part, int64_t* stats, cudaStream_t st);
 int launch_place(const GfGrid& grid, const RoundBufs& RB, const uint32_t* run, const BucketBufs& Bk, int64_t n_cells,
                  int stride, int half, int round, int64_t max_rows, cudaStream_t st);
 
