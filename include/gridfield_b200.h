@@ -70,7 +70,8 @@ typedef struct {
   int32_t eps_compare_f64; /* 0: transmittance < float32(eps) (Python float, NEP 50); 1: float64 compare */
   double epsilon;          /* ERT threshold, 0 disables                       */
   float background[3];
-  float _pad;
+  int32_t rays_f64;        /* 1: origins / dirs are double (n, 3): the slab test runs on them,
+                              samples on their float32 roundings (render.py:292-306) */
   uint64_t seed;           /* render_rays(seed=...)                           */
 } gf_march_cfg_t;
 

@@ -55,7 +55,7 @@ class GridGeom(C.Structure):
 class MarchCfg(C.Structure):
     _fields_ = [
         ("k", C.c_int32), ("ert_chunk", C.c_int32), ("stratified", C.c_int32), ("eps_compare_f64", C.c_int32),
-        ("epsilon", C.c_double), ("background", C.c_float * 3), ("_pad", C.c_float), ("seed", C.c_uint64),
+        ("epsilon", C.c_double), ("background", C.c_float * 3), ("rays_f64", C.c_int32), ("seed", C.c_uint64),
     ]
 
 

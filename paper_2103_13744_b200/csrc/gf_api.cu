@@ -662,6 +662,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
   }
   P.origins = origins;
   P.dirs = dirs;
+  P.rays_f64 = cfg->rays_f64 ? 1 : 0;
   P.ray_offset = ray_offset;
   P.block_stride = ray_block_stride;
   P.n_rays = n_rays;

@@ -156,6 +156,7 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
   if (i >= P.n_rays) return;
   const int64_t g = global_ray(P, i);  // ray index within the render_rays call
   float o32[3], d32[3];
+  double o64[3], d64[3];
   if (P.use_cam) {
     const gf_camera_t& c = P.cam;
     int64_t px = g % c.width, py = g / c.width;
@@ -171,6 +172,14 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
       d32[a] = __double2float_rn(__ddiv_rn(d[a], nn));
       o32[a] = __double2float_rn(c.c2w[4 * a + 3]);
     }
+  } else if (P.rays_f64) {  // render.py:368: the slab test on the caller's float64 rays
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      o64[a] = reinterpret_cast<const double*>(P.origins)[3 * i + a];
+      d64[a] = reinterpret_cast<const double*>(P.dirs)[3 * i + a];
+      o32[a] = __double2float_rn(o64[a]);  // render.py:304-305: samples use the float32 roundings
+      d32[a] = __double2float_rn(d64[a]);
+    }
   } else {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -178,11 +187,18 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
       d32[a] = P.dirs[3 * i + a];
     }
   }
+  if (!P.rays_f64 || P.use_cam) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      o64[a] = (double)o32[a];
+      d64[a] = (double)d32[a];
+    }
+  }
   // slab test in f64 (render.py:151-171)
   double lo_max = -INFINITY, hi_min = INFINITY;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    double o = (double)o32[a], d = (double)d32[a];
+    const double o = o64[a], d = d64[a];
     double lo, hi;
     if (d == 0.0) {
       bool inside = (o >= P.grid.b_min[a]) && (o <= P.grid.b_max[a]);

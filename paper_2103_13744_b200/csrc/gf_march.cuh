@@ -30,8 +30,9 @@ struct MarchParams {
                               // pre-test at the segment midpoint, before the jitter and the exact placement
   gf_camera_t cam;
   int use_cam;
-  const float* origins;
+  const float* origins;   // (n, 3) float32, or double when rays_f64
   const float* dirs;
+  int rays_f64;
   int64_t ray_offset, n_rays, first_block, block_stride;
   const u128* block_seeds;  // [2*b] state, [2*b+1] inc
   const u128* jump;         // [2*d] A^d, [2*d+1] sum_{k<d} A^k  (d <= GF_JUMP_MAX)

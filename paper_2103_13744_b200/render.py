@@ -372,11 +372,16 @@ def render_rays_device(grid, occupancy, cfg: RenderConfig, seed=0, *, cam: Camer
         o_d = d_d = None
         ccam = N.make_camera(cam)
     else:
-        o_d = D.to_device(origins, t.float32).reshape(-1, 3)
-        d_d = D.to_device(directions, t.float32).reshape(-1, 3)
+        f64 = getattr(origins, "dtype", None) in (np.float64, t.float64) or \
+            getattr(directions, "dtype", None) in (np.float64, t.float64)
+        rdt = t.float64 if f64 else t.float32
+        o_d = D.to_device(origins, rdt).reshape(-1, 3)
+        d_d = D.to_device(directions, rdt).reshape(-1, 3)
         n = o_d.shape[0]
         ccam = None
     ncfg = cfg.native(seed)
+    if cam is None:
+        ncfg.rays_f64 = int(o_d.dtype == t.float64)
     if occupancy is not None:
         occ_geom, occ_bits = occupancy.native_geom(), occupancy.device_bits()
     else:
@@ -429,15 +434,17 @@ def render_rays(field, occupancy, origins, directions, cfg: RenderConfig, seed: 
     device result is identical for any value (ray blocks keep their own
     jitter streams)."""
     grid = _field_grid(field)
-    o = np.asarray(origins, dtype=np.float64).reshape(-1, 3)
-    d = np.asarray(directions, dtype=np.float64).reshape(-1, 3)
-    # render.py:368-369 upcasts to float64 and the slab test runs on those
-    # values; the device takes float32 rays, so float64 rays must round-trip
-    if not (np.array_equal(o.astype(np.float32).astype(np.float64), o)
-            and np.array_equal(d.astype(np.float32).astype(np.float64), d)):
-        raise ValueError("render_rays on the device requires float32-representable origins/directions")
-    rgb, st, _ = render_rays_device(grid, occupancy, cfg, seed, origins=o.astype(np.float32),
-                                    directions=d.astype(np.float32), precision=precision)
+    o = np.asarray(origins)
+    d = np.asarray(directions)
+    # render.py:368-369 upcasts to float64: the slab test runs on those values
+    # and the samples on their float32 roundings (render.py:304-306).
+    # float32 rays go as they are (their float64 upcast is exact); anything
+    # else goes as float64.
+    f32 = o.dtype == np.float32 and d.dtype == np.float32
+    dt = np.float32 if f32 else np.float64
+    o = np.ascontiguousarray(o, dtype=dt).reshape(-1, 3)
+    d = np.ascontiguousarray(d, dtype=dt).reshape(-1, 3)
+    rgb, st, _ = render_rays_device(grid, occupancy, cfg, seed, origins=o, directions=d, precision=precision)
     return rgb.cpu().numpy(), _stats_from(st)
 
 

@@ -560,6 +560,23 @@ def gen_generic():
     stt = train.AdamState.for_params(student.params)
     out["ds_loss"] = np.array([train.distill_step(student, teacher, dcfg, stt, np.random.default_rng(27), delta_ref=0.01)])
     out.update(_grads_dict("ds_p_", student.params))
+    # render_rays on float64 rays that float32 cannot represent (render.py:368:
+    # the slab test sees them, the samples their float32 roundings)
+    g16 = ggrid.init_network_grid(aabb, (16, 16, 16), seed=0)
+    g16.params.biases["density"][:] = 5.0
+    rng64 = np.random.default_rng(31)
+    n64 = 3000
+    o64 = rng64.uniform(-3, 3, (n64, 3))
+    o64[:, 0] = -3.0 + rng64.uniform(0, 1e-9, n64)  # a float32-invisible offset
+    tgt = rng64.uniform(-0.9, 0.9, (n64, 3))
+    d64 = tgt - o64
+    d64 /= np.linalg.norm(d64, axis=-1, keepdims=True)
+    d64[:40, 1:] = 0.0  # axis-parallel rays
+    d64[:40, 0] = 1.0
+    o64[:40, 1:] = rng64.uniform(-1.2, 1.2, (40, 2))
+    rgb64, st64 = render.render_rays(g16, None, o64, d64, render.RenderConfig(k=64), seed=3)
+    out.update(f64_o=o64, f64_d=d64, f64_rgb=rgb64,
+               f64_stats=np.array([st64.total_queries, st64.ess_skipped, st64.ert_terminated_rays, st64.n_rays], np.int64))
     save("generic", **out)
     print("  distill loss", out["ds_loss"], "render Q", st.total_queries)
 

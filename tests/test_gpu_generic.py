@@ -127,3 +127,19 @@ def test_generic_grouped_backward_matches_reference_math():
         for name in ref.weights:
             _close(grads.weights[name][c], ref.weights[name], f"cell {c} w {name}", rel=1e-3, scale=1e-4)
             _close(grads.biases[name][c], ref.biases[name], f"cell {c} b {name}", rel=1e-3, scale=1e-4)
+
+
+def test_render_rays_float64_rays_match_reference():
+    """render_rays with float64 rays float32 cannot represent (render.py:368):
+    the device slab test runs on the float64 values, the samples on their
+    float32 roundings, exactly as the reference (counts exact)."""
+    gf = _gf()
+    z = golden("generic")
+    aabb = gf.Aabb((-1.0,) * 3, (1.0,) * 3)
+    g = gf.init_network_grid(aabb, (16, 16, 16), seed=0)
+    g.params.biases["density"][:] = 5.0
+    o, d = z["f64_o"], z["f64_d"]
+    assert not np.array_equal(o.astype(np.float32).astype(np.float64), o)
+    rgb, st = gf.render_rays(g, None, o, d, gf.RenderConfig(k=64), seed=3, precision="fp32")
+    assert [st.total_queries, st.ess_skipped, st.ert_terminated_rays, st.n_rays] == list(z["f64_stats"])
+    assert float(np.abs(rgb - z["f64_rgb"]).max()) <= 2e-5

@@ -246,3 +246,16 @@ def test_generic_manifest_oracle_pinned(tag):
     rgb, sig = O.query_points(lat, z[f"{tag}_pts"], z[f"{tag}_dirs"])
     assert np.abs(rgb - z[f"{tag}_rgb"]).max() <= 1e-6
     assert np.abs(sig - z[f"{tag}_sigma"]).max() <= 1e-5 * max(1.0, float(np.abs(z[f"{tag}_sigma"]).max()))
+
+
+def test_float64_rays_oracle_pinned():
+    """The oracle's render_rays on float64 rays float32 cannot represent
+    (slab test in float64, samples on the float32 roundings, render.py:292-306)
+    reproduces the reference's counts and image."""
+    z = golden("generic")
+    lat = O.init_lattice(UNIT_MIN, UNIT_MAX, (16, 16, 16), seed=0)
+    lat.biases["density"][:] = 5.0
+    q = lambda p, d: O.query_points(lat, p, d)
+    rgb, ctr = O.render_rays(q, lat.b_min, lat.b_max, None, z["f64_o"], z["f64_d"], O.MarchConfig(k=64), seed=3)
+    assert [ctr.total_queries, ctr.ess_skipped, ctr.ert_terminated_rays, ctr.n_rays] == list(z["f64_stats"])
+    assert float(np.abs(rgb - z["f64_rgb"]).max()) <= 1e-6
