@@ -170,6 +170,13 @@ GF_API int gf_bin_points(const gf_grid_geom_t* grid, const void* x_dev, int32_t 
 /* occupancy.py:76-79 occupied_at.                                          */
 GF_API int gf_occupied_at(const gf_grid_geom_t* occ, const uint8_t* bits_dev, const void* x_dev, int32_t x_f64,
                           int64_t n, uint8_t* out_dev, int64_t* err_dev, void* stream);
+/* render.py:151-171 intersect_aabb: float64 rays (n, 3) -> t0, t1 (n,).   */
+GF_API int gf_intersect_aabb(const double* o_dev, const double* d_dev, int64_t n, const double* b_min,
+                             const double* b_max, double* t0_dev, double* t1_dev, void* stream);
+/* render.py:256-258 sample_ray positions: out[j] = float32(o + (t0 + (j +
+ * jitter[j]) * seg) * d) in float64, for the caller's k jitter values.   */
+GF_API int gf_ray_samples(const double* origin3, const double* direction3, double t0, double seg,
+                          const double* jitter_dev, int64_t k, float* out_dev, void* stream);
 /* core.py:52-68 clip_into (float32 points).                                */
 GF_API int gf_clip_into(const double* b_min, const double* b_max, const float* x_dev, int64_t n, float* out_dev,
                  void* stream);

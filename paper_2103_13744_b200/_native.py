@@ -106,6 +106,9 @@ _SIGS = {
     "gf_bin_points": (C.c_int, [C.POINTER(GridGeom), _P, C.c_int32, C.c_int64, _P, _P, _P]),
     "gf_occupied_at": (C.c_int, [C.POINTER(GridGeom), _P, _P, C.c_int32, C.c_int64, _P, _P, _P]),
     "gf_clip_into": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), _P, C.c_int64, _P, _P]),
+    "gf_intersect_aabb": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P, _P]),
+    "gf_ray_samples": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double, C.c_double, _P,
+                                 C.c_int64, _P, _P]),
     "gf_positional_encode": (C.c_int, [_P, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "gf_density_to_alpha": (C.c_int, [_P, _P, C.c_int32, C.c_int64, _P, _P]),
     "gf_composite": (C.c_int, [_P, _P, C.c_int64, C.c_int64, _P, _P, _P]),

@@ -26,6 +26,10 @@ void launch_gather_rows3(const void* x, int f64, const int64_t* idx, int64_t n, 
 void launch_occupied_at(const GfGrid& g, const uint8_t* bits, const void* x, int f64, int64_t n, uint8_t* out,
                         int64_t* err, cudaStream_t st);
 void launch_clip(const double* lo, const double* hi, const float* x, int64_t n, float* out, cudaStream_t st);
+void launch_intersect_aabb(const double* o, const double* d, int64_t n, const double* lo, const double* hi, double* t0,
+                           double* t1, cudaStream_t st);
+void launch_ray_samples(const double* o, const double* d, double t0, double seg, const double* jit, int64_t k,
+                        float* out, cudaStream_t st);
 void launch_encode(const void* v, int f64, int64_t n, int dim, int L, int raw, void* out, cudaStream_t st);
 void launch_alpha(const void* s, const void* d, int f64, int64_t n, void* out, cudaStream_t st);
 void launch_composite(const float* c, const float* a, int64_t nr, int64_t ns, float* rgb, float* tr, cudaStream_t st);
@@ -1278,6 +1282,20 @@ int gf_occupied_at(const gf_grid_geom_t* occ, const uint8_t* bits, const void* x
   if (!valid_grid(occ) || n < 0) return fail(GF_ERR_INVALID, "gf_occupied_at: bad grid");
   launch_occupied_at(gf_make_grid(occ), bits, x, x_f64, n, out, err, (cudaStream_t)stream);
   return check_cuda("gf_occupied_at");
+}
+
+int gf_intersect_aabb(const double* o, const double* d, int64_t n, const double* b_min, const double* b_max, double* t0,
+                      double* t1, void* stream) {
+  if (n < 0 || !b_min || !b_max) return fail(GF_ERR_INVALID, "gf_intersect_aabb: bad arguments");
+  launch_intersect_aabb(o, d, n, b_min, b_max, t0, t1, (cudaStream_t)stream);
+  return check_cuda("gf_intersect_aabb");
+}
+
+int gf_ray_samples(const double* origin, const double* direction, double t0, double seg, const double* jitter,
+                   int64_t k, float* out, void* stream) {
+  if (k < 0 || !origin || !direction) return fail(GF_ERR_INVALID, "gf_ray_samples: bad arguments");
+  launch_ray_samples(origin, direction, t0, seg, jitter, k, out, (cudaStream_t)stream);
+  return check_cuda("gf_ray_samples");
 }
 
 int gf_clip_into(const double* b_min, const double* b_max, const float* x, int64_t n, float* out, void* stream) {

@@ -197,6 +197,55 @@ void launch_composite_f64(const double* c, const double* a, int64_t nr, int64_t 
                           cudaStream_t st) {
   if (nr > 0) k_composite<double><<<blocks(nr, 128), 128, 0, st>>>(c, a, nr, ns, rgb, tr);
 }
+// render.py:151-171 intersect_aabb: float64 slab test (division, parallel
+// axes by the inside test), t0 = max(near, 0), t1 = min(far)
+__global__ void k_intersect_aabb(const double* __restrict__ o, const double* __restrict__ d, int64_t n, double lx,
+                                 double ly, double lz, double hx, double hy, double hz, double* t0, double* t1) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double lo[3] = {lx, ly, lz}, hi[3] = {hx, hy, hz};
+  double near = -INFINITY, far = INFINITY;
+  for (int a = 0; a < 3; ++a) {
+    const double oa = o[3 * i + a], da = d[3 * i + a];
+    double nl, fr;
+    if (da == 0.0) {
+      const bool inside = oa >= lo[a] && oa <= hi[a];
+      nl = inside ? -INFINITY : INFINITY;
+      fr = inside ? INFINITY : -INFINITY;
+    } else {
+      const double ta = __ddiv_rn(__dsub_rn(lo[a], oa), da), tb = __ddiv_rn(__dsub_rn(hi[a], oa), da);
+      nl = fmin(ta, tb);
+      fr = fmax(ta, tb);
+    }
+    near = a == 0 ? nl : fmax(near, nl);
+    far = a == 0 ? fr : fmin(far, fr);
+  }
+  t0[i] = fmax(near, 0.0);
+  t1[i] = far;
+}
+
+// render.py:256-258 sample_ray positions: f32(o + (t0 + (j + jit_j) seg) d), float64 arithmetic in numpy's order
+__global__ void k_ray_samples(double ox, double oy, double oz, double dx, double dy, double dz, double t0, double seg,
+                              const double* __restrict__ jit, int64_t k, float* out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  const double t = __dadd_rn(t0, __dmul_rn(__dadd_rn((double)j, jit[j]), seg));
+  out[3 * j + 0] = __double2float_rn(__dadd_rn(ox, __dmul_rn(t, dx)));
+  out[3 * j + 1] = __double2float_rn(__dadd_rn(oy, __dmul_rn(t, dy)));
+  out[3 * j + 2] = __double2float_rn(__dadd_rn(oz, __dmul_rn(t, dz)));
+}
+
+void launch_intersect_aabb(const double* o, const double* d, int64_t n, const double* lo, const double* hi, double* t0,
+                           double* t1, cudaStream_t st) {
+  if (n > 0) k_intersect_aabb<<<blocks(n, 256), 256, 0, st>>>(o, d, n, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], t0, t1);
+}
+
+void launch_ray_samples(const double* o, const double* d, double t0, double seg, const double* jit, int64_t k,
+                        float* out, cudaStream_t st) {
+  if (k > 0)
+    k_ray_samples<<<blocks(k, 256), 256, 0, st>>>(o[0], o[1], o[2], d[0], d[1], d[2], t0, seg, jit, k, out);
+}
+
 void launch_gen_rays(const gf_camera_t& c, float* o, float* d, cudaStream_t st) {
   int64_t n = (int64_t)c.width * c.height;
   if (n > 0) k_gen_rays<<<blocks(n, 256), 256, 0, st>>>(c, o, d);

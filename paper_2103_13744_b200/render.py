@@ -121,19 +121,21 @@ def generate_rays(cam: Camera):
 
 
 def intersect_aabb(origins, directions, aabb: Aabb):
-    """render.py:151-171 slab test (float64).  Host helper for single rays and
-    tests; the marcher runs its own copy of this arithmetic on the device."""
+    """render.py:151-171 slab test in float64 on the device (gf_intersect_aabb;
+    the marcher runs the same arithmetic inside k_ray_init)."""
     o = np.asarray(origins, dtype=np.float64)
     d = np.asarray(directions, dtype=np.float64)
-    with np.errstate(divide="ignore", invalid="ignore"):
-        t_lo = (aabb.b_min - o) / d
-        t_hi = (aabb.b_max - o) / d
-    near, far = np.minimum(t_lo, t_hi), np.maximum(t_lo, t_hi)
-    par = d == 0
-    inside = (o >= aabb.b_min) & (o <= aabb.b_max)
-    near = np.where(par, np.where(inside, -np.inf, np.inf), near)
-    far = np.where(par, np.where(inside, np.inf, -np.inf), far)
-    return np.maximum(near.max(axis=-1), 0.0), far.min(axis=-1)
+    shape = np.broadcast_shapes(o.shape, d.shape)[:-1]
+    o2 = np.ascontiguousarray(np.broadcast_to(o, shape + (3,))).reshape(-1, 3)
+    d2 = np.ascontiguousarray(np.broadcast_to(d, shape + (3,))).reshape(-1, 3)
+    t = D.require_cuda()
+    od, dd = D.to_device(o2, t.float64), D.to_device(d2, t.float64)
+    t0, t1 = D.empty((o2.shape[0],), t.float64), D.empty((o2.shape[0],), t.float64)
+    lo = (N.C.c_double * 3)(*aabb.b_min)
+    hi = (N.C.c_double * 3)(*aabb.b_max)
+    N.check(N.lib().gf_intersect_aabb(N.ptr(od), N.ptr(dd), o2.shape[0], lo, hi, N.ptr(t0), N.ptr(t1),
+                                      D.stream_handle()), "intersect_aabb")
+    return t0.cpu().numpy().reshape(shape), t1.cpu().numpy().reshape(shape)
 
 
 @dataclass
@@ -197,8 +199,10 @@ class RenderStats:
 
 
 def sample_ray(ray: Ray, aabb: Aabb, occ=None, cfg: RenderConfig | None = None, rng=None):
-    """render.py:234-266: single-ray sampler used by tests and tools (float64
-    jitter from the caller's Generator; not the marcher's path)."""
+    """render.py:234-266: one ray's k jittered samples minus unoccupied ones.
+    The jitter comes from the caller's Generator on the host, exactly as in
+    the reference; the slab test, the float64 placement, clip_into and the
+    occupancy test run on the device."""
     from .core import clip_into
 
     cfg = cfg or RenderConfig()
@@ -208,8 +212,13 @@ def sample_ray(ray: Ray, aabb: Aabb, occ=None, cfg: RenderConfig | None = None, 
         return np.zeros((0, 3), dtype=np.float32), np.zeros(0, dtype=np.float32)
     seg = (t1 - t0) / cfg.k
     jitter = (rng or np.random.default_rng()).random(cfg.k) if cfg.stratified else np.full(cfg.k, 0.5)
-    ts = t0 + (np.arange(cfg.k) + jitter) * seg
-    pts = clip_into((ray.origin[None, :] + ts[:, None] * ray.direction[None, :]).astype(np.float32), aabb)
+    t = D.require_cuda()
+    jd = D.to_device(np.asarray(jitter, np.float64), t.float64)
+    pts = D.empty((cfg.k, 3), t.float32)
+    o3 = (N.C.c_double * 3)(*np.asarray(ray.origin, np.float64))
+    d3 = (N.C.c_double * 3)(*np.asarray(ray.direction, np.float64))
+    N.check(N.lib().gf_ray_samples(o3, d3, t0, seg, N.ptr(jd), cfg.k, N.ptr(pts), D.stream_handle()), "sample_ray")
+    pts = clip_into(pts.cpu().numpy(), aabb)
     if occ is not None:
         pts = pts[occ.occupied_at(pts)]
     return pts, np.full(len(pts), seg, dtype=np.float32)
