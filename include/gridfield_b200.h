@@ -220,6 +220,16 @@ typedef struct {
 /* AnalyticScene.query_points (scene.py:115-135) for n float32 points.      */
 GF_API int gf_query_analytic(const gf_analytic_t* scene, const float* pos_dev, const float* dir_dev, int64_t n,
                              float* rgb_dev, float* sigma_dev, void* stream);
+/* scene.py:214-252 render_brute_force: dense Simpson quadrature (n_samples
+ * segments per ray over the box interval, no occupancy, no termination) of
+ * the camera's rays [ray0, ray0 + n_rays) -> out (n_rays, 3) in [0, 1].   */
+GF_API size_t gf_brute_force_workspace_bytes(int32_t n_samples, int64_t n_rays);
+GF_API int gf_render_brute_force(const gf_analytic_t* scene, const gf_camera_t* cam, int32_t n_samples,
+                                 const float* background3, int64_t ray0, int64_t n_rays, float* out_dev, void* ws_dev,
+                                 size_t ws_bytes, void* stream);
+/* scene.py:186-211 analytically_empty_cells: out[c] = 1 when no primitive
+ * touches cell c of a res[0] x res[1] x res[2] grid over the scene box.   */
+GF_API int gf_analytic_empty_cells(const gf_analytic_t* scene, const int32_t* res3, uint8_t* out_dev, void* stream);
 /* render.render_rays / render_image with an AnalyticScene field: arguments as
  * gf_render_rays minus the network (the scene box is the march box).       */
 GF_API size_t gf_render_analytic_workspace_bytes(const gf_analytic_t* scene, const gf_march_cfg_t* cfg,

@@ -126,6 +126,10 @@ _SIGS = {
     "gf_extract_occupancy_network": (C.c_int, [C.POINTER(Arch), C.POINTER(GridGeom), _P, C.c_int,
                                                C.POINTER(C.c_float), C.POINTER(GridGeom), C.c_double, C.c_int64, _P,
                                                _P, _P, C.c_size_t, _P]),
+    "gf_brute_force_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int64]),
+    "gf_render_brute_force": (C.c_int, [C.POINTER(Analytic), C.POINTER(CameraT), C.c_int32, C.POINTER(C.c_float),
+                                        C.c_int64, C.c_int64, _P, _P, C.c_size_t, _P]),
+    "gf_analytic_empty_cells": (C.c_int, [C.POINTER(Analytic), C.POINTER(C.c_int32), _P, _P]),
     "gf_render_field_workspace_bytes": (C.c_size_t, [C.POINTER(GridGeom), C.POINTER(MarchCfg), C.c_int64]),
     "gf_render_rays_field": (C.c_int, [FIELD_FN, _P, C.POINTER(GridGeom), C.POINTER(GridGeom), _P,
                                        C.POINTER(MarchCfg), C.POINTER(CameraT), _P, _P, C.c_int64, C.c_int64,

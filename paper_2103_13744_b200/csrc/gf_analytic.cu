@@ -10,6 +10,8 @@
 // that operation order with explicitly rounded intrinsics, so densities are
 // bit-exact.  Colours use sinf (texture) and a 3-term dot (view tint), which
 // numpy evaluates with its own SIMD sin / BLAS order: equal to ~1 ulp.
+#include <algorithm>
+
 #include "gf_analytic.cuh"
 
 namespace gf {
@@ -82,6 +84,139 @@ __global__ void __launch_bounds__(256) k_query_analytic(AnalyticDev A, const flo
     rgb[3 * i + 2] = c[2];
     sigma[i] = s;
   }
+}
+
+// scene.py:214-252 render_brute_force, segment stage: ray r's segment i of
+// n (Simpson optical depth from the half-step lattice ends 2i, 2i+2 and
+// midpoint 2i+1, colour at the midpoint), float64 placement, float32 field
+__global__ void __launch_bounds__(256) k_brute_segments(AnalyticDev A, gf_camera_t cam, double lx, double ly,
+                                                        double lz, double hx, double hy, double hz, int64_t ray0,
+                                                        int64_t n_rays, int n, float* alpha, float* color) {
+  const double lo[3] = {lx, ly, lz}, hi[3] = {hx, hy, hz};
+  const int64_t total = n_rays * (int64_t)n;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rl = q / n, g = ray0 + rl;
+    const int i = (int)(q % n);
+    // render.py:139-148 generate_rays (float32 rays), then .astype(float64)
+    const int64_t px = g % cam.width, py = g / cam.width;
+    const double u = __ddiv_rn(__dsub_rn(__dadd_rn((double)px, 0.5), cam.cx), cam.fx);
+    const double v = __ddiv_rn(__dsub_rn(__dadd_rn((double)py, 0.5), cam.cy), cam.fy);
+    double dv[3];
+    for (int a = 0; a < 3; ++a)
+      dv[a] = __dadd_rn(__dadd_rn(__dmul_rn(u, cam.c2w[4 * a + 0]), __dmul_rn(v, cam.c2w[4 * a + 1])), cam.c2w[4 * a + 2]);
+    const double nn = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dv[0], dv[0]), __dmul_rn(dv[1], dv[1])),
+                                           __dmul_rn(dv[2], dv[2])));
+    float d32[3];
+    double o[3], d[3];
+    for (int a = 0; a < 3; ++a) {
+      d32[a] = __double2float_rn(__ddiv_rn(dv[a], nn));
+      d[a] = (double)d32[a];
+      o[a] = (double)__double2float_rn(cam.c2w[4 * a + 3]);
+    }
+    // render.py:151-171 slab test
+    double near = -INFINITY, far = INFINITY;
+    for (int a = 0; a < 3; ++a) {
+      double nl, fr;
+      if (d[a] == 0.0) {
+        const bool inside = o[a] >= lo[a] && o[a] <= hi[a];
+        nl = inside ? -INFINITY : INFINITY;
+        fr = inside ? INFINITY : -INFINITY;
+      } else {
+        const double ta = __ddiv_rn(__dsub_rn(lo[a], o[a]), d[a]), tb = __ddiv_rn(__dsub_rn(hi[a], o[a]), d[a]);
+        nl = fmin(ta, tb);
+        fr = fmax(ta, tb);
+      }
+      near = a == 0 ? nl : fmax(near, nl);
+      far = a == 0 ? fr : fmin(far, fr);
+    }
+    const double t0 = fmax(near, 0.0), t1 = far;
+    float al = 0.f, c[3] = {0.f, 0.f, 0.f};
+    if (t1 > t0) {  // a miss blends nothing: its composite is exactly the background
+      const double seg = __ddiv_rn(__dsub_rn(t1, t0), (double)n), hs = __dmul_rn(0.5, seg);
+      float sg[3];
+      for (int m = 0; m < 3; ++m) {
+        const double t = __dadd_rn(t0, __dmul_rn((double)(2 * i + m), hs));
+        float p[3];
+        for (int a = 0; a < 3; ++a) {  // .astype(float32), then np.clip against the float64 box
+          const double pa = (double)__double2float_rn(__dadd_rn(o[a], __dmul_rn(t, d[a])));
+          p[a] = __double2float_rn(fmin(fmax(pa, lo[a]), hi[a]));
+        }
+        float cc[3];
+        analytic_eval(A, p[0], p[1], p[2], d32[0], d32[1], d32[2], cc, &sg[m]);
+        if (m == 1) { c[0] = cc[0]; c[1] = cc[1]; c[2] = cc[2]; }
+      }
+      // depth = (seg32 / 6) * (s_2i + 4 s_2i+1 + s_2i+2), alpha = -expm1(-depth)
+      const float depth = __fmul_rn(__fdiv_rn(__double2float_rn(seg), 6.0f),
+                                    __fadd_rn(__fadd_rn(sg[0], __fmul_rn(4.0f, sg[1])), sg[2]));
+      al = -expm1f(-depth);
+    }
+    alpha[q] = al;
+    color[3 * q + 0] = c[0];
+    color[3 * q + 1] = c[1];
+    color[3 * q + 2] = c[2];
+  }
+}
+
+// out = clip(rgb + T * bg, 0, 1) (scene.py:249-252)
+__global__ void k_brute_finish(const float* rgb, const float* trans, int64_t n, float b0, float b1, float b2,
+                               float* out) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const float bg[3] = {b0, b1, b2};
+  for (int a = 0; a < 3; ++a)
+    out[3 * r + a] = fminf(fmaxf(__fadd_rn(rgb[3 * r + a], __fmul_rn(trans[r], bg[a])), 0.f), 1.f);
+}
+
+void launch_brute_force(const AnalyticDev& A, const gf_camera_t& cam, const double* lo, const double* hi, int64_t ray0,
+                        int64_t n_rays, int n, const float* bg, float* alpha, float* color, float* rgb, float* trans,
+                        float* out, cudaStream_t st) {
+  if (n_rays <= 0) return;
+  const int64_t total = n_rays * (int64_t)n;
+  const unsigned grid = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(total, 256), (int64_t)num_sms() * 16);
+  k_brute_segments<<<grid, 256, 0, st>>>(A, cam, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2], ray0, n_rays, n, alpha,
+                                         color);
+  launch_composite(color, alpha, n_rays, n, rgb, trans, st);  // render.py:269-284, sequential in sample order
+  k_brute_finish<<<(unsigned)gf_div_up<int64_t>(n_rays, 128), 128, 0, st>>>(rgb, trans, n_rays, bg[0], bg[1], bg[2],
+                                                                           out);
+}
+
+// scene.py:186-211 analytically_empty_cells: a cell is touched by a sphere
+// if the clamped distance from the centre is within the radius, by a box on
+// interval overlap (float64); out[c] = 1 for untouched cells
+__global__ void k_empty_cells(gf_analytic_t S, int rx, int ry, int rz, uint8_t* out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)rx * ry * rz;
+  if (c >= n) return;
+  const int64_t ix = c % rx, iy = (c / rx) % ry, iz = c / ((int64_t)rx * ry);
+  const int64_t id[3] = {ix, iy, iz};
+  const int res[3] = {rx, ry, rz};
+  double lo[3], hi[3];
+  for (int a = 0; a < 3; ++a) {
+    const double cell = __ddiv_rn(__dsub_rn(S.b_max[a], S.b_min[a]), (double)res[a]);
+    lo[a] = __dadd_rn(S.b_min[a], __dmul_rn((double)id[a], cell));
+    hi[a] = __dadd_rn(lo[a], cell);
+  }
+  bool touched = false;
+  for (int k = 0; k < S.n_prims && !touched; ++k) {
+    const gf_prim_t& p = S.prims[k];
+    if (p.kind == 0) {
+      double d2 = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        const double q = __dsub_rn(fmin(fmax(p.a[a], lo[a]), hi[a]), p.a[a]);
+        d2 = __dadd_rn(d2, __dmul_rn(q, q));
+      }
+      touched = __dsqrt_rn(d2) <= p.radius;
+    } else {
+      touched = hi[0] >= p.a[0] && lo[0] <= p.b[0] && hi[1] >= p.a[1] && lo[1] <= p.b[1] && hi[2] >= p.a[2] &&
+                lo[2] <= p.b[2];
+    }
+  }
+  out[c] = touched ? 0 : 1;
+}
+
+void launch_empty_cells(const gf_analytic_t& S, const int* res, uint8_t* out, cudaStream_t st) {
+  const int64_t n = (int64_t)res[0] * res[1] * res[2];
+  if (n > 0) k_empty_cells<<<(unsigned)gf_div_up<int64_t>(n, 256), 256, 0, st>>>(S, res[0], res[1], res[2], out);
 }
 
 bool make_analytic(const gf_analytic_t* s, AnalyticDev* A) {

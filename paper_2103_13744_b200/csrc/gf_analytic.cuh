@@ -57,6 +57,11 @@ __device__ __forceinline__ float analytic_density(const AnalyticDev& A, float x,
 
 int num_sms();
 bool make_analytic(const gf_analytic_t* s, AnalyticDev* A);
+void launch_composite(const float* c, const float* a, int64_t nr, int64_t ns, float* rgb, float* tr, cudaStream_t st);
+void launch_brute_force(const AnalyticDev& A, const gf_camera_t& cam, const double* lo, const double* hi, int64_t ray0,
+                        int64_t n_rays, int n, const float* bg, float* alpha, float* color, float* rgb, float* trans,
+                        float* out, cudaStream_t st);
+void launch_empty_cells(const gf_analytic_t& S, const int* res, uint8_t* out, cudaStream_t st);
 void launch_field_analytic(const AnalyticDev& A, const uint32_t* offsets, const float4* srec, const float4* ray_dir,
                            int stride_shift, uint32_t stride, float4* res, int64_t max_rows, cudaStream_t st);
 void launch_query_analytic(const AnalyticDev& A, const float* pos, const float* dir, int64_t n, float* rgb,

@@ -1009,6 +1009,43 @@ int gf_field_scatter(const void* srec, int64_t n, const float* rgb_, const float
   return check_cuda("gf_field_scatter");
 }
 
+size_t gf_brute_force_workspace_bytes(int32_t n_samples, int64_t n_rays) {
+  if (n_samples < 1 || n_rays < 0) return 0;
+  const size_t ns = (size_t)n_rays * (size_t)n_samples;
+  return gf_align(ns * 4) + gf_align(ns * 12) + gf_align((size_t)n_rays * 12) + gf_align((size_t)n_rays * 4);
+}
+
+int gf_render_brute_force(const gf_analytic_t* scene, const gf_camera_t* cam, int32_t n_samples, const float* bg,
+                          int64_t ray0, int64_t n_rays, float* out, void* ws, size_t ws_bytes, void* stream) {
+  AnalyticDev A;
+  memset(&A, 0, sizeof(A));
+  if (!make_analytic(scene, &A) || !cam || !bg || n_samples < 1 || n_rays < 0 || ray0 < 0 ||
+      ray0 + n_rays > (int64_t)cam->width * cam->height)
+    return fail(GF_ERR_INVALID, "gf_render_brute_force: bad scene, camera or range");
+  if (gf_brute_force_workspace_bytes(n_samples, n_rays) > ws_bytes)
+    return fail(GF_ERR_WORKSPACE, "gf_render_brute_force: workspace too small");
+  const size_t ns = (size_t)n_rays * (size_t)n_samples;
+  uint8_t* p = (uint8_t*)ws;
+  float* alpha = (float*)p;
+  p += gf_align(ns * 4);
+  float* color = (float*)p;
+  p += gf_align(ns * 12);
+  float* rgb = (float*)p;
+  p += gf_align((size_t)n_rays * 12);
+  float* trans = (float*)p;
+  launch_brute_force(A, *cam, scene->b_min, scene->b_max, ray0, n_rays, n_samples, bg, alpha, color, rgb, trans, out,
+                     (cudaStream_t)stream);
+  return check_cuda("gf_render_brute_force");
+}
+
+int gf_analytic_empty_cells(const gf_analytic_t* scene, const int32_t* res, uint8_t* out, void* stream) {
+  if (!scene || !res || res[0] < 1 || res[1] < 1 || res[2] < 1 || scene->n_prims < 0 || scene->n_prims > GF_MAX_PRIMS)
+    return fail(GF_ERR_INVALID, "gf_analytic_empty_cells: bad scene or resolution");
+  const int r[3] = {res[0], res[1], res[2]};
+  launch_empty_cells(*scene, r, out, (cudaStream_t)stream);
+  return check_cuda("gf_analytic_empty_cells");
+}
+
 int gf_query_analytic(const gf_analytic_t* scene, const float* pos, const float* dir, int64_t n, float* rgb,
                       float* sigma, void* stream) {
   AnalyticDev A;

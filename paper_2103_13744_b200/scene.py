@@ -161,3 +161,40 @@ def sphere_cameras(aabb: Aabb, n_views: int, image_size: int, seed: int, radius_
         pose = look_at_pose(center + orbit_r * v, center)
         cams.append(Camera(image_size, image_size, focal, focal, image_size / 2.0, image_size / 2.0, pose))
     return cams
+
+
+def analytically_empty_cells(scene: AnalyticScene, resolution) -> np.ndarray:
+    """scene.py:186-211: flat indices of the grid cells no primitive touches
+    (sphere: clamped distance to the cell box within the radius; box:
+    interval overlap), decided per cell on the device in float64."""
+    res = np.asarray(resolution, dtype=np.int64).reshape(3)
+    t = D.require_cuda()
+    out = D.empty((int(np.prod(res)),), t.uint8)
+    r3 = (N.C.c_int32 * 3)(*[int(v) for v in res])
+    N.check(N.lib().gf_analytic_empty_cells(scene.native(), r3, N.ptr(out), D.stream_handle()),
+            "analytically_empty_cells")
+    return np.flatnonzero(out.cpu().numpy())
+
+
+def render_brute_force(scene, cam: Camera, n_samples: int, background=(1.0, 1.0, 1.0), chunk_rays: int = 128) -> np.ndarray:
+    """scene.py:214-252: ground-truth quadrature (no occupancy, no
+    termination, no networks) on the device: every ray's box interval in
+    ``n_samples`` segments with a Simpson optical depth from both ends and
+    the midpoint, the midpoint's colour, composited in sample order.  Rays
+    are independent, so ``chunk_rays`` (kept for the reference signature)
+    does not change the result; the device works in chunks sized to its
+    workspace."""
+    if n_samples < 1:
+        raise ValueError("n_samples must be >= 1")
+    t = D.require_cuda()
+    n = cam.width * cam.height
+    chunk = int(max(1, min(n, (256 << 20) // (16 * int(n_samples)))))
+    out = D.empty((n, 3), t.float32)
+    bg = (N.C.c_float * 3)(*[float(np.float32(b)) for b in background])
+    ws = D.workspace(N.lib().gf_brute_force_workspace_bytes(int(n_samples), chunk))
+    sc, cc = scene.native(), N.make_camera(cam)
+    for r0 in range(0, n, chunk):
+        nr = min(chunk, n - r0)
+        N.check(N.lib().gf_render_brute_force(sc, cc, int(n_samples), bg, r0, nr, N.ptr(out[r0:]), N.ptr(ws),
+                                              ws.numel(), D.stream_handle()), "render_brute_force")
+    return out.cpu().numpy().reshape(cam.height, cam.width, 3)

@@ -581,9 +581,26 @@ def gen_generic():
     print("  distill loss", out["ds_loss"], "render Q", st.total_queries)
 
 
+def gen_brute():
+    """scene.render_brute_force (scene.py:214-252) and analytically_empty_cells
+    (scene.py:186-211) through the reference."""
+    out = {}
+    for tag, sc, size, ns, seed in (("toy", scene.standard_toy_scene(), 24, 96, 3),
+                                    ("spec", scene.specular_toy_scene(), 20, 64, 4),
+                                    ("rand", scene.random_toy_scene(7), 16, 40, 5)):
+        cam = scene.sphere_cameras(sc.aabb, 1, size, seed=seed)[0]
+        out[f"{tag}_img"] = scene.render_brute_force(sc, cam, ns, background=(1.0, 0.5, 0.25))
+        out.update({f"{k}_{tag}": v for k, v in cam_arrays(cam).items()})
+        out[f"{tag}_ns"] = np.int64(ns)
+    for tag, sc, res in (("toy", scene.standard_toy_scene(), (16, 16, 16)), ("rand", scene.random_toy_scene(7), (8, 5, 7))):
+        out[f"empty_{tag}"] = scene.analytically_empty_cells(sc, res)
+        out[f"empty_{tag}_res"] = np.array(res)
+    save("brute", **out)
+
+
 def main():
     what = sys.argv[1:] or ["rays", "pcg", "pointwise", "query", "render", "wide", "bulk", "scene", "ckpt", "extract",
-                            "train", "c2", "generic"]
+                            "train", "c2", "generic", "brute"]
     for w in what:
         t = time.time()
         globals()[f"gen_{w}"]()
