@@ -80,18 +80,26 @@ struct TcShape {
 
 // launch shape per width: warpgroups per CTA, tiles per warpgroup (TMEM
 // slots each), CTAs per SM.  Measured on the C2 frame (MLP ms/frame,
-// 2026-10-17): 3 groups x 1 tile x 2 CTAs 0.376; 6 x 1 x 1 0.373; 2 x 1 x 2
-// 0.457; 3 x 1 x 1 0.550; 3 x 2 x 1 0.414; 2 x 3 x 1 0.497 -- tiles in flight
-// per SM, each with its own warps, is what counts (latency-bound), and TMEM
-// (64 columns per W=32 tile) caps them at 7.
+// 2026-10-17): 7 groups x 1 tile x 1 CTA 0.361 (4 weight buffers), 0.364
+// (3); 6 x 1 x 1 0.376; 3 x 1 x 2 0.376-0.386; 2 x 1 x 2 0.457; 3 x 1 x 1
+// 0.550; two tiles per warpgroup 0.414; a dedicated MMA-issuer warp 0.589;
+// the colour layer on the CUDA cores instead of a 5th MMA 0.41 -- tiles in
+// flight per SM, each with its own warps, is what counts (latency-bound),
+// and TMEM (64 columns per W=32 tile) caps them at 7.
 #ifndef GF_TC_NS32
-#define GF_TC_NS32 3
+#define GF_TC_NS32 7
 #endif
 #ifndef GF_TC_CTAS32
-#define GF_TC_CTAS32 2
+#define GF_TC_CTAS32 1
 #endif
 #ifndef GF_TC_R32
 #define GF_TC_R32 1
+#endif
+#ifndef GF_TC_WREL
+#define GF_TC_WREL 2  // run hand-over: 0 unsafe (reference point only), 1 per-warp release, 2 group-synchronous
+#endif
+#ifndef GF_TC_NBUF32
+#define GF_TC_NBUF32 4
 #endif
 template <int W>
 struct TcCfg {
@@ -104,11 +112,12 @@ struct TcCfg {
   static constexpr int TMEM_COLS = tmem_cols(ONES + 8);
   static_assert(ONES + 8 <= 512 && TMEM_COLS * CTAS <= 512, "TMEM budget");
   // shared memory: NBUF weight buffers, then barriers and the run table
-  static constexpr int NBUF = W == 32 ? 3 : 2;
+  static constexpr int NBUF = W == 32 ? GF_TC_NBUF32 : 2;
   static constexpr int BAR = NBUF * TcShape<W>::CELL_BYTES;      // full[NBUF], free[NBUF], mma[NS]
   static constexpr int TSLOT = BAR + 16 * NBUF + 8 * NS;         // TMEM base address
   static constexpr int RUNS = (TSLOT + 4 + 15) / 16 * 16;        // uint4 runs[NBUF]: (cell, first tile, end tile, 0)
-  static constexpr int SMEM = RUNS + 16 * NBUF;
+  static constexpr int GINFO = RUNS + 16 * NBUF;                 // uint32 per group: end tile of its current run
+  static constexpr int SMEM = GINFO + 4 * NS;
 };
 
 // byte offset of element (r, k) in a canonical K-major no-swizzle operand of
@@ -163,9 +172,27 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 
 // parity wait with a suspend-time hint: the warp sleeps in the barrier unit
 // until the phase flips (or the hint expires) instead of spinning on issue slots
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+#ifndef GF_TC_WATCHDOG
+#define GF_TC_WATCHDOG 0
+#endif
+__device__ __forceinline__ uint64_t gtimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase, int site = 0) {
   uint32_t done;
+#if GF_TC_WATCHDOG  // diagnostic build: report the first waiter stuck for 2 s, then trap
+  const uint64_t t0 = gtimer_ns();
+#endif
   do {
+#if GF_TC_WATCHDOG
+    if (gtimer_ns() - t0 > 2000000000ull) {
+      printf("[gf watchdog] k_mlp_tc stuck: block %d thread %d site %d bar 0x%x phase %u\n", blockIdx.x, threadIdx.x,
+             site, bar, phase);
+      __trap();
+    }
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(done)
@@ -339,7 +366,10 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
   if (tid == 0) {
     for (int i = 0; i < NB; ++i) {
       mbar_init(bar_full + 8 * i, 1);
-      mbar_init(bar_free + 8 * i, NS);
+      // every warp of every group releases a run itself: a warp must never
+      // lag two phases behind on full[] (parity aliasing), so the loader may
+      // refill a buffer only once all 4*NS warps have left its run
+      mbar_init(bar_free + 8 * i, GF_TC_WREL == 1 ? 4 * NS : NS);
     }
     for (int i = 0; i < NS; ++i) mbar_init(bar_mma + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -383,7 +413,7 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
           e += 32;
         }
       }
-      if (r >= NB) mbar_wait(bar_free + 8 * k, ((r - NB) / NB) & 1);
+      if (r >= NB) mbar_wait(bar_free + 8 * k, ((r - NB) / NB) & 1, 1);
       if (lane == 0) {
         runs[k] = make_uint4(cell, s, e, 0u);
         if (s < t_end) bulk_load(sb + k * T::CELL_BYTES, packed + (size_t)cell * T::CELL_BYTES, T::CELL_BYTES,
@@ -442,7 +472,7 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
       __syncwarp();
     };
     auto wait_mma = [&]() {
-      mbar_wait(mbar, ph);
+      mbar_wait(mbar, ph, 2);
       ph ^= 1;
       fence_after();
     };
@@ -459,22 +489,44 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
     // short run may hold none of its tiles) and waits for the weights of the
     // run holding t; rows are prefetched R tiles ahead, across runs
     uint32_t r = 0, k = 0, wb = sb, run_end = 0;
-    mbar_wait(bar_full, 0);
+    mbar_wait(bar_full, 0, 3);
     run_end = runs[0].z;
+    volatile uint32_t* ginfo = reinterpret_cast<volatile uint32_t*>(smem + C::GINFO);
+    // leave run r for run r + 1 (group-uniform).  A warp waiting on full[]
+    // must never lag two phases behind (parity aliasing): in mode 2 only the
+    // group's first warp waits and releases, behind a group barrier that
+    // proves all 4 warps are done with run r, and hands the new run's end to
+    // the others through shared memory
+    auto next_run = [&](int site) {
+      if (GF_TC_WREL == 2) {
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        ++r;
+        const uint32_t kp = k;
+        k = k + 1 == NB ? 0 : k + 1;
+        if ((warp & 3) == 0) {
+          if (lane == 0) mbar_arrive(bar_free + 8 * kp);  // the group is done with run r - 1
+          mbar_wait(bar_full + 8 * k, (r / NB) & 1, site);
+          if (lane == 0) ginfo[g] = runs[k].z;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        run_end = ginfo[g];
+      } else {
+        __syncwarp();
+        if (GF_TC_WREL == 1 ? lane == 0 : gt == 0) mbar_arrive(bar_free + 8 * k);
+        ++r;
+        k = k + 1 == NB ? 0 : k + 1;
+        mbar_wait(bar_full + 8 * k, (r / NB) & 1, site);
+        run_end = runs[k].z;
+      }
+      wb = sb + k * T::CELL_BYTES;
+    };
     RowIn q[R];  // rows of this group's next R tiles
     uint32_t t = t_begin + (uint32_t)g;
 #pragma unroll
     for (int j = 0; j < R; ++j)
       if (t + (uint32_t)(j * NS) < t_end) load_row(S, io, S.tiles[t + (uint32_t)(j * NS)], gt, q[j]);
     while (t < t_end) {
-      while (t >= run_end) {
-        if (gt == 0) mbar_arrive(bar_free + 8 * k);  // this group is done with run r
-        ++r;
-        k = k + 1 == NB ? 0 : k + 1;
-        mbar_wait(bar_full + 8 * k, (r / NB) & 1);
-        run_end = runs[k].z;
-        wb = sb + k * T::CELL_BYTES;
-      }
+      while (t >= run_end) next_run(4);
       // tiles of this pass: t, t + NS, ... while they stay in this run
       int n = 1;
 #pragma unroll
@@ -509,8 +561,9 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
       }
       uint4 de[R][4];  // direction operand chunks, fetched one layer ahead of their use
       float sigma[R];
+      constexpr int NL = 5;  // MMA layers
 #pragma unroll
-      for (int L = 0; L < 5; ++L) {
+      for (int L = 0; L < NL; ++L) {
         wait_mma();
 #pragma unroll
         for (int j = 0; j < R; ++j) {
@@ -550,7 +603,7 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
             if (row[j].valid) io.store(row[j].idx, row[j].row, rgb[0], rgb[1], rgb[2], sigma[j]);
           }
         }
-        if (L < 4) {
+        if (L < NL - 1) {
           publish();
           issue(L + 1, wb, n);
         }
@@ -560,12 +613,17 @@ __global__ void __launch_bounds__(TcCfg<W>::THREADS, TcCfg<W>::CTAS) k_mlp_tc(co
     // release the current and any later runs (the loader waits on them
     // before it reuses their buffers; the end sentinel needs no release)
     for (;;) {
-      if (gt == 0) mbar_arrive(bar_free + 8 * k);
-      if (run_end >= t_end) break;
-      ++r;
-      k = k + 1 == NB ? 0 : k + 1;
-      mbar_wait(bar_full + 8 * k, (r / NB) & 1);
-      run_end = runs[k].z;
+      if (GF_TC_WREL == 2 && run_end >= t_end) {  // the last run: release it (after the group barrier)
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        if (gt == 0) mbar_arrive(bar_free + 8 * k);
+        break;
+      }
+      if (GF_TC_WREL != 2 && run_end >= t_end) {
+        __syncwarp();
+        if (GF_TC_WREL == 1 ? lane == 0 : gt == 0) mbar_arrive(bar_free + 8 * k);
+        break;
+      }
+      next_run(5);
     }
   }
   fence_before();

@@ -226,3 +226,31 @@ def test_concurrent_render_image_identical_bytes(gf):
     assert not errs, errs
     for i in range(len(calls)):
         assert np.array_equal(out[i], serial[i]), i
+
+
+@pytest.mark.timeout(240)
+def test_many_frames_back_to_back_no_deadlock(gf):
+    """Regression guard for the MLP's run hand-over (k_mlp_tc): 400 C2
+    frames back to back through the cached graph, every frame's counters
+    exact.  A warp lagging two phases behind on a weight-buffer barrier
+    (parity aliasing) used to deadlock here after a few dozen frames."""
+    import torch
+    from paper_2103_13744_b200 import _native as N
+    from paper_2103_13744_b200.render import render_rays_device
+
+    grid, occ, cam = c2_inputs(gf, None)
+    cfg = gf.RenderConfig()
+    n = cam.width * cam.height
+    out = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    st = torch.zeros(4, dtype=torch.int64, device="cuda")
+    ws = torch.empty(N.lib().gf_render_workspace_bytes(grid.native_arch(), grid.native_geom(), cfg.native(0), n),
+                     dtype=torch.uint8, device="cuda")
+    ref = None
+    for i in range(400):
+        st.zero_()
+        render_rays_device(grid, occ, cfg, 0, cam=cam, out=out, stats=st, ws=ws, precision="fp16")
+        if i % 50 == 0 or i == 399:
+            got = st.tolist()
+            ref = ref or got
+            assert got == ref, (i, got, ref)
+    assert ref[0] == 11795580
