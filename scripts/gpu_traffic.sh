@@ -11,6 +11,6 @@ for k in k_mlp_tc:6:6 k_march:7:7 k_place:6:6; do  # launches per C2 frame with 
     > gpurun_out/${TAG}_$name.log 2>&1
   echo "$name rc=$?"
 done
-python scripts/ncu_traffic.py gpurun_out/${TAG}_k_mlp_tc.ncu-rep gpurun_out/${TAG}_k_march.ncu-rep \
+python scripts/ncu_traffic.py --workload c2 gpurun_out/${TAG}_k_mlp_tc.ncu-rep gpurun_out/${TAG}_k_march.ncu-rep \
   gpurun_out/${TAG}_k_place.ncu-rep > gpurun_out/ncu_traffic.json
 cat gpurun_out/ncu_traffic.json

@@ -1,7 +1,10 @@
 #!/usr/bin/env python
 """Average per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum)
 and duration of each kernel in ncu reports covering one frame's launches.
-Prints JSON keyed "<stage>_fp16" as bench.py's roofline.traffic expects."""
+Prints JSON keyed "<workload>_<stage>_fp16" as bench.py's roofline.traffic
+expects (bench.py looks up f"{workload}_{dominant}_{precision}").
+
+  python scripts/ncu_traffic.py [--workload c2] report.ncu-rep ..."""
 import csv
 import io
 import json
@@ -11,8 +14,12 @@ import sys
 STAGE = {"k_mlp_tc": "mlp", "k_march": "march", "k_place": "scatter"}
 
 
-def main(paths):
-    out = {"how": "ncu --set full --clock-control none, every launch of one C2 frame (bench.py --steps 1 "
+def main(argv):
+    wl = "c2"
+    if argv and argv[0] == "--workload":
+        wl, argv = argv[1], argv[2:]
+    paths = argv
+    out = {"how": f"ncu --set full --clock-control none, every launch of one {wl.upper()} frame (bench.py --steps 1 "
                   "--warmup 1), mean over launches of dram__bytes_read.sum + dram__bytes_write.sum"}
     for p in paths:
         raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -32,9 +39,9 @@ def main(paths):
 
         rd, wr, dur = col("dram__bytes_read.sum"), col("dram__bytes_write.sum"), col("gpu__time_duration.sum")
         n = len(data)
-        out[f"{name}_fp16"] = (sum(rd) + sum(wr)) / n
-        out[f"{name}_detail"] = {"launches": n, "dram_read_per_launch": sum(rd) / n,
-                                 "dram_write_per_launch": sum(wr) / n, "mean_duration_s": sum(dur) / n}
+        out[f"{wl}_{name}_fp16"] = (sum(rd) + sum(wr)) / n
+        out[f"{wl}_{name}_detail"] = {"launches": n, "dram_read_per_launch": sum(rd) / n,
+                                      "dram_write_per_launch": sum(wr) / n, "mean_duration_us": 1e6 * sum(dur) / n}
     print(json.dumps(out, indent=1))
 
 
