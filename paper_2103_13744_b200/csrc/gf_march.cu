@@ -373,16 +373,18 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
     __shared__ uint32_t wsum[2][16];
     uint32_t* s_off = s_scan;
     uint32_t* s_toff = s_scan + n_cells + 1;
-    const int per = (int)((n_cells + 511) / 512);
+    const int per = (int)((n_cells + 511) / 512);  // <= 16 (n_cells <= 8192 on this path)
     const int64_t c0 = (int64_t)tid * per;
-    uint32_t a = 0, b = 0;
-    for (int q = 0; q < per; ++q) {
+    uint32_t a = 0, b = 0, cv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {  // all loads in flight at once, kept for the second pass
       const int64_t c = c0 + q;
-      if (c < n_cells) {
-        const uint32_t v = counts[c];
-        a += v;
-        b += (v + GF_TILE_ROWS - 1) / GF_TILE_ROWS;
-      }
+      cv[q] = (q < per && c < n_cells) ? counts[c] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      a += cv[q];
+      b += (cv[q] + GF_TILE_ROWS - 1) / GF_TILE_ROWS;
     }
     // block exclusive scan of (a, b)
     const int lane = tid & 31, wid = tid >> 5;
@@ -405,10 +407,11 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
     }
     __syncthreads();
     uint32_t ea = (wid ? wsum[0][wid - 1] : 0) + xa - a, eb = (wid ? wsum[1][wid - 1] : 0) + xb - b;
-    for (int q = 0; q < per; ++q) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
       const int64_t c = c0 + q;
-      if (c < n_cells) {
-        const uint32_t v = counts[c];
+      if (q < per && c < n_cells) {
+        const uint32_t v = cv[q];
         s_off[c] = ea;
         s_toff[c] = eb;
         ea += v;
@@ -429,13 +432,18 @@ __global__ void __launch_bounds__(512) k_place(GfGrid grid, RoundBufs RB, const 
       }
     }
     uint32_t* other = RB.counts + (size_t)((round + 1) & 1) * (size_t)n_cells;  // next round's histogram
-    for (uint64_t c = gtid; c < (uint64_t)n_cells; c += gthreads) {
-      other[c] = 0;
-      const uint32_t n_seg = s_off[c + 1] - s_off[c];
-      for (uint32_t t = s_toff[c]; t < s_toff[c + 1]; ++t) {
-        const uint32_t r0 = (t - s_toff[c]) * GF_TILE_ROWS;
-        Bk.tiles[t] = gf_make_tile((uint32_t)c, s_off[c] + r0, min(n_seg - r0, (uint32_t)GF_TILE_ROWS));
+    for (uint64_t c = gtid; c < (uint64_t)n_cells; c += gthreads) other[c] = 0;
+    // one thread per tile (a large cell's tiles would serialise one thread):
+    // the tile's cell is the last c with s_toff[c] <= u (binary search)
+    for (uint64_t u = gtid; u < (uint64_t)n_tiles; u += gthreads) {
+      uint32_t lo = 0, hi = (uint32_t)n_cells;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s_toff[mid] <= (uint32_t)u) lo = mid;
+        else hi = mid;
       }
+      const uint32_t n_seg = s_off[lo + 1] - s_off[lo], r0 = ((uint32_t)u - s_toff[lo]) * GF_TILE_ROWS;
+      Bk.tiles[u] = gf_make_tile(lo, s_off[lo] + r0, min(n_seg - r0, (uint32_t)GF_TILE_ROWS));
     }
     off = s_off;
   } else if (gtid == 0) {
