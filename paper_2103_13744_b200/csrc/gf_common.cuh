@@ -29,6 +29,17 @@ __host__ __device__ __forceinline__ uint64_t gf_pcg_output(u128 s) {
   return (x >> rot) | (x << ((64u - rot) & 63u));
 }
 
+// one 32-bit half of gf_pcg_output(s) (the float32 draw numpy takes from
+// it): the 64-bit rotate collapses to one funnel shift of the xor'd halves
+__device__ __forceinline__ uint32_t gf_pcg_output_half(u128 s, uint32_t hi_half) {
+  const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+  const uint64_t x = hi ^ lo;
+  const uint32_t rot = (uint32_t)(hi >> 58);
+  const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+  const bool sw = (((rot >> 5) ^ hi_half) & 1u) != 0;
+  return __funnelshift_r(sw ? xh : xl, sw ? xl : xh, rot);
+}
+
 __host__ __device__ __forceinline__ u128 gf_pcg_step(u128 s, u128 inc) { return s * GF_PCG_MULT + inc; }
 
 // LCG jump-ahead by `delta` steps (Brown, "Random number generation with

@@ -625,8 +625,16 @@ void launch_stats_fold(const unsigned long long* part, int64_t* stats, cudaStrea
 // -------------------------------------------------------------------------
 // one round's sampling for the marcher's ray i (render.py:311-330): placement,
 // ESS, histogram ranks, staging records, counters; `fw` is the ray's flag word
+// FAST: the benchmarked configuration fixed at compile time -- stratified,
+// float32-exact clip, network cell from the occupancy cell, no trace, no fine
+// pre-test -- so the candidate loop carries no flag tests or their constants.
+template <bool FAST>
 __device__ __forceinline__ void march_sample(const MarchParams& P, const RayState& R, const RoundBufs& B, int64_t i,
                                              uint32_t& fw, int round, int phase, MarchStats& ST) {
+  const bool stratified = FAST || P.stratified;
+  const bool from_occ = FAST || P.net_from_occ;
+  const bool tracing = !FAST && P.trace;
+  const uint32_t* fine_bits = FAST ? nullptr : P.fine_bits;
   // ---- sample round r (render.py:311-330)
   const int s0 = round * P.chunk;
   const int m = min(P.chunk, P.k - s0);
@@ -648,7 +656,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
   uint64_t outw = 0;
   uint64_t draw = 0;
   uint32_t blk = 0;
-  if (P.stratified && active) {
+  if (stratified && active) {
     // state of the word holding this round's first draw: a tabulated jump
     // from the ray's slot-0 state (R.rng stays read-only)
     const int64_t g = global_ray(P, i);
@@ -681,7 +689,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
     }
     cmask &= msk;
   }
-  const bool fast_clip = P.grid.fast != 0;
+  const bool fast_clip = FAST || P.grid.fast != 0;
   uint32_t* counts_r = B.counts + (size_t)par * (size_t)P.n_cells;  // this round's histogram
   uint32_t kept = 0;
   if (m <= 32) {
@@ -691,11 +699,13 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
     // on idle lanes.  Each candidate lane reads its ray's parameters from
     // shared memory (broadcast when several lanes share a ray).
     struct RayPar {
-      float4 o, d;      // origin + t0, direction + seg
+      double t0, seg, ox, oy, oz, dx, dy, dz;  // the float32 ray, widened once per round
       uint4 S;          // PCG64 state at draw d0 (rounded down to a word)
+      uint64_t rec;     // record index of the ray's first sample of this round
+      const u128* ci;   // the ray's block row of (sum_{k<d} A^k) * inc
       uint32_t i, d0;   // call-local ray index, float32 draw index of slot s0
       uint32_t carry;   // kept samples so far this round
-      uint32_t blk;     // the ray's slot in the per-block tables (seeds, C^d * inc)
+      uint32_t pad;
     };
     __shared__ RayPar s_ray[4][32];
     __shared__ uint16_t s_list[4][32 * 32];
@@ -714,10 +724,17 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
     const uint32_t d0 = (uint32_t)draw;  // float32 draw index of slot s0 in the ray's block stream
     {
       RayPar& rp = s_ray[wib][lane];
-      rp.o = o;
-      rp.d = d;
+      rp.t0 = t0;
+      rp.seg = sg64;
+      rp.ox = ox;
+      rp.oy = oy;
+      rp.oz = oz;
+      rp.dx = dx;
+      rp.dy = dy;
+      rp.dz = dz;
       rp.S = make_uint4((uint32_t)S, (uint32_t)(S >> 32), (uint32_t)(S >> 64), (uint32_t)(S >> 96));
-      rp.blk = blk;
+      rp.rec = base + half;
+      rp.ci = P.block_ci + (size_t)blk * GF_CI_N;
       rp.i = (uint32_t)i;
       rp.d0 = d0;
       rp.carry = 0;
@@ -730,7 +747,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
     }
     __syncwarp();
     uint32_t total = total_c;
-    if (P.fine_bits) {
+    if (fine_bits) {
       // pre-test at the segment midpoint against the dilated fine bitmap:
       // the exact sample lies within seg/2 (+ float32 margin) of it, so a
       // clear bit proves an ESS skip; survivors are compacted in place
@@ -747,12 +764,13 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
           bit[u] = 0u;
           if (e[u] != 0xFFFFFFFFu) {
             const RayPar& rp = s_ray[wib][e[u] >> 5];
-            const float tm = fmaf((float)(s0 + (int)(e[u] & 31u)) + 0.5f, rp.d.w, rp.o.w);
-            const float px = fmaf(tm, rp.d.x, rp.o.x), py = fmaf(tm, rp.d.y, rp.o.y), pz = fmaf(tm, rp.d.z, rp.o.z);
+            const float tm = fmaf((float)(s0 + (int)(e[u] & 31u)) + 0.5f, (float)rp.seg, (float)rp.t0);
+            const float px = fmaf(tm, (float)rp.dx, (float)rp.ox), py = fmaf(tm, (float)rp.dy, (float)rp.oy),
+                        pz = fmaf(tm, (float)rp.dz, (float)rp.oz);
             const uint32_t f = (uint32_t)(gf_bin_axis_fast(P.occ, 0, px) +
                                           P.occ.res[0] * (gf_bin_axis_fast(P.occ, 1, py) +
                                                           P.occ.res[1] * gf_bin_axis_fast(P.occ, 2, pz)));
-            word[u] = __ldg(P.fine_bits + (f >> 5));
+            word[u] = __ldg(fine_bits + (f >> 5));
             bit[u] = f & 31u;
           }
         }
@@ -787,37 +805,37 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       const uint32_t e = has ? (uint32_t)s_list[wib][k] : (32u << 5);
       const int own = (int)(e >> 5);  // 32 for idle lanes
       const int j = (int)(e & 31u);
-      double jit = 0.5;
-      float4 ro = make_float4(0.f, 0.f, 0.f, 0.f), rd = ro;
+      bool keep = false;
+      uint32_t cell = 0;
+      float px = 0.f, py = 0.f, pz = 0.f;
+      uint64_t rec = 0;
       uint32_t i_o = 0;
       if (has) {
         const RayPar& rp = s_ray[wib][own];
-        ro = rp.o;
-        rd = rp.d;
+        rec = rp.rec;
         i_o = rp.i;
-        if (P.stratified) {
+        // slot + jitter: f64(slot) + (u >> 8) * 2^-24 is exact (< 2^52 in
+        // units of 2^-24), so it is built as one integer and scaled
+        uint64_t v = ((uint64_t)(uint32_t)(s0 + j) << 24) | (1ull << 23);  // unstratified: slot + 0.5
+        if (stratified) {
           const uint32_t d0_o = rp.d0;
           const uint4 sv = rp.S;
           const u128 So = ((u128)(((uint64_t)sv.w << 32) | sv.z) << 64) | (((uint64_t)sv.y << 32) | sv.x);
           const uint32_t dd = d0_o + (uint32_t)j;
           const uint32_t delta = (dd >> 1) - (d0_o >> 1);
           // S_delta = A^delta S + (sum_{k<delta} A^k) inc; the second term is tabulated per block
-          const u128 Sj = ldg_u128(&P.jump[2 * delta]) * So + ldg_u128(&P.block_ci[(size_t)rp.blk * GF_CI_N + delta]);
-          const uint64_t w = gf_pcg_output(Sj);
-          const uint32_t u = (dd & 1) ? (uint32_t)(w >> 32) : (uint32_t)w;
-          jit = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, (int)(u >> 8)), 4503599627370496.0),
-                          5.9604644775390625e-8);
+          const u128 Sj = ldg_u128(&P.jump[2 * delta]) * So + ldg_u128(rp.ci + delta);
+          const uint32_t u = gf_pcg_output_half(Sj, dd & 1);
+          v = ((uint64_t)(uint32_t)(s0 + j) << 24) | (uint64_t)(u >> 8);
         }
-      }
-      bool keep = false;
-      uint32_t cell = 0;
-      float px = 0.f, py = 0.f, pz = 0.f;
-      if (has) {
+        const double x = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000 | (int)(v >> 32), (int)(uint32_t)v),
+                                             4503599627370496.0),
+                                   5.9604644775390625e-8);
         // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
-        const double t = __dadd_rn((double)ro.w, __dmul_rn(__dadd_rn((double)(s0 + j), jit), (double)rd.w));
-        px = __double2float_rn(__dadd_rn((double)ro.x, __dmul_rn(t, (double)rd.x)));
-        py = __double2float_rn(__dadd_rn((double)ro.y, __dmul_rn(t, (double)rd.y)));
-        pz = __double2float_rn(__dadd_rn((double)ro.z, __dmul_rn(t, (double)rd.z)));
+        const double t = __dadd_rn(rp.t0, __dmul_rn(x, rp.seg));
+        px = __double2float_rn(__dadd_rn(rp.ox, __dmul_rn(t, rp.dx)));
+        py = __double2float_rn(__dadd_rn(rp.oy, __dmul_rn(t, rp.dy)));
+        pz = __double2float_rn(__dadd_rn(rp.oz, __dmul_rn(t, rp.dz)));
         if (fast_clip) {
           px = gf_clip_fast(px, P.grid.b_min_f[0], P.grid.b_max_f[0]);
           py = gf_clip_fast(py, P.grid.b_min_f[1], P.grid.b_max_f[1]);
@@ -828,7 +846,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
           pz = gf_clip_component(pz, P.grid.b_min[2], P.grid.b_max[2]);
         }
         keep = true;
-        if (P.net_from_occ) {  // both grids fast, same box, occupancy cells nest 2^s per network cell
+        if (from_occ) {  // both grids fast, same box, occupancy cells nest 2^s per network cell
           const int ox = gf_bin_axis_fast(P.occ, 0, px), oy = gf_bin_axis_fast(P.occ, 1, py),
                     oz = gf_bin_axis_fast(P.occ, 2, pz);
           const uint32_t f = (uint32_t)(ox + P.occ.res[0] * (oy + P.occ.res[1] * oz));
@@ -867,11 +885,11 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       pend_leader = leader;
       if (keep) {
         const uint32_t pos = s_ray[wib][own].carry + __popc(kb & same & ((1u << lane) - 1u));
-        pend_addr = (uint64_t)i_o * (uint64_t)P.stride + half + pos;
+        pend_addr = rec + pos;
         pend_x = px;
         pend_y = py;
         pend_z = pz;
-        if (P.trace) {
+        if (tracing) {
           unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
           if ((int64_t)slotpos < P.trace_capacity)
             P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, (int64_t)i_o), (uint32_t)(s0 + j), cell};
@@ -962,6 +980,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
 
 // 7 CTAs/SM (<= 72 registers): measured faster than the unconstrained 85
 // registers despite a few spilled bytes
+template <bool FAST>
 __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
   gf_pdl_wait();     // the previous MLP / marcher pass
   const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
@@ -1056,9 +1075,12 @@ __global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, Rou
   // is placed by this one pass, else one round per launch (phase)
   const int nsub = P.fuse ? min(P.group, P.n_rounds - round) : 1;
 #pragma unroll 1
-  for (int sub = 0; sub < nsub; ++sub) march_sample(P, R, B, i, fw, round + sub, phase + sub, ST);
+  for (int sub = 0; sub < nsub; ++sub) march_sample<FAST>(P, R, B, i, fw, round + sub, phase + sub, ST);
   if (in_range && fw != fw0) R.flags[i] = fw;
   flush_stats(P, ST);
 }
+
+template __global__ void k_march<false>(MarchParams, RayState, RoundBufs, int, int);
+template __global__ void k_march<true>(MarchParams, RayState, RoundBufs, int, int);
 
 }  // namespace gf

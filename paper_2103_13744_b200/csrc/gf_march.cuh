@@ -138,6 +138,7 @@ __device__ __forceinline__ uint32_t gf_coarse_cell(const GfGrid& g, float x, flo
   }
   return (uint32_t)(idx[0] + g.res[0] * (idx[1] + g.res[1] * idx[2]));
 }
+template <bool FAST>
 __global__ void k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase);
 
 }  // namespace gf
