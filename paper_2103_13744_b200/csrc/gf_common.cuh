@@ -161,6 +161,14 @@ __device__ __forceinline__ int gf_bin_axis_fast(const GfGrid& g, int a, float x)
   return i < g.res[a] - 1 ? i : g.res[a] - 1;
 }
 
+// gf_bin_axis_fast for x already clipped into [b_min_f, b_max_f]: q >= 0,
+// so only the upper clamp (x == b_max) remains
+__device__ __forceinline__ int gf_bin_axis_clipped(const GfGrid& g, int a, float x) {
+  const float q = __fmul_rn(__fsub_rz(x, g.b_min_f[a]), g.inv_cell_f[a]);
+  const int i = __float_as_int(__fadd_rz(q, 8388608.0f)) - 0x4B000000;
+  return i < g.res[a] - 1 ? i : g.res[a] - 1;
+}
+
 __device__ __forceinline__ uint32_t gf_flat_cell_fast(const GfGrid& g, float x, float y, float z) {
   int ix = gf_bin_axis_fast(g, 0, x), iy = gf_bin_axis_fast(g, 1, y), iz = gf_bin_axis_fast(g, 2, z);
   return (uint32_t)(ix + g.res[0] * (iy + g.res[1] * iz));

@@ -705,7 +705,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       const u128* ci;   // the ray's block row of (sum_{k<d} A^k) * inc
       uint32_t i, d0;   // call-local ray index, float32 draw index of slot s0
       uint32_t carry;   // kept samples so far this round
-      uint32_t pad;
+      uint32_t span;    // the ray's candidates in the list: [span & 0xFFFF, span >> 16)
     };
     __shared__ RayPar s_ray[4][32];
     __shared__ uint16_t s_list[4][32 * 32];
@@ -738,6 +738,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       rp.i = (uint32_t)i;
       rp.d0 = d0;
       rp.carry = 0;
+      rp.span = (incl - cnt) | (incl << 16);
       uint32_t msk = cmask, pos = incl - cnt;  // candidate list in (lane, slot) order
       while (msk) {  // this lane's candidate slots, ascending
         const int j = __ffs(msk) - 1;
@@ -792,91 +793,98 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
     int pend_leader = (int)lane;
     uint64_t pend_addr = 0;
     float pend_x = 0.f, pend_y = 0.f, pend_z = 0.f;
+    const uint64_t pol_last = gf_pol_last();
     auto resolve = [&]() {  // warp-uniform
       const uint32_t b = __shfl_sync(0xffffffffu, pend_raw, pend_leader);
       if (pend_ok) {
         const uint32_t crank = b + __popc(pend_peers & ((1u << lane) - 1u));
-        gf_st_hint(B.rec + pend_addr, make_float4(pend_x, pend_y, pend_z, __uint_as_float(crank)), gf_pol_last());
+        gf_st_hint(B.rec + pend_addr, make_float4(pend_x, pend_y, pend_z, __uint_as_float(crank)), pol_last);
       }
     };
     for (uint32_t b0 = 0; b0 < total; b0 += 32) {
       const uint32_t k = b0 + lane;
       const bool has = k < total;
-      const uint32_t e = has ? (uint32_t)s_list[wib][k] : (32u << 5);
-      const int own = (int)(e >> 5);  // 32 for idle lanes
+      // idle lanes of a partial batch redo the list's last candidate (valid
+      // addresses, no divergent branches) and keep nothing
+      const uint32_t e = (uint32_t)s_list[wib][has ? k : total - 1u];
+      const int own = (int)(e >> 5);
       const int j = (int)(e & 31u);
-      bool keep = false;
-      uint32_t cell = 0;
-      float px = 0.f, py = 0.f, pz = 0.f;
-      uint64_t rec = 0;
-      uint32_t i_o = 0;
-      if (has) {
-        const RayPar& rp = s_ray[wib][own];
-        rec = rp.rec;
-        i_o = rp.i;
-        // slot + jitter: f64(slot) + (u >> 8) * 2^-24 is exact (< 2^52 in
-        // units of 2^-24), so it is built as one integer and scaled
-        uint64_t v = ((uint64_t)(uint32_t)(s0 + j) << 24) | (1ull << 23);  // unstratified: slot + 0.5
-        if (stratified) {
-          const uint32_t d0_o = rp.d0;
-          const uint4 sv = rp.S;
-          const u128 So = ((u128)(((uint64_t)sv.w << 32) | sv.z) << 64) | (((uint64_t)sv.y << 32) | sv.x);
-          const uint32_t dd = d0_o + (uint32_t)j;
-          const uint32_t delta = (dd >> 1) - (d0_o >> 1);
-          // S_delta = A^delta S + (sum_{k<delta} A^k) inc; the second term is tabulated per block
-          const u128 Sj = ldg_u128(&P.jump[2 * delta]) * So + ldg_u128(rp.ci + delta);
-          const uint32_t u = gf_pcg_output_half(Sj, dd & 1);
-          v = ((uint64_t)(uint32_t)(s0 + j) << 24) | (uint64_t)(u >> 8);
+      const RayPar& rp = s_ray[wib][own];
+      const uint64_t rec = rp.rec;
+      // slot + jitter: f64(slot) + (u >> 8) * 2^-24 is exact (< 2^52 in
+      // units of 2^-24), so it is built as one integer and scaled
+      uint64_t v = ((uint64_t)(uint32_t)(s0 + j) << 24) | (1ull << 23);  // unstratified: slot + 0.5
+      if (stratified) {
+        const uint32_t d0_o = rp.d0;
+        const uint4 sv = rp.S;
+        const u128 So = ((u128)(((uint64_t)sv.w << 32) | sv.z) << 64) | (((uint64_t)sv.y << 32) | sv.x);
+        const uint32_t dd = d0_o + (uint32_t)j;
+        const uint32_t delta = (dd >> 1) - (d0_o >> 1);
+        // S_delta = A^delta S + (sum_{k<delta} A^k) inc; the second term is tabulated per block
+        const u128 Sj = ldg_u128(&P.jump[2 * delta]) * So + ldg_u128(rp.ci + delta);
+        const uint32_t u = gf_pcg_output_half(Sj, dd & 1);
+        v = ((uint64_t)(uint32_t)(s0 + j) << 24) | (uint64_t)(u >> 8);
+      }
+      const double x = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000 | (int)(v >> 32), (int)(uint32_t)v),
+                                           4503599627370496.0),
+                                 5.9604644775390625e-8);
+      // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
+      const double t = __dadd_rn(rp.t0, __dmul_rn(x, rp.seg));
+      float px = __double2float_rn(__dadd_rn(rp.ox, __dmul_rn(t, rp.dx)));
+      float py = __double2float_rn(__dadd_rn(rp.oy, __dmul_rn(t, rp.dy)));
+      float pz = __double2float_rn(__dadd_rn(rp.oz, __dmul_rn(t, rp.dz)));
+      if (fast_clip) {
+        px = gf_clip_fast(px, P.grid.b_min_f[0], P.grid.b_max_f[0]);
+        py = gf_clip_fast(py, P.grid.b_min_f[1], P.grid.b_max_f[1]);
+        pz = gf_clip_fast(pz, P.grid.b_min_f[2], P.grid.b_max_f[2]);
+      } else {
+        px = gf_clip_component(px, P.grid.b_min[0], P.grid.b_max[0]);
+        py = gf_clip_component(py, P.grid.b_min[1], P.grid.b_max[1]);
+        pz = gf_clip_component(pz, P.grid.b_min[2], P.grid.b_max[2]);
+      }
+      bool keep;
+      uint32_t cell;
+      if (from_occ) {  // both grids fast, same box, occupancy cells nest 2^s per network cell
+        const int ox = gf_bin_axis_clipped(P.occ, 0, px), oy = gf_bin_axis_clipped(P.occ, 1, py),
+                  oz = gf_bin_axis_clipped(P.occ, 2, pz);
+        const uint32_t f = (uint32_t)(ox + P.occ.res[0] * (oy + P.occ.res[1] * oz));
+        keep = has && ((__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1);
+        cell = (uint32_t)((ox >> P.net_shift[0]) +
+                          P.grid.res[0] * ((oy >> P.net_shift[1]) + P.grid.res[1] * (oz >> P.net_shift[2])));
+      } else {
+        keep = has;
+        if (P.occ_bits) {
+          const uint32_t f = gf_flat_cell(P.occ, px, py, pz);
+          keep = keep && ((__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1);
         }
-        const double x = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000 | (int)(v >> 32), (int)(uint32_t)v),
-                                             4503599627370496.0),
-                                   5.9604644775390625e-8);
-        // t = f64(t0_32) + (f64(slot) + f64(jit)) * f64(seg_32); p = f32(f64(o32) + t*f64(d32))
-        const double t = __dadd_rn(rp.t0, __dmul_rn(x, rp.seg));
-        px = __double2float_rn(__dadd_rn(rp.ox, __dmul_rn(t, rp.dx)));
-        py = __double2float_rn(__dadd_rn(rp.oy, __dmul_rn(t, rp.dy)));
-        pz = __double2float_rn(__dadd_rn(rp.oz, __dmul_rn(t, rp.dz)));
-        if (fast_clip) {
-          px = gf_clip_fast(px, P.grid.b_min_f[0], P.grid.b_max_f[0]);
-          py = gf_clip_fast(py, P.grid.b_min_f[1], P.grid.b_max_f[1]);
-          pz = gf_clip_fast(pz, P.grid.b_min_f[2], P.grid.b_max_f[2]);
-        } else {
-          px = gf_clip_component(px, P.grid.b_min[0], P.grid.b_max[0]);
-          py = gf_clip_component(py, P.grid.b_min[1], P.grid.b_max[1]);
-          pz = gf_clip_component(pz, P.grid.b_min[2], P.grid.b_max[2]);
-        }
-        keep = true;
-        if (from_occ) {  // both grids fast, same box, occupancy cells nest 2^s per network cell
-          const int ox = gf_bin_axis_fast(P.occ, 0, px), oy = gf_bin_axis_fast(P.occ, 1, py),
-                    oz = gf_bin_axis_fast(P.occ, 2, pz);
-          const uint32_t f = (uint32_t)(ox + P.occ.res[0] * (oy + P.occ.res[1] * oz));
-          keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
-          cell = (uint32_t)((ox >> P.net_shift[0]) +
-                            P.grid.res[0] * ((oy >> P.net_shift[1]) + P.grid.res[1] * (oz >> P.net_shift[2])));
-        } else {
-          if (P.occ_bits) {
-            const uint32_t f = gf_flat_cell(P.occ, px, py, pz);
-            keep = (__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1;
-          }
-          if (keep) cell = gf_flat_cell(P.grid, px, py, pz);
-        }
-        if (!keep) cell = 0;
+        cell = keep ? gf_flat_cell(P.grid, px, py, pz) : 0u;
       }
       // position of this sample in its ray's run: kept items of the same ray
       // earlier in this batch + kept items of earlier batches
       const unsigned kb = __ballot_sync(0xffffffffu, keep);
-      const unsigned same = __match_any_sync(0xffffffffu, has ? own : 32 + (int)lane);
+      // lanes of this lane's ray in the batch up to and including it, and
+      // whether it is the ray's last lane here: a ray's candidates are
+      // contiguous in the list, unless the fine pre-test compacted it
+      unsigned run_le;
+      bool run_last;
+      if (fine_bits) {
+        const unsigned same = __match_any_sync(0xffffffffu, has ? own : 32 + (int)lane);
+        run_le = same & ((2u << lane) - 1u);
+        run_last = (int)lane == 31 - __clz(same);
+      } else {
+        const uint32_t span = rp.span;
+        const int lo = max((int)(span & 0xFFFFu) - (int)b0, 0);
+        run_le = ((2u << lane) - 1u) & ~((1u << lo) - 1u);
+        run_last = lane == 31u || k + 1u >= (span >> 16);
+      }
       // issue this batch's warp-aggregated rank atomic now, consume it one
       // batch later: the previous batch's records are stored meanwhile
       uint32_t peers = 0, raw = 0;
       int leader = (int)lane;
-      {
-        const unsigned act = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-          peers = __match_any_sync(act, cell);
-          leader = __ffs(peers) - 1;
-          if ((int)lane == leader) raw = atomicAdd(&counts_r[cell], (uint32_t)__popc(peers));
-        }
+      if (keep) {
+        peers = __match_any_sync(kb, cell);
+        leader = __ffs(peers) - 1;
+        if ((int)lane == leader) raw = atomicAdd(&counts_r[cell], (uint32_t)__popc(peers));
       }
       resolve();
       pend_ok = keep;
@@ -884,7 +892,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       pend_peers = peers;
       pend_leader = leader;
       if (keep) {
-        const uint32_t pos = s_ray[wib][own].carry + __popc(kb & same & ((1u << lane) - 1u));
+        const uint32_t pos = s_ray[wib][own].carry + __popc(kb & run_le & ((1u << lane) - 1u));
         pend_addr = rec + pos;
         pend_x = px;
         pend_y = py;
@@ -892,11 +900,11 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
         if (tracing) {
           unsigned long long slotpos = atomicAdd((unsigned long long*)P.trace_count, 1ull);
           if ((int64_t)slotpos < P.trace_capacity)
-            P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, (int64_t)i_o), (uint32_t)(s0 + j), cell};
+            P.trace[slotpos] = gf_trace_rec_t{px, py, pz, (uint32_t)global_ray(P, (int64_t)rp.i), (uint32_t)(s0 + j), cell};
         }
       }
       __syncwarp();
-      if (has && (int)lane == 31 - __clz(same)) s_ray[wib][own].carry += __popc(kb & same);
+      if (has && run_last) s_ray[wib][own].carry += __popc(kb & run_le);
       __syncwarp();
     }
     resolve();  // the last batch's records
@@ -980,8 +988,11 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
 
 // 7 CTAs/SM (<= 72 registers): measured faster than the unconstrained 85
 // registers despite a few spilled bytes
+#ifndef GF_MARCH_MINB
+#define GF_MARCH_MINB 7
+#endif
 template <bool FAST>
-__global__ void __launch_bounds__(128, 7) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
+__global__ void __launch_bounds__(128, GF_MARCH_MINB) k_march(MarchParams P, RayState R, RoundBufs B, int round, int phase) {
   gf_pdl_wait();     // the previous MLP / marcher pass
   const int64_t i = march_ray(P, (int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   const bool in_range = i < P.n_rays;
