@@ -586,6 +586,16 @@ struct MarchStats {
 
 __device__ __forceinline__ void flush_stats(const MarchParams& P, MarchStats& S) {  // warp-uniform
   const uint32_t slot = ((blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5)) & (GF_STAT_SLOTS - 1);
+  if (P.k < (1 << 24)) {
+    // a thread's counts in one pass are below 2k: the warp sum fits 32 bits,
+    // one REDUX per counter
+#pragma unroll
+    for (int c = 0; c < GF_STAT_COUNT; ++c) {
+      const unsigned v = __reduce_add_sync(0xffffffffu, (unsigned)S.v[c]);
+      if (gf_lane() == 0 && v) atomicAdd(P.stats_part + slot * GF_STAT_COUNT + c, (unsigned long long)v);
+    }
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < GF_STAT_COUNT; ++c) {
     unsigned long long v = S.v[c];
@@ -645,7 +655,7 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
   // samples may still die at their ERT checks, so its counters wait in R.pend
   const bool earlier = phase > 0 && (fw & gf_had_below(phase));
   const bool defer = alive && earlier;
-  const int par = (round / P.group) & 1;                       // histogram / emit-list parity
+  const int par = ((round - phase) / P.group) & 1;             // histogram / emit-list parity (group-uniform)
   const uint32_t half = (uint32_t)phase * (uint32_t)P.chunk;   // staging offset of the group's round
   ST.v[GF_STAT_ESS_SKIPPED] += (alive && !active && !defer) ? (unsigned long long)m : 0ull;
   if (defer && !active) R.pend[4 * (uint64_t)i + phase] = (uint32_t)m << 16;

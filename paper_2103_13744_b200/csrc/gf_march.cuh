@@ -96,9 +96,9 @@ __device__ __forceinline__ int64_t global_ray(const MarchParams& P, int64_t i) {
 // branches); out-of-image lanes get n_rays (inactive).
 __device__ __forceinline__ int64_t march_ray(const MarchParams& P, int64_t t) {
   if (!P.tile2d) return t;
-  const int64_t warp = t >> 5;
-  const int lane = (int)(t & 31);
-  const int64_t x = (warp % P.tiles_x) * 8 + (lane & 7), y = (warp / P.tiles_x) * 4 + (lane >> 3);
+  const uint32_t warp = (uint32_t)(t >> 5), lane = (uint32_t)t & 31u;  // < 2^32 warps per call
+  const uint32_t ty = warp / (uint32_t)P.tiles_x, tx = warp - ty * (uint32_t)P.tiles_x;
+  const int64_t x = (int64_t)(tx * 8u + (lane & 7u)), y = (int64_t)(ty * 4u + (lane >> 3));
   return (x < P.cam.width && y < P.cam.height) ? y * P.cam.width + x : P.n_rays;
 }
 // slot of the ray's block in the per-call seed table
