@@ -381,16 +381,24 @@ def measure_train(gf, torch, aabb, occ, cam, reps=5, cpu=True):
     ev[2].record()
     torch.cuda.synchronize()
     fwd_ms, bwd_ms = ev[0].elapsed_time(ev[1]) / reps, ev[1].elapsed_time(ev[2]) / reps
-    t0 = time.perf_counter()
+    # one untimed API step first: the kernel timing above left other packed
+    # weights and workspaces cached, and the first step re-validates them
+    loss, grads = train.photometric_loss_and_grads(grid, smp, gt, cfg.background)
+    train.adam_update(grid.params, grads, state, cfg.learning_rate, cfg)
+    torch.cuda.synchronize()
+    api = []
     for _ in range(reps):
+        t0 = time.perf_counter()
         loss, grads = train.photometric_loss_and_grads(grid, smp, gt, cfg.background)
         train.adam_update(grid.params, grads, state, cfg.learning_rate, cfg)
-    api_ms = (time.perf_counter() - t0) / reps * 1e3
+        torch.cuda.synchronize()
+        api.append(time.perf_counter() - t0)
+    api_ms = statistics.median(api) * 1e3
     flop = 3 * 12392 * q  # forward + backward data + parameter gradients, count_flops units
     out = {"samples": q, "rays": len(pix), "k_train": cfg.k_train, "forward_kernel_ms": fwd_ms,
            "backward_kernel_ms": bwd_ms, "backward_tflops": flop * 2 / 3 / (bwd_ms * 1e-3) / 1e12,
            "api_step_ms": api_ms, "loss": loss,
-           "note": "api_step_ms = photometric_loss_and_grads + adam_update through the reference API: the "
+           "note": "api_step_ms = median of 5 synchronised photometric_loss_and_grads + adam_update steps through the reference API (after one untimed step): the "
                    "gradients stay on the device unless read (DeviceGrads); the numpy parameters are updated in "
                    "place by one DMA into their page-locked storage; Adam moments stay on the device"}
     if cpu:

@@ -171,6 +171,80 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const float* __restrict__ sc
   }
 }
 
+// Phase B of one layer: gw[o][i] = sum_rows dz[o] * in[i] (fmaf chain in row
+// order from 0) and gb[o] = sum_rows dz[o] (fadd chain), accumulated into the
+// chunk's partial sums (first tile stores).  Threads own 4x4 (o, i) blocks:
+// 8 shared loads per 16 FMAs instead of 2 per FMA, and no per-parameter index
+// arithmetic; the per-parameter arithmetic sequence is unchanged.
+template <class S, int OUT, int IN, int DZ, int INO, int NT>
+__device__ __forceinline__ void bwd_layer_sums(const float* srow, int n_in, float* part, bool first, int tid, int& u) {
+  constexpr int LD = S::LD, OB = (OUT + 3) / 4, IB = (IN + 3) / 4, NB = OB * IB;
+  // units: NB weight blocks, then OB bias quads; unit u of the whole tile is
+  // handled by thread u % NT (u runs over every layer's units in order)
+  for (int b = (tid - u % NT + NT) % NT; b < NB + OB; b += NT) {
+    if (b < NB) {
+      const int o0 = (b / IB) * 4, i0 = (b % IB) * 4;
+      float acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
+      const float* dzp = srow + DZ + o0;
+      const float* inp = srow + INO + i0;
+      for (int rr = 0; rr < n_in; ++rr) {
+        float dz[4], in[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) dz[a] = (o0 + a < OUT) ? dzp[rr * LD + a] : 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) in[c] = (i0 + c < IN) ? inp[rr * LD + c] : 0.f;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[a][c] = fmaf(dz[a], in[c], acc[a][c]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (o0 + a < OUT && i0 + c < IN) {
+            float* q = part + (o0 + a) * IN + i0 + c;
+            *q = first ? acc[a][c] : __fadd_rn(*q, acc[a][c]);
+          }
+    } else {
+      const int o0 = (b - NB) * 4;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* dzp = srow + DZ + o0;
+      for (int rr = 0; rr < n_in; ++rr)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+          if (o0 + a < OUT) acc[a] = __fadd_rn(acc[a], dzp[rr * LD + a]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (o0 + a < OUT) {
+          float* q = part + OUT * IN + o0 + a;
+          *q = first ? acc[a] : __fadd_rn(*q, acc[a]);
+        }
+    }
+  }
+  u += NB + OB;
+}
+
+template <class S, int NT>
+__device__ __forceinline__ void bwd_param_sums(const float* srow, int n_in, float* part, bool first, int tid) {
+  int u = 0;  // running unit count: spreads the layers' remainders over different threads
+  bwd_layer_sums<S, S::out_dim(0), S::in_dim(0), S::dz_off(0), S::in_off(0), NT>(srow, n_in, part, first, tid, u);
+  part += S::count(0);
+  bwd_layer_sums<S, S::out_dim(1), S::in_dim(1), S::dz_off(1), S::in_off(1), NT>(srow, n_in, part, first, tid, u);
+  part += S::count(1);
+  bwd_layer_sums<S, S::out_dim(2), S::in_dim(2), S::dz_off(2), S::in_off(2), NT>(srow, n_in, part, first, tid, u);
+  part += S::count(2);
+  bwd_layer_sums<S, S::out_dim(3), S::in_dim(3), S::dz_off(3), S::in_off(3), NT>(srow, n_in, part, first, tid, u);
+  part += S::count(3);
+  bwd_layer_sums<S, S::out_dim(4), S::in_dim(4), S::dz_off(4), S::in_off(4), NT>(srow, n_in, part, first, tid, u);
+  part += S::count(4);
+  bwd_layer_sums<S, S::out_dim(5), S::in_dim(5), S::dz_off(5), S::in_off(5), NT>(srow, n_in, part, first, tid, u);
+}
+
 template <int W>
 __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const float* __restrict__ packed,
                                                                            Fp32Layout L, BwdArgs A,
@@ -297,22 +371,7 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
     }
     __syncthreads();
     // ---------------- phase B: parameter sums over this tile's rows (gw = dz^T in, gb = sum dz)
-    for (int p = tid; p < S::TOTAL; p += NT) {
-      int l = 0, qq = p;
-      while (qq >= S::count(l)) qq -= S::count(l++);
-      const int in = S::in_dim(l), out = S::out_dim(l);
-      const bool bias = qq >= out * in;
-      const int o = bias ? qq - out * in : qq / in, i = bias ? 0 : qq % in;
-      const float* dzp = srow + S::dz_off(l) + o;
-      const float* inp = srow + S::in_off(l) + i;
-      float acc = 0.f;
-      if (bias) {
-        for (int rr = 0; rr < n_in; ++rr) acc = __fadd_rn(acc, dzp[rr * LD]);
-      } else {
-        for (int rr = 0; rr < n_in; ++rr) acc = fmaf(dzp[rr * LD], inp[rr * LD], acc);
-      }
-      part[p] = t == 0 ? acc : __fadd_rn(part[p], acc);
-    }
+    bwd_param_sums<S, NT>(srow, n_in, part, t == 0, tid);
   }
 }
 
