@@ -51,6 +51,21 @@ struct BwdShape {
   static constexpr int LANES = 4;         // threads per row in phase A
   static constexpr int TR = 32;           // rows per tile
   static constexpr int THREADS = TR * LANES;
+  // W = 32: the four wide forward layers also staged transposed (wt[i][o],
+  // row stride OS = W + 4: 16-byte rows, 4-way conflicts on the one-time fill)
+  static constexpr bool WT = W == 32;
+  static constexpr int OS = W + 4;
+  static constexpr int T0 = 0, T1 = T0 + P * OS, T3 = T1 + W * OS, T4 = T3 + W * OS;
+  static constexpr int WT_FLOATS = WT ? T4 + (W + D) * OS : 0;
+  // ... and the rest of the cell's parameters (biases, density and colour
+  // weights) in a small block; the natural copy of the wide layers is not kept
+  static constexpr int WP = (W + 3) & ~3;
+  static constexpr int SB0 = 0, SB1 = W, SB2 = 2 * W, SB3 = 2 * W + 4, SB4 = 3 * W + 4, SB5 = 4 * W + 4;
+  static constexpr int SWD = 4 * W + 8, SWC = 5 * W + 8;
+  static constexpr int SM_FLOATS = WT ? SWC + 3 * WP : 0;
+  __host__ __device__ static constexpr int sb(int l) {
+    return l == 0 ? SB0 : (l == 1 ? SB1 : (l == 2 ? SB2 : (l == 3 ? SB3 : (l == 4 ? SB4 : SB5))));
+  }
   static constexpr int N_LAYERS = 6;
   // manifest order (mlp.py:73-84): trunk0, trunk1, density, feature, direction, color
   __host__ __device__ static constexpr int in_dim(int l) { return l == 0 ? P : (l == 4 ? W + D : W); }
@@ -91,6 +106,37 @@ __device__ __forceinline__ void dense_part(const float* __restrict__ w, const fl
   }
 }
 
+// dense_part with the layer's weights transposed in shared memory (wt[i][o],
+// OUT floats per input): each lane keeps NO independent accumulators and
+// streams the input once, instead of NO serial FMA chains over a register
+// copy of the input.  Same per-output arithmetic (fmaf over i ascending from
+// 0, then + b), so the values are identical.
+template <int IN, int OS, int NO, bool RELU>
+__device__ __forceinline__ void dense_part_t(const float* __restrict__ wt, const float* __restrict__ b,
+                                             const float* in_s, int o0, float* out_s) {
+  float acc[NO];
+#pragma unroll
+  for (int oo = 0; oo < NO; ++oo) acc[oo] = 0.f;
+#pragma unroll 4
+  for (int i = 0; i < IN; ++i) {
+    const float x = in_s[i];
+    const float4* wr = reinterpret_cast<const float4*>(wt + i * OS + o0);
+#pragma unroll
+    for (int v = 0; v < NO / 4; ++v) {
+      const float4 q = wr[v];
+      acc[4 * v + 0] = fmaf(x, q.x, acc[4 * v + 0]);
+      acc[4 * v + 1] = fmaf(x, q.y, acc[4 * v + 1]);
+      acc[4 * v + 2] = fmaf(x, q.z, acc[4 * v + 2]);
+      acc[4 * v + 3] = fmaf(x, q.w, acc[4 * v + 3]);
+    }
+  }
+#pragma unroll
+  for (int oo = 0; oo < NO; ++oo) {
+    const float z = __fadd_rn(acc[oo], b[o0 + oo]);
+    out_s[o0 + oo] = RELU ? fmaxf(z, 0.f) : z;
+  }
+}
+
 // dx[i] = sum_o dz[o] * W[o][i] for i in [i0, i0 + NI)  (matmul(dz, W), mlp.py:294-297)
 template <int NI, int INP, int OUT>
 __device__ __forceinline__ void dense_t_part(const float* __restrict__ w, const float* dz_s, int i0, float* dx) {
@@ -102,6 +148,28 @@ __device__ __forceinline__ void dense_t_part(const float* __restrict__ w, const 
     const float* wr = w + o * INP + i0;
 #pragma unroll
     for (int i = 0; i < NI; ++i) dx[i] = fmaf(g, wr[i], dx[i]);
+  }
+}
+
+// dense_t_part over weights transposed in shared memory (wt[i][o], row
+// stride OS): lane q owns inputs i = q + 4v (v < NI), so the four lanes of a
+// row read four different bank groups; dx[v] = sum_o dz[o] * W[o][i] as an
+// fmaf chain over o ascending from 0, like dense_t_part.
+template <int NI, int OUT, int OS>
+__device__ __forceinline__ void dense_t_part_t(const float* __restrict__ wt, const float* dz_s, int q, float* dx) {
+#pragma unroll
+  for (int v = 0; v < NI; ++v) dx[v] = 0.f;
+#pragma unroll 2
+  for (int o = 0; o < OUT; o += 4) {
+    const float g0 = dz_s[o], g1 = dz_s[o + 1], g2 = dz_s[o + 2], g3 = dz_s[o + 3];
+#pragma unroll
+    for (int v = 0; v < NI; ++v) {
+      const float4 w = *reinterpret_cast<const float4*>(wt + (q + 4 * v) * OS + o);
+      dx[v] = fmaf(g0, w.x, dx[v]);
+      dx[v] = fmaf(g1, w.y, dx[v]);
+      dx[v] = fmaf(g2, w.z, dx[v]);
+      dx[v] = fmaf(g3, w.w, dx[v]);
+    }
   }
 }
 
@@ -255,17 +323,47 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
   constexpr int P = S::P, D = S::D, TR = S::TR, LD = S::LD, NT = S::THREADS, Q = W / S::LANES;
   constexpr int PP = (P + 3) & ~3, WP = (W + 3) & ~3, DP = (W + D + 3) & ~3;
   extern __shared__ float4 smem4[];
+  // WT: [transposed wide layers | small block | rows]; else [packed cell | rows]
   float* sw = reinterpret_cast<float*>(smem4);
-  float* srow = sw + L.cell_floats;  // TR rows x LD floats
+  float* swt = sw;
+  float* ssm = sw + S::WT_FLOATS;
+  float* srow = S::WT ? ssm + S::SM_FLOATS : sw + L.cell_floats;  // TR rows x LD floats
   if (blockIdx.x >= *n_chunks) return;
   const uint2 ch = chunks[blockIdx.x];
   const int64_t cell = ch.x;
   const int tid = threadIdx.x;
   const int r = tid / S::LANES, q = tid % S::LANES;  // row of the tile, lane within the row
-  {
-    const float4* src = reinterpret_cast<const float4*>(packed + (size_t)cell * L.cell_floats);
+  const float* gsrc = packed + (size_t)cell * L.cell_floats;
+  if constexpr (S::WT) {
+    auto transpose = [&](int l, int in, int t_off) {
+      const float* w = gsrc + L.w_off[l];
+      const int inp = (in + 3) & ~3;
+      for (int e = tid; e < in * W; e += NT) {
+        const int o = e / in, i = e - o * in;  // contiguous reads of w[o][*]
+        swt[t_off + i * S::OS + o] = __ldg(w + o * inp + i);
+      }
+    };
+    transpose(0, P, S::T0);
+    transpose(1, W, S::T1);
+    transpose(3, W, S::T3);
+    transpose(4, W + D, S::T4);
+    auto copy = [&](int dst, int src, int n) {
+      for (int j = tid; j < n; j += NT) ssm[dst + j] = __ldg(gsrc + src + j);
+    };
+#pragma unroll
+    for (int l = 0; l < 6; ++l) copy(S::sb(l), L.b_off[l], S::out_dim(l));
+    copy(S::SWD, L.w_off[2], W);
+    copy(S::SWC, L.w_off[5], 3 * WP);
+  } else {
+    const float4* src = reinterpret_cast<const float4*>(gsrc);
     for (int j = tid; j < L.cell_floats / 4; j += NT) smem4[j] = __ldg(src + j);
   }
+  auto bias = [&](int l) -> const float* {
+    if constexpr (S::WT) return ssm + S::sb(l);
+    else return sw + L.b_off[l];
+  };
+  const float* w_den = S::WT ? ssm + S::SWD : sw + L.w_off[2];
+  const float* w_col = S::WT ? ssm + S::SWC : sw + L.w_off[5];
   const int64_t r0 = A.offsets[cell] + (int64_t)ch.y * GF_BWD_CHUNK;
   const int64_t r1 = min(A.offsets[cell + 1], r0 + (int64_t)GF_BWD_CHUNK);
   const int n_tiles = (int)((r1 - r0 + TR - 1) / TR);  // >= 1: chunks hold rows
@@ -318,20 +416,34 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
     }
     __syncwarp();
     // ---- forward (mlp.py:238-266)
-    if (on) dense_part<P, PP, Q, true>(sw + L.w_off[0], sw + L.b_off[0], s + S::X, q * Q, s + S::H0);
-    __syncwarp();
-    if (on) dense_part<W, WP, Q, true>(sw + L.w_off[1], sw + L.b_off[1], s + S::H0, q * Q, s + S::H1);
-    __syncwarp();
-    if (on) {
-      dense_part<W, WP, Q, false>(sw + L.w_off[3], sw + L.b_off[3], s + S::H1, q * Q, s + S::CAT);  // feature
-      if (q == 0) dense_part<W, WP, 1, true>(sw + L.w_off[2], sw + L.b_off[2], s + S::H1, 0, s + S::SIG);
+    if constexpr (S::WT) {
+      if (on) dense_part_t<P, S::OS, Q, true>(swt + S::T0, bias(0), s + S::X, q * Q, s + S::H0);
+      __syncwarp();
+      if (on) dense_part_t<W, S::OS, Q, true>(swt + S::T1, bias(1), s + S::H0, q * Q, s + S::H1);
+      __syncwarp();
+      if (on) {
+        dense_part_t<W, S::OS, Q, false>(swt + S::T3, bias(3), s + S::H1, q * Q, s + S::CAT);  // feature
+        if (q == 0) dense_part<W, WP, 1, true>(w_den, bias(2), s + S::H1, 0, s + S::SIG);
+      }
+      __syncwarp();
+      if (on) dense_part_t<W + D, S::OS, Q, true>(swt + S::T4, bias(4), s + S::CAT, q * Q, s + S::G);
+      __syncwarp();
+    } else {
+      if (on) dense_part<P, PP, Q, true>(sw + L.w_off[0], sw + L.b_off[0], s + S::X, q * Q, s + S::H0);
+      __syncwarp();
+      if (on) dense_part<W, WP, Q, true>(sw + L.w_off[1], sw + L.b_off[1], s + S::H0, q * Q, s + S::H1);
+      __syncwarp();
+      if (on) {
+        dense_part<W, WP, Q, false>(sw + L.w_off[3], sw + L.b_off[3], s + S::H1, q * Q, s + S::CAT);  // feature
+        if (q == 0) dense_part<W, WP, 1, true>(sw + L.w_off[2], sw + L.b_off[2], s + S::H1, 0, s + S::SIG);
+      }
+      __syncwarp();
+      if (on) dense_part<W + D, DP, Q, true>(sw + L.w_off[4], sw + L.b_off[4], s + S::CAT, q * Q, s + S::G);
+      __syncwarp();
     }
-    __syncwarp();
-    if (on) dense_part<W + D, DP, Q, true>(sw + L.w_off[4], sw + L.b_off[4], s + S::CAT, q * Q, s + S::G);
-    __syncwarp();
     // ---- backward (mlp.py:291-316)
     if (on && q < 3) {
-      dense_part<W, WP, 1, false>(sw + L.w_off[5], sw + L.b_off[5], s + S::G, q, s + S::ZC);  // logit q
+      dense_part<W, WP, 1, false>(w_col, bias(5), s + S::G, q, s + S::ZC);  // logit q
       const float col = sigmoid_split(s[S::ZC + q]);
       s[S::DZC + q] = __fmul_rn(__fmul_rn(A.d_color[3 * src + q], col), __fsub_rn(1.0f, col));
     }
@@ -339,35 +451,67 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
     __syncwarp();
     if (on) {  // dz_dir = (dz_color W_color) * (g > 0)
       float dv[Q];
-      dense_t_part<Q, WP, 3>(sw + L.w_off[5], s + S::DZC, q * Q, dv);
+      dense_t_part<Q, WP, 3>(w_col, s + S::DZC, q * Q, dv);
 #pragma unroll
       for (int i = 0; i < Q; ++i) s[S::DZD + q * Q + i] = s[S::G + q * Q + i] > 0.f ? dv[i] : 0.f;
     }
     __syncwarp();
-    if (on) {  // dfeat = first W columns of dz_dir W_direction
-      float dv[Q];
-      dense_t_part<Q, DP, W>(sw + L.w_off[4], s + S::DZD, q * Q, dv);
+    if constexpr (S::WT) {
+      // transposed wide layers: lane q owns inputs q + 4v
+      if (on) {  // dfeat = first W columns of dz_dir W_direction
+        float dv[Q];
+        dense_t_part_t<Q, W, S::OS>(swt + S::T4, s + S::DZD, q, dv);
 #pragma unroll
-      for (int i = 0; i < Q; ++i) s[S::DZF + q * Q + i] = dv[i];
-    }
-    __syncwarp();
-    if (on) {  // dz trunk1 = (dfeat W_feature + dz_density W_density) * (h1 > 0)
-      float dv[Q];
-      dense_t_part<Q, WP, W>(sw + L.w_off[3], s + S::DZF, q * Q, dv);
-      const float dzs = s[S::DZS];
-      const float* wd = sw + L.w_off[2] + q * Q;
-#pragma unroll
-      for (int i = 0; i < Q; ++i) {
-        const float h = __fadd_rn(dv[i], __fmul_rn(dzs, wd[i]));
-        s[S::DZ1 + q * Q + i] = s[S::H1 + q * Q + i] > 0.f ? h : 0.f;
+        for (int v = 0; v < Q; ++v) s[S::DZF + q + 4 * v] = dv[v];
       }
-    }
-    __syncwarp();
-    if (on) {  // dz trunk0 = (dz1 W_trunk1) * (h0 > 0)
-      float dv[Q];
-      dense_t_part<Q, WP, W>(sw + L.w_off[1], s + S::DZ1, q * Q, dv);
+      __syncwarp();
+      if (on) {  // dz trunk1 = (dfeat W_feature + dz_density W_density) * (h1 > 0)
+        float dv[Q];
+        dense_t_part_t<Q, W, S::OS>(swt + S::T3, s + S::DZF, q, dv);
+        const float dzs = s[S::DZS];
 #pragma unroll
-      for (int i = 0; i < Q; ++i) s[S::DZ0 + q * Q + i] = s[S::H0 + q * Q + i] > 0.f ? dv[i] : 0.f;
+        for (int v = 0; v < Q; ++v) {
+          const int i = q + 4 * v;
+          const float h = __fadd_rn(dv[v], __fmul_rn(dzs, w_den[i]));
+          s[S::DZ1 + i] = s[S::H1 + i] > 0.f ? h : 0.f;
+        }
+      }
+      __syncwarp();
+      if (on) {  // dz trunk0 = (dz1 W_trunk1) * (h0 > 0)
+        float dv[Q];
+        dense_t_part_t<Q, W, S::OS>(swt + S::T1, s + S::DZ1, q, dv);
+#pragma unroll
+        for (int v = 0; v < Q; ++v) {
+          const int i = q + 4 * v;
+          s[S::DZ0 + i] = s[S::H0 + i] > 0.f ? dv[v] : 0.f;
+        }
+      }
+    } else {
+      if (on) {  // dfeat = first W columns of dz_dir W_direction
+        float dv[Q];
+        dense_t_part<Q, DP, W>(sw + L.w_off[4], s + S::DZD, q * Q, dv);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) s[S::DZF + q * Q + i] = dv[i];
+      }
+      __syncwarp();
+      if (on) {  // dz trunk1 = (dfeat W_feature + dz_density W_density) * (h1 > 0)
+        float dv[Q];
+        dense_t_part<Q, WP, W>(sw + L.w_off[3], s + S::DZF, q * Q, dv);
+        const float dzs = s[S::DZS];
+        const float* wd = w_den + q * Q;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          const float h = __fadd_rn(dv[i], __fmul_rn(dzs, wd[i]));
+          s[S::DZ1 + q * Q + i] = s[S::H1 + q * Q + i] > 0.f ? h : 0.f;
+        }
+      }
+      __syncwarp();
+      if (on) {  // dz trunk0 = (dz1 W_trunk1) * (h0 > 0)
+        float dv[Q];
+        dense_t_part<Q, WP, W>(sw + L.w_off[1], s + S::DZ1, q * Q, dv);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) s[S::DZ0 + q * Q + i] = s[S::H0 + q * Q + i] > 0.f ? dv[i] : 0.f;
+      }
     }
     __syncthreads();
     // ---------------- phase B: parameter sums over this tile's rows (gw = dz^T in, gb = sum dz)
@@ -381,7 +525,8 @@ template <int W>
 static bool launch_bwd_width(const float* packed, const Fp32Layout& L, const BwdArgs& A, int64_t n_cells, int64_t n,
                              void* ws, cudaStream_t st) {
   using S = BwdShape<W>;
-  const size_t smem = (size_t)L.cell_floats * 4 + (size_t)S::TR * S::LD * 4;
+  const size_t smem =
+      (S::WT ? (size_t)(S::WT_FLOATS + S::SM_FLOATS) * 4 : (size_t)L.cell_floats * 4) + (size_t)S::TR * S::LD * 4;
   static thread_local size_t set = 0;
   if (set < smem) {
     if (cudaFuncSetAttribute(k_grouped_backward<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
