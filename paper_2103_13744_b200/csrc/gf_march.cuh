@@ -103,7 +103,8 @@ __device__ __forceinline__ int64_t march_ray(const MarchParams& P, int64_t t) {
 }
 // slot of the ray's block in the per-call seed table
 __device__ __forceinline__ int64_t seed_slot(const MarchParams& P, int64_t g) {
-  return (g / GF_RAY_BLOCK - P.first_block) / P.block_stride;
+  const int64_t b = g / GF_RAY_BLOCK - P.first_block;
+  return P.block_stride == 1 ? b : b / P.block_stride;  // no 64-bit division on the unsharded path
 }
 
 #define GF_JUMP_MAX 32  // largest PCG64 jump inside one round (chunk <= 32 -> <= 16 outputs)
