@@ -259,6 +259,14 @@ __device__ __forceinline__ void bwd_layer_sums(const float* srow, int n_in, floa
         for (int c = 0; c < 4; ++c) acc[a][c] = 0.f;
       const float* dzp = srow + DZ + o0;
       const float* inp = srow + INO + i0;
+      // later tiles add to the chunk's partial sums: their loads are issued
+      // before the row loop so the global latency overlaps it
+      float old[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          old[a][c] = (!first && o0 + a < OUT && i0 + c < IN) ? part[(o0 + a) * IN + i0 + c] : 0.f;
       for (int rr = 0; rr < n_in; ++rr) {
         float dz[4], in[4];
 #pragma unroll
@@ -274,24 +282,20 @@ __device__ __forceinline__ void bwd_layer_sums(const float* srow, int n_in, floa
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          if (o0 + a < OUT && i0 + c < IN) {
-            float* q = part + (o0 + a) * IN + i0 + c;
-            *q = first ? acc[a][c] : __fadd_rn(*q, acc[a][c]);
-          }
+          if (o0 + a < OUT && i0 + c < IN) part[(o0 + a) * IN + i0 + c] = first ? acc[a][c] : __fadd_rn(old[a][c], acc[a][c]);
     } else {
       const int o0 = (b - NB) * 4;
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float acc[4] = {0.f, 0.f, 0.f, 0.f}, old[4];
       const float* dzp = srow + DZ + o0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) old[a] = (!first && o0 + a < OUT) ? part[OUT * IN + o0 + a] : 0.f;
       for (int rr = 0; rr < n_in; ++rr)
 #pragma unroll
         for (int a = 0; a < 4; ++a)
           if (o0 + a < OUT) acc[a] = __fadd_rn(acc[a], dzp[rr * LD + a]);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
-        if (o0 + a < OUT) {
-          float* q = part + OUT * IN + o0 + a;
-          *q = first ? acc[a] : __fadd_rn(*q, acc[a]);
-        }
+        if (o0 + a < OUT) part[OUT * IN + o0 + a] = first ? acc[a] : __fadd_rn(old[a], acc[a]);
     }
   }
   u += NB + OB;
@@ -335,12 +339,18 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
   const int r = tid / S::LANES, q = tid % S::LANES;  // row of the tile, lane within the row
   const float* gsrc = packed + (size_t)cell * L.cell_floats;
   if constexpr (S::WT) {
+    // asynchronous 4-byte global -> shared copies (cp.async): every element
+    // is in flight at once instead of one load -> store round trip each
+    auto async4 = [&](float* dst, const float* src) {
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+    };
     auto transpose = [&](int l, int in, int t_off) {
       const float* w = gsrc + L.w_off[l];
       const int inp = (in + 3) & ~3;
       for (int e = tid; e < in * W; e += NT) {
         const int o = e / in, i = e - o * in;  // contiguous reads of w[o][*]
-        swt[t_off + i * S::OS + o] = __ldg(w + o * inp + i);
+        async4(swt + t_off + i * S::OS + o, w + o * inp + i);
       }
     };
     transpose(0, P, S::T0);
@@ -348,12 +358,13 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
     transpose(3, W, S::T3);
     transpose(4, W + D, S::T4);
     auto copy = [&](int dst, int src, int n) {
-      for (int j = tid; j < n; j += NT) ssm[dst + j] = __ldg(gsrc + src + j);
+      for (int j = tid; j < n; j += NT) async4(ssm + dst + j, gsrc + src + j);
     };
 #pragma unroll
     for (int l = 0; l < 6; ++l) copy(S::sb(l), L.b_off[l], S::out_dim(l));
     copy(S::SWD, L.w_off[2], W);
     copy(S::SWC, L.w_off[5], 3 * WP);
+    asm volatile("cp.async.wait_all;" ::: "memory");  // the tile loop's __syncthreads publishes them
   } else {
     const float4* src = reinterpret_cast<const float4*>(gsrc);
     for (int j = tid; j < L.cell_floats / 4; j += NT) smem4[j] = __ldg(src + j);
