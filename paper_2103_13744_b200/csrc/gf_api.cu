@@ -510,6 +510,7 @@ struct RenderWs {
   uint8_t* coarse_tmp;
   uint32_t* coarse_bits;
   uint32_t* fine_bits;
+  uint64_t* occ_brick;
   unsigned long long* stats_part;
 };
 
@@ -528,6 +529,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->coarse_tmp = c.take<uint8_t>((size_t)kMaxCoarseCells);
   w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->fine_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
+  w->occ_brick = c.take<uint64_t>((size_t)kMaxCoarseCells / 64);
   w->stats_part = c.take<unsigned long long>((size_t)GF_STAT_SLOTS * GF_STAT_COUNT);
   w->R.org = c.take<float4>((size_t)n_rays);
   w->R.dir = c.take<float4>((size_t)n_rays);
@@ -752,6 +754,11 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
         cplan.ores = make_int3(occ->res[0], occ->res[1], occ->res[2]);
         cplan.cres = make_int3(cplan.ores.x / f, cplan.ores.y / f, cplan.ores.z / f);
         cplan.word = cplan.ores.x % (32 * f) == 0;  // word-parallel OR-reduce + separable dilation
+        if (cplan.word && f == 4 && P.net_from_occ && !getenv("GF_NO_BRICK")) {  // the reduce also writes bricks
+          P.occ_brick = w.occ_brick;
+          P.brick_cx = cplan.cres.x;
+          P.brick_cy = cplan.cres.y;
+        }
         coarse_launches = cplan.word ? 4 : 2;
         const int3 cres = cplan.cres;
         gf_grid_geom_t cg = *occ;
@@ -791,7 +798,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
       uint32_t* t0 = reinterpret_cast<uint32_t*>(w.coarse_tmp);
       uint32_t* t1 = t0 + nw;
       gf_launch_pdl(k_coarse_reduce_w, dim3(gb), dim3(128), 0, s, reinterpret_cast<const uint32_t*>(occ_bits), ores,
-                    cplan.f, cres, t0);
+                    cplan.f, cres, t0, P.occ_brick ? w.occ_brick : (uint64_t*)nullptr);
       gf_launch_pdl(k_dilate_x, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, t1, cres, cplan.radius);
       gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t1, t0, cres, cplan.radius, 1);
       gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, w.coarse_bits, cres, cplan.radius, 2);
@@ -858,7 +865,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
     stage_mark(s, GF_STAGE_SETUP, (P.stratified ? 2 : 1) + coarse_launches);
     const int step = P.group;
     // the benchmarked configuration runs the marcher specialised for it
-    const bool fast_march = P.stratified && P.net_from_occ && P.grid.fast && !P.trace && !P.fine_bits &&
+    const bool fast_march = P.stratified && P.net_from_occ && P.occ_brick && P.grid.fast && !P.trace && !P.fine_bits &&
                             !getenv("GF_MARCH_GENERIC");
     auto* k_march_sel = fast_march ? k_march<true> : k_march<false>;
     for (int r = 0; r < P.n_rounds; r += step) {

@@ -303,12 +303,41 @@ __global__ void k_coarse_dilate(const uint8_t* __restrict__ coarse, int3 cres, i
 
 // Word-parallel variants (fine rows 32-bit aligned: occ res.x % (32*factor) == 0).
 // One thread = 32 coarse cells along x.
-__global__ void k_coarse_reduce_w(const uint32_t* __restrict__ fine, int3 ores, int f, int3 cres, uint32_t* out) {
+__global__ void k_coarse_reduce_w(const uint32_t* __restrict__ fine, int3 ores, int f, int3 cres, uint32_t* out,
+                                  uint64_t* brick) {
   gf_pdl_wait();
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int wpr = cres.x / 32;
   if (w >= (int64_t)wpr * cres.y * cres.z) return;
   const int wx = (int)(w % wpr), cy = (int)((w / wpr) % cres.y), cz = (int)(w / ((int64_t)wpr * cres.y));
+  if (brick && f == 4) {
+    // this word's 32 coarse cells as 4^3 bricks (bit dx + 4 dy + 16 dz) and
+    // their OR (the coarse bit): 16 fine rows of 4 words each
+    uint64_t br[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) br[b] = 0;
+#pragma unroll
+    for (int dz = 0; dz < 4; ++dz)
+#pragma unroll
+      for (int dy = 0; dy < 4; ++dy) {
+        const int64_t row = ((int64_t)ores.x * (4 * cy + dy + (int64_t)ores.y * (4 * cz + dz))) / 32 + (int64_t)wx * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t v = __ldg(fine + row + q);
+#pragma unroll
+          for (int bb = 0; bb < 8; ++bb) br[8 * q + bb] |= (uint64_t)((v >> (4 * bb)) & 0xFu) << (4 * dy + 16 * dz);
+        }
+      }
+    uint32_t res = 0;
+    uint64_t* dst = brick + ((int64_t)cz * cres.y + cy) * cres.x + 32 * wx;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      dst[b] = br[b];
+      res |= (br[b] != 0 ? 1u : 0u) << b;
+    }
+    out[w] = res;
+    return;
+  }
   uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int fz = cz * f; fz < cz * f + f; ++fz)
     for (int fy = cy * f; fy < cy * f + f; ++fy) {
@@ -857,8 +886,14 @@ __device__ __forceinline__ void march_sample(const MarchParams& P, const RayStat
       if (from_occ) {  // both grids fast, same box, occupancy cells nest 2^s per network cell
         const int ox = gf_bin_axis_clipped(P.occ, 0, px), oy = gf_bin_axis_clipped(P.occ, 1, py),
                   oz = gf_bin_axis_clipped(P.occ, 2, pz);
-        const uint32_t f = (uint32_t)(ox + P.occ.res[0] * (oy + P.occ.res[1] * oz));
-        keep = has && ((__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1);
+        if (FAST) {  // brick word of the sample's 4^3 block (k_coarse_reduce_w)
+          const uint32_t bi = (uint32_t)((ox >> 2) + P.brick_cx * ((oy >> 2) + P.brick_cy * (oz >> 2)));
+          const uint32_t bit = (uint32_t)((ox & 3) | ((oy & 3) << 2) | ((oz & 3) << 4));
+          keep = has && ((__ldg(P.occ_brick + bi) >> bit) & 1ull);
+        } else {
+          const uint32_t f = (uint32_t)(ox + P.occ.res[0] * (oy + P.occ.res[1] * oz));
+          keep = has && ((__ldg(P.occ_bits + (f >> 3)) >> (f & 7)) & 1);
+        }
         cell = (uint32_t)((ox >> P.net_shift[0]) +
                           P.grid.res[0] * ((oy >> P.net_shift[1]) + P.grid.res[1] * (oz >> P.net_shift[2])));
       } else {

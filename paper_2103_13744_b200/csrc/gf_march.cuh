@@ -28,6 +28,9 @@ struct MarchParams {
   unsigned long long* stats_part;  // GF_STAT_SLOTS x GF_STAT_COUNT partial counters (spread: no hot address)
   const uint32_t* fine_bits;  // occupancy dilated by >= seg/2 + margin (occupancy geometry): per-candidate
                               // pre-test at the segment midpoint, before the jitter and the exact placement
+  const uint64_t* occ_brick;  // the occupancy bits regrouped per 4^3 brick (one u64 per coarse cell, bit
+                              // x + 4y + 16z): a ray's consecutive samples share a word (k_march<true>)
+  int brick_cx, brick_cy;     // bricks per row / per column
   gf_camera_t cam;
   int use_cam;
   const float* origins;   // (n, 3) float32, or double when rays_f64
@@ -122,7 +125,7 @@ __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_
 __global__ void k_ray_init(MarchParams P, RayState R);
 __global__ void k_coarse_reduce(const uint8_t* occ_bits, int3 occ_res, int factor, int3 cres, uint8_t* coarse);
 __global__ void k_coarse_dilate(const uint8_t* coarse, int3 cres, int radius, uint32_t* bits);
-__global__ void k_coarse_reduce_w(const uint32_t* fine, int3 ores, int f, int3 cres, uint32_t* out);
+__global__ void k_coarse_reduce_w(const uint32_t* fine, int3 ores, int f, int3 cres, uint32_t* out, uint64_t* brick);
 __global__ void k_dilate_x(const uint32_t* in, uint32_t* out, int3 cres, int r);
 __global__ void k_dilate_yz(const uint32_t* in, uint32_t* out, int3 cres, int r, int axis);
 
