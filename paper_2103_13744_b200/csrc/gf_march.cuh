@@ -47,7 +47,7 @@ struct MarchParams {
   int k, chunk, n_rounds, stride, stratified, ert, eps_f64;
   int group;          // rounds per group (1, 2 or 4): placed by G passes, evaluated together, composited in order
   int fuse;           // one marcher launch places all of a group's rounds
-  int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp (whole-image camera calls)
+  int tile2d, tiles_x;  // k_march thread -> ray map: 8x4 pixel tiles per warp, 2x2 of them per CTA (whole-image calls)
   int64_t n_cells;
   int64_t march_threads;
   int count_candidates;  // diagnostics (GF_COUNT_CANDIDATES=1): exact-path candidates added to stats[N_RAYS]
@@ -100,7 +100,16 @@ __device__ __forceinline__ int64_t global_ray(const MarchParams& P, int64_t i) {
 __device__ __forceinline__ int64_t march_ray(const MarchParams& P, int64_t t) {
   if (!P.tile2d) return t;
   const uint32_t warp = (uint32_t)(t >> 5), lane = (uint32_t)t & 31u;  // < 2^32 warps per call
-  const uint32_t ty = warp / (uint32_t)P.tiles_x, tx = warp - ty * (uint32_t)P.tiles_x;
+  uint32_t ty, tx;
+  if (P.tile2d == 2) {  // a CTA's 4 warps cover 2x2 tiles (16x8 pixels): P.tiles_x counts CTA columns
+    const uint32_t cta = warp >> 2, wib = warp & 3u;
+    const uint32_t cy = cta / (uint32_t)P.tiles_x, cx = cta - cy * (uint32_t)P.tiles_x;
+    tx = 2 * cx + (wib & 1u);
+    ty = 2 * cy + (wib >> 1);
+  } else {
+    ty = warp / (uint32_t)P.tiles_x;
+    tx = warp - ty * (uint32_t)P.tiles_x;
+  }
   const int64_t x = (int64_t)(tx * 8u + (lane & 7u)), y = (int64_t)(ty * 4u + (lane >> 3));
   return (x < P.cam.width && y < P.cam.height) ? y * P.cam.width + x : P.n_rays;
 }
