@@ -447,11 +447,20 @@ def main():
     from paper_2103_13744_b200 import _native as N
     from paper_2103_13744_b200.render import ShardedFrame, render_image_distributed, render_rays_device
 
+    # GF_BENCH_SHARE_GPU=1 (test only): several ranks on one device over gloo,
+    # to exercise the multi-rank path (shards, gather, max-over-ranks timing)
+    # on a single-GPU box; the numbers of such a run mean nothing
+    share = os.environ.get("GF_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        if rank == 0:
-            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator log: N ranks, NVLS/P2P transport
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            if rank == 0:
+                os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator log: N ranks, NVLS/P2P transport
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.workload == "c4":
         aabb, grid, occ, cam = build_c4(gf)
     else:

@@ -254,3 +254,30 @@ def test_many_frames_back_to_back_no_deadlock(gf):
             ref = ref or got
             assert got == ref, (i, got, ref)
     assert ref[0] == 11795580
+
+
+@pytest.mark.timeout(600)
+def test_bench_two_ranks_share_one_gpu():
+    """The bench's multi-rank path end to end (torchrun, 2 ranks): each rank
+    renders its interleaved blocks of the C2 frame, the shards are gathered
+    and un-sharded inside the timed step and rank 0 prints one JSON line with
+    the whole frame's counters.  GF_BENCH_SHARE_GPU=1 puts both ranks on this
+    one device over gloo (the box has one GPU), so only the plumbing and the
+    counts are checked, not the speed."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, GF_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2", "--steps", "3",
+           "--warmup", "3", "--no-extras", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=540)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["steps"] == 3
+    assert d["queries_per_frame"] == 11795580
