@@ -7,6 +7,7 @@
 // atomic scatter; the public group_by_network entry point uses the stable
 // variant in gf_group.cu.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gf_bucket.cuh"
 
@@ -120,6 +121,69 @@ __global__ void __launch_bounds__(256) k_fill_tiles(BucketBufs B, int64_t n_cell
   }
 }
 
+// large grids: a two-kernel multi-CTA scan, 1024 cells per CTA, coalesced.
+// (a) every CTA's (rows, tiles) total into B.tile_off (as uint2 pairs)
+__global__ void __launch_bounds__(1024) k_scan_tot(BucketBufs B, int64_t n_cells) {
+  gf_pdl_wait();  // counts from the preceding pass
+  __shared__ uint2 warp_tot[32];
+  const int64_t c = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const uint32_t cnt = c < n_cells ? B.counts[c] : 0u;
+  uint2 tot;
+  block_exclusive_scan2<1024>(make_uint2(cnt, gf_div_up<uint32_t>(cnt, GF_TILE_ROWS)), warp_tot, tot);
+  if (threadIdx.x == 0) reinterpret_cast<uint2*>(B.tile_off)[blockIdx.x] = tot;
+}
+
+// (b) the predecessors' totals + this CTA's cells: offsets, cursors, cleared
+// counts, and the tiles of this CTA's cells (binary search in shared memory;
+// empty cells share their successor's first tile)
+__global__ void __launch_bounds__(1024) k_scan_apply(BucketBufs B, int64_t n_cells) {
+  gf_pdl_wait();
+  __shared__ uint2 warp_tot[32];
+  __shared__ uint32_t s_off[1025], s_toff[1025];
+  const int tid = threadIdx.x;
+  const uint2* tot = reinterpret_cast<const uint2*>(B.tile_off);
+  uint2 p = make_uint2(0, 0);
+  for (uint32_t k = tid; k < blockIdx.x; k += 1024) {
+    const uint2 v = tot[k];
+    p.x += v.x;
+    p.y += v.y;
+  }
+  uint2 pre;
+  block_exclusive_scan2<1024>(p, warp_tot, pre);
+  const int64_t cell0 = (int64_t)blockIdx.x * 1024, c = cell0 + tid;
+  const uint32_t cnt = c < n_cells ? B.counts[c] : 0u, nt = gf_div_up<uint32_t>(cnt, GF_TILE_ROWS);
+  uint2 mine;
+  uint2 ex = block_exclusive_scan2<1024>(make_uint2(cnt, nt), warp_tot, mine);
+  ex.x += pre.x;
+  ex.y += pre.y;
+  if (c < n_cells) {
+    B.offsets[c] = ex.x;
+    B.cursor[c] = ex.x;
+    B.counts[c] = 0;
+  }
+  s_off[tid] = ex.x;
+  s_toff[tid] = ex.y;
+  if (tid == 1023) {
+    s_off[1024] = ex.x + cnt;
+    s_toff[1024] = ex.y + nt;
+    if (blockIdx.x == gridDim.x - 1) {
+      B.offsets[n_cells] = ex.x + cnt;
+      *B.n_tiles = ex.y + nt;
+    }
+  }
+  __syncthreads();
+  for (uint32_t t = s_toff[0] + tid; t < s_toff[1024]; t += 1024) {
+    int lo = 0, hi = 1024;  // invariant: s_toff[lo] <= t < s_toff[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_toff[mid] <= t) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t r0 = (t - s_toff[lo]) * GF_TILE_ROWS, n_seg = s_off[lo + 1] - s_off[lo];
+    B.tiles[t] = gf_make_tile((uint32_t)(cell0 + lo), s_off[lo] + r0, min(n_seg - r0, (uint32_t)GF_TILE_ROWS));
+  }
+}
+
 // offsets + tile list.  Small grids: one CTA does both with the tile table in
 // shared memory.  Large grids / many tiles: the scan CTA writes the table to
 // global memory and a grid-wide kernel fills the tiles.
@@ -129,6 +193,16 @@ int launch_scan_cells(const BucketBufs& B, int64_t n_cells, cudaStream_t st, int
   const bool one_cta = n_cells <= smem_cells && max_rows <= (int64_t)1 << 20;
   b.scan_smem_cells = one_cta ? n_cells : 0;
   const size_t smem = one_cta ? (size_t)(n_cells + 1) * 4 : 0;
+  if (n_cells > smem_cells && !getenv("GF_SCAN_ONE_CTA")) {
+    // grids too large for one CTA's shared memory (C4: 32768 cells):
+    // per-CTA totals, then offsets + tiles (one CTA scanning 4096 cells at a
+    // time took 45 us + 9 us for the tiles; C4 frame 2.50 -> 2.24 ms).  Few
+    // cells with very many rows (C5) keep the grid-wide tile fill below.
+    const unsigned g = (unsigned)gf_div_up<int64_t>(n_cells, 1024);
+    gf_launch_pdl(k_scan_tot, dim3(g), dim3(1024), 0, st, b, n_cells);
+    gf_launch_pdl(k_scan_apply, dim3(g), dim3(1024), 0, st, b, n_cells);
+    return 2;
+  }
   gf_launch_pdl(k_scan_cells<1024, 4>, dim3(1), dim3(1024), smem, st, b, n_cells);
   if (!one_cta) {
     const int64_t max_tiles = max_rows / GF_TILE_ROWS + n_cells + 1;
