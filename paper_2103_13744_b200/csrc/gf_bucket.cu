@@ -465,7 +465,11 @@ int launch_query_bucket(const GfGrid& g, const float* pos, const float* dir, int
   cudaMemcpyAsync(cursor2, B.cursor, (size_t)n_cells * 4, cudaMemcpyDeviceToDevice, st);
   k_query_move_super<<<num_sms() * 2, GF_QB_THREADS, smem, st>>>(pos, dir, n, sb, keys, cursor2, trec, tdir, dest2);
   const int n_super = (int)((n_cells - 1) >> sb) + 1;
-  const unsigned per_super = (unsigned)std::max<int64_t>(1, (int64_t)num_sms() * 2 / n_super + 1);
+  // about 8 waves of CTAs (2 per SM): with one wave and a bit the last few
+  // CTAs ran alone (C5 move_cell 1.56 ms; 8 waves: scatter 4.13 -> 3.50 ms)
+  const char* pse = getenv("GF_QB_PER_SUPER");
+  const unsigned per_super =
+      pse ? (unsigned)atoi(pse) : (unsigned)std::max<int64_t>(1, gf_div_up<int64_t>((int64_t)num_sms() * 2 * 8, n_super));
   k_query_move_cell<<<dim3(per_super, (unsigned)n_super), GF_QB_THREADS, smem, st>>>(B.offsets, n_cells, sb, trec, tdir,
                                                                                       B.cursor, B.srec, B.sdir, dest3);
   return 2;
