@@ -24,11 +24,19 @@ def torch():
     return _torch
 
 
+_cuda_ok = False
+
+
 def require_cuda():
+    # checked once per process (is_available() queries NVML: ~1 us per call,
+    # and every render call passes through here several times)
+    global _cuda_ok
     t = torch()
-    if not t.cuda.is_available():
-        raise N.NativeError("no CUDA device: the gridfield B200 hot path has no CPU fallback")
-    N.lib()
+    if not _cuda_ok:
+        if not t.cuda.is_available():
+            raise N.NativeError("no CUDA device: the gridfield B200 hot path has no CPU fallback")
+        N.lib()
+        _cuda_ok = True
     return t
 
 
@@ -38,7 +46,12 @@ def device():
 
 
 def stream_handle() -> int:
-    return torch().cuda.current_stream().cuda_stream
+    """The caller's current CUDA stream as a raw cudaStream_t."""
+    t = torch()
+    raw = getattr(t._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return int(raw(t.cuda.current_device()))
+    return t.cuda.current_stream().cuda_stream
 
 
 def is_tensor(a) -> bool:
