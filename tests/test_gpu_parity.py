@@ -380,3 +380,29 @@ def test_grouped_rounds_bit_identical(precision, monkeypatch):
         for mode, img, st in runs[1:]:
             assert st == st0, (k, mode, st, st0)
             assert np.array_equal(img, img0), (k, mode)
+
+
+@pytest.mark.parametrize("w,h", [(37, 23), (130, 9), (16, 8), (17, 9)])
+def test_ragged_image_shapes_match_oracle(gf, w, h):
+    """Images whose sides are not multiples of the marcher's 16x8-pixel CTA
+    tiles (partial tiles at the right and bottom edges), on the toy 256^3
+    occupancy (occupancy bricks, specialised marcher): counts exact, colours
+    within the fp16 / fp32 bounds of the oracle."""
+    from oracle import gridfield_oracle as O
+
+    aabb = unit(gf)
+    g = gf.init_network_grid(aabb, (16, 16, 16), seed=0)
+    g.params.biases["density"][:] = 8.0
+    res, bits = toy_occupancy_bits()
+    occ = gf.OccupancyGrid(aabb, res, bits.copy())
+    c = gf.sphere_cameras(aabb, 1, 64, seed=7)[0]
+    cam = gf.Camera(w, h, c.fx * w / 64, c.fy * h / 64, w / 2, h / 2, c.c2w)
+    lat = O.init_lattice(aabb.b_min, aabb.b_max, (16, 16, 16), seed=0)
+    lat.biases["density"][:] = 8.0
+    occ_o = O.Occupancy(aabb.b_min, aabb.b_max, np.asarray(res), np.asarray(bits))
+    ref_img, ref = O.render_image(lat, occ_o, cam, O.MarchConfig(), seed=0)
+    for precision, tol in (("fp16", 1e-3), ("fp32", 2e-5)):
+        img, st = gf.render_image(g, occ, cam, gf.RenderConfig(), seed=0, precision=precision)
+        assert (st.total_queries, st.ess_skipped, st.ert_terminated_rays) == \
+            (ref.total_queries, ref.ess_skipped, ref.ert_terminated_rays), (w, h, precision)
+        assert float(np.abs(img - ref_img).max()) <= tol, (w, h, precision)
