@@ -406,3 +406,49 @@ def test_ragged_image_shapes_match_oracle(gf, w, h):
         assert (st.total_queries, st.ess_skipped, st.ert_terminated_rays) == \
             (ref.total_queries, ref.ess_skipped, ref.ert_terminated_rays), (w, h, precision)
         assert float(np.abs(img - ref_img).max()) <= tol, (w, h, precision)
+
+
+FUZZ = [  # (k, ert_chunk, epsilon, stratified, density bias, occupancy, grid res, image, seed)
+    (37, 5, 0.01, True, 12.0, "toy", (16, 16, 16), (20, 13), 1),
+    (96, 32, 0.2, True, 20.0, "toy", (4, 4, 4), (24, 24), 2),
+    (64, 17, 0.0, True, 3.0, "solid", (2, 3, 4), (11, 31), 3),
+    (50, 64, 0.05, True, 25.0, "toy", (16, 16, 16), (16, 16), 4),
+    (128, 32, 0.01, False, 20.0, "toy", (8, 8, 8), (19, 17), 5),
+    (33, 1, 0.3, True, 30.0, None, (16, 16, 16), (9, 7), 6),
+    (200, 24, 0.001, True, 15.0, "toy", (16, 16, 16), (32, 8), 7),
+]
+
+
+@pytest.mark.parametrize("case", FUZZ, ids=[f"k{c[0]}c{c[1]}e{c[2]}" for c in FUZZ])
+def test_config_fuzz_matches_oracle(gf, case):
+    """Assorted RenderConfig / lattice / occupancy / image combinations (chunk
+    sizes that are not 32, chunks longer than 32 (sequential marcher), k not
+    a multiple of the chunk, no ERT, unstratified, no occupancy, ragged
+    images) against the oracle: counts exact, colours within the fp16 / fp32
+    bounds."""
+    from oracle import gridfield_oracle as O
+
+    k, chunk, eps, strat, bias, oname, gres, (w, h), seed = case
+    aabb = unit(gf)
+    g = gf.init_network_grid(aabb, gres, seed=seed)
+    g.params.biases["density"][:] = bias
+    lat = O.init_lattice(aabb.b_min, aabb.b_max, gres, seed=seed)
+    lat.biases["density"][:] = bias
+    occ = occ_o = None
+    if oname == "toy":
+        res, bits = toy_occupancy_bits()
+    elif oname == "solid":
+        res, bits = np.array([128] * 3), np.asarray(gf.OccupancyGrid.solid(aabb, (128, 128, 128)).bits)
+    if oname is not None:
+        occ = gf.OccupancyGrid(aabb, res, np.asarray(bits).copy())
+        occ_o = O.Occupancy(aabb.b_min, aabb.b_max, np.asarray(res), np.asarray(bits))
+    c = gf.sphere_cameras(aabb, 1, 64, seed=seed + 10)[0]
+    cam = gf.Camera(w, h, c.fx * w / 64, c.fy * h / 64, w / 2, h / 2, c.c2w)
+    cfg = gf.RenderConfig(k=k, ert_chunk=chunk, epsilon=eps, stratified=strat)
+    ref_img, ref = O.render_image(lat, occ_o, cam, O.MarchConfig(k=k, ert_chunk=chunk, epsilon=eps,
+                                                                   stratified=strat), seed=seed)
+    for precision, tol in (("fp16", 1e-3), ("fp32", 2e-5)):
+        img, st = gf.render_image(g, occ, cam, cfg, seed=seed, precision=precision)
+        assert (st.total_queries, st.ess_skipped, st.ert_terminated_rays, st.n_rays) == \
+            (ref.total_queries, ref.ess_skipped, ref.ert_terminated_rays, w * h), (case, precision)
+        assert float(np.abs(img - ref_img).max()) <= tol, (case, precision)
