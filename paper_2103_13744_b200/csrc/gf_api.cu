@@ -511,6 +511,7 @@ struct RenderWs {
   uint32_t* coarse_bits;
   uint32_t* fine_bits;
   uint64_t* occ_brick;
+  uint32_t* occ_bbox;
   unsigned long long* stats_part;
 };
 
@@ -530,6 +531,7 @@ static size_t render_carve(Carve& c, int64_t n_rays, int64_t n_blocks, int strid
   w->coarse_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->fine_bits = c.take<uint32_t>((size_t)kMaxCoarseCells / 32);
   w->occ_brick = c.take<uint64_t>((size_t)kMaxCoarseCells / 64);
+  w->occ_bbox = c.take<uint32_t>(8);
   w->stats_part = c.take<unsigned long long>((size_t)GF_STAT_SLOTS * GF_STAT_COUNT);
   w->R.org = c.take<float4>((size_t)n_rays);
   w->R.dir = c.take<float4>((size_t)n_rays);
@@ -754,6 +756,7 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
         cplan.ores = make_int3(occ->res[0], occ->res[1], occ->res[2]);
         cplan.cres = make_int3(cplan.ores.x / f, cplan.ores.y / f, cplan.ores.z / f);
         cplan.word = cplan.ores.x % (32 * f) == 0;  // word-parallel OR-reduce + separable dilation
+        if (cplan.word && !getenv("GF_NO_BBOX")) P.occ_bbox = w.occ_bbox;  // DDA clipped to the set cells
         if (cplan.word && f == 4 && P.net_from_occ && !getenv("GF_NO_BRICK")) {  // the reduce also writes bricks
           P.occ_brick = w.occ_brick;
           P.brick_cx = cplan.cres.x;
@@ -797,11 +800,14 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
       const unsigned gb = (unsigned)gf_div_up<int64_t>(nw, 128);
       uint32_t* t0 = reinterpret_cast<uint32_t*>(w.coarse_tmp);
       uint32_t* t1 = t0 + nw;
+      uint32_t* bbox = (uint32_t*)P.occ_bbox;
       gf_launch_pdl(k_coarse_reduce_w, dim3(gb), dim3(128), 0, s, reinterpret_cast<const uint32_t*>(occ_bits), ores,
-                    cplan.f, cres, t0, P.occ_brick ? w.occ_brick : (uint64_t*)nullptr);
+                    cplan.f, cres, t0, P.occ_brick ? w.occ_brick : (uint64_t*)nullptr, bbox);
       gf_launch_pdl(k_dilate_x, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, t1, cres, cplan.radius);
-      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t1, t0, cres, cplan.radius, 1);
-      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, w.coarse_bits, cres, cplan.radius, 2);
+      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t1, t0, cres, cplan.radius, 1,
+                    (uint32_t*)nullptr);
+      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, w.coarse_bits, cres, cplan.radius, 2,
+                    bbox);
     } else {
       k_coarse_reduce<<<(unsigned)gf_div_up<int64_t>(ncc, 256), 256, 0, s>>>(occ_bits, ores, cplan.f, cres,
                                                                               w.coarse_tmp);
@@ -815,9 +821,10 @@ static int render_impl(const gf_arch_t* arch, const AnalyticDev* an, const ExtFi
       uint32_t* t1 = t0 + nw;
       gf_launch_pdl(k_dilate_x, dim3(gb), dim3(128), 0, s, reinterpret_cast<const uint32_t*>(occ_bits), t1, ores,
                     cplan.fine_radius);
-      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t1, t0, ores, cplan.fine_radius, 1);
+      gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t1, t0, ores, cplan.fine_radius, 1,
+                    (uint32_t*)nullptr);
       gf_launch_pdl(k_dilate_yz, dim3(gb), dim3(128), 0, s, (const uint32_t*)t0, w.fine_bits, ores,
-                    cplan.fine_radius, 2);
+                    cplan.fine_radius, 2, (uint32_t*)nullptr);
     }
   };
 

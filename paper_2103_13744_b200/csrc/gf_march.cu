@@ -69,9 +69,11 @@ __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_
 // non-candidate slot's sample provably lands in an empty fine cell.
 // -------------------------------------------------------------------------
 __device__ void coarse_intervals(const MarchParams& P, uint32_t* out, float ex, float ey, float ez, const float* d,
-                                 float smax, float seg) {
+                                 float smax, float seg, float s_lo, float s_hi) {
   const GfGrid& g = P.coarse;
-  const float pos[3] = {ex, ey, ez};
+  // the walk runs over [s_lo, s_hi] of the ray (distances from its entry):
+  // outside that range every coarse cell is clear (k_ray_init)
+  const float pos[3] = {fmaf(d[0], s_lo, ex), fmaf(d[1], s_lo, ey), fmaf(d[2], s_lo, ez)};
   int cell[3], step[3];
   float snext[3], sdelta[3];
 #pragma unroll
@@ -113,14 +115,14 @@ __device__ void coarse_intervals(const MarchParams& P, uint32_t* out, float ex, 
   // per-axis state in scalars (no local-memory arrays): next crossing
   // distance, crossing spacing, flat-index delta and steps left in the grid
   const int rx = g.res[0], rxy = g.res[0] * g.res[1];
-  float n0 = snext[0], n1 = snext[1], n2 = snext[2];
+  float n0 = s_lo + snext[0], n1 = s_lo + snext[1], n2 = s_lo + snext[2];
   const float e0 = sdelta[0], e1 = sdelta[1], e2 = sdelta[2];
   const int f0 = step[0], f1 = step[1] * rx, f2 = step[2] * rxy;
   int l0 = step[0] > 0 ? g.res[0] - 1 - cell[0] : cell[0];
   int l1 = step[1] > 0 ? g.res[1] - 1 - cell[1] : cell[1];
   int l2 = step[2] > 0 ? g.res[2] - 1 - cell[2] : cell[2];
   int c = cell[0] + rx * cell[1] + rxy * cell[2];
-  float s = 0.f, s_open = 0.f;
+  float s = s_lo, s_open = s_lo;
   bool open = false;
   for (int it = 0; it < 4096; ++it) {
     const bool occ = (__ldg(P.coarse_bits + (c >> 5)) >> (c & 31)) & 1;
@@ -132,7 +134,7 @@ __device__ void coarse_intervals(const MarchParams& P, uint32_t* out, float ex, 
     const bool a0 = n0 < n1 && n0 < n2;
     const bool a1 = !a0 && n1 < n2;
     const float sn = a0 ? n0 : (a1 ? n1 : n2);
-    if (!(sn < smax)) break;
+    if (!(sn < s_hi)) break;
     const int left = a0 ? l0 : (a1 ? l1 : l2);
     if (left == 0) break;  // the next crossing leaves the grid
     s = sn;
@@ -141,7 +143,7 @@ __device__ void coarse_intervals(const MarchParams& P, uint32_t* out, float ex, 
     else if (a1) { n1 += e1; --l1; }
     else { n2 += e2; --l2; }
   }
-  if (open) emit(s_open, smax);
+  if (open) emit(s_open, s_hi);
   for (int k = n; k < GF_MAX_IVL; ++k) out[k] = 0x0000FFFFu;  // empty (lo > hi)
 }
 
@@ -231,7 +233,34 @@ __global__ void k_ray_init(MarchParams P, RayState R) {
     const float ex = __double2float_rn(__dadd_rn((double)o32[0], __dmul_rn(t0, (double)d32[0])));
     const float ey = __double2float_rn(__dadd_rn((double)o32[1], __dmul_rn(t0, (double)d32[1])));
     const float ez = __double2float_rn(__dadd_rn((double)o32[2], __dmul_rn(t0, (double)d32[2])));
-    coarse_intervals(P, R.ivl + i * GF_MAX_IVL, ex, ey, ez, d32, (float)(t1 - t0), seg);
+    const float smax = (float)(t1 - t0);
+    // clip the walk to the set cells' bounding box, enlarged by one coarse
+    // cell on every side (float32 slab test; a miss leaves no candidate)
+    float s_lo = 0.f, s_hi = smax;
+    if (P.occ_bbox) {
+      const uint32_t* bb = P.occ_bbox;
+      const float e[3] = {ex, ey, ez};
+      if (bb[0] > bb[3]) s_hi = -1.f;  // no set coarse cell
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float cs = 1.f / P.coarse.inv_cell_f[a];
+        const float lo_w = fmaf((float)bb[a] - 1.f, cs, P.coarse.b_min_f[a]);
+        const float hi_w = fmaf((float)bb[3 + a] + 2.f, cs, P.coarse.b_min_f[a]);
+        if (d32[a] != 0.f) {
+          const float ta = (lo_w - e[a]) / d32[a], tb = (hi_w - e[a]) / d32[a];
+          s_lo = fmaxf(s_lo, fminf(ta, tb));
+          s_hi = fminf(s_hi, fmaxf(ta, tb));
+        } else if (e[a] < lo_w || e[a] > hi_w) {
+          s_hi = -1.f;
+        }
+      }
+    }
+    if (s_lo < s_hi) {
+      coarse_intervals(P, R.ivl + i * GF_MAX_IVL, ex, ey, ez, d32, smax, seg, s_lo, s_hi);
+    } else {
+#pragma unroll
+      for (int k = 0; k < GF_MAX_IVL; ++k) R.ivl[i * GF_MAX_IVL + k] = 0x0000FFFFu;  // no candidate slot
+    }
     if (P.n_rounds <= 24) {  // rounds holding at least one candidate slot
       const uint4* iv = reinterpret_cast<const uint4*>(R.ivl + i * GF_MAX_IVL);
       const uint4 q0 = iv[0], q1 = iv[1];
@@ -304,9 +333,10 @@ __global__ void k_coarse_dilate(const uint8_t* __restrict__ coarse, int3 cres, i
 // Word-parallel variants (fine rows 32-bit aligned: occ res.x % (32*factor) == 0).
 // One thread = 32 coarse cells along x.
 __global__ void k_coarse_reduce_w(const uint32_t* __restrict__ fine, int3 ores, int f, int3 cres, uint32_t* out,
-                                  uint64_t* brick) {
+                                  uint64_t* brick, uint32_t* bbox) {
   gf_pdl_wait();
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bbox && w < 6) bbox[w] = w < 3 ? 0xFFFFFFFFu : 0u;  // reduced by the last dilation pass
   const int wpr = cres.x / 32;
   if (w >= (int64_t)wpr * cres.y * cres.z) return;
   const int wx = (int)(w % wpr), cy = (int)((w / wpr) % cres.y), cz = (int)(w / ((int64_t)wpr * cres.y));
@@ -366,17 +396,39 @@ __global__ void k_dilate_x(const uint32_t* __restrict__ in, uint32_t* out, int3 
 }
 
 // axis 1: y (stride = words per row), axis 2: z (stride = words per plane)
-__global__ void k_dilate_yz(const uint32_t* __restrict__ in, uint32_t* out, int3 cres, int r, int axis) {
+__global__ void k_dilate_yz(const uint32_t* __restrict__ in, uint32_t* out, int3 cres, int r, int axis,
+                            uint32_t* bbox) {
   gf_pdl_wait();
   const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int wpr = cres.x / 32;
-  if (w >= (int64_t)wpr * cres.y * cres.z) return;
-  const int64_t stride = axis == 1 ? wpr : (int64_t)wpr * cres.y;
-  const int n = axis == 1 ? cres.y : cres.z;
-  const int c = axis == 1 ? (int)((w / wpr) % cres.y) : (int)(w / ((int64_t)wpr * cres.y));
+  const bool valid = w < (int64_t)wpr * cres.y * cres.z;
   uint32_t res = 0;
-  for (int o = max(c - r, 0); o <= min(c + r, n - 1); ++o) res |= in[w + (int64_t)(o - c) * stride];
-  out[w] = res;
+  if (valid) {
+    const int64_t stride = axis == 1 ? wpr : (int64_t)wpr * cres.y;
+    const int n = axis == 1 ? cres.y : cres.z;
+    const int c = axis == 1 ? (int)((w / wpr) % cres.y) : (int)(w / ((int64_t)wpr * cres.y));
+    for (int o = max(c - r, 0); o <= min(c + r, n - 1); ++o) res |= in[w + (int64_t)(o - c) * stride];
+    out[w] = res;
+  }
+  if (bbox) {  // the final pass: bounding box of the set cells (warp-reduced, then 6 atomics per warp)
+    uint32_t lo[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, hi[3] = {0u, 0u, 0u};
+    if (res) {
+      const uint32_t wx = (uint32_t)(w % wpr), y = (uint32_t)((w / wpr) % cres.y),
+                     z = (uint32_t)(w / ((int64_t)wpr * cres.y));
+      lo[0] = 32u * wx + (uint32_t)(__ffs(res) - 1);
+      hi[0] = 32u * wx + 31u - (uint32_t)__clz(res);
+      lo[1] = hi[1] = y;
+      lo[2] = hi[2] = z;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const uint32_t l = __reduce_min_sync(0xffffffffu, lo[a]), h = __reduce_max_sync(0xffffffffu, hi[a]);
+      if (gf_lane() == 0 && l <= h) {
+        atomicMin(bbox + a, l);
+        atomicMax(bbox + 3 + a, h);
+      }
+    }
+  }
 }
 
 // -------------------------------------------------------------------------

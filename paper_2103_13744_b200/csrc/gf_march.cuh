@@ -31,6 +31,8 @@ struct MarchParams {
   const uint64_t* occ_brick;  // the occupancy bits regrouped per 4^3 brick (one u64 per coarse cell, bit
                               // x + 4y + 16z): a ray's consecutive samples share a word (k_march<true>)
   int brick_cx, brick_cy;     // bricks per row / per column
+  const uint32_t* occ_bbox;   // set cells of the dilated coarse mip: x,y,z min then max (coarse cells);
+                              // the ray's DDA runs only inside this box (min > max: no set cell)
   gf_camera_t cam;
   int use_cam;
   const float* origins;   // (n, 3) float32, or double when rays_f64
@@ -134,9 +136,10 @@ __global__ void k_seed_blocks(uint64_t seed, int64_t first_block, int64_t block_
 __global__ void k_ray_init(MarchParams P, RayState R);
 __global__ void k_coarse_reduce(const uint8_t* occ_bits, int3 occ_res, int factor, int3 cres, uint8_t* coarse);
 __global__ void k_coarse_dilate(const uint8_t* coarse, int3 cres, int radius, uint32_t* bits);
-__global__ void k_coarse_reduce_w(const uint32_t* fine, int3 ores, int f, int3 cres, uint32_t* out, uint64_t* brick);
+__global__ void k_coarse_reduce_w(const uint32_t* fine, int3 ores, int f, int3 cres, uint32_t* out, uint64_t* brick,
+                                  uint32_t* bbox);
 __global__ void k_dilate_x(const uint32_t* in, uint32_t* out, int3 cres, int r);
-__global__ void k_dilate_yz(const uint32_t* in, uint32_t* out, int3 cres, int r, int axis);
+__global__ void k_dilate_yz(const uint32_t* in, uint32_t* out, int3 cres, int r, int axis, uint32_t* bbox);
 
 // Approximate (clamped) coarse cell of a float32 point; exactness is not
 // needed because the mip is dilated past the evaluation error.
