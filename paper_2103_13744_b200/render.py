@@ -12,6 +12,7 @@ host only transfers the camera in and the image + 4 counters out.
 from __future__ import annotations
 
 import threading
+import os
 import time
 from dataclasses import dataclass
 
@@ -285,12 +286,25 @@ def _box_geom(aabb):
     return N.make_geom(aabb, (1, 1, 1))
 
 
+_WS_CACHE: dict = {}
+
+
 def _render_ws_bytes(field, ncfg, n: int) -> int:
     if _is_analytic(field):
         return N.lib().gf_render_analytic_workspace_bytes(field.native(), ncfg, n)
     if _is_caller_field(field):
         return N.lib().gf_render_field_workspace_bytes(_box_geom(field.aabb), ncfg, n)
-    return N.lib().gf_render_workspace_bytes(field.native_arch(), field.native_geom(), ncfg, n)
+    # cached per (architecture, resolution, k, chunk, rays, GF_GROUP): one
+    # native call and two struct builds saved on every render_image
+    key = (field.params.arch, tuple(int(r) for r in field.resolution), ncfg.k, ncfg.ert_chunk, int(n),
+           os.environ.get("GF_GROUP"))
+    b = _WS_CACHE.get(key)
+    if b is None:
+        b = N.lib().gf_render_workspace_bytes(field.native_arch(), field.native_geom(), ncfg, n)
+        if len(_WS_CACHE) > 256:
+            _WS_CACHE.clear()
+        _WS_CACHE[key] = b
+    return b
 
 
 def _field_callback(field, errors: list):
@@ -468,7 +482,9 @@ def render_image(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0
     ncfg = cfg.native(seed)
     ws_bytes = _render_ws_bytes(grid, ncfg, n)
     c = _render_context(n, ws_bytes)
-    c["stats"].zero_()
+    if not c.get("stats_zero"):  # normally zeroed at the end of the previous call, off the critical path
+        c["stats"].zero_()
+    c["stats_zero"] = False
     rgb, st, _ = render_rays_device(grid, occupancy, cfg, seed, cam=cam, precision=precision, out=c["rgb"],
                                     stats=c["stats"], ws=c["ws"])
     # fresh pinned block per call (torch's caching host allocator recycles it
@@ -476,7 +492,9 @@ def render_image(field, occupancy, cam: Camera, cfg: RenderConfig, seed: int = 0
     host = t.empty(rgb.shape, dtype=t.float32, pin_memory=True)
     host.copy_(rgb, non_blocking=True)
     c["host_stats"].copy_(st, non_blocking=True)
+    c["stats"].zero_()  # stream-ordered after the copy: ready for the next call
     t.cuda.current_stream().synchronize()
+    c["stats_zero"] = True
     stats = _stats_from(c["host_stats"])
     stats.wall_ms = (time.perf_counter() - t_start) * 1000.0
     return host.numpy().reshape(cam.height, cam.width, 3), stats
