@@ -31,6 +31,10 @@ DEFAULT_PRECISION = "fp32"
 RENDER_DEFAULT_PRECISION = "fp16"  # GF_RENDER_PRECISION=fp32 restores the reference's float32 renders
 
 
+
+_TC_ARCH: dict = {}  # (arch, encoding) -> tcgen05 kernel covers it
+_NATIVE_ARCH: dict = {}  # (arch, encoding) -> gf_arch_t
+
 @dataclass
 class NetworkGrid:
     """grid.py:19-56."""
@@ -78,10 +82,20 @@ class NetworkGrid:
     def tensor_core_arch(self) -> bool:
         """True if the fused tcgen05 kernel covers this manifest (4 hidden
         layers of width 32 or 64, no skip layer, 10/4 octaves with raw input)."""
-        return N.lib().gf_packed_bytes(C.byref(self.native_arch()), 1, N.PRECISION["fp16"]) > 0
+        key = (self.arch, self.encoding)
+        hit = _TC_ARCH.get(key)
+        if hit is None:
+            hit = _TC_ARCH[key] = N.lib().gf_packed_bytes(C.byref(self.native_arch()), 1, N.PRECISION["fp16"]) > 0
+        return hit
 
     def native_arch(self) -> N.Arch:
-        return N.make_arch(self.arch, self.encoding)
+        # one struct per (architecture, encoding): both are frozen dataclasses,
+        # and the library only reads it (const gf_arch_t*)
+        key = (self.arch, self.encoding)
+        a = _NATIVE_ARCH.get(key)
+        if a is None:
+            a = _NATIVE_ARCH[key] = N.make_arch(self.arch, self.encoding)
+        return a
 
     def native_geom(self) -> N.GridGeom:
         return N.make_geom(self.aabb, self.resolution)
