@@ -16,6 +16,11 @@
 // device results are deterministic run to run.
 #include "gf_mlp_simt.cuh"
 #include "gf_train.cuh"
+#include "gf_tc_ptx.cuh"
+
+#include <cuda_bf16.h>
+
+#include <cstdlib>
 
 namespace gf {
 
@@ -178,20 +183,16 @@ __device__ __forceinline__ void dense_t_part_t(const float* __restrict__ wt, con
 // sums land in scratch row k and k_bwd_reduce adds a cell's chunks in order
 #define GF_BWD_CHUNK 256
 
-__global__ void __launch_bounds__(1024) k_bwd_plan(const int64_t* __restrict__ offsets, int64_t n_cells, uint2* chunks,
-                                                   uint32_t* chunk_off, uint32_t* n_chunks) {
-  __shared__ uint32_t wsum[32];
+// 1024-thread exclusive scan of one value per thread (wsum: 32 words of shared memory)
+__device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t local, uint32_t* wsum) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t per = (n_cells + 1023) / 1024, c0 = (int64_t)tid * per;
-  uint32_t local = 0;
-  for (int64_t c = c0; c < c0 + per && c < n_cells; ++c)
-    local += (uint32_t)((offsets[c + 1] - offsets[c] + GF_BWD_CHUNK - 1) / GF_BWD_CHUNK);
   uint32_t x = local;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
+  __syncthreads();  // wsum free (a previous scan's readers are done)
   if (lane == 31) wsum[wid] = x;
   __syncthreads();
   if (wid == 0) {
@@ -204,38 +205,113 @@ __global__ void __launch_bounds__(1024) k_bwd_plan(const int64_t* __restrict__ o
     wsum[lane] = t;
   }
   __syncthreads();
-  uint32_t base = (wid ? wsum[wid - 1] : 0u) + x - local;
+  return (wid ? wsum[wid - 1] : 0u) + x - local;
+}
+
+// chunk_tile (tensor-core path): index of the chunk's first 32-row operand
+// tile; a cell's chunks are 256-row aligned, so chunk j of cell c starts at
+// tile(c) + 8 j with tile(c) = sum over earlier cells of ceil(rows / 32)
+__global__ void __launch_bounds__(1024) k_bwd_plan(const int64_t* __restrict__ offsets, int64_t n_cells, uint2* chunks,
+                                                   uint32_t* chunk_off, uint32_t* n_chunks, uint32_t* chunk_tile,
+                                                   uint4* red_cells, uint32_t* n_red, int red_blocks) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t s_red;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_red = 0;
+  const int64_t per = (n_cells + 1023) / 1024, c0 = (int64_t)tid * per;
+  uint32_t local = 0, local_t = 0;
+  for (int64_t c = c0; c < c0 + per && c < n_cells; ++c) {
+    const int64_t rows = offsets[c + 1] - offsets[c];
+    local += (uint32_t)((rows + GF_BWD_CHUNK - 1) / GF_BWD_CHUNK);
+    local_t += (uint32_t)((rows + 31) / 32);
+  }
+  uint32_t base = block_excl_scan_1024(local, wsum);
+  uint32_t tbase = chunk_tile ? block_excl_scan_1024(local_t, wsum) : 0u;
   for (int64_t c = c0; c < c0 + per && c < n_cells; ++c) {
     chunk_off[c] = base;
-    const uint32_t nch = (uint32_t)((offsets[c + 1] - offsets[c] + GF_BWD_CHUNK - 1) / GF_BWD_CHUNK);
-    for (uint32_t j = 0; j < nch; ++j) chunks[base + j] = make_uint2((uint32_t)c, j);
+    const int64_t rows = offsets[c + 1] - offsets[c];
+    const uint32_t nch = (uint32_t)((rows + GF_BWD_CHUNK - 1) / GF_BWD_CHUNK);
+    // reduce work: cells without rows (zeros) or with 2..8 chunks as one
+    // item; a cell with more chunks as one item per 256-parameter block
+    if (nch == 0 || (nch > 1 && nch <= 8)) {
+      red_cells[atomicAdd(&s_red, 1u)] = make_uint4((uint32_t)c, base, base + nch, 0xFFFFFFFFu);
+    } else if (nch > 8) {
+      const uint32_t nb = (uint32_t)red_blocks, at = atomicAdd(&s_red, nb);
+      for (uint32_t j = 0; j < nb; ++j) red_cells[at + j] = make_uint4((uint32_t)c, base, base + nch, j);
+    }
+    for (uint32_t j = 0; j < nch; ++j) {
+      chunks[base + j] = make_uint2((uint32_t)c, j);
+      if (chunk_tile) chunk_tile[base + j] = tbase + j * (GF_BWD_CHUNK / 32);
+    }
     base += nch;
+    tbase += (uint32_t)((rows + 31) / 32);
   }
   if (tid == 1023) {
     chunk_off[n_cells] = base;
     *n_chunks = base;
   }
+  __syncthreads();
+  if (tid == 0) *n_red = s_red;
 }
 
-// chunk sums -> reference-layout gradients; cells without rows get zeros
+// chunk sums -> reference-layout gradients for the items k_bwd_plan listed
+// (cell, first chunk, end chunk, parameter block or ALL): cells without rows
+// (zeros) or with several chunks (added in chunk order); single-chunk cells
+// were written in place.  One CTA per item (grid-stride); a crowded cell's
+// parameters are split over 256-parameter items so its long chunk sums run
+// on many SMs.
+template <class S>
+__device__ __forceinline__ void bwd_reduce_one(const float* __restrict__ scratch, const BwdArgs& A, size_t cell,
+                                               uint32_t k0, uint32_t k1, int p) {
+  float acc = 0.f;
+  if (k1 > k0) {
+    acc = scratch[(size_t)k0 * S::TOTAL + p];
+#pragma unroll 8
+    for (uint32_t k = k0 + 1; k < k1; ++k) acc = __fadd_rn(acc, scratch[(size_t)k * S::TOTAL + p]);
+  }
+  int l = 0, q = p;
+#pragma unroll
+  for (int j = 0; j < S::N_LAYERS - 1; ++j)
+    if (l == j && q >= S::count(j)) {
+      q -= S::count(j);
+      l = j + 1;
+    }
+  const int in = S::in_dim(l), out = S::out_dim(l);
+  if (q < out * in) A.gw[l][cell * (out * in) + q] = acc;
+  else A.gb[l][cell * out + (q - out * in)] = acc;
+}
+
 template <int W>
 __global__ void __launch_bounds__(256) k_bwd_reduce(const float* __restrict__ scratch,
-                                                    const uint32_t* __restrict__ chunk_off, int64_t n_cells,
-                                                    BwdArgs A) {
+                                                    const uint4* __restrict__ red_cells,
+                                                    const uint32_t* __restrict__ n_red, BwdArgs A) {
   using S = BwdShape<W>;
-  const int64_t n = n_cells * S::TOTAL;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t cell = e / S::TOTAL;
-    const int p = (int)(e % S::TOTAL);
-    float acc = 0.f;
-    const uint32_t k0 = chunk_off[cell], k1 = chunk_off[cell + 1];
-    for (uint32_t k = k0; k < k1; ++k) acc = k == k0 ? scratch[(size_t)k * S::TOTAL + p]
-                                                    : __fadd_rn(acc, scratch[(size_t)k * S::TOTAL + p]);
-    int l = 0, qq = p;
-    while (qq >= S::count(l)) qq -= S::count(l++);
-    const int in = S::in_dim(l), out = S::out_dim(l);
-    if (qq >= out * in) A.gb[l][cell * out + (qq - out * in)] = acc;
-    else A.gw[l][(cell * out + qq / in) * in + qq % in] = acc;
+  const uint32_t nr = *n_red;
+  for (uint32_t ri = blockIdx.x; ri < nr; ri += gridDim.x) {
+    const uint4 e = red_cells[ri];
+    if (e.w != 0xFFFFFFFFu) {
+      const int p = (int)e.w * 256 + threadIdx.x;
+      if (p < S::TOTAL) bwd_reduce_one<S>(scratch, A, e.x, e.y, e.z, p);
+      continue;
+    }
+    // whole cell, layer by layer (compile-time shapes, no per-parameter lookup)
+    int base = 0;
+#pragma unroll
+    for (int l = 0; l < S::N_LAYERS; ++l) {
+      const int in = S::in_dim(l), out = S::out_dim(l), cnt = S::count(l);
+      float* gw = A.gw[l] + (size_t)e.x * (out * in);
+      float* gb = A.gb[l] + (size_t)e.x * out;
+      for (int q = threadIdx.x; q < cnt; q += 256) {
+        float acc = 0.f;
+        if (e.z > e.y) {
+          acc = scratch[(size_t)e.y * S::TOTAL + base + q];
+          for (uint32_t k = e.y + 1; k < e.z; ++k) acc = __fadd_rn(acc, scratch[(size_t)k * S::TOTAL + base + q]);
+        }
+        if (q < out * in) gw[q] = acc;
+        else gb[q - out * in] = acc;
+      }
+      base += cnt;
+    }
   }
 }
 
@@ -245,7 +321,8 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const float* __restrict__ sc
 // 8 shared loads per 16 FMAs instead of 2 per FMA, and no per-parameter index
 // arithmetic; the per-parameter arithmetic sequence is unchanged.
 template <class S, int OUT, int IN, int DZ, int INO, int NT>
-__device__ __forceinline__ void bwd_layer_sums(const float* srow, int n_in, float* part, bool first, int tid, int& u) {
+__device__ __forceinline__ void bwd_layer_sums(const float* srow, int n_in, float* pw, float* pb, bool first, int tid,
+                                               int& u) {
   constexpr int LD = S::LD, OB = (OUT + 3) / 4, IB = (IN + 3) / 4, NB = OB * IB;
   // units: NB weight blocks, then OB bias quads; unit u of the whole tile is
   // handled by thread u % NT (u runs over every layer's units in order)
@@ -266,7 +343,7 @@ __device__ __forceinline__ void bwd_layer_sums(const float* srow, int n_in, floa
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          old[a][c] = (!first && o0 + a < OUT && i0 + c < IN) ? part[(o0 + a) * IN + i0 + c] : 0.f;
+          old[a][c] = (!first && o0 + a < OUT && i0 + c < IN) ? pw[(o0 + a) * IN + i0 + c] : 0.f;
       for (int rr = 0; rr < n_in; ++rr) {
         float dz[4], in[4];
 #pragma unroll
@@ -282,47 +359,303 @@ __device__ __forceinline__ void bwd_layer_sums(const float* srow, int n_in, floa
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          if (o0 + a < OUT && i0 + c < IN) part[(o0 + a) * IN + i0 + c] = first ? acc[a][c] : __fadd_rn(old[a][c], acc[a][c]);
+          if (o0 + a < OUT && i0 + c < IN) pw[(o0 + a) * IN + i0 + c] = first ? acc[a][c] : __fadd_rn(old[a][c], acc[a][c]);
     } else {
       const int o0 = (b - NB) * 4;
       float acc[4] = {0.f, 0.f, 0.f, 0.f}, old[4];
       const float* dzp = srow + DZ + o0;
 #pragma unroll
-      for (int a = 0; a < 4; ++a) old[a] = (!first && o0 + a < OUT) ? part[OUT * IN + o0 + a] : 0.f;
+      for (int a = 0; a < 4; ++a) old[a] = (!first && o0 + a < OUT) ? pb[o0 + a] : 0.f;
       for (int rr = 0; rr < n_in; ++rr)
 #pragma unroll
         for (int a = 0; a < 4; ++a)
           if (o0 + a < OUT) acc[a] = __fadd_rn(acc[a], dzp[rr * LD + a]);
 #pragma unroll
       for (int a = 0; a < 4; ++a)
-        if (o0 + a < OUT) part[OUT * IN + o0 + a] = first ? acc[a] : __fadd_rn(old[a], acc[a]);
+        if (o0 + a < OUT) pb[o0 + a] = first ? acc[a] : __fadd_rn(old[a], acc[a]);
     }
   }
   u += NB + OB;
 }
 
-template <class S, int NT>
-__device__ __forceinline__ void bwd_param_sums(const float* srow, int n_in, float* part, bool first, int tid) {
-  int u = 0;  // running unit count: spreads the layers' remainders over different threads
-  bwd_layer_sums<S, S::out_dim(0), S::in_dim(0), S::dz_off(0), S::in_off(0), NT>(srow, n_in, part, first, tid, u);
-  part += S::count(0);
-  bwd_layer_sums<S, S::out_dim(1), S::in_dim(1), S::dz_off(1), S::in_off(1), NT>(srow, n_in, part, first, tid, u);
-  part += S::count(1);
-  bwd_layer_sums<S, S::out_dim(2), S::in_dim(2), S::dz_off(2), S::in_off(2), NT>(srow, n_in, part, first, tid, u);
-  part += S::count(2);
-  bwd_layer_sums<S, S::out_dim(3), S::in_dim(3), S::dz_off(3), S::in_off(3), NT>(srow, n_in, part, first, tid, u);
-  part += S::count(3);
-  bwd_layer_sums<S, S::out_dim(4), S::in_dim(4), S::dz_off(4), S::in_off(4), NT>(srow, n_in, part, first, tid, u);
-  part += S::count(4);
-  bwd_layer_sums<S, S::out_dim(5), S::in_dim(5), S::dz_off(5), S::in_off(5), NT>(srow, n_in, part, first, tid, u);
+// where a chunk's parameter sums go: its scratch row (several chunks per
+// cell, added by k_bwd_reduce in chunk order) or, for a cell with a single
+// chunk, straight into the reference-layout gradients
+struct GradDst {
+  float* part;         // scratch row of the chunk, or NULL: direct
+  const BwdArgs* A;
+  int64_t cell;
+  template <class S>
+  __device__ __forceinline__ float* w(int l) const {
+    if (part) {
+      int off = 0;
+      for (int k = 0; k < l; ++k) off += S::count(k);
+      return part + off;
+    }
+    return A->gw[l] + cell * (S::out_dim(l) * S::in_dim(l));
+  }
+  template <class S>
+  __device__ __forceinline__ float* b(int l) const {
+    return part ? w<S>(l) + S::out_dim(l) * S::in_dim(l) : A->gb[l] + cell * S::out_dim(l);
+  }
+};
+
+template <class S, int NT, int L>
+__device__ __forceinline__ void bwd_sums_l(const float* srow, int n_in, const GradDst& g, bool first, int tid, int& u) {
+  bwd_layer_sums<S, S::out_dim(L), S::in_dim(L), S::dz_off(L), S::in_off(L), NT>(srow, n_in, g.w<S>(L), g.b<S>(L),
+                                                                                first, tid, u);
 }
 
-template <int W>
+template <class S, int NT>
+__device__ __forceinline__ void bwd_param_sums(const float* srow, int n_in, const GradDst& g, bool first, int tid) {
+  int u = 0;  // running unit count: spreads the layers' remainders over different threads
+  bwd_sums_l<S, NT, 0>(srow, n_in, g, first, tid, u);
+  bwd_sums_l<S, NT, 1>(srow, n_in, g, first, tid, u);
+  bwd_sums_l<S, NT, 2>(srow, n_in, g, first, tid, u);
+  bwd_sums_l<S, NT, 3>(srow, n_in, g, first, tid, u);
+  bwd_sums_l<S, NT, 4>(srow, n_in, g, first, tid, u);
+  bwd_sums_l<S, NT, 5>(srow, n_in, g, first, tid, u);
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core weight gradients (W = 32).  Phase A of k_grouped_backward
+// writes every 32-row tile as bf16 operand pieces (x = hi + mid + lo, each
+// the bf16 rounding of what the previous pieces leave: 24 significant bits,
+// float32's precision) in the canonical K-major layout, K = the tile's rows,
+// one 16-row sub-tile after the other:
+//   A (M = 128): the stacked deltas  [dz0 | dz1 | dz_feature | dz_direction]
+//   B (N = 192): the stacked inputs  [gamma(x) 63 | 1 | h0 | h1 | [feat, gamma(d)] 59 | 0 x5]
+// k_bwd_tc accumulates D = A B^T over a chunk's tiles in TMEM, six MMAs per
+// K step (the piece products down to 2^-16: lo.hi, hi.lo, mid.mid, mid.hi,
+// hi.mid, hi.hi; the dropped ones are <= 2^-24 relative), so D[o][i] of the
+// four diagonal blocks is gw = sum_rows dz[o] in[i] and column 63 (the ones
+// row) is gb = sum_rows dz[o].  A tile with at most 16 rows has no second
+// sub-tile (not written, not loaded).  The density and colour layers (33 + 99
+// parameters) stay on the CUDA cores in phase B.
+// ---------------------------------------------------------------------------
+#ifndef GF_BWD_TC_PIECES
+#define GF_BWD_TC_PIECES 3
+#endif
+#define GF_BWD_TC_A 4096                                         // one piece of A: 128 x 16 bf16
+#define GF_BWD_TC_B 6144                                         // one piece of B: 192 x 16 bf16
+#define GF_BWD_TC_SUB (GF_BWD_TC_PIECES * (GF_BWD_TC_A + GF_BWD_TC_B))  // one 16-row sub-tile
+#define GF_BWD_TC_TILE (2 * GF_BWD_TC_SUB)
+
+// bf16 pieces of two values (rows k, k+1: low half = even row)
+__device__ __forceinline__ void bf16_pieces2(float a, float b, uint32_t (&out)[GF_BWD_TC_PIECES]) {
+#pragma unroll
+  for (int p = 0; p < GF_BWD_TC_PIECES; ++p) {
+    const __nv_bfloat16 ha = __float2bfloat16_rn(a), hb = __float2bfloat16_rn(b);
+    out[p] = (uint32_t)__bfloat16_as_ushort(ha) | ((uint32_t)__bfloat16_as_ushort(hb) << 16);
+    a = __fsub_rn(a, __bfloat162float(ha));  // exact (Sterbenz / bf16 grid)
+    b = __fsub_rn(b, __bfloat162float(hb));
+  }
+}
+
+// one tile's operands: 16-byte units (8 consecutive rows of one feature),
+// numbered so that consecutive threads store consecutive 16 bytes
+template <class S>
+__device__ __forceinline__ void bwd_tc_operands(const float* srow, int n_in, uint8_t* tile, int tid) {
+  constexpr int LD = S::LD, W = 32, UNITS = 256 + 384;  // per 16-row sub-tile
+  const int n_units = n_in > 16 ? 2 * UNITS : UNITS;
+  for (int uu = tid; uu < n_units; uu += S::THREADS) {
+    const int ks = uu >= UNITS, u = uu - ks * UNITS;
+    const bool is_a = u < 256;
+    const int v = is_a ? u : u - 256;
+    const int f = ((v >> 4) << 3) | (v & 7), kg = (v >> 3) & 1;  // feature (M or N index), 8-row group
+    int off = -1;  // srow offset; -1: zero; -2: the ones row
+    if (is_a) {
+      const int blk = f >> 5;
+      off = (blk == 0 ? S::DZ0 : blk == 1 ? S::DZ1 : blk == 2 ? S::DZF : S::DZD) + (f & 31);
+    } else if (f < 63) {
+      off = S::X + f;
+    } else if (f == 63) {
+      off = -2;
+    } else if (f < 64 + W) {
+      off = S::H0 + f - 64;
+    } else if (f < 64 + 2 * W) {
+      off = S::H1 + f - 96;
+    } else if (f < 128 + W + S::D) {
+      off = S::CAT + f - 128;
+    }
+    uint32_t w[4][GF_BWD_TC_PIECES];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r0 = ks * 16 + kg * 8 + 2 * p, r1 = r0 + 1;
+      const float x0 = r0 < n_in ? (off >= 0 ? srow[r0 * LD + off] : (off == -2 ? 1.f : 0.f)) : 0.f;
+      const float x1 = r1 < n_in ? (off >= 0 ? srow[r1 * LD + off] : (off == -2 ? 1.f : 0.f)) : 0.f;
+      bf16_pieces2(x0, x1, w[p]);
+    }
+    uint8_t* d = tile + ks * GF_BWD_TC_SUB + (is_a ? 0 : GF_BWD_TC_PIECES * GF_BWD_TC_A) + v * 16;
+#pragma unroll
+    for (int p = 0; p < GF_BWD_TC_PIECES; ++p)
+      *reinterpret_cast<uint4*>(d + p * (is_a ? GF_BWD_TC_A : GF_BWD_TC_B)) = make_uint4(w[0][p], w[1][p], w[2][p], w[3][p]);
+  }
+}
+
+// phase B of the two narrow layers (density, colour) when the wide ones go to
+// the tensor cores
+template <class S, int NT>
+__device__ __forceinline__ void bwd_narrow_sums(const float* srow, int n_in, const GradDst& g, bool first, int tid) {
+  int u = 0;
+  bwd_sums_l<S, NT, 2>(srow, n_in, g, first, tid, u);
+  bwd_sums_l<S, NT, 5>(srow, n_in, g, first, tid, u);
+}
+
+// k_bwd_tc: persistent, one CTA per SM.  Warp 4 streams the chunk's operand
+// tiles into a 4-stage shared-memory ring (one bulk copy per tile), warp 5
+// issues the MMAs into one of two TMEM accumulators (192 columns each), and
+// warps 0-3 drain the other accumulator: warp w owns TMEM lanes 32w..32w+31 =
+// the outputs of one layer (trunk0, trunk1, feature, direction), staged in
+// shared memory and written to the chunk's partial sums in reference order.
+namespace bwdtc {
+constexpr int NST = GF_BWD_TC_PIECES == 3 ? 3 : 4, THREADS = 192, N = 192, ACC_COLS = 256, EPI_LD = 65;
+constexpr int EPI = NST * GF_BWD_TC_TILE;
+constexpr int BAR = EPI + 128 * EPI_LD * 4;  // full[NST], empty[NST], tfull[2], tempty[2], tmem slot
+constexpr int SMEM = BAR + 8 * (2 * NST + 4) + 16;
+static_assert(SMEM <= 227 * 1024, "k_bwd_tc shared memory");
+}  // namespace bwdtc
+
+__global__ void __launch_bounds__(bwdtc::THREADS, 1)
+    k_bwd_tc(const uint8_t* __restrict__ opbuf, const uint2* __restrict__ chunks,
+             const uint32_t* __restrict__ chunk_tile, const uint32_t* __restrict__ n_chunks,
+             const int64_t* __restrict__ offsets, const uint32_t* __restrict__ chunk_off, float* scratch,
+             BwdArgs A) {
+  using namespace tcx;
+  using S = BwdShape<32>;
+  using namespace bwdtc;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t full = sb + BAR, empty = full + 8 * NST, tfull = empty + 8 * NST, tempty = tfull + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + BAR + 8 * (2 * NST + 4));
+  float* epi = reinterpret_cast<float*>(smem + EPI);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2u * ACC_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      mbar_init(full + 8 * i, 1);
+      mbar_init(empty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(tfull + 8 * i, 1);
+      mbar_init(tempty + 8 * i, 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t nch = *n_chunks;
+  auto chunk_rows = [&](uint32_t ci) -> uint32_t {
+    const uint2 ch = chunks[ci];
+    return (uint32_t)min(offsets[ch.x + 1] - offsets[ch.x] - (int64_t)ch.y * GF_BWD_CHUNK, (int64_t)GF_BWD_CHUNK);
+  };
+  if (warp == 4) {  // ---- producer
+    if (lane == 0) {
+      uint32_t g = 0;
+      for (uint32_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
+        const uint32_t rows = chunk_rows(ci), nt = (rows + 31) / 32, t0 = chunk_tile[ci];
+        for (uint32_t t = 0; t < nt; ++t, ++g) {
+          const uint32_t s = g % NST, ph = (g / NST) & 1u;
+          const uint32_t bytes = rows - 32 * t > 16 ? GF_BWD_TC_TILE : GF_BWD_TC_SUB;
+          mbar_wait(empty + 8 * s, ph ^ 1u);
+          bulk_load(sb + s * GF_BWD_TC_TILE, opbuf + (size_t)(t0 + t) * GF_BWD_TC_TILE, bytes, full + 8 * s);
+        }
+      }
+    }
+  } else if (warp == 5) {  // ---- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, N);
+      uint32_t g = 0, it = 0;
+      for (uint32_t ci = blockIdx.x; ci < nch; ci += gridDim.x, ++it) {
+        const uint32_t acc = it & 1u, aph = (it >> 1) & 1u, rows = chunk_rows(ci), nt = (rows + 31) / 32;
+        mbar_wait(tempty + 8 * acc, aph ^ 1u);
+        fence_after();
+        const uint32_t d = tmem + acc * ACC_COLS;
+        for (uint32_t t = 0; t < nt; ++t, ++g) {
+          const uint32_t s = g % NST, ph = (g / NST) & 1u, nks = rows - 32 * t > 16 ? 2u : 1u;
+          mbar_wait(full + 8 * s, ph);
+          fence_after();
+          for (uint32_t ks = 0; ks < nks; ++ks) {
+            const uint32_t base = sb + s * GF_BWD_TC_TILE + ks * GF_BWD_TC_SUB;
+            uint64_t a[GF_BWD_TC_PIECES], b[GF_BWD_TC_PIECES];
+#pragma unroll
+            for (int p = 0; p < GF_BWD_TC_PIECES; ++p) {
+              a[p] = desc_kmajor(base + p * GF_BWD_TC_A, 16);
+              b[p] = desc_kmajor(base + GF_BWD_TC_PIECES * GF_BWD_TC_A + p * GF_BWD_TC_B, 16);
+            }
+            uint32_t accf = (t | ks) ? 1u : 0u;
+#if GF_BWD_TC_PIECES == 3
+            mma_ss(d, a[2], b[0], idesc, accf);  // small terms first
+            mma_ss(d, a[0], b[2], idesc, 1u);
+            mma_ss(d, a[1], b[1], idesc, 1u);
+            accf = 1u;
+#endif
+            mma_ss(d, a[1], b[0], idesc, accf);
+            mma_ss(d, a[0], b[1], idesc, 1u);
+            mma_ss(d, a[0], b[0], idesc, 1u);
+          }
+          mma_commit(empty + 8 * s);  // the stage is free once these MMAs have read it
+        }
+        mma_commit(tfull + 8 * acc);
+      }
+    }
+  } else {  // ---- epilogue: warp w = layer (trunk0, trunk1, feature, direction)
+    const int layer = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 3 : 4;
+    const int in = S::in_dim(layer);
+    const int col0 = warp == 0 ? 0 : warp == 1 ? 64 : warp == 2 ? 96 : 128;
+    int base = 0;
+    for (int l = 0; l < layer; ++l) base += S::count(l);
+    float* er = epi + tid * EPI_LD;
+    uint32_t it = 0;
+    for (uint32_t ci = blockIdx.x; ci < nch; ci += gridDim.x, ++it) {
+      const uint32_t acc = it & 1u, aph = (it >> 1) & 1u;
+      mbar_wait(tfull + 8 * acc, aph);
+      fence_after();
+      const uint32_t ta = tmem + acc * ACC_COLS + ((uint32_t)(warp * 32) << 16);
+      for (int c = 0; c < in; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(ta + col0 + c, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          if (c + q < in) er[c + q] = __uint_as_float(r[q]);
+      }
+      const uint32_t b = tmem_ld1(ta + 63);
+      tmem_wait_ld();
+      er[64] = __uint_as_float(b);
+      fence_before();
+      mbar_arrive(tempty + 8 * acc);  // the accumulator may take the next chunk
+      __syncwarp();
+      const uint32_t cell = chunks[ci].x;
+      const bool direct = chunk_off[cell + 1] - chunk_off[cell] == 1;
+      float* dw = direct ? A.gw[layer] + (size_t)cell * (32 * in) : scratch + (size_t)ci * S::TOTAL + base;
+      float* db = direct ? A.gb[layer] + (size_t)cell * 32 : dw + 32 * in;
+      const float* ew = epi + warp * 32 * EPI_LD;
+      for (int e = lane; e < 32 * in; e += 32) dw[e] = ew[(e / in) * EPI_LD + e % in];
+      db[lane] = ew[lane * EPI_LD + 64];
+      __syncwarp();
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * ACC_COLS));
+}
+
+template <int W, bool TCB>
 __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const float* __restrict__ packed,
                                                                            Fp32Layout L, BwdArgs A,
                                                                            const uint2* __restrict__ chunks,
                                                                            const uint32_t* __restrict__ n_chunks,
-                                                                           float* scratch) {
+                                                                           const uint32_t* __restrict__ chunk_off,
+                                                                           float* scratch, uint8_t* opbuf,
+                                                                           const uint32_t* __restrict__ chunk_tile) {
   using S = BwdShape<W>;
   constexpr int P = S::P, D = S::D, TR = S::TR, LD = S::LD, NT = S::THREADS, Q = W / S::LANES;
   constexpr int PP = (P + 3) & ~3, WP = (W + 3) & ~3, DP = (W + D + 3) & ~3;
@@ -378,7 +711,10 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
   const int64_t r0 = A.offsets[cell] + (int64_t)ch.y * GF_BWD_CHUNK;
   const int64_t r1 = min(A.offsets[cell + 1], r0 + (int64_t)GF_BWD_CHUNK);
   const int n_tiles = (int)((r1 - r0 + TR - 1) / TR);  // >= 1: chunks hold rows
-  float* part = scratch + (size_t)blockIdx.x * S::TOTAL;
+  GradDst gd;
+  gd.part = chunk_off[cell + 1] - chunk_off[cell] > 1 ? scratch + (size_t)blockIdx.x * S::TOTAL : nullptr;
+  gd.A = &A;
+  gd.cell = cell;
   for (int t = 0; t < n_tiles; ++t) {
     const int64_t first = r0 + (int64_t)t * TR;
     const int n_in = (int)(r1 - first < (int64_t)TR ? r1 - first : (int64_t)TR);  // <= 0 for an empty cell
@@ -526,22 +862,48 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
     }
     __syncthreads();
     // ---------------- phase B: parameter sums over this tile's rows (gw = dz^T in, gb = sum dz)
-    bwd_param_sums<S, NT>(srow, n_in, part, t == 0, tid);
+    if constexpr (TCB) {
+      bwd_tc_operands<S>(srow, n_in, opbuf + ((size_t)chunk_tile[blockIdx.x] + t) * GF_BWD_TC_TILE, tid);
+      bwd_narrow_sums<S, NT>(srow, n_in, gd, t == 0, tid);
+    } else {
+      bwd_param_sums<S, NT>(srow, n_in, gd, t == 0, tid);
+    }
   }
 }
 
-int64_t bwd_max_chunks(int64_t n_cells, int64_t n);
+int64_t bwd_max_chunks(int64_t n_cells, int64_t n) { return n / GF_BWD_CHUNK + std::min<int64_t>(n_cells, n) + 1; }
+// reduce items: one per cell, plus (blocks - 1) per cell with more than 8 chunks
+static size_t bwd_red_items(int64_t n_cells, int64_t n, int total) {
+  return (size_t)n_cells + (size_t)(n / (8 * GF_BWD_CHUNK) + 1) * (size_t)((total + 255) / 256);
+}
+static int64_t bwd_max_tiles(int64_t n_cells, int64_t n) { return n / 32 + std::min<int64_t>(n_cells, n) + 1; }
+
+// GF_BWD_TC=0: the wide layers' weight gradients on the CUDA cores too
+static bool bwd_tc_enabled(int width) {
+  static const bool on = [] {
+    const char* e = std::getenv("GF_BWD_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on && width == 32;
+}
 
 template <int W>
 static bool launch_bwd_width(const float* packed, const Fp32Layout& L, const BwdArgs& A, int64_t n_cells, int64_t n,
                              void* ws, cudaStream_t st) {
   using S = BwdShape<W>;
+  constexpr bool TC_OK = W == 32;
+  const bool tc = TC_OK && bwd_tc_enabled(W);
   const size_t smem =
       (S::WT ? (size_t)(S::WT_FLOATS + S::SM_FLOATS) * 4 : (size_t)L.cell_floats * 4) + (size_t)S::TR * S::LD * 4;
   static thread_local size_t set = 0;
   if (set < smem) {
-    if (cudaFuncSetAttribute(k_grouped_backward<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(k_grouped_backward<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
+      return false;
+    if (TC_OK && (cudaFuncSetAttribute(k_grouped_backward<W, TC_OK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem) != cudaSuccess ||
+                  cudaFuncSetAttribute(k_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, bwdtc::SMEM) !=
+                      cudaSuccess))
       return false;
     set = smem;
   }
@@ -555,23 +917,41 @@ static bool launch_bwd_width(const float* packed, const Fp32Layout& L, const Bwd
   uint32_t* n_chunks = (uint32_t*)p;
   p += gf_align(4);
   float* scratch = (float*)p;
-  k_bwd_plan<<<1, 1024, 0, st>>>(A.offsets, n_cells, chunks, chunk_off, n_chunks);
-  if (max_chunks > 0)
-    k_grouped_backward<W><<<(unsigned)max_chunks, S::THREADS, smem, st>>>(packed, L, A, chunks, n_chunks, scratch);
-  const int64_t elems = n_cells * S::TOTAL;
-  k_bwd_reduce<W><<<(unsigned)std::min<int64_t>(gf_div_up<int64_t>(elems, 256), (int64_t)num_sms() * 16), 256, 0, st>>>(
-      scratch, chunk_off, n_cells, A);
+  p += gf_align((size_t)max_chunks * S::TOTAL * 4);
+  uint4* red_cells = (uint4*)p;
+  p += gf_align(bwd_red_items(n_cells, n, S::TOTAL) * 16);
+  uint32_t* n_red = (uint32_t*)p;
+  p += gf_align(4);
+  uint32_t* chunk_tile = tc ? (uint32_t*)p : nullptr;
+  p += gf_align((size_t)max_chunks * 4);
+  uint8_t* opbuf = (uint8_t*)p;
+  k_bwd_plan<<<1, 1024, 0, st>>>(A.offsets, n_cells, chunks, chunk_off, n_chunks, chunk_tile, red_cells, n_red,
+                                 (S::TOTAL + 255) / 256);
+  if (max_chunks > 0) {
+    if (tc) {
+      k_grouped_backward<W, TC_OK><<<(unsigned)max_chunks, S::THREADS, smem, st>>>(packed, L, A, chunks, n_chunks, chunk_off,
+                                                                                  scratch, opbuf, chunk_tile);
+      k_bwd_tc<<<(unsigned)std::min<int64_t>(max_chunks, (int64_t)num_sms()), bwdtc::THREADS, bwdtc::SMEM, st>>>(
+          opbuf, chunks, chunk_tile, n_chunks, A.offsets, chunk_off, scratch, A);
+    } else {
+      k_grouped_backward<W, false><<<(unsigned)max_chunks, S::THREADS, smem, st>>>(packed, L, A, chunks, n_chunks, chunk_off,
+                                                                                 scratch, nullptr, nullptr);
+    }
+  }
+  k_bwd_reduce<W><<<(unsigned)std::min<int64_t>(n_cells, (int64_t)num_sms() * 8), 256, 0, st>>>(scratch, red_cells,
+                                                                                                 n_red, A);
   return true;
 }
-
-int64_t bwd_max_chunks(int64_t n_cells, int64_t n) { return n / GF_BWD_CHUNK + std::min<int64_t>(n_cells, n) + 1; }
 
 size_t bwd_workspace(const LayerTable& t, int64_t n_cells, int64_t n) {
   if (!prepare_mlp_fp32(t)) return 0;
   const int total = t.width == 32 ? BwdShape<32>::TOTAL : BwdShape<64>::TOTAL;
   const int64_t mc = bwd_max_chunks(n_cells, n);
-  return gf_align((size_t)mc * 8) + gf_align((size_t)(n_cells + 1) * 4) + gf_align(4) +
-         gf_align((size_t)mc * total * 4);
+  size_t bytes = gf_align((size_t)mc * 8) + gf_align((size_t)(n_cells + 1) * 4) + gf_align(4) +
+                 gf_align((size_t)mc * total * 4) + gf_align(bwd_red_items(n_cells, n, total) * 16) + gf_align(4);
+  if (bwd_tc_enabled(t.width))
+    bytes += gf_align((size_t)mc * 4) + (size_t)bwd_max_tiles(n_cells, n) * GF_BWD_TC_TILE;
+  return bytes;
 }
 
 bool launch_grouped_backward(const LayerTable& t, const float* packed, const BwdArgs& A, int64_t n_cells, int64_t n,

@@ -240,3 +240,51 @@ def test_photometric_step_matches_reference():
         assert np.abs(g.params.weights[name] - z[f"step_p_w_{name}"]).max() <= 5e-6, name
         assert np.abs(g.params.biases[name] - z[f"step_p_b_{name}"]).max() <= 5e-6, name
     assert train.mean_free_space_density(g, np.arange(0, 8, 3)) == pytest.approx(float(z["free_space"]), rel=1e-5)
+
+
+@pytest.mark.parametrize("width", [32, 64])
+def test_grouped_backward_chunking_edge_cases(width):
+    """Cells with no rows (zero gradients); a crowded cell of 2316 rows = ten
+    256-row chunks whose last tile holds 12 rows (more than 8 chunks: its
+    chunk sums are split over parameter blocks; on the tensor-core path a
+    tile of <= 16 rows has no second K sub-tile); a cell of 600 rows = three
+    chunks; single-chunk cells of 1..40 rows (written in place); against the
+    training oracle (batched.py:154-187, mlp.py:269-316)."""
+    from oracle import gridfield_oracle as O
+    from oracle import train_oracle as T
+
+    gf = _gf()
+    rng = np.random.default_rng(7)
+    res = (4, 4, 4)
+    aabb = gf.Aabb((0.0,) * 3, (1.0,) * 3)
+    arch = None if width == 32 else gf.MlpArchitecture(hidden_width=64)
+    g = gf.init_network_grid(aabb, res, seed=3, arch=arch)
+    for k in g.params.biases:
+        g.params.biases[k][...] = rng.normal(0.0, 0.3, g.params.biases[k].shape).astype(np.float32)
+    pts = [rng.uniform(0.0, 0.25, (2316, 3)), rng.uniform(0.75, 1.0, (600, 3))]  # cells 0 and 63
+    for c in range(1, 63, 3):  # every third cell; the rest stay empty
+        ix, iy, iz = c % 4, (c // 4) % 4, c // 16
+        n = 1 + (c * 7) % 40
+        pts.append((np.array([ix, iy, iz]) + rng.uniform(0.05, 0.95, (n, 3))) / 4.0)
+    pts = np.concatenate(pts).astype(np.float32)
+    perm = rng.permutation(len(pts))
+    pts = pts[perm]
+    dirs = rng.normal(size=pts.shape).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    dcol = rng.normal(0.0, 1e-2, (len(pts), 3)).astype(np.float32)
+    dsig = rng.normal(0.0, 1e-2, len(pts)).astype(np.float32)
+    layout = gf.group_by_network(gf.QueryBatch(pts, dirs, g.cell_index(pts)), g.n_cells)
+    caches = []
+    gf.grouped_forward(g, layout, caches=caches)
+    grads = gf.batched.grouped_backward(g, layout, caches, dcol, dsig)
+    lat = O.init_lattice(np.zeros(3), np.ones(3), res, seed=3, width=width)
+    for k in lat.weights:
+        lat.weights[k][...] = g.params.weights[k]
+        lat.biases[k][...] = g.params.biases[k]
+    _, _, gw, gb = T.grouped_forward_backward(lat, pts, dirs, dcol, dsig)
+    counts = np.bincount(g.cell_index(pts), minlength=g.n_cells)
+    assert counts[0] == 2316 and counts[63] == 600 and (counts == 0).sum() > 30
+    for name in LAYERS:
+        _close(grads.weights[name], gw[name], name)
+        _close(grads.biases[name], gb[name], name)
+        assert not np.asarray(grads.weights[name])[counts == 0].any(), name
