@@ -13,7 +13,7 @@ timeout 600 python bench.py --workload c4 --steps 5 --warmup 3 > gpurun_out/benc
 timeout 600 python bench.py --workload c5 --steps 5 --warmup 3 > gpurun_out/bench_c5.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --clock-preroll 0 > /dev/null 2>&1
-for k in k_mlp_tc:${MLP_SKIP:-8} k_march:${MARCH_SKIP:-9} k_place:${PLACE_SKIP:-8} k_ray_init:1 k_extract_analytic:1 k_grouped_backward:2 k_photo_ray:2; do
+for k in k_mlp_tc:${MLP_SKIP:-8} k_march:${MARCH_SKIP:-9} k_place:${PLACE_SKIP:-8} k_ray_init:1 k_extract_analytic:1 k_grouped_backward:2 k_bwd_tc:2 k_photo_ray:2; do
   name=${k%%:*}; skip=${k##*:}
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$name -s $skip -c 1 \
     -o gpurun_out/prof_${TAG}_$name -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --clock-preroll 0 > /dev/null 2>&1
