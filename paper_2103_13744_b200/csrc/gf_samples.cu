@@ -15,8 +15,12 @@
 // (gf_pcg_advance) and steps from there; the host advances the Generator by
 // the same number of draws afterwards.
 //
-// Output order is np.nonzero's (ray-major, slot ascending): a count pass,
-// a single-CTA exclusive scan, and a write pass that recomputes the samples.
+// One warp per ray: lane l takes the contiguous slot slice [l*S, (l+1)*S),
+// S = ceil(k / 32), jumping straight to the slice's first draw.  Output order
+// is np.nonzero's (ray-major, slot ascending): a count pass (lane counts summed
+// per ray), a single-CTA exclusive scan over rays, and a write pass that
+// recounts, places each lane's slice after the lower lanes' samples, and
+// recomputes the samples.
 #include "gf_common.cuh"
 #include "gf_samples.cuh"
 
@@ -99,18 +103,17 @@ struct DrawStream {
   }
 };
 
-// samples of ray i: count them, or write them from row `out0`
+// samples of ray i in slots [j0, j1): count them, or write them from row `out0`
 template <bool WRITE>
-__device__ __forceinline__ uint32_t ray_samples(const PrepArgs& A, int64_t i, int64_t out0) {
-  const RaySetup r = ray_setup(A, i);
-  if (WRITE) A.deltas[i] = r.seg;
+__device__ __forceinline__ uint32_t ray_samples(const PrepArgs& A, const RaySetup& r, int64_t i, int j0, int j1,
+                                                int64_t out0) {
+  if (!r.hit) return 0;  // a miss keeps nothing (its draws are accounted for by the host's Generator advance)
   DrawStream ds;
-  if (A.stratified) ds.init(A, (uint64_t)i * (uint64_t)A.k);
+  if (A.stratified && j0 < j1) ds.init(A, (uint64_t)i * (uint64_t)A.k + (uint64_t)j0);
   uint32_t c = 0;
-  for (int j = 0; j < A.k; ++j) {
+  for (int j = j0; j < j1; ++j) {
     float jit = 0.5f;
     if (A.stratified) jit = (float)(ds.next() >> 8) * (1.0f / 16777216.0f);
-    if (!r.hit) continue;
     const double t = __dadd_rn(r.t0_32, __dmul_rn(__dadd_rn((double)j, (double)jit), (double)r.seg));
     double p[3];
 #pragma unroll
@@ -142,8 +145,13 @@ __device__ __forceinline__ uint32_t ray_samples(const PrepArgs& A, int64_t i, in
 }
 
 __global__ void __launch_bounds__(128) k_prep_count(PrepArgs A) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < A.n) A.offsets[i] = ray_samples<false>(A, i, 0);
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= A.n) return;  // warp-uniform
+  const int S = (A.k + 31) / 32, j0 = min(A.k, lane * S), j1 = min(A.k, j0 + S);
+  const RaySetup r = ray_setup(A, i);
+  const uint32_t c = __reduce_add_sync(0xffffffffu, ray_samples<false>(A, r, i, j0, j1, 0));
+  if (lane == 0) A.offsets[i] = c;
 }
 
 // exclusive scan of the per-ray counts (one CTA, fixed order); offsets[n] = total
@@ -181,20 +189,33 @@ __global__ void __launch_bounds__(1024) k_prep_scan(PrepArgs A) {
 }
 
 __global__ void __launch_bounds__(128) k_prep_write(PrepArgs A) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < A.n) ray_samples<true>(A, i, A.offsets[i]);
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= A.n) return;  // warp-uniform
+  const int S = (A.k + 31) / 32, j0 = min(A.k, lane * S), j1 = min(A.k, j0 + S);
+  const RaySetup r = ray_setup(A, i);
+  if (lane == 0) A.deltas[i] = r.seg;
+  if (!r.hit) return;  // no samples (the draws only matter for the host-side Generator advance)
+  const uint32_t c = ray_samples<false>(A, r, i, j0, j1, 0);
+  uint32_t x = c;  // inclusive scan of the lane counts
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (c) ray_samples<true>(A, r, i, j0, j1, A.offsets[i] + (x - c));
 }
 
 void launch_prepare_count(const PrepArgs& A, cudaStream_t st) {
   if (A.n <= 0) return;
-  const unsigned g = (unsigned)gf_div_up<int64_t>(A.n, 128);
+  const unsigned g = (unsigned)gf_div_up<int64_t>(A.n * 32, 128);
   k_prep_count<<<g, 128, 0, st>>>(A);
   k_prep_scan<<<1, 1024, 0, st>>>(A);
 }
 
 void launch_prepare_write(const PrepArgs& A, cudaStream_t st) {
   if (A.n <= 0) return;
-  k_prep_write<<<(unsigned)gf_div_up<int64_t>(A.n, 128), 128, 0, st>>>(A);
+  k_prep_write<<<(unsigned)gf_div_up<int64_t>(A.n * 32, 128), 128, 0, st>>>(A);
 }
 
 }  // namespace gf

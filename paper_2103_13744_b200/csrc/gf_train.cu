@@ -988,56 +988,130 @@ __global__ void k_photo_scatter(PhotoArgs A, float4* dense, int32_t* qidx, uint8
 
 // one thread per ray: forward composite (cumprod transmittance, weights,
 // prediction + background), squared error in float64, then the backward
-// rest-of-ray recurrence from the last slot down (no division by 1 - alpha)
-__global__ void k_photo_ray(PhotoArgs A, const float4* __restrict__ dense, const int32_t* __restrict__ qidx,
-                            const uint8_t* __restrict__ nmask, float* tb, double* loss_parts) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= A.n_rays) return;
+// rest-of-ray recurrence from the last slot down (no division by 1 - alpha).
+// A warp owns 32 consecutive rays and stages PH_CS slots of all of them at a
+// time through shared memory: the dense rows, t_before and the query indices
+// move as whole 128-byte lines instead of one strided element per lane.
+#define PH_CS 8
+#define PH_WARPS 4
+__global__ void __launch_bounds__(32 * PH_WARPS) k_photo_ray(PhotoArgs A, const float4* __restrict__ dense,
+                                                             const int32_t* __restrict__ qidx,
+                                                             const uint8_t* __restrict__ nmask, float* tb,
+                                                             double* loss_parts) {
+  __shared__ float4 s_v[PH_WARPS][32][PH_CS + 1];
+  __shared__ float s_t[PH_WARPS][32][PH_CS + 1];
+  __shared__ int32_t s_q[PH_WARPS][32][PH_CS + 1];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int64_t b0 = ((int64_t)blockIdx.x * PH_WARPS + wp) * 32;
+  if (b0 >= A.n_rays) return;  // warp-uniform
+  const int64_t b = b0 + lane;
+  const bool on = b < A.n_rays;
+  const int nr = A.n_rays - b0 < 32 ? (int)(A.n_rays - b0) : 32;
   const int k = A.k;
-  const float4* dr = dense + b * k;
-  float* tbr = tb + b * k;
+  float4(*sv)[PH_CS + 1] = s_v[wp];
+  float(*st)[PH_CS + 1] = s_t[wp];
+  int32_t(*sq)[PH_CS + 1] = s_q[wp];
+  // slots [i0, i0 + PH_CS) of the warp's rays, ray-major (lanes read
+  // consecutive slots of a ray): element u of this lane is (e / PH_CS,
+  // e % PH_CS), e = lane + 32 u.  The next chunk is fetched into registers
+  // while the current one is composited (software pipelining).
+  float4 pv[PH_CS];
+  float pt[PH_CS];
+  int32_t pq[PH_CS];
+  auto fetch = [&](int i0, bool with_t) {
+#pragma unroll
+    for (int u = 0; u < PH_CS; ++u) {
+      const int e = lane + 32 * u, r = e / PH_CS, j = e % PH_CS;
+      if (i0 >= 0 && r < nr && i0 + j < k) {
+        const size_t g = (size_t)(b0 + r) * k + i0 + j;
+        pv[u] = dense[g];
+        if (with_t) {
+          pt[u] = tb[g];
+          pq[u] = qidx[g];
+        }
+      }
+    }
+  };
+  auto stage = [&](bool with_t) {
+#pragma unroll
+    for (int u = 0; u < PH_CS; ++u) {
+      const int e = lane + 32 * u, r = e / PH_CS, j = e % PH_CS;
+      sv[r][j] = pv[u];
+      if (with_t) {
+        st[r][j] = pt[u];
+        sq[r][j] = pq[u];
+      }
+    }
+    __syncwarp();
+  };
   float tr = 1.0f, p0 = 0.f, p1 = 0.f, p2 = 0.f;
-  for (int i = 0; i < k; ++i) {
-    const float4 v = dr[i];
-    tbr[i] = tr;                          // t_before
-    const float w = __fmul_rn(tr, v.w);   // weights = t_before * alpha
-    p0 = __fadd_rn(p0, __fmul_rn(w, v.x));
-    p1 = __fadd_rn(p1, __fmul_rn(w, v.y));
-    p2 = __fadd_rn(p2, __fmul_rn(w, v.z));
-    tr = __fmul_rn(tr, __fsub_rn(1.0f, v.w));  // cumprod(1 - alpha)
+  fetch(0, false);
+  for (int i0 = 0; i0 < k; i0 += PH_CS) {
+    stage(false);
+    fetch(i0 + PH_CS, false);
+    if (on) {
+      for (int j = 0; j < PH_CS && i0 + j < k; ++j) {
+        const float4 v = sv[lane][j];
+        st[lane][j] = tr;                     // t_before
+        const float w = __fmul_rn(tr, v.w);   // weights = t_before * alpha
+        p0 = __fadd_rn(p0, __fmul_rn(w, v.x));
+        p1 = __fadd_rn(p1, __fmul_rn(w, v.y));
+        p2 = __fadd_rn(p2, __fmul_rn(w, v.z));
+        tr = __fmul_rn(tr, __fsub_rn(1.0f, v.w));  // cumprod(1 - alpha)
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < PH_CS; ++u) {
+      const int e = lane + 32 * u, r = e / PH_CS, j = e % PH_CS;
+      if (r < nr && i0 + j < k) tb[(size_t)(b0 + r) * k + i0 + j] = st[r][j];
+    }
+    __syncwarp();
   }
-  const float r0 = __fsub_rn(__fadd_rn(p0, __fmul_rn(tr, A.bg[0])), A.gt[3 * b + 0]);
-  const float r1 = __fsub_rn(__fadd_rn(p1, __fmul_rn(tr, A.bg[1])), A.gt[3 * b + 1]);
-  const float r2 = __fsub_rn(__fadd_rn(p2, __fmul_rn(tr, A.bg[2])), A.gt[3 * b + 2]);
-  loss_parts[b] = __dadd_rn(__dadd_rn(__dmul_rn((double)r0, (double)r0), __dmul_rn((double)r1, (double)r1)),
-                            __dmul_rn((double)r2, (double)r2));
+  float r0 = 0.f, r1 = 0.f, r2 = 0.f;
+  if (on) {
+    r0 = __fsub_rn(__fadd_rn(p0, __fmul_rn(tr, A.bg[0])), A.gt[3 * b + 0]);
+    r1 = __fsub_rn(__fadd_rn(p1, __fmul_rn(tr, A.bg[1])), A.gt[3 * b + 1]);
+    r2 = __fsub_rn(__fadd_rn(p2, __fmul_rn(tr, A.bg[2])), A.gt[3 * b + 2]);
+    loss_parts[b] = __dadd_rn(__dadd_rn(__dmul_rn((double)r0, (double)r0), __dmul_rn((double)r1, (double)r1)),
+                              __dmul_rn((double)r2, (double)r2));
+  }
   if (!A.d_color_q) return;
   const float d0 = __fmul_rn(A.two_over_b, r0), d1 = __fmul_rn(A.two_over_b, r1), d2 = __fmul_rn(A.two_over_b, r2);
-  const float delta = A.deltas[b];
+  const float delta = on ? A.deltas[b] : 0.f;
   float re0 = A.bg[0], re1 = A.bg[1], re2 = A.bg[2];  // rest[:, k-1] = bg
-  for (int i = k - 1; i >= 0; --i) {
-    const float4 v = dr[i];
-    const int32_t q = qidx[b * k + i];
-    if (q >= 0) {
-      const float t = tbr[i];
-      // d_alpha = sum_c (dpred_c * t_before) * (color_c - rest_c)
-      const float e0 = __fmul_rn(__fmul_rn(d0, t), __fsub_rn(v.x, re0));
-      const float e1 = __fmul_rn(__fmul_rn(d1, t), __fsub_rn(v.y, re1));
-      const float e2 = __fmul_rn(__fmul_rn(d2, t), __fsub_rn(v.z, re2));
-      const float da = __fadd_rn(__fadd_rn(e0, e1), e2);
-      const float w = __fmul_rn(t, v.w);
-      A.d_color_q[3 * q + 0] = __fmul_rn(w, d0);
-      A.d_color_q[3 * q + 1] = __fmul_rn(w, d1);
-      A.d_color_q[3 * q + 2] = __fmul_rn(w, d2);
-      float ds = __fmul_rn(__fmul_rn(da, delta), __fsub_rn(1.0f, v.w));
-      if (A.noise && !nmask[q]) ds = __fmul_rn(ds, 0.f);  // d_sigma_q * noise_mask
-      A.d_sigma_q[q] = ds;
+  const int last = ((k - 1) / PH_CS) * PH_CS;
+  fetch(last, true);  // t_before of these slots was stored above (same lanes' earlier stores: program order)
+  for (int i0 = last; i0 >= 0; i0 -= PH_CS) {
+    stage(true);
+    fetch(i0 - PH_CS, true);
+    if (on) {
+      for (int j = min(PH_CS, k - i0) - 1; j >= 0; --j) {
+        const float4 v = sv[lane][j];
+        const int32_t q = sq[lane][j];
+        if (q >= 0) {
+          const float t = st[lane][j];
+          // d_alpha = sum_c (dpred_c * t_before) * (color_c - rest_c)
+          const float e0 = __fmul_rn(__fmul_rn(d0, t), __fsub_rn(v.x, re0));
+          const float e1 = __fmul_rn(__fmul_rn(d1, t), __fsub_rn(v.y, re1));
+          const float e2 = __fmul_rn(__fmul_rn(d2, t), __fsub_rn(v.z, re2));
+          const float da = __fadd_rn(__fadd_rn(e0, e1), e2);
+          const float w = __fmul_rn(t, v.w);
+          A.d_color_q[3 * q + 0] = __fmul_rn(w, d0);
+          A.d_color_q[3 * q + 1] = __fmul_rn(w, d1);
+          A.d_color_q[3 * q + 2] = __fmul_rn(w, d2);
+          float ds = __fmul_rn(__fmul_rn(da, delta), __fsub_rn(1.0f, v.w));
+          if (A.noise && !nmask[q]) ds = __fmul_rn(ds, 0.f);  // d_sigma_q * noise_mask
+          A.d_sigma_q[q] = ds;
+        }
+        // rest[:, i-1] = alpha_i * color_i + (1 - alpha_i) * rest[:, i]
+        const float om = __fsub_rn(1.0f, v.w);
+        re0 = __fadd_rn(__fmul_rn(v.w, v.x), __fmul_rn(om, re0));
+        re1 = __fadd_rn(__fmul_rn(v.w, v.y), __fmul_rn(om, re1));
+        re2 = __fadd_rn(__fmul_rn(v.w, v.z), __fmul_rn(om, re2));
+      }
     }
-    // rest[:, i-1] = alpha_i * color_i + (1 - alpha_i) * rest[:, i]
-    const float om = __fsub_rn(1.0f, v.w);
-    re0 = __fadd_rn(__fmul_rn(v.w, v.x), __fmul_rn(om, re0));
-    re1 = __fadd_rn(__fmul_rn(v.w, v.y), __fmul_rn(om, re1));
-    re2 = __fadd_rn(__fmul_rn(v.w, v.z), __fmul_rn(om, re2));
+    __syncwarp();
   }
 }
 
@@ -1079,8 +1153,9 @@ void launch_photometric(const PhotoArgs& A, void* ws, double* loss_sum, cudaStre
     const unsigned g = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(A.n_queries, 256), (int64_t)num_sms() * 8);
     k_photo_scatter<<<g, 256, 0, st>>>(A, dense, qidx, nmask);
   }
-  if (A.n_rays > 0) k_photo_ray<<<(unsigned)gf_div_up<int64_t>(A.n_rays, 128), 128, 0, st>>>(A, dense, qidx, nmask, tb,
-                                                                                            parts);
+  if (A.n_rays > 0)
+    k_photo_ray<<<(unsigned)gf_div_up<int64_t>(A.n_rays, 32 * PH_WARPS), 32 * PH_WARPS, 0, st>>>(A, dense, qidx, nmask,
+                                                                                               tb, parts);
   k_sum_f64<<<1, 1024, 0, st>>>(parts, A.n_rays, loss_sum);
 }
 

@@ -5,7 +5,7 @@ timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 300 -
 timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_train.log 2>&1
 python -c "
 import json; d=json.loads(open('gpurun_out/bench_train.log').read().strip().splitlines()[-1]); t=d.get('training_step'); print({k:v for k,v in (t or {}).items() if k!='note'}); print('frame', d['ms_per_step'])" || tail -5 gpurun_out/bench_train.log
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -k regex:"k_grouped_backward|k_bwd|k_group_|k_adam|k_photo" \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -k regex:"k_grouped_backward|k_bwd|k_group_|k_adam|k_photo|k_prep" \
   --log-file gpurun_out/bwd_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --clock-preroll 0 > /dev/null 2>&1
 python - <<PY
 import csv, collections
