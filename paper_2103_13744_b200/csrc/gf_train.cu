@@ -1164,17 +1164,41 @@ void launch_photometric(const PhotoArgs& A, void* ws, double* loss_sum, cudaStre
 // float32 with numpy's operation order (NEP 50: Python-float coefficients are
 // rounded to float32 before use); L2 term sum(x^2) in float64.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, const AdamCoef& c) {
+  float mj = __fmul_rn(m, c.b1);                             // m *= b1
+  mj = __fadd_rn(mj, __fmul_rn(c.one_minus_b1, g));          // m += (1 - b1) * g
+  float vj = __fmul_rn(v, c.b2);                             // v *= b2
+  vj = __fadd_rn(vj, __fmul_rn(__fmul_rn(c.one_minus_b2, g), g));  // v += (1 - b2) * g * g
+  // p -= lr * (m / bc1) / (sqrt(v / bc2) + eps)
+  const float num = __fmul_rn(c.lr, __fdiv_rn(mj, c.bc1));
+  const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(vj, c.bc2)), c.eps);
+  p = __fsub_rn(p, __fdiv_rn(num, den));
+  m = mj;
+  v = vj;
+}
+
 __global__ void k_adam(float* p, const float* g, float* m, float* v, int64_t n, AdamCoef c) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    const float gj = g[j];
-    float mj = __fmul_rn(m[j], c.b1);                          // m *= b1
-    mj = __fadd_rn(mj, __fmul_rn(c.one_minus_b1, gj));         // m += (1 - b1) * g
-    float vj = __fmul_rn(v[j], c.b2);                          // v *= b2
-    vj = __fadd_rn(vj, __fmul_rn(__fmul_rn(c.one_minus_b2, gj), gj));  // v += (1 - b2) * g * g
-    // p -= lr * (m / bc1) / (sqrt(v / bc2) + eps)
-    const float num = __fmul_rn(c.lr, __fdiv_rn(mj, c.bc1));
-    const float den = __fadd_rn(__fsqrt_rn(__fdiv_rn(vj, c.bc2)), c.eps);
-    p[j] = __fsub_rn(p[j], __fdiv_rn(num, den));
+    float pj = p[j], mj = m[j], vj = v[j];
+    adam_one(pj, g[j], mj, vj, c);
+    p[j] = pj;
+    m[j] = mj;
+    v[j] = vj;
+  }
+}
+
+// 16-byte aligned arrays: four parameters per thread and 16-byte accesses
+// (same per-element arithmetic)
+__global__ void __launch_bounds__(256) k_adam4(float4* p, const float4* g, float4* m, float4* v, int64_t n4,
+                                               AdamCoef c) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
+    float4 pj = p[j], mj = m[j], vj = v[j];
+    const float4 gj = g[j];
+    adam_one(pj.x, gj.x, mj.x, vj.x, c);
+    adam_one(pj.y, gj.y, mj.y, vj.y, c);
+    adam_one(pj.z, gj.z, mj.z, vj.z, c);
+    adam_one(pj.w, gj.w, mj.w, vj.w, c);
+    p[j] = pj;
     m[j] = mj;
     v[j] = vj;
   }
@@ -1182,8 +1206,17 @@ __global__ void k_adam(float* p, const float* g, float* m, float* v, int64_t n, 
 
 void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, const AdamCoef& c, cudaStream_t st) {
   if (n <= 0) return;
-  const unsigned grid = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(n, 256), (int64_t)num_sms() * 16);
-  k_adam<<<grid, 256, 0, st>>>(p, g, m, v, n, c);
+  const bool al = (((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) == 0;
+  const int64_t n4 = al ? n / 4 : 0;
+  if (n4 > 0) {
+    const unsigned grid = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(n4, 256), (int64_t)num_sms() * 8);
+    k_adam4<<<grid, 256, 0, st>>>((float4*)p, (const float4*)g, (float4*)m, (float4*)v, n4, c);
+  }
+  const int64_t rest = n - 4 * n4;
+  if (rest > 0) {
+    const unsigned grid = (unsigned)std::min<int64_t>(gf_div_up<int64_t>(rest, 256), (int64_t)num_sms() * 16);
+    k_adam<<<grid, 256, 0, st>>>(p + 4 * n4, g + 4 * n4, m + 4 * n4, v + 4 * n4, rest, c);
+  }
 }
 
 // partial sums of squares in float64, then one fixed-order CTA sum
