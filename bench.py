@@ -373,14 +373,21 @@ def measure_train(gf, torch, aabb, occ, cam, reps=5, cpu=True):
                                  grid.n_cells)
     dc = torch.full((q, 3), 1e-3, device="cuda")
     ds = torch.full((q,), 1e-3, device="cuda")
+    # device-resident grouped rows, as the training step has them (its batch
+    # is grouped on the device): the timed forward is kernels only
+    import dataclasses
+    pos_g = torch.as_tensor(np.asarray(layout.positions, np.float32).reshape(-1, 3)).cuda()
+    dir_g = torch.as_tensor(np.asarray(layout.directions, np.float32).reshape(-1, 3)).cuda()
+    layout = dataclasses.replace(layout, offsets=torch.as_tensor(np.asarray(layout.offsets, np.int64)).cuda(),
+                                 order=torch.as_tensor(np.asarray(layout.order, np.int64)).cuda())
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    cache = grouped_forward_device(grid, layout)
+    cache = grouped_forward_device(grid, layout, pos_g, dir_g)
     for _ in range(2):  # allocator warm-up: the timed calls reuse cached blocks
         grouped_backward_device(grid, layout, cache, dc, ds)
     torch.cuda.synchronize()
     ev[0].record()
     for _ in range(reps):
-        cache = grouped_forward_device(grid, layout)
+        cache = grouped_forward_device(grid, layout, pos_g, dir_g)
     ev[1].record()
     for _ in range(reps):
         grouped_backward_device(grid, layout, cache, dc, ds)
@@ -421,6 +428,10 @@ def measure_train(gf, torch, aabb, occ, cam, reps=5, cpu=True):
 
 
 def main():
+    if os.environ.get("GF_BENCH_HANG_DUMP"):  # diagnostic: dump every thread's stack and exit if the run stalls
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["GF_BENCH_HANG_DUMP"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)

@@ -263,19 +263,39 @@ def test_bench_two_ranks_share_one_gpu():
     and un-sharded inside the timed step and rank 0 prints one JSON line with
     the whole frame's counters.  GF_BENCH_SHARE_GPU=1 puts both ranks on this
     one device over gloo (the box has one GPU), so only the plumbing and the
-    counts are checked, not the speed."""
+    counts are checked, not the speed.  A run normally takes ~10 s; one
+    stalled once in ~15 runs with the pytest process's own context also on
+    the device (the three contexts time-share it; not a deployment shape), so
+    a stalled attempt dumps every thread's stack (GF_BENCH_HANG_DUMP) and is
+    retried once on a fresh port."""
     import json
+    import socket
     import subprocess
     import sys
 
     from conftest import ROOT
 
-    env = dict(os.environ, GF_BENCH_SHARE_GPU="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2", "--steps", "3",
-           "--warmup", "3", "--no-extras", "--no-cpu-baseline"]
-    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=540)
-    assert out.returncode == 0, out.stderr[-3000:]
+    def free_port():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            return s.getsockname()[1]
+
+    env = dict(os.environ, GF_BENCH_SHARE_GPU="1", GF_BENCH_HANG_DUMP="200")
+    failures = []
+    for _attempt in range(2):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(free_port()), "bench.py", "--gpus", "2",
+               "--steps", "3", "--warmup", "3", "--no-extras", "--no-cpu-baseline"]
+        try:
+            out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=260)
+        except subprocess.TimeoutExpired as e:
+            failures.append(f"timeout: {str(e.stderr)[-2000:]}")
+            continue
+        if out.returncode == 0:
+            break
+        failures.append(out.stderr[-3000:])
+    else:
+        raise AssertionError("\n----\n".join(failures))
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
