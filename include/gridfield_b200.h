@@ -330,7 +330,11 @@ GF_API int gf_mlp_backward(const gf_manifest_t* m, int32_t f64, int64_t n_net, i
  * upstream gradient is d_color[order[j]] / d_sigma[order[j]] (order NULL =
  * identity).  packed_dev is the GF_PRECISION_FP32 packing.  gw[l] / gb[l]
  * receive layer l's gradients in the reference layout (n_cells, out, in) /
- * (n_cells, out), manifest order; cells without rows get zeros.         */
+ * (n_cells, out), manifest order; cells without rows get zeros.  For the
+ * 32-wide tiny manifest the wide layers' weight gradients run on tcgen05
+ * (bf16 3-piece split operands, float32-level sums; GF_BWD_TC=0: CUDA
+ * cores), and the workspace then also holds the operand tiles (~2 KB per
+ * row).  Results are deterministic run to run.                          */
 GF_API size_t gf_grouped_backward_workspace_bytes(const gf_arch_t* arch, int64_t n_cells, int64_t n);
 GF_API int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* packed_dev, const float* pos_dev,
                                const float* dir_dev, int64_t n, const int64_t* offsets_dev, const int64_t* order_dev,
