@@ -302,10 +302,19 @@ __global__ void __launch_bounds__(256) k_bwd_reduce(const float* __restrict__ sc
       float* gw = A.gw[l] + (size_t)e.x * (out * in);
       float* gb = A.gb[l] + (size_t)e.x * out;
       for (int q = threadIdx.x; q < cnt; q += 256) {
+        // whole-cell items: no rows (zeros), or 2..8 chunks: all loads
+        // issued, then added in chunk order
         float acc = 0.f;
         if (e.z > e.y) {
-          acc = scratch[(size_t)e.y * S::TOTAL + base + q];
-          for (uint32_t k = e.y + 1; k < e.z; ++k) acc = __fadd_rn(acc, scratch[(size_t)k * S::TOTAL + base + q]);
+          const float* src = scratch + (size_t)e.y * S::TOTAL + base + q;
+          const uint32_t nk = e.z - e.y;
+          float vals[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) vals[u] = (uint32_t)u < nk ? src[(size_t)u * S::TOTAL] : 0.f;
+          acc = vals[0];
+#pragma unroll
+          for (int u = 1; u < 8; ++u)
+            if ((uint32_t)u < nk) acc = __fadd_rn(acc, vals[u]);
         }
         if (q < out * in) gw[q] = acc;
         else gb[q - out * in] = acc;
