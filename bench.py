@@ -381,13 +381,13 @@ def measure_train(gf, torch, aabb, occ, cam, reps=5, cpu=True):
     layout = dataclasses.replace(layout, offsets=torch.as_tensor(np.asarray(layout.offsets, np.int64)).cuda(),
                                  order=torch.as_tensor(np.asarray(layout.order, np.int64)).cuda())
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    cache = grouped_forward_device(grid, layout, pos_g, dir_g)
+    cache = grouped_forward_device(grid, layout, pos_g, dir_g, keep_activations=True)
     for _ in range(2):  # allocator warm-up: the timed calls reuse cached blocks
         grouped_backward_device(grid, layout, cache, dc, ds)
     torch.cuda.synchronize()
     ev[0].record()
     for _ in range(reps):
-        cache = grouped_forward_device(grid, layout, pos_g, dir_g)
+        cache = grouped_forward_device(grid, layout, pos_g, dir_g, keep_activations=True)
     ev[1].record()
     for _ in range(reps):
         grouped_backward_device(grid, layout, cache, dc, ds)

@@ -135,6 +135,17 @@ GF_API int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void
                               const float* pos_dev, const float* dir_dev, int64_t n, const int64_t* offsets_dev,
                               const int64_t* order_dev, float* rgb_dev, float* sigma_dev, void* ws_dev,
                               size_t ws_bytes, void* stream);
+/* The training forward (batched.py:141-150 with caches): gf_grouped_forward
+ * in fp32 that also keeps, per grouped row j, the activations the backward
+ * needs in act_dev[j * 132 ...] = [h0 | h1 | feature | g | sigma | 3 colour
+ * logits] (the reference's per-bucket caches).  Only the 32-wide tiny
+ * manifest (GF_ERR_UNSUPPORTED otherwise).  Pass act_dev to
+ * gf_grouped_backward_act: the backward then reads them instead of
+ * recomputing the forward (identical values: same fp32 operation order). */
+GF_API int gf_grouped_forward_act(const gf_arch_t* arch, int64_t n_cells, const void* packed_dev,
+                                  const float* pos_dev, const float* dir_dev, int64_t n, const int64_t* offsets_dev,
+                                  const int64_t* order_dev, float* rgb_dev, float* sigma_dev, float* act_dev,
+                                  void* ws_dev, size_t ws_bytes, void* stream);
 
 /* --- render.render_rays / render_image (render.py:351-400) ---------------
  * Rays come either from `cam` (pixel index = ray_offset + i, row-major) or
@@ -340,6 +351,14 @@ GF_API int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const voi
                                const float* dir_dev, int64_t n, const int64_t* offsets_dev, const int64_t* order_dev,
                                const float* d_color_dev, const float* d_sigma_dev, float* const* gw_dev,
                                float* const* gb_dev, void* ws_dev, size_t ws_bytes, void* stream);
+/* gf_grouped_backward reading the training forward's activations
+ * (gf_grouped_forward_act on the same grouped rows); act_dev is ignored for
+ * manifests other than the 32-wide tiny one.                              */
+GF_API int gf_grouped_backward_act(const gf_arch_t* arch, int64_t n_cells, const void* packed_dev,
+                                   const float* pos_dev, const float* dir_dev, int64_t n, const int64_t* offsets_dev,
+                                   const int64_t* order_dev, const float* d_color_dev, const float* d_sigma_dev,
+                                   const float* act_dev, float* const* gw_dev, float* const* gb_dev, void* ws_dev,
+                                   size_t ws_bytes, void* stream);
 /* train.photometric_loss_and_grads compositing (train.py:243-288): queries
  * (ray_index, slot) of B rays x k slots with colours and densities (noise:
  * optional density perturbation, train.py:245-249), per-ray deltas, ground

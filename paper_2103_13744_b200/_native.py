@@ -145,6 +145,10 @@ _SIGS = {
     "gf_grouped_backward_workspace_bytes": (C.c_size_t, [C.POINTER(Arch), C.c_int64, C.c_int64]),
     "gf_grouped_backward": (C.c_int, [C.POINTER(Arch), C.c_int64, _P, _P, _P, C.c_int64, _P, _P, _P, _P,
                                       C.POINTER(_P), C.POINTER(_P), _P, C.c_size_t, _P]),
+    "gf_grouped_backward_act": (C.c_int, [C.POINTER(Arch), C.c_int64, _P, _P, _P, C.c_int64, _P, _P, _P, _P, _P,
+                                          C.POINTER(_P), C.POINTER(_P), _P, C.c_size_t, _P]),
+    "gf_grouped_forward_act": (C.c_int, [C.POINTER(Arch), C.c_int64, _P, _P, _P, C.c_int64, _P, _P, _P, _P, _P,
+                                         _P, C.c_size_t, _P]),
     "gf_photometric_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int64]),
     "gf_photometric_loss": (C.c_int, [C.c_int64, C.c_int32, C.c_int64, _P, _P, _P, _P, _P, _P, _P,
                                       C.POINTER(C.c_float), C.c_float, _P, _P, _P, _P, C.c_size_t, _P]),

@@ -80,9 +80,16 @@ def group_by_network(batch: QueryBatch, n_networks: int) -> GroupedLayout:
     )
 
 
-def grouped_forward_device(grid, layout: GroupedLayout, pos=None, dirs=None, precision="fp32") -> "GroupedCache":
+ACT_FLOATS = 132  # gf_grouped_forward_act: [h0 | h1 | feature | g | sigma | 3 logits] per row (32-wide)
+
+
+def grouped_forward_device(grid, layout: GroupedLayout, pos=None, dirs=None, precision="fp32",
+                           keep_activations=False) -> "GroupedCache":
     """The fused grouped forward on device tensors (results in query order);
-    ``pos``/``dirs`` may be given as device tensors already in grouped order."""
+    ``pos``/``dirs`` may be given as device tensors already in grouped order.
+    ``keep_activations`` (training, fp32): also keep the per-row activations
+    the backward needs (batched.py:143-150's caches) when the kernel supports
+    the manifest, so grouped_backward reads them instead of recomputing."""
     t = D.require_cuda()
     n = layout.n_queries
     packed = grid.device_params(precision)
@@ -96,10 +103,22 @@ def grouped_forward_device(grid, layout: GroupedLayout, pos=None, dirs=None, pre
     rgb = D.empty((n, 3), t.float32)
     sigma = D.empty((n,), t.float32)
     ws = D.workspace(N.lib().gf_grouped_workspace_bytes(grid.n_cells, n))
-    N.check(N.lib().gf_grouped_forward(grid.native_arch(), grid.n_cells, N.ptr(packed), N.PRECISION[precision],
-                                       N.ptr(pos), N.ptr(dirs), n, N.ptr(offs), N.ptr(order), N.ptr(rgb),
-                                       N.ptr(sigma), N.ptr(ws), ws.numel(), D.stream_handle()), "grouped_forward")
-    return GroupedCache(packed, pos, dirs, offs, order, rgb, sigma)
+    arch = grid.native_arch()
+    act = None
+    if keep_activations and precision == "fp32" and grid.arch.hidden_width == 32:
+        act = D.empty((max(n, 1) * ACT_FLOATS,), t.float32)
+        rc = N.lib().gf_grouped_forward_act(arch, grid.n_cells, N.ptr(packed), N.ptr(pos), N.ptr(dirs), n,
+                                            N.ptr(offs), N.ptr(order), N.ptr(rgb), N.ptr(sigma), N.ptr(act),
+                                            N.ptr(ws), ws.numel(), D.stream_handle())
+        if rc == N.GF_ERR_UNSUPPORTED:  # not the fused kernel's manifest: the backward recomputes
+            act = None
+        else:
+            N.check(rc, "grouped_forward")
+    if act is None:
+        N.check(N.lib().gf_grouped_forward(arch, grid.n_cells, N.ptr(packed), N.PRECISION[precision],
+                                           N.ptr(pos), N.ptr(dirs), n, N.ptr(offs), N.ptr(order), N.ptr(rgb),
+                                           N.ptr(sigma), N.ptr(ws), ws.numel(), D.stream_handle()), "grouped_forward")
+    return GroupedCache(packed, pos, dirs, offs, order, rgb, sigma, act)
 
 
 def grouped_forward(grid, layout: GroupedLayout, caches: list | None = None, precision=None):
@@ -112,7 +131,7 @@ def grouped_forward(grid, layout: GroupedLayout, caches: list | None = None, pre
     parameters it used; ``grouped_backward`` recomputes the activations from
     them in its fused kernel instead of keeping (n, width) activation arrays."""
     p = "fp32" if caches is not None else grid.resolved_precision(precision)
-    c = grouped_forward_device(grid, layout, precision=p)
+    c = grouped_forward_device(grid, layout, precision=p, keep_activations=caches is not None)
     if caches is not None:
         caches.append(c)
     dtype = grid.params.dtype
@@ -132,6 +151,7 @@ class GroupedCache:
     order: object
     rgb: object
     sigma: object
+    act: object = None  # per-row activations (keep_activations), or None: the backward recomputes them
 
 
 def grouped_backward_device(grid, layout: GroupedLayout, cache: GroupedCache, d_color, d_sigma):
@@ -162,6 +182,12 @@ def grouped_backward_device(grid, layout: GroupedLayout, cache: GroupedCache, d_
         _grouped_backward_dense(grid, cache, dc, ds, flat, gw, gb)
         return gw, gb, flat
     ws = D.workspace(ws_bytes)
+    if cache.act is not None:
+        N.check(N.lib().gf_grouped_backward_act(arch, grid.n_cells, N.ptr(cache.packed), N.ptr(cache.pos),
+                                                N.ptr(cache.dirs), n, N.ptr(cache.offsets), N.ptr(cache.order),
+                                                N.ptr(dc), N.ptr(ds), N.ptr(cache.act), wp, bp, N.ptr(ws), ws.numel(),
+                                                D.stream_handle()), "grouped_backward")
+        return gw, gb, flat
     N.check(N.lib().gf_grouped_backward(arch, grid.n_cells, N.ptr(cache.packed), N.ptr(cache.pos), N.ptr(cache.dirs),
                                         n, N.ptr(cache.offsets), N.ptr(cache.order), N.ptr(dc), N.ptr(ds), wp, bp,
                                         N.ptr(ws), ws.numel(), D.stream_handle()), "grouped_backward")

@@ -442,11 +442,14 @@ int gf_query_points(const gf_arch_t* arch, const gf_grid_geom_t* grid, const voi
   return check_cuda("gf_query_points");
 }
 
-int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packed, int precision, const float* pos,
-                       const float* dir, int64_t n, const int64_t* offsets, const int64_t* order, float* rgb,
-                       float* sigma, void* ws, size_t ws_bytes, void* stream) {
+static int grouped_forward_impl(const gf_arch_t* arch, int64_t n_cells, const void* packed, int precision,
+                                const float* pos, const float* dir, int64_t n, const int64_t* offsets,
+                                const int64_t* order, float* rgb, float* sigma, float* act, void* ws, size_t ws_bytes,
+                                void* stream) {
   LayerTable t;
   if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_grouped_forward: bad architecture");
+  if (act && !(precision == GF_PRECISION_FP32 && prepare_mlp_fp32(t) && t.width == 32))
+    return fail(GF_ERR_UNSUPPORTED, "gf_grouped_forward_act: activations only for the fp32 32-wide tiny manifest");
   if (n_cells < 1 || n < 0 || n >= (int64_t)0xFFFFFFF0ll) return fail(GF_ERR_INVALID, "gf_grouped_forward: bad sizes");
   Carve c(ws);
   QueryWs w;
@@ -454,10 +457,25 @@ int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packe
   cudaStream_t st = (cudaStream_t)stream;
   launch_segments_from_offsets(offsets, n_cells, n, w.B, st);
   TileSched S{w.B.tiles, w.B.n_tiles, nullptr, nullptr, nullptr};  // rows already grouped: identity
-  QueryIO io{pos, dir, rgb, sigma, order, nullptr, nullptr};
+  QueryIO io{pos, dir, rgb, sigma, order, nullptr, nullptr, act};
   if (!run_mlp(t, arch, packed, precision, S, nullptr, &io, st))
     return fail(GF_ERR_UNSUPPORTED, "gf_grouped_forward: no MLP kernel for this architecture/precision");
   return check_cuda("gf_grouped_forward");
+}
+
+int gf_grouped_forward(const gf_arch_t* arch, int64_t n_cells, const void* packed, int precision, const float* pos,
+                       const float* dir, int64_t n, const int64_t* offsets, const int64_t* order, float* rgb,
+                       float* sigma, void* ws, size_t ws_bytes, void* stream) {
+  return grouped_forward_impl(arch, n_cells, packed, precision, pos, dir, n, offsets, order, rgb, sigma, nullptr, ws,
+                              ws_bytes, stream);
+}
+
+int gf_grouped_forward_act(const gf_arch_t* arch, int64_t n_cells, const void* packed, const float* pos,
+                           const float* dir, int64_t n, const int64_t* offsets, const int64_t* order, float* rgb,
+                           float* sigma, float* act, void* ws, size_t ws_bytes, void* stream) {
+  if (!act) return fail(GF_ERR_INVALID, "gf_grouped_forward_act: act is NULL");
+  return grouped_forward_impl(arch, n_cells, packed, GF_PRECISION_FP32, pos, dir, n, offsets, order, rgb, sigma, act,
+                              ws, ws_bytes, stream);
 }
 
 int gf_mlp_forward(const gf_manifest_t* m, int32_t f64, int64_t n_net, int64_t rows, const void* const* w,
@@ -1171,10 +1189,10 @@ size_t gf_grouped_backward_workspace_bytes(const gf_arch_t* arch, int64_t n_cell
   return bwd_workspace(t, n_cells, n);
 }
 
-int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* packed, const float* pos, const float* dir,
-                        int64_t n, const int64_t* offsets, const int64_t* order, const float* d_color,
-                        const float* d_sigma, float* const* gw, float* const* gb, void* ws, size_t ws_bytes,
-                        void* stream) {
+static int grouped_backward_impl(const gf_arch_t* arch, int64_t n_cells, const void* packed, const float* pos,
+                                 const float* dir, int64_t n, const int64_t* offsets, const int64_t* order,
+                                 const float* d_color, const float* d_sigma, const float* act, float* const* gw,
+                                 float* const* gb, void* ws, size_t ws_bytes, void* stream) {
   LayerTable t;
   if (!arch || !make_layer_table(arch, &t)) return fail(GF_ERR_INVALID, "gf_grouped_backward: bad architecture");
   if (n_cells < 1 || n < 0 || !gw || !gb) return fail(GF_ERR_INVALID, "gf_grouped_backward: bad sizes");
@@ -1187,6 +1205,7 @@ int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* pack
   A.order = order;
   A.d_color = d_color;
   A.d_sigma = d_sigma;
+  A.act = (prepare_mlp_fp32(t) && t.width == 32) ? act : nullptr;
   for (int l = 0; l < t.n_layers; ++l) {
     A.gw[l] = gw[l];
     A.gb[l] = gb[l];
@@ -1194,6 +1213,22 @@ int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* pack
   if (!launch_grouped_backward(t, (const float*)packed, A, n_cells, n, ws, (cudaStream_t)stream))
     return fail(GF_ERR_UNSUPPORTED, "gf_grouped_backward: no backward kernel for this architecture");
   return check_cuda("gf_grouped_backward");
+}
+
+int gf_grouped_backward(const gf_arch_t* arch, int64_t n_cells, const void* packed, const float* pos, const float* dir,
+                        int64_t n, const int64_t* offsets, const int64_t* order, const float* d_color,
+                        const float* d_sigma, float* const* gw, float* const* gb, void* ws, size_t ws_bytes,
+                        void* stream) {
+  return grouped_backward_impl(arch, n_cells, packed, pos, dir, n, offsets, order, d_color, d_sigma, nullptr, gw, gb,
+                               ws, ws_bytes, stream);
+}
+
+int gf_grouped_backward_act(const gf_arch_t* arch, int64_t n_cells, const void* packed, const float* pos,
+                            const float* dir, int64_t n, const int64_t* offsets, const int64_t* order,
+                            const float* d_color, const float* d_sigma, const float* act, float* const* gw,
+                            float* const* gb, void* ws, size_t ws_bytes, void* stream) {
+  return grouped_backward_impl(arch, n_cells, packed, pos, dir, n, offsets, order, d_color, d_sigma, act, gw, gb, ws,
+                               ws_bytes, stream);
 }
 
 size_t gf_photometric_workspace_bytes(int64_t n_rays, int32_t k, int64_t n_queries) {

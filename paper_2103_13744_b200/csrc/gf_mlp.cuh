@@ -76,6 +76,7 @@ struct TileSched {
 
 struct RenderIO {
   static constexpr bool kDirEnc = true;  // tensor-core path reads the ray's pre-encoded gamma(d)
+  static constexpr bool kHasAct = false;
   float4* res;
   const float4* ray_dir;
   uint32_t stride;
@@ -108,6 +109,7 @@ struct RenderIO {
 // Bulk query: caller's float32 (N,3) arrays, results in caller order.
 struct QueryIO {
   static constexpr bool kDirEnc = true;  // direction gathered + encoded one layer ahead of its use (load_denc)
+  static constexpr bool kHasAct = true;
   const float* pos;
   const float* dir;
   float* rgb;
@@ -147,7 +149,12 @@ struct QueryIO {
     sigma[idx] = s;
   }
   __device__ __forceinline__ void load_denc(uint32_t idx, uint32_t row, uint4* de) const;  // gf_mlp_tc.cu
+  // training forward (fp32 SIMT kernel, 32-wide tiny manifest): per grouped
+  // row the activations the backward needs, GF_ACT_FLOATS floats:
+  // [h0 | h1 | feature | g | sigma | color logits]
+  float* act;
 };
+#define GF_ACT_FLOATS 132
 
 // launchers (gf_mlp_simt.cu / gf_mlp_tc.cu); return false if the architecture
 // has no compiled variant

@@ -82,12 +82,20 @@ __global__ void __launch_bounds__(128) k_mlp_fp32(const float* __restrict__ pack
     encode_f32<LX>(x, xe);
     float h[W], h2[W];
     dense_f32<P, PP, W, true>(sw + L.w_off[0], sw + L.b_off[0], xe, h);
+    float4* act = nullptr;
+    if constexpr (IO::kHasAct && W == 32 && T == 2)
+      if (io.act) act = reinterpret_cast<float4*>(io.act + (size_t)(tl.y + threadIdx.x) * GF_ACT_FLOATS);
+    auto put = [&](int at, const float* v, int nv) {  // nv a multiple of 4
+      for (int q = 0; q < nv; q += 4) act[at / 4 + q / 4] = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+    };
+    if (act) put(0, h, W);
 #pragma unroll
     for (int k = 1; k < T; ++k) {
       dense_f32<W, WP, W, true>(sw + L.w_off[k], sw + L.b_off[k], h, h2);
 #pragma unroll
       for (int q = 0; q < W; ++q) h[q] = h2[q];
     }
+    if (act) put(W, h, W);
     float sig[1];
     dense_f32<W, WP, 1, true>(sw + L.w_off[T], sw + L.b_off[T], h, sig);
     float cat[W + D];
@@ -96,6 +104,11 @@ __global__ void __launch_bounds__(128) k_mlp_fp32(const float* __restrict__ pack
     dense_f32<W + D, DP, W, true>(sw + L.w_off[T + 2], sw + L.b_off[T + 2], cat, h2);
     float z[3];
     dense_f32<W, WP, 3, false>(sw + L.w_off[T + 3], sw + L.b_off[T + 3], h2, z);
+    if (act) {
+      put(2 * W, cat, W);
+      put(3 * W, h2, W);
+      act[W] = make_float4(sig[0], z[0], z[1], z[2]);
+    }
     io.store(idx, tl.y + threadIdx.x, sigmoid_split(z[0]), sigmoid_split(z[1]), sigmoid_split(z[2]), sig[0]);
   }
 }

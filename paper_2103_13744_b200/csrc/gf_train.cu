@@ -771,8 +771,30 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
       }
     }
     __syncwarp();
-    // ---- forward (mlp.py:238-266)
-    if constexpr (S::WT) {
+    // ---- forward (mlp.py:238-266): recomputed, or (W = 32) read from the
+    // training forward's activations -- the same fp32 operation order, so
+    // the same values
+    const bool have_act = S::WT && A.act != nullptr;
+    if (have_act) {
+      if (on) {
+        const float4* av = reinterpret_cast<const float4*>(A.act + (size_t)row * GF_ACT_FLOATS);
+        for (int v = q; v < GF_ACT_FLOATS / 4; v += S::LANES) {
+          const float4 x = av[v];
+          const float e4[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int f = 4 * v + e;
+            const int d = f < W ? S::H0 + f
+                                : f < 2 * W ? S::H1 + f - W
+                                            : f < 3 * W ? S::CAT + f - 2 * W
+                                                        : f < 4 * W ? S::G + f - 3 * W
+                                                                    : f == 4 * W ? S::SIG : S::ZC + f - 4 * W - 1;
+            s[d] = e4[e];
+          }
+        }
+      }
+      __syncwarp();
+    } else if constexpr (S::WT) {
       if (on) dense_part_t<P, S::OS, Q, true>(swt + S::T0, bias(0), s + S::X, q * Q, s + S::H0);
       __syncwarp();
       if (on) dense_part_t<W, S::OS, Q, true>(swt + S::T1, bias(1), s + S::H0, q * Q, s + S::H1);
@@ -799,7 +821,7 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
     }
     // ---- backward (mlp.py:291-316)
     if (on && q < 3) {
-      dense_part<W, WP, 1, false>(w_col, bias(5), s + S::G, q, s + S::ZC);  // logit q
+      if (!have_act) dense_part<W, WP, 1, false>(w_col, bias(5), s + S::G, q, s + S::ZC);  // logit q
       const float col = sigmoid_split(s[S::ZC + q]);
       s[S::DZC + q] = __fmul_rn(__fmul_rn(A.d_color[3 * src + q], col), __fsub_rn(1.0f, col));
     }

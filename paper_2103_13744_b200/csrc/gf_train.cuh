@@ -13,6 +13,7 @@ struct BwdArgs {
   const float* d_sigma;     // (n,)
   float* gw[GF_MAX_LAYERS]; // reference layout (n_cells, out, in)
   float* gb[GF_MAX_LAYERS]; // (n_cells, out)
+  const float* act;         // NULL, or the training forward's activations per grouped row (GF_ACT_FLOATS, W = 32)
 };
 
 struct PhotoArgs {

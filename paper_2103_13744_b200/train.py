@@ -468,7 +468,7 @@ def photometric_loss_and_grads(model, samples: RaySamples, gt: np.ndarray, backg
     t = D.require_cuda()
     b, k = samples.n_rays, samples.k
     layout = _device_layout(model, samples.positions, samples.directions)
-    cache = grouped_forward_device(model, layout, layout.pos, layout.dirs)
+    cache = grouped_forward_device(model, layout, layout.pos, layout.dirs, keep_activations=True)
     q = layout.n_queries
     ri = D.to_device(np.asarray(samples.ray_index, np.int64), t.int64)
     sl = D.to_device(np.asarray(samples.slot, np.int64), t.int64)
@@ -531,7 +531,7 @@ def distill_step(student, teacher, cfg: TrainConfig, state: AdamState, rng, delt
     layout = GroupedLayout(positions=positions, directions=directions, order=np.arange(m, dtype=np.int64),
                            inverse=np.arange(m, dtype=np.int64), offsets=np.arange(0, m + 1, p, dtype=np.int64),
                            n_networks=n)
-    cache = grouped_forward_device(student, layout, pos_d, dir_d)
+    cache = grouped_forward_device(student, layout, pos_d, dir_d, keep_activations=True)
     w_a = cfg.distill_alpha_weight
     dc = D.empty((m, 3), t.float32)
     ds = D.empty((m,), t.float32)

@@ -288,3 +288,35 @@ def test_grouped_backward_chunking_edge_cases(width):
         _close(grads.weights[name], gw[name], name)
         _close(grads.biases[name], gb[name], name)
         assert not np.asarray(grads.weights[name])[counts == 0].any(), name
+
+
+def test_backward_from_kept_activations_bit_identical():
+    """The training forward's kept activations (gf_grouped_forward_act) feed
+    the backward instead of its fp32 recompute: same operation order, so the
+    gradients are bit-identical to the recomputing path, and the forward's
+    colours / densities are those of the plain forward."""
+    import dataclasses
+
+    from paper_2103_13744_b200.batched import grouped_backward_device, grouped_forward_device
+
+    gf = _gf()
+    rng = np.random.default_rng(5)
+    aabb = gf.Aabb((0.0,) * 3, (1.0,) * 3)
+    g = gf.init_network_grid(aabb, (4, 4, 4), seed=9)
+    for k in g.params.biases:
+        g.params.biases[k][...] = rng.normal(0.0, 0.3, g.params.biases[k].shape).astype(np.float32)
+    pts = rng.uniform(0.0, 1.0, (5000, 3)).astype(np.float32)
+    pts[:700] *= 0.25  # one crowded cell: several chunks
+    dirs = rng.normal(size=pts.shape).astype(np.float32)
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    dcol = rng.normal(0.0, 1e-2, (len(pts), 3)).astype(np.float32)
+    dsig = rng.normal(0.0, 1e-2, len(pts)).astype(np.float32)
+    layout = gf.group_by_network(gf.QueryBatch(pts, dirs, g.cell_index(pts)), g.n_cells)
+    kept = grouped_forward_device(g, layout, keep_activations=True)
+    plain = grouped_forward_device(g, layout)
+    assert kept.act is not None and plain.act is None
+    assert np.array_equal(kept.rgb.cpu().numpy(), plain.rgb.cpu().numpy())
+    assert np.array_equal(kept.sigma.cpu().numpy(), plain.sigma.cpu().numpy())
+    _, _, f_act = grouped_backward_device(g, layout, kept, dcol, dsig)
+    _, _, f_rec = grouped_backward_device(g, layout, dataclasses.replace(kept, act=None), dcol, dsig)
+    assert np.array_equal(f_act.cpu().numpy(), f_rec.cpu().numpy())
