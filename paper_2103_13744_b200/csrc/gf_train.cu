@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(BwdShape<W>::THREADS) k_grouped_backward(const
         async4(swt + t_off + i * S::OS + o, w + o * inp + i);
       }
     };
-    transpose(0, P, S::T0);
+    if (!A.act) transpose(0, P, S::T0);  // trunk0 is only needed to recompute the forward
     transpose(1, W, S::T1);
     transpose(3, W, S::T3);
     transpose(4, W + D, S::T4);
