@@ -1023,8 +1023,8 @@ __global__ void k_photo_scatter(PhotoArgs A, float4* dense, int32_t* qidx, uint8
 // A warp owns 32 consecutive rays and stages PH_CS slots of all of them at a
 // time through shared memory: the dense rows, t_before and the query indices
 // move as whole 128-byte lines instead of one strided element per lane.
-#define PH_CS 8
-#define PH_WARPS 4
+#define PH_CS 16
+#define PH_WARPS 1  // one warp (32 rays) per CTA: 8192 rays -> 256 CTAs cover all 148 SMs
 __global__ void __launch_bounds__(32 * PH_WARPS) k_photo_ray(PhotoArgs A, const float4* __restrict__ dense,
                                                              const int32_t* __restrict__ qidx,
                                                              const uint8_t* __restrict__ nmask, float* tb,
